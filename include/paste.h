@@ -1,0 +1,206 @@
+/*
+ * paste.h -- C ABI of libpaste.so, the B200 (sm_100a) engine for the
+ * data-parallel core of PASTE (arXiv 2603.18897).
+ *
+ * The reference (spectool, /root/reference/pkg/src/spectool) is a pure-Python
+ * library with no FFI layer; its drop-in surface is the Python API re-exported
+ * in spectool/__init__.py:9-90.  The Python package paper_2603_18897_b200
+ * mirrors that API and binds the entry points below with ctypes
+ * (paper_2603_18897_b200/_native.py).  Each entry point names the reference
+ * function(s) whose computation it replaces.
+ *
+ * Conventions
+ *   - every pointer inside a *_desc / *_out struct is a DEVICE pointer
+ *     (caller-owned, e.g. torch tensors); the structs themselves live in host
+ *     memory and are read during the call only.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); calls are
+ *     asynchronous with respect to the host unless stated otherwise.
+ *   - return value: PASTE_OK (0) or a negative error class; the message of
+ *     the last failure on the calling thread is available from
+ *     paste_last_error().
+ *   - no pointer is retained past the call.
+ */
+#ifndef PASTE_H
+#define PASTE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PASTE_OK 0
+#define PASTE_ERR_INVALID (-1)     /* bad argument (maps to ValueError)            */
+#define PASTE_ERR_CUDA (-2)        /* CUDA runtime failure (maps to RuntimeError)  */
+#define PASTE_ERR_UNSUPPORTED (-3) /* outside the engine's envelope                */
+
+#define PASTE_ABI_VERSION 1
+
+/* ---------------------------------------------------------------------- */
+/* Payload tapes (see paper_2603_18897_b200/tape.py)                        */
+/* ---------------------------------------------------------------------- */
+
+enum {
+  PASTE_T_NULL = 0, PASTE_T_FALSE = 1, PASTE_T_TRUE = 2, PASTE_T_INT = 3,
+  PASTE_T_FLOAT = 4, PASTE_T_STR = 5, PASTE_T_LIST = 6, PASTE_T_DICT = 7
+};
+enum { PASTE_F_NFC = 1, PASTE_F_FLOATSRC = 2, PASTE_F_NAN = 4 };
+
+typedef struct {
+  uint8_t type;   /* PASTE_T_*                                                */
+  uint8_t flags;  /* PASTE_F_*                                                */
+  uint16_t pad;
+  int32_t key;    /* interned key inside the parent dict, -1 otherwise        */
+  uint32_t a;     /* container: #children      | scalar: byte offset          */
+  uint32_t b;     /* container: subtree nodes  | scalar: byte length          */
+} paste_tape_node; /* 16 bytes */
+
+/* Event payload directory entry: where one event's tape starts.            */
+typedef struct {
+  int64_t node_base;
+  int64_t byte_base;
+} paste_event_ref;
+
+/* ---------------------------------------------------------------------- */
+/* Compiled pattern pool (PoolImage, paper_2603_18897_b200/packing.py)      */
+/* ---------------------------------------------------------------------- */
+
+enum { PASTE_REL_ANCHORED = 0, PASTE_REL_SUFFIX = 1 };       /* mining.py:42-51 */
+enum { PASTE_X_PATH = 0, PASTE_X_FALLBACK = 1, PASTE_X_FORMAT = 2 }; /* mappings.py:47-89 */
+enum { PASTE_PF_HAS_MAPPING = 1, PASTE_PF_STRUCT_ERR = 2 };
+
+typedef struct {
+  int32_t ctx_off;     /* into ctx_sig                                        */
+  int32_t ctx_len;
+  int32_t target_tool; /* tool id (sig >> 1)                                  */
+  int32_t bind_off;    /* into bindings                                       */
+  int32_t n_bind;
+  int32_t flags;       /* PASTE_PF_*                                          */
+  double p;            /* PatternTuple.p                                      */
+} paste_pattern;       /* 32 bytes */
+
+typedef struct {
+  int32_t kind;       /* PASTE_X_*                                           */
+  int32_t ctx_pos;    /* PathLookup.ctx_pos / IndexedFallback.ctx_pos / hole  */
+  int32_t step_off;   /* path (PATH, FORMAT hole) or path_prefix (FALLBACK)   */
+  int32_t step_cnt;
+  int32_t suf_off;    /* FALLBACK path_suffix                                 */
+  int32_t suf_cnt;
+  int32_t start_index;/* FALLBACK start_index (clamped; <0 never resolves)    */
+  int32_t fail_tool;  /* FALLBACK fail_tool id, -1 = unknown tool             */
+} paste_binding;      /* 32 bytes */
+
+/* A path step is a pair (kind, value): kind 0 = dict key id, 1 = list index
+ * (negative / out of int32 range = never resolves).                         */
+typedef struct {
+  int32_t n_patterns;
+  int32_t n_bucket_sigs;   /* buckets exist for sig < n_bucket_sigs           */
+  int32_t k;               /* MiningConfig.k of the pool                      */
+  int32_t relation;        /* PASTE_REL_*                                     */
+  int32_t max_ctx;         /* longest context                                 */
+  int32_t max_bindings;
+  const paste_pattern* patterns;
+  const paste_binding* bindings;
+  const int32_t* ctx_sig;
+  const int32_t* steps;        /* 2 x int32 per step                          */
+  const int32_t* bucket_off;   /* [n_bucket_sigs + 1]                         */
+  const int32_t* bucket_pat;   /* pattern ids, static rank (-p, pattern_id)   */
+  const uint8_t* bucket_scan_all; /* 1 = bucket holds a struct-error pattern  */
+} paste_pool_desc;
+
+/* Per-tool admission tables (policy.py:207-244, scheduling.py:218-219).    */
+typedef struct {
+  int32_t enabled;          /* 0 = predict only                               */
+  int32_t n_tools;
+  const uint8_t* allow;     /* [n_tools] ToolRule.allow                       */
+  const uint8_t* max_level; /* [n_tools] 1 warm_only, 2 dry_run, 3 full       */
+  const double* benefit;    /* [n_tools] benefit_of(tool), e.g. EWMA duration */
+} paste_admit_desc;
+
+/* ---------------------------------------------------------------------- */
+/* Live session windows (PredictionWindow, prediction.py:40-58)             */
+/* ---------------------------------------------------------------------- */
+
+typedef struct {
+  int64_t n_sessions;
+  int32_t capacity;            /* W (ring slots per session)                  */
+  int32_t pad;
+  int32_t* tok;                /* [n*W] sig id, -1 = LLM step                 */
+  int32_t* evt;                /* [n*W] event index into refs                 */
+  int64_t* count;              /* [n] events observed so far                  */
+  const paste_tape_node* nodes;
+  const uint8_t* bytes;
+  paste_event_ref* refs;       /* event directory (written by observe)        */
+  /* optional observe-before-predict: session s first observes one new event
+   * (token new_tok[s]); it becomes event new_evt_base + s and its directory
+   * entry is new_ref[s] with byte_base taken relative to new_byte_base.     */
+  const int32_t* new_tok;      /* [n] or NULL                                 */
+  const paste_event_ref* new_ref; /* [n]                                      */
+  int64_t new_evt_base;
+  int64_t new_byte_base;
+} paste_windows;
+
+enum { PASTE_C_FULL = 0, PASTE_C_PARTIAL = 1, PASTE_C_TOOL_ONLY = 2 };
+
+typedef struct {
+  int32_t max_candidates;  /* K: per-session prediction slots                 */
+  int32_t max_bindings;    /* slots per prediction in pred_arg                */
+  int32_t* n_pred;         /* [n]                                             */
+  int32_t* pred_pat;       /* [n*K] pattern index                             */
+  uint8_t* pred_comp;      /* [n*K] PASTE_C_*                                 */
+  int64_t* pred_arg;       /* [n*K*B] (event << 32 | node) or -1 = UNBOUND    */
+  int32_t* n_act;          /* [n]                                             */
+  int16_t* act_pred;       /* [n*K] prediction slot of each action, in order  */
+  uint8_t* act_level;      /* [n*K] SpecLevel                                 */
+  double* act_util;        /* [n*K] expected utility p * benefit              */
+  int32_t* struct_err;     /* [n] structural errors met (diagnostics)         */
+} paste_predict_out;
+
+/* ---------------------------------------------------------------------- */
+/* Entry points                                                             */
+/* ---------------------------------------------------------------------- */
+
+const char* paste_last_error(void);
+int paste_abi_version(void);
+
+/* K4: batched Predictor.predict + admit.
+ * Replaces prediction.py:76-118 (Predictor.predict, incl. match_at
+ * mining.py:119-156 and evaluate mappings.py:207-223) and policy.py:207-244
+ * (admit) for every session of the batch; when windows->new_tok is non-NULL
+ * each session first observes one new event (PredictionWindow.observe,
+ * prediction.py:48-49).                                                    */
+int paste_predict_batch(const paste_pool_desc* pool, paste_windows* windows,
+                        const paste_admit_desc* admit, paste_predict_out* out,
+                        void* stream);
+
+/* K4 epilogue as a standalone op: admit() over many prediction lists.
+ * Replaces policy.py:207-244 (admit + _beats).  Per prediction: tool id,
+ * full (1 = Completeness.FULL), probability, benefit_of(prediction) and
+ * created_at; lists are CSR (list_off[n_lists+1]).  Output per list: the
+ * number of actions and, in first-appearance order, the winning prediction
+ * (index within its list), level and expected utility; slots are
+ * list_off-aligned (at most one action per prediction).                    */
+typedef struct {
+  int64_t n_lists;
+  const int64_t* list_off;  /* [n_lists + 1]                                 */
+  const int32_t* tool;      /* [N]                                           */
+  const uint8_t* full;      /* [N]                                           */
+  const double* p;          /* [N]                                           */
+  const double* benefit;    /* [N]                                           */
+  const double* created_at; /* [N]                                           */
+  int32_t* n_act;           /* [n_lists]                                     */
+  int32_t* act_pred;        /* [N]                                           */
+  uint8_t* act_level;       /* [N]                                           */
+  double* act_util;         /* [N]                                           */
+} paste_admit_lists_desc;
+
+int paste_admit_lists(const paste_admit_desc* policy, paste_admit_lists_desc* lists,
+                      void* stream);
+
+/* Number of kernel launches the last paste_* call on this thread issued.   */
+int paste_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PASTE_H */

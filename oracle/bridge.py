@@ -1,0 +1,81 @@
+"""ctypes bridge to the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Imported by tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs
+to run oracle/paste_oracle.c on the same packed host arrays the device path
+consumes.  The product package never imports this module.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from ctypes import POINTER, c_char_p, c_int, c_void_p
+
+import numpy as np
+
+from paper_2603_18897_b200._native import AdmitDesc, PoolDesc, PredictOut, WindowsDesc
+from paper_2603_18897_b200.packing import PoolImage, PredictResult, WindowBatch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "_build", "libpaste_oracle.so")
+
+_lib = None
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+    return LIB
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            build()
+        _lib = ctypes.CDLL(LIB)
+        _lib.oracle_predict_batch.restype = c_int
+        _lib.oracle_predict_batch.argtypes = [POINTER(PoolDesc), c_char_p, POINTER(WindowsDesc),
+                                              POINTER(AdmitDesc), POINTER(PredictOut), c_int]
+    return _lib
+
+
+def _p(a: np.ndarray | None) -> int:
+    return 0 if a is None else a.ctypes.data
+
+
+def pool_desc(im: PoolImage) -> tuple[PoolDesc, bytes, list]:
+    keep = [im.patterns, im.bindings, im.ctx_sig, im.steps, im.bucket_off, im.bucket_pat,
+            im.bucket_scan_all if len(im.bucket_scan_all) else np.zeros(1, np.uint8)]
+    desc = PoolDesc(len(im.pool.patterns), im.n_bucket_sigs, im.k, im.relation, im.max_ctx,
+                    im.max_bindings, *[_p(a) for a in keep])
+    pids = b"".join(pid.encode().ljust(16, b"\0") for pid in im.pattern_ids) or b"\0" * 16
+    return desc, pids, keep
+
+
+def predict(im: PoolImage, batch: WindowBatch, K: int,
+            admit: tuple[np.ndarray, np.ndarray, np.ndarray] | None = None,
+            new_tok: np.ndarray | None = None, new_ref: np.ndarray | None = None,
+            new_evt_base: int = 0, new_byte_base: int = 0,
+            threads: int = 1) -> PredictResult:
+    """Run the oracle; like the device it mutates the window rings (and the
+    event directory) when new_tok / new_ref are given."""
+    desc, pids, keep = pool_desc(im)
+    nodes, data, refs = batch.arena.arrays() if hasattr(batch.arena, "arrays") else batch.arena
+    win = WindowsDesc(batch.n, batch.capacity, 0, _p(batch.tok), _p(batch.evt), _p(batch.count),
+                      _p(nodes), _p(data), _p(refs), _p(new_tok), _p(new_ref), new_evt_base,
+                      new_byte_base)
+    res = PredictResult.empty(batch.n, K, max(im.max_bindings, 1), admit is not None)
+    if admit is not None:
+        adm = AdmitDesc(1, len(admit[0]), *[_p(a) for a in admit])
+    else:
+        adm = AdmitDesc(0, 0, 0, 0, 0)
+    out = PredictOut(K, res.B, _p(res.n_pred), _p(res.pred_pat), _p(res.pred_comp),
+                     _p(res.pred_arg), _p(res.n_act), _p(res.act_pred), _p(res.act_level),
+                     _p(res.act_util), _p(res.struct_err))
+    rc = lib().oracle_predict_batch(ctypes.byref(desc), pids, ctypes.byref(win),
+                                    ctypes.byref(adm), ctypes.byref(out), threads)
+    if rc != 0:
+        raise RuntimeError(f"oracle_predict_batch failed: {rc}")
+    del keep
+    return res

@@ -1,0 +1,261 @@
+/*
+ * paste_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain-C restatement of the reference's hot-path algorithms
+ * (spectool, /root/reference/pkg/src/spectool), operating on the same packed
+ * inputs as libpaste (include/paste.h) so its outputs can be compared with
+ * the CUDA kernels record for record.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it; the
+ * product path never does.
+ *
+ * It deliberately follows the reference's control flow rather than the
+ * device's shortcuts: predict scans the whole pool in pool order, collects
+ * every match and sorts by (-p, pattern_id) with a stable sort
+ * (prediction.py:88-117) instead of using pre-ranked buckets; admit keeps
+ * incumbents in a map keyed by tool (policy.py:207-244).
+ *
+ * Pinning: tests/test_oracle_golden.py checks this oracle (through the host
+ * packing/decoding of paper_2603_18897_b200) against golden vectors produced
+ * by running the reference itself (tests/golden/make_golden.py).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "paste.h"
+
+typedef struct {
+  const paste_tape_node* nodes;
+  const paste_event_ref* refs;
+} tapes_t;
+
+
+static uint32_t node_size(const paste_tape_node* n) {
+  return n->type >= PASTE_T_LIST ? n->b : 1u;
+}
+
+/* _walk (mappings.py:143-153) over one step; returns child or -1 */
+static int64_t walk_step(const tapes_t* T, int64_t base, int64_t cur, int32_t kind, int32_t value) {
+  const paste_tape_node* nd = &T->nodes[base + cur];
+  int64_t child = cur + 1;
+  uint32_t c;
+  if (kind == 0) { /* str step: node must be a dict holding the key */
+    if (nd->type != PASTE_T_DICT) return -1;
+    for (c = 0; c < nd->a; ++c) {
+      if (T->nodes[base + child].key == value) return child;
+      child += node_size(&T->nodes[base + child]);
+    }
+    return -1;
+  }
+  /* int step: node must be a list and 0 <= step < len */
+  if (nd->type != PASTE_T_LIST || value < 0 || (uint32_t)value >= nd->a) return -1;
+  for (c = 0; c < (uint32_t)value; ++c) child += node_size(&T->nodes[base + child]);
+  return child;
+}
+
+static int64_t walk_path(const tapes_t* T, int64_t base, int64_t cur, const int32_t* steps,
+                         int32_t off, int32_t cnt) {
+  int32_t s;
+  for (s = 0; s < cnt && cur >= 0; ++s)
+    cur = walk_step(T, base, cur, steps[2 * (off + s)], steps[2 * (off + s) + 1]);
+  return cur;
+}
+
+typedef struct {
+  double p;
+  const char* pid;
+  int32_t pat;
+  int32_t pool_order;
+  uint8_t comp;
+  int64_t args[64];
+} cand_t;
+
+/* stable insertion sort by (-p, pattern_id) -- prediction.py:115 */
+static int cand_before(const cand_t* a, const cand_t* b) {
+  if (a->p != b->p) return a->p > b->p;
+  return strncmp(a->pid, b->pid, 16) < 0;
+}
+
+/* One session: Predictor.predict (prediction.py:76-118) + admit (policy.py:207-244). */
+static void predict_one(const paste_pool_desc* pool, const char* pids, const paste_windows* win,
+                        const paste_admit_desc* adm, paste_predict_out* out, int64_t s,
+                        cand_t* cands, int32_t* stream_tok, int32_t* stream_slot) {
+  const int W = win->capacity;
+  const int K = out->max_candidates, B = out->max_bindings;
+  int32_t* tok = win->tok + s * W;
+  int32_t* evt = win->evt + s * W;
+  int64_t cnt = win->count[s];
+  int len, i, n_stream = 0, n_cand = 0, n_err = 0, p;
+  tapes_t T = {win->nodes, win->refs};
+
+  if (win->new_tok) { /* PredictionWindow.observe */
+    const int64_t ev = win->new_evt_base + s;
+    win->refs[ev].node_base = win->new_ref[s].node_base;
+    win->refs[ev].byte_base = win->new_ref[s].byte_base + win->new_byte_base;
+    tok[cnt % W] = win->new_tok[s];
+    evt[cnt % W] = (int32_t)ev;
+    win->count[s] = ++cnt;
+  }
+  len = (int)(cnt < W ? cnt : W);
+  /* window.tool_events(): oldest..newest */
+  for (i = 0; i < len; ++i) {
+    int slot = (int)((cnt - len + i) % W);
+    if (tok[slot] >= 0) {
+      stream_tok[n_stream] = tok[slot];
+      stream_slot[n_stream] = slot;
+      ++n_stream;
+    }
+  }
+  out->n_pred[s] = 0;
+  out->struct_err[s] = 0;
+  if (adm->enabled) out->n_act[s] = 0;
+  if (n_stream == 0) return;
+  {
+    const int anchor = n_stream - 1;
+    for (p = 0; p < pool->n_patterns; ++p) {
+      const paste_pattern* pt = &pool->patterns[p];
+      const int32_t* ctx = pool->ctx_sig + pt->ctx_off;
+      const int n = pt->ctx_len;
+      int mpos[64], first_pos, ok = 1, b;
+      uint8_t comp;
+      if (n == 0 || n > 64 || ctx[n - 1] != stream_tok[anchor]) continue; /* bucket */
+      /* match_at (mining.py:119-156) */
+      if (pool->relation == PASTE_REL_SUFFIX) {
+        int start = anchor - n + 1;
+        if (start < 0) continue;
+        for (i = 0; i < n; ++i)
+          if (stream_tok[start + i] != ctx[i]) { ok = 0; break; }
+        if (!ok) continue;
+        for (i = 0; i < n; ++i) mpos[i] = start + i;
+        first_pos = start;
+      } else {
+        int lo = anchor - pool->k + 1, j = n - 2, pos = anchor - 1;
+        if (lo < 0) lo = 0;
+        mpos[n - 1] = anchor;
+        while (j >= 0 && pos >= lo) {
+          if (stream_tok[pos] == ctx[j]) mpos[j--] = pos;
+          --pos;
+        }
+        if (j >= 0) continue;
+        first_pos = mpos[0];
+      }
+      /* evaluate (mappings.py:207-223); ctx_pos out of range raises
+       * MappingStructureError, which predict tallies and skips. */
+      comp = PASTE_C_TOOL_ONLY;
+      if (pt->flags & PASTE_PF_HAS_MAPPING) {
+        int bad = 0;
+        for (b = 0; b < pt->n_bind; ++b) {
+          int cp = pool->bindings[pt->bind_off + b].ctx_pos;
+          if (cp < 0 || cp >= n) bad = 1;
+        }
+        if (bad) { ++n_err; continue; }
+        comp = PASTE_C_FULL;
+        for (b = 0; b < pt->n_bind; ++b) {
+          const paste_binding* bd = &pool->bindings[pt->bind_off + b];
+          const int src = mpos[bd->ctx_pos];
+          const int32_t ev = evt[stream_slot[src]];
+          const int64_t base = T.refs[ev].node_base;
+          int64_t cur;
+          if (bd->kind == PASTE_X_FALLBACK) {
+            /* _failures_after over history = stream[first_pos..anchor] */
+            int fails = 0, q;
+            for (q = first_pos; q <= anchor; ++q)
+              if (q > src && (stream_tok[q] >> 1) == bd->fail_tool && !(stream_tok[q] & 1)) ++fails;
+            cur = walk_path(&T, base, 0, pool->steps, bd->step_off, bd->step_cnt);
+            if (cur >= 0) cur = bd->start_index < 0 ? -1 : walk_step(&T, base, cur, 1, bd->start_index + fails);
+            if (cur >= 0) cur = walk_path(&T, base, cur, pool->steps, bd->suf_off, bd->suf_cnt);
+          } else {
+            cur = walk_path(&T, base, 0, pool->steps, bd->step_off, bd->step_cnt);
+            if (cur >= 0 && bd->kind == PASTE_X_FORMAT) {
+              int t = T.nodes[base + cur].type; /* _leaf_str: str or number */
+              if (t != PASTE_T_STR && t != PASTE_T_INT && t != PASTE_T_FLOAT) cur = -1;
+            }
+          }
+          if (cur < 0) comp = PASTE_C_PARTIAL;
+          cands[n_cand].args[b] = cur < 0 ? -1 : (((int64_t)ev << 32) | cur);
+        }
+      }
+      cands[n_cand].p = pt->p;
+      cands[n_cand].pid = pids + 16 * (int64_t)p;
+      cands[n_cand].pat = p;
+      cands[n_cand].pool_order = p;
+      cands[n_cand].comp = comp;
+      /* stable insertion */
+      {
+        cand_t tmp = cands[n_cand];
+        int at = n_cand;
+        while (at > 0 && cand_before(&tmp, &cands[at - 1])) {
+          cands[at] = cands[at - 1];
+          --at;
+        }
+        cands[at] = tmp;
+      }
+      ++n_cand;
+    }
+  }
+  out->struct_err[s] = n_err;
+  if (n_cand > K) n_cand = K; /* predictions[:max_candidates] */
+  out->n_pred[s] = n_cand;
+  for (i = 0; i < n_cand; ++i) {
+    const int64_t slot = s * K + i;
+    const paste_pattern* pt = &pool->patterns[cands[i].pat];
+    int b;
+    out->pred_pat[slot] = cands[i].pat;
+    out->pred_comp[slot] = cands[i].comp;
+    if (cands[i].comp != PASTE_C_TOOL_ONLY)
+      for (b = 0; b < pt->n_bind; ++b) out->pred_arg[slot * B + b] = cands[i].args[b];
+  }
+  if (!adm->enabled) return;
+  {
+    /* admit: best[tool] with first-appearance order */
+    int n_act = 0, j;
+    for (i = 0; i < n_cand; ++i) {
+      const paste_pattern* pt = &pool->patterns[cands[i].pat];
+      const int tool = pt->target_tool;
+      int implied, cap, level;
+      double util;
+      if (tool >= adm->n_tools || !adm->allow[tool]) continue;
+      implied = cands[i].comp == PASTE_C_FULL ? 3 : 1;
+      cap = adm->max_level[tool];
+      level = cap < implied ? cap : implied;
+      util = pt->p * adm->benefit[tool];
+      for (j = 0; j < n_act; ++j)
+        if (pool->patterns[cands[out->act_pred[s * K + j]].pat].target_tool == tool) break;
+      if (j == n_act) {
+        out->act_pred[s * K + j] = (int16_t)i;
+        out->act_level[s * K + j] = (uint8_t)level;
+        out->act_util[s * K + j] = util;
+        ++n_act;
+      } else {
+        const double iu = out->act_util[s * K + j];
+        const double ip = pool->patterns[cands[out->act_pred[s * K + j]].pat].p;
+        int beats = (util != iu) ? (util > iu) : (pt->p > ip);
+        if (beats) {
+          out->act_pred[s * K + j] = (int16_t)i;
+          out->act_level[s * K + j] = (uint8_t)level;
+          out->act_util[s * K + j] = util;
+        }
+      }
+    }
+    out->n_act[s] = n_act;
+  }
+}
+
+/* Batched oracle predict.  All pointers are HOST pointers.  `pids` holds the
+ * pattern ids as 16-byte NUL-padded strings. */
+int oracle_predict_batch(const paste_pool_desc* pool, const char* pids, paste_windows* win,
+                         const paste_admit_desc* adm, paste_predict_out* out, int n_threads) {
+  int64_t s;
+  if (pool->max_bindings > 64) return PASTE_ERR_UNSUPPORTED;
+#pragma omp parallel num_threads(n_threads > 0 ? n_threads : 1)
+  {
+    cand_t* cands = (cand_t*)malloc(sizeof(cand_t) * (size_t)(pool->n_patterns + 1));
+    int32_t* st = (int32_t*)malloc(sizeof(int32_t) * (size_t)win->capacity * 2);
+#pragma omp for schedule(static)
+    for (s = 0; s < win->n_sessions; ++s)
+      predict_one(pool, pids, win, adm, out, s, cands, st, st + win->capacity);
+    free(cands);
+    free(st);
+  }
+  return PASTE_OK;
+}

@@ -1,0 +1,145 @@
+"""ctypes binding of libpaste.so (the C ABI declared in include/paste.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` (or
+``python -m paper_2603_18897_b200.build``).  There is no fallback: if the
+library or a CUDA device is missing, every hot-path call raises
+:class:`NativeUnavailable`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_int, c_int32, c_int64, c_void_p
+
+import numpy as np
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpaste.so")
+
+PASTE_OK = 0
+PASTE_ERR_INVALID = -1
+PASTE_ERR_CUDA = -2
+PASTE_ERR_UNSUPPORTED = -3
+
+
+class NativeUnavailable(RuntimeError):
+    """libpaste.so or the CUDA device it needs is not available."""
+
+
+class PasteError(RuntimeError):
+    pass
+
+
+class PasteUnsupported(PasteError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# struct mirrors (field order and types must match include/paste.h)
+# ---------------------------------------------------------------------------
+
+class PoolDesc(ctypes.Structure):
+    _fields_ = [("n_patterns", c_int32), ("n_bucket_sigs", c_int32), ("k", c_int32),
+                ("relation", c_int32), ("max_ctx", c_int32), ("max_bindings", c_int32),
+                ("patterns", c_void_p), ("bindings", c_void_p), ("ctx_sig", c_void_p),
+                ("steps", c_void_p), ("bucket_off", c_void_p), ("bucket_pat", c_void_p),
+                ("bucket_scan_all", c_void_p)]
+
+
+class AdmitDesc(ctypes.Structure):
+    _fields_ = [("enabled", c_int32), ("n_tools", c_int32), ("allow", c_void_p),
+                ("max_level", c_void_p), ("benefit", c_void_p)]
+
+
+class WindowsDesc(ctypes.Structure):
+    _fields_ = [("n_sessions", c_int64), ("capacity", c_int32), ("pad", c_int32),
+                ("tok", c_void_p), ("evt", c_void_p), ("count", c_void_p),
+                ("nodes", c_void_p), ("bytes", c_void_p), ("refs", c_void_p),
+                ("new_tok", c_void_p), ("new_ref", c_void_p), ("new_evt_base", c_int64),
+                ("new_byte_base", c_int64)]
+
+
+class PredictOut(ctypes.Structure):
+    _fields_ = [("max_candidates", c_int32), ("max_bindings", c_int32),
+                ("n_pred", c_void_p), ("pred_pat", c_void_p), ("pred_comp", c_void_p),
+                ("pred_arg", c_void_p), ("n_act", c_void_p), ("act_pred", c_void_p),
+                ("act_level", c_void_p), ("act_util", c_void_p), ("struct_err", c_void_p)]
+
+
+class AdmitListsDesc(ctypes.Structure):
+    _fields_ = [("n_lists", c_int64), ("list_off", c_void_p), ("tool", c_void_p),
+                ("full", c_void_p), ("p", c_void_p), ("benefit", c_void_p),
+                ("created_at", c_void_p), ("n_act", c_void_p), ("act_pred", c_void_p),
+                ("act_level", c_void_p), ("act_util", c_void_p)]
+
+
+# numpy mirrors of the element structs
+PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
+                          ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
+BINDING_DTYPE = np.dtype([(name, "i4") for name in
+                          ("kind", "ctx_pos", "step_off", "step_cnt", "suf_off", "suf_cnt",
+                           "start_index", "fail_tool")])
+assert PATTERN_DTYPE.itemsize == 32 and BINDING_DTYPE.itemsize == 32
+
+# symbol -> (restype, argtypes); the list is checked against include/paste.h by tests
+EXPORTS = {
+    "paste_last_error": (c_char_p, []),
+    "paste_abi_version": (c_int, []),
+    "paste_last_launch_count": (c_int, []),
+    "paste_predict_batch": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc),
+                                    POINTER(AdmitDesc), POINTER(PredictOut), c_void_p]),
+    "paste_admit_lists": (c_int, [POINTER(AdmitDesc), POINTER(AdmitListsDesc), c_void_p]),
+}
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libpaste.so and declare every export (no device needed)."""
+    global _lib
+    if _lib is not None and path == LIB_PATH:
+        return _lib
+    if not os.path.exists(path):
+        raise NativeUnavailable(
+            f"{path} is missing: run __graft_entry__.build() to compile the sm_100a library")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in EXPORTS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.paste_abi_version() != 1:
+        raise NativeUnavailable("libpaste ABI version mismatch")
+    if path == LIB_PATH:
+        _lib = lib
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    """The library, with a CUDA device required (hot-path entry)."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device: the PASTE engine runs on B200 only "
+                                "(there is no CPU fallback)")
+    return load_library()
+
+
+def check(status: int, lib_handle: ctypes.CDLL | None = None) -> None:
+    if status == PASTE_OK:
+        return
+    handle = lib_handle or _lib
+    msg = handle.paste_last_error().decode() if handle is not None else "unknown error"
+    if status == PASTE_ERR_INVALID:
+        raise ValueError(msg)
+    if status == PASTE_ERR_UNSUPPORTED:
+        raise PasteUnsupported(msg)
+    raise PasteError(msg)
+
+
+def ptr(t) -> int:
+    """Device (or host) address of a torch tensor / numpy array, 0 for None."""
+    if t is None:
+        return 0
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()

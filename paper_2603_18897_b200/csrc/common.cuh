@@ -1,0 +1,80 @@
+// Shared device helpers for libpaste (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+
+#include "paste.h"
+
+namespace paste {
+
+// ---------------------------------------------------------------------------
+// error plumbing (thread-local last error, launch counting)
+// ---------------------------------------------------------------------------
+void set_error(const char* fmt, ...);
+void count_launch(int n = 1);
+void reset_launches();
+
+#define PASTE_CUDA_CHECK(expr)                                                   \
+  do {                                                                           \
+    cudaError_t _e = (expr);                                                     \
+    if (_e != cudaSuccess) {                                                     \
+      ::paste::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,              \
+                         cudaGetErrorString(_e));                                \
+      return PASTE_ERR_CUDA;                                                     \
+    }                                                                            \
+  } while (0)
+
+#define PASTE_REQUIRE(cond, ...)                                                 \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      ::paste::set_error(__VA_ARGS__);                                           \
+      return PASTE_ERR_INVALID;                                                  \
+    }                                                                            \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// tape access
+// ---------------------------------------------------------------------------
+struct Node {
+  uint32_t type_flags;  // byte0 type, byte1 flags
+  int32_t key;
+  uint32_t a, b;
+  __device__ __forceinline__ int type() const { return type_flags & 0xff; }
+  __device__ __forceinline__ int flags() const { return (type_flags >> 8) & 0xff; }
+  __device__ __forceinline__ uint32_t size() const { return type() >= PASTE_T_LIST ? b : 1u; }
+};
+
+__device__ __forceinline__ Node load_node(const paste_tape_node* nodes, int64_t i) {
+  uint4 v = __ldg(reinterpret_cast<const uint4*>(nodes) + i);
+  Node n;
+  n.type_flags = v.x;
+  n.key = (int32_t)v.y;
+  n.a = v.z;
+  n.b = v.w;
+  return n;
+}
+
+// Walk one path step from node `cur` (relative to node_base).  Returns the
+// child node index, or -1 when the step does not resolve (mappings.py:143-153:
+// int step needs a list and 0 <= step < len; key step needs a dict holding it).
+__device__ __forceinline__ int64_t step_child(const paste_tape_node* nodes, int64_t base,
+                                              int64_t cur, int32_t kind, int32_t value) {
+  Node nd = load_node(nodes, base + cur);
+  int64_t child = cur + 1;
+  if (kind == 0) {
+    if (nd.type() != PASTE_T_DICT) return -1;
+    for (uint32_t c = 0; c < nd.a; ++c) {
+      Node cn = load_node(nodes, base + child);
+      if (cn.key == value) return child;
+      child += cn.size();
+    }
+    return -1;
+  }
+  if (nd.type() != PASTE_T_LIST || value < 0 || (uint32_t)value >= nd.a) return -1;
+  for (int32_t c = 0; c < value; ++c) child += load_node(nodes, base + child).size();
+  return child;
+}
+
+}  // namespace paste

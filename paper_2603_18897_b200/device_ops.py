@@ -1,0 +1,183 @@
+"""Device execution of the reference-shaped API calls.
+
+Each function here packs host objects (:mod:`.packing`), moves the arrays to
+HBM with torch, calls one libpaste entry point through the C ABI, copies the
+compact result records back and rebuilds reference objects.  torch is used
+for device memory and streams only.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Any, Callable, Sequence
+
+import numpy as np
+
+from . import _native
+from ._native import AdmitDesc, AdmitListsDesc, PoolDesc, PredictOut, WindowsDesc, check, ptr
+from .packing import (C_FULL, PoolImage, PredictResult, SigTable, admit_tables, decode_actions,
+                      decode_predictions, pack_windows)
+from .tape import KeyTable
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def to_dev(arr: np.ndarray):
+    """numpy (incl. structured) -> contiguous CUDA tensor with the same bytes."""
+    torch = _torch()
+    a = np.ascontiguousarray(arr)
+    if a.dtype.names is not None or a.dtype == np.uint8:
+        t = torch.from_numpy(a.view(np.uint8).reshape(-1))
+    else:
+        t = torch.from_numpy(a)
+    return t.to("cuda", non_blocking=False)
+
+
+def stream_handle() -> int:
+    return _torch().cuda.current_stream().cuda_stream
+
+
+class DevicePool:
+    """A pattern pool compiled into a device-resident PoolImage."""
+
+    def __init__(self, pool, sigs: SigTable | None = None, keys: KeyTable | None = None):
+        self.pool = pool
+        self.sigs = SigTable() if sigs is None else sigs
+        self.keys = KeyTable() if keys is None else keys
+        self.image = PoolImage.compile(pool, self.sigs, self.keys)
+        self._dev: dict[str, Any] | None = None
+
+    def device_arrays(self) -> dict[str, Any]:
+        if self._dev is None:
+            _native.lib()  # fail loudly without the library / a device
+            im = self.image
+            self._dev = {name: to_dev(getattr(im, name)) for name in
+                         ("patterns", "bindings", "ctx_sig", "steps", "bucket_off", "bucket_pat")}
+            self._dev["bucket_scan_all"] = to_dev(
+                im.bucket_scan_all if len(im.bucket_scan_all) else np.zeros(1, np.uint8))
+        return self._dev
+
+    def desc(self) -> PoolDesc:
+        d = self.device_arrays()
+        im = self.image
+        return PoolDesc(len(im.pool.patterns), im.n_bucket_sigs, im.k, im.relation, im.max_ctx,
+                        im.max_bindings, ptr(d["patterns"]), ptr(d["bindings"]), ptr(d["ctx_sig"]),
+                        ptr(d["steps"]), ptr(d["bucket_off"]), ptr(d["bucket_pat"]),
+                        ptr(d["bucket_scan_all"]))
+
+    # -- predict -------------------------------------------------------------
+
+    def _run(self, batch, K: int, admit: tuple[np.ndarray, np.ndarray, np.ndarray] | None
+             ) -> PredictResult:
+        torch = _torch()
+        lib = _native.lib()
+        n = batch.n
+        B = max(self.image.max_bindings, 1)
+        nodes, data, refs = batch.arena.arrays()
+        tok, evt, count = to_dev(batch.tok), to_dev(batch.evt), to_dev(batch.count)
+        d_nodes, d_data, d_refs = to_dev(nodes), to_dev(data), to_dev(refs)
+        win = WindowsDesc(n, batch.capacity, 0, ptr(tok), ptr(evt), ptr(count), ptr(d_nodes),
+                          ptr(d_data), ptr(d_refs), 0, 0, 0, 0)
+        dev = torch.device("cuda")
+        o = {"n_pred": torch.zeros(n, dtype=torch.int32, device=dev),
+             "pred_pat": torch.zeros(n * K, dtype=torch.int32, device=dev),
+             "pred_comp": torch.zeros(n * K, dtype=torch.uint8, device=dev),
+             "pred_arg": torch.full((n * K * B,), -1, dtype=torch.int64, device=dev),
+             "struct_err": torch.zeros(n, dtype=torch.int32, device=dev)}
+        if admit is not None:
+            o["n_act"] = torch.zeros(n, dtype=torch.int32, device=dev)
+            o["act_pred"] = torch.zeros(n * K, dtype=torch.int16, device=dev)
+            o["act_level"] = torch.zeros(n * K, dtype=torch.uint8, device=dev)
+            o["act_util"] = torch.zeros(n * K, dtype=torch.float64, device=dev)
+            allow, level, bene = (to_dev(x) for x in admit)
+            adm = AdmitDesc(1, len(admit[0]), ptr(allow), ptr(level), ptr(bene))
+        else:
+            adm = AdmitDesc(0, 0, 0, 0, 0)
+        out = PredictOut(K, B, ptr(o["n_pred"]), ptr(o["pred_pat"]), ptr(o["pred_comp"]),
+                         ptr(o["pred_arg"]), ptr(o.get("n_act")), ptr(o.get("act_pred")),
+                         ptr(o.get("act_level")), ptr(o.get("act_util")), ptr(o["struct_err"]))
+        pool = self.desc()
+        check(lib.paste_predict_batch(ctypes.byref(pool), ctypes.byref(win), ctypes.byref(adm),
+                                      ctypes.byref(out), stream_handle()), lib)
+        h = {k: v.cpu().numpy() for k, v in o.items()}
+        return PredictResult(K, B, h["n_pred"], h["pred_pat"], h["pred_comp"], h["pred_arg"],
+                             h.get("n_act"), h.get("act_pred"), h.get("act_level"),
+                             h.get("act_util"), h["struct_err"])
+
+    def _k_for(self, max_candidates: int | None) -> tuple[int, bool]:
+        """Kernel slot count; truncation with Python slice semantics for
+        non-positive values is applied on the host."""
+        if max_candidates is not None and max_candidates > 0:
+            return max_candidates, False
+        return max(self.image.max_bucket, 1), max_candidates is not None
+
+    def predict_windows(self, windows: Sequence[Sequence], now: float | None,
+                        max_candidates: int | None):
+        K, slice_after = self._k_for(max_candidates)
+        batch = pack_windows(windows, self.sigs, self.keys)
+        res = self._run(batch, K, None)
+        preds = decode_predictions(res, self.image, batch.arena, batch.created, now)
+        if slice_after:
+            preds = [p[:max_candidates] for p in preds]
+        return preds, int(res.struct_err.sum())
+
+    def predict_admit_windows(self, windows: Sequence[Sequence], policy, estimates,
+                              now: float | None, max_candidates: int | None):
+        K, slice_after = self._k_for(max_candidates)
+        if slice_after:
+            raise ValueError("predict_admit_batch needs a positive max_candidates")
+        batch = pack_windows(windows, self.sigs, self.keys)
+        tables = admit_tables(self.sigs, policy, estimates.duration)
+        res = self._run(batch, K, tables)
+        preds = decode_predictions(res, self.image, batch.arena, batch.created, now)
+        return preds, decode_actions(res, preds), int(res.struct_err.sum())
+
+
+# ---------------------------------------------------------------------------
+# standalone admit
+# ---------------------------------------------------------------------------
+
+
+def admit_lists(lists: Sequence[Sequence], policy, benefit_of: Callable[[Any], float]):
+    from .policy import SpecLevel, SpeculativeAction
+    from .prediction import Completeness
+
+    torch = _torch()
+    lib = _native.lib()
+    sigs = SigTable()
+    flat = [p for lst in lists for p in lst]
+    off = np.zeros(len(lists) + 1, np.int64)
+    off[1:] = np.cumsum([len(lst) for lst in lists])
+    tool = np.array([sigs.tool(p.tool_type) for p in flat] or [0], np.int32)
+    full = np.array([p.completeness is Completeness.FULL for p in flat] or [0], np.uint8)
+    prob = np.array([p.probability for p in flat] or [0], np.float64)
+    bene = np.array([benefit_of(p) for p in flat] or [0], np.float64)
+    created = np.array([p.created_at for p in flat] or [0], np.float64)
+    allow, level, _ = admit_tables(sigs, policy, lambda name: 0.0)
+    d = {k: to_dev(v) for k, v in dict(off=off, tool=tool, full=full, prob=prob, bene=bene,
+                                       created=created, allow=allow, level=level).items()}
+    N = max(len(flat), 1)
+    dev = torch.device("cuda")
+    n_act = torch.zeros(len(lists) or 1, dtype=torch.int32, device=dev)
+    act_pred = torch.zeros(N, dtype=torch.int32, device=dev)
+    act_level = torch.zeros(N, dtype=torch.uint8, device=dev)
+    act_util = torch.zeros(N, dtype=torch.float64, device=dev)
+    adm = AdmitDesc(1, len(allow), ptr(d["allow"]), ptr(d["level"]), 0)
+    desc = AdmitListsDesc(len(lists), ptr(d["off"]), ptr(d["tool"]), ptr(d["full"]),
+                          ptr(d["prob"]), ptr(d["bene"]), ptr(d["created"]), ptr(n_act),
+                          ptr(act_pred), ptr(act_level), ptr(act_util))
+    check(lib.paste_admit_lists(ctypes.byref(adm), ctypes.byref(desc), stream_handle()), lib)
+    n_act, act_pred = n_act.cpu().numpy(), act_pred.cpu().numpy()
+    act_level, act_util = act_level.cpu().numpy(), act_util.cpu().numpy()
+    out = []
+    for li, lst in enumerate(lists):
+        b0 = int(off[li])
+        out.append([SpeculativeAction(prediction=lst[int(act_pred[b0 + j])],
+                                      level=SpecLevel(int(act_level[b0 + j])),
+                                      expected_utility=float(act_util[b0 + j]))
+                    for j in range(int(n_act[li]))])
+    return out

@@ -1,0 +1,227 @@
+"""Columnar synthetic agent traces for the benchmark configurations.
+
+The reference generates traces object by object (workloads.py:297-331, about
+0.3 s per 1k sessions); 1M live sessions need a vectorised generator.  This
+one reproduces the reference's motif structure and payload shapes:
+
+* motifs (workloads.py:102-214): search -> web_fetch (+ retry after a
+  failure), file_editor -> terminal, grep -> file_editor, search -> batch of
+  web_fetch;
+* results use the shapes of ``tool_result`` (simulation.py:150-178): url_list
+  ``{"list": [{"url", "rank"}...], "total"}``, file_hits ``{"hits": [{"path",
+  "line"}...], "count"}``, edit ``{"path", "applied"}``, echo ``{"ok",
+  "token"}`` and the failure form ``{"ok": false, "error", "token"}``.
+
+Payload tapes are *shape-interned*: every payload of one kind has the same
+node array (only its scalar bytes differ), so events share one node template
+and carry only their own bytes -- ``paste_event_ref.node_base`` points at the
+template, ``byte_base`` at the event's bytes.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .tape import KeyTable, TapeArena
+
+TOOLS = ("search", "web_fetch", "file_editor", "terminal", "grep")
+SEARCH, FETCH, EDITOR, TERMINAL, GREP = range(5)
+MOTIFS = ("search_visit", "edit_verify", "locate_examine", "batch_fetch")
+
+# payload kinds
+K_SEARCH, K_GREP, K_EDIT, K_ECHO, K_FAIL = range(5)
+_HEX = np.frombuffer(b"0123456789abcdef", dtype=np.uint8)
+
+
+def _sample_payloads() -> dict[int, tuple[object, bool]]:
+    """Payload samples with 'X' placeholders; bool = all runs share one value."""
+    return {
+        K_SEARCH: ({"list": [{"url": f"https://XXXXXXXX-{i}.example/doc", "rank": i}
+                             for i in range(5)], "total": 5}, True),
+        K_GREP: ({"hits": [{"path": f"src/mXXXXXXXX_{i}.py", "line": 10 * (i + 1)}
+                           for i in range(4)], "count": 4}, True),
+        K_EDIT: ({"path": "src/fix_XXXXXXXXXX.py", "applied": True}, False),
+        K_ECHO: ({"ok": True, "token": "XXXXXXXXXXXXXXXX"}, False),
+        K_FAIL: ({"ok": False, "error": "execution_failed", "token": "XXXXXXXXXXXXXXXX"}, False),
+    }
+
+
+@dataclass
+class ShapeTemplates:
+    nodes: np.ndarray              # NODE_DTYPE, all templates back to back
+    node_base: np.ndarray          # i64[kind]
+    byte_tmpl: list[np.ndarray]    # per kind template bytes
+    runs: list[np.ndarray]         # per kind: [n_runs, run_len] byte positions of 'X'
+    shared: list[bool]
+
+
+def make_templates(keys: KeyTable) -> ShapeTemplates:
+    arena = TapeArena(keys, keep_objects=False)
+    samples = _sample_payloads()
+    for k in range(len(samples)):
+        arena.add(samples[k][0])
+    nodes, data, refs = arena.arrays()
+    byte_tmpl, runs, shared = [], [], []
+    for k in range(len(samples)):
+        b0 = int(refs[k, 1])
+        b1 = int(refs[k + 1, 1]) if k + 1 < len(samples) else len(data)
+        tmpl = data[b0:b1].copy()
+        pos = np.flatnonzero(tmpl == ord("X"))
+        # split into runs of consecutive positions
+        cuts = np.flatnonzero(np.diff(pos) != 1) + 1
+        groups = np.split(pos, cuts) if len(pos) else []
+        runs.append(np.stack(groups) if groups else np.zeros((0, 0), np.int64))
+        byte_tmpl.append(tmpl)
+        shared.append(samples[k][1])
+    return ShapeTemplates(nodes, refs[:, 0].copy(), byte_tmpl, runs, shared)
+
+
+def payload_kind(tool: np.ndarray, ok: np.ndarray) -> np.ndarray:
+    kind = np.full(tool.shape, K_ECHO, np.int8)
+    kind[tool == SEARCH] = K_SEARCH
+    kind[tool == GREP] = K_GREP
+    kind[tool == EDITOR] = K_EDIT
+    kind[~ok] = K_FAIL
+    return kind
+
+
+def fill_payloads(tmpl: ShapeTemplates, kind: np.ndarray, rng: np.random.Generator,
+                  byte_offset: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    """Bytes for a batch of payloads: returns (bytes u8[], refs i64[n,2])."""
+    n = len(kind)
+    # bytes are laid out grouped by kind (refs carry each event's byte base)
+    starts = np.zeros(n, np.int64)
+    blocks = []
+    at = 0
+    for k in range(len(tmpl.byte_tmpl)):
+        idx = np.flatnonzero(kind == k)
+        if not len(idx):
+            continue
+        t = tmpl.byte_tmpl[k]
+        block = np.broadcast_to(t, (len(idx), len(t))).copy()
+        runs = tmpl.runs[k]
+        if runs.size:
+            n_runs, run_len = runs.shape
+            if tmpl.shared[k]:
+                hexes = _HEX[rng.integers(0, 16, (len(idx), run_len), dtype=np.uint8)]
+                for r in range(n_runs):
+                    block[:, runs[r]] = hexes
+            else:
+                hexes = _HEX[rng.integers(0, 16, (len(idx), n_runs * run_len), dtype=np.uint8)]
+                block[:, runs.reshape(-1)] = hexes
+        starts[idx] = at + np.arange(len(idx), dtype=np.int64) * len(t)
+        at += block.size
+        blocks.append(block.reshape(-1))
+    out = np.concatenate(blocks) if blocks else np.zeros(1, np.uint8)
+    refs = np.empty((n, 2), np.int64)
+    refs[:, 0] = tmpl.node_base[kind]
+    refs[:, 1] = starts + byte_offset
+    return out, refs
+
+
+class MotifStream:
+    """Per-session motif state machines advanced one tool call at a time.
+
+    Transitions follow the reference's scripts with its default rates
+    (visit 0.51, verify 0.55, open 0.38; batch_fetch issues ``fetch_count``
+    fetches after one search); web_fetch / terminal fail with probability
+    ``fail_rate`` and a failed fetch is retried once (search_visit retry).
+    """
+
+    def __init__(self, n_sessions: int, seed: int, fail_rate: float = 0.05,
+                 fetch_count: int = 15):
+        self.n = n_sessions
+        self.rng = np.random.default_rng(seed)
+        self.motif = self.rng.integers(0, len(MOTIFS), n_sessions, dtype=np.int8)
+        self.prev = np.full(n_sessions, -1, np.int8)
+        self.prev_ok = np.ones(n_sessions, bool)
+        self.run = np.zeros(n_sessions, np.int16)  # fetches since last search (batch)
+        self.fail_rate = fail_rate
+        self.fetch_count = fetch_count
+
+    def step(self) -> tuple[np.ndarray, np.ndarray]:
+        """Next (tool id in TOOLS, ok) per session."""
+        u = self.rng.random(self.n)
+        m, prev, ok_prev = self.motif, self.prev, self.prev_ok
+        nxt = np.empty(self.n, np.int8)
+        # search_visit: search -> fetch (0.51) | search; failed fetch -> retry fetch
+        sv = m == 0
+        nxt[sv] = SEARCH
+        sel = sv & (prev == SEARCH) & (u < 0.51)
+        nxt[sel] = FETCH
+        nxt[sv & (prev == FETCH) & ~ok_prev] = FETCH
+        # edit_verify: editor -> terminal (0.55) | editor
+        ev = m == 1
+        nxt[ev] = EDITOR
+        nxt[ev & (prev == EDITOR) & (u < 0.55)] = TERMINAL
+        # locate_examine: grep -> editor (0.38) | grep
+        le = m == 2
+        nxt[le] = GREP
+        nxt[le & (prev == GREP) & (u < 0.38)] = EDITOR
+        # batch_fetch: search then fetch_count fetches, repeat
+        bf = m == 3
+        nxt[bf] = FETCH
+        restart = bf & ((prev == -1) | (self.run >= self.fetch_count))
+        nxt[restart] = SEARCH
+        self.run[bf & (nxt == SEARCH)] = 0
+        self.run[bf & (nxt == FETCH)] += 1
+        ok = np.ones(self.n, bool)
+        may_fail = (nxt == FETCH) | (nxt == TERMINAL)
+        ok[may_fail] = self.rng.random(int(may_fail.sum())) >= self.fail_rate
+        self.prev, self.prev_ok = nxt, ok
+        return nxt, ok
+
+
+def sig_map(sigs) -> np.ndarray:
+    """TOOLS index -> tool id in a SigTable (interning missing tools)."""
+    return np.array([sigs.tool(t) for t in TOOLS], np.int32)
+
+
+def tokens(tool: np.ndarray, ok: np.ndarray, tool_ids: np.ndarray) -> np.ndarray:
+    return (2 * tool_ids[tool] + ok.astype(np.int32)).astype(np.int32)
+
+
+class LiveWorkload:
+    """C3 generator: N sessions, one new tool event per session per batch."""
+
+    def __init__(self, sigs, keys, n_sessions: int, seed: int = 2603, fail_rate: float = 0.05):
+        self.n = n_sessions
+        self.tmpl = make_templates(keys)
+        self.stream = MotifStream(n_sessions, seed, fail_rate=fail_rate)
+        self.tool_ids = sig_map(sigs)
+        self.rng = np.random.default_rng(seed + 1)
+        self.max_batch_bytes = n_sessions * max(len(t) for t in self.tmpl.byte_tmpl)
+
+    def next_batch(self):
+        from .live import EventBatch
+
+        tool, ok = self.stream.step()
+        kind = payload_kind(tool, ok)
+        data, ref = fill_payloads(self.tmpl, kind, self.rng)
+        return EventBatch(tokens(tool, ok, self.tool_ids), ref, data)
+
+
+def stress_pool(seed: int = 1001, n_patterns: int = 1000, n_tools: int = 20):
+    """The 1,000-pattern / 20-tool stress pool of the reference's runtime
+    overhead criterion (test_acceptance.py:507-527), regenerated from its
+    recipe: random contexts of 1-3 signatures, distinct (context, target)."""
+    import random
+
+    from .events import EventSignature, Status
+    from .mining import MiningConfig, PatternPool, PatternTuple
+
+    rng = random.Random(seed)
+    tools = [f"tool{i}" for i in range(n_tools)]
+    pats, seen = [], set()
+    while len(pats) < n_patterns:
+        ctx = tuple(EventSignature(rng.choice(tools), rng.choice([Status.SUCCESS, Status.FAIL]))
+                    for _ in range(rng.randint(1, 3)))
+        target = rng.choice(tools)
+        if (ctx, target) in seen:
+            continue
+        seen.add((ctx, target))
+        pats.append(PatternTuple(context=ctx, target=target, mapping=None,
+                                 p=round(rng.uniform(0.3, 1.0), 4), support=5))
+    return PatternPool(config=MiningConfig(), patterns=tuple(pats))

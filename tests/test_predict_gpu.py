@@ -1,0 +1,170 @@
+"""K4 parity on the GPU: the CUDA predict / admit path against the reference's
+golden vectors and, at scale, against the pinned CPU oracle (bit-exact)."""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import bridge  # noqa: E402
+from paper_2603_18897_b200 import admit  # noqa: E402
+from paper_2603_18897_b200.device_ops import DevicePool  # noqa: E402
+from paper_2603_18897_b200.live import LiveSessionTable  # noqa: E402
+from paper_2603_18897_b200.mining import load_pool  # noqa: E402
+from paper_2603_18897_b200.packing import PredictResult, WindowBatch, admit_tables  # noqa: E402
+from paper_2603_18897_b200.policy import parse_policy  # noqa: E402
+from paper_2603_18897_b200.prediction import PredictionWindow, Predictor  # noqa: E402
+from paper_2603_18897_b200.scheduling import EstimateBook  # noqa: E402
+from paper_2603_18897_b200.synth import LiveWorkload, stress_pool  # noqa: E402
+
+CASES = G.golden("predict_golden.json")["cases"]
+MOTIF_POLICY = """
+speculation_policy:
+  default: {allow: false}
+  tools:
+    web_fetch: {allow: true, max_speculation: full}
+    terminal: {allow: true, max_speculation: dry_run}
+    search: {allow: true, max_speculation: full}
+    file_editor: {allow: true, max_speculation: dry_run}
+"""
+
+
+def _windows(case):
+    out = []
+    for w in case["windows"]:
+        win = PredictionWindow(16)
+        for e in w:
+            win.observe(G.event(e))
+        out.append(win)
+    return out
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_predict_matches_reference_golden(case):
+    pool = G.pool(case["pool"])
+    predictor = Predictor(pool)
+    wins = _windows(case)
+    K = case["max_candidates"]
+    preds = predictor.predict_batch(wins, max_candidates=K)
+    for got, exp in zip(preds, case["expected"]):
+        assert G.same([G.pred_dict(p) for p in got], exp)
+    assert predictor.diagnostics.structural_errors == case["structural_errors"]
+    pol = G.policy(case["policy"])
+    if pol is None:
+        return
+    book = G.estimates(case["estimates"])
+    if K is not None and K <= 32:  # fused predict + admit kernel
+        preds2, acts = predictor.predict_admit_batch(wins, pol, book, max_candidates=K)
+    else:  # standalone admit kernel on the predictions
+        preds2 = preds
+        acts = [admit(p, pol, lambda pr: book.duration(pr.tool_type)) for p in preds]
+    for s, (got, exp) in enumerate(zip(acts, case["expected_actions"])):
+        assert [(preds2[s].index(a.prediction), int(a.level), a.expected_utility)
+                for a in got] == [(e["pred"], e["level"], e["utility"]) for e in exp]
+
+
+def test_single_window_predict_api():
+    case = next(c for c in CASES if c["name"] == "fetch_pool")
+    predictor = Predictor(G.pool(case["pool"]))
+    for win, exp in zip(_windows(case), case["expected"]):
+        assert G.same([G.pred_dict(p) for p in predictor.predict(win)], exp)
+
+
+def test_admit_matches_reference_golden():
+    from paper_2603_18897_b200.prediction import Completeness, PredictedInvocation
+
+    g = G.golden("admit_golden.json")
+    pol = G.policy(g["policy"])
+    bene = g["benefit"]
+    for item in g["lists"]:
+        preds = [PredictedInvocation(p["tool"], p["args"], Completeness(p["completeness"]), p["p"],
+                                     p["pattern"], p["created_at"]) for p in item["preds"]]
+        acts = admit(preds, pol, lambda p: bene[p.tool_type] * (1 + p.created_at % 2))
+        assert [(preds.index(a.prediction), int(a.level), a.expected_utility) for a in acts] == \
+            [(a["pred"], a["level"], a["utility"]) for a in item["actions"]]
+
+
+def _compare(dev: PredictResult, ora: PredictResult):
+    assert np.array_equal(dev.n_pred, ora.n_pred)
+    assert np.array_equal(dev.struct_err, ora.struct_err)
+    K, B = dev.K, dev.B
+    slot_valid = (np.arange(K)[None, :] < dev.n_pred[:, None]).reshape(-1)
+    assert np.array_equal(dev.pred_pat[slot_valid], ora.pred_pat[slot_valid])
+    assert np.array_equal(dev.pred_comp[slot_valid], ora.pred_comp[slot_valid])
+    arg_valid = np.repeat(slot_valid & (dev.pred_comp != 2), B)
+    assert np.array_equal(dev.pred_arg[arg_valid], ora.pred_arg[arg_valid])
+    assert np.array_equal(dev.n_act, ora.n_act)
+    act_valid = (np.arange(K)[None, :] < dev.n_act[:, None]).reshape(-1)
+    assert np.array_equal(dev.act_pred[act_valid], ora.act_pred[act_valid])
+    assert np.array_equal(dev.act_level[act_valid], ora.act_level[act_valid])
+    # fp64 utilities: same single multiply -> bit-exact (tolerance 1e-6 rel not needed)
+    assert np.array_equal(dev.act_util[act_valid].view(np.int64),
+                          ora.act_util[act_valid].view(np.int64))
+
+
+def _live_vs_oracle(dp, n, steps, seed, policy, book, K=8, workload=None):
+    wl = workload or LiveWorkload(dp.sigs, dp.keys, n, seed=seed)
+    table = LiveSessionTable(dp, n, wl.tmpl.nodes, wl.max_batch_bytes, policy, book,
+                             max_candidates=K)
+    W, R = table.W, table.regions
+    host = WindowBatch(W, np.full(n * W, -1, np.int32), np.full(n * W, -1, np.int32),
+                       np.zeros(n, np.int64), None, [])
+    refs = np.zeros((R * n, 2), np.int64)
+    host.arena = (wl.tmpl.nodes, np.zeros(1, np.uint8), refs)
+    tables = admit_tables(dp.sigs, policy, book.duration)
+    total_preds = 0
+    for step in range(steps):
+        batch = wl.next_batch()
+        region = step % R
+        table.step(batch)
+        dev = table.fetch()
+        ora = bridge.predict(dp.image, host, K, tables, new_tok=batch.tok,
+                             new_ref=np.ascontiguousarray(batch.ref), new_evt_base=region * n,
+                             new_byte_base=region * table.max_batch_bytes, threads=8)
+        _compare(dev, ora)
+        total_preds += int(dev.n_pred.sum())
+    state = table.host_state()
+    assert np.array_equal(state["tok"], host.tok) and np.array_equal(state["count"], host.count)
+    return total_preds
+
+
+def test_live_c3_pool_matches_oracle():
+    pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
+    book = EstimateBook()
+    for tool, ms in (("search", 700.0), ("web_fetch", 1080.0), ("file_editor", 300.0),
+                     ("terminal", 1420.0), ("grep", 400.0)):
+        book.update(tool, ms)
+    n_preds = _live_vs_oracle(DevicePool(pool), 20_000, 24, 7, parse_policy(MOTIF_POLICY).policy, book)
+    assert n_preds > 20_000 * 24  # the pool fires on this workload
+
+
+def test_live_stress_pool_matches_oracle():
+    """1,000-pattern pool; the synthetic tools are renamed onto the pool's tools."""
+    from paper_2603_18897_b200 import synth
+    from paper_2603_18897_b200.policy import SpeculationPolicy
+
+    pool = stress_pool()
+    dp = DevicePool(pool)
+
+    class Renamed(LiveWorkload):
+        def __init__(self):
+            super().__init__(dp.sigs, dp.keys, 10_000, seed=3)
+            self.rng2 = np.random.default_rng(9)
+
+        def next_batch(self):
+            b = super().next_batch()
+            tools = self.rng2.integers(0, 20, len(b.tok))
+            ok = self.rng2.random(len(b.tok)) < 0.7
+            b.tok = (2 * np.array([dp.sigs.tool(f"tool{t}") for t in range(20)])[tools]
+                     + ok).astype(np.int32)
+            return b
+
+    n = _live_vs_oracle(dp, 10_000, 20, 3, SpeculationPolicy(default_allow=True), EstimateBook(),
+                        K=8, workload=Renamed())
+    assert n > 0
