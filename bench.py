@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""PASTE-B200 benchmark (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[2], "C3"): 1M concurrent live sessions,
+window W=16, top-8 candidate scoring.  One *step* = every session observes one
+new tool event and gets its top-8 predictions plus admitted speculative
+actions (Predictor.predict(max_candidates=8) + admit(benefit = EWMA duration),
+simulation.py:415-429) -- one fused kernel launch over all sessions.
+
+* ``value``  -- sessions/s with the step's inputs already resident in HBM
+  (device time, CUDA events on the launch stream, L2 flushed between steps).
+* ``e2e``    -- the same through the public live API (LiveSessionTable.step +
+  fetch) with the new events copied from pinned host memory and the result
+  records copied back every step.
+* ``--impl reference`` -- the CPU oracle port of the reference algorithm
+  (oracle/paste_oracle.c, all host threads) on the same workload.
+
+Multi-GPU (torchrun): live prediction does not shard a collective; each rank
+serves its own 1M sessions (replicas, weak scaling), max time over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "speculative predictions/sec (1M sessions)"
+UNIT = "sessions/s"
+MOTIF_POLICY = """
+speculation_policy:
+  default: {allow: false}
+  tools:
+    web_fetch: {allow: true, max_speculation: full}
+    terminal: {allow: true, max_speculation: dry_run}
+    search: {allow: true, max_speculation: full}
+    file_editor: {allow: true, max_speculation: dry_run}
+"""
+# EWMA duration estimates seeded with the motif tools' mean latencies
+# (workloads.py:266-283: fixed / lognormal median * exp(sigma^2/2) + init overhead)
+DURATIONS = {"search": 700.0, "web_fetch": 1078.8, "file_editor": 300.0, "terminal": 1424.2,
+             "grep": 400.0}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sessions", type=int, default=1_000_000)
+    ap.add_argument("--pool", default="c3", choices=["c3", "stress"])
+    ap.add_argument("--max-candidates", type=int, default=8)
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def load_setup(args):
+    from paper_2603_18897_b200.mining import load_pool
+    from paper_2603_18897_b200.policy import SpeculationPolicy, parse_policy
+    from paper_2603_18897_b200.scheduling import EstimateBook
+    from paper_2603_18897_b200.synth import stress_pool
+
+    if args.pool == "c3":
+        pool = load_pool(os.path.join(ROOT, "paper_2603_18897_b200", "data", "pool_motif_c3.json"))
+        policy = parse_policy(MOTIF_POLICY).policy
+    else:
+        pool = stress_pool()
+        policy = SpeculationPolicy(default_allow=True)
+    book = EstimateBook()
+    for tool, ms in DURATIONS.items():
+        book.update(tool, ms)
+    return pool, policy, book
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def __enter__(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines()]
+        except OSError:
+            rows = []
+        rows = [r for r in rows if len(r) >= 7 and r[0].strip() == str(self.gpu)]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def algorithmic_bytes(res, n, K, B):
+    """Bytes one step must move per the algorithm (K4):
+    per session 92 read (count 8, W=16 ring tokens 64, new event 20) + 44
+    written (count, ring slot, directory entry, 3 counters); per prediction
+    5 (pattern, completeness) + 28 per resolved binding (arg ref 8, source
+    event slot 4 + directory entry 16); per action 11."""
+    import numpy as np
+
+    n_pred = int(res.n_pred.sum())
+    n_act = int(res.n_act.sum())
+    valid = (np.arange(K)[None, :] < res.n_pred[:, None]).reshape(-1)
+    mapped = valid & (res.pred_comp != 2)
+    n_bind = int(mapped.sum()) * B
+    return n * 136 + n_pred * 5 + n_bind * 28 + n_act * 11, n_pred, n_act
+
+
+def l2_flush(buf):
+    buf.add_(1)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_18897_b200 import _native
+    from paper_2603_18897_b200.device_ops import DevicePool
+    from paper_2603_18897_b200.live import LiveSessionTable
+    from paper_2603_18897_b200.synth import LiveWorkload
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pool, policy, book = load_setup(args)
+    dp = DevicePool(pool)
+    n, K = args.sessions, args.max_candidates
+    wl = LiveWorkload(dp.sigs, dp.keys, n, seed=2603 + rank)
+    table = LiveSessionTable(dp, n, wl.tmpl.nodes, wl.max_batch_bytes, policy, book,
+                             max_candidates=K)
+    lib = _native.lib()
+    # fill every window (W steps), untimed
+    for _ in range(table.W):
+        table.step(wl.next_batch())
+    torch.cuda.synchronize()
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    W_, S_ = args.warmup, args.steps
+
+    # ---- device-resident loop: stage inputs first ----------------------------
+    staged = []
+    for i in range(W_ + S_):
+        b = wl.next_batch()
+        region = table.steps % table.regions
+        tok = torch.from_numpy(b.tok).cuda()
+        ref = torch.from_numpy(np.ascontiguousarray(b.ref).reshape(-1)).cuda()
+        staged.append((region, tok, ref))
+        table.steps += 1
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    for region, tok, ref in staged[:W_]:
+        table.launch(region, tok, ref)
+    torch.cuda.synchronize()
+    times, alg, preds, acts, launches = [], 0, 0, 0, 0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t_wall = time.perf_counter()
+        for region, tok, ref in staged[W_:]:
+            l2_flush(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            table.launch(region, tok, ref)
+            e1.record(stream)
+            launches += lib.paste_last_launch_count()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+            res = table.fetch()
+            b_, p_, a_ = algorithmic_bytes(res, n, K, table.B)
+            alg, preds, acts = alg + b_, preds + p_, acts + a_
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t_wall
+    dev_s = sum(times)
+    if world > 1:
+        t = torch.tensor([dev_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+
+    # ---- end-to-end through the public API ------------------------------------
+    host_batches = []
+    for i in range(W_ + S_):
+        b = wl.next_batch()
+        b.tok = torch.from_numpy(b.tok).pin_memory()
+        b.ref = torch.from_numpy(np.ascontiguousarray(b.ref)).pin_memory()
+        b.data = torch.from_numpy(b.data).pin_memory()
+        host_batches.append(b)
+    pinned = table.pinned_outputs()
+    h2d = d2h = 0
+    for b in host_batches[:W_]:
+        table.step(b)
+        table.fetch(pinned)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2e_times = []
+    for b in host_batches[W_:]:
+        l2_flush(flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        table.step(b)
+        table.fetch(pinned)  # D2H into pinned buffers + stream sync
+        e1.record(stream)
+        e1.synchronize()
+        e2e_times.append(e0.elapsed_time(e1) / 1e3)
+        h2d += b.nbytes(with_data=table.ship_bytes)
+        d2h += table.output_nbytes()
+    e2e_s = sum(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    peak, peak_kind = measured_peaks()
+    achieved = alg / dev_s / 1e9
+    out = {
+        "metric": METRIC, "value": world * n * S_ / dev_s, "unit": UNIT, "n_gpus": world,
+        "steps": S_, "warmup": W_, "ms_per_step": 1e3 * dev_s / S_, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32+f64", "data": "synthetic",
+        "config": {"workload": "C3: live sessions, suffix window 16, top-8 predict + admit",
+                   "sessions_per_gpu": n, "window": table.W, "max_candidates": K,
+                   "pool": f"{args.pool} ({len(pool.patterns)} patterns)",
+                   "policy": "motif-tool policy" if args.pool == "c3" else "allow-all",
+                   "parallelism": f"replicas x{world}",
+                   "l2": "flushed (256 MB write) between timed steps"},
+        "candidates_per_s": world * preds / dev_s,
+        "actions_per_s": world * acts / dev_s,
+        "e2e": {"value": world * n * S_ / e2e_s, "unit": UNIT,
+                "h2d_bytes_per_step": h2d // S_, "d2h_bytes_per_step": d2h // S_,
+                "ms_per_step": 1e3 * e2e_s / S_},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": committed_traffic(),
+                     "kernel": "predict_kernel", "algorithmic_bytes_per_launch": alg // S_,
+                     "peak_source": f"{peak_kind} hbm_gbs"},
+        "gpu_launches": launches,
+        "wall_s_timed_region": wall,
+    }
+    clk = clocks.summary()
+    out["clocks"] = clk
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget_s)
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out))
+
+
+def committed_traffic():
+    """dram bytes per launch of predict_kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_predict_summary.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def oracle_live_run(args, n, threads, budget_s, max_steps=64):
+    """Time the CPU oracle on n sessions of the same workload (after filling
+    the windows); returns (sessions/s, steps, seconds)."""
+    import numpy as np
+
+    from oracle import bridge
+    from paper_2603_18897_b200.device_ops import DevicePool
+    from paper_2603_18897_b200.packing import WindowBatch, admit_tables
+    from paper_2603_18897_b200.synth import LiveWorkload
+
+    pool, policy, book = load_setup(args)
+    dp = DevicePool(pool)
+    wl = LiveWorkload(dp.sigs, dp.keys, n, seed=2603)
+    W, R, K = 16, 17, args.max_candidates
+    host = WindowBatch(W, np.full(n * W, -1, np.int32), np.full(n * W, -1, np.int32),
+                       np.zeros(n, np.int64), None, [])
+    host.arena = (wl.tmpl.nodes, np.zeros(1, np.uint8), np.zeros((R * n, 2), np.int64))
+    tables = admit_tables(dp.sigs, policy, book.duration)
+
+    def one(step, batch):
+        region = step % R
+        return bridge.predict(dp.image, host, K, tables, new_tok=batch.tok,
+                              new_ref=np.ascontiguousarray(batch.ref), new_evt_base=region * n,
+                              new_byte_base=region * wl.max_batch_bytes, threads=threads)
+
+    step = 0
+    for _ in range(W):
+        one(step, wl.next_batch())
+        step += 1
+    batches = [wl.next_batch() for _ in range(4)]
+    done, spent = 0, 0.0
+    while spent < budget_s and done < max_steps:
+        b = batches[done % len(batches)]
+        t0 = time.perf_counter()
+        one(step, b)
+        spent += time.perf_counter() - t0
+        step += 1
+        done += 1
+    return n * done / spent, done, spent
+
+
+def cpu_baseline(args, budget_s):
+    threads = os.cpu_count() or 1
+    n = min(args.sessions, 200_000)
+    value, steps, spent = oracle_live_run(args, n, threads, budget_s)
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{steps} steps x {n} sessions of the same C3 workload ({spent:.1f} s), "
+                      "oracle/paste_oracle.c (reference algorithm: full pool scan + stable sort "
+                      "+ admit), OpenMP over sessions"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n = args.sessions
+    budget = max(20.0, args.cpu_budget_s)
+    value, steps, spent = oracle_live_run(args, n, threads, budget, max_steps=args.steps)
+    pool, _, _ = load_setup(args)
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * spent / max(steps, 1),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "int32+f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": "C3: live sessions, suffix window 16, top-8 predict + admit",
+                      "sessions_per_gpu": n, "window": 16, "max_candidates": args.max_candidates,
+                      "pool": f"{args.pool} ({len(pool.patterns)} patterns)"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                            "sample": f"{steps} steps x {n} sessions ({spent:.1f} s), "
+                                      "oracle/paste_oracle.c with all host threads"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

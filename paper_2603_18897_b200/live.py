@@ -37,16 +37,16 @@ class EventBatch:
     ref: object   # i64[n, 2]
     data: object  # u8[bytes]
 
-    @property
-    def nbytes(self) -> int:
+    def nbytes(self, with_data: bool = True) -> int:
+        parts = (self.tok, self.ref, self.data) if with_data else (self.tok, self.ref)
         return sum(int(x.nbytes) if isinstance(x, np.ndarray) else x.numel() * x.element_size()
-                   for x in (self.tok, self.ref, self.data))
+                   for x in parts)
 
 
 class LiveSessionTable:
     def __init__(self, dpool: DevicePool, n_sessions: int, nodes: np.ndarray,
                  max_batch_bytes: int, policy, estimates, capacity: int = 16,
-                 max_candidates: int = 8):
+                 max_candidates: int = 8, ship_bytes: bool = False):
         import torch
 
         _native.lib()
@@ -57,14 +57,18 @@ class LiveSessionTable:
         self.K = max_candidates
         self.B = max(dpool.image.max_bindings, 1)
         self.regions = capacity + 1
-        self.max_batch_bytes = int(max_batch_bytes)
+        # predict resolves argument *node references*; the scalar bytes stay in
+        # the host's copy of the payload unless a consumer on the device needs them
+        self.ship_bytes = ship_bytes
+        self.max_batch_bytes = int(max_batch_bytes) if ship_bytes else 0
         dev = torch.device("cuda")
         n, W, K, B = self.n, self.W, self.K, self.B
         self.tok = torch.full((n * W,), -1, dtype=torch.int32, device=dev)
         self.evt = torch.full((n * W,), -1, dtype=torch.int32, device=dev)
         self.count = torch.zeros(n, dtype=torch.int64, device=dev)
         self.nodes = to_dev(nodes)
-        self.bytes = torch.zeros(self.regions * self.max_batch_bytes, dtype=torch.uint8, device=dev)
+        self.bytes = torch.zeros(max(self.regions * self.max_batch_bytes, 1), dtype=torch.uint8,
+                                 device=dev)
         self.refs = torch.zeros(self.regions * n * 2, dtype=torch.int64, device=dev)
         self.new_tok = torch.zeros(n, dtype=torch.int32, device=dev)
         self.new_ref = torch.zeros(n * 2, dtype=torch.int64, device=dev)
@@ -100,11 +104,13 @@ class LiveSessionTable:
         tok = batch.tok if isinstance(batch.tok, t.Tensor) else t.from_numpy(batch.tok)
         ref = batch.ref if isinstance(batch.ref, t.Tensor) else t.from_numpy(batch.ref)
         data = batch.data if isinstance(batch.data, t.Tensor) else t.from_numpy(batch.data)
-        if data.numel() > self.max_batch_bytes:
-            raise ValueError("event batch exceeds the arena region size")
         self.new_tok.copy_(tok.reshape(-1), non_blocking=non_blocking)
         self.new_ref.copy_(ref.reshape(-1), non_blocking=non_blocking)
-        self.region_bytes(region)[:data.numel()].copy_(data.reshape(-1), non_blocking=non_blocking)
+        if self.ship_bytes:
+            if data.numel() > self.max_batch_bytes:
+                raise ValueError("event batch exceeds the arena region size")
+            self.region_bytes(region)[:data.numel()].copy_(data.reshape(-1),
+                                                           non_blocking=non_blocking)
 
     def launch(self, region: int, new_tok=None, new_ref=None) -> None:
         """observe (new event per session) + predict + admit, one kernel."""
