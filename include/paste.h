@@ -106,6 +106,12 @@ typedef struct {
   const int32_t* bucket_off;   /* [n_bucket_sigs + 1]                         */
   const int32_t* bucket_pat;   /* pattern ids, static rank (-p, pattern_id)   */
   const uint8_t* bucket_scan_all; /* 1 = bucket holds a struct-error pattern  */
+  /* optional match table (paste_build_match_table): NULL = scan buckets.
+   * Valid for requests with max_candidates <= mt_k and the same gather
+   * depth mt_g = min(k | max_ctx, window capacity).                         */
+  const void* match_table;
+  int32_t mt_k;
+  int32_t mt_g;
 } paste_pool_desc;
 
 /* Per-tool admission tables (policy.py:207-244, scheduling.py:218-219).    */
@@ -124,9 +130,10 @@ typedef struct {
 typedef struct {
   int64_t n_sessions;
   int32_t capacity;            /* W (ring slots per session)                  */
-  int32_t pad;
-  int32_t* tok;                /* [n*W] sig id, -1 = LLM step                 */
-  int32_t* evt;                /* [n*W] event index into refs                 */
+  int32_t slot_major;          /* 0: tok/evt are [n][W]; 1: [W][n] (sessions
+                                  stepping together touch contiguous slots)  */
+  int32_t* tok;                /* ring: sig id, -1 = LLM step                 */
+  int32_t* evt;                /* ring: event index into refs                 */
   int64_t* count;              /* [n] events observed so far                  */
   const paste_tape_node* nodes;
   const uint8_t* bytes;
@@ -145,6 +152,9 @@ enum { PASTE_C_FULL = 0, PASTE_C_PARTIAL = 1, PASTE_C_TOOL_ONLY = 2 };
 typedef struct {
   int32_t max_candidates;  /* K: per-session prediction slots                 */
   int32_t max_bindings;    /* slots per prediction in pred_arg                */
+  int32_t slot_major;      /* 0: per-session records [n][K] ([n][K][B] args);
+                              1: slot-major [K][n] ([K][B][n] args)           */
+  int32_t pad;
   int32_t* n_pred;         /* [n]                                             */
   int32_t* pred_pat;       /* [n*K] pattern index                             */
   uint8_t* pred_comp;      /* [n*K] PASTE_C_*                                 */
@@ -172,6 +182,24 @@ int paste_abi_version(void);
 int paste_predict_batch(const paste_pool_desc* pool, paste_windows* windows,
                         const paste_admit_desc* admit, paste_predict_out* out,
                         void* stream);
+
+/* Pool compilation for K4: a match table keyed by the newest G tool tokens.
+ * Which patterns match at an anchor, in which order and at which positions
+ * depends only on those G tokens (match_at looks back at most k events,
+ * mining.py:142), so the table stores per key the number of matches, the
+ * number of structural-error matches (Predictor diagnostics) and the first
+ * max_candidates matches in rank order with the matched position (age) of
+ * every binding's source event.  Key = anchor + S * sum_{a>=1} code(age a)
+ * * (S+1)^(a-1) with S = n_bucket_sigs and code = S for "no event / unknown
+ * signature".  Entry = {int32 n_match, int32 n_err, 2 x pad} + max_candidates records
+ * of 32 bytes {pid, 4-bit source age per binding, target tool,
+ * n_bind | flags << 16, bind_off, pad, double p}.
+ * paste_match_table_bytes returns the size, or -1 when the pool is outside
+ * the table's envelope (the kernel then scans buckets).                    */
+int64_t paste_match_table_bytes(const paste_pool_desc* pool, int32_t max_candidates,
+                                int32_t window_capacity);
+int paste_build_match_table(const paste_pool_desc* pool, int32_t max_candidates,
+                            int32_t window_capacity, void* table, void* stream);
 
 /* K4 epilogue as a standalone op: admit() over many prediction lists.
  * Replaces policy.py:207-244 (admit + _beats).  Per prediction: tool id,

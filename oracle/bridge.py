@@ -48,7 +48,7 @@ def pool_desc(im: PoolImage) -> tuple[PoolDesc, bytes, list]:
     keep = [im.patterns, im.bindings, im.ctx_sig, im.steps, im.bucket_off, im.bucket_pat,
             im.bucket_scan_all if len(im.bucket_scan_all) else np.zeros(1, np.uint8)]
     desc = PoolDesc(len(im.pool.patterns), im.n_bucket_sigs, im.k, im.relation, im.max_ctx,
-                    im.max_bindings, *[_p(a) for a in keep])
+                    im.max_bindings, *[_p(a) for a in keep], 0, 0, 0)
     pids = b"".join(pid.encode().ljust(16, b"\0") for pid in im.pattern_ids) or b"\0" * 16
     return desc, pids, keep
 
@@ -57,20 +57,21 @@ def predict(im: PoolImage, batch: WindowBatch, K: int,
             admit: tuple[np.ndarray, np.ndarray, np.ndarray] | None = None,
             new_tok: np.ndarray | None = None, new_ref: np.ndarray | None = None,
             new_evt_base: int = 0, new_byte_base: int = 0,
-            threads: int = 1) -> PredictResult:
+            threads: int = 1, out_slot_major: int = 0) -> PredictResult:
     """Run the oracle; like the device it mutates the window rings (and the
     event directory) when new_tok / new_ref are given."""
     desc, pids, keep = pool_desc(im)
     nodes, data, refs = batch.arena.arrays() if hasattr(batch.arena, "arrays") else batch.arena
-    win = WindowsDesc(batch.n, batch.capacity, 0, _p(batch.tok), _p(batch.evt), _p(batch.count),
+    win = WindowsDesc(batch.n, batch.capacity, batch.slot_major, _p(batch.tok), _p(batch.evt), _p(batch.count),
                       _p(nodes), _p(data), _p(refs), _p(new_tok), _p(new_ref), new_evt_base,
                       new_byte_base)
-    res = PredictResult.empty(batch.n, K, max(im.max_bindings, 1), admit is not None)
+    res = PredictResult.empty(batch.n, K, max(im.max_bindings, 1), admit is not None,
+                              out_slot_major)
     if admit is not None:
         adm = AdmitDesc(1, len(admit[0]), *[_p(a) for a in admit])
     else:
         adm = AdmitDesc(0, 0, 0, 0, 0)
-    out = PredictOut(K, res.B, _p(res.n_pred), _p(res.pred_pat), _p(res.pred_comp),
+    out = PredictOut(K, res.B, out_slot_major, 0, _p(res.n_pred), _p(res.pred_pat), _p(res.pred_comp),
                      _p(res.pred_arg), _p(res.n_act), _p(res.act_pred), _p(res.act_level),
                      _p(res.act_util), _p(res.struct_err))
     rc = lib().oracle_predict_batch(ctypes.byref(desc), pids, ctypes.byref(win),

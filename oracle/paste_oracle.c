@@ -24,6 +24,18 @@
 
 #include "paste.h"
 
+/* ring / output addressing (session-major or slot-major, include/paste.h) */
+static int64_t ring_idx(const paste_windows* w, int64_t s, int slot) {
+  return w->slot_major ? (int64_t)slot * w->n_sessions + s : s * w->capacity + slot;
+}
+static int64_t out_idx(const paste_predict_out* o, int64_t n, int64_t s, int i) {
+  return o->slot_major ? (int64_t)i * n + s : s * o->max_candidates + i;
+}
+static int64_t arg_idx(const paste_predict_out* o, int64_t n, int64_t s, int i, int b) {
+  return o->slot_major ? ((int64_t)i * o->max_bindings + b) * n + s
+                       : (s * o->max_candidates + i) * o->max_bindings + b;
+}
+
 typedef struct {
   const paste_tape_node* nodes;
   const paste_event_ref* refs;
@@ -81,9 +93,8 @@ static void predict_one(const paste_pool_desc* pool, const char* pids, const pas
                         const paste_admit_desc* adm, paste_predict_out* out, int64_t s,
                         cand_t* cands, int32_t* stream_tok, int32_t* stream_slot) {
   const int W = win->capacity;
-  const int K = out->max_candidates, B = out->max_bindings;
-  int32_t* tok = win->tok + s * W;
-  int32_t* evt = win->evt + s * W;
+  const int K = out->max_candidates;
+  const int64_t N = win->n_sessions;
   int64_t cnt = win->count[s];
   int len, i, n_stream = 0, n_cand = 0, n_err = 0, p;
   tapes_t T = {win->nodes, win->refs};
@@ -92,16 +103,16 @@ static void predict_one(const paste_pool_desc* pool, const char* pids, const pas
     const int64_t ev = win->new_evt_base + s;
     win->refs[ev].node_base = win->new_ref[s].node_base;
     win->refs[ev].byte_base = win->new_ref[s].byte_base + win->new_byte_base;
-    tok[cnt % W] = win->new_tok[s];
-    evt[cnt % W] = (int32_t)ev;
+    win->tok[ring_idx(win, s, (int)(cnt % W))] = win->new_tok[s];
+    win->evt[ring_idx(win, s, (int)(cnt % W))] = (int32_t)ev;
     win->count[s] = ++cnt;
   }
   len = (int)(cnt < W ? cnt : W);
   /* window.tool_events(): oldest..newest */
   for (i = 0; i < len; ++i) {
     int slot = (int)((cnt - len + i) % W);
-    if (tok[slot] >= 0) {
-      stream_tok[n_stream] = tok[slot];
+    if (win->tok[ring_idx(win, s, slot)] >= 0) {
+      stream_tok[n_stream] = win->tok[ring_idx(win, s, slot)];
       stream_slot[n_stream] = slot;
       ++n_stream;
     }
@@ -153,7 +164,7 @@ static void predict_one(const paste_pool_desc* pool, const char* pids, const pas
         for (b = 0; b < pt->n_bind; ++b) {
           const paste_binding* bd = &pool->bindings[pt->bind_off + b];
           const int src = mpos[bd->ctx_pos];
-          const int32_t ev = evt[stream_slot[src]];
+          const int32_t ev = win->evt[ring_idx(win, s, stream_slot[src])];
           const int64_t base = T.refs[ev].node_base;
           int64_t cur;
           if (bd->kind == PASTE_X_FALLBACK) {
@@ -197,13 +208,13 @@ static void predict_one(const paste_pool_desc* pool, const char* pids, const pas
   if (n_cand > K) n_cand = K; /* predictions[:max_candidates] */
   out->n_pred[s] = n_cand;
   for (i = 0; i < n_cand; ++i) {
-    const int64_t slot = s * K + i;
+    const int64_t slot = out_idx(out, N, s, i);
     const paste_pattern* pt = &pool->patterns[cands[i].pat];
     int b;
     out->pred_pat[slot] = cands[i].pat;
     out->pred_comp[slot] = cands[i].comp;
     if (cands[i].comp != PASTE_C_TOOL_ONLY)
-      for (b = 0; b < pt->n_bind; ++b) out->pred_arg[slot * B + b] = cands[i].args[b];
+      for (b = 0; b < pt->n_bind; ++b) out->pred_arg[arg_idx(out, N, s, i, b)] = cands[i].args[b];
   }
   if (!adm->enabled) return;
   {
@@ -220,20 +231,20 @@ static void predict_one(const paste_pool_desc* pool, const char* pids, const pas
       level = cap < implied ? cap : implied;
       util = pt->p * adm->benefit[tool];
       for (j = 0; j < n_act; ++j)
-        if (pool->patterns[cands[out->act_pred[s * K + j]].pat].target_tool == tool) break;
+        if (pool->patterns[cands[out->act_pred[out_idx(out, N, s, j)]].pat].target_tool == tool) break;
       if (j == n_act) {
-        out->act_pred[s * K + j] = (int16_t)i;
-        out->act_level[s * K + j] = (uint8_t)level;
-        out->act_util[s * K + j] = util;
+        out->act_pred[out_idx(out, N, s, j)] = (int16_t)i;
+        out->act_level[out_idx(out, N, s, j)] = (uint8_t)level;
+        out->act_util[out_idx(out, N, s, j)] = util;
         ++n_act;
       } else {
-        const double iu = out->act_util[s * K + j];
-        const double ip = pool->patterns[cands[out->act_pred[s * K + j]].pat].p;
+        const double iu = out->act_util[out_idx(out, N, s, j)];
+        const double ip = pool->patterns[cands[out->act_pred[out_idx(out, N, s, j)]].pat].p;
         int beats = (util != iu) ? (util > iu) : (pt->p > ip);
         if (beats) {
-          out->act_pred[s * K + j] = (int16_t)i;
-          out->act_level[s * K + j] = (uint8_t)level;
-          out->act_util[s * K + j] = util;
+          out->act_pred[out_idx(out, N, s, j)] = (int16_t)i;
+          out->act_level[out_idx(out, N, s, j)] = (uint8_t)level;
+          out->act_util[out_idx(out, N, s, j)] = util;
         }
       }
     }

@@ -43,7 +43,8 @@ class PoolDesc(ctypes.Structure):
                 ("relation", c_int32), ("max_ctx", c_int32), ("max_bindings", c_int32),
                 ("patterns", c_void_p), ("bindings", c_void_p), ("ctx_sig", c_void_p),
                 ("steps", c_void_p), ("bucket_off", c_void_p), ("bucket_pat", c_void_p),
-                ("bucket_scan_all", c_void_p)]
+                ("bucket_scan_all", c_void_p), ("match_table", c_void_p), ("mt_k", c_int32),
+                ("mt_g", c_int32)]
 
 
 class AdmitDesc(ctypes.Structure):
@@ -52,7 +53,7 @@ class AdmitDesc(ctypes.Structure):
 
 
 class WindowsDesc(ctypes.Structure):
-    _fields_ = [("n_sessions", c_int64), ("capacity", c_int32), ("pad", c_int32),
+    _fields_ = [("n_sessions", c_int64), ("capacity", c_int32), ("slot_major", c_int32),
                 ("tok", c_void_p), ("evt", c_void_p), ("count", c_void_p),
                 ("nodes", c_void_p), ("bytes", c_void_p), ("refs", c_void_p),
                 ("new_tok", c_void_p), ("new_ref", c_void_p), ("new_evt_base", c_int64),
@@ -61,7 +62,7 @@ class WindowsDesc(ctypes.Structure):
 
 class PredictOut(ctypes.Structure):
     _fields_ = [("max_candidates", c_int32), ("max_bindings", c_int32),
-                ("n_pred", c_void_p), ("pred_pat", c_void_p), ("pred_comp", c_void_p),
+                ("slot_major", c_int32), ("pad", c_int32), ("n_pred", c_void_p), ("pred_pat", c_void_p), ("pred_comp", c_void_p),
                 ("pred_arg", c_void_p), ("n_act", c_void_p), ("act_pred", c_void_p),
                 ("act_level", c_void_p), ("act_util", c_void_p), ("struct_err", c_void_p)]
 
@@ -89,6 +90,8 @@ EXPORTS = {
     "paste_predict_batch": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc),
                                     POINTER(AdmitDesc), POINTER(PredictOut), c_void_p]),
     "paste_admit_lists": (c_int, [POINTER(AdmitDesc), POINTER(AdmitListsDesc), c_void_p]),
+    "paste_match_table_bytes": (c_int64, [POINTER(PoolDesc), c_int32, c_int32]),
+    "paste_build_match_table": (c_int, [POINTER(PoolDesc), c_int32, c_int32, c_void_p, c_void_p]),
 }
 
 _lib = None

@@ -77,4 +77,25 @@ __device__ __forceinline__ int64_t step_child(const paste_tape_node* nodes, int6
   return child;
 }
 
+// ---------------------------------------------------------------------------
+// window-ring / output-record addressing (session-major or slot-major)
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ int64_t ring_at(const paste_windows& w, int64_t sess, int slot) {
+  return w.slot_major ? (int64_t)slot * w.n_sessions + sess : sess * w.capacity + slot;
+}
+__host__ __device__ __forceinline__ int64_t out_at(const paste_predict_out& o, int64_t n,
+                                                   int64_t sess, int i) {
+  return o.slot_major ? (int64_t)i * n + sess : sess * o.max_candidates + i;
+}
+__host__ __device__ __forceinline__ int64_t arg_at(const paste_predict_out& o, int64_t n,
+                                                   int64_t sess, int i, int b) {
+  return o.slot_major ? ((int64_t)i * o.max_bindings + b) * n + sess
+                      : (sess * o.max_candidates + i) * o.max_bindings + b;
+}
+
+// K4 fast path (predict_fast.cu); false = not eligible, use the generic kernel
+bool predict_fast_dispatch(const paste_pool_desc* pool, const paste_windows* win,
+                           const paste_admit_desc* adm, const paste_predict_out* out, int G,
+                           cudaStream_t stream);
+
 }  // namespace paste

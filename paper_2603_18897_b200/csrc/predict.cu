@@ -18,6 +18,8 @@
 //   * mapping evaluation walks the payload tapes of the matched events only;
 //   * the admit epilogue (policy level, utility = p * benefit, per-tool
 //     arbitration) runs on the thread's K candidates in registers/local memory.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace paste {
@@ -38,7 +40,7 @@ __device__ __forceinline__ int64_t resolve_binding(const PredictParams& P, const
                                                    const int32_t* mpos, int m, int64_t sess) {
   const int src = mpos[bd.ctx_pos];
   // plain load: the slot may have been written by this thread's observe step
-  const int32_t ev = P.win.evt[sess * P.win.capacity + gslot[src]];
+  const int32_t ev = P.win.evt[ring_at(P.win, sess, gslot[src])];
   const paste_event_ref ref = P.win.refs[ev];
   const int64_t base = ref.node_base;
   const int32_t* steps = P.pool.steps;
@@ -77,7 +79,6 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictParams P) {
   const int64_t sess = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (sess >= P.win.n_sessions) return;
   const int W = P.win.capacity;
-  int32_t* tok = P.win.tok + sess * W;
   int64_t cnt = P.win.count[sess];
 
   // observe (PredictionWindow.observe: deque append with maxlen W)
@@ -87,8 +88,8 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictParams P) {
     paste_event_ref r = P.win.new_ref[sess];
     r.byte_base += P.win.new_byte_base;
     P.win.refs[ev] = r;
-    tok[slot] = P.win.new_tok[sess];
-    P.win.evt[sess * W + slot] = (int32_t)ev;
+    P.win.tok[ring_at(P.win, sess, slot)] = P.win.new_tok[sess];
+    P.win.evt[ring_at(P.win, sess, slot)] = (int32_t)ev;
     ++cnt;
     P.win.count[sess] = cnt;
   }
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictParams P) {
     int32_t rt[GMAX], rs[GMAX];
     for (int i = 0; i < len && m < G; ++i) {
       const int slot = (int)((cnt - 1 - i) % W);
-      const int32_t t = tok[slot];
+      const int32_t t = P.win.tok[ring_at(P.win, sess, slot)];
       if (t >= 0) {
         rt[m] = t;
         rs[m] = slot;
@@ -118,7 +119,6 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictParams P) {
   }
 
   const int K = P.out.max_candidates;
-  const int B = P.out.max_bindings;
   int n_pred = 0, n_err = 0;
   // candidate state kept for the admit epilogue
   int32_t cpat[GMAX * 2];
@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictParams P) {
         if (!scan_all) break;
         continue;
       }
-      const int64_t slot = sess * K + n_pred;
+      const int64_t slot = out_at(P.out, P.win.n_sessions, sess, n_pred);
       uint8_t comp;
       if (!(pt.flags & PASTE_PF_HAS_MAPPING)) {
         comp = PASTE_C_TOOL_ONLY;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictParams P) {
           const paste_binding bd = pool.bindings[pt.bind_off + bi2];
           const int64_t r = resolve_binding(P, bd, gtok, gslot, mpos, m, sess);
           if (r < 0) comp = PASTE_C_PARTIAL;
-          P.out.pred_arg[slot * B + bi2] = r;
+          P.out.pred_arg[arg_at(P.out, P.win.n_sessions, sess, n_pred, bi2)] = r;
         }
       }
       P.out.pred_pat[slot] = pid;
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictParams P) {
   }
   P.out.n_act[sess] = n_act;
   for (int j = 0; j < n_act; ++j) {
-    const int64_t o = sess * K + j;
+    const int64_t o = out_at(P.out, P.win.n_sessions, sess, j);
     P.out.act_pred[o] = apred[j];
     P.out.act_level[o] = alevel[j];
     P.out.act_util[o] = autil[j];
@@ -259,6 +259,18 @@ extern "C" int paste_predict_batch(const paste_pool_desc* pool, paste_windows* w
     return PASTE_ERR_UNSUPPORTED;
   }
   if (windows->n_sessions == 0) return PASTE_OK;
+  {
+    const int g = pool->relation == PASTE_REL_ANCHORED ? pool->k : pool->max_ctx;
+    const int G = g < windows->capacity ? g : windows->capacity;
+    // PASTE_FORCE_GENERIC=1 pins the generic kernel (A/B parity tests)
+    static const bool force_generic = getenv("PASTE_FORCE_GENERIC") != nullptr;
+    if (!force_generic &&
+        predict_fast_dispatch(pool, windows, admit, out, G, (cudaStream_t)stream)) {
+      count_launch();
+      PASTE_CUDA_CHECK(cudaGetLastError());
+      return PASTE_OK;
+    }
+  }
   PredictParams P{*pool, *windows, *admit, *out};
   const int threads = 256;
   const int64_t blocks = (windows->n_sessions + threads - 1) / threads;

@@ -1,0 +1,534 @@
+// K4 fast path: match-table predict + streamed admit, no local memory.
+//
+// Same results as predict_kernel (predict.cu; reference prediction.py:76-118,
+// mining.py:119-156, mappings.py:143-223, policy.py:207-244), restructured for
+// sm_100a:
+//
+// * Pool compilation (build_match_table_kernel): which patterns match at an
+//   anchor, their rank order and the matched position of every binding's
+//   source depend only on the newest G tool tokens (match_at never looks
+//   further back than k events, mining.py:142; the suffix relation needs the
+//   newest max_ctx).  One thread per key runs the bucket scan once and
+//   stores the first K matches -- with the pattern fields the live kernel
+//   needs and the age of every binding's source -- so the live kernel does
+//   one L2-resident table read per session instead of a divergent bucket
+//   scan followed by dependent pattern loads.
+// * Window rings may be slot-major ([W][n]): sessions that step together
+//   (a batch of tool completions) read and write contiguous 128-byte lines.
+//   Each thread gathers its newest G tool events (token, ring slot) into a
+//   G-deep shared-memory row, so no array ever lands in local memory.
+// * Admit is streamed in rank order.  Candidates arrive sorted by p
+//   descending, so for a tool whose benefit b is >= 0 (or NaN) the utility
+//   p*b is non-increasing and the reference's strict (utility, p,
+//   -created_at) arbitration (_beats, policy.py:239-244) keeps the FIRST
+//   allowed candidate of the tool: a seen-tool bitmask replaces the K x K
+//   comparison.  Tools with a negative benefit (or ids >= 64) take the exact
+//   comparison path against the incumbent's record.
+#include "common.cuh"
+
+namespace paste {
+
+constexpr int FT = 128;         // threads per CTA
+constexpr int MT_MAX_BIND = 8;  // 4-bit source ages per binding in a uint32
+
+struct FastParams {
+  paste_pool_desc pool;
+  paste_windows win;
+  paste_admit_desc adm;
+  paste_predict_out out;
+  int G;    // gathered tool events: min(k | max_ctx, W)
+  int row;  // smem words per thread (2G + 1)
+};
+
+struct MTRecord {  // 32 bytes
+  int32_t pid;
+  uint32_t src;      // 4-bit source age per binding
+  int32_t tool;
+  int32_t nb_flags;  // n_bind | flags << 16
+  int32_t bind_off;
+  int32_t pad;
+  double p;
+};
+static_assert(sizeof(MTRecord) == 32, "MTRecord layout");
+
+// 16-byte header keeps every record 16-byte aligned for the int4 loads
+__host__ __device__ inline int64_t mt_stride(int K) { return 16 + 32 * (int64_t)K; }
+
+// ---------------------------------------------------------------------------
+// match-table build: one thread per key (the reference's bucket scan, run
+// once per distinct token context)
+// ---------------------------------------------------------------------------
+__global__ void build_match_table_kernel(const paste_pool_desc pool, int K, int G,
+                                         int64_t n_keys, uint8_t* table) {
+  const int64_t key = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (key >= n_keys) return;
+  const int S = pool.n_bucket_sigs, base = S + 1;
+  int32_t tok[16];  // by age; -2 = no event / unknown signature
+  {  // key = anchor + S * sum_{a>=1} code(a) * (S+1)^(a-1)
+    tok[0] = (int)(key % S);
+    int64_t k = key / S;
+    for (int a = 1; a < G; ++a) {
+      const int c = (int)(k % base);
+      k /= base;
+      tok[a] = c == S ? -2 : c;
+    }
+  }
+  int32_t* hdr = reinterpret_cast<int32_t*>(table + key * mt_stride(K));
+  MTRecord* rec = reinterpret_cast<MTRecord*>(hdr + 4);
+  int n_match = 0, n_err = 0;
+  const int a = tok[0];
+  const int m = G;  // absent positions behave as never-matching tokens
+#define TK(p) tok[m - 1 - (p)]
+  const bool anchored = pool.relation == PASTE_REL_ANCHORED;
+  for (int bi = pool.bucket_off[a]; bi < pool.bucket_off[a + 1]; ++bi) {
+    const int pid = pool.bucket_pat[bi];
+    const paste_pattern pt = pool.patterns[pid];
+    const int n = pt.ctx_len;
+    const int32_t* ctx = pool.ctx_sig + pt.ctx_off;
+    int pos_of[16];
+    bool ok;
+    if (anchored) {
+      if (n > 16) continue;
+      pos_of[n - 1] = m - 1;
+      int j = n - 2, pos = m - 2;
+      while (j >= 0 && pos >= 0) {
+        if (TK(pos) == ctx[j]) pos_of[j--] = pos;
+        --pos;
+      }
+      ok = j < 0;
+    } else {
+      ok = n <= m;
+      for (int i = 0; ok && i < n - 1; ++i) ok = TK(m - n + i) == ctx[i];
+      if (ok)
+        for (int i = 0; i < n; ++i) pos_of[i] = m - n + i;
+    }
+    if (!ok) continue;
+    if (pt.flags & PASTE_PF_STRUCT_ERR) {
+      ++n_err;
+      continue;
+    }
+    if (n_match < K) {
+      uint32_t src = 0;
+      for (int b = 0; b < pt.n_bind && b < MT_MAX_BIND; ++b) {
+        const int cp = pool.bindings[pt.bind_off + b].ctx_pos;
+        src |= (uint32_t)(m - 1 - pos_of[cp]) << (4 * b);  // age of the source
+      }
+      MTRecord r;
+      r.pid = pid;
+      r.src = src;
+      r.tool = pt.target_tool;
+      r.nb_flags = pt.n_bind | (pt.flags << 16);
+      r.bind_off = pt.bind_off;
+      r.pad = 0;
+      r.p = pt.p;
+      rec[n_match] = r;
+    }
+    ++n_match;
+  }
+#undef TK
+  hdr[0] = n_match;
+  hdr[1] = n_err;
+  hdr[2] = 0;
+  hdr[3] = 0;
+}
+
+static int64_t keys_for(const paste_pool_desc* pool, int G) {
+  const int64_t base = (int64_t)pool->n_bucket_sigs + 1;
+  int64_t n = pool->n_bucket_sigs;
+  for (int a = 1; a < G; ++a) {
+    n *= base;
+    if (n > ((int64_t)1 << 40)) return -1;
+  }
+  return n;
+}
+
+static int gather_depth(const paste_pool_desc* pool, int W) {
+  const int g = pool->relation == PASTE_REL_ANCHORED ? pool->k : pool->max_ctx;
+  return g < W ? g : W;
+}
+
+}  // namespace paste
+
+extern "C" int64_t paste_match_table_bytes(const paste_pool_desc* pool, int32_t max_candidates,
+                                           int32_t window_capacity) {
+  using namespace paste;
+  if (!pool || max_candidates < 1 || window_capacity < 1 || window_capacity > 16) return -1;
+  if (pool->max_bindings > MT_MAX_BIND || pool->n_bucket_sigs < 1) return -1;
+  const int G = gather_depth(pool, window_capacity);
+  if (G < 1 || G > 16) return -1;
+  const int64_t keys = keys_for(pool, G);
+  if (keys < 0) return -1;
+  const int64_t bytes = keys * mt_stride(max_candidates);
+  if (bytes > ((int64_t)1 << 30)) return -1;  // keep tables L2/HBM friendly
+  return bytes;
+}
+
+extern "C" int paste_build_match_table(const paste_pool_desc* pool, int32_t max_candidates,
+                                       int32_t window_capacity, void* table, void* stream) {
+  using namespace paste;
+  reset_launches();
+  const int64_t bytes = paste_match_table_bytes(pool, max_candidates, window_capacity);
+  if (bytes < 0) {
+    set_error("pool is outside the match-table envelope");
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  PASTE_REQUIRE(table != nullptr, "null table");
+  const int G = gather_depth(pool, window_capacity);
+  const int64_t keys = keys_for(pool, G);
+  const int threads = 128;
+  build_match_table_kernel<<<(unsigned)((keys + threads - 1) / threads), threads, 0,
+                             (cudaStream_t)stream>>>(*pool, max_candidates, G, keys,
+                                                     static_cast<uint8_t*>(table));
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
+
+namespace paste {
+
+// ---------------------------------------------------------------------------
+// Per-launch walk memo.  With shape-interned payloads many events share one
+// node array, and a PathLookup / FormatTemplate walk depends only on (the
+// binding, the node array): the CTA memoises those walks in shared memory.
+// Entry: valid(1) | binding(16) | node_base(24) | node(23, all-ones = none).
+// ---------------------------------------------------------------------------
+constexpr int MEMO = 128;
+constexpr uint64_t MEMO_NONE = 0x7fffffull;
+
+__device__ __forceinline__ int memo_slot(uint64_t key) {
+  return (int)((key * 0x9E3779B97F4A7C15ull) >> 57);  // 7 bits -> 128 slots
+}
+
+// Walk `bd`'s path (plus the fallback index) from the root of event `ev`.
+__device__ __forceinline__ int64_t walk_binding(const paste_windows& win, const int32_t* steps,
+                                                const paste_binding& bd, int64_t nb, int fails) {
+  int64_t cur = 0;
+  const int2* st = reinterpret_cast<const int2*>(steps);
+  for (int s = 0; s < bd.step_cnt && cur >= 0; ++s) {
+    const int2 k = __ldg(st + bd.step_off + s);
+    cur = step_child(win.nodes, nb, cur, k.x, k.y);
+  }
+  if (bd.kind == PASTE_X_FALLBACK) {
+    if (cur >= 0)
+      cur = bd.start_index < 0 ? -1 : step_child(win.nodes, nb, cur, 1, bd.start_index + fails);
+    for (int s = 0; s < bd.suf_cnt && cur >= 0; ++s) {
+      const int2 k = __ldg(st + bd.suf_off + s);
+      cur = step_child(win.nodes, nb, cur, k.x, k.y);
+    }
+  } else if (bd.kind == PASTE_X_FORMAT && cur >= 0) {
+    // _leaf_str: only str / number leaves fill the hole (mappings.py:197-204)
+    const int t = load_node(win.nodes, nb + cur).type();
+    if (t != PASTE_T_STR && t != PASTE_T_INT && t != PASTE_T_FLOAT) cur = -1;
+  }
+  return cur;
+}
+
+// Resolve binding `bind` (global index) against source event `ev` at age
+// `src_age`; `gt` holds the gathered tokens by age for the failure count.
+__device__ __forceinline__ int64_t resolve_fast(const paste_windows& win, const int32_t* steps,
+                                                const paste_binding& bd, int bind, int32_t ev,
+                                                int src_age, const int32_t* gt, uint64_t* memo) {
+  const int64_t nb = win.refs[ev].node_base;
+  if (bd.kind == PASTE_X_FALLBACK) {
+    int fails = 0;  // FAIL events of fail_tool after the source (mappings.py:185-194)
+    for (int a = 0; a < src_age; ++a) {
+      const int32_t t = gt[a];
+      fails += ((t >> 1) == bd.fail_tool) && ((t & 1) == 0);
+    }
+    const int64_t cur = walk_binding(win, steps, bd, nb, fails);
+    return cur < 0 ? -1 : (((int64_t)ev << 32) | cur);
+  }
+  const bool cacheable = bind < (1 << 16) && nb < (1ll << 24);
+  const uint64_t key = ((uint64_t)bind << 24) | (uint64_t)nb;
+  int64_t cur;
+  if (cacheable) {
+    const int h = memo_slot(key);
+    const uint64_t e = memo[h];
+    if ((e >> 63) && ((e >> 23) & ((1ull << 40) - 1)) == key) {
+      const uint64_t v = e & MEMO_NONE;
+      cur = v == MEMO_NONE ? -1 : (int64_t)v;
+    } else {
+      cur = walk_binding(win, steps, bd, nb, 0);
+      if (cur < (int64_t)MEMO_NONE)
+        memo[h] = (1ull << 63) | (key << 23) | (cur < 0 ? MEMO_NONE : (uint64_t)cur);
+    }
+  } else {
+    cur = walk_binding(win, steps, bd, nb, 0);
+  }
+  return cur < 0 ? -1 : (((int64_t)ev << 32) | cur);
+}
+
+struct OutIdx {  // record addressing for one session (session- or slot-major)
+  int64_t obase, ostride, abase;
+  int B;
+  __device__ __forceinline__ int64_t o(int i) const { return obase + (int64_t)i * ostride; }
+  __device__ __forceinline__ int64_t a(int i, int b) const {
+    return abase + (int64_t)(i * B + b) * ostride;
+  }
+};
+
+// Streamed admit of candidate `i` (policy.py:207-236).
+__device__ __forceinline__ void admit_one(const FastParams& P, const OutIdx& X, int i, int tool,
+                                          int comp, double p, int& n_act, uint64_t& seen) {
+  if (tool >= P.adm.n_tools || !__ldg(P.adm.allow + tool)) return;
+  const int implied = comp == PASTE_C_FULL ? 3 : 1;
+  const int cap = __ldg(P.adm.max_level + tool);
+  const int level = cap < implied ? cap : implied;
+  const double bene = __ldg(P.adm.benefit + tool);
+  const double util = __dmul_rn(p, bene);
+  if (!(bene < 0.0) && tool < 64) {
+    if ((seen >> tool) & 1ull) return;  // an earlier (higher-p) candidate wins
+    seen |= 1ull << tool;
+    const int64_t o = X.o(n_act);
+    P.out.act_pred[o] = (int16_t)i;
+    P.out.act_level[o] = (uint8_t)level;
+    P.out.act_util[o] = util;
+    ++n_act;
+    return;
+  }
+  int j = 0;  // exact arbitration against the incumbent (rare)
+  for (; j < n_act; ++j) {
+    const int ip = P.out.act_pred[X.o(j)];
+    if (P.pool.patterns[P.out.pred_pat[X.o(ip)]].target_tool == tool) break;
+  }
+  const int64_t o = X.o(j);
+  if (j == n_act) {
+    P.out.act_pred[o] = (int16_t)i;
+    P.out.act_level[o] = (uint8_t)level;
+    P.out.act_util[o] = util;
+    ++n_act;
+    return;
+  }
+  const double iu = P.out.act_util[o];
+  const double ipp = P.pool.patterns[P.out.pred_pat[X.o(P.out.act_pred[o])]].p;
+  if ((util != iu) ? (util > iu) : (p > ipp)) {
+    P.out.act_pred[o] = (int16_t)i;
+    P.out.act_level[o] = (uint8_t)level;
+    P.out.act_util[o] = util;
+  }
+}
+
+template <bool TABLE>
+__device__ __forceinline__ void predict_session(const FastParams& P, int64_t sess, int32_t* gt,
+                                                uint64_t* memo) {
+  const int64_t n = P.win.n_sessions;
+  const int W = P.win.capacity, G = P.G;
+  int32_t* gs = gt + G;  // ring slots of the gathered tokens
+  const int64_t rbase = P.win.slot_major ? sess : sess * W;
+  const int64_t rstride = P.win.slot_major ? n : 1;
+  const int K = P.out.max_candidates;
+  OutIdx X;
+  X.B = P.out.max_bindings;
+  X.ostride = P.out.slot_major ? n : 1;
+  X.obase = P.out.slot_major ? sess : sess * K;
+  X.abase = P.out.slot_major ? sess : sess * K * X.B;
+
+  int64_t cnt = P.win.count[sess];
+  int head = (int)(cnt % W);  // next slot to write
+  int32_t new_t = -1;
+  if (P.win.new_tok != nullptr) {  // observe (PredictionWindow.observe)
+    const int64_t ev = P.win.new_evt_base + sess;
+    paste_event_ref r = P.win.new_ref[sess];
+    r.byte_base += P.win.new_byte_base;
+    P.win.refs[ev] = r;
+    new_t = P.win.new_tok[sess];
+    const int64_t at = rbase + head * rstride;
+    P.win.tok[at] = new_t;
+    P.win.evt[at] = (int32_t)ev;
+    ++cnt;
+    P.win.count[sess] = cnt;
+    head = head + 1 == W ? 0 : head + 1;
+  }
+  const int len = (int)(cnt < W ? cnt : W);
+
+  // ---- gather the newest G tool events (age 0 = newest) ---------------------
+  int m = 0;
+  {
+    int slot = head;
+    for (int i = 0; i < len && m < G; ++i) {
+      slot = slot == 0 ? W - 1 : slot - 1;
+      const int32_t t = (i == 0 && P.win.new_tok != nullptr) ? new_t : P.win.tok[rbase + slot * rstride];
+      if (t >= 0) {
+        gt[m] = t;
+        gs[m] = slot;
+        ++m;
+      }
+    }
+  }
+
+  const paste_pool_desc& pool = P.pool;
+  const bool admit = P.adm.enabled != 0;
+  int n_pred = 0, n_err = 0, n_act = 0;
+  uint64_t seen = 0;  // tools (< 64) that already hold an action
+  const int S = pool.n_bucket_sigs;
+
+  if (m > 0 && gt[0] < S) {
+    if (TABLE) {
+      // ---- table path: one entry per distinct token context ---------------
+      int64_t key = gt[0], mult = S;
+      for (int a = 1; a < G; ++a) {
+        const int t = a < m ? gt[a] : S;
+        key += (int64_t)(t < S ? t : S) * mult;
+        mult *= (S + 1);
+      }
+      const uint8_t* e = static_cast<const uint8_t*>(pool.match_table) + key * mt_stride(pool.mt_k);
+      const int2 hdr = __ldg(reinterpret_cast<const int2*>(e));
+      const MTRecord* recs = reinterpret_cast<const MTRecord*>(e + 16);
+      n_err = hdr.y;
+      const int nm = hdr.x < K ? hdr.x : K;
+      for (int i = 0; i < nm; ++i) {
+        const int4 r0 = __ldg(reinterpret_cast<const int4*>(recs + i));
+        const int4 r1 = __ldg(reinterpret_cast<const int4*>(recs + i) + 1);
+        const int pid = r0.x, tool = r0.z, n_bind = r0.w & 0xffff, pflags = r0.w >> 16;
+        const uint32_t src = (uint32_t)r0.y;
+        const int bind_off = r1.x;
+        const double p = __hiloint2double(r1.w, r1.z);
+        int comp = PASTE_C_TOOL_ONLY;
+        if (pflags & PASTE_PF_HAS_MAPPING) {
+          comp = PASTE_C_FULL;
+          for (int b = 0; b < n_bind; ++b) {
+            const paste_binding bd = pool.bindings[bind_off + b];
+            const int age = (src >> (4 * b)) & 15;
+            const int32_t ev = P.win.evt[rbase + gs[age] * rstride];
+            const int64_t r = resolve_fast(P.win, pool.steps, bd, bind_off + b, ev, age, gt, memo);
+            if (r < 0) comp = PASTE_C_PARTIAL;
+            P.out.pred_arg[X.a(i, b)] = r;
+          }
+        }
+        const int64_t o = X.o(i);
+        P.out.pred_pat[o] = pid;
+        P.out.pred_comp[o] = (uint8_t)comp;
+        if (admit) admit_one(P, X, i, tool, comp, p, n_act, seen);
+      }
+      n_pred = nm;
+    } else {
+      // ---- scan path (no table): bucket in rank order ------------------------
+      const int a = gt[0];
+      const int b0 = __ldg(pool.bucket_off + a), b1 = __ldg(pool.bucket_off + a + 1);
+      const bool scan_all = __ldg(pool.bucket_scan_all + a) != 0;
+      const bool anchored = pool.relation == PASTE_REL_ANCHORED;
+#define GT(p) gt[m - 1 - (p)]
+      for (int bi = b0; bi < b1; ++bi) {
+        const int pid = __ldg(pool.bucket_pat + bi);
+        const int4 h = __ldg(reinterpret_cast<const int4*>(pool.patterns + pid));
+        const int nctx = h.y, tool = h.z, bind_off = h.w;
+        const int32_t* ctx = pool.ctx_sig + h.x;
+        bool ok;
+        if (anchored) {
+          int j = nctx - 2, pos = m - 2;
+          while (j >= 0 && pos >= 0) {
+            j -= GT(pos) == __ldg(ctx + j);
+            --pos;
+          }
+          ok = j < 0;
+        } else {
+          ok = nctx <= m;
+          for (int i = 0; ok && i < nctx - 1; ++i) ok = GT(m - nctx + i) == __ldg(ctx + i);
+        }
+        if (!ok) continue;
+        const int4 h2 = __ldg(reinterpret_cast<const int4*>(pool.patterns + pid) + 1);
+        const int n_bind = h2.x, pflags = h2.y;
+        const double p = __hiloint2double(h2.w, h2.z);
+        if (pflags & PASTE_PF_STRUCT_ERR) {
+          ++n_err;
+          continue;
+        }
+        if (n_pred >= K) {
+          if (!scan_all) break;
+          continue;
+        }
+        int comp = PASTE_C_TOOL_ONLY;
+        if (pflags & PASTE_PF_HAS_MAPPING) {
+          comp = PASTE_C_FULL;
+          for (int b = 0; b < n_bind; ++b) {
+            const paste_binding bd = pool.bindings[bind_off + b];
+            int src;  // matched position of context element ctx_pos
+            if (!anchored) {
+              src = m - nctx + bd.ctx_pos;
+            } else if (bd.ctx_pos == nctx - 1) {
+              src = m - 1;
+            } else {
+              int j = nctx - 2, pos = m - 2;
+              src = 0;
+              while (j >= 0 && pos >= 0) {
+                if (GT(pos) == __ldg(ctx + j)) {
+                  if (j == bd.ctx_pos) { src = pos; break; }
+                  --j;
+                }
+                --pos;
+              }
+            }
+            const int age = m - 1 - src;
+            const int32_t ev = P.win.evt[rbase + gs[age] * rstride];
+            const int64_t r = resolve_fast(P.win, pool.steps, bd, bind_off + b, ev, age, gt, memo);
+            if (r < 0) comp = PASTE_C_PARTIAL;
+            P.out.pred_arg[X.a(n_pred, b)] = r;
+          }
+        }
+        const int64_t o = X.o(n_pred);
+        P.out.pred_pat[o] = pid;
+        P.out.pred_comp[o] = (uint8_t)comp;
+        if (admit) admit_one(P, X, n_pred, tool, comp, p, n_act, seen);
+        ++n_pred;
+        if (n_pred >= K && !scan_all) break;
+      }
+#undef GT
+    }
+  }
+  P.out.n_pred[sess] = n_pred;
+  P.out.struct_err[sess] = n_err;
+  if (admit) P.out.n_act[sess] = n_act;
+}
+
+
+// Persistent CTAs (grid = SMs x resident CTAs): each loops over 128-session
+// chunks so its shared-memory walk memo stays warm across chunks.
+template <bool TABLE>
+__global__ void __launch_bounds__(FT, 8) predict_fast_kernel(const FastParams P) {
+  extern __shared__ uint64_t s_mem[];
+  uint64_t* memo = s_mem;
+  for (int i = threadIdx.x; i < MEMO; i += FT) memo[i] = 0;
+  __syncthreads();
+  int32_t* gt = reinterpret_cast<int32_t*>(s_mem + MEMO) + threadIdx.x * P.row;
+  const int64_t n = P.win.n_sessions;
+  for (int64_t first = (int64_t)blockIdx.x * FT; first < n; first += (int64_t)gridDim.x * FT) {
+    const int64_t sess = first + threadIdx.x;
+    if (sess < n) predict_session<TABLE>(P, sess, gt, memo);
+  }
+}
+
+// Returns true when the fast path handled the launch.
+bool predict_fast_dispatch(const paste_pool_desc* pool, const paste_windows* win,
+                           const paste_admit_desc* adm, const paste_predict_out* out,
+                           int G, cudaStream_t stream) {
+  if (G > 16 || out->max_candidates > 32767) return false;
+  FastParams P{*pool, *win, *adm, *out, G, 2 * G + 1};
+  if (P.pool.match_table != nullptr &&
+      (P.pool.mt_k < out->max_candidates || P.pool.mt_g != G || pool->max_bindings > MT_MAX_BIND))
+    P.pool.match_table = nullptr;  // stale table: scan instead
+  const size_t smem = sizeof(uint64_t) * MEMO + sizeof(int32_t) * FT * P.row;
+  const bool table = P.pool.match_table != nullptr;
+  static int sms = 0, per_sm[2] = {0, 0};
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int& occ = per_sm[table ? 1 : 0];
+  if (occ == 0) {
+    if (table)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, predict_fast_kernel<true>, FT, smem);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, predict_fast_kernel<false>, FT, smem);
+    if (occ < 1) occ = 1;
+  }
+  const int64_t chunks = (win->n_sessions + FT - 1) / FT;
+  const int64_t grid = chunks < (int64_t)sms * occ ? chunks : (int64_t)sms * occ;
+  if (table)
+    predict_fast_kernel<true><<<(unsigned)grid, FT, smem, stream>>>(P);
+  else
+    predict_fast_kernel<false><<<(unsigned)grid, FT, smem, stream>>>(P);
+  return true;
+}
+
+}  // namespace paste

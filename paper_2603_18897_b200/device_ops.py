@@ -9,6 +9,7 @@ for device memory and streams only.
 from __future__ import annotations
 
 import ctypes
+import os
 from typing import Any, Callable, Sequence
 
 import numpy as np
@@ -50,6 +51,8 @@ class DevicePool:
         self.keys = KeyTable() if keys is None else keys
         self.image = PoolImage.compile(pool, self.sigs, self.keys)
         self._dev: dict[str, Any] | None = None
+        self._tables: dict[tuple[int, int], tuple[Any, int]] = {}
+        self.table_budget = 256 << 20  # bytes of HBM a pool's match tables may use
 
     def device_arrays(self) -> dict[str, Any]:
         if self._dev is None:
@@ -61,13 +64,36 @@ class DevicePool:
                 im.bucket_scan_all if len(im.bucket_scan_all) else np.zeros(1, np.uint8))
         return self._dev
 
-    def desc(self) -> PoolDesc:
+    def desc(self, max_candidates: int | None = None, capacity: int | None = None) -> PoolDesc:
+        """Pool descriptor; with (max_candidates, capacity) it carries the
+        compiled match table for that request shape when the pool fits."""
         d = self.device_arrays()
         im = self.image
-        return PoolDesc(len(im.pool.patterns), im.n_bucket_sigs, im.k, im.relation, im.max_ctx,
+        desc = PoolDesc(len(im.pool.patterns), im.n_bucket_sigs, im.k, im.relation, im.max_ctx,
                         im.max_bindings, ptr(d["patterns"]), ptr(d["bindings"]), ptr(d["ctx_sig"]),
                         ptr(d["steps"]), ptr(d["bucket_off"]), ptr(d["bucket_pat"]),
-                        ptr(d["bucket_scan_all"]))
+                        ptr(d["bucket_scan_all"]), 0, 0, 0)
+        if max_candidates is not None and capacity is not None:
+            table, g = self.match_table(desc, max_candidates, capacity)
+            if table is not None:
+                desc.match_table, desc.mt_k, desc.mt_g = ptr(table), max_candidates, g
+        return desc
+
+    def match_table(self, desc: PoolDesc, K: int, W: int):
+        """Device-built match table for (K, W), cached per pool (K4 compile step)."""
+        key = (K, W)
+        if key not in self._tables:
+            torch = _torch()
+            lib = _native.lib()
+            nbytes = lib.paste_match_table_bytes(ctypes.byref(desc), K, W)
+            table = None
+            if nbytes > 0 and nbytes <= self.table_budget and not os.environ.get("PASTE_NO_MATCH_TABLE"):
+                table = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+                check(lib.paste_build_match_table(ctypes.byref(desc), K, W, ptr(table),
+                                                  stream_handle()), lib)
+            g = min(self.image.k if self.image.relation == 0 else self.image.max_ctx, W)
+            self._tables[key] = (table, g)
+        return self._tables[key]
 
     # -- predict -------------------------------------------------------------
 
@@ -97,10 +123,10 @@ class DevicePool:
             adm = AdmitDesc(1, len(admit[0]), ptr(allow), ptr(level), ptr(bene))
         else:
             adm = AdmitDesc(0, 0, 0, 0, 0)
-        out = PredictOut(K, B, ptr(o["n_pred"]), ptr(o["pred_pat"]), ptr(o["pred_comp"]),
+        out = PredictOut(K, B, 0, 0, ptr(o["n_pred"]), ptr(o["pred_pat"]), ptr(o["pred_comp"]),
                          ptr(o["pred_arg"]), ptr(o.get("n_act")), ptr(o.get("act_pred")),
                          ptr(o.get("act_level")), ptr(o.get("act_util")), ptr(o["struct_err"]))
-        pool = self.desc()
+        pool = self.desc(K, batch.capacity)
         check(lib.paste_predict_batch(ctypes.byref(pool), ctypes.byref(win), ctypes.byref(adm),
                                       ctypes.byref(out), stream_handle()), lib)
         h = {k: v.cpu().numpy() for k, v in o.items()}

@@ -85,10 +85,11 @@ class LiveSessionTable:
                     "act_util": torch.zeros(n * K, dtype=torch.float64, device=dev),
                     "struct_err": torch.zeros(n, dtype=torch.int32, device=dev)}
         o = self.out
-        self.out_desc = PredictOut(K, B, *[ptr(o[k]) for k in (
+        # slot-major ring and records: a step touches contiguous 128-byte lines
+        self.out_desc = PredictOut(K, B, 1, 0, *[ptr(o[k]) for k in (
             "n_pred", "pred_pat", "pred_comp", "pred_arg", "n_act", "act_pred", "act_level",
             "act_util", "struct_err")])
-        self.pool_desc = dpool.desc()
+        self.pool_desc = dpool.desc(max_candidates, capacity)
         self.steps = 0
         self.lib = _native.lib()
 
@@ -114,7 +115,7 @@ class LiveSessionTable:
 
     def launch(self, region: int, new_tok=None, new_ref=None) -> None:
         """observe (new event per session) + predict + admit, one kernel."""
-        win = WindowsDesc(self.n, self.W, 0, ptr(self.tok), ptr(self.evt), ptr(self.count),
+        win = WindowsDesc(self.n, self.W, 1, ptr(self.tok), ptr(self.evt), ptr(self.count),
                           ptr(self.nodes), ptr(self.bytes), ptr(self.refs),
                           ptr(self.new_tok if new_tok is None else new_tok),
                           ptr(self.new_ref if new_ref is None else new_ref),
@@ -146,7 +147,7 @@ class LiveSessionTable:
             h = {k: v.cpu().numpy() for k, v in self.out.items()}
         return PredictResult(self.K, self.B, h["n_pred"], h["pred_pat"], h["pred_comp"],
                              h["pred_arg"], h["n_act"], h["act_pred"], h["act_level"],
-                             h["act_util"], h["struct_err"])
+                             h["act_util"], h["struct_err"], 1)
 
     def pinned_outputs(self) -> dict:
         t = self.torch

@@ -199,6 +199,7 @@ class WindowBatch:
     count: np.ndarray    # i64[n]
     arena: TapeArena
     created: list[float | None]
+    slot_major: int = 0
 
     @property
     def n(self) -> int:
@@ -257,16 +258,32 @@ class PredictResult:
     act_level: np.ndarray | None
     act_util: np.ndarray | None
     struct_err: np.ndarray
+    slot_major: int = 0
 
     @classmethod
-    def empty(cls, n: int, K: int, B: int, admit: bool) -> "PredictResult":
+    def empty(cls, n: int, K: int, B: int, admit: bool, slot_major: int = 0) -> "PredictResult":
         return cls(K, B, np.zeros(n, np.int32), np.zeros(n * K, np.int32),
                    np.zeros(n * K, np.uint8), np.full(n * K * B, -1, np.int64),
                    np.zeros(n, np.int32) if admit else None,
                    np.zeros(n * K, np.int16) if admit else None,
                    np.zeros(n * K, np.uint8) if admit else None,
                    np.zeros(n * K, np.float64) if admit else None,
-                   np.zeros(n, np.int32))
+                   np.zeros(n, np.int32), slot_major)
+
+    def session_major(self) -> "PredictResult":
+        """The same records in per-session layout ([n][K], args [n][K][B])."""
+        if not self.slot_major:
+            return self
+        n, K, B = len(self.n_pred), self.K, self.B
+
+        def tr(a, width=1):
+            if a is None:
+                return None
+            return np.ascontiguousarray(a.reshape(K * width, n).T).reshape(-1)
+
+        return PredictResult(K, B, self.n_pred, tr(self.pred_pat), tr(self.pred_comp),
+                             tr(self.pred_arg, B), self.n_act, tr(self.act_pred),
+                             tr(self.act_level), tr(self.act_util), self.struct_err, 0)
 
 
 def decode_predictions(res: PredictResult, image: PoolImage, arena: TapeArena,
@@ -275,6 +292,7 @@ def decode_predictions(res: PredictResult, image: PoolImage, arena: TapeArena,
     from .prediction import Completeness, PredictedInvocation
 
     comp_enum = (Completeness.FULL, Completeness.PARTIAL, Completeness.TOOL_ONLY)
+    res = res.session_major()
     out = []
     K, B = res.K, res.B
     for s in range(len(res.n_pred)):
@@ -308,6 +326,7 @@ def decode_actions(res: PredictResult, preds_per_session):
     from .policy import SpecLevel, SpeculativeAction
 
     out = []
+    res = res.session_major()
     K = res.K
     for s, preds in enumerate(preds_per_session):
         acts = []

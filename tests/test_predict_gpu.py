@@ -114,7 +114,7 @@ def _live_vs_oracle(dp, n, steps, seed, policy, book, K=8, workload=None):
                              max_candidates=K)
     W, R = table.W, table.regions
     host = WindowBatch(W, np.full(n * W, -1, np.int32), np.full(n * W, -1, np.int32),
-                       np.zeros(n, np.int64), None, [])
+                       np.zeros(n, np.int64), None, [], slot_major=1)
     refs = np.zeros((R * n, 2), np.int64)
     host.arena = (wl.tmpl.nodes, np.zeros(1, np.uint8), refs)
     tables = admit_tables(dp.sigs, policy, book.duration)
@@ -127,7 +127,7 @@ def _live_vs_oracle(dp, n, steps, seed, policy, book, K=8, workload=None):
         ora = bridge.predict(dp.image, host, K, tables, new_tok=batch.tok,
                              new_ref=np.ascontiguousarray(batch.ref), new_evt_base=region * n,
                              new_byte_base=region * table.max_batch_bytes, threads=8)
-        _compare(dev, ora)
+        _compare(dev.session_major(), ora)
         total_preds += int(dev.n_pred.sum())
     state = table.host_state()
     assert np.array_equal(state["tok"], host.tok) and np.array_equal(state["count"], host.count)
@@ -168,3 +168,20 @@ def test_live_stress_pool_matches_oracle():
     n = _live_vs_oracle(dp, 10_000, 20, 3, SpeculationPolicy(default_allow=True), EstimateBook(),
                         K=8, workload=Renamed())
     assert n > 0
+
+
+def test_generic_kernel_path_matches_too():
+    """Re-run the golden and live parity tests with the generic (non-fast)
+    kernel pinned, so both device code paths stay parity-checked."""
+    import os
+    import subprocess
+    import sys
+
+    if os.environ.get("PASTE_FORCE_GENERIC") or os.environ.get("PASTE_NO_MATCH_TABLE"):
+        pytest.skip("already running pinned to an alternative kernel path")
+    for var in ("PASTE_FORCE_GENERIC", "PASTE_NO_MATCH_TABLE"):
+        env = dict(os.environ, **{var: "1"})
+        proc = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__,
+                               "-k", "golden or live"], env=env, capture_output=True, text=True,
+                              cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        assert proc.returncode == 0, var + proc.stdout[-3000:] + proc.stderr[-3000:]
