@@ -225,6 +225,42 @@ typedef struct {
 int paste_admit_lists(const paste_admit_desc* policy, paste_admit_lists_desc* lists,
                       void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* Mining (K1 ingest, K2 count, selection; mining.py:164-292)               */
+/* ---------------------------------------------------------------------- */
+
+/* Token stream: int32 sig ids, bit 31 set on the first tool event of every
+ * segment (session after inactivity splitting).  Tables are dense over
+ * S = n_sigs signatures and contexts of length 1..k: context (c_1..c_n) has
+ * index sum_{m<n} S^m + sum_i c_i * S^(n-i); T = S / 2 tools.             */
+typedef struct {
+  int32_t n_sigs;
+  int32_t k;                 /* MiningConfig.k (1..6)                          */
+  int32_t relation;          /* PASTE_REL_*                                    */
+  int32_t pad;
+  const int32_t* tokens;     /* [n_tokens] flagged token stream               */
+  int64_t n_tokens;
+  uint32_t* hist;            /* [(S+2)^(k+1)] (k+1)-gram histogram (zeroed)    */
+  uint64_t* tool_count;      /* [T]        occurrences per tool (zeroed)       */
+  uint64_t* support;         /* [T][n_ctx] window support (zeroed)             */
+  uint64_t* match;           /* [n_ctx]    anchored matches (zeroed)           */
+  uint64_t* follow;          /* [n_ctx][T] matches followed by the tool (zeroed)*/
+} paste_mine_desc;
+
+/* Sizes of the dense histogram and context space for (n_sigs, k).          */
+int paste_mine_geometry(int32_t n_sigs, int32_t k, int64_t* n_bins, int64_t* n_ctx);
+/* K2: accumulate the (k+1)-gram histogram of a token stream (adds to hist,
+ * so shards can be counted into one histogram or merged by all-reduce).    */
+int paste_mine_count(const paste_mine_desc* d, void* stream);
+/* Expand the histogram into tool_count / support / match / follow.         */
+int paste_mine_expand(const paste_mine_desc* d, void* stream);
+/* Candidates (target, context) with tool_count >= sigma, support >= sigma,
+ * match > 0 and follow / match >= tau (the upper bound of p for any
+ * mapping): out[5*i..] = {tool, context index, support, match, follow};
+ * *n_out receives the number found (only the first `cap` are written).    */
+int paste_mine_select(const paste_mine_desc* d, int64_t sigma, double tau, int64_t cap,
+                      uint64_t* n_out, int64_t* out, void* stream);
+
 /* Number of kernel launches the last paste_* call on this thread issued.   */
 int paste_last_launch_count(void);
 

@@ -80,3 +80,42 @@ def predict(im: PoolImage, batch: WindowBatch, K: int,
         raise RuntimeError(f"oracle_predict_batch failed: {rc}")
     del keep
     return res
+
+
+def mine_counts(tokens: np.ndarray, n_sigs: int, k: int, relation: int):
+    """Oracle mining tables (tool_count, support, match, follow) as numpy."""
+    L = lib()
+    fn = L.oracle_mine_counts
+    fn.restype = c_int
+    fn.argtypes = [c_void_p, ctypes.c_int64, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                   c_void_p]
+    T = (n_sigs + 1) // 2
+    n_ctx = sum(n_sigs ** q for q in range(1, k + 1))
+    tool_count = np.zeros(T, np.uint64)
+    support = np.zeros(T * n_ctx, np.uint64)
+    match = np.zeros(n_ctx, np.uint64)
+    follow = np.zeros(n_ctx * T, np.uint64)
+    tok = np.ascontiguousarray(tokens, np.int32)
+    rc = fn(_p(tok), len(tok), n_sigs, k, relation, _p(tool_count), _p(support), _p(match),
+            _p(follow))
+    if rc != 0:
+        raise RuntimeError("oracle_mine_counts failed")
+    return tool_count, support, match, follow
+
+
+def select_candidates(tool_count, support, match, follow, n_sigs, k, sigma, tau):
+    """Host restatement of the mine() gates over oracle tables:
+    [(tool, ctx index, support, match, follow)] with follow/match >= tau."""
+    T = (n_sigs + 1) // 2
+    n_ctx = len(match)
+    out = []
+    sup = support.reshape(T, n_ctx)
+    fol = follow.reshape(n_ctx, T)
+    for t in range(T):
+        if tool_count[t] < sigma:
+            continue
+        for c in np.flatnonzero(sup[t] >= sigma):
+            m = int(match[c])
+            if m and int(fol[c, t]) / m >= tau:
+                out.append((t, int(c), int(sup[t, c]), m, int(fol[c, t])))
+    return out

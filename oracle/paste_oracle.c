@@ -270,3 +270,122 @@ int oracle_predict_batch(const paste_pool_desc* pool, const char* pids, paste_wi
   }
   return PASTE_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Mining counts (mine(), mining.py:248-292), restated per the reference:    */
+/*  - tool_count / support from the windows of every target occurrence       */
+/*    (mining.py:258-275, distinct subsequences :164-183, suffixes :186-194); */
+/*  - match / follow by running the literal match_at greedy (mining.py:119-  */
+/*    156) for every context that could match at an anchor (all sequences   */
+/*    over the signatures seen in the last k events ending with the anchor), */
+/*    counting exactly what _collect_occurrences (mining.py:215-227) counts. */
+/* Tables are dense as in paste_mine_desc.                                   */
+/* ------------------------------------------------------------------------ */
+
+static int64_t o_ctx_index(const int* c, int n, int S) {
+  /* offset of length-n contexts = S + S^2 + ... + S^(n-1), then base-S digits */
+  int64_t off = 0, p = 1, v = 0;
+  int i;
+  for (i = 1; i < n; ++i) { p *= S; off += p; }
+  for (i = 0; i < n; ++i) v = v * S + c[i];
+  return off + v;
+}
+
+/* literal match_at on a signature stream (anchored subsequence / suffix) */
+static int o_match_at(const int* st, int anchor, const int* ctx, int n, int k, int relation) {
+  int lo, j, pos, start, i;
+  if (n == 0 || st[anchor] != ctx[n - 1]) return 0;
+  if (relation == PASTE_REL_SUFFIX) {
+    start = anchor - n + 1;
+    if (start < 0) return 0;
+    for (i = 0; i < n; ++i)
+      if (st[start + i] != ctx[i]) return 0;
+    return 1;
+  }
+  lo = anchor - k + 1;
+  if (lo < 0) lo = 0;
+  j = n - 2;
+  pos = anchor - 1;
+  while (j >= 0 && pos >= lo) {
+    if (st[pos] == ctx[j]) --j;
+    --pos;
+  }
+  return j < 0;
+}
+
+int oracle_mine_counts(const int32_t* tokens, int64_t n_tokens, int S, int k, int relation,
+                       uint64_t* tool_count, uint64_t* support, uint64_t* match,
+                       uint64_t* follow) {
+  const int T = (S + 1) / 2;
+  int64_t n_ctx = 0, p = 1, i0, i;
+  int q;
+  for (q = 1; q <= k; ++q) { p *= S; n_ctx += p; }
+  i0 = 0;
+  while (i0 < n_tokens) { /* one stream */
+    int64_t i1 = i0 + 1;
+    int L, j, a;
+    int* st;
+    while (i1 < n_tokens && !(tokens[i1] & (int32_t)0x80000000)) ++i1;
+    L = (int)(i1 - i0);
+    st = (int*)malloc(sizeof(int) * (size_t)L);
+    for (i = 0; i < L; ++i) st[i] = (int)(tokens[i0 + i] & 0x7fffffff);
+    /* targets: windows of the <= k events before j */
+    for (j = 0; j < L; ++j) {
+      const int tool = st[j] >> 1;
+      const int lo = j - k < 0 ? 0 : j - k;
+      const int wl = j - lo;
+      tool_count[tool] += 1;
+      if (relation == PASTE_REL_SUFFIX) {
+        int s;
+        for (s = lo; s < j; ++s) support[(int64_t)tool * n_ctx + o_ctx_index(st + s, j - s, S)] += 1;
+      } else {
+        /* distinct subsequences: collect all, dedupe by index */
+        int64_t seen[64];
+        int ns = 0, mask, b;
+        for (mask = 1; mask < (1 << wl); ++mask) {
+          int c[8], len = 0, dup = 0;
+          int64_t idx;
+          for (b = 0; b < wl; ++b)
+            if (mask & (1 << b)) c[len++] = st[lo + b];
+          idx = o_ctx_index(c, len, S);
+          for (b = 0; b < ns; ++b) dup |= seen[b] == idx;
+          if (dup) continue;
+          seen[ns++] = idx;
+          support[(int64_t)tool * n_ctx + idx] += 1;
+        }
+      }
+    }
+    /* anchors: every candidate context over the signatures of the last k
+     * events that ends with the anchor, tested with the literal match_at */
+    for (a = 0; a < L; ++a) {
+      int alpha[8], na = 0, s, d, n;
+      const int lo = a - k + 1 < 0 ? 0 : a - k + 1;
+      const int lo2 = relation == PASTE_REL_SUFFIX ? (a - k + 1 < 0 ? 0 : a - k + 1) : lo;
+      for (s = lo2; s < a; ++s) {
+        int dup = 0;
+        for (d = 0; d < na; ++d) dup |= alpha[d] == st[s];
+        if (!dup) alpha[na++] = st[s];
+      }
+      for (n = 1; n <= k; ++n) {
+        /* all sequences of length n-1 over alpha, then the anchor */
+        int64_t combos = 1, cidx;
+        for (d = 0; d < n - 1; ++d) combos *= na;
+        for (cidx = 0; cidx < combos; ++cidx) {
+          int c[8];
+          int64_t v = cidx;
+          for (d = n - 2; d >= 0; --d) { c[d] = alpha[v % (na ? na : 1)]; v /= (na ? na : 1); }
+          c[n - 1] = st[a];
+          if (!o_match_at(st, a, c, n, k, relation)) continue;
+          {
+            const int64_t ci = o_ctx_index(c, n, S);
+            match[ci] += 1;
+            if (a + 1 < L) follow[ci * T + (st[a + 1] >> 1)] += 1;
+          }
+        }
+      }
+    }
+    free(st);
+    i0 = i1;
+  }
+  return PASTE_OK;
+}

@@ -74,6 +74,13 @@ class AdmitListsDesc(ctypes.Structure):
                 ("act_level", c_void_p), ("act_util", c_void_p)]
 
 
+class MineDesc(ctypes.Structure):
+    _fields_ = [("n_sigs", c_int32), ("k", c_int32), ("relation", c_int32), ("pad", c_int32),
+                ("tokens", c_void_p), ("n_tokens", c_int64), ("hist", c_void_p),
+                ("tool_count", c_void_p), ("support", c_void_p), ("match", c_void_p),
+                ("follow", c_void_p)]
+
+
 # numpy mirrors of the element structs
 PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
                           ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
@@ -92,6 +99,11 @@ EXPORTS = {
     "paste_admit_lists": (c_int, [POINTER(AdmitDesc), POINTER(AdmitListsDesc), c_void_p]),
     "paste_match_table_bytes": (c_int64, [POINTER(PoolDesc), c_int32, c_int32]),
     "paste_build_match_table": (c_int, [POINTER(PoolDesc), c_int32, c_int32, c_void_p, c_void_p]),
+    "paste_mine_geometry": (c_int, [c_int32, c_int32, POINTER(c_int64), POINTER(c_int64)]),
+    "paste_mine_count": (c_int, [POINTER(MineDesc), c_void_p]),
+    "paste_mine_expand": (c_int, [POINTER(MineDesc), c_void_p]),
+    "paste_mine_select": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64, c_void_p,
+                                  c_void_p, c_void_p]),
 }
 
 _lib = None

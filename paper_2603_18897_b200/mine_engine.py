@@ -1,0 +1,318 @@
+"""Device mining engine: packing, K2 count / expand / select, Phase II glue.
+
+``mine()`` (mining.py:248-292) becomes:
+
+1. pack every session's tool events into one flagged token stream (tools
+   interned in sorted name order, so sig order == the reference's
+   (tool_type, status.value) order);
+2. K2 on the device: (k+1)-gram histogram -> tool_count / support / match /
+   follow tables -> candidate (target, context) pairs that clear sigma and
+   whose follow/match bound clears tau (libpaste: paste_mine_*);
+3. per candidate, Phase II mapping inference on its occurrences (host, see
+   phase2.py) and p = hits / matches;
+4. the reference's deterministic output order (_sort_key, mining.py:105-111).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Any, Sequence
+
+import numpy as np
+
+from . import _native
+from ._native import MineDesc, check, ptr
+from .events import Event, EventSignature, Session, Status, signature_of
+from .mappings import MatchedContext, ValueMapping
+from .mining import MatchRelation, MiningConfig, PatternTuple, pattern_sort_key
+from .packing import SigTable
+from . import phase2
+
+SEG_START = np.int32(-2**31)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# packing
+# ---------------------------------------------------------------------------
+
+def pack_streams(streams: Sequence[Sequence[Event]], sigs: SigTable) -> np.ndarray:
+    """Flagged token stream: sig ids, bit 31 on each stream's first event."""
+    total = sum(len(s) for s in streams)
+    tok = np.empty(total, np.int32)
+    at = 0
+    for st in streams:
+        for i, ev in enumerate(st):
+            t = sigs.sig(ev.tool_type, ev.status)
+            tok[at] = t | SEG_START if i == 0 else t
+            at += 1
+    return tok
+
+
+def ctx_offsets(S: int, k: int) -> list[int]:
+    off = [0, 0]
+    for n in range(1, k + 1):
+        off.append(off[-1] + S ** n)
+    return off
+
+
+def decode_context(idx: int, S: int, k: int) -> tuple[int, ...]:
+    off = ctx_offsets(S, k)
+    n = next(n for n in range(1, k + 1) if off[n] <= idx < off[n + 1])
+    v = idx - off[n]
+    out = []
+    for _ in range(n):
+        out.append(v % S)
+        v //= S
+    return tuple(reversed(out))
+
+
+def encode_context(ctx: Sequence[int], S: int, k: int) -> int:
+    v = 0
+    for c in ctx:
+        v = v * S + c
+    return ctx_offsets(S, k)[len(ctx)] + v
+
+
+# ---------------------------------------------------------------------------
+# device tables
+# ---------------------------------------------------------------------------
+
+@dataclass
+class MineTables:
+    """Device-resident K2 state for one (n_sigs, k, relation) geometry."""
+
+    n_sigs: int
+    k: int
+    relation: int
+    n_bins: int
+    n_ctx: int
+    hist: Any
+    tool_count: Any
+    support: Any
+    match: Any
+    follow: Any
+
+    @classmethod
+    def allocate(cls, n_sigs: int, k: int, relation: int) -> "MineTables":
+        torch = _torch()
+        lib = _native.lib()
+        nb, nc = ctypes.c_int64(), ctypes.c_int64()
+        check(lib.paste_mine_geometry(n_sigs, k, ctypes.byref(nb), ctypes.byref(nc)), lib)
+        T = (n_sigs + 1) // 2
+        dev = torch.device("cuda")
+        return cls(n_sigs, k, relation, nb.value, nc.value,
+                   torch.zeros(nb.value, dtype=torch.int32, device=dev),
+                   torch.zeros(T, dtype=torch.int64, device=dev),
+                   torch.zeros(T * nc.value, dtype=torch.int64, device=dev),
+                   torch.zeros(nc.value, dtype=torch.int64, device=dev),
+                   torch.zeros(nc.value * T, dtype=torch.int64, device=dev))
+
+    def desc(self, tokens=None, n_tokens: int = 0) -> MineDesc:
+        return MineDesc(self.n_sigs, self.k, self.relation, 0, ptr(tokens), n_tokens,
+                        ptr(self.hist), ptr(self.tool_count), ptr(self.support), ptr(self.match),
+                        ptr(self.follow))
+
+    def count(self, tokens) -> None:
+        """Accumulate the (k+1)-gram histogram of a device token stream."""
+        from .device_ops import stream_handle
+
+        lib = _native.lib()
+        d = self.desc(tokens, int(tokens.numel()))
+        check(lib.paste_mine_count(ctypes.byref(d), stream_handle()), lib)
+
+    def expand(self) -> None:
+        from .device_ops import stream_handle
+
+        lib = _native.lib()
+        for t in (self.tool_count, self.support, self.match, self.follow):
+            t.zero_()
+        d = self.desc()
+        check(lib.paste_mine_expand(ctypes.byref(d), stream_handle()), lib)
+
+    def select(self, sigma: int, tau: float) -> np.ndarray:
+        """Candidates [m, 5] = (tool, ctx index, support, match, follow)."""
+        from .device_ops import stream_handle
+
+        torch = _torch()
+        lib = _native.lib()
+        cap = 1 << 16
+        while True:
+            n_out = torch.zeros(1, dtype=torch.int64, device="cuda")
+            out = torch.empty(5 * cap, dtype=torch.int64, device="cuda")
+            d = self.desc()
+            check(lib.paste_mine_select(ctypes.byref(d), sigma, float(tau), cap, ptr(n_out),
+                                        ptr(out), stream_handle()), lib)
+            m = int(n_out.item())
+            if m <= cap:
+                return out[:5 * m].view(m, 5).cpu().numpy()
+            cap = m
+
+
+# ---------------------------------------------------------------------------
+# host matching (Phase II occurrences and the match_at utility)
+# ---------------------------------------------------------------------------
+
+def match_events(stream: Sequence[Event], sig_stream: Sequence, anchor: int, context: Sequence,
+                 k: int, relation: MatchRelation) -> MatchedContext | None:
+    """match_at over a precomputed signature stream (mining.py:119-156)."""
+    n = len(context)
+    if n == 0 or anchor >= len(stream) or sig_stream[anchor] != context[-1]:
+        return None
+    if relation is MatchRelation.CONTIGUOUS_SUFFIX:
+        start = anchor - n + 1
+        if start < 0 or any(sig_stream[start + i] != context[i] for i in range(n)):
+            return None
+        sl = tuple(stream[start:anchor + 1])
+        return MatchedContext(events=sl, history=sl)
+    lo = max(0, anchor - k + 1)
+    picked = [anchor]
+    j, pos = n - 2, anchor - 1
+    while j >= 0 and pos >= lo:
+        if sig_stream[pos] == context[j]:
+            picked.append(pos)
+            j -= 1
+        pos -= 1
+    if j >= 0:
+        return None
+    picked.reverse()
+    return MatchedContext(events=tuple(stream[p] for p in picked),
+                          history=tuple(stream[picked[0]:anchor + 1]))
+
+
+def match_at(stream, anchor, context, k, relation):
+    sig_stream = [signature_of(e) for e in stream]
+    return match_events(stream, sig_stream, anchor, context, k, relation)
+
+
+def _occurrences(streams, sig_streams, context: tuple, target: str, cfg: MiningConfig):
+    """(matched, next) pairs whose next event is ``target``, in stream order."""
+    occ = []
+    for st, sg in zip(streams, sig_streams):
+        for a in range(len(st) - 1):
+            if st[a + 1].tool_type != target or sg[a] != context[-1]:
+                continue
+            m = match_events(st, sg, a, context, cfg.k, cfg.match_relation)
+            if m is not None:
+                occ.append((m, st[a + 1]))
+    return occ
+
+
+# ---------------------------------------------------------------------------
+# public entry points
+# ---------------------------------------------------------------------------
+
+def _count_corpus(streams, cfg: MiningConfig):
+    torch = _torch()
+    tools = sorted({e.tool_type for st in streams for e in st})
+    sigs = SigTable(tools)
+    relation = 0 if cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE else 1
+    tables = MineTables.allocate(max(sigs.n_sigs, 2), cfg.k, relation)
+    tok = pack_streams(streams, sigs)
+    if len(tok):
+        tables.count(torch.from_numpy(tok).cuda())
+    tables.expand()
+    return sigs, tables
+
+
+def mine(traces: Sequence[Session], cfg: MiningConfig) -> list[PatternTuple]:
+    if not traces:
+        raise ValueError("traces must be non-empty")
+    streams = [s.tool_events() for s in traces]
+    sigs, tables = _count_corpus(streams, cfg)
+    cands = tables.select(cfg.sigma, cfg.tau)
+    S = tables.n_sigs
+    sig_streams = None
+    patterns = []
+    for tool, cidx, support, n_match, follow in cands.tolist():
+        context = tuple(sigs.signature(x) for x in decode_context(cidx, S, cfg.k))
+        target = sigs.tools[tool]
+        mapping = None
+        hits = follow
+        if follow >= 2:
+            if sig_streams is None:
+                sig_streams = [[signature_of(e) for e in st] for st in streams]
+            occ = _occurrences(streams, sig_streams, context, target, cfg)
+            mapping = phase2.infer_mapping(occ, cfg.validation_fraction)
+            if mapping is not None:
+                hits = sum(1 for m, nxt in occ if phase2.mapping_holds(mapping, m, nxt))
+        p = hits / n_match
+        if p >= cfg.tau:
+            patterns.append(PatternTuple(context=context, target=target, mapping=mapping, p=p,
+                                         support=support))
+    patterns.sort(key=pattern_sort_key)
+    return patterns
+
+
+def validate(context, target: str, mapping: ValueMapping | None, traces: Sequence[Session],
+             cfg: MiningConfig) -> float:
+    streams = [s.tool_events() for s in traces]
+    if len(context) > cfg.k and cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE:
+        raise ValueError("context has no matches in the given traces")
+    tools = sorted({e.tool_type for st in streams for e in st} | {s.tool_type for s in context}
+                   | {target})
+    sigs = SigTable(tools)
+    relation = 0 if cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE else 1
+    k = max(cfg.k, len(context))
+    tables = MineTables.allocate(max(sigs.n_sigs, 2), k, relation)
+    torch = _torch()
+    tok = pack_streams(streams, sigs)
+    if len(tok):
+        tables.count(torch.from_numpy(tok).cuda())
+    tables.expand()
+    if k != cfg.k:  # contexts longer than k only exist under the suffix relation
+        pass
+    cidx = encode_context([sigs.sig_of(s) for s in context], tables.n_sigs, k)
+    n_match = int(tables.match[cidx].item())
+    if n_match == 0:
+        raise ValueError("context has no matches in the given traces")
+    follow = int(tables.follow[cidx * ((tables.n_sigs + 1) // 2) + sigs.tool(target)].item())
+    if mapping is None:
+        return follow / n_match
+    sig_streams = [[signature_of(e) for e in st] for st in streams]
+    occ = _occurrences(streams, sig_streams, tuple(context), target,
+                       MiningConfig(k=cfg.k, sigma=cfg.sigma, tau=cfg.tau,
+                                    validation_fraction=cfg.validation_fraction,
+                                    match_relation=cfg.match_relation))
+    hits = sum(1 for m, nxt in occ if phase2.mapping_holds(mapping, m, nxt))
+    return hits / n_match
+
+
+def frequent_subsequences(windows, sigma: int) -> dict:
+    """Distinct-subsequence support over arbitrary windows (mining.py:164-183):
+    each window becomes a segment ``window + [probe]`` and its support is
+    read from the probe tool's row of the device support table."""
+    torch = _torch()
+    windows = [tuple(w) for w in windows]
+    kmax = max((len(w) for w in windows), default=0)
+    if kmax == 0:
+        return {}
+    if kmax > 6:
+        raise _native.PasteUnsupported("windows longer than 6 signatures")
+    tools = sorted({s.tool_type for w in windows for s in w})
+    probe = "\x00probe"
+    sigs = SigTable(tools + [probe])
+    tables = MineTables.allocate(sigs.n_sigs, kmax, 0)
+    toks = []
+    for w in windows:
+        seg = [sigs.sig_of(s) for s in w] + [sigs.sig(probe, Status.SUCCESS)]
+        seg[0] |= int(SEG_START)
+        toks += seg
+    tables.count(torch.from_numpy(np.array(toks, np.int32)).cuda())
+    tables.expand()
+    row = tables.support[sigs.tool(probe) * tables.n_ctx:(sigs.tool(probe) + 1) * tables.n_ctx]
+    sup = row.cpu().numpy()
+    out = {}
+    for cidx in np.flatnonzero(sup >= sigma):
+        ctx = decode_context(int(cidx), tables.n_sigs, kmax)
+        if any(c == sigs.sig(probe, Status.SUCCESS) or c == sigs.sig(probe, Status.FAIL)
+               for c in ctx):
+            continue
+        out[tuple(sigs.signature(c) for c in ctx)] = int(sup[cidx])
+    return out

@@ -60,7 +60,7 @@ def _c_sizeof(struct_name: str) -> int:
 @pytest.mark.parametrize("cname,pyname", [
     ("paste_pool_desc", "PoolDesc"), ("paste_admit_desc", "AdmitDesc"),
     ("paste_windows", "WindowsDesc"), ("paste_predict_out", "PredictOut"),
-    ("paste_admit_lists_desc", "AdmitListsDesc"),
+    ("paste_admit_lists_desc", "AdmitListsDesc"), ("paste_mine_desc", "MineDesc"),
 ])
 def test_struct_layouts_match_header(cname, pyname):
     assert ctypes.sizeof(getattr(_native, pyname)) == _c_sizeof(cname)

@@ -1,0 +1,111 @@
+"""K2 parity on the GPU: mine() against the reference's golden outputs, and
+the device count tables against the CPU oracle (bit-exact) at larger sizes."""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from oracle import bridge  # noqa: E402
+from paper_2603_18897_b200 import mine, mine_frequent_subsequences, validate  # noqa: E402
+from paper_2603_18897_b200.events import EventSignature, Status  # noqa: E402
+from paper_2603_18897_b200.mappings import mapping_to_json  # noqa: E402
+from paper_2603_18897_b200.mine_engine import MineTables  # noqa: E402
+from paper_2603_18897_b200.mining import MatchRelation, MiningConfig  # noqa: E402
+
+MINE = G.golden("mine_golden.json")
+
+
+def _cfg(d):
+    return MiningConfig(k=d["k"], sigma=d["sigma"], tau=d["tau"],
+                        match_relation=MatchRelation(d["match_relation"]))
+
+
+def _as_json(p):
+    return {"context": [{"tool": s.tool_type, "status": s.status.value} for s in p.context],
+            "target": p.target, "mapping": mapping_to_json(p.mapping) if p.mapping else None,
+            "p": p.p, "support": p.support, "pattern_id": p.pattern_id}
+
+
+@pytest.mark.parametrize("group,idx", [("corpora", i) for i in range(len(MINE["corpora"]))]
+                         + [("mapped", i) for i in range(len(MINE["mapped"]))])
+def test_mine_matches_reference_golden(group, idx):
+    corpus = MINE[group][idx]
+    sessions = [G.session(s) for s in corpus["sessions"]]
+    got = [_as_json(p) for p in mine(sessions, _cfg(corpus["config"]))]
+    assert got == corpus["expected"]
+
+
+def _random_stream(n_sessions, n_sigs, seed, mean_len=8, planted=True):
+    rng = np.random.default_rng(seed)
+    lens = rng.geometric(1.0 / mean_len, n_sessions)
+    total = int(lens.sum())
+    tok = rng.integers(0, n_sigs, total, dtype=np.int32)
+    if planted:  # skew: a first-order chain so some grams repeat a lot
+        nxt = rng.integers(0, n_sigs, n_sigs)
+        follow = rng.random(total) < 0.5
+        tok[1:][follow[1:]] = nxt[tok[:-1][follow[1:]]]
+    starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    tok[starts] |= np.int32(-2**31)
+    return tok
+
+
+@pytest.mark.parametrize("n_sigs,k,rel", [(32, 3, 0), (32, 3, 1), (8, 4, 0), (8, 4, 1),
+                                          (16, 1, 0), (12, 2, 1), (6, 5, 0)])
+def test_count_tables_match_oracle(n_sigs, k, rel):
+    tok = _random_stream(20_000, n_sigs, seed=n_sigs * 10 + k)
+    t = MineTables.allocate(n_sigs, k, rel)
+    t.count(torch.from_numpy(tok).cuda())
+    t.expand()
+    ora = bridge.mine_counts(tok, n_sigs, k, rel)
+    for dev, ref in zip((t.tool_count, t.support, t.match, t.follow), ora):
+        assert np.array_equal(dev.cpu().numpy().astype(np.uint64), ref)
+
+
+def test_count_is_additive_across_shards():
+    """Shards counted into one histogram == the whole corpus (K3 merge basis)."""
+    tok = _random_stream(50_000, 32, seed=5)
+    cut = int(np.flatnonzero(tok < 0)[len(np.flatnonzero(tok < 0)) // 2])
+    whole = MineTables.allocate(32, 3, 0)
+    whole.count(torch.from_numpy(tok).cuda())
+    parts = MineTables.allocate(32, 3, 0)
+    parts.count(torch.from_numpy(tok[:cut]).cuda())
+    parts.count(torch.from_numpy(tok[cut:]).cuda())
+    assert torch.equal(whole.hist, parts.hist)
+
+
+def test_frequent_subsequences_spec_example():
+    A, B, C = (EventSignature(t, Status.SUCCESS) for t in "ABC")
+    got = mine_frequent_subsequences([[A, B], [A, C], [A, B]], 2)
+    assert got == {(A,): 3, (B,): 2, (A, B): 2}
+
+
+def test_frequent_subsequences_random_vs_bruteforce():
+    import itertools
+    import random
+
+    rng = random.Random(3)
+    sigs = [EventSignature(t, s) for t in "abc" for s in (Status.SUCCESS, Status.FAIL)]
+    windows = [[rng.choice(sigs) for _ in range(rng.randint(0, 5))] for _ in range(300)]
+    exp: dict = {}
+    for w in windows:
+        subs = {tuple(w[i] for i in range(len(w)) if m >> i & 1) for m in range(1, 1 << len(w))}
+        for s in subs:
+            exp[s] = exp.get(s, 0) + 1
+    exp = {s: c for s, c in exp.items() if c >= 4}
+    assert mine_frequent_subsequences(windows, 4) == exp
+
+
+def test_validate_matches_counts():
+    corpus = MINE["corpora"][0]
+    sessions = [G.session(s) for s in corpus["sessions"]]
+    cfg = _cfg(corpus["config"])
+    for p in corpus["expected"][:5]:
+        ctx = tuple(EventSignature(c["tool"], Status(c["status"])) for c in p["context"])
+        assert validate(ctx, p["target"], None, sessions, cfg) == p["p"]
