@@ -261,6 +261,26 @@ int paste_mine_expand(const paste_mine_desc* d, void* stream);
 int paste_mine_select(const paste_mine_desc* d, int64_t sigma, double tau, int64_t cap,
                       uint64_t* n_out, int64_t* out, void* stream);
 
+/* K1 + K2 fused over a columnar trace of tool events grouped by session
+ * (sessions in first-appearance order, events sorted by (t_start, seq)):
+ * segments split where t_start - prev.t_end > inactivity_ms (events.py:
+ * 196-252), then the (k+1)-gram histogram is accumulated into d->hist.
+ * Order violations are counted in *n_unsorted (callers must reject them).  */
+typedef struct {
+  int64_t n_events;
+  const int32_t* session;   /* [n] session index, non-decreasing             */
+  const int32_t* seq;       /* [n]                                           */
+  const double* t_start;    /* [n] ms                                        */
+  const double* t_end;      /* [n] ms                                        */
+  const int32_t* sig;       /* [n] tool signature id                         */
+  double inactivity_ms;
+  int32_t* tokens_out;      /* optional [n]: flagged token stream            */
+  uint64_t* n_segments;     /* optional counter                              */
+  uint64_t* n_unsorted;     /* optional counter                              */
+} paste_columnar_desc;
+
+int paste_mine_ingest_count(const paste_columnar_desc* c, const paste_mine_desc* d, void* stream);
+
 /* Number of kernel launches the last paste_* call on this thread issued.   */
 int paste_last_launch_count(void);
 

@@ -81,6 +81,13 @@ class MineDesc(ctypes.Structure):
                 ("follow", c_void_p)]
 
 
+class ColumnarDesc(ctypes.Structure):
+    _fields_ = [("n_events", c_int64), ("session", c_void_p), ("seq", c_void_p),
+                ("t_start", c_void_p), ("t_end", c_void_p), ("sig", c_void_p),
+                ("inactivity_ms", ctypes.c_double), ("tokens_out", c_void_p),
+                ("n_segments", c_void_p), ("n_unsorted", c_void_p)]
+
+
 # numpy mirrors of the element structs
 PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
                           ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
@@ -101,6 +108,7 @@ EXPORTS = {
     "paste_build_match_table": (c_int, [POINTER(PoolDesc), c_int32, c_int32, c_void_p, c_void_p]),
     "paste_mine_geometry": (c_int, [c_int32, c_int32, POINTER(c_int64), POINTER(c_int64)]),
     "paste_mine_count": (c_int, [POINTER(MineDesc), c_void_p]),
+    "paste_mine_ingest_count": (c_int, [POINTER(ColumnarDesc), POINTER(MineDesc), c_void_p]),
     "paste_mine_expand": (c_int, [POINTER(MineDesc), c_void_p]),
     "paste_mine_select": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64, c_void_p,
                                   c_void_p, c_void_p]),

@@ -306,3 +306,248 @@ extern "C" int paste_mine_select(const paste_mine_desc* d, int64_t sigma, double
   PASTE_CUDA_CHECK(cudaGetLastError());
   return PASTE_OK;
 }
+
+// ---------------------------------------------------------------------------
+// K1 + K2 fused: columnar trace events -> segments -> (k+1)-gram histogram.
+//
+// Ingest semantics (ingest_trace / _split_on_gaps, events.py:196-252) for a
+// columnar trace whose events are already grouped by session in first-
+// appearance order and sorted by (t_start, seq) inside a session: a new
+// segment starts at event y when y opens a session or
+// t_start[y] - t_end[y-1] > inactivity (fp64, strict).  Order violations are
+// counted (the host rejects unsorted input).  Each CTA stages a tile of
+// events plus a (k+1)-event halo in shared memory with coalesced loads.
+// ---------------------------------------------------------------------------
+constexpr int CT = 256;                 // threads
+constexpr int CTILE = 1024;             // events per tile
+constexpr int CPRE = 8;                 // halo before the tile (>= k + 1, 16-B aligned)
+constexpr int CSPAN = CTILE + 16;       // staged events per tile (halo + 1 after, padded)
+constexpr int CSTAGES = 2;
+constexpr int CHASH = 2048;             // per-CTA heavy-hitter table (keys, counts)
+constexpr uint32_t HEMPTY = 0xffffffffu;
+
+// Per-CTA aggregation: hot grams (e.g. the (BEGIN, .., BEGIN, s) grams every
+// session starts with) would otherwise serialise on a few L2 atomic units.
+__device__ __forceinline__ void hh_add(uint32_t* hkey, uint32_t* hcnt, uint32_t* hist, uint32_t key,
+                                       uint32_t inc) {
+  const uint32_t h = (key * 2654435761u) >> (32 - 11);  // log2(CHASH) = 11
+#pragma unroll
+  for (int probe = 0; probe < 4; ++probe) {
+    const uint32_t slot = (h + probe) & (CHASH - 1);
+    const uint32_t k0 = atomicCAS(hkey + slot, HEMPTY, key);
+    if (k0 == HEMPTY || k0 == key) {
+      atomicAdd(hcnt + slot, inc);
+      return;
+    }
+  }
+  atomicAdd(hist + key, inc);  // table region full: straight to L2
+}
+
+// one stage of staged columns
+struct __align__(16) ColumnTile {
+  double ts[CSPAN];
+  double te[CSPAN];
+  int32_t sess[CSPAN];
+  int32_t seq[CSPAN];
+  int32_t sig[CSPAN];
+  uint32_t v[CSPAN];  // sig | segment-start flag << 31 (computed)
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Issue the bulk copies for tile `t` into `T`; returns the staged range.
+__device__ __forceinline__ void stage_tile(const paste_columnar_desc& C, int64_t t, ColumnTile* T,
+                                           uint64_t* bar) {
+  const int64_t n = C.n_events;
+  const int64_t g0 = t * CTILE - CPRE;
+  const int64_t lo = g0 < 0 ? 0 : g0;
+  int64_t hi = g0 + CSPAN;
+  if (hi > n) hi = n;
+  int64_t cnt = hi - lo;
+  cnt &= ~(int64_t)3;  // 16-byte granularity; the tail (< 4 events) is loaded by threads
+  const int off = (int)(lo - g0);
+  if (cnt > 0) {
+    const uint32_t b4 = (uint32_t)cnt * 4, b8 = (uint32_t)cnt * 8;
+    mbar_expect_tx(bar, 3 * b4 + 2 * b8);
+    bulk_g2s(T->ts + off, C.t_start + lo, b8, bar);
+    bulk_g2s(T->te + off, C.t_end + lo, b8, bar);
+    bulk_g2s(T->sess + off, C.session + lo, b4, bar);
+    bulk_g2s(T->seq + off, C.seq + lo, b4, bar);
+    bulk_g2s(T->sig + off, C.sig + lo, b4, bar);
+  } else {
+    mbar_expect_tx(bar, 0);
+  }
+}
+
+__global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar_desc C,
+                                                            MineGeom g, uint32_t* __restrict__ hist,
+                                                            int32_t* __restrict__ tok_out) {
+  extern __shared__ __align__(16) uint8_t c_smem[];
+  ColumnTile* tiles = reinterpret_cast<ColumnTile*>(c_smem);
+  uint32_t* hkey = reinterpret_cast<uint32_t*>(tiles + CSTAGES);
+  uint32_t* hcnt = hkey + CHASH;
+  __shared__ uint64_t bars[CSTAGES];
+  for (int i = threadIdx.x; i < CHASH; i += CT) {
+    hkey[i] = HEMPTY;
+    hcnt[i] = 0;
+  }
+  const int64_t n = C.n_events;
+  const int64_t n_tiles = (n + CTILE - 1) / CTILE;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < CSTAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int64_t t = blockIdx.x;
+  if (threadIdx.x == 0 && t < n_tiles) stage_tile(C, t, &tiles[0], &bars[0]);
+  unsigned long long segs = 0, bad = 0;
+  for (int it = 0; t < n_tiles; ++it, t += gridDim.x) {
+    const int st = it & 1;
+    ColumnTile* T = &tiles[st];
+    // prefetch the next tile into the other stage (freed by the previous sync)
+    const int64_t tn = t + gridDim.x;
+    if (threadIdx.x == 0 && tn < n_tiles) stage_tile(C, tn, &tiles[st ^ 1], &bars[st ^ 1]);
+    mbar_wait(&bars[st], (it >> 1) & 1);
+    const int64_t g0 = t * CTILE - CPRE;
+    // tail events not covered by the 16-byte-granular bulk copy
+    {
+      const int64_t lo = g0 < 0 ? 0 : g0;
+      int64_t hi = g0 + CSPAN;
+      if (hi > n) hi = n;
+      const int64_t bulk_hi = lo + ((hi - lo) & ~(int64_t)3);
+      for (int64_t x = bulk_hi + threadIdx.x; x < hi; x += CT) {
+        const int l = (int)(x - g0);
+        T->ts[l] = C.t_start[x];
+        T->te[l] = C.t_end[x];
+        T->sess[l] = C.session[x];
+        T->seq[l] = C.seq[x];
+        T->sig[l] = C.sig[x];
+      }
+    }
+    __syncthreads();
+    // segment-start flags packed with the sig; order checks for the tile's own events
+    for (int l = 1 + threadIdx.x; l < CSPAN; l += CT) {
+      const int64_t x = g0 + l;
+      uint32_t b = 1;
+      if (x > 0 && x < n) {
+        const int32_t ss = T->sess[l], ps = T->sess[l - 1];
+        const double ts = T->ts[l];
+        b = (ss != ps) || (__dsub_rn(ts, T->te[l - 1]) > C.inactivity_ms);
+        if (l >= CPRE && l < CPRE + CTILE) {
+          const double pts = T->ts[l - 1];
+          if (ss < ps) ++bad;
+          else if (ss == ps && (ts < pts || (ts == pts && T->seq[l] <= T->seq[l - 1]))) ++bad;
+        }
+      }
+      T->v[l] = (uint32_t)T->sig[l] | (b << 31);
+    }
+    __syncthreads();
+    const uint32_t S = (uint32_t)g.S, base = (uint32_t)g.base;
+    for (int j = 0; j < CTILE / CT; ++j) {
+      const int li = CPRE + j * CT + threadIdx.x;
+      const int64_t x = g0 + li;
+      const bool valid = x < n;
+      const unsigned lanes = __ballot_sync(0xffffffffu, valid);
+      if (!valid) continue;
+      // the window words are independent loads (no dependent walk-back chain)
+      uint32_t w[8];
+#pragma unroll
+      for (int d = 0; d < 7; ++d) w[d] = d <= g.k ? T->v[li - d] : 0u;
+      const bool last = (x + 1 == n) || (T->v[li + 1] >> 31);
+      // gram ending at x: BEGIN once a segment start has been passed
+      uint32_t key = w[0] & 0x7fffffffu, mult = base, kend = S + 1, mul2 = base;
+      bool stop = w[0] >> 31, stop2 = false;
+#pragma unroll
+      for (int d = 1; d < 7; ++d) {
+        if (d <= g.k) {
+          key += (stop ? S : (w[d] & 0x7fffffffu)) * mult;
+          stop = stop || (w[d] >> 31);
+          mult *= base;
+          // END gram: positions x-(d-1)
+          kend += (stop2 ? S : (w[d - 1] & 0x7fffffffu)) * mul2;
+          stop2 = stop2 || (w[d - 1] >> 31);
+          mul2 *= base;
+        }
+      }
+      (void)lanes;
+      hh_add(hkey, hcnt, hist, key, 1u);
+      segs += last;
+      if (last) hh_add(hkey, hcnt, hist, kend, 1u);
+      if (tok_out) tok_out[x] = (int32_t)(w[0] & 0x7fffffffu) | ((w[0] >> 31) ? (int32_t)SEG_START : 0);
+    }
+    __syncthreads();  // stage `st` is free for the prefetch two iterations on
+  }
+  // flush the heavy-hitter table
+  __syncthreads();
+  for (int i = threadIdx.x; i < CHASH; i += CT)
+    if (hkey[i] != HEMPTY) atomicAdd(hist + hkey[i], hcnt[i]);
+  // block-reduce the counters
+  for (int o = 16; o > 0; o >>= 1) {
+    segs += __shfl_xor_sync(0xffffffffu, segs, o);
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (C.n_segments && segs) atomicAdd(reinterpret_cast<unsigned long long*>(C.n_segments), segs);
+    if (C.n_unsorted && bad) atomicAdd(reinterpret_cast<unsigned long long*>(C.n_unsorted), bad);
+  }
+}
+
+extern "C" int paste_mine_ingest_count(const paste_columnar_desc* c, const paste_mine_desc* d,
+                                       void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(c != nullptr && d != nullptr, "null descriptor");
+  MineGeom g;
+  if (make_geom(d->n_sigs, d->k, &g) != 0 || d->k + 1 > CPRE) {
+    set_error("mining geometry out of range (n_sigs=%d, k=%d)", d->n_sigs, d->k);
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  if (c->n_events == 0) return PASTE_OK;
+  const uintptr_t mis = (uintptr_t)c->session | (uintptr_t)c->seq | (uintptr_t)c->t_start |
+                        (uintptr_t)c->t_end | (uintptr_t)c->sig;
+  PASTE_REQUIRE((mis & 15) == 0, "columnar arrays must be 16-byte aligned");
+  const size_t smem = sizeof(ColumnTile) * CSTAGES + 2 * CHASH * sizeof(uint32_t);
+  static int grid_cap = 0;
+  if (grid_cap == 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(columnar_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, columnar_count_kernel, CT, smem);
+    grid_cap = sms * (occ > 0 ? occ : 1);
+  }
+  const int64_t tiles = (c->n_events + CTILE - 1) / CTILE;
+  const int64_t grid = tiles < grid_cap ? tiles : grid_cap;
+  columnar_count_kernel<<<(unsigned)grid, CT, smem, (cudaStream_t)stream>>>(*c, g, d->hist,
+                                                                            c->tokens_out);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}

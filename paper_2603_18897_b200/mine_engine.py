@@ -316,3 +316,80 @@ def frequent_subsequences(windows, sigma: int) -> dict:
             continue
         out[tuple(sigs.signature(c) for c in ctx)] = int(sup[cidx])
     return out
+
+
+# ---------------------------------------------------------------------------
+# columnar traces (K1 + K2 fused) and sharded mining (K3)
+# ---------------------------------------------------------------------------
+
+def ingest_count(tables: MineTables, trace: dict, inactivity_ms: float = 300_000.0,
+                 tokens_out=None):
+    """Fused ingest + count of a device-resident columnar trace into
+    ``tables.hist``; returns device counters (n_segments, n_unsorted)."""
+    from .device_ops import stream_handle
+    from ._native import ColumnarDesc
+
+    torch = _torch()
+    lib = _native.lib()
+    counters = torch.zeros(2, dtype=torch.int64, device="cuda")
+    n = int(trace["sig"].numel())
+    c = ColumnarDesc(n, ptr(trace["session"]), ptr(trace["seq"]), ptr(trace["t_start"]),
+                     ptr(trace["t_end"]), ptr(trace["sig"]), float(inactivity_ms), ptr(tokens_out),
+                     ptr(counters), ptr(counters) + 8)
+    d = tables.desc()
+    check(lib.paste_mine_ingest_count(ctypes.byref(c), ctypes.byref(d), stream_handle()), lib)
+    return counters
+
+
+def patterns_from_candidates(cands: np.ndarray, sigs: SigTable, S: int, cfg: MiningConfig):
+    """Mapping-free patterns (columnar traces carry no payloads): p = follow /
+    match, the tau gate, and the reference's output order."""
+    if len(cands) == 0:
+        return []
+    cands = np.asarray(cands, np.int64).reshape(-1, 5)
+    p = cands[:, 4] / cands[:, 3]  # IEEE division of exact ints == Python's int / int
+    cands, p = cands[p >= cfg.tau], p[p >= cfg.tau]
+    # decode context indices into (length, digits) without Python loops
+    off = np.array(ctx_offsets(S, cfg.k), np.int64)
+    cidx = cands[:, 1]
+    length = np.searchsorted(off[1:], cidx, side="right")
+    local = cidx - off[length]
+    digits = np.zeros((len(cands), cfg.k), np.int64)
+    for d in range(cfg.k):  # most significant first, left-aligned
+        shift = length - 1 - d
+        ok = shift >= 0
+        digits[ok, d] = (local[ok] // (S ** shift[ok])) % S
+    # the reference order (mining.py:105-111): -p, -len, target name, context;
+    # sig ids preserve (tool_type, status.value) order (sorted interning)
+    keys = [digits[:, d] for d in reversed(range(cfg.k))] + [cands[:, 0], -length, -p]
+    order = np.lexsort(keys)
+    sig_obj = [sigs.signature(x) for x in range(S)]
+    out = []
+    for i in order.tolist():
+        n = int(length[i])
+        ctx = tuple(sig_obj[x] for x in digits[i, :n].tolist())
+        out.append(PatternTuple(context=ctx, target=sigs.tools[int(cands[i, 0])], mapping=None,
+                                p=float(p[i]), support=int(cands[i, 2])))
+    return out
+
+
+def mine_columnar(trace: dict, sigs: SigTable, cfg: MiningConfig,
+                  inactivity_ms: float = 300_000.0, group=None) -> list[PatternTuple]:
+    """mine() over a columnar trace shard on this device.  With a
+    torch.distributed ``group`` every rank counts its shard (whole sessions)
+    and the (k+1)-gram histograms are summed with one NCCL all-reduce before
+    expansion -- windows and matches never cross a session, so the merged
+    histogram equals the single-device one."""
+    relation = 0 if cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE else 1
+    tables = MineTables.allocate(max(sigs.n_sigs, 2), cfg.k, relation)
+    counters = ingest_count(tables, trace, inactivity_ms)
+    if group is not None:
+        import torch.distributed as dist
+
+        dist.all_reduce(tables.hist, group=group)
+        dist.all_reduce(counters, group=group)
+    if int(counters[1].item()):
+        raise _native.PasteUnsupported(
+            "columnar trace is not grouped by session / sorted by (t_start, seq)")
+    tables.expand()
+    return patterns_from_candidates(tables.select(cfg.sigma, cfg.tau), sigs, tables.n_sigs, cfg)

@@ -225,3 +225,76 @@ def stress_pool(seed: int = 1001, n_patterns: int = 1000, n_tools: int = 20):
         pats.append(PatternTuple(context=ctx, target=target, mapping=None,
                                  p=round(rng.uniform(0.3, 1.0), 4), support=5))
     return PatternPool(config=MiningConfig(), patterns=tuple(pats))
+
+
+# ---------------------------------------------------------------------------
+# C4: columnar mining corpus
+# ---------------------------------------------------------------------------
+
+C4_TOOLS = tuple(f"tool{i:02d}" for i in range(16))
+# planted motifs at the paper's transition rates:
+# edit -> verify 0.55, grep -> editor 0.38, search -> fetch 0.51
+C4_PLANTED = ((0, 1, 0.55), (2, 0, 0.38), (3, 4, 0.51))
+
+
+def columnar_corpus(n_events: int, seed: int = 2603, mean_len: float = 8.0,
+                    fail_rate: float = 0.05, split_rate: float = 0.01, max_len: int = 64):
+    """Columnar trace of ``n_events`` tool events: session idx (first-appearance
+    order), seq, t_start / t_end (ms), sig over the 16 C4 tools (interned in
+    sorted order, so sig = 2 * tool + success).  Tools follow a first-order
+    chain with the planted motifs; ``split_rate`` of the think gaps exceed the
+    300 s inactivity threshold (ingest splits them into new segments)."""
+    rng = np.random.default_rng(seed)
+    lens = np.minimum(rng.geometric(1.0 / mean_len, int(n_events / mean_len * 1.2) + 16), max_len)
+    csum = np.cumsum(lens)
+    n_sess = int(np.searchsorted(csum, n_events)) + 1
+    lens = lens[:n_sess].copy()
+    lens[-1] -= int(csum[n_sess - 1] - n_events)
+    starts = np.zeros(n_sess, np.int64)
+    starts[1:] = np.cumsum(lens)[:-1]
+    session = np.repeat(np.arange(n_sess, dtype=np.int32), lens)
+    seq = (np.arange(n_events, dtype=np.int64) - np.repeat(starts, lens)).astype(np.int32)
+
+    # tool chain, vectorised across sessions (longest first so active = prefix)
+    order = np.argsort(-lens, kind="stable")
+    olens, ostarts = lens[order], starts[order]
+    tool = np.empty(n_events, np.int8)
+    nxt_planted = np.full(16, -1, np.int8)
+    p_planted = np.zeros(16)
+    for a, b, p in C4_PLANTED:
+        nxt_planted[a], p_planted[a] = b, p
+    prev = rng.integers(0, 16, n_sess, dtype=np.int8)
+    for pos in range(int(olens.max())):
+        m = int(np.searchsorted(-olens, -pos, side="left"))  # sessions longer than pos
+        if m == 0:
+            break
+        pv = prev[:m]
+        u = rng.random(m)
+        t = rng.integers(0, 16, m, dtype=np.int8)
+        planted = (nxt_planted[pv] >= 0) & (u < p_planted[pv])
+        t[planted] = nxt_planted[pv][planted]
+        tool[ostarts[:m] + pos] = t
+        prev[:m] = t
+    ok = rng.random(n_events) >= fail_rate
+    sig = (2 * tool.astype(np.int32) + ok).astype(np.int32)
+
+    dur = rng.exponential(800.0, n_events)
+    think = rng.exponential(2000.0, n_events)
+    think[rng.random(n_events) < split_rate] += 400_000.0
+    think[starts] = 0.0
+    step = think + dur
+    cum = np.cumsum(step)
+    cum -= np.repeat(cum[starts] - step[starts], lens)  # restart per session
+    t0 = np.repeat(rng.uniform(0, 1e9, n_sess), lens)
+    t_end = t0 + cum
+    t_start = t_end - dur
+    return {"session": session, "seq": seq, "t_start": t_start, "t_end": t_end, "sig": sig}
+
+
+def columnar_flags(c, inactivity_ms: float = 300_000.0) -> np.ndarray:
+    """Segment-start flags of a columnar corpus (host restatement of the gap
+    split, used by the CPU baseline and tests)."""
+    s, ts, te = c["session"], c["t_start"], c["t_end"]
+    b = np.ones(len(s), bool)
+    b[1:] = (s[1:] != s[:-1]) | ((ts[1:] - te[:-1]) > inactivity_ms)
+    return b

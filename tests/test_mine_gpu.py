@@ -109,3 +109,62 @@ def test_validate_matches_counts():
     for p in corpus["expected"][:5]:
         ctx = tuple(EventSignature(c["tool"], Status(c["status"])) for c in p["context"])
         assert validate(ctx, p["target"], None, sessions, cfg) == p["p"]
+
+
+def _host_tokens(c):
+    from paper_2603_18897_b200.synth import columnar_flags
+
+    tok = c["sig"].copy()
+    tok[columnar_flags(c)] |= np.int32(-2**31)
+    return tok
+
+
+def _dev(c):
+    return {k: torch.from_numpy(v).cuda() for k, v in c.items()}
+
+
+def test_columnar_ingest_count_matches_oracle():
+    from paper_2603_18897_b200.mine_engine import ingest_count
+    from paper_2603_18897_b200.synth import columnar_corpus
+
+    c = columnar_corpus(300_000, seed=11)
+    tok = _host_tokens(c)
+    for k, rel in ((3, 0), (3, 1), (2, 0)):
+        t = MineTables.allocate(32, k, rel)
+        out = torch.empty(len(tok), dtype=torch.int32, device="cuda")
+        counters = ingest_count(t, _dev(c), tokens_out=out)
+        assert np.array_equal(out.cpu().numpy(), tok)
+        assert int(counters[0]) == int((tok < 0).sum()) and int(counters[1]) == 0
+        t.expand()
+        ora = bridge.mine_counts(tok, 32, k, rel)
+        for dev, ref in zip((t.tool_count, t.support, t.match, t.follow), ora):
+            assert np.array_equal(dev.cpu().numpy().astype(np.uint64), ref)
+
+
+def test_mine_columnar_patterns_match_oracle_selection():
+    from paper_2603_18897_b200.mine_engine import mine_columnar, patterns_from_candidates
+    from paper_2603_18897_b200.packing import SigTable
+    from paper_2603_18897_b200.synth import C4_TOOLS, columnar_corpus
+
+    c = columnar_corpus(200_000, seed=12)
+    sigs = SigTable(C4_TOOLS)
+    cfg = MiningConfig(k=3, sigma=5, tau=0.3)
+    got = mine_columnar(_dev(c), sigs, cfg)
+    ora = bridge.mine_counts(_host_tokens(c), 32, 3, 0)
+    cands = np.array(bridge.select_candidates(*ora, 32, 3, cfg.sigma, cfg.tau), np.int64)
+    exp = patterns_from_candidates(cands.reshape(-1, 5), sigs, 32, cfg)
+    assert got == exp and len(got) > 0
+
+
+def test_columnar_rejects_unsorted_trace():
+    from paper_2603_18897_b200._native import PasteUnsupported
+    from paper_2603_18897_b200.mine_engine import mine_columnar
+    from paper_2603_18897_b200.packing import SigTable
+    from paper_2603_18897_b200.synth import C4_TOOLS, columnar_corpus
+
+    c = columnar_corpus(10_000, seed=13)
+    i = int(np.flatnonzero(c["session"][1:] == c["session"][:-1])[5])
+    for key in ("t_start", "t_end", "seq", "sig"):
+        c[key][[i, i + 1]] = c[key][[i + 1, i]]
+    with pytest.raises(PasteUnsupported):
+        mine_columnar(_dev(c), SigTable(C4_TOOLS), MiningConfig())

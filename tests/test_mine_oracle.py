@@ -66,3 +66,32 @@ def test_phase2_reproduces_reference_mappings():
             mapping = phase2.infer_mapping(occ, cfg.validation_fraction) if len(occ) >= 2 else None
             got = mapping_to_json(mapping) if mapping is not None else None
             assert got == p["mapping"], (p["context"], p["target"])
+
+
+def test_vectorised_pattern_order_equals_reference_sort_key():
+    import numpy as np
+
+    from paper_2603_18897_b200.mine_engine import (decode_context, encode_context,
+                                                   patterns_from_candidates)
+    from paper_2603_18897_b200.mining import PatternTuple
+
+    rng = np.random.default_rng(0)
+    S, k = 10, 3
+    sigs = SigTable([f"t{i}" for i in range(5)])
+    rows = set()
+    while len(rows) < 400:
+        n = int(rng.integers(1, k + 1))
+        ctx = tuple(int(x) for x in rng.integers(0, S, n))
+        match = int(rng.integers(1, 6))
+        rows.add((int(rng.integers(0, 5)), encode_context(ctx, S, k), int(rng.integers(5, 50)),
+                  match, int(rng.integers(0, match + 1))))
+    cands = np.array(sorted(rows), np.int64)
+    cfg = MiningConfig(k=k, sigma=1, tau=0.3)
+    got = patterns_from_candidates(cands, sigs, S, cfg)
+    exp = []
+    for t, c, sup, m, f in cands.tolist():
+        if f / m >= cfg.tau:
+            exp.append(PatternTuple(tuple(sigs.signature(x) for x in decode_context(c, S, k)),
+                                    sigs.tools[t], None, f / m, sup))
+    exp.sort(key=pattern_sort_key)
+    assert got == exp
