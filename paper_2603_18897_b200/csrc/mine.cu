@@ -319,7 +319,7 @@ extern "C" int paste_mine_select(const paste_mine_desc* d, int64_t sigma, double
 // events plus a (k+1)-event halo in shared memory with coalesced loads.
 // ---------------------------------------------------------------------------
 constexpr int CT = 256;                 // threads
-constexpr int CTILE = 1024;             // events per tile
+constexpr int CTILE = 512;              // events per tile
 constexpr int CPRE = 8;                 // halo before the tile (>= k + 1, 16-B aligned)
 constexpr int CSPAN = CTILE + 16;       // staged events per tile (halo + 1 after, padded)
 constexpr int CSTAGES = 2;
@@ -332,9 +332,10 @@ __device__ __forceinline__ void hh_add(uint32_t* hkey, uint32_t* hcnt, uint32_t*
                                        uint32_t inc) {
   const uint32_t h = (key * 2654435761u) >> (32 - 11);  // log2(CHASH) = 11
 #pragma unroll
-  for (int probe = 0; probe < 4; ++probe) {
+  for (int probe = 0; probe < 2; ++probe) {
     const uint32_t slot = (h + probe) & (CHASH - 1);
-    const uint32_t k0 = atomicCAS(hkey + slot, HEMPTY, key);
+    uint32_t k0 = *(volatile uint32_t*)(hkey + slot);  // read first: CAS only to claim
+    if (k0 == HEMPTY) k0 = atomicCAS(hkey + slot, HEMPTY, key);
     if (k0 == HEMPTY || k0 == key) {
       atomicAdd(hcnt + slot, inc);
       return;
@@ -406,6 +407,7 @@ __device__ __forceinline__ void stage_tile(const paste_columnar_desc& C, int64_t
   }
 }
 
+template <int K, bool WRITE_TOK>
 __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar_desc C,
                                                             MineGeom g, uint32_t* __restrict__ hist,
                                                             int32_t* __restrict__ tok_out) {
@@ -434,7 +436,7 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
     // prefetch the next tile into the other stage (freed by the previous sync)
     const int64_t tn = t + gridDim.x;
     if (threadIdx.x == 0 && tn < n_tiles) stage_tile(C, tn, &tiles[st ^ 1], &bars[st ^ 1]);
-    mbar_wait(&bars[st], (it >> 1) & 1);
+    if (threadIdx.x < 32) mbar_wait(&bars[st], (it >> 1) & 1);  // one warp spins
     const int64_t g0 = t * CTILE - CPRE;
     // tail events not covered by the 16-byte-granular bulk copy
     {
@@ -462,45 +464,40 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
         b = (ss != ps) || (__dsub_rn(ts, T->te[l - 1]) > C.inactivity_ms);
         if (l >= CPRE && l < CPRE + CTILE) {
           const double pts = T->ts[l - 1];
-          if (ss < ps) ++bad;
-          else if (ss == ps && (ts < pts || (ts == pts && T->seq[l] <= T->seq[l - 1]))) ++bad;
+          const bool back = (ts < pts) | ((ts == pts) & (T->seq[l] <= T->seq[l - 1]));
+          bad += (ss < ps) | ((ss == ps) & back);
         }
       }
       T->v[l] = (uint32_t)T->sig[l] | (b << 31);
     }
     __syncthreads();
     const uint32_t S = (uint32_t)g.S, base = (uint32_t)g.base;
+    const int valid_hi = (int)((n - g0) < (int64_t)CSPAN ? (n - g0) : (int64_t)CSPAN);  // slots < valid_hi hold events
     for (int j = 0; j < CTILE / CT; ++j) {
       const int li = CPRE + j * CT + threadIdx.x;
-      const int64_t x = g0 + li;
-      const bool valid = x < n;
-      const unsigned lanes = __ballot_sync(0xffffffffu, valid);
-      if (!valid) continue;
+      if (li >= valid_hi) continue;
       // the window words are independent loads (no dependent walk-back chain)
-      uint32_t w[8];
+      uint32_t w[K + 1];
 #pragma unroll
-      for (int d = 0; d < 7; ++d) w[d] = d <= g.k ? T->v[li - d] : 0u;
-      const bool last = (x + 1 == n) || (T->v[li + 1] >> 31);
+      for (int d = 0; d <= K; ++d) w[d] = T->v[li - d];
+      const bool last = (li + 1 == valid_hi) || (T->v[li + 1] >> 31);
       // gram ending at x: BEGIN once a segment start has been passed
       uint32_t key = w[0] & 0x7fffffffu, mult = base, kend = S + 1, mul2 = base;
       bool stop = w[0] >> 31, stop2 = false;
 #pragma unroll
-      for (int d = 1; d < 7; ++d) {
-        if (d <= g.k) {
-          key += (stop ? S : (w[d] & 0x7fffffffu)) * mult;
-          stop = stop || (w[d] >> 31);
-          mult *= base;
-          // END gram: positions x-(d-1)
-          kend += (stop2 ? S : (w[d - 1] & 0x7fffffffu)) * mul2;
-          stop2 = stop2 || (w[d - 1] >> 31);
-          mul2 *= base;
-        }
+      for (int d = 1; d <= K; ++d) {
+        key += (stop ? S : (w[d] & 0x7fffffffu)) * mult;
+        stop = stop || (w[d] >> 31);
+        mult *= base;
+        // END gram: positions x-(d-1)
+        kend += (stop2 ? S : (w[d - 1] & 0x7fffffffu)) * mul2;
+        stop2 = stop2 || (w[d - 1] >> 31);
+        mul2 *= base;
       }
-      (void)lanes;
       hh_add(hkey, hcnt, hist, key, 1u);
       segs += last;
       if (last) hh_add(hkey, hcnt, hist, kend, 1u);
-      if (tok_out) tok_out[x] = (int32_t)(w[0] & 0x7fffffffu) | ((w[0] >> 31) ? (int32_t)SEG_START : 0);
+      if (WRITE_TOK) tok_out[g0 + li] = (int32_t)(w[0] & 0x7fffffffu) | ((w[0] >> 31) ? (int32_t)SEG_START : 0);
     }
     __syncthreads();  // stage `st` is free for the prefetch two iterations on
   }
@@ -519,6 +516,24 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
   }
 }
 
+template <int K, bool WT>
+static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint32_t* hist,
+                           size_t smem, int64_t tiles, cudaStream_t stream) {
+  static int grid_cap = 0;
+  if (grid_cap == 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(columnar_count_kernel<K, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, columnar_count_kernel<K, WT>, CT, smem);
+    grid_cap = sms * (occ > 0 ? occ : 1);
+  }
+  const int64_t grid = tiles < grid_cap ? tiles : grid_cap;
+  columnar_count_kernel<K, WT><<<(unsigned)grid, CT, smem, stream>>>(c, g, hist, c.tokens_out);
+  return 0;
+}
+
 extern "C" int paste_mine_ingest_count(const paste_columnar_desc* c, const paste_mine_desc* d,
                                        void* stream) {
   reset_launches();
@@ -533,20 +548,21 @@ extern "C" int paste_mine_ingest_count(const paste_columnar_desc* c, const paste
                         (uintptr_t)c->t_end | (uintptr_t)c->sig;
   PASTE_REQUIRE((mis & 15) == 0, "columnar arrays must be 16-byte aligned");
   const size_t smem = sizeof(ColumnTile) * CSTAGES + 2 * CHASH * sizeof(uint32_t);
-  static int grid_cap = 0;
-  if (grid_cap == 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(columnar_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, columnar_count_kernel, CT, smem);
-    grid_cap = sms * (occ > 0 ? occ : 1);
-  }
   const int64_t tiles = (c->n_events + CTILE - 1) / CTILE;
-  const int64_t grid = tiles < grid_cap ? tiles : grid_cap;
-  columnar_count_kernel<<<(unsigned)grid, CT, smem, (cudaStream_t)stream>>>(*c, g, d->hist,
-                                                                            c->tokens_out);
+  const bool wt = c->tokens_out != nullptr;
+  int rc = -1;
+#define PASTE_COLUMNAR(KV)                                                                      \
+  if (d->k == KV) {                                                                             \
+    if (wt) rc = launch_columnar<KV, true>(*c, g, d->hist, smem, tiles, (cudaStream_t)stream);   \
+    else rc = launch_columnar<KV, false>(*c, g, d->hist, smem, tiles, (cudaStream_t)stream);     \
+  }
+  PASTE_COLUMNAR(1) PASTE_COLUMNAR(2) PASTE_COLUMNAR(3) PASTE_COLUMNAR(4) PASTE_COLUMNAR(5)
+  PASTE_COLUMNAR(6)
+#undef PASTE_COLUMNAR
+  if (rc != 0) {
+    set_error("k=%d outside the columnar kernel's range", d->k);
+    return PASTE_ERR_UNSUPPORTED;
+  }
   count_launch();
   PASTE_CUDA_CHECK(cudaGetLastError());
   return PASTE_OK;
