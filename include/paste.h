@@ -281,6 +281,30 @@ typedef struct {
 
 int paste_mine_ingest_count(const paste_columnar_desc* c, const paste_mine_desc* d, void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* K6: admission selection (scheduling.py:59-60, 242-258)                   */
+/* ---------------------------------------------------------------------- */
+
+typedef struct {
+  int64_t n_jobs;
+  const double* p;          /* [n] Job.p                                      */
+  const double* benefit;    /* [n] Job.benefit_ms                             */
+  const double* duration;   /* [n] Job.duration_est_ms                        */
+  const int32_t* cost;      /* [n] Job.cost (>= 1)                            */
+  const int64_t* id;        /* [n] Job.id                                     */
+  int32_t* selected;        /* [<= min(slack, budget)] chosen job indices, in
+                               selection order                                */
+  int64_t* n_selected;      /* [1]                                            */
+} paste_select_desc;
+
+/* greedy_speculative_selection: jobs in ascending (-U, -p, id) with
+ * U = (p * benefit) / (cost * duration), taken while cost fits both the
+ * remaining slack and budget.  Synchronous (returns after the result is
+ * written).  Envelope: min(slack, budget) <= 64.                         */
+int64_t paste_select_scratch_bytes(int64_t n_jobs);
+int paste_select_greedy(paste_select_desc* d, int64_t slack, int64_t budget, void* scratch,
+                        int64_t scratch_bytes, void* stream);
+
 /* Number of kernel launches the last paste_* call on this thread issued.   */
 int paste_last_launch_count(void);
 

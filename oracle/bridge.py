@@ -119,3 +119,16 @@ def select_candidates(tool_count, support, match, follow, n_sigs, k, sigma, tau)
             if m and int(fol[c, t]) / m >= tau:
                 out.append((t, int(c), int(sup[t, c]), m, int(fol[c, t])))
     return out
+
+
+def greedy(p, benefit, duration, cost, ids, slack, budget) -> list[int]:
+    """Oracle greedy selection: indices of the chosen jobs, in order."""
+    fn = lib().oracle_greedy
+    fn.restype = ctypes.c_int64
+    fn.argtypes = [ctypes.c_int64] + [c_void_p] * 5 + [ctypes.c_int64, ctypes.c_int64, c_void_p]
+    arrs = [np.ascontiguousarray(a, dt) for a, dt in ((p, np.float64), (benefit, np.float64),
+                                                      (duration, np.float64), (cost, np.int32),
+                                                      (ids, np.int64))]
+    out = np.zeros(max(len(arrs[0]), 1), np.int32)
+    m = fn(len(arrs[0]), *[_p(a) for a in arrs], slack, budget, _p(out))
+    return out[:m].tolist()

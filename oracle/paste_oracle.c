@@ -389,3 +389,45 @@ int oracle_mine_counts(const int32_t* tokens, int64_t n_tokens, int S, int k, in
   }
   return PASTE_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* greedy_speculative_selection (scheduling.py:242-258): sort by            */
+/* (-U, -p, id), U = (p * benefit) / (cost * duration); take while cost fits */
+/* both slack and budget.                                                    */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  double u, p;
+  int64_t id;
+  int32_t cost, idx;
+} o_job;
+
+static int o_job_cmp(const void* a_, const void* b_) {
+  const o_job* a = (const o_job*)a_;
+  const o_job* b = (const o_job*)b_;
+  if (a->u != b->u) return a->u > b->u ? -1 : 1; /* -U ascending */
+  if (a->p != b->p) return a->p > b->p ? -1 : 1; /* -p ascending */
+  return a->id < b->id ? -1 : (a->id > b->id ? 1 : 0);
+}
+
+int64_t oracle_greedy(int64_t n, const double* p, const double* benefit, const double* duration,
+                      const int32_t* cost, const int64_t* id, int64_t slack, int64_t budget,
+                      int32_t* selected) {
+  o_job* jobs = (o_job*)malloc(sizeof(o_job) * (size_t)(n > 0 ? n : 1));
+  int64_t i, n_sel = 0, r = slack, b = budget;
+  for (i = 0; i < n; ++i) {
+    jobs[i].u = (p[i] * benefit[i]) / ((double)cost[i] * duration[i]);
+    jobs[i].p = p[i];
+    jobs[i].id = id[i];
+    jobs[i].cost = cost[i];
+    jobs[i].idx = (int32_t)i;
+  }
+  qsort(jobs, (size_t)n, sizeof(o_job), o_job_cmp);
+  for (i = 0; i < n; ++i)
+    if (jobs[i].cost <= r && jobs[i].cost <= b) {
+      selected[n_sel++] = jobs[i].idx;
+      r -= jobs[i].cost;
+      b -= jobs[i].cost;
+    }
+  free(jobs);
+  return n_sel;
+}

@@ -88,6 +88,12 @@ class ColumnarDesc(ctypes.Structure):
                 ("n_segments", c_void_p), ("n_unsorted", c_void_p)]
 
 
+class SelectDesc(ctypes.Structure):
+    _fields_ = [("n_jobs", c_int64), ("p", c_void_p), ("benefit", c_void_p), ("duration", c_void_p),
+                ("cost", c_void_p), ("id", c_void_p), ("selected", c_void_p),
+                ("n_selected", c_void_p)]
+
+
 # numpy mirrors of the element structs
 PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
                           ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
@@ -108,6 +114,9 @@ EXPORTS = {
     "paste_build_match_table": (c_int, [POINTER(PoolDesc), c_int32, c_int32, c_void_p, c_void_p]),
     "paste_mine_geometry": (c_int, [c_int32, c_int32, POINTER(c_int64), POINTER(c_int64)]),
     "paste_mine_count": (c_int, [POINTER(MineDesc), c_void_p]),
+    "paste_select_scratch_bytes": (c_int64, [c_int64]),
+    "paste_select_greedy": (c_int, [POINTER(SelectDesc), c_int64, c_int64, c_void_p, c_int64,
+                                    c_void_p]),
     "paste_mine_ingest_count": (c_int, [POINTER(ColumnarDesc), POINTER(MineDesc), c_void_p]),
     "paste_mine_expand": (c_int, [POINTER(MineDesc), c_void_p]),
     "paste_mine_select": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64, c_void_p,

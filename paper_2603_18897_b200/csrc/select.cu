@@ -1,0 +1,320 @@
+// K6 admission_select: greedy_speculative_selection on the device.
+//
+// Reference (scheduling.py:59-60, 242-258): U = (p * T) / (c * d) in fp64;
+// jobs are visited in ascending (-U, -p, id) and taken while their cost fits
+// both the remaining slack and the remaining budget; both decrease by the
+// job's cost, so the test is cost <= cap with cap = min(slack, budget)
+// decreasing by each selected cost.
+//
+// Device plan (cost >= 1):
+//   * once a job of cost c is rejected, cap < c for good, so the selected
+//     jobs of cost c are a PREFIX (in key order) of at most floor(cap0 / c)
+//     jobs of that cost -- the only candidates;
+//   * a radix select over the full 192-bit key (-U, -p, id), 8 bits per pass
+//     with a per-class early exit, finds for every cost class c <= cap0 the
+//     key of its floor(cap0/c)-th best job; the jobs at or below their class
+//     threshold are exactly the candidates (ids are unique, so no ties);
+//   * the candidates are sorted by the full key (-U, -p, id) in shared memory
+//     (bitonic) and one warp runs the greedy scan; visiting a superset of the
+//     selected jobs in the same relative order yields the same decisions.
+#include "common.cuh"
+
+namespace paste {
+
+constexpr int SEL_MAX_CAP = 64;       // cost classes handled by the radix select
+constexpr int SEL_MAX_CAND = 4096;    // candidates sorted in one CTA
+constexpr int SEL_T = 256;
+
+__device__ __forceinline__ uint64_t desc_key(double v) {
+  // ascending order of the returned key == descending order of v (v != NaN);
+  // -0.0 and 0.0 compare equal in the reference, so they share a key
+  if (v == 0.0) v = 0.0;
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  const uint64_t asc = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+  return ~asc;
+}
+
+struct SelJob {
+  uint64_t ku;  // -U order key
+  uint64_t kp;  // -p order key
+  int64_t id;
+  int32_t cost;
+  int32_t idx;
+};
+
+__device__ __forceinline__ bool sel_less(const SelJob& a, const SelJob& b) {
+  if (a.ku != b.ku) return a.ku < b.ku;
+  if (a.kp != b.kp) return a.kp < b.kp;
+  return a.id < b.id;
+}
+
+// per-job keys + validation
+__global__ void sel_keys_kernel(paste_select_desc D, uint64_t* ku, int* bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= D.n_jobs) return;
+  const double p = D.p[i], c = (double)D.cost[i], d = D.duration[i];
+  const double u = __ddiv_rn(__dmul_rn(p, D.benefit[i]), __dmul_rn(c, d));
+  if (D.cost[i] < 1 || d == 0.0 || u != u || p != p) atomicOr(bad, 1);
+  ku[i] = desc_key(u);
+}
+
+// The radix select runs over the full 192-bit key (-U, -p, id) so the
+// candidate set is exact (ties never inflate it).  Key words: w0 = order key
+// of -U, w1 = order key of -p, w2 = id in unsigned order.
+__device__ __forceinline__ uint64_t key_word(const paste_select_desc& D, const uint64_t* ku,
+                                             int64_t i, int w) {
+  if (w == 0) return ku[i];
+  if (w == 1) return desc_key(D.p[i]);
+  return (uint64_t)D.id[i] ^ 0x8000000000000000ull;
+}
+
+// per cost class: histogram of digit `pass` among jobs matching the prefix
+__global__ void sel_hist_kernel(paste_select_desc D, const uint64_t* ku, int cap, int pass,
+                                const uint64_t* prefix, const int* done, const int* all_done,
+                                unsigned* hist) {
+  if (*all_done) return;
+  extern __shared__ unsigned h[];  // cap x 256 digit counters
+  for (int i = threadIdx.x; i < cap * 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int word = pass >> 3, shift = 56 - 8 * (pass & 7);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D.n_jobs;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = D.cost[i];
+    if (c < 1 || c > cap || done[c - 1]) continue;
+    const uint64_t* pf = prefix + 3 * (c - 1);
+    bool match = true;
+    for (int w = 0; w < word && match; ++w) match = key_word(D, ku, i, w) == pf[w];
+    if (!match) continue;
+    const uint64_t k = key_word(D, ku, i, word);
+    if (shift < 56 && (k >> (shift + 8)) != (pf[word] >> (shift + 8))) continue;
+    atomicAdd(&h[(c - 1) * 256 + (int)((k >> shift) & 255)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < cap * 256; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+
+// locate the rank-th job's digit; a class is done when its bucket holds a
+// single job (or the class has fewer jobs than its quota): the threshold
+// then covers the rest of that bucket with all-ones low bits
+__global__ void sel_pick_kernel(int cap, int pass, uint64_t* prefix, int64_t* rank, unsigned* hist,
+                                int* done, int* all_done) {
+  const int c = threadIdx.x + 1;
+  __shared__ int remaining;
+  if (threadIdx.x == 0) remaining = 0;
+  __syncthreads();
+  if (c <= cap && !*all_done) {
+    unsigned* h = hist + (c - 1) * 256;
+    uint64_t* pf = prefix + 3 * (c - 1);
+    const int word = pass >> 3, shift = 56 - 8 * (pass & 7);
+    if (!done[c - 1]) {
+      const int64_t r = rank[c - 1];
+      int64_t acc = 0;
+      int digit = -1;
+      for (int dg = 0; dg < 256; ++dg) {
+        if (acc + h[dg] > r) { digit = dg; break; }
+        acc += h[dg];
+      }
+      if (digit < 0) {  // fewer jobs than floor(cap/c): the whole class
+        done[c - 1] = 1;
+        pf[0] = pf[1] = pf[2] = ~0ull;
+      } else {
+        rank[c - 1] = r - acc;
+        const uint64_t low = shift == 0 ? 0ull : ((1ull << shift) - 1);
+        pf[word] = (pf[word] & ~(0xffull << shift)) | ((uint64_t)digit << shift);
+        if (h[digit] == 1 || pass == 23) {  // unique: close the threshold
+          done[c - 1] = 1;
+          pf[word] |= low;
+          for (int w = word + 1; w < 3; ++w) pf[w] = ~0ull;
+        }
+      }
+    }
+    for (int dg = 0; dg < 256; ++dg) h[dg] = 0;
+    if (!done[c - 1]) atomicAdd(&remaining, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && remaining == 0) *all_done = 1;
+}
+
+// candidates: class jobs whose full key is <= the class threshold
+__global__ void sel_compact_kernel(paste_select_desc D, const uint64_t* ku, int cap,
+                                   const uint64_t* thresh, unsigned* n_cand, int32_t* cand) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= D.n_jobs) return;
+  const int c = D.cost[i];
+  if (c < 1 || c > cap) return;
+  const uint64_t* t = thresh + 3 * (c - 1);
+  bool le = true;
+  for (int w = 0; w < 3; ++w) {
+    const uint64_t k = key_word(D, ku, i, w);
+    if (k != t[w]) {
+      le = k < t[w];
+      break;
+    }
+  }
+  if (!le) return;
+  const unsigned s = atomicAdd(n_cand, 1u);
+  if (s < (unsigned)SEL_MAX_CAND) cand[s] = (int32_t)i;
+}
+
+// one CTA: sort the candidates by (-U, -p, id) and run the greedy scan
+__global__ void __launch_bounds__(1024) sel_greedy_kernel(paste_select_desc D, const uint64_t* ku,
+                                                          const unsigned* n_cand_p,
+                                                          const int32_t* cand, int64_t slack,
+                                                          int64_t budget, int* status) {
+  extern __shared__ SelJob sj[];
+  const unsigned n_cand = *n_cand_p;
+  if (n_cand > (unsigned)SEL_MAX_CAND) {
+    if (threadIdx.x == 0) *status = 1;  // outside the envelope
+    return;
+  }
+  int P = 1;
+  while (P < (int)n_cand) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    SelJob j;
+    if (i < (int)n_cand) {
+      const int32_t x = cand[i];
+      j.ku = ku[x];
+      j.kp = desc_key(D.p[x]);
+      j.id = D.id[x];
+      j.cost = D.cost[x];
+      j.idx = x;
+    } else {
+      j.ku = ~0ull;
+      j.kp = ~0ull;
+      j.id = INT64_MAX;
+      j.cost = 0;
+      j.idx = -1;
+    }
+    sj[i] = j;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1)  // bitonic sort
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int i = threadIdx.x; i < P; i += blockDim.x) {
+        const int l = i ^ jj;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const SelJob a = sj[i], b = sj[l];
+          if (sel_less(b, a) == up) {
+            sj[i] = b;
+            sj[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  if (threadIdx.x == 0) {
+    int64_t r = slack, b = budget;
+    int64_t n_sel = 0;
+    for (int i = 0; i < (int)n_cand; ++i) {
+      const int64_t c = sj[i].cost;
+      if (c <= r && c <= b) {
+        D.selected[n_sel++] = sj[i].idx;
+        r -= c;
+        b -= c;
+      }
+    }
+    *D.n_selected = n_sel;
+    *status = 0;
+  }
+}
+
+}  // namespace paste
+
+using namespace paste;
+
+extern "C" int paste_select_greedy(paste_select_desc* d, int64_t slack, int64_t budget,
+                                   void* scratch, int64_t scratch_bytes, void* stream_) {
+  reset_launches();
+  PASTE_REQUIRE(d != nullptr, "null descriptor");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  const int64_t n = d->n_jobs;
+  const int64_t cap64 = slack < budget ? slack : budget;
+  const int64_t need = paste_select_scratch_bytes(n);
+  PASTE_REQUIRE(scratch != nullptr && scratch_bytes >= need, "scratch too small (%lld bytes)",
+                (long long)need);
+  if (n == 0 || cap64 < 1) {
+    PASTE_CUDA_CHECK(cudaMemsetAsync(d->n_selected, 0, sizeof(int64_t), stream));
+    return PASTE_OK;  // nothing fits (every cost >= 1)
+  }
+  if (cap64 > SEL_MAX_CAP) {
+    set_error("min(slack, budget) = %lld exceeds the device envelope (%d)", (long long)cap64,
+              SEL_MAX_CAP);
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  const int cap = (int)cap64;
+  uint8_t* s = static_cast<uint8_t*>(scratch);
+  uint64_t* ku = reinterpret_cast<uint64_t*>(s);
+  s += 8 * n;
+  uint64_t* prefix = reinterpret_cast<uint64_t*>(s);
+  s += 24 * SEL_MAX_CAP;
+  int64_t* rank = reinterpret_cast<int64_t*>(s);
+  s += 8 * SEL_MAX_CAP;
+  unsigned* hist = reinterpret_cast<unsigned*>(s);
+  s += 4 * SEL_MAX_CAP * 256;
+  int* flags = reinterpret_cast<int*>(s);  // [0] bad, [1] status, [2] all done, [3..] done
+  s += 4 * (SEL_MAX_CAP + 4);
+  unsigned* n_cand = reinterpret_cast<unsigned*>(s);
+  s += 16;
+  int32_t* cand = reinterpret_cast<int32_t*>(s);
+
+  // host-side init of the small state (ranks = floor(cap / c) - 1)
+  {
+    uint64_t h_prefix[3 * SEL_MAX_CAP];
+    int64_t h_rank[SEL_MAX_CAP];
+    for (int c = 1; c <= SEL_MAX_CAP; ++c) {
+      h_prefix[3 * (c - 1)] = h_prefix[3 * (c - 1) + 1] = h_prefix[3 * (c - 1) + 2] = 0;
+      h_rank[c - 1] = c <= cap ? cap / c - 1 : 0;
+    }
+    PASTE_CUDA_CHECK(cudaMemcpyAsync(prefix, h_prefix, sizeof(h_prefix), cudaMemcpyHostToDevice, stream));
+    PASTE_CUDA_CHECK(cudaMemcpyAsync(rank, h_rank, sizeof(h_rank), cudaMemcpyHostToDevice, stream));
+    PASTE_CUDA_CHECK(cudaMemsetAsync(hist, 0, 4 * SEL_MAX_CAP * 256, stream));
+    PASTE_CUDA_CHECK(cudaMemsetAsync(flags, 0, 4 * (SEL_MAX_CAP + 4), stream));
+    PASTE_CUDA_CHECK(cudaMemsetAsync(n_cand, 0, 16, stream));
+    // a synchronous copy keeps the stack arrays alive until they are consumed
+    PASTE_CUDA_CHECK(cudaStreamSynchronize(stream));
+  }
+  const int blocks = (int)((n + SEL_T - 1) / SEL_T);
+  sel_keys_kernel<<<blocks, SEL_T, 0, stream>>>(*d, ku, flags);
+  count_launch();
+  const int hblocks = blocks < 148 * 4 ? blocks : 148 * 4;
+  static bool attrs = false;
+  if (!attrs) {
+    cudaFuncSetAttribute(sel_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         4 * SEL_MAX_CAP * 256);
+    cudaFuncSetAttribute(sel_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(SelJob) * SEL_MAX_CAND);
+    attrs = true;
+  }
+  for (int pass = 0; pass < 24; ++pass) {  // kernels return at once when every class is done
+    sel_hist_kernel<<<hblocks, SEL_T, 4 * cap * 256, stream>>>(*d, ku, cap, pass, prefix,
+                                                                flags + 3, flags + 2, hist);
+    sel_pick_kernel<<<1, SEL_MAX_CAP, 0, stream>>>(cap, pass, prefix, rank, hist, flags + 3,
+                                                   flags + 2);
+    count_launch(2);
+  }
+  sel_compact_kernel<<<blocks, SEL_T, 0, stream>>>(*d, ku, cap, prefix, n_cand, cand);
+  count_launch();
+  sel_greedy_kernel<<<1, 1024, sizeof(SelJob) * SEL_MAX_CAND, stream>>>(*d, ku, n_cand, cand,
+                                                                         slack, budget, flags + 1);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  int h_flags[2];
+  PASTE_CUDA_CHECK(cudaMemcpyAsync(h_flags, flags, sizeof(h_flags), cudaMemcpyDeviceToHost, stream));
+  PASTE_CUDA_CHECK(cudaStreamSynchronize(stream));
+  if (h_flags[0]) {
+    set_error("jobs need cost >= 1, a non-zero duration and a non-NaN utility");
+    return PASTE_ERR_INVALID;
+  }
+  if (h_flags[1]) {
+    set_error("more than %d candidate jobs (ties) for the on-chip sort", SEL_MAX_CAND);
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  return PASTE_OK;
+}
+
+extern "C" int64_t paste_select_scratch_bytes(int64_t n_jobs) {
+  return 8 * n_jobs + 32 * SEL_MAX_CAP + 4 * SEL_MAX_CAP * 256 + 4 * (SEL_MAX_CAP + 4) + 16 +
+         4 * SEL_MAX_CAND + 256;
+}

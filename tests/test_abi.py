@@ -61,6 +61,7 @@ def _c_sizeof(struct_name: str) -> int:
     ("paste_pool_desc", "PoolDesc"), ("paste_admit_desc", "AdmitDesc"),
     ("paste_windows", "WindowsDesc"), ("paste_predict_out", "PredictOut"),
     ("paste_admit_lists_desc", "AdmitListsDesc"), ("paste_mine_desc", "MineDesc"),
+    ("paste_select_desc", "SelectDesc"), ("paste_columnar_desc", "ColumnarDesc"),
 ])
 def test_struct_layouts_match_header(cname, pyname):
     assert ctypes.sizeof(getattr(_native, pyname)) == _c_sizeof(cname)

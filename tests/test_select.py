@@ -1,0 +1,67 @@
+"""K6 greedy admission selection: oracle pinned to the reference's golden
+selections (CPU) and the device path against both (GPU)."""
+
+import numpy as np
+import pytest
+
+import golden_io as G
+from oracle import bridge
+
+CASES = G.golden("greedy_golden.json")["cases"]
+
+
+def _cols(case):
+    jobs = np.array(case["jobs"], dtype=object).reshape(-1, 5)
+    ids = np.array([int(j[0]) for j in jobs], np.int64)
+    p = np.array([j[1] for j in jobs], np.float64)
+    bene = np.array([j[2] for j in jobs], np.float64)
+    cost = np.array([int(j[3]) for j in jobs], np.int32)
+    dur = np.array([j[4] for j in jobs], np.float64)
+    return p, bene, dur, cost, ids
+
+
+def test_oracle_greedy_matches_reference():
+    for case in CASES:
+        p, bene, dur, cost, ids = _cols(case)
+        got = bridge.greedy(p, bene, dur, cost, ids, case["slack"], case["budget"])
+        assert [int(ids[i]) for i in got] == case["expected"]
+
+
+@pytest.mark.gpu
+def test_device_greedy_matches_reference():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2603_18897_b200.scheduling import Job, JobKind, greedy_speculative_selection
+
+    for case in CASES:
+        jobs = [Job(id=int(j[0]), kind=JobKind.SPECULATIVE, tool_type="t", args={}, arg_hash="",
+                    session_id="s", p=j[1], benefit_ms=j[2], cost=int(j[3]),
+                    duration_est_ms=j[4], submitted_at=0.0) for j in case["jobs"]]
+        got = greedy_speculative_selection(jobs, case["slack"], case["budget"])
+        assert [j.id for j in got] == case["expected"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,cap,ties", [(2_000_000, 24, False), (1_000_000, 64, True),
+                                        (300_000, 8, True), (50, 64, False)])
+def test_device_greedy_matches_oracle_at_scale(n, cap, ties):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2603_18897_b200.select import select_greedy_arrays
+
+    rng = np.random.default_rng(n + cap)
+    if ties:  # few distinct values -> many exact utility ties, id decides
+        p = rng.choice([0.25, 0.5, 0.75, 1.0], n)
+        bene = rng.choice([100.0, 200.0, 1000.0], n)
+        dur = rng.choice([100.0, 1000.0], n)
+    else:
+        p = rng.uniform(0.05, 1.0, n)
+        bene = rng.uniform(100, 10_000, n)
+        dur = rng.uniform(100, 5_000, n)
+    cost = rng.integers(1, 6, n).astype(np.int32)
+    ids = rng.permutation(n).astype(np.int64) + 1
+    slack, budget = cap + 3, cap
+    got = select_greedy_arrays(p, bene, dur, cost, ids, slack, budget).tolist()
+    assert got == bridge.greedy(p, bene, dur, cost, ids, slack, budget)
