@@ -305,6 +305,55 @@ int64_t paste_select_scratch_bytes(int64_t n_jobs);
 int paste_select_greedy(paste_select_desc* d, int64_t slack, int64_t budget, void* scratch,
                         int64_t scratch_bytes, void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* K5: leaf scan and expression resolution over payload tapes               */
+/* ---------------------------------------------------------------------- */
+
+/* candidate_paths (mappings.py:237-266) for many (payload, target) pairs:
+ * the first node_budget nodes of each payload (pre-order = tape order) are
+ * compared with the target scalar (values_equal, events.py:125-130); the
+ * matching node indices are written in order (at most out_off[q+1] -
+ * out_off[q] of them; n_out[q] is the full count).  target_type is the
+ * tape type of the target scalar, -1 for a container (never equal);
+ * target bytes are its canonical bytes (NFC for strings).                  */
+typedef struct {
+  int64_t n_queries;
+  int64_t node_budget;
+  const paste_tape_node* nodes;
+  const uint8_t* bytes;
+  const paste_event_ref* refs;
+  const int32_t* event;        /* [n] payload (event) index                   */
+  const int32_t* target_type;  /* [n]                                         */
+  const uint8_t* target_nan;   /* [n]                                         */
+  const int64_t* target_off;   /* [n+1] into target_bytes                     */
+  const uint8_t* target_bytes;
+  const int64_t* out_off;      /* [n+1] into out_nodes                        */
+  int32_t* out_nodes;
+  int64_t* n_out;              /* [n]                                         */
+  uint8_t* truncated;          /* [n]                                         */
+} paste_leaf_scan_desc;
+
+int paste_leaf_scan(const paste_leaf_scan_desc* d, void* stream);
+
+/* evaluate()'s resolution (mappings.py:143-194) of one binding per query
+ * against an explicit source event; for IndexedFallback the history tokens
+ * after src_pos are scanned for FAIL events of fail_tool (-1 tokens mark the
+ * source event itself and are skipped).  result[q] = node index or -1.     */
+typedef struct {
+  int64_t n_queries;
+  const paste_binding* bindings; /* [n]                                       */
+  const int32_t* steps;
+  const paste_tape_node* nodes;
+  const paste_event_ref* refs;
+  const int32_t* src_event;      /* [n]                                       */
+  const int32_t* hist_off;       /* [n+1]                                     */
+  const int32_t* hist_tok;       /* sig per history event, -1 = source        */
+  const int32_t* src_pos;        /* [n] source position in its history, -1    */
+  int64_t* result;               /* [n]                                       */
+} paste_resolve_desc;
+
+int paste_resolve(const paste_resolve_desc* d, void* stream);
+
 /* Number of kernel launches the last paste_* call on this thread issued.   */
 int paste_last_launch_count(void);
 

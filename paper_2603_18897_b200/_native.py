@@ -94,6 +94,21 @@ class SelectDesc(ctypes.Structure):
                 ("n_selected", c_void_p)]
 
 
+class LeafScanDesc(ctypes.Structure):
+    _fields_ = [("n_queries", c_int64), ("node_budget", c_int64), ("nodes", c_void_p),
+                ("bytes", c_void_p), ("refs", c_void_p), ("event", c_void_p),
+                ("target_type", c_void_p), ("target_nan", c_void_p), ("target_off", c_void_p),
+                ("target_bytes", c_void_p), ("out_off", c_void_p), ("out_nodes", c_void_p),
+                ("n_out", c_void_p), ("truncated", c_void_p)]
+
+
+class ResolveDesc(ctypes.Structure):
+    _fields_ = [("n_queries", c_int64), ("bindings", c_void_p), ("steps", c_void_p),
+                ("nodes", c_void_p), ("refs", c_void_p), ("src_event", c_void_p),
+                ("hist_off", c_void_p), ("hist_tok", c_void_p), ("src_pos", c_void_p),
+                ("result", c_void_p)]
+
+
 # numpy mirrors of the element structs
 PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
                           ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
@@ -114,6 +129,8 @@ EXPORTS = {
     "paste_build_match_table": (c_int, [POINTER(PoolDesc), c_int32, c_int32, c_void_p, c_void_p]),
     "paste_mine_geometry": (c_int, [c_int32, c_int32, POINTER(c_int64), POINTER(c_int64)]),
     "paste_mine_count": (c_int, [POINTER(MineDesc), c_void_p]),
+    "paste_leaf_scan": (c_int, [POINTER(LeafScanDesc), c_void_p]),
+    "paste_resolve": (c_int, [POINTER(ResolveDesc), c_void_p]),
     "paste_select_scratch_bytes": (c_int64, [c_int64]),
     "paste_select_greedy": (c_int, [POINTER(SelectDesc), c_int64, c_int64, c_void_p, c_int64,
                                     c_void_p]),

@@ -1,0 +1,134 @@
+// K5 leaf_scan and the resolve kernel over payload tapes.
+//
+// leaf_scan -- candidate_paths (mappings.py:237-266): the pre-order DFS that
+// visits at most node_budget nodes and collects the scalar leaves equal to a
+// target (values_equal, events.py:125-130).  On the tape the DFS order IS the
+// node order, so a warp sweeps the first min(n_nodes, budget) nodes of one
+// payload, 32 at a time, and compacts the matches in order with a ballot;
+// truncated = n_nodes > budget.  Equality on canonical scalar bytes: same
+// type class (str / int / float / bool value / null), same canonical bytes
+// (NFC for strings), never NaN.
+//
+// resolve -- evaluate()'s expression resolution (mappings.py:143-194) for
+// explicit (binding, source event, history) queries: the fallback index
+// counts FAIL events of fail_tool after the source in its history.
+#include "common.cuh"
+
+namespace paste {
+
+__device__ __forceinline__ int type_class(int t) {
+  // TRUE and FALSE are distinct values of one class; compare them by type id
+  return t;
+}
+
+__device__ __forceinline__ const uint8_t* canon_bytes(const uint8_t* bytes, int64_t byte_base,
+                                                      const Node& nd, uint32_t* len) {
+  const uint8_t* p = bytes + byte_base + nd.a;
+  if (nd.type() == PASTE_T_STR && (nd.flags() & PASTE_F_NFC)) {
+    const uint8_t* q = p + nd.b;  // [raw][u32 nfc_len][nfc]
+    *len = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) | ((uint32_t)q[3] << 24);
+    return q + 4;
+  }
+  *len = nd.b;
+  return p;
+}
+
+__global__ void leaf_scan_kernel(const paste_leaf_scan_desc D) {
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (q >= D.n_queries) return;
+  const paste_event_ref ref = D.refs[D.event[q]];
+  const Node root = load_node(D.nodes, ref.node_base);
+  const int64_t n_nodes = root.size();
+  const int64_t limit = n_nodes < D.node_budget ? n_nodes : D.node_budget;
+  // target scalar
+  const int tt = D.target_type[q];
+  const uint8_t* tb = D.target_bytes + D.target_off[q];
+  const uint32_t tl = (uint32_t)(D.target_off[q + 1] - D.target_off[q]);
+  const bool tnan = D.target_nan[q] != 0;
+  int64_t n_out = 0;
+  const int64_t out0 = D.out_off[q], cap = D.out_off[q + 1] - out0;
+  for (int64_t base = 0; base < limit; base += 32) {
+    const int64_t i = base + lane;
+    bool eq = false;
+    if (i < limit && !tnan && tt >= 0) {
+      const Node nd = load_node(D.nodes, ref.node_base + i);
+      const int t = nd.type();
+      if (t < PASTE_T_LIST && type_class(t) == tt && !(nd.flags() & PASTE_F_NAN)) {
+        if (t == PASTE_T_NULL || t == PASTE_T_TRUE || t == PASTE_T_FALSE) {
+          eq = true;
+        } else {
+          uint32_t len;
+          const uint8_t* b = canon_bytes(D.bytes, ref.byte_base, nd, &len);
+          eq = len == tl;
+          for (uint32_t k = 0; eq && k < len; ++k) eq = b[k] == tb[k];
+        }
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, eq);
+    if (eq) {
+      const int64_t slot = n_out + __popc(m & ((1u << lane) - 1));
+      if (slot < cap) D.out_nodes[out0 + slot] = (int32_t)i;
+    }
+    n_out += __popc(m);
+  }
+  if (lane == 0) {
+    D.n_out[q] = n_out;
+    D.truncated[q] = n_nodes > D.node_budget;
+  }
+}
+
+__global__ void resolve_kernel(const paste_resolve_desc D) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= D.n_queries) return;
+  const paste_binding bd = D.bindings[q];
+  const int64_t nb = D.refs[D.src_event[q]].node_base;
+  const int32_t* steps = D.steps;
+  int64_t cur = 0;
+  for (int s = 0; s < bd.step_cnt && cur >= 0; ++s)
+    cur = step_child(D.nodes, nb, cur, steps[2 * (bd.step_off + s)], steps[2 * (bd.step_off + s) + 1]);
+  if (bd.kind == PASTE_X_FALLBACK) {
+    int fails = 0;
+    const int32_t sp = D.src_pos[q];
+    if (sp >= 0)
+      for (int32_t h = D.hist_off[q] + sp + 1; h < D.hist_off[q + 1]; ++h) {
+        const int32_t t = D.hist_tok[h];  // -1: the source event itself (skipped)
+        fails += t >= 0 && (t >> 1) == bd.fail_tool && (t & 1) == 0;
+      }
+    if (cur >= 0) cur = bd.start_index < 0 ? -1 : step_child(D.nodes, nb, cur, 1, bd.start_index + fails);
+    for (int s = 0; s < bd.suf_cnt && cur >= 0; ++s)
+      cur = step_child(D.nodes, nb, cur, steps[2 * (bd.suf_off + s)], steps[2 * (bd.suf_off + s) + 1]);
+  } else if (bd.kind == PASTE_X_FORMAT && cur >= 0) {
+    const int t = load_node(D.nodes, nb + cur).type();
+    if (t != PASTE_T_STR && t != PASTE_T_INT && t != PASTE_T_FLOAT) cur = -1;
+  }
+  D.result[q] = cur;
+}
+
+}  // namespace paste
+
+using namespace paste;
+
+extern "C" int paste_leaf_scan(const paste_leaf_scan_desc* d, void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(d != nullptr, "null descriptor");
+  if (d->n_queries == 0) return PASTE_OK;
+  const int warps = 8;
+  const int64_t blocks = (d->n_queries + warps - 1) / warps;
+  leaf_scan_kernel<<<(unsigned)blocks, warps * 32, 0, (cudaStream_t)stream>>>(*d);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
+
+extern "C" int paste_resolve(const paste_resolve_desc* d, void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(d != nullptr, "null descriptor");
+  if (d->n_queries == 0) return PASTE_OK;
+  const int threads = 128;
+  resolve_kernel<<<(unsigned)((d->n_queries + threads - 1) / threads), threads, 0,
+                   (cudaStream_t)stream>>>(*d);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}

@@ -31,6 +31,8 @@ def to_dev(arr: np.ndarray):
     """numpy (incl. structured) -> contiguous CUDA tensor with the same bytes."""
     torch = _torch()
     a = np.ascontiguousarray(arr)
+    if not a.flags.writeable:
+        a = a.copy()
     if a.dtype.names is not None or a.dtype == np.uint8:
         t = torch.from_numpy(a.view(np.uint8).reshape(-1))
     else:
@@ -207,3 +209,202 @@ def admit_lists(lists: Sequence[Sequence], policy, benefit_of: Callable[[Any], f
                                       expected_utility=float(act_util[b0 + j]))
                     for j in range(int(n_act[li]))])
     return out
+
+
+# ---------------------------------------------------------------------------
+# K5: candidate_paths (leaf scan) and evaluate (resolve)
+# ---------------------------------------------------------------------------
+
+
+def _target_scalar(value):
+    """(tape type or -1, is_nan, canonical bytes) of a candidate_paths target."""
+    import unicodedata
+
+    from .tape import T_STR, scalar_bytes
+
+    try:
+        typ, flags, data = scalar_bytes(value)
+    except TypeError:
+        return -1, 0, b""  # containers / non-JSON objects never equal a scalar leaf
+    if typ == T_STR:
+        data = unicodedata.normalize("NFC", value).encode("utf-8", "surrogatepass")
+    return typ, 1 if (flags & 4) else 0, data
+
+
+def candidate_paths_batch(payloads: Sequence[Any], targets: Sequence[Any], node_budget: int):
+    from ._native import LeafScanDesc
+    from .mappings import PathSearch
+    from .tape import TapeArena
+
+    torch = _torch()
+    lib = _native.lib()
+    arena = TapeArena(keep_objects=False)
+    events = np.array([arena.add(p) for p in payloads] or [0], np.int32)
+    nodes, data, refs = arena.arrays()
+    n = len(payloads)
+    sizes = []
+    for e in range(n):
+        root = nodes[int(refs[e, 0])]
+        sizes.append(int(root["b"]) if root["type"] >= 6 else 1)
+    cap = np.minimum(np.array(sizes or [0], np.int64), max(node_budget, 0))
+    out_off = np.zeros(n + 1, np.int64)
+    out_off[1:] = np.cumsum(cap[:n])
+    tt, tn, tb = zip(*[_target_scalar(t) for t in targets]) if n else ((), (), ())
+    target_off = np.zeros(n + 1, np.int64)
+    target_off[1:] = np.cumsum([len(b) for b in tb])
+    tbytes = np.frombuffer(b"".join(tb) + b"\0", np.uint8)
+    d = {k: to_dev(v) for k, v in dict(
+        nodes=nodes, data=data, refs=refs, events=events,
+        tt=np.array(list(tt) or [0], np.int32), tn=np.array(list(tn) or [0], np.uint8),
+        toff=target_off, tbytes=tbytes, out_off=out_off).items()}
+    dev = torch.device("cuda")
+    out_nodes = torch.zeros(max(int(out_off[-1]), 1), dtype=torch.int32, device=dev)
+    n_out = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
+    trunc = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)
+    desc = LeafScanDesc(n, int(node_budget), ptr(d["nodes"]), ptr(d["data"]), ptr(d["refs"]),
+                        ptr(d["events"]), ptr(d["tt"]), ptr(d["tn"]), ptr(d["toff"]),
+                        ptr(d["tbytes"]), ptr(d["out_off"]), ptr(out_nodes), ptr(n_out), ptr(trunc))
+    check(lib.paste_leaf_scan(ctypes.byref(desc), stream_handle()), lib)
+    out_nodes, n_out, trunc = out_nodes.cpu().numpy(), n_out.cpu().numpy(), trunc.cpu().numpy()
+    res = []
+    for q in range(n):
+        found = out_nodes[out_off[q]:out_off[q] + min(int(n_out[q]), int(cap[q]))]
+        res.append(PathSearch(paths=tuple(arena.path_of(q, int(x)) for x in found),
+                              truncated=bool(trunc[q])))
+    return res
+
+
+def evaluate_mapping(mapping, ctx):
+    """evaluate() (mappings.py:207-223) with the resolution on the device."""
+    from ._native import BINDING_DTYPE, ResolveDesc
+    from .mappings import FormatTemplate, MappingResult, MappingStructureError, expr_ctx_pos
+    from .packing import encode_binding
+    from .tape import TapeArena, leaf_str_of
+
+    torch = _torch()
+    lib = _native.lib()
+    for b in mapping.bindings:  # structural errors raise before any work
+        pos = expr_ctx_pos(b.expr)
+        if not 0 <= pos < len(ctx.events):
+            raise MappingStructureError(f"ctx_pos {pos} out of range")
+    if not mapping.bindings:
+        return MappingResult(args={}, unbound=())
+    sigs, keys = SigTable(), KeyTable()
+    arena = TapeArena(keys)
+    slot_of: dict[int, int] = {}
+    steps: list[int] = []
+    rows, src_event, src_pos, hist_tok, hist_off = [], [], [], [], [0]
+    for b in mapping.bindings:
+        rows.append(encode_binding(b.expr, sigs, keys, steps))
+        src = ctx.events[expr_ctx_pos(b.expr)]
+        if id(src) not in slot_of:
+            slot_of[id(src)] = arena.add(src.result)
+        src_event.append(slot_of[id(src)])
+        first = next((j for j, ev in enumerate(ctx.history) if ev is src), -1)
+        src_pos.append(first)
+        for j, ev in enumerate(ctx.history):
+            hist_tok.append(-1 if (ev is src or ev.kind.value != "tool_call")
+                            else sigs.sig(ev.tool_type, ev.status))
+        hist_off.append(len(hist_tok))
+    nodes, data, refs = arena.arrays()
+    d = {k: to_dev(v) for k, v in dict(
+        bindings=np.array(rows, dtype=BINDING_DTYPE), steps=np.array(steps or [0, 0], np.int32),
+        nodes=nodes, refs=refs, src_event=np.array(src_event, np.int32),
+        hist_off=np.array(hist_off, np.int32), hist_tok=np.array(hist_tok or [0], np.int32),
+        src_pos=np.array(src_pos, np.int32)).items()}
+    result = torch.zeros(len(rows), dtype=torch.int64, device="cuda")
+    desc = ResolveDesc(len(rows), ptr(d["bindings"]), ptr(d["steps"]), ptr(d["nodes"]),
+                       ptr(d["refs"]), ptr(d["src_event"]), ptr(d["hist_off"]), ptr(d["hist_tok"]),
+                       ptr(d["src_pos"]), ptr(result))
+    check(lib.paste_resolve(ctypes.byref(desc), stream_handle()), lib)
+    res = result.cpu().numpy()
+    args, unbound = {}, []
+    for b, ev, node in zip(mapping.bindings, src_event, res.tolist()):
+        if node < 0:
+            unbound.append(b.arg_name)
+            continue
+        value = arena.node_object(ev, node)
+        if isinstance(b.expr, FormatTemplate):
+            value = b.expr.prefix + b.expr.normalization.apply(leaf_str_of(value)) + b.expr.suffix
+        args[b.arg_name] = value
+    return MappingResult(args=args, unbound=tuple(unbound))
+
+
+# ---------------------------------------------------------------------------
+# score_accuracy replay (prediction.py:133-169)
+# ---------------------------------------------------------------------------
+
+
+def score_replay(traces, pool, window_capacity: int, max_candidates):
+    from .events import EventKind, canonical_arg_hash
+    from .packing import C_FULL, WindowBatch
+    from .prediction import AccuracyReport
+    from .tape import TapeArena
+
+    if window_capacity < 1:
+        raise ValueError("window capacity must be >= 1")
+    dp = DevicePool(pool)
+    arena = TapeArena(dp.keys)
+    ev_tok, ev_evt, calls, call_len, actual = [], [], [], [], []
+    g = 0
+    for session in traces:
+        start = g
+        seen_tool = False
+        for ev in session.events:
+            if ev.kind is EventKind.TOOL_CALL:
+                if seen_tool:
+                    calls.append(g)
+                    call_len.append(min(window_capacity, g - start))
+                    actual.append(ev)
+                seen_tool = True
+                ev_tok.append(dp.sigs.sig(ev.tool_type, ev.status))
+                ev_evt.append(arena.add(ev.result))
+            else:
+                ev_tok.append(-1)
+                ev_evt.append(-1)
+            g += 1
+    scored = len(calls)
+    if scored == 0:
+        return AccuracyReport(0.0, 0.0, 0.0, 0)
+    W = window_capacity
+    ev_tok_a = np.array(ev_tok + [-1], np.int32)
+    ev_evt_a = np.array(ev_evt + [-1], np.int32)
+    calls_a, lens = np.array(calls, np.int64), np.array(call_len, np.int64)
+    idx = (calls_a - lens)[:, None] + np.arange(W)[None, :]
+    valid = np.arange(W)[None, :] < lens[:, None]
+    idx = np.where(valid, idx, len(ev_tok))  # the -1 sentinel
+    batch = WindowBatch(W, ev_tok_a[idx].reshape(-1), ev_evt_a[idx].reshape(-1),
+                        lens.astype(np.int64), arena, [None] * scored)
+    K, slice_after = dp._k_for(max_candidates)
+    res = dp._run(batch, K, None)
+    n_pred = res.n_pred
+    if slice_after:
+        n_pred = np.array([len(range(int(x))[:max_candidates]) for x in n_pred], np.int32)
+    pat = res.pred_pat.reshape(scored, K)
+    tool_of = dp.image.patterns["target_tool"]
+    pred_tool = np.where(np.arange(K)[None, :] < n_pred[:, None], tool_of[pat], -1)
+    act_tool = np.array([dp.sigs.tool(e.tool_type) for e in actual], np.int64)
+    top1 = int(((n_pred > 0) & (pred_tool[:, 0] == act_tool)).sum())
+    top3 = int((pred_tool[:, :min(3, K)] == act_tool[:, None]).any(axis=1).sum())
+    # hit: a FULL prediction of the right tool whose canonical args hash equals
+    comp = res.pred_comp.reshape(scored, K)
+    cand = (pred_tool == act_tool[:, None]) & (comp == C_FULL)
+    hits = 0
+    rows = np.flatnonzero(cand.any(axis=1))
+    if len(rows):
+        from .packing import PredictResult
+
+        sub = PredictResult(K, res.B, n_pred[rows], pat[rows].reshape(-1),
+                            comp[rows].reshape(-1),
+                            res.pred_arg.reshape(scored, K * res.B)[rows].reshape(-1), None, None,
+                            None, None, res.struct_err[rows])
+        from .packing import decode_predictions
+
+        preds = decode_predictions(sub, dp.image, arena, [0.0] * len(rows), 0.0)
+        for r, plist in zip(rows.tolist(), preds):
+            ev = actual[r]
+            h = canonical_arg_hash(ev.args)
+            if any(p.completeness.value == "full" and p.tool_type == ev.tool_type
+                   and canonical_arg_hash(p.args) == h for p in plist):
+                hits += 1
+    return AccuracyReport(top1 / scored, top3 / scored, hits / scored, scored)

@@ -78,6 +78,30 @@ def _encode_steps(path, keys: KeyTable, out: list[int]) -> None:
             out += [0, -2]
 
 
+def encode_binding(expr, sigs: SigTable, keys: KeyTable, steps: list[int]) -> tuple:
+    """One ``paste_binding`` row for a mapping expression (steps appended)."""
+    pos = expr_ctx_pos(expr)
+    step_off = len(steps) // 2
+    suf_off, suf_cnt, start, fail = 0, 0, -1, -1
+    if isinstance(expr, PathLookup):
+        kind, path = X_PATH, expr.path
+    elif isinstance(expr, FormatTemplate):
+        kind, path = X_FORMAT, expr.hole.path
+    elif isinstance(expr, IndexedFallback):
+        kind, path = X_FALLBACK, expr.path_prefix
+        start = expr.start_index if expr.start_index <= INT32_MAX - 64 else -1
+        fail = sigs.tool(expr.fail_tool)
+    else:
+        raise TypeError(f"unknown expression type: {type(expr)!r}")
+    _encode_steps(path, keys, steps)
+    step_cnt = len(steps) // 2 - step_off
+    if kind == X_FALLBACK:
+        suf_off = len(steps) // 2
+        _encode_steps(expr.path_suffix, keys, steps)
+        suf_cnt = len(steps) // 2 - suf_off
+    return (kind, max(min(pos, INT32_MAX), -1), step_off, step_cnt, suf_off, suf_cnt, start, fail)
+
+
 @dataclass
 class PoolImage:
     """Compiled pattern pool: the arrays behind ``paste_pool_desc``."""
@@ -135,30 +159,10 @@ class PoolImage:
             if pat.mapping is not None:
                 flags |= PF_HAS_MAPPING
                 for b in pat.mapping.bindings:
-                    expr = b.expr
-                    pos = expr_ctx_pos(expr)
+                    pos = expr_ctx_pos(b.expr)
                     if not 0 <= pos < len(pat.context):
                         flags |= PF_STRUCT_ERR  # mappings.py:164-169 raise
-                    step_off = len(steps) // 2
-                    suf_off, suf_cnt, start, fail = 0, 0, -1, -1
-                    if isinstance(expr, PathLookup):
-                        kind, path = X_PATH, expr.path
-                    elif isinstance(expr, FormatTemplate):
-                        kind, path = X_FORMAT, expr.hole.path
-                    elif isinstance(expr, IndexedFallback):
-                        kind, path = X_FALLBACK, expr.path_prefix
-                        start = expr.start_index if expr.start_index <= INT32_MAX - 64 else -1
-                        fail = sigs.tool(expr.fail_tool)
-                    else:
-                        raise TypeError(f"unknown expression type: {type(expr)!r}")
-                    _encode_steps(path, keys, steps)
-                    step_cnt = len(steps) // 2 - step_off
-                    if kind == X_FALLBACK:
-                        suf_off = len(steps) // 2
-                        _encode_steps(expr.path_suffix, keys, steps)
-                        suf_cnt = len(steps) // 2 - suf_off
-                    binds.append((kind, max(min(pos, INT32_MAX), -1), step_off, step_cnt,
-                                  suf_off, suf_cnt, start, fail))
+                    binds.append(encode_binding(b.expr, sigs, keys, steps))
             pats[i]["n_bind"] = len(binds) - pats[i]["bind_off"]
             pats[i]["flags"] = flags
 
