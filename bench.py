@@ -10,8 +10,8 @@ simulation.py:415-429) -- one fused kernel launch over all sessions.
 * ``value``  -- sessions/s with the step's inputs already resident in HBM
   (device time, CUDA events on the launch stream, L2 flushed between steps).
 * ``e2e``    -- the same through the public live API (LiveSessionTable.step +
-  fetch) with the new events copied from pinned host memory and the result
-  records copied back every step.
+  fetch_compact) with the new events copied from pinned host memory and the
+  step's compacted result records (CSR streams) copied back every step.
 * ``--impl reference`` -- the CPU oracle port of the reference algorithm
   (oracle/paste_oracle.c, all host threads) on the same workload.
 
@@ -253,11 +253,14 @@ def run_ours(args):
         b.ref = torch.from_numpy(np.ascontiguousarray(b.ref)).pin_memory()
         b.data = torch.from_numpy(b.data).pin_memory()
         host_batches.append(b)
-    pinned = table.pinned_outputs()
+    cpinned = None  # pinned staging for the compacted record streams
     h2d = d2h = 0
     for b in host_batches[:W_]:
         table.step(b)
-        table.fetch(pinned)
+        comp = table.fetch_compact(cpinned)
+        if cpinned is None:
+            cpinned = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                       for k, v in table.cbuf.items()}
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -267,12 +270,12 @@ def run_ours(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         table.step(b)
-        table.fetch(pinned)  # D2H into pinned buffers + stream sync
+        comp = table.fetch_compact(cpinned)  # compaction + sized D2H + stream sync
         e1.record(stream)
         e1.synchronize()
         e2e_times.append(e0.elapsed_time(e1) / 1e3)
         h2d += b.nbytes(with_data=table.ship_bytes)
-        d2h += table.output_nbytes()
+        d2h += comp.nbytes
     e2e_s = sum(e2e_times)
     if world > 1:
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
@@ -308,7 +311,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget_s)
     if args.mine_events > 0:
-        del table, staged, host_batches, pinned
+        del table, staged, host_batches, cpinned
         torch.cuda.empty_cache()
         out["mining"] = run_mining(args, world, rank, local)
     if world > 1:

@@ -354,6 +354,26 @@ typedef struct {
 
 int paste_resolve(const paste_resolve_desc* d, void* stream);
 
+/* Live-path record compaction: the K-slot records of paste_predict_batch
+ * -> CSR streams in session order (decoupled look-back scan).  Capacities:
+ * pred/act/util n*K, arg n*K*B.  totals = {predictions, arguments, actions}.
+ * hdr = n_pred | n_act << 8; pred = pattern | completeness << 30; arg holds
+ * the n_bind references of mapped predictions only; act = slot | level << 5.
+ * Requires max_candidates <= 31.                                           */
+typedef struct {
+  uint16_t* hdr;     /* [n]                                                  */
+  uint32_t* pred;
+  int64_t* arg;
+  uint8_t* act;
+  double* util;
+  int64_t* totals;   /* [3]                                                  */
+} paste_compact_desc;
+
+int64_t paste_compact_scratch_bytes(int64_t n_sessions);
+int paste_compact_records(const paste_predict_out* out, int64_t n_sessions,
+                          const paste_pool_desc* pool, paste_compact_desc* c, void* scratch,
+                          void* stream);
+
 /* Number of kernel launches the last paste_* call on this thread issued.   */
 int paste_last_launch_count(void);
 

@@ -109,6 +109,11 @@ class ResolveDesc(ctypes.Structure):
                 ("result", c_void_p)]
 
 
+class CompactDesc(ctypes.Structure):
+    _fields_ = [("hdr", c_void_p), ("pred", c_void_p), ("arg", c_void_p), ("act", c_void_p),
+                ("util", c_void_p), ("totals", c_void_p)]
+
+
 # numpy mirrors of the element structs
 PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
                           ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
@@ -129,6 +134,9 @@ EXPORTS = {
     "paste_build_match_table": (c_int, [POINTER(PoolDesc), c_int32, c_int32, c_void_p, c_void_p]),
     "paste_mine_geometry": (c_int, [c_int32, c_int32, POINTER(c_int64), POINTER(c_int64)]),
     "paste_mine_count": (c_int, [POINTER(MineDesc), c_void_p]),
+    "paste_compact_scratch_bytes": (c_int64, [c_int64]),
+    "paste_compact_records": (c_int, [POINTER(PredictOut), c_int64, POINTER(PoolDesc),
+                                      POINTER(CompactDesc), c_void_p, c_void_p]),
     "paste_leaf_scan": (c_int, [POINTER(LeafScanDesc), c_void_p]),
     "paste_resolve": (c_int, [POINTER(ResolveDesc), c_void_p]),
     "paste_select_scratch_bytes": (c_int64, [c_int64]),

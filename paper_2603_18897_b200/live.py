@@ -159,3 +159,91 @@ class LiveSessionTable:
                 "count": self.count.cpu().numpy(),
                 "refs": self.refs.cpu().numpy().reshape(-1, 2),
                 "bytes": self.bytes.cpu().numpy()}
+
+
+@dataclass
+class CompactRecords:
+    """Host copy of the CSR record streams of one live step (compact.cu)."""
+
+    K: int
+    B: int
+    hdr: np.ndarray    # u16[n]: n_pred | n_act << 8
+    pred: np.ndarray   # u32[P]: pattern | completeness << 30
+    arg: np.ndarray    # i64[A]: argument refs of mapped predictions
+    act: np.ndarray    # u8[Q]:  slot | level << 5
+    util: np.ndarray   # f64[Q]
+
+    @property
+    def nbytes(self) -> int:
+        return 24 + sum(a.nbytes for a in (self.hdr, self.pred, self.arg, self.act, self.util))
+
+    def expand(self, patterns: np.ndarray) -> PredictResult:
+        """Back to fixed per-session records (for decoding / comparisons)."""
+        K, B = self.K, self.B
+        hdr = self.hdr.astype(np.int64)
+        n_pred, n_act = hdr & 0xFF, hdr >> 8
+        n = len(hdr)
+        res = PredictResult.empty(n, K, B, True)
+        res.n_pred[:] = n_pred
+        res.n_act[:] = n_act
+        sess = np.repeat(np.arange(n), n_pred)
+        slot = np.arange(len(sess)) - np.repeat(np.cumsum(n_pred) - n_pred, n_pred)
+        pid = (self.pred & 0x3FFFFFFF).astype(np.int64)
+        res.pred_pat[sess * K + slot] = pid
+        res.pred_comp[sess * K + slot] = (self.pred >> 30).astype(np.uint8)
+        mapped = (patterns["flags"][pid] & 1) != 0
+        nb = np.where(mapped, patterns["n_bind"][pid], 0)
+        p_sess, p_slot = np.repeat(sess, nb), np.repeat(slot, nb)
+        b_idx = np.arange(int(nb.sum())) - np.repeat(np.cumsum(nb) - nb, nb)
+        res.pred_arg[(p_sess * K + p_slot) * B + b_idx] = self.arg
+        a_sess = np.repeat(np.arange(n), n_act)
+        a_slot = np.arange(len(a_sess)) - np.repeat(np.cumsum(n_act) - n_act, n_act)
+        res.act_pred[a_sess * K + a_slot] = (self.act & 31).astype(np.int16)
+        res.act_level[a_sess * K + a_slot] = self.act >> 5
+        res.act_util[a_sess * K + a_slot] = self.util
+        return res
+
+
+def _compact_init(table: "LiveSessionTable") -> None:
+    t = table.torch
+    n, K, B = table.n, table.K, table.B
+    dev = t.device("cuda")
+    table.cbuf = {"hdr": t.zeros(n, dtype=t.int16, device=dev),
+                  "pred": t.zeros(n * K, dtype=t.int32, device=dev),
+                  "arg": t.zeros(n * K * B, dtype=t.int64, device=dev),
+                  "act": t.zeros(n * K, dtype=t.uint8, device=dev),
+                  "util": t.zeros(n * K, dtype=t.float64, device=dev),
+                  "totals": t.zeros(3, dtype=t.int64, device=dev)}
+    table.cscratch = t.empty(table.lib.paste_compact_scratch_bytes(n), dtype=t.uint8, device=dev)
+    c = table.cbuf
+    from ._native import CompactDesc
+
+    table.cdesc = CompactDesc(ptr(c["hdr"]), ptr(c["pred"]), ptr(c["arg"]), ptr(c["act"]),
+                              ptr(c["util"]), ptr(c["totals"]))
+
+
+def fetch_compact(table: "LiveSessionTable", pinned: dict | None = None) -> CompactRecords:
+    """Compact the step's records on the device (one scan kernel) and copy
+    only the produced bytes back: totals first, then the sized streams."""
+    t = table.torch
+    if not hasattr(table, "cbuf"):
+        _compact_init(table)
+    check(table.lib.paste_compact_records(ctypes.byref(table.out_desc), table.n,
+                                          ctypes.byref(table.pool_desc), ctypes.byref(table.cdesc),
+                                          ptr(table.cscratch), stream_handle()), table.lib)
+    c = table.cbuf
+    if pinned is None:
+        pinned = {k: t.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in c.items()}
+    pinned["totals"].copy_(c["totals"], non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    P, A, Q = (int(x) for x in pinned["totals"].tolist())
+    sizes = {"hdr": table.n, "pred": P, "arg": A, "act": Q, "util": Q}
+    for k, m in sizes.items():
+        pinned[k][:m].copy_(c[k][:m], non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    h = {k: pinned[k][:m].numpy() for k, m in sizes.items()}
+    return CompactRecords(table.K, table.B, h["hdr"].view(np.uint16), h["pred"].view(np.uint32),
+                          h["arg"], h["act"], h["util"])
+
+
+LiveSessionTable.fetch_compact = fetch_compact

@@ -185,3 +185,19 @@ def test_generic_kernel_path_matches_too():
                                "-k", "golden or live"], env=env, capture_output=True, text=True,
                               cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         assert proc.returncode == 0, var + proc.stdout[-3000:] + proc.stderr[-3000:]
+
+
+def test_compact_records_expand_to_the_full_records():
+    pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
+    book = EstimateBook()
+    dp = DevicePool(pool)
+    n = 50_000
+    wl = LiveWorkload(dp.sigs, dp.keys, n, seed=21)
+    table = LiveSessionTable(dp, n, wl.tmpl.nodes, wl.max_batch_bytes,
+                             parse_policy(MOTIF_POLICY).policy, book, max_candidates=8)
+    for step in range(20):
+        table.step(wl.next_batch())
+        full = table.fetch().session_major()
+        comp = table.fetch_compact()
+        _compare(comp.expand(dp.image.patterns), full)
+        assert comp.nbytes < 0.5 * table.output_nbytes()
