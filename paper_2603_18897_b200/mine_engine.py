@@ -373,6 +373,17 @@ def patterns_from_candidates(cands: np.ndarray, sigs: SigTable, S: int, cfg: Min
     return out
 
 
+def merge_shard_histograms(hist, counters, group) -> None:
+    """K3: sum the per-shard (k+1)-gram histograms (and the ingest counters)
+    across ranks.  Windows and matches never cross a session, so with shards
+    made of whole sessions the summed histogram is exactly the one of the
+    whole corpus; over NCCL this is one in-place all-reduce on the device."""
+    import torch.distributed as dist
+
+    dist.all_reduce(hist, group=group)
+    dist.all_reduce(counters, group=group)
+
+
 def mine_columnar(trace: dict, sigs: SigTable, cfg: MiningConfig,
                   inactivity_ms: float = 300_000.0, group=None) -> list[PatternTuple]:
     """mine() over a columnar trace shard on this device.  With a
@@ -384,10 +395,7 @@ def mine_columnar(trace: dict, sigs: SigTable, cfg: MiningConfig,
     tables = MineTables.allocate(max(sigs.n_sigs, 2), cfg.k, relation)
     counters = ingest_count(tables, trace, inactivity_ms)
     if group is not None:
-        import torch.distributed as dist
-
-        dist.all_reduce(tables.hist, group=group)
-        dist.all_reduce(counters, group=group)
+        merge_shard_histograms(tables.hist, counters, group)
     if int(counters[1].item()):
         raise _native.PasteUnsupported(
             "columnar trace is not grouped by session / sorted by (t_start, seq)")
