@@ -132,3 +132,27 @@ def greedy(p, benefit, duration, cost, ids, slack, budget) -> list[int]:
     out = np.zeros(max(len(arrs[0]), 1), np.int32)
     m = fn(len(arrs[0]), *[_p(a) for a in arrs], slack, budget, _p(out))
     return out[:m].tolist()
+
+
+def leaf_scan(nodes, data, refs, target_off, target_bytes, node_budget=10_000, target_type=5,
+              max_matches=4, threads=1):
+    """Oracle candidate_paths over a tape batch: (n_out, first matches, truncated)."""
+    from paper_2603_18897_b200._native import LeafScanDesc
+
+    fn = lib().oracle_leaf_scan
+    fn.restype = c_int
+    fn.argtypes = [POINTER(LeafScanDesc), c_int]
+    n = len(refs)
+    arrs = dict(nodes=np.ascontiguousarray(nodes), data=np.ascontiguousarray(data),
+                refs=np.ascontiguousarray(refs, np.int64), ev=np.arange(n, dtype=np.int32),
+                tt=np.full(n, target_type, np.int32), tn=np.zeros(n, np.uint8),
+                toff=np.ascontiguousarray(target_off, np.int64),
+                tb=np.ascontiguousarray(target_bytes, np.uint8),
+                oo=np.arange(n + 1, dtype=np.int64) * max_matches,
+                out=np.zeros(n * max_matches, np.int32), n_out=np.zeros(n, np.int64),
+                tr=np.zeros(n, np.uint8))
+    d = LeafScanDesc(n, node_budget, *[_p(arrs[k]) for k in (
+        "nodes", "data", "refs", "ev", "tt", "tn", "toff", "tb", "oo", "out", "n_out", "tr")])
+    if fn(ctypes.byref(d), threads) != 0:
+        raise RuntimeError("oracle_leaf_scan failed")
+    return arrs["n_out"], arrs["out"].reshape(n, max_matches), arrs["tr"]

@@ -431,3 +431,49 @@ int64_t oracle_greedy(int64_t n, const double* p, const double* benefit, const d
   free(jobs);
   return n_sel;
 }
+
+/* ------------------------------------------------------------------------ */
+/* candidate_paths (mappings.py:237-266) over tapes: pre-order visit of at   */
+/* most node_budget nodes, scalar leaves equal to the target (values_equal,  */
+/* events.py:125-130: same type class, same canonical bytes, not NaN).       */
+/* ------------------------------------------------------------------------ */
+int oracle_leaf_scan(const paste_leaf_scan_desc* d, int n_threads) {
+  int64_t q;
+#pragma omp parallel for num_threads(n_threads > 0 ? n_threads : 1) schedule(dynamic, 64)
+  for (q = 0; q < d->n_queries; ++q) {
+    const paste_event_ref ref = d->refs[d->event[q]];
+    const paste_tape_node* root = &d->nodes[ref.node_base];
+    const int64_t total = root->type >= PASTE_T_LIST ? root->b : 1;
+    const int64_t limit = total < d->node_budget ? total : d->node_budget;
+    const int tt = d->target_type[q];
+    const uint8_t* tb = d->target_bytes + d->target_off[q];
+    const int64_t tl = d->target_off[q + 1] - d->target_off[q];
+    const int64_t cap = d->out_off[q + 1] - d->out_off[q];
+    int64_t i, n_out = 0;
+    for (i = 0; i < limit; ++i) {
+      const paste_tape_node* nd = &d->nodes[ref.node_base + i];
+      int eq = 0;
+      if (nd->type < PASTE_T_LIST && nd->type == tt && !d->target_nan[q] && !(nd->flags & PASTE_F_NAN)) {
+        if (nd->type <= PASTE_T_TRUE) {
+          eq = 1;
+        } else {
+          const uint8_t* b = d->bytes + ref.byte_base + nd->a;
+          int64_t len = nd->b;
+          if (nd->type == PASTE_T_STR && (nd->flags & PASTE_F_NFC)) {
+            const uint8_t* x = b + nd->b;
+            len = (int64_t)x[0] | ((int64_t)x[1] << 8) | ((int64_t)x[2] << 16) | ((int64_t)x[3] << 24);
+            b = x + 4;
+          }
+          eq = len == tl && memcmp(b, tb, (size_t)len) == 0;
+        }
+      }
+      if (eq) {
+        if (n_out < cap) d->out_nodes[d->out_off[q] + n_out] = (int32_t)i;
+        ++n_out;
+      }
+    }
+    d->n_out[q] = n_out;
+    d->truncated[q] = total > d->node_budget;
+  }
+  return PASTE_OK;
+}

@@ -408,3 +408,36 @@ def score_replay(traces, pool, window_capacity: int, max_candidates):
                    and canonical_arg_hash(p.args) == h for p in plist):
                 hits += 1
     return AccuracyReport(top1 / scored, top3 / scored, hits / scored, scored)
+
+
+class LeafScanBatch:
+    """Device-resident K5 batch: one (payload, target) query per session."""
+
+    def __init__(self, nodes, data, refs, target_off, target_bytes, node_budget: int = 10_000,
+                 target_type: int = 5, max_matches: int = 4):
+        torch = _torch()
+        self.lib = _native.lib()
+        n = len(refs)
+        self.n = n
+        self.nodes, self.data, self.refs = to_dev(nodes), to_dev(data), to_dev(refs)
+        self.events = torch.arange(n, dtype=torch.int32, device="cuda")
+        self.tt = torch.full((n,), target_type, dtype=torch.int32, device="cuda")
+        self.tn = torch.zeros(n, dtype=torch.uint8, device="cuda")
+        self.toff, self.tbytes = to_dev(target_off), to_dev(target_bytes)
+        self.out_off = torch.arange(n + 1, dtype=torch.int64, device="cuda") * max_matches
+        self.out_nodes = torch.zeros(n * max_matches, dtype=torch.int32, device="cuda")
+        self.n_out = torch.zeros(n, dtype=torch.int64, device="cuda")
+        self.trunc = torch.zeros(n, dtype=torch.uint8, device="cuda")
+        self.budget = node_budget
+
+    def desc(self):
+        from ._native import LeafScanDesc
+
+        return LeafScanDesc(self.n, self.budget, ptr(self.nodes), ptr(self.data), ptr(self.refs),
+                            ptr(self.events), ptr(self.tt), ptr(self.tn), ptr(self.toff),
+                            ptr(self.tbytes), ptr(self.out_off), ptr(self.out_nodes),
+                            ptr(self.n_out), ptr(self.trunc))
+
+    def launch(self) -> None:
+        d = self.desc()
+        check(self.lib.paste_leaf_scan(ctypes.byref(d), stream_handle()), self.lib)

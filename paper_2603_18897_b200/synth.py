@@ -298,3 +298,45 @@ def columnar_flags(c, inactivity_ms: float = 300_000.0) -> np.ndarray:
     b = np.ones(len(s), bool)
     b[1:] = (s[1:] != s[:-1]) | ((ts[1:] - te[:-1]) > inactivity_ms)
     return b
+
+
+# ---------------------------------------------------------------------------
+# C5: long tool outputs (64 KB url_list results)
+# ---------------------------------------------------------------------------
+
+def long_output_corpus(n_sessions: int, seed: int = 2603, result_size: int = 1120):
+    """Per session one ``tool_result(url_list, result_size)`` payload
+    (simulation.py:150-178; 65,005 B of canonical JSON at 1120 entries) and
+    the next call's argument ``list[(37 * s) % result_size].url``
+    (SURVEY.md 8(d) C5).  Payloads are shape-interned: one node template,
+    per-session bytes."""
+    from .tape import KeyTable, TapeArena
+
+    keys = KeyTable()
+    arena = TapeArena(keys, keep_objects=False)
+    sample = {"list": [{"url": f"https://XXXXXXXX-{i}.example/doc", "rank": i}
+                       for i in range(result_size)], "total": result_size}
+    arena.add(sample)
+    nodes, data, refs = arena.arrays()
+    tmpl = data.copy()
+    pos = np.flatnonzero(tmpl == ord("X"))
+    runs = pos.reshape(-1, 8)
+    rng = np.random.default_rng(seed)
+    L = len(tmpl)
+    out = np.broadcast_to(tmpl, (n_sessions, L)).copy()
+    hexes = _HEX[rng.integers(0, 16, (n_sessions, 8), dtype=np.uint8)]
+    for r in range(len(runs)):
+        out[:, runs[r]] = hexes
+    byte_base = np.arange(n_sessions, dtype=np.int64) * L
+    ev_refs = np.stack([np.zeros(n_sessions, np.int64), byte_base], axis=1)
+    j = (37 * np.arange(n_sessions)) % result_size
+    url_node = 3 + 3 * j  # root dict, "list", then (dict, url, rank) per entry
+    a = nodes["a"][url_node].astype(np.int64)
+    b = nodes["b"][url_node].astype(np.int64)
+    t_off = np.zeros(n_sessions + 1, np.int64)
+    t_off[1:] = np.cumsum(b)
+    flat = out.reshape(-1)
+    gather = np.repeat(byte_base + a, b) + (np.arange(int(b.sum())) - np.repeat(t_off[:-1], b))
+    return {"nodes": nodes, "bytes": flat, "refs": ev_refs, "target_off": t_off,
+            "target_bytes": flat[gather], "expected_node": url_node, "keys": keys,
+            "payload_bytes": L, "canonical_json_bytes": None}

@@ -85,3 +85,25 @@ def test_score_accuracy_matches_reference():
         rep = score_accuracy(sessions, G.pool(case["pool"]), window_capacity=case["window"],
                              max_candidates=case["max_candidates"])
         assert rep.to_json() == case["expected"]
+
+
+@pytest.mark.parametrize("budget", [10_000, 2_000, 1])
+def test_long_output_leaf_scan_matches_oracle(budget):
+    import numpy as np
+
+    from oracle import bridge
+    from paper_2603_18897_b200.device_ops import LeafScanBatch
+    from paper_2603_18897_b200.synth import long_output_corpus
+
+    c = long_output_corpus(3000, seed=5)
+    b = LeafScanBatch(c["nodes"], c["bytes"], c["refs"], c["target_off"], c["target_bytes"],
+                      node_budget=budget)
+    b.launch()
+    n_out, out, tr = bridge.leaf_scan(c["nodes"], c["bytes"], c["refs"], c["target_off"],
+                                      c["target_bytes"], node_budget=budget, threads=8)
+    assert np.array_equal(b.n_out.cpu().numpy(), n_out)
+    assert np.array_equal(b.trunc.cpu().numpy(), tr)
+    dev = b.out_nodes.view(3000, -1).cpu().numpy()
+    for q in range(3000):
+        k = min(int(n_out[q]), 4)
+        assert np.array_equal(dev[q, :k], out[q, :k])
