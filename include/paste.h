@@ -374,6 +374,47 @@ int paste_compact_records(const paste_predict_out* out, int64_t n_sessions,
                           const paste_pool_desc* pool, paste_compact_desc* c, void* scratch,
                           void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* K7: Phase II hypothesis hit counts (mappings.py:276-417, 326-335)        */
+/* ---------------------------------------------------------------------- */
+
+/* For every (hypothesis h, occurrence m): resolve hypothesis h's expression
+ * against occurrence m's matched context and compare it with m's actual
+ * argument (values_equal).  hits[h] / unsure[h] are accumulated (zero them
+ * first); eq[h*n_occ + m] (optional) = 1 equal, 0 not, 2 unsure.  FormatTemplate
+ * pairs involving non-ASCII text are "unsure" (the caller re-evaluates them
+ * with Unicode string semantics).  fmt[5*h..] = prefix offset / length,
+ * suffix offset / length (into fmt_bytes), normalization (0 none, 1 trim,
+ * 2 lowercase).  occ_event / src_pos are [n_occ][n_ctx]; src_pos is the
+ * matched event's first position in the occurrence's history (-1 absent),
+ * history tokens of later copies of the same event are -1.                 */
+typedef struct {
+  int64_t n_hyp;
+  int64_t n_occ;
+  int32_t n_ctx;
+  int32_t pad;
+  const paste_binding* hyp;
+  const int32_t* steps;
+  const int32_t* fmt;
+  const uint8_t* fmt_bytes;
+  const paste_tape_node* nodes;
+  const uint8_t* bytes;
+  const paste_event_ref* refs;
+  const int32_t* occ_event;
+  const int32_t* src_pos;
+  const int32_t* hist_off;   /* [n_occ + 1]                                   */
+  const int32_t* hist_tok;
+  const int32_t* act_type;   /* [n_occ] tape type of the actual argument      */
+  const uint8_t* act_nan;    /* [n_occ]                                       */
+  const int64_t* act_off;    /* [n_occ + 1] canonical bytes of the actual     */
+  const uint8_t* act_bytes;
+  int64_t* hits;             /* [n_hyp]                                       */
+  int64_t* unsure;           /* [n_hyp]                                       */
+  uint8_t* eq;               /* optional [n_hyp * n_occ]                      */
+} paste_holds_desc;
+
+int paste_holds(const paste_holds_desc* d, void* stream);
+
 /* Number of kernel launches the last paste_* call on this thread issued.   */
 int paste_last_launch_count(void);
 

@@ -114,6 +114,13 @@ class CompactDesc(ctypes.Structure):
                 ("util", c_void_p), ("totals", c_void_p)]
 
 
+class HoldsDesc(ctypes.Structure):
+    _fields_ = [("n_hyp", c_int64), ("n_occ", c_int64), ("n_ctx", c_int32), ("pad", c_int32)] + \
+        [(name, c_void_p) for name in ("hyp", "steps", "fmt", "fmt_bytes", "nodes", "bytes", "refs",
+                                       "occ_event", "src_pos", "hist_off", "hist_tok", "act_type",
+                                       "act_nan", "act_off", "act_bytes", "hits", "unsure", "eq")]
+
+
 # numpy mirrors of the element structs
 PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
                           ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
@@ -134,6 +141,7 @@ EXPORTS = {
     "paste_build_match_table": (c_int, [POINTER(PoolDesc), c_int32, c_int32, c_void_p, c_void_p]),
     "paste_mine_geometry": (c_int, [c_int32, c_int32, POINTER(c_int64), POINTER(c_int64)]),
     "paste_mine_count": (c_int, [POINTER(MineDesc), c_void_p]),
+    "paste_holds": (c_int, [POINTER(HoldsDesc), c_void_p]),
     "paste_compact_scratch_bytes": (c_int64, [c_int64]),
     "paste_compact_records": (c_int, [POINTER(PredictOut), c_int64, POINTER(PoolDesc),
                                       POINTER(CompactDesc), c_void_p, c_void_p]),

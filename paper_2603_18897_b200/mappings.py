@@ -160,7 +160,7 @@ def infer_mapping(occurrences: Sequence[Occurrence],
     argument; the first hypothesis holding on >= ``validation_fraction`` of the
     occurrences wins (mappings.py:276-417).  Hypothesis hit counts run on the
     device (:mod:`.phase2`)."""
-    from .phase2 import infer_mapping as _infer
+    from .phase2_device import infer_mapping as _infer
 
     return _infer(occurrences, validation_fraction)
 

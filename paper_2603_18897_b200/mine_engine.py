@@ -221,6 +221,24 @@ def _count_corpus(streams, cfg: MiningConfig):
     return sigs, tables
 
 
+def _phase2(occ, cfg: MiningConfig, hits: int):
+    """Mapping inference for one candidate and its hit count (K7 on device)."""
+    from . import phase2_device
+
+    if len(occ) < 2 or not phase2.common_scalar_args(occ):
+        return None, hits
+    if phase2_device._aliased_histories(occ):
+        mapping = phase2.infer_mapping(occ, cfg.validation_fraction)
+        if mapping is None:
+            return None, hits
+        return mapping, sum(1 for m, nxt in occ if phase2.mapping_holds(mapping, m, nxt))
+    occs = phase2_device.OccurrenceSet(occ, occ[0][1].tool_type)
+    mapping = phase2_device.infer_mapping(occ, cfg.validation_fraction, occs)
+    if mapping is None:
+        return None, hits
+    return mapping, phase2_device.count_mapping_hits(mapping, occs)
+
+
 def mine(traces: Sequence[Session], cfg: MiningConfig) -> list[PatternTuple]:
     if not traces:
         raise ValueError("traces must be non-empty")
@@ -239,9 +257,7 @@ def mine(traces: Sequence[Session], cfg: MiningConfig) -> list[PatternTuple]:
             if sig_streams is None:
                 sig_streams = [[signature_of(e) for e in st] for st in streams]
             occ = _occurrences(streams, sig_streams, context, target, cfg)
-            mapping = phase2.infer_mapping(occ, cfg.validation_fraction)
-            if mapping is not None:
-                hits = sum(1 for m, nxt in occ if phase2.mapping_holds(mapping, m, nxt))
+            mapping, hits = _phase2(occ, cfg, hits)
         p = hits / n_match
         if p >= cfg.tau:
             patterns.append(PatternTuple(context=context, target=target, mapping=mapping, p=p,
@@ -276,11 +292,16 @@ def validate(context, target: str, mapping: ValueMapping | None, traces: Sequenc
     if mapping is None:
         return follow / n_match
     sig_streams = [[signature_of(e) for e in st] for st in streams]
-    occ = _occurrences(streams, sig_streams, tuple(context), target,
-                       MiningConfig(k=cfg.k, sigma=cfg.sigma, tau=cfg.tau,
-                                    validation_fraction=cfg.validation_fraction,
-                                    match_relation=cfg.match_relation))
-    hits = sum(1 for m, nxt in occ if phase2.mapping_holds(mapping, m, nxt))
+    occ = _occurrences(streams, sig_streams, tuple(context), target, cfg)
+    if not occ:
+        return 0.0
+    from . import phase2_device
+
+    if phase2_device._aliased_histories(occ):
+        hits = sum(1 for m, nxt in occ if phase2.mapping_holds(mapping, m, nxt))
+    else:
+        hits = phase2_device.count_mapping_hits(
+            mapping, phase2_device.OccurrenceSet(occ, occ[0][1].tool_type))
     return hits / n_match
 
 

@@ -107,3 +107,41 @@ def test_long_output_leaf_scan_matches_oracle(budget):
     for q in range(3000):
         k = min(int(n_out[q]), 4)
         assert np.array_equal(dev[q, :k], out[q, :k])
+
+
+def _occ(context_tool, target_tool, result, actual_args, fails=0, seq0=0):
+    src = Event("s", seq0, EventKind.TOOL_CALL, context_tool, Status.SUCCESS, {"q": seq0}, result,
+                0.0, 1.0)
+    history = [src]
+    for j in range(fails):
+        history.append(Event("s", seq0 + 1 + j, EventKind.TOOL_CALL, target_tool, Status.FAIL,
+                             {"r": j}, {"ok": False}, 2.0 + j, 3.0 + j))
+    ctx_events = (src,) if fails == 0 else (src, history[-1])
+    actual = Event("s", seq0 + 1 + fails, EventKind.TOOL_CALL, target_tool, Status.SUCCESS,
+                   actual_args, {"ok": True}, 9.0, 10.0)
+    return (MatchedContext(events=ctx_events, history=tuple(history)), actual)
+
+
+def test_device_infer_mapping_matches_host_search():
+    """K7 inference == the host restatement (pinned by the reference goldens)
+    over the acceptance criterion's occurrence families, incl. Unicode."""
+    from paper_2603_18897_b200 import infer_mapping
+
+    fams = [
+        [_occ("grep", "file_editor", {"hits": [{"path": f"src/м{i}.py"}], "n": 1},
+              {"path": f"src/м{i}.py"}, seq0=i) for i in range(10)],
+        [_occ("search", "web_fetch", {"list": [{"url": f"u{i}-{j}.example"} for j in range(4)]},
+              {"url": f"u{i}-{1 + i % 2}.example"}, fails=1 + i % 2, seq0=i * 10) for i in range(10)],
+        [_occ("file_editor", "terminal", {"path": f"pkg/x{i}.py"}, {"cmd": f"pytest pkg/x{i}.py"},
+              seq0=i) for i in range(10)],
+        [_occ("file_editor", "terminal", {"title": f"  Ünïcode {i} "},
+              {"cmd": f"open ünïcode {i}!"}, seq0=i) for i in range(10)],
+        [_occ("file_editor", "terminal", {"t": f" Name{i} "}, {"cmd": f"name{i}", "x": i},
+              seq0=i) for i in range(10)],
+        [_occ("search", "web_fetch", {"v": 1.0 * i, "w": str(i)}, {"a": i, "b": f"id-{i}"},
+              seq0=i) for i in range(12)],
+    ]
+    for occ in fams:
+        got = infer_mapping(occ)
+        exp = phase2.infer_mapping(occ)
+        assert got == exp, (got, exp)
