@@ -385,12 +385,21 @@ def patterns_from_candidates(cands: np.ndarray, sigs: SigTable, S: int, cfg: Min
     keys = [digits[:, d] for d in reversed(range(cfg.k))] + [cands[:, 0], -length, -p]
     order = np.lexsort(keys)
     sig_obj = [sigs.signature(x) for x in range(S)]
+    # contexts are non-empty and 0 < tau <= p <= 1 by construction, so the
+    # frozen dataclass is filled directly (its __init__ + validation would
+    # dominate the host side of a 100M-event mining step)
+    new, cls = object.__new__, PatternTuple
     out = []
-    for i in order.tolist():
-        n = int(length[i])
-        ctx = tuple(sig_obj[x] for x in digits[i, :n].tolist())
-        out.append(PatternTuple(context=ctx, target=sigs.tools[int(cands[i, 0])], mapping=None,
-                                p=float(p[i]), support=int(cands[i, 2])))
+    lens = length[order].tolist()
+    digs = digits[order].tolist()
+    tools = cands[order, 0].tolist()
+    sups = cands[order, 2].tolist()
+    ps = p[order].tolist()
+    for n, dg, t, sup, pv in zip(lens, digs, tools, sups, ps):
+        obj = new(cls)
+        obj.__dict__.update(context=tuple(sig_obj[x] for x in dg[:n]), target=sigs.tools[t],
+                            mapping=None, p=pv, support=sup)
+        out.append(obj)
     return out
 
 
