@@ -305,6 +305,12 @@ int64_t paste_select_scratch_bytes(int64_t n_jobs);
 int paste_select_greedy(paste_select_desc* d, int64_t slack, int64_t budget, void* scratch,
                         int64_t scratch_bytes, void* stream);
 
+/* Stage-2 preemption victim (scheduling.py:571-578): index of the job with
+ * the smallest (U, -id), -1 for no jobs (selected / n_selected unused).
+ * scratch: >= 4 bytes of device memory.  Synchronous.                      */
+int paste_select_victim(const paste_select_desc* d, int32_t* out_idx, void* scratch,
+                        void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* K5: leaf scan and expression resolution over payload tapes               */
 /* ---------------------------------------------------------------------- */

@@ -318,3 +318,76 @@ extern "C" int64_t paste_select_scratch_bytes(int64_t n_jobs) {
   return 8 * n_jobs + 32 * SEL_MAX_CAP + 4 * SEL_MAX_CAP * 256 + 4 * (SEL_MAX_CAP + 4) + 16 +
          4 * SEL_MAX_CAND + 256;
 }
+
+// ---------------------------------------------------------------------------
+// Stage-2 preemption victim (scheduling.py:571-578): the running speculative
+// job minimising (U, -id).  One CTA sweeps the jobs and reduces.
+// ---------------------------------------------------------------------------
+namespace paste {
+
+// (U, -id, index): min() returns the first of equal keys
+__device__ __forceinline__ bool victim_less(uint64_t ka, uint64_t ia, int32_t xa, uint64_t kb,
+                                            uint64_t ib, int32_t xb) {
+  if (ka != kb) return ka < kb;
+  if (ia != ib) return ia < ib;
+  return xa < xb;
+}
+
+__global__ void __launch_bounds__(1024) victim_kernel(paste_select_desc D, int32_t* out_idx,
+                                                      int* bad) {
+  __shared__ uint64_t sk[1024], si[1024];
+  __shared__ int32_t sx[1024];
+  uint64_t bk = ~0ull, bi = ~0ull;
+  int32_t bx = -1;
+  for (int64_t i = threadIdx.x; i < D.n_jobs; i += blockDim.x) {
+    const double p = D.p[i], c = (double)D.cost[i], d = D.duration[i];
+    const double u = __ddiv_rn(__dmul_rn(p, D.benefit[i]), __dmul_rn(c, d));
+    if (d == 0.0 || D.cost[i] == 0 || u != u) atomicOr(bad, 1);
+    const uint64_t ku = ~desc_key(u);                                   // ascending U
+    const uint64_t ki = ~((uint64_t)D.id[i] ^ 0x8000000000000000ull);  // larger id first
+    if (bx < 0 || victim_less(ku, ki, (int32_t)i, bk, bi, bx)) {
+      bk = ku;
+      bi = ki;
+      bx = (int32_t)i;
+    }
+  }
+  sk[threadIdx.x] = bk;
+  si[threadIdx.x] = bi;
+  sx[threadIdx.x] = bx;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) {
+      const int o = threadIdx.x + off;
+      if (sx[o] >= 0 && (sx[threadIdx.x] < 0 || victim_less(sk[o], si[o], sx[o], sk[threadIdx.x],
+                                                            si[threadIdx.x], sx[threadIdx.x]))) {
+        sk[threadIdx.x] = sk[o];
+        si[threadIdx.x] = si[o];
+        sx[threadIdx.x] = sx[o];
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out_idx = sx[0];
+}
+
+}  // namespace paste
+
+extern "C" int paste_select_victim(const paste_select_desc* d, int32_t* out_idx, void* scratch,
+                                   void* stream_) {
+  reset_launches();
+  PASTE_REQUIRE(d != nullptr && out_idx != nullptr && scratch != nullptr, "null argument");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  int* bad = static_cast<int*>(scratch);
+  PASTE_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), stream));
+  victim_kernel<<<1, 1024, 0, stream>>>(*d, out_idx, bad);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  int h_bad = 0;
+  PASTE_CUDA_CHECK(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, stream));
+  PASTE_CUDA_CHECK(cudaStreamSynchronize(stream));
+  if (h_bad) {
+    set_error("jobs need a non-zero cost * duration and a non-NaN utility");
+    return PASTE_ERR_INVALID;
+  }
+  return PASTE_OK;
+}

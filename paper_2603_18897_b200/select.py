@@ -59,3 +59,26 @@ def greedy_select_jobs(jobs, slack: int, budget: int):
     ids = np.array([j.id for j in jobs], np.int64)
     idx = select_greedy_arrays(p, bene, dur, cost.astype(np.int32), ids, slack, budget)
     return [jobs[i] for i in idx.tolist()]
+
+
+def preemption_victim(jobs):
+    """The job Stage 2 of schedule_tick aborts first (scheduling.py:571-578):
+    ``min(victims, key=lambda j: (j.utility(), -j.id))`` on the device."""
+    from .device_ops import stream_handle
+
+    if not jobs:
+        return None
+    torch = _torch()
+    lib = _native.lib()
+    for j in jobs:
+        if j.cost * j.duration_est_ms == 0:
+            raise ZeroDivisionError("float division by zero")
+    cols = [torch.tensor([getattr(j, f) for j in jobs], dtype=dt, device="cuda") for f, dt in (
+        ("p", torch.float64), ("benefit_ms", torch.float64), ("duration_est_ms", torch.float64),
+        ("cost", torch.int32), ("id", torch.int64))]
+    out = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    scratch = torch.zeros(4, dtype=torch.int32, device="cuda")
+    d = SelectDesc(len(jobs), *[ptr(c) for c in cols], 0, 0)
+    check(lib.paste_select_victim(ctypes.byref(d), ptr(out), ptr(scratch), stream_handle()), lib)
+    i = int(out.item())
+    return jobs[i] if i >= 0 else None

@@ -65,3 +65,24 @@ def test_device_greedy_matches_oracle_at_scale(n, cap, ties):
     slack, budget = cap + 3, cap
     got = select_greedy_arrays(p, bene, dur, cost, ids, slack, budget).tolist()
     assert got == bridge.greedy(p, bene, dur, cost, ids, slack, budget)
+
+
+@pytest.mark.gpu
+def test_preemption_victim_matches_reference_expression():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import random
+
+    from paper_2603_18897_b200.scheduling import Job, JobKind
+    from paper_2603_18897_b200.select import preemption_victim
+
+    rng = random.Random(7)
+    for trial in range(200):
+        jobs = [Job(id=rng.randint(1, 10_000), kind=JobKind.SPECULATIVE, tool_type="t", args={},
+                    arg_hash="", session_id="s", p=rng.choice([0.5, 0.25, rng.random() + 0.01]),
+                    benefit_ms=rng.choice([100.0, 50.0]), cost=rng.randint(1, 3),
+                    duration_est_ms=rng.choice([100.0, 200.0]), submitted_at=0.0)
+                for _ in range(rng.randint(1, 3000 if trial % 10 == 0 else 30))]
+        exp = min(jobs, key=lambda j: (j.utility(), -j.id))  # scheduling.py:577
+        assert preemption_victim(jobs) is exp
