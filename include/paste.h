@@ -421,6 +421,52 @@ typedef struct {
 
 int paste_holds(const paste_holds_desc* d, void* stream);
 
+/* ---------------------------------------------------------------------- */
+/* C2 replay: score_accuracy (prediction.py:133-169)                        */
+/* ---------------------------------------------------------------------- */
+
+/* Replays a trace corpus: every tool call after a session's first is
+ * predicted from the window of the `call_len` events before it (the event
+ * stream is all sessions back to back, LLM steps included as token -1), and
+ * scored: top1 = first candidate's tool equals the call's tool, top3 = one of
+ * the first three does, hit = some FULL candidate of that tool has canonical
+ * arguments equal to the call's (canonical_arg_hash, events.py:117-118).
+ * Arguments are compared by key set (key-set ids interned by the caller:
+ * call_keyset / pat_keyset, -1 = "let the host decide", -2 = args are not a
+ * dict) and per binding by canonical value: scalar type class + canonical
+ * bytes (NFC for strings); FormatTemplate values compose prefix +
+ * norm(leaf text) + suffix when everything is ASCII.  Calls whose outcome
+ * needs Unicode or container semantics are flagged in `unsure` (the caller
+ * re-checks them; their hit is not counted).  tallies = {top1, top3, hits,
+ * unsure} (accumulated: zero them first).  cand_limit applies Python's
+ * preds[:m] to each candidate list (INT32_MAX = no limit).  The prediction
+ * records land in `out` (any layout) for the caller's re-check.            */
+typedef struct {
+  int64_t n_calls;
+  int32_t capacity;          /* W = window_capacity                           */
+  int32_t cand_limit;
+  const int32_t* ev_tok;     /* [n_events] sig, -1 = LLM step                 */
+  const int32_t* ev_evt;     /* [n_events] result payload index into refs     */
+  const int64_t* call_pos;   /* [n_calls] stream index of the scored call     */
+  const int32_t* call_len;   /* [n_calls] window length (<= W)                */
+  const int32_t* call_tool;  /* [n_calls] tool id of the call                 */
+  const int32_t* call_args;  /* [n_calls] args payload index into refs        */
+  const int32_t* call_keyset;/* [n_calls]                                     */
+  const int32_t* pat_keyset; /* [n_patterns]                                  */
+  const int32_t* bind_key;   /* [n_bindings] key id of each binding's arg name*/
+  const int32_t* fmt;        /* [5 * n_bindings] as paste_holds_desc.fmt      */
+  const uint8_t* fmt_bytes;
+  const paste_tape_node* nodes;
+  const uint8_t* bytes;
+  const paste_event_ref* refs;
+  int64_t* tallies;          /* [4]                                           */
+  uint8_t* unsure;           /* [n_calls]                                     */
+} paste_replay_desc;
+
+int64_t paste_replay_scratch_bytes(int64_t n_calls, int32_t capacity);
+int paste_replay_score(const paste_pool_desc* pool, const paste_replay_desc* d,
+                       paste_predict_out* out, void* scratch, void* stream);
+
 /* Number of kernel launches the last paste_* call on this thread issued.   */
 int paste_last_launch_count(void);
 

@@ -156,3 +156,50 @@ def leaf_scan(nodes, data, refs, target_off, target_bytes, node_budget=10_000, t
     if fn(ctypes.byref(d), threads) != 0:
         raise RuntimeError("oracle_leaf_scan failed")
     return arrs["n_out"], arrs["out"].reshape(n, max_matches), arrs["tr"]
+
+
+def score_corpus(im: PoolImage, corpus, keys, window_capacity: int, max_candidates,
+                 threads: int = 1, calls: slice | None = None) -> tuple[int, int, int, int]:
+    """score_accuracy (prediction.py:133-169) over a ReplayCorpus with the C
+    oracle's predictions and the Python canonical_arg_hash check.  Returns
+    (top1, top3, hits, scored) over ``calls`` (default: all)."""
+    from paper_2603_18897_b200.events import canonical_arg_hash
+    from paper_2603_18897_b200.packing import WindowBatch, decode_predictions
+    from paper_2603_18897_b200.tape import ArrayTapes
+
+    W = window_capacity
+    sl = calls or slice(None)
+    pos = corpus.call_pos[sl]
+    lens = corpus.call_len[sl].astype(np.int64)
+    n = len(pos)
+    if n == 0:
+        return 0, 0, 0, 0
+    idx = (pos - lens)[:, None] + np.arange(W)[None, :]
+    valid = np.arange(W)[None, :] < lens[:, None]
+    idx = np.where(valid, idx, 0)
+    tok = np.where(valid, corpus.ev_tok[idx], -1).astype(np.int32).reshape(-1)
+    evt = np.where(valid, corpus.ev_evt[idx], -1).astype(np.int32).reshape(-1)
+    tapes = ArrayTapes(corpus.nodes, corpus.data, corpus.refs, keys)
+    if max_candidates is not None and max_candidates > 0:
+        K, lim = max_candidates, None
+    else:
+        K, lim = max(im.max_bucket, 1), max_candidates
+    batch = WindowBatch(W, tok, evt, lens, tapes, [None] * n)
+    res = predict(im, batch, K, threads=threads)
+    tool_of = im.patterns["target_tool"]
+    act_tool = corpus.call_tool[sl]
+    args_pid = corpus.call_args[sl]
+    preds = decode_predictions(res, im, tapes, [0.0] * n, 0.0)
+    top1 = top3 = hits = 0
+    for r, plist in enumerate(preds):
+        plist = plist[:lim]
+        pats = [int(res.pred_pat[r * K + i]) for i in range(len(plist))]
+        tools = [int(tool_of[p]) for p in pats]
+        t = int(act_tool[r])
+        top1 += bool(tools) and tools[0] == t
+        top3 += t in tools[:3]
+        cand = [p for p, pt in zip(plist, tools) if pt == t and p.completeness.value == "full"]
+        if cand:
+            want = canonical_arg_hash(tapes.node_object(int(args_pid[r]), 0))
+            hits += any(canonical_arg_hash(p.args) == want for p in cand)
+    return top1, top3, hits, n

@@ -121,6 +121,13 @@ class HoldsDesc(ctypes.Structure):
                                        "act_nan", "act_off", "act_bytes", "hits", "unsure", "eq")]
 
 
+class ReplayDesc(ctypes.Structure):
+    _fields_ = [("n_calls", c_int64), ("capacity", c_int32), ("cand_limit", c_int32)] + \
+        [(name, c_void_p) for name in ("ev_tok", "ev_evt", "call_pos", "call_len", "call_tool",
+                                       "call_args", "call_keyset", "pat_keyset", "bind_key", "fmt",
+                                       "fmt_bytes", "nodes", "bytes", "refs", "tallies", "unsure")]
+
+
 # numpy mirrors of the element structs
 PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
                           ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
@@ -142,6 +149,9 @@ EXPORTS = {
     "paste_mine_geometry": (c_int, [c_int32, c_int32, POINTER(c_int64), POINTER(c_int64)]),
     "paste_mine_count": (c_int, [POINTER(MineDesc), c_void_p]),
     "paste_holds": (c_int, [POINTER(HoldsDesc), c_void_p]),
+    "paste_replay_scratch_bytes": (c_int64, [c_int64, c_int32]),
+    "paste_replay_score": (c_int, [POINTER(PoolDesc), POINTER(ReplayDesc), POINTER(PredictOut),
+                                   c_void_p, c_void_p]),
     "paste_compact_scratch_bytes": (c_int64, [c_int64]),
     "paste_compact_records": (c_int, [POINTER(PredictOut), c_int64, POINTER(PoolDesc),
                                       POINTER(CompactDesc), c_void_p, c_void_p]),

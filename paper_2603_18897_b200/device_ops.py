@@ -336,78 +336,10 @@ def evaluate_mapping(mapping, ctx):
 
 
 def score_replay(traces, pool, window_capacity: int, max_candidates):
-    from .events import EventKind, canonical_arg_hash
-    from .packing import C_FULL, WindowBatch
-    from .prediction import AccuracyReport
-    from .tape import TapeArena
+    """Device replay with the hit check on the device (replay.py, C2)."""
+    from .replay import score_replay as _score
 
-    if window_capacity < 1:
-        raise ValueError("window capacity must be >= 1")
-    dp = DevicePool(pool)
-    arena = TapeArena(dp.keys)
-    ev_tok, ev_evt, calls, call_len, actual = [], [], [], [], []
-    g = 0
-    for session in traces:
-        start = g
-        seen_tool = False
-        for ev in session.events:
-            if ev.kind is EventKind.TOOL_CALL:
-                if seen_tool:
-                    calls.append(g)
-                    call_len.append(min(window_capacity, g - start))
-                    actual.append(ev)
-                seen_tool = True
-                ev_tok.append(dp.sigs.sig(ev.tool_type, ev.status))
-                ev_evt.append(arena.add(ev.result))
-            else:
-                ev_tok.append(-1)
-                ev_evt.append(-1)
-            g += 1
-    scored = len(calls)
-    if scored == 0:
-        return AccuracyReport(0.0, 0.0, 0.0, 0)
-    W = window_capacity
-    ev_tok_a = np.array(ev_tok + [-1], np.int32)
-    ev_evt_a = np.array(ev_evt + [-1], np.int32)
-    calls_a, lens = np.array(calls, np.int64), np.array(call_len, np.int64)
-    idx = (calls_a - lens)[:, None] + np.arange(W)[None, :]
-    valid = np.arange(W)[None, :] < lens[:, None]
-    idx = np.where(valid, idx, len(ev_tok))  # the -1 sentinel
-    batch = WindowBatch(W, ev_tok_a[idx].reshape(-1), ev_evt_a[idx].reshape(-1),
-                        lens.astype(np.int64), arena, [None] * scored)
-    K, slice_after = dp._k_for(max_candidates)
-    res = dp._run(batch, K, None)
-    n_pred = res.n_pred
-    if slice_after:
-        n_pred = np.array([len(range(int(x))[:max_candidates]) for x in n_pred], np.int32)
-    pat = res.pred_pat.reshape(scored, K)
-    tool_of = dp.image.patterns["target_tool"]
-    pred_tool = np.where(np.arange(K)[None, :] < n_pred[:, None], tool_of[pat], -1)
-    act_tool = np.array([dp.sigs.tool(e.tool_type) for e in actual], np.int64)
-    top1 = int(((n_pred > 0) & (pred_tool[:, 0] == act_tool)).sum())
-    top3 = int((pred_tool[:, :min(3, K)] == act_tool[:, None]).any(axis=1).sum())
-    # hit: a FULL prediction of the right tool whose canonical args hash equals
-    comp = res.pred_comp.reshape(scored, K)
-    cand = (pred_tool == act_tool[:, None]) & (comp == C_FULL)
-    hits = 0
-    rows = np.flatnonzero(cand.any(axis=1))
-    if len(rows):
-        from .packing import PredictResult
-
-        sub = PredictResult(K, res.B, n_pred[rows], pat[rows].reshape(-1),
-                            comp[rows].reshape(-1),
-                            res.pred_arg.reshape(scored, K * res.B)[rows].reshape(-1), None, None,
-                            None, None, res.struct_err[rows])
-        from .packing import decode_predictions
-
-        preds = decode_predictions(sub, dp.image, arena, [0.0] * len(rows), 0.0)
-        for r, plist in zip(rows.tolist(), preds):
-            ev = actual[r]
-            h = canonical_arg_hash(ev.args)
-            if any(p.completeness.value == "full" and p.tool_type == ev.tool_type
-                   and canonical_arg_hash(p.args) == h for p in plist):
-                hits += 1
-    return AccuracyReport(top1 / scored, top3 / scored, hits / scored, scored)
+    return _score(traces, pool, window_capacity, max_candidates)
 
 
 class LeafScanBatch:

@@ -340,3 +340,150 @@ def long_output_corpus(n_sessions: int, seed: int = 2603, result_size: int = 112
     return {"nodes": nodes, "bytes": flat, "refs": ev_refs, "target_off": t_off,
             "target_bytes": flat[gather], "expected_node": url_node, "keys": keys,
             "payload_bytes": L, "canonical_json_bytes": None}
+
+
+# ---------------------------------------------------------------------------
+# C2: coding-agent replay corpus (edit_verify / locate_examine)
+# ---------------------------------------------------------------------------
+
+class FieldTemplates:
+    """Shape-interned payload templates whose variable text is marked by runs
+    of one uppercase placeholder letter per field ('A', 'B', ...)."""
+
+    def __init__(self, keys: KeyTable, samples: list):
+        arena = TapeArena(keys, keep_objects=False)
+        for s in samples:
+            arena.add(s)
+        self.nodes, data, refs = arena.arrays()
+        self.node_base = refs[:, 0].copy()
+        self.byte_tmpl, self.fields = [], []
+        for k in range(len(samples)):
+            b0 = int(refs[k, 1])
+            b1 = int(refs[k + 1, 1]) if k + 1 < len(samples) else len(data)
+            t = data[b0:b1].copy()
+            f = {}
+            for letter in b"ABCDEFGH":
+                pos = np.flatnonzero(t == letter)
+                if len(pos):
+                    cuts = np.flatnonzero(np.diff(pos) != 1) + 1
+                    f[chr(letter)] = np.stack(np.split(pos, cuts))  # [n_runs, run_len]
+            self.byte_tmpl.append(t)
+            self.fields.append(f)
+
+    def fill(self, kind: int, values: dict[str, np.ndarray]) -> np.ndarray:
+        """[n, len] payload bytes of template ``kind``; values[letter] is [n, run_len]
+        (every run of a field gets the same text)."""
+        n = len(next(iter(values.values())))
+        t = self.byte_tmpl[kind]
+        block = np.broadcast_to(t, (n, len(t))).copy()
+        for letter, runs in self.fields[kind].items():
+            for r in range(len(runs)):
+                block[:, runs[r]] = values[letter]
+        return block
+
+
+# payload templates of the two coding motifs (workloads.py:139-193, shapes of
+# simulation.py:150-178): edit / verify / grep / open, args then results
+_C2_SAMPLES = [
+    {"path": "src/fix_AAAAAAAAAA.py", "change": "BBBBBBBBBB"},          # 0 edit args
+    {"path": "src/fix_AAAAAAAAAA.py", "applied": True},                 # 1 edit result
+    {"cmd": "pytest src/fix_AAAAAAAAAA.py"},                            # 2 verify args
+    {"ok": True, "token": "CCCCCCCCCCCCCCCC"},                          # 3 verify result
+    {"pattern": "sym_AAAAAAAAAA"},                                      # 4 grep args
+    {"hits": [{"path": f"src/mBBBBBBBB_{i}.py", "line": 10 * (i + 1)} for i in range(4)],
+     "count": 4},                                                       # 5 grep result
+    {"path": "src/mBBBBBBBB_0.py"},                                     # 6 open args
+    {"path": "src/mBBBBBBBB_0.py", "applied": True},                    # 7 open result
+]
+C2_EDIT, C2_VERIFY, C2_GREP, C2_OPEN = range(4)
+_C2_TOOL = ("file_editor", "terminal", "grep", "file_editor")
+
+
+def _hex(rng: np.random.Generator, n: int, width: int) -> np.ndarray:
+    return _HEX[rng.integers(0, 16, (n, width), dtype=np.uint8)]
+
+
+def coding_replay_corpus(dp, n_sessions: int, window_capacity: int = 16, seed: int = 2,
+                         ksets=None, rounds: int = 4, verify_rate: float = 0.55,
+                         open_rate: float = 0.38):
+    """C2 replay corpus as a ReplayCorpus: ``n_sessions`` coding sessions, half
+    edit_verify (file_editor -> terminal "pytest <path>" at ``verify_rate``),
+    half locate_examine (grep -> file_editor hits[0].path at ``open_rate``),
+    ``rounds`` rounds each, every tool call preceded by an LLM step
+    (workloads.py:297-366).  Token / path text is random hex; the planted
+    dependencies are exact, so mined PathLookup / FormatTemplate bindings hit."""
+    from .events import Status
+    from .replay import KeysetTable, ReplayCorpus
+
+    ksets = KeysetTable() if ksets is None else ksets
+    rng = np.random.default_rng(seed)
+    n = n_sessions
+    motif = rng.random(n) < 0.5                       # True = locate_examine
+    fired = rng.random((n, rounds)) < np.where(motif, open_rate, verify_rate)[:, None]
+    kind = np.empty((n, rounds, 2), np.int8)
+    kind[:, :, 0] = np.where(motif, C2_GREP, C2_EDIT)[:, None]
+    kind[:, :, 1] = np.where(motif, C2_OPEN, C2_VERIFY)[:, None]
+    valid = np.ones((n, rounds, 2), bool)
+    valid[:, :, 1] = fired
+    # per-round field text: A (10 hex), B (10 hex: edit change / 8 hex: grep hash)
+    a_txt = _hex(rng, n * rounds, 10).reshape(n, rounds, 10)
+    b_txt = _hex(rng, n * rounds, 10).reshape(n, rounds, 10)
+    flat_valid = valid.reshape(-1)
+    call_kind = kind.reshape(-1)[flat_valid]
+    call_round = np.broadcast_to(np.arange(n * rounds).reshape(n, rounds, 1),
+                                 (n, rounds, 2)).reshape(-1)[flat_valid]
+    call_sess = call_round // rounds
+    n_calls_s = valid.reshape(n, -1).sum(axis=1)
+    T = len(call_kind)
+    call_start = np.zeros(n + 1, np.int64)
+    call_start[1:] = np.cumsum(n_calls_s)
+    j = np.arange(T, dtype=np.int64) - call_start[call_sess]     # call index in session
+    sess_ev0 = 2 * call_start[:-1]                               # LLM + tool per call
+    tool_pos = sess_ev0[call_sess] + 2 * j + 1
+
+    tmpl = FieldTemplates(dp.keys, _C2_SAMPLES)
+    tool_ids = np.array([dp.sigs.sig(t, Status.SUCCESS) for t in _C2_TOOL], np.int32)
+    E = int(2 * T)
+    ev_tok = np.full(E, -1, np.int32)
+    ev_tok[tool_pos] = tool_ids[call_kind]
+    scored = np.flatnonzero(j >= 1)
+    C = len(scored)
+    # payload ids: results 0..T-1 (call order), then args of scored calls
+    ev_evt = np.full(E, -1, np.int32)
+    ev_evt[tool_pos] = np.arange(T, dtype=np.int32)
+
+    blocks, bases, node_base = [], np.zeros(T + C, np.int64), np.zeros(T + C, np.int64)
+    at = 0
+
+    def emit(tk: int, pids: np.ndarray, values: dict[str, np.ndarray]):
+        nonlocal at
+        if not len(pids):
+            return
+        blk = tmpl.fill(tk, values)
+        bases[pids] = at + np.arange(len(pids), dtype=np.int64) * blk.shape[1]
+        node_base[pids] = tmpl.node_base[tk]
+        at += blk.size
+        blocks.append(blk.reshape(-1))
+
+    a_of = a_txt.reshape(-1, 10)[call_round]
+    b_of = b_txt.reshape(-1, 10)[call_round]
+    for ck in range(4):
+        ids = np.flatnonzero(call_kind == ck)
+        res_vals = {C2_EDIT: {"A": a_of[ids]}, C2_VERIFY: {"C": _hex(rng, len(ids), 16)},
+                    C2_GREP: {"B": b_of[ids, :8]}, C2_OPEN: {"B": b_of[ids, :8]}}[ck]
+        emit(2 * ck + 1, ids, res_vals)
+        sc = np.intersect1d(ids, scored, assume_unique=True)
+        args_pid = T + np.searchsorted(scored, sc)
+        arg_vals = {C2_EDIT: {"A": a_of[sc], "B": b_of[sc]}, C2_VERIFY: {"A": a_of[sc]},
+                    C2_GREP: {"A": a_of[sc]}, C2_OPEN: {"B": b_of[sc, :8]}}[ck]
+        emit(2 * ck, args_pid, arg_vals)
+    refs = np.stack([node_base, bases], axis=1)
+    keysets = np.array([ksets.of_args(s) for s in _C2_SAMPLES[0::2]], np.int32)
+    sk = call_kind[scored]
+    return ReplayCorpus(
+        ev_tok=ev_tok, ev_evt=ev_evt, call_pos=tool_pos[scored].astype(np.int64),
+        call_len=np.minimum(window_capacity, 2 * j[scored] + 1).astype(np.int32),
+        call_tool=(tool_ids[sk] >> 1).astype(np.int32),
+        call_args=(T + np.arange(C)).astype(np.int32), call_keyset=keysets[sk],
+        nodes=tmpl.nodes, data=np.concatenate(blocks) if blocks else np.zeros(1, np.uint8),
+        refs=refs)

@@ -244,3 +244,17 @@ def leaf_str_of(value: Any) -> str | None:
     if isinstance(value, float) and value.is_integer():
         return str(int(value))
     return str(value)
+
+
+class ArrayTapes:
+    """Read-only arena view over (nodes, data, refs) arrays, for decoding."""
+
+    def __init__(self, nodes: np.ndarray, data: np.ndarray, refs: np.ndarray, keys: KeyTable):
+        self.nodes, self.data, self.refs, self.keys = nodes, data, refs, keys
+
+    def arrays(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+        return self.nodes, self.data, self.refs
+
+    def node_object(self, event: int, node: int) -> Any:
+        return decode_node(self.nodes, self.data, int(self.refs[event, 0]),
+                           int(self.refs[event, 1]), node, self.keys)

@@ -467,6 +467,8 @@ def dump(name, obj):
 def main(which):
     if "c3pool" in which:
         make_c3_pool()
+    if "c2" in which:
+        make_c2()
     if "fixtures" not in which:
         return
     dump("predict_golden.json", make_predict())
@@ -490,6 +492,33 @@ def make_c3_pool():
                         "pool_motif_c3.json")
     save_pool(pool, path)
     print(f"pool_motif_c3.json: {len(pool)} patterns", file=sys.stderr)
+
+
+CODING_MIX = {"edit_verify": 0.5, "locate_examine": 0.5}
+
+
+def make_c2():
+    """C2: pools mined by the reference from
+    generate_corpus(edit_verify/locate_examine, 1000, seed=1) with the default
+    MiningConfig (tau 0.5) and with tau 0.3 (FormatTemplate bindings), plus
+    the reference's score_accuracy on a 400-session replay corpus (seed=2)."""
+    data = os.path.join(os.path.dirname(os.path.dirname(OUT)), "paper_2603_18897_b200", "data")
+    train = generate_corpus(CODING_MIX, 1000, seed=1)
+    pools = {"pool_coding_c2.json": mine_pool(train.sessions, MiningConfig()),
+             "pool_coding_c2_t03.json": mine_pool(train.sessions, MiningConfig(tau=0.3))}
+    for name, pool in pools.items():
+        save_pool(pool, os.path.join(data, name))
+        print(f"{name}: {len(pool)} patterns", file=sys.stderr)
+    held = generate_corpus(CODING_MIX, 400, seed=2)
+    cases = []
+    for name, pool in pools.items():
+        pool = roundtrip(pool)
+        for W, K in ((16, 8), (16, None), (2, 1)):
+            rep = score_accuracy(held.sessions, pool, window_capacity=W, max_candidates=K)
+            cases.append({"pool_file": name, "window": W, "max_candidates": K,
+                          "expected": rep.to_json()})
+    dump("score_c2_golden.json", {"sessions": [sess_json(s) for s in held.sessions],
+                                  "cases": cases})
 
 
 if __name__ == "__main__":
