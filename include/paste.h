@@ -44,7 +44,8 @@ enum {
   PASTE_T_NULL = 0, PASTE_T_FALSE = 1, PASTE_T_TRUE = 2, PASTE_T_INT = 3,
   PASTE_T_FLOAT = 4, PASTE_T_STR = 5, PASTE_T_LIST = 6, PASTE_T_DICT = 7
 };
-enum { PASTE_F_NFC = 1, PASTE_F_FLOATSRC = 2, PASTE_F_NAN = 4 };
+enum { PASTE_F_NFC = 1, PASTE_F_FLOATSRC = 2, PASTE_F_NAN = 4,
+       PASTE_F_ASCII = 8 /* scalar bytes all < 0x80 (optional hint; absent = scan) */ };
 
 typedef struct {
   uint8_t type;   /* PASTE_T_*                                                */
@@ -145,6 +146,11 @@ typedef struct {
   const paste_event_ref* new_ref; /* [n]                                      */
   int64_t new_evt_base;
   int64_t new_byte_base;
+  /* optional stream mode (replay): windows are views into one event stream.
+   * tok / evt are then the stream, count[s] (<= capacity) is window s's
+   * length and window s = stream[stream_end[s] - count[s] .. stream_end[s]);
+   * new_tok must be NULL.                                                  */
+  const int64_t* stream_end;
 } paste_windows;
 
 enum { PASTE_C_FULL = 0, PASTE_C_PARTIAL = 1, PASTE_C_TOOL_ONLY = 2 };
@@ -440,7 +446,9 @@ int paste_holds(const paste_holds_desc* d, void* stream);
  * re-checks them; their hit is not counted).  tallies = {top1, top3, hits,
  * unsure} (accumulated: zero them first).  cand_limit applies Python's
  * preds[:m] to each candidate list (INT32_MAX = no limit).  The prediction
- * records land in `out` (any layout) for the caller's re-check.            */
+ * records land in `out` (any layout) for the caller's re-check.  Windows are
+ * read in place from the event stream (paste_windows stream mode).         */
+enum { PASTE_FMT_NON_ASCII = 0x100 };
 typedef struct {
   int64_t n_calls;
   int32_t capacity;          /* W = window_capacity                           */
@@ -448,13 +456,15 @@ typedef struct {
   const int32_t* ev_tok;     /* [n_events] sig, -1 = LLM step                 */
   const int32_t* ev_evt;     /* [n_events] result payload index into refs     */
   const int64_t* call_pos;   /* [n_calls] stream index of the scored call     */
-  const int32_t* call_len;   /* [n_calls] window length (<= W)                */
+  const int64_t* call_len;   /* [n_calls] window length (<= W)                */
   const int32_t* call_tool;  /* [n_calls] tool id of the call                 */
   const int32_t* call_args;  /* [n_calls] args payload index into refs        */
   const int32_t* call_keyset;/* [n_calls]                                     */
   const int32_t* pat_keyset; /* [n_patterns]                                  */
   const int32_t* bind_key;   /* [n_bindings] key id of each binding's arg name*/
-  const int32_t* fmt;        /* [5 * n_bindings] as paste_holds_desc.fmt      */
+  const int32_t* fmt;        /* [5 * n_bindings] as paste_holds_desc.fmt, the
+                                normalization word may carry
+                                PASTE_FMT_NON_ASCII (prefix/suffix not ASCII) */
   const uint8_t* fmt_bytes;
   const paste_tape_node* nodes;
   const uint8_t* bytes;
@@ -463,9 +473,8 @@ typedef struct {
   uint8_t* unsure;           /* [n_calls]                                     */
 } paste_replay_desc;
 
-int64_t paste_replay_scratch_bytes(int64_t n_calls, int32_t capacity);
 int paste_replay_score(const paste_pool_desc* pool, const paste_replay_desc* d,
-                       paste_predict_out* out, void* scratch, void* stream);
+                       paste_predict_out* out, void* stream);
 
 /* Number of kernel launches the last paste_* call on this thread issued.   */
 int paste_last_launch_count(void);

@@ -57,14 +57,15 @@ def predict(im: PoolImage, batch: WindowBatch, K: int,
             admit: tuple[np.ndarray, np.ndarray, np.ndarray] | None = None,
             new_tok: np.ndarray | None = None, new_ref: np.ndarray | None = None,
             new_evt_base: int = 0, new_byte_base: int = 0,
-            threads: int = 1, out_slot_major: int = 0) -> PredictResult:
+            threads: int = 1, out_slot_major: int = 0,
+            stream_end: np.ndarray | None = None) -> PredictResult:
     """Run the oracle; like the device it mutates the window rings (and the
     event directory) when new_tok / new_ref are given."""
     desc, pids, keep = pool_desc(im)
     nodes, data, refs = batch.arena.arrays() if hasattr(batch.arena, "arrays") else batch.arena
     win = WindowsDesc(batch.n, batch.capacity, batch.slot_major, _p(batch.tok), _p(batch.evt), _p(batch.count),
                       _p(nodes), _p(data), _p(refs), _p(new_tok), _p(new_ref), new_evt_base,
-                      new_byte_base)
+                      new_byte_base, _p(stream_end))
     res = PredictResult.empty(batch.n, K, max(im.max_bindings, 1), admit is not None,
                               out_slot_major)
     if admit is not None:
@@ -159,7 +160,8 @@ def leaf_scan(nodes, data, refs, target_off, target_bytes, node_budget=10_000, t
 
 
 def score_corpus(im: PoolImage, corpus, keys, window_capacity: int, max_candidates,
-                 threads: int = 1, calls: slice | None = None) -> tuple[int, int, int, int]:
+                 threads: int = 1, calls: slice | None = None,
+                 stream: bool = True) -> tuple[int, int, int, int]:
     """score_accuracy (prediction.py:133-169) over a ReplayCorpus with the C
     oracle's predictions and the Python canonical_arg_hash check.  Returns
     (top1, top3, hits, scored) over ``calls`` (default: all)."""
@@ -174,18 +176,23 @@ def score_corpus(im: PoolImage, corpus, keys, window_capacity: int, max_candidat
     n = len(pos)
     if n == 0:
         return 0, 0, 0, 0
-    idx = (pos - lens)[:, None] + np.arange(W)[None, :]
-    valid = np.arange(W)[None, :] < lens[:, None]
-    idx = np.where(valid, idx, 0)
-    tok = np.where(valid, corpus.ev_tok[idx], -1).astype(np.int32).reshape(-1)
-    evt = np.where(valid, corpus.ev_evt[idx], -1).astype(np.int32).reshape(-1)
     tapes = ArrayTapes(corpus.nodes, corpus.data, corpus.refs, keys)
+    if stream:  # windows read in place (paste_windows stream mode)
+        tok, evt = corpus.ev_tok, corpus.ev_evt
+        stream_end = np.ascontiguousarray(pos, np.int64)
+    else:  # gathered [n][W] rings
+        idx = (pos - lens)[:, None] + np.arange(W)[None, :]
+        valid = np.arange(W)[None, :] < lens[:, None]
+        idx = np.where(valid, idx, 0)
+        tok = np.where(valid, corpus.ev_tok[idx], -1).astype(np.int32).reshape(-1)
+        evt = np.where(valid, corpus.ev_evt[idx], -1).astype(np.int32).reshape(-1)
+        stream_end = None
     if max_candidates is not None and max_candidates > 0:
         K, lim = max_candidates, None
     else:
         K, lim = max(im.max_bucket, 1), max_candidates
-    batch = WindowBatch(W, tok, evt, lens, tapes, [None] * n)
-    res = predict(im, batch, K, threads=threads)
+    batch = WindowBatch(W, tok, evt, np.ascontiguousarray(lens, np.int64), tapes, [None] * n)
+    res = predict(im, batch, K, threads=threads, stream_end=stream_end)
     tool_of = im.patterns["target_tool"]
     act_tool = corpus.call_tool[sl]
     args_pid = corpus.call_args[sl]

@@ -26,6 +26,7 @@
 
 /* ring / output addressing (session-major or slot-major, include/paste.h) */
 static int64_t ring_idx(const paste_windows* w, int64_t s, int slot) {
+  if (w->stream_end) return w->stream_end[s] - w->count[s] + slot; /* stream mode: count <= W */
   return w->slot_major ? (int64_t)slot * w->n_sessions + s : s * w->capacity + slot;
 }
 static int64_t out_idx(const paste_predict_out* o, int64_t n, int64_t s, int i) {

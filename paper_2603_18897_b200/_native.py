@@ -57,7 +57,7 @@ class WindowsDesc(ctypes.Structure):
                 ("tok", c_void_p), ("evt", c_void_p), ("count", c_void_p),
                 ("nodes", c_void_p), ("bytes", c_void_p), ("refs", c_void_p),
                 ("new_tok", c_void_p), ("new_ref", c_void_p), ("new_evt_base", c_int64),
-                ("new_byte_base", c_int64)]
+                ("new_byte_base", c_int64), ("stream_end", c_void_p)]
 
 
 class PredictOut(ctypes.Structure):
@@ -149,9 +149,8 @@ EXPORTS = {
     "paste_mine_geometry": (c_int, [c_int32, c_int32, POINTER(c_int64), POINTER(c_int64)]),
     "paste_mine_count": (c_int, [POINTER(MineDesc), c_void_p]),
     "paste_holds": (c_int, [POINTER(HoldsDesc), c_void_p]),
-    "paste_replay_scratch_bytes": (c_int64, [c_int64, c_int32]),
     "paste_replay_score": (c_int, [POINTER(PoolDesc), POINTER(ReplayDesc), POINTER(PredictOut),
-                                   c_void_p, c_void_p]),
+                                   c_void_p]),
     "paste_compact_scratch_bytes": (c_int64, [c_int64]),
     "paste_compact_records": (c_int, [POINTER(PredictOut), c_int64, POINTER(PoolDesc),
                                       POINTER(CompactDesc), c_void_p, c_void_p]),

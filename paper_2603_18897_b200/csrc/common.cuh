@@ -81,6 +81,7 @@ __device__ __forceinline__ int64_t step_child(const paste_tape_node* nodes, int6
 // window-ring / output-record addressing (session-major or slot-major)
 // ---------------------------------------------------------------------------
 __host__ __device__ __forceinline__ int64_t ring_at(const paste_windows& w, int64_t sess, int slot) {
+  if (w.stream_end) return w.stream_end[sess] - w.count[sess] + slot;  // stream mode (count <= W)
   return w.slot_major ? (int64_t)slot * w.n_sessions + sess : sess * w.capacity + slot;
 }
 __host__ __device__ __forceinline__ int64_t out_at(const paste_predict_out& o, int64_t n,

@@ -245,6 +245,7 @@ extern "C" int paste_predict_batch(const paste_pool_desc* pool, paste_windows* w
   PASTE_REQUIRE(out->max_candidates >= 1, "max_candidates must be >= 1");
   PASTE_REQUIRE(out->max_bindings >= pool->max_bindings, "max_bindings below pool maximum");
   PASTE_REQUIRE(pool->k >= 1, "k must be >= 1");
+  PASTE_REQUIRE(!(windows->stream_end && windows->new_tok), "stream-mode windows cannot observe");
   {
     const int g = pool->relation == PASTE_REL_ANCHORED ? pool->k : pool->max_ctx;
     if ((g < windows->capacity ? g : windows->capacity) > GMAX) {

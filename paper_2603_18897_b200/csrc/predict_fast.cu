@@ -314,8 +314,9 @@ __device__ __forceinline__ void predict_session(const FastParams& P, int64_t ses
   const int64_t n = P.win.n_sessions;
   const int W = P.win.capacity, G = P.G;
   int32_t* gs = gt + G;  // ring slots of the gathered tokens
-  const int64_t rbase = P.win.slot_major ? sess : sess * W;
-  const int64_t rstride = P.win.slot_major ? n : 1;
+  const int64_t rbase = P.win.stream_end ? P.win.stream_end[sess] - P.win.count[sess]
+                                          : (P.win.slot_major ? sess : sess * W);
+  const int64_t rstride = (P.win.slot_major && !P.win.stream_end) ? n : 1;
   const int K = P.out.max_candidates;
   OutIdx X;
   X.B = P.out.max_bindings;

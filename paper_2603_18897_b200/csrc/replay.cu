@@ -1,10 +1,9 @@
-// C2 replay: score_accuracy (prediction.py:133-169) as three launches.
+// C2 replay: score_accuracy (prediction.py:133-169) as two launches.
 //
-//   1. replay_windows_kernel: each scored call's window (the `call_len` events
-//      before it in the event stream) is gathered into a slot-major ring, the
-//      layout K4 reads;
-//   2. K4 (paste_predict_batch) predicts every window;
-//   3. replay_score_kernel: one thread per call tallies top1 / top3 and the
+//   1. K4 (paste_predict_batch) predicts every window, reading it in place
+//      from the event stream (paste_windows stream mode: the `call_len`
+//      events before each call);
+//   2. replay_score_kernel: one thread per call tallies top1 / top3 and the
 //      hit check -- a FULL candidate of the call's tool whose arguments
 //      canonically equal the call's (canonical_arg_hash, events.py:95-118).
 //
@@ -21,25 +20,62 @@
 
 namespace paste {
 
-__global__ void replay_windows_kernel(const paste_replay_desc D, int32_t* __restrict__ tok,
-                                      int32_t* __restrict__ evt, int64_t* __restrict__ count) {
-  const int64_t n = D.n_calls;
-  const int W = D.capacity;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n * W;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int slot = (int)(t / n);
-    const int64_t c = t - (int64_t)slot * n;
-    const int len = D.call_len[c];
-    int32_t tk = -1, ev = -1;
-    if (slot < len) {
-      const int64_t g = D.call_pos[c] - len + slot;
-      tk = D.ev_tok[g];
-      ev = D.ev_evt[g];
+// ---------------------------------------------------------------------------
+// byte-range helpers: 32-bit word loads (2 aligned loads + funnel shift) so a
+// ~20-byte comparison is ~10 loads in flight instead of ~40 dependent byte
+// loads.  Loads never touch a 4-byte word that holds no byte of the range, so
+// they stay inside the allocation.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_part(const uint8_t* p, int r) {  // r in 1..4 bytes
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+  const uint32_t sh = (uint32_t)(a & 3);
+  const uint32_t lo = __ldg(w);
+  const uint32_t hi = (sh + r > 4) ? __ldg(w + 1) : 0u;
+  const uint32_t v = __funnelshift_r(lo, hi, sh * 8);
+  return r >= 4 ? v : (v & ((1u << (8 * r)) - 1u));
+}
+
+__device__ __forceinline__ bool bytes_eq(const uint8_t* a, const uint8_t* b, int64_t n) {
+  for (int64_t k = 0; k < n; k += 16) {
+    uint32_t diff = 0;
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+      const int64_t r = n - k - j;
+      if (r > 0) {
+        const int rr = r < 4 ? (int)r : 4;
+        diff |= ld_part(a + k + j, rr) ^ ld_part(b + k + j, rr);
+      }
     }
-    tok[t] = tk;
-    evt[t] = ev;
-    if (slot == 0) count[c] = len;
+    if (diff) return false;
   }
+  return true;
+}
+
+// a == lower(b) over n ASCII bytes (str.lower on ASCII text)
+__device__ __forceinline__ bool bytes_eq_lower(const uint8_t* a, const uint8_t* b, int64_t n) {
+  for (int64_t k = 0; k < n; k += 4) {
+    const int64_t r = n - k;
+    const int rr = r < 4 ? (int)r : 4;
+    uint32_t y = ld_part(b + k, rr);
+    const uint32_t up = __vcmpgeu4(y, 0x41414141u) & __vcmpleu4(y, 0x5a5a5a5au);
+    y += up & 0x20202020u;
+    if (ld_part(a + k, rr) != y) return false;
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool bytes_ascii(const uint8_t* a, int64_t n) {
+  uint32_t acc = 0;
+  for (int64_t k = 0; k < n; k += 4) {
+    const int64_t r = n - k;
+    acc |= ld_part(a + k, r < 4 ? (int)r : 4);
+  }
+  return (acc & 0x80808080u) == 0;
+}
+
+__device__ __forceinline__ bool node_ascii(const Node& nd, const uint8_t* b, int64_t n) {
+  return (nd.flags() & PASTE_F_ASCII) || bytes_ascii(b, n);
 }
 
 __device__ __forceinline__ bool has_surrogate(const uint8_t* b, int64_t n) {
@@ -76,7 +112,7 @@ __device__ int compare_binding(const paste_replay_desc& D, int bind, int kind, i
   const Node pn = load_node(D.nodes, pr.node_base + (pref & 0xFFFFFFFF));
   const Node a = load_node(D.nodes, ar.node_base + an);
   const int at = a.type();
-  int64_t al;
+  int64_t al = 0;
   const uint8_t* ab = at < PASTE_T_LIST ? canon_bytes(D, a, ar.byte_base, &al) : nullptr;
   if (kind != PASTE_X_FORMAT) {
     const int pt = pn.type();
@@ -85,41 +121,30 @@ __device__ int compare_binding(const paste_replay_desc& D, int bind, int kind, i
     if (pt <= PASTE_T_TRUE) return CMP_EQ;
     int64_t pl;
     const uint8_t* pb = canon_bytes(D, pn, pr.byte_base, &pl);
-    if (pt == PASTE_T_STR && (has_surrogate(pb, pl) || has_surrogate(ab, al))) return CMP_UNSURE;
-    if (pl != al) return CMP_NE;
-    for (int64_t k = 0; k < pl; ++k)
-      if (pb[k] != ab[k]) return CMP_NE;
-    return CMP_EQ;
+    if (pt == PASTE_T_STR && !((pn.flags() & a.flags()) & PASTE_F_ASCII) &&
+        (has_surrogate(pb, pl) || has_surrogate(ab, al)))
+      return CMP_UNSURE;  // json.dumps(...).encode("utf-8") raises on lone surrogates
+    return (pl == al && bytes_eq(pb, ab, pl)) ? CMP_EQ : CMP_NE;
   }
   // FormatTemplate: prefix + norm(leaf_str(leaf)) + suffix (mappings.py:197-223)
   if (at != PASTE_T_STR) return CMP_NE;
   const uint8_t* tb = D.bytes + pr.byte_base + pn.a;  // leaf_str: raw text / number text
   int64_t lo = 0, hi = pn.b;
   const int* f = D.fmt + 5 * bind;
+  const int pl = f[1], sl = f[3], norm = f[4] & 0xff;
+  if ((f[4] & PASTE_FMT_NON_ASCII) || !node_ascii(pn, tb, hi) || !node_ascii(a, ab, al))
+    return CMP_UNSURE;  // Unicode str.strip / str.lower / NFC: the host decides
   const uint8_t* pre = D.fmt_bytes + f[0];
   const uint8_t* suf = D.fmt_bytes + f[2];
-  const int pl = f[1], sl = f[3], norm = f[4];
-  bool ascii = true;
-  for (int64_t k = 0; k < hi; ++k) ascii &= tb[k] < 0x80;
-  for (int k = 0; k < pl; ++k) ascii &= pre[k] < 0x80;
-  for (int k = 0; k < sl; ++k) ascii &= suf[k] < 0x80;
-  for (int64_t k = 0; k < al; ++k) ascii &= ab[k] < 0x80;
-  if (!ascii) return CMP_UNSURE;
   if (norm == 1) {  // str.strip()
     while (lo < hi && py_space_ascii(tb[lo])) ++lo;
     while (hi > lo && py_space_ascii(tb[hi - 1])) --hi;
   }
   if ((int64_t)pl + (hi - lo) + sl != al) return CMP_NE;
-  for (int k = 0; k < pl; ++k)
-    if (pre[k] != ab[k]) return CMP_NE;
-  for (int64_t k = lo; k < hi; ++k) {
-    uint8_t c = tb[k];
-    if (norm == 2 && c >= 'A' && c <= 'Z') c += 32;  // str.lower()
-    if (c != ab[pl + (k - lo)]) return CMP_NE;
-  }
-  for (int k = 0; k < sl; ++k)
-    if (suf[k] != ab[pl + (hi - lo) + k]) return CMP_NE;
-  return CMP_EQ;
+  if (!bytes_eq(pre, ab, pl)) return CMP_NE;
+  if (!(norm == 2 ? bytes_eq_lower(ab + pl, tb + lo, hi - lo) : bytes_eq(ab + pl, tb + lo, hi - lo)))
+    return CMP_NE;
+  return bytes_eq(suf, ab + pl + (hi - lo), sl) ? CMP_EQ : CMP_NE;
 }
 
 __device__ __forceinline__ int64_t lookup_key(const paste_tape_node* nodes, int64_t base,
@@ -127,72 +152,154 @@ __device__ __forceinline__ int64_t lookup_key(const paste_tape_node* nodes, int6
   return step_child(nodes, base, 0, 0, key);
 }
 
-__global__ void __launch_bounds__(256) replay_score_kernel(const paste_pool_desc pool,
-                                                           const paste_replay_desc D,
-                                                           const paste_predict_out out) {
-  unsigned long long c1 = 0, c3 = 0, ch = 0, cu = 0;
+// Verdict of candidate i of call c (a FULL candidate of the call's tool with
+// the call's key set): every binding's value must equal the argument.
+__device__ __forceinline__ int candidate_verdict(const paste_pool_desc& pool,
+                                                 const paste_replay_desc& D,
+                                                 const paste_predict_out& out, int64_t c, int i) {
   const int64_t n = D.n_calls;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < n;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    int np = out.n_pred[c];
-    const int lim = D.cand_limit;
-    np = lim >= 0 ? (np < lim ? np : lim) : (np + lim > 0 ? np + lim : 0);
-    const int32_t tool = D.call_tool[c];
-    bool top1 = false, top3 = false, hit = false, unsure = false;
-    const int32_t cks = D.call_keyset[c];
-    const int32_t aev = D.call_args[c];
-    for (int i = 0; i < np && !hit; ++i) {
-      const int64_t o = out_at(out, n, c, i);
-      const int32_t pid = out.pred_pat[o];
-      const paste_pattern pat = pool.patterns[pid];
-      const bool same = pat.target_tool == tool;
-      if (i == 0) top1 = same;
-      if (i < 3) top3 |= same;
-      if (!same || out.pred_comp[o] != PASTE_C_FULL) continue;
-      const int32_t pks = D.pat_keyset[pid];
-      if (cks == -2) continue;                       // args not a dict: never equal
-      if (pks < 0 || cks < 0) { unsure = true; continue; }
-      if (pks != cks) continue;
-      const int nb = (pat.flags & PASTE_PF_HAS_MAPPING) ? pat.n_bind : 0;
-      int verdict = CMP_EQ;
-      for (int b = 0; b < nb && verdict != CMP_NE; ++b) {
-        const int bind = pat.bind_off + b;
-        const int64_t pref = out.pred_arg[arg_at(out, n, c, i, b)];
-        const int64_t an = lookup_key(D.nodes, D.refs[aev].node_base, D.bind_key[bind]);
-        if (pref < 0 || an < 0) { verdict = CMP_UNSURE; continue; }  // FULL + equal key sets
-        const int r = compare_binding(D, bind, pool.bindings[bind].kind, pref, aev, an);
-        if (r == CMP_NE) verdict = CMP_NE;
-        else if (r == CMP_UNSURE) verdict = CMP_UNSURE;
-      }
-      if (verdict == CMP_EQ) hit = true;
-      else if (verdict == CMP_UNSURE) unsure = true;
+  const int32_t pid = out.pred_pat[out_at(out, n, c, i)];
+  const paste_pattern pat = pool.patterns[pid];
+  const int nb = (pat.flags & PASTE_PF_HAS_MAPPING) ? pat.n_bind : 0;
+  const int32_t aev = D.call_args[c];
+  const int64_t abase = D.refs[aev].node_base;
+  int verdict = CMP_EQ;
+  for (int b = 0; b < nb && verdict != CMP_NE; ++b) {
+    const int bind = pat.bind_off + b;
+    const int64_t pref = out.pred_arg[arg_at(out, n, c, i, b)];
+    const int64_t an = lookup_key(D.nodes, abase, D.bind_key[bind]);
+    if (pref < 0 || an < 0) {  // cannot happen for FULL + equal key sets; stay exact
+      verdict = CMP_UNSURE;
+      continue;
     }
-    if (hit) unsure = false;  // (the loop stops at a hit, after top1/top3 are settled)
-    D.unsure[c] = unsure;
-    c1 += top1;
-    c3 += top3;
-    ch += hit;
-    cu += unsure;
+    const int r = compare_binding(D, bind, pool.bindings[bind].kind, pref, aev, an);
+    if (r == CMP_NE) verdict = CMP_NE;
+    else if (r == CMP_UNSURE) verdict = CMP_UNSURE;
   }
-  // block reduction then one atomic per counter per block
-  __shared__ unsigned long long red[4][8];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  return verdict;
+}
+
+// One warp scores 32 calls (lane = call) per iteration.  The cheap part --
+// top1 / top3 and the key-set filter -- runs lane per call; the candidates that
+// need argument comparison go through a per-warp queue in shared memory and
+// are compared one candidate per lane, so lanes stay busy however unevenly
+// the comparisons fall over the calls (a lane-per-call loop ran ~6 of 32
+// lanes active).  Verdicts land in per-warp bit masks (bit = call lane).
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_CHUNK = 8;  // candidate records loaded per round
+
+__global__ void __launch_bounds__(RS_THREADS, 4) replay_score_kernel(const paste_pool_desc pool,
+                                                                  const paste_replay_desc D,
+                                                                  const paste_predict_out out) {
+  __shared__ uint16_t queue[RS_WARPS][32 + RS_CHUNK * 32];
+  __shared__ unsigned hit_mask[RS_WARPS], unsure_mask[RS_WARPS];
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t n = D.n_calls;
+  const int64_t stride = (int64_t)gridDim.x * RS_WARPS * 32;
+  unsigned long long c1 = 0, c3 = 0, ch = 0, cu = 0;
+  for (int64_t base = ((int64_t)blockIdx.x * RS_WARPS + w) * 32; base < n; base += stride) {
+    const int64_t c = base + lane;
+    const bool live = c < n;
+    int np = 0;
+    int32_t tool = -1, cks = -2;
+    if (live) {
+      np = out.n_pred[c];
+      const int lim = D.cand_limit;
+      np = lim >= 0 ? (np < lim ? np : lim) : (np + lim > 0 ? np + lim : 0);
+      tool = D.call_tool[c];
+      cks = D.call_keyset[c];
+    }
+    if (lane == 0) {
+      hit_mask[w] = 0u;
+      unsure_mask[w] = 0u;
+    }
+    __syncwarp();
+    bool top1 = false, top3 = false, unsure = false;
+    int count = 0;
+    const int max_np = __reduce_max_sync(FULL, (unsigned)np);
+    for (int i0 = 0; i0 < max_np; i0 += RS_CHUNK) {
+      // issue the chunk's record loads together (independent, slot-major rows)
+      int32_t pidv[RS_CHUNK];
+      uint8_t compv[RS_CHUNK];
+#pragma unroll
+      for (int j = 0; j < RS_CHUNK; ++j) {
+        pidv[j] = 0;
+        compv[j] = 0xff;
+        if (i0 + j < np) {
+          const int64_t o = out_at(out, n, c, i0 + j);
+          pidv[j] = out.pred_pat[o];
+          compv[j] = out.pred_comp[o];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < RS_CHUNK; ++j) {
+        const int i = i0 + j;
+        bool need = false;
+        if (i < np) {
+          const bool same = __ldg(&pool.patterns[pidv[j]].target_tool) == tool;
+          if (i == 0) top1 = same;
+          if (i < 3) top3 |= same;
+          if (same && compv[j] == PASTE_C_FULL && cks != -2) {  // -2: args not a dict
+            const int32_t pks = __ldg(D.pat_keyset + pidv[j]);
+            if (pks < 0 || cks < 0) unsure = true;
+            else need = pks == cks;
+          }
+        }
+        const unsigned m = __ballot_sync(FULL, need);
+        if (need) queue[w][count + __popc(m & lt)] = (uint16_t)((lane << 8) | i);
+        count += __popc(m);
+      }
+      __syncwarp();
+      // drain full rounds of 32 (one queued candidate per lane); after the
+      // last chunk also the remainder.  Newest entries first, so the kept
+      // ones stay at the front of the queue.
+      const bool last = i0 + RS_CHUNK >= max_np;
+      while (count >= 32 || (last && count > 0)) {
+        const int take = count < 32 ? count : 32;
+        if (lane < take) {
+          const uint16_t it = queue[w][count - take + lane];
+          const int src = it >> 8;
+          const int v = candidate_verdict(pool, D, out, base + src, it & 0xff);
+          if (v == CMP_EQ) atomicOr(&hit_mask[w], 1u << src);
+          else if (v == CMP_UNSURE) atomicOr(&unsure_mask[w], 1u << src);
+        }
+        count -= take;
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+    if (live) {
+      const bool hit = (hit_mask[w] >> lane) & 1u;
+      unsure = (unsure || ((unsure_mask[w] >> lane) & 1u)) && !hit;
+      D.unsure[c] = unsure;
+      c1 += top1;
+      c3 += top3;
+      ch += hit;
+      cu += unsure;
+    }
+    __syncwarp();
+  }
+  // block reduction, one atomic per counter per block
+  __shared__ unsigned long long red[4][RS_WARPS];
   for (int off = 16; off; off >>= 1) {
-    c1 += __shfl_down_sync(0xffffffffu, c1, off);
-    c3 += __shfl_down_sync(0xffffffffu, c3, off);
-    ch += __shfl_down_sync(0xffffffffu, ch, off);
-    cu += __shfl_down_sync(0xffffffffu, cu, off);
+    c1 += __shfl_down_sync(FULL, c1, off);
+    c3 += __shfl_down_sync(FULL, c3, off);
+    ch += __shfl_down_sync(FULL, ch, off);
+    cu += __shfl_down_sync(FULL, cu, off);
   }
   if (lane == 0) {
-    red[0][wid] = c1;
-    red[1][wid] = c3;
-    red[2][wid] = ch;
-    red[3][wid] = cu;
+    red[0][w] = c1;
+    red[1][w] = c3;
+    red[2][w] = ch;
+    red[3][w] = cu;
   }
   __syncthreads();
   if (threadIdx.x < 4) {
     unsigned long long s = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[threadIdx.x][w];
+    for (int k = 0; k < RS_WARPS; ++k) s += red[threadIdx.x][k];
     if (s) atomicAdd(reinterpret_cast<unsigned long long*>(D.tallies) + threadIdx.x, s);
   }
 }
@@ -201,49 +308,31 @@ __global__ void __launch_bounds__(256) replay_score_kernel(const paste_pool_desc
 
 using namespace paste;
 
-extern "C" int64_t paste_replay_scratch_bytes(int64_t n_calls, int32_t capacity) {
-  if (n_calls < 0 || capacity < 1) return -1;
-  const int64_t ring = ((n_calls * capacity * 4 + 255) / 256) * 256;
-  return 2 * ring + ((n_calls * 8 + 255) / 256) * 256;
-}
-
 extern "C" int paste_replay_score(const paste_pool_desc* pool, const paste_replay_desc* d,
-                                  paste_predict_out* out, void* scratch, void* stream) {
+                                  paste_predict_out* out, void* stream) {
   reset_launches();
   PASTE_REQUIRE(pool && d && out, "null descriptor");
   PASTE_REQUIRE(d->capacity >= 1, "window capacity must be >= 1");
   if (d->n_calls == 0) return PASTE_OK;
-  PASTE_REQUIRE(scratch != nullptr, "null scratch");
   const cudaStream_t st = (cudaStream_t)stream;
-  const int64_t ring = ((d->n_calls * d->capacity * 4 + 255) / 256) * 256;
-  uint8_t* s = static_cast<uint8_t*>(scratch);
-  int32_t* tok = reinterpret_cast<int32_t*>(s);
-  int32_t* evt = reinterpret_cast<int32_t*>(s + ring);
-  int64_t* count = reinterpret_cast<int64_t*>(s + 2 * ring);
-  const int threads = 256;
-  int64_t blocks = (d->n_calls * d->capacity + threads - 1) / threads;
-  if (blocks > 148 * 32) blocks = 148 * 32;
-  replay_windows_kernel<<<(unsigned)blocks, threads, 0, st>>>(*d, tok, evt, count);
-  PASTE_CUDA_CHECK(cudaGetLastError());
-
   paste_windows win{};
   win.n_sessions = d->n_calls;
   win.capacity = d->capacity;
-  win.slot_major = 1;
-  win.tok = tok;
-  win.evt = evt;
-  win.count = count;
+  win.tok = const_cast<int32_t*>(d->ev_tok);  // read-only in stream mode
+  win.evt = const_cast<int32_t*>(d->ev_evt);
+  win.count = const_cast<int64_t*>(d->call_len);
+  win.stream_end = d->call_pos;
   win.nodes = d->nodes;
   win.bytes = d->bytes;
-  win.refs = const_cast<paste_event_ref*>(d->refs);  // read-only: no observe step
+  win.refs = const_cast<paste_event_ref*>(d->refs);
+  PASTE_REQUIRE(out->max_candidates <= 256, "replay supports at most 256 candidates per call");
   paste_admit_desc adm{};
   const int rc = paste_predict_batch(pool, &win, &adm, out, stream);
   if (rc != PASTE_OK) return rc;
-
-  blocks = (d->n_calls + threads - 1) / threads;
+  int64_t blocks = (d->n_calls + RS_THREADS - 1) / RS_THREADS;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  replay_score_kernel<<<(unsigned)blocks, threads, 0, st>>>(*pool, *d, *out);
+  replay_score_kernel<<<(unsigned)blocks, RS_THREADS, 0, st>>>(*pool, *d, *out);
   PASTE_CUDA_CHECK(cudaGetLastError());
-  count_launch(2);  // + the K4 launches counted by paste_predict_batch
+  count_launch(1);  // + the K4 launches counted by paste_predict_batch
   return PASTE_OK;
 }

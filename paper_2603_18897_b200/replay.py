@@ -5,9 +5,9 @@ after a session's first it predicts from the window of preceding events
 (LLM steps take window slots), then tallies top-1, top-3 and "hit" -- some
 FULL prediction of the call's tool whose ``canonical_arg_hash`` equals the
 call's.  Here the corpus is one event stream in HBM (tokens, payload
-indices, the calls' argument tapes) and ``paste_replay_score`` gathers every
-call's window, runs K4 on all of them and tallies the three counts on the
-device.  Hit checks that need Unicode or container semantics come back
+indices, the calls' argument tapes) and ``paste_replay_score`` runs K4 on
+every call's window -- read in place from the stream -- and tallies the
+three counts on the device.  Hit checks that need Unicode or container semantics come back
 "unsure" and are decided on the host with the reference's hash, so the
 report is exact.
 """
@@ -25,6 +25,7 @@ from ._native import PredictOut, ReplayDesc, check, ptr
 from .mappings import FormatTemplate
 
 INT32_MAX = 2**31 - 1
+FMT_NON_ASCII = 0x100  # PASTE_FMT_NON_ASCII
 _NORM_CODE = {"none": 0, "trim": 1, "lowercase": 2}
 
 
@@ -63,8 +64,9 @@ def pool_hit_tables(dp, ksets: KeysetTable):
             if isinstance(b.expr, FormatTemplate):
                 pre = b.expr.prefix.encode("utf-8", "surrogatepass")
                 suf = b.expr.suffix.encode("utf-8", "surrogatepass")
+                flag = 0 if (pre + suf).isascii() else FMT_NON_ASCII
                 fmt += [len(fbytes), len(pre), len(fbytes) + len(pre), len(suf),
-                        _NORM_CODE[b.expr.normalization.value]]
+                        _NORM_CODE[b.expr.normalization.value] | flag]
                 fbytes += pre + suf
             else:
                 fmt += [0, 0, 0, 0, 0]
@@ -79,7 +81,7 @@ class ReplayCorpus:
     ev_tok: np.ndarray      # i32[E] sig, -1 = LLM step
     ev_evt: np.ndarray      # i32[E] result payload index, -1 for LLM steps
     call_pos: np.ndarray    # i64[C] stream index of each scored call
-    call_len: np.ndarray    # i32[C] window length
+    call_len: np.ndarray    # i64[C] window length
     call_tool: np.ndarray   # i32[C] tool id
     call_args: np.ndarray   # i32[C] args payload index
     call_keyset: np.ndarray # i32[C]
@@ -130,7 +132,7 @@ def corpus_from_traces(traces, dp, window_capacity: int, ksets: KeysetTable):
     nodes, data, refs = arena.arrays()
     corpus = ReplayCorpus(
         np.array(ev_tok or [-1], np.int32), np.array(ev_evt or [-1], np.int32),
-        np.array(calls, np.int64), np.array(call_len, np.int32),
+        np.array(calls, np.int64), np.array(call_len, np.int64),
         np.array([dp.sigs.tool(e.tool_type) for e in actual], np.int32),
         np.array(call_args, np.int32), np.array(call_ks, np.int32), nodes, data, refs)
     return corpus, actual, arena
@@ -169,10 +171,8 @@ class ReplayBatch:
                   "struct_err": torch.zeros(m, dtype=torch.int32, device=dev)}
         self.tallies = torch.zeros(4, dtype=torch.int64, device=dev)
         self.unsure = torch.zeros(m, dtype=torch.uint8, device=dev)
-        nbytes = self.lib.paste_replay_scratch_bytes(n, window_capacity)
-        if nbytes < 0:
+        if window_capacity < 1:
             raise ValueError("window capacity must be >= 1")
-        self.scratch = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
         o = self.o
         self.out = PredictOut(self.K, self.B, 1, 0, ptr(o["n_pred"]), ptr(o["pred_pat"]),
                               ptr(o["pred_comp"]), ptr(o["pred_arg"]), 0, 0, 0, 0,
@@ -197,8 +197,7 @@ class ReplayBatch:
 
         self.tallies.zero_()
         check(self.lib.paste_replay_score(ctypes.byref(self.pool_desc), ctypes.byref(self.desc),
-                                          ctypes.byref(self.out), ptr(self.scratch),
-                                          stream_handle() if stream is None else stream), self.lib)
+                                          ctypes.byref(self.out), stream_handle() if stream is None else stream), self.lib)
 
     def launch_count(self) -> int:
         return int(self.lib.paste_last_launch_count())

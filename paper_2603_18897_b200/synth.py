@@ -482,7 +482,7 @@ def coding_replay_corpus(dp, n_sessions: int, window_capacity: int = 16, seed: i
     sk = call_kind[scored]
     return ReplayCorpus(
         ev_tok=ev_tok, ev_evt=ev_evt, call_pos=tool_pos[scored].astype(np.int64),
-        call_len=np.minimum(window_capacity, 2 * j[scored] + 1).astype(np.int32),
+        call_len=np.minimum(window_capacity, 2 * j[scored] + 1).astype(np.int64),
         call_tool=(tool_ids[sk] >> 1).astype(np.int32),
         call_args=(T + np.arange(C)).astype(np.int32), call_keyset=keysets[sk],
         nodes=tmpl.nodes, data=np.concatenate(blocks) if blocks else np.zeros(1, np.uint8),

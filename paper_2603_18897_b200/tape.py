@@ -41,7 +41,7 @@ NODE_DTYPE = np.dtype([("type", "u1"), ("flags", "u1"), ("pad", "u2"),
 assert NODE_DTYPE.itemsize == 16
 
 T_NULL, T_FALSE, T_TRUE, T_INT, T_FLOAT, T_STR, T_LIST, T_DICT = range(8)
-F_NFC, F_FLOATSRC, F_NAN = 1, 2, 4
+F_NFC, F_FLOATSRC, F_NAN, F_ASCII = 1, 2, 4, 8
 
 
 class KeyTable:
@@ -75,12 +75,14 @@ def scalar_bytes(value: Any) -> tuple[int, int, bytes]:
     if isinstance(value, bool):  # numpy bools etc.
         return (T_TRUE if value else T_FALSE), 0, b""
     if isinstance(value, int):
-        return T_INT, 0, str(int(value)).encode()
+        return T_INT, F_ASCII, str(int(value)).encode()
     if isinstance(value, float):
         if value.is_integer():
-            return T_INT, F_FLOATSRC, str(int(value)).encode()
-        return T_FLOAT, (F_NAN if value != value else 0), repr(value).encode()
+            return T_INT, F_FLOATSRC | F_ASCII, str(int(value)).encode()
+        return T_FLOAT, (F_NAN if value != value else 0) | F_ASCII, repr(value).encode()
     if isinstance(value, str):
+        if value.isascii():
+            return T_STR, F_ASCII, value.encode()
         raw = value.encode("utf-8", "surrogatepass")
         nfc = unicodedata.normalize("NFC", value)
         if nfc != value:

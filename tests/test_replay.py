@@ -62,6 +62,10 @@ def test_coding_corpus_shape():
     assert ((c.ev_tok[c.call_pos - c.call_len] == -1)).all()  # windows start at an LLM step
     top1, top3, hits, n = bridge.score_corpus(dp.image, c, dp.keys, 16, 8)
     assert n == c.n_calls and hits > 0 and top3 >= top1
+    # stream-mode windows (read in place) == gathered rings
+    assert bridge.score_corpus(dp.image, c, dp.keys, 16, 8, stream=False) == (top1, top3, hits, n)
+    assert bridge.score_corpus(dp.image, c, dp.keys, 3, None, calls=slice(100, 900)) == \
+        bridge.score_corpus(dp.image, c, dp.keys, 3, None, calls=slice(100, 900), stream=False)
 
 
 @pytest.mark.gpu
@@ -129,3 +133,71 @@ def test_device_replay_unsure_calls_go_to_the_host():
     rep = score_accuracy(sessions, pool, window_capacity=16)
     assert rep.to_json() == _report(*expect)
     assert 0 < expect[2] < 40
+
+
+@pytest.mark.gpu
+def test_device_hit_check_fuzz_matches_oracle():
+    """Word-wise byte comparison at every length / alignment, lowercase and
+    strip normalizations, numbers vs strings, near-miss mutations."""
+    import random
+
+    from paper_2603_18897_b200.events import Event, EventKind, EventSignature, Session, Status
+    from paper_2603_18897_b200.mappings import (ArgBinding, FormatTemplate, Normalization,
+                                                PathLookup, ValueMapping)
+    from paper_2603_18897_b200.mining import MiningConfig, PatternPool, PatternTuple
+    from paper_2603_18897_b200.replay import ReplayBatch
+
+    S = Status.SUCCESS
+    rng = random.Random(7)
+    alphabet = "abcXYZ019 _-/."
+
+    def mutate(s):
+        r = rng.random()
+        if r < 0.5 or not s:
+            return s
+        if r < 0.7:
+            i = rng.randrange(len(s))
+            return s[:i] + ("q" if s[i] != "q" else "r") + s[i + 1:]
+        if r < 0.85:
+            return s + "z"
+        return s[:-1]
+
+    def mapping(norm, pre, suf):
+        return ValueMapping((ArgBinding("a", PathLookup(0, ("v",))),
+                             ArgBinding("b", FormatTemplate(pre, PathLookup(0, ("v",)), suf, norm))))
+
+    pats = (PatternTuple((EventSignature("t0", S),), "t1", mapping(Normalization.LOWERCASE, "P:", ""), 0.9, 5),
+            PatternTuple((EventSignature("t0", S),), "t2", mapping(Normalization.TRIM, "", "?x=1"), 0.8, 5),
+            PatternTuple((EventSignature("t0", S),), "t3", mapping(Normalization.NONE, "pre ", " suf"), 0.7, 5))
+    pool = PatternPool(MiningConfig(k=1), pats)
+    norms = {"t1": lambda s: "P:" + s.lower(), "t2": lambda s: s.strip() + "?x=1",
+             "t3": lambda s: "pre " + s + " suf"}
+    sessions = []
+    for i in range(3000):
+        kind = rng.random()
+        if kind < 0.8:
+            v = "".join(rng.choice(alphabet) for _ in range(rng.randrange(0, 41)))
+        elif kind < 0.9:
+            v = rng.randrange(-10**6, 10**6)
+        else:
+            v = rng.choice([1.5, 2.0, -0.25, True, None])
+        tgt = rng.choice(["t1", "t2", "t3"])
+        a_val = mutate(v) if isinstance(v, str) else (v if rng.random() < 0.7 else str(v))
+        text = v if isinstance(v, str) else (str(int(v)) if isinstance(v, float) and v.is_integer()
+                                             else str(v))
+        b_val = mutate(norms[tgt](text)) if isinstance(v, (str, int, float)) and v is not True \
+            else "P:true"
+        evs = [Event(f"s{i}", 0, EventKind.TOOL_CALL, "t0", S, {}, {"v": v}, 0, 1),
+               Event(f"s{i}", 1, EventKind.LLM_STEP, "", S, None, None, 1, 2),
+               Event(f"s{i}", 2, EventKind.TOOL_CALL, tgt, S, {"a": a_val, "b": b_val}, None, 2, 3)]
+        sessions.append(Session(f"s{i}", tuple(evs)))
+    dp = DevicePool(pool)
+    ks = KeysetTable()
+    corpus, _, _ = corpus_from_traces(sessions, dp, 16, ks)
+    rb = ReplayBatch(dp, corpus, 16, 3, ks)
+    rb.launch()
+    top1, top3, hits, unsure = rb.tallies.cpu().numpy().tolist()
+    assert unsure == 0
+    expect = bridge.score_corpus(dp.image, corpus, dp.keys, 16, 3)
+    assert (top1, top3, hits, corpus.n_calls) == expect
+    assert 200 < hits < 2800
