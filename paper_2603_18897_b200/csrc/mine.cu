@@ -318,11 +318,19 @@ extern "C" int paste_mine_select(const paste_mine_desc* d, int64_t sigma, double
 // counted (the host rejects unsorted input).  Each CTA stages a tile of
 // events plus a (k+1)-event halo in shared memory with coalesced loads.
 // ---------------------------------------------------------------------------
-constexpr int CT = 256;                 // threads
-constexpr int CTILE = 512;              // events per tile
+// Pipeline: one producer warp streams tiles of CTILE events (five columns,
+// TMA bulk copies) into CNST shared-memory stages guarded by full / empty
+// mbarriers; CW consumer warps each take 32 consecutive events at a time
+// (lane = event).  Segment flags and the (k+1)-gram window come from warp
+// shuffles (lanes 0..k-1 also compute the k events before the chunk, lane 31
+// the flag of the event after it), so consumers never wait on each other:
+// there is no __syncthreads in the steady state.
+constexpr int CW = 8;                   // consumer warps
+constexpr int CT = 32 * (CW + 1);       // + one producer warp
+constexpr int CTILE = 512;              // events per tile (= 2 chunks of 32 per consumer warp)
 constexpr int CPRE = 8;                 // halo before the tile (>= k + 1, 16-B aligned)
 constexpr int CSPAN = CTILE + 16;       // staged events per tile (halo + 1 after, padded)
-constexpr int CSTAGES = 2;
+constexpr int CNST = 4;                 // pipeline stages
 constexpr int CHASH = 2048;             // per-CTA heavy-hitter table (keys, counts)
 constexpr uint32_t HEMPTY = 0xffffffffu;
 
@@ -351,7 +359,6 @@ struct __align__(16) ColumnTile {
   int32_t sess[CSPAN];
   int32_t seq[CSPAN];
   int32_t sig[CSPAN];
-  uint32_t v[CSPAN];  // sig | segment-start flag << 31 (computed)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -364,6 +371,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -383,28 +393,47 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Issue the bulk copies for tile `t` into `T`; returns the staged range.
-__device__ __forceinline__ void stage_tile(const paste_columnar_desc& C, int64_t t, ColumnTile* T,
-                                           uint64_t* bar) {
+// Producer warp: fill stage T with tile t.  The 16-byte-granular part goes by
+// bulk copy; the last < 4 events of the trace (arrays need not be padded) are
+// stored by the lanes before lane 0's arrive releases them with the copy.
+__device__ __forceinline__ void produce_tile(const paste_columnar_desc& C, int64_t t, ColumnTile* T,
+                                             uint64_t* full, int lane) {
   const int64_t n = C.n_events;
   const int64_t g0 = t * CTILE - CPRE;
   const int64_t lo = g0 < 0 ? 0 : g0;
   int64_t hi = g0 + CSPAN;
   if (hi > n) hi = n;
-  int64_t cnt = hi - lo;
-  cnt &= ~(int64_t)3;  // 16-byte granularity; the tail (< 4 events) is loaded by threads
-  const int off = (int)(lo - g0);
-  if (cnt > 0) {
-    const uint32_t b4 = (uint32_t)cnt * 4, b8 = (uint32_t)cnt * 8;
-    mbar_expect_tx(bar, 3 * b4 + 2 * b8);
-    bulk_g2s(T->ts + off, C.t_start + lo, b8, bar);
-    bulk_g2s(T->te + off, C.t_end + lo, b8, bar);
-    bulk_g2s(T->sess + off, C.session + lo, b4, bar);
-    bulk_g2s(T->seq + off, C.seq + lo, b4, bar);
-    bulk_g2s(T->sig + off, C.sig + lo, b4, bar);
-  } else {
-    mbar_expect_tx(bar, 0);
+  const int64_t cnt = (hi - lo) & ~(int64_t)3;
+  for (int64_t x = lo + cnt + lane; x < hi; x += 32) {
+    const int l = (int)(x - g0);
+    T->ts[l] = C.t_start[x];
+    T->te[l] = C.t_end[x];
+    T->sess[l] = C.session[x];
+    T->seq[l] = C.seq[x];
+    T->sig[l] = C.sig[x];
   }
+  __syncwarp();
+  if (lane == 0) {
+    const int off = (int)(lo - g0);
+    const uint32_t b4 = (uint32_t)cnt * 4, b8 = (uint32_t)cnt * 8;
+    mbar_expect_tx(full, cnt > 0 ? 3 * b4 + 2 * b8 : 0);
+    if (cnt > 0) {
+      bulk_g2s(T->ts + off, C.t_start + lo, b8, full);
+      bulk_g2s(T->te + off, C.t_end + lo, b8, full);
+      bulk_g2s(T->sess + off, C.session + lo, b4, full);
+      bulk_g2s(T->seq + off, C.seq + lo, b4, full);
+      bulk_g2s(T->sig + off, C.sig + lo, b4, full);
+    }
+  }
+}
+
+// v(l) = sig | segment-start flag << 31 for staged slot l (event g0 + l).
+// Events before the trace start or past its end read as segment starts.
+__device__ __forceinline__ uint32_t slot_word(const ColumnTile* T, int l, int64_t x, int64_t n,
+                                              double gap) {
+  if (x <= 0 || x >= n) return (x == 0 ? (uint32_t)T->sig[l] : 0u) | SEG_START;
+  const bool b = (T->sess[l] != T->sess[l - 1]) || (__dsub_rn(T->ts[l], T->te[l - 1]) > gap);
+  return (uint32_t)T->sig[l] | (b ? SEG_START : 0u);
 }
 
 template <int K, bool WRITE_TOK>
@@ -413,104 +442,103 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
                                                             int32_t* __restrict__ tok_out) {
   extern __shared__ __align__(16) uint8_t c_smem[];
   ColumnTile* tiles = reinterpret_cast<ColumnTile*>(c_smem);
-  uint32_t* hkey = reinterpret_cast<uint32_t*>(tiles + CSTAGES);
+  uint32_t* hkey = reinterpret_cast<uint32_t*>(tiles + CNST);
   uint32_t* hcnt = hkey + CHASH;
-  __shared__ uint64_t bars[CSTAGES];
+  __shared__ uint64_t full[CNST], empty[CNST];
   for (int i = threadIdx.x; i < CHASH; i += CT) {
     hkey[i] = HEMPTY;
     hcnt[i] = 0;
   }
-  const int64_t n = C.n_events;
-  const int64_t n_tiles = (n + CTILE - 1) / CTILE;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < CSTAGES; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < CNST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CW);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  int64_t t = blockIdx.x;
-  if (threadIdx.x == 0 && t < n_tiles) stage_tile(C, t, &tiles[0], &bars[0]);
+  const int64_t n = C.n_events;
+  const int64_t n_tiles = (n + CTILE - 1) / CTILE;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned long long segs = 0, bad = 0;
-  for (int it = 0; t < n_tiles; ++it, t += gridDim.x) {
-    const int st = it & 1;
-    ColumnTile* T = &tiles[st];
-    // prefetch the next tile into the other stage (freed by the previous sync)
-    const int64_t tn = t + gridDim.x;
-    if (threadIdx.x == 0 && tn < n_tiles) stage_tile(C, tn, &tiles[st ^ 1], &bars[st ^ 1]);
-    if (threadIdx.x < 32) mbar_wait(&bars[st], (it >> 1) & 1);  // one warp spins
-    const int64_t g0 = t * CTILE - CPRE;
-    // tail events not covered by the 16-byte-granular bulk copy
-    {
-      const int64_t lo = g0 < 0 ? 0 : g0;
-      int64_t hi = g0 + CSPAN;
-      if (hi > n) hi = n;
-      const int64_t bulk_hi = lo + ((hi - lo) & ~(int64_t)3);
-      for (int64_t x = bulk_hi + threadIdx.x; x < hi; x += CT) {
-        const int l = (int)(x - g0);
-        T->ts[l] = C.t_start[x];
-        T->te[l] = C.t_end[x];
-        T->sess[l] = C.session[x];
-        T->seq[l] = C.seq[x];
-        T->sig[l] = C.sig[x];
-      }
+  if (warp == CW) {
+    // ---- producer ----------------------------------------------------------
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      const int st = it % CNST;
+      if (it >= CNST) mbar_wait(&empty[st], ((it / CNST) - 1) & 1);
+      produce_tile(C, t, &tiles[st], &full[st], lane);
     }
-    __syncthreads();
-    // segment-start flags packed with the sig; order checks for the tile's own events
-    for (int l = 1 + threadIdx.x; l < CSPAN; l += CT) {
-      const int64_t x = g0 + l;
-      uint32_t b = 1;
-      if (x > 0 && x < n) {
-        const int32_t ss = T->sess[l], ps = T->sess[l - 1];
-        const double ts = T->ts[l];
-        b = (ss != ps) || (__dsub_rn(ts, T->te[l - 1]) > C.inactivity_ms);
-        if (l >= CPRE && l < CPRE + CTILE) {
-          const double pts = T->ts[l - 1];
+  } else {
+    // ---- consumers ---------------------------------------------------------
+    const uint32_t S = (uint32_t)g.S, base = (uint32_t)g.base;
+    const double gap = C.inactivity_ms;
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+      const int st = it % CNST;
+      const ColumnTile* T = &tiles[st];
+      mbar_wait(&full[st], (it / CNST) & 1);
+      const int64_t g0 = t * CTILE - CPRE;
+#pragma unroll
+      for (int j = 0; j < CTILE / (32 * CW); ++j) {
+        const int l0 = CPRE + (j * CW + warp) * 32;  // chunk's first slot
+        const int l = l0 + lane;
+        const int64_t x = g0 + l;
+        const uint32_t v = slot_word(T, l, x, n, gap);
+        // the k words before the chunk (lane d-1 holds slot l0 - d) and the
+        // flag of the slot after it (lane 31)
+        uint32_t h = 0;
+        if (lane < K) h = slot_word(T, l0 - 1 - lane, g0 + l0 - 1 - lane, n, gap);
+        if (lane == 31) h = slot_word(T, l + 1, x + 1, n, gap);
+        uint32_t w[K + 1];
+        w[0] = v;
+#pragma unroll
+        for (int d = 1; d <= K; ++d) {
+          const uint32_t a = __shfl_up_sync(0xffffffffu, v, d);
+          const uint32_t b = __shfl_sync(0xffffffffu, h, (d - lane - 1) & 31);
+          w[d] = lane >= d ? a : b;
+        }
+        const uint32_t nx = __shfl_down_sync(0xffffffffu, v, 1);
+        if (x >= n) continue;  // past the trace end (after the shuffles)
+        const bool last = (lane == 31 ? h : nx) >> 31;
+        // gram ending at x: BEGIN once a segment start has been passed
+        uint32_t key = w[0] & 0x7fffffffu, mult = base, kend = S + 1, mul2 = base;
+        bool stop = w[0] >> 31, stop2 = false;
+#pragma unroll
+        for (int d = 1; d <= K; ++d) {
+          key += (stop ? S : (w[d] & 0x7fffffffu)) * mult;
+          stop = stop || (w[d] >> 31);
+          mult *= base;
+          // END gram: positions x-(d-1)
+          kend += (stop2 ? S : (w[d - 1] & 0x7fffffffu)) * mul2;
+          stop2 = stop2 || (w[d - 1] >> 31);
+          mul2 *= base;
+        }
+        hh_add(hkey, hcnt, hist, key, 1u);
+        segs += last;
+        if (last) hh_add(hkey, hcnt, hist, kend, 1u);
+        if (x > 0) {  // order check (the host rejects unsorted traces)
+          const int32_t ss = T->sess[l], ps = T->sess[l - 1];
+          const double ts = T->ts[l], pts = T->ts[l - 1];
           const bool back = (ts < pts) | ((ts == pts) & (T->seq[l] <= T->seq[l - 1]));
           bad += (ss < ps) | ((ss == ps) & back);
         }
+        if (WRITE_TOK) tok_out[x] = (int32_t)v;
       }
-      T->v[l] = (uint32_t)T->sig[l] | (b << 31);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
     }
-    __syncthreads();
-    const uint32_t S = (uint32_t)g.S, base = (uint32_t)g.base;
-    const int valid_hi = (int)((n - g0) < (int64_t)CSPAN ? (n - g0) : (int64_t)CSPAN);  // slots < valid_hi hold events
-    for (int j = 0; j < CTILE / CT; ++j) {
-      const int li = CPRE + j * CT + threadIdx.x;
-      if (li >= valid_hi) continue;
-      // the window words are independent loads (no dependent walk-back chain)
-      uint32_t w[K + 1];
-#pragma unroll
-      for (int d = 0; d <= K; ++d) w[d] = T->v[li - d];
-      const bool last = (li + 1 == valid_hi) || (T->v[li + 1] >> 31);
-      // gram ending at x: BEGIN once a segment start has been passed
-      uint32_t key = w[0] & 0x7fffffffu, mult = base, kend = S + 1, mul2 = base;
-      bool stop = w[0] >> 31, stop2 = false;
-#pragma unroll
-      for (int d = 1; d <= K; ++d) {
-        key += (stop ? S : (w[d] & 0x7fffffffu)) * mult;
-        stop = stop || (w[d] >> 31);
-        mult *= base;
-        // END gram: positions x-(d-1)
-        kend += (stop2 ? S : (w[d - 1] & 0x7fffffffu)) * mul2;
-        stop2 = stop2 || (w[d - 1] >> 31);
-        mul2 *= base;
-      }
-      hh_add(hkey, hcnt, hist, key, 1u);
-      segs += last;
-      if (last) hh_add(hkey, hcnt, hist, kend, 1u);
-      if (WRITE_TOK) tok_out[g0 + li] = (int32_t)(w[0] & 0x7fffffffu) | ((w[0] >> 31) ? (int32_t)SEG_START : 0);
-    }
-    __syncthreads();  // stage `st` is free for the prefetch two iterations on
   }
   // flush the heavy-hitter table
   __syncthreads();
   for (int i = threadIdx.x; i < CHASH; i += CT)
     if (hkey[i] != HEMPTY) atomicAdd(hist + hkey[i], hcnt[i]);
-  // block-reduce the counters
+  // warp-reduce the counters
   for (int o = 16; o > 0; o >>= 1) {
     segs += __shfl_xor_sync(0xffffffffu, segs, o);
     bad += __shfl_xor_sync(0xffffffffu, bad, o);
   }
-  if ((threadIdx.x & 31) == 0) {
+  if (lane == 0) {
     if (C.n_segments && segs) atomicAdd(reinterpret_cast<unsigned long long*>(C.n_segments), segs);
     if (C.n_unsorted && bad) atomicAdd(reinterpret_cast<unsigned long long*>(C.n_unsorted), bad);
   }
@@ -547,7 +575,7 @@ extern "C" int paste_mine_ingest_count(const paste_columnar_desc* c, const paste
   const uintptr_t mis = (uintptr_t)c->session | (uintptr_t)c->seq | (uintptr_t)c->t_start |
                         (uintptr_t)c->t_end | (uintptr_t)c->sig;
   PASTE_REQUIRE((mis & 15) == 0, "columnar arrays must be 16-byte aligned");
-  const size_t smem = sizeof(ColumnTile) * CSTAGES + 2 * CHASH * sizeof(uint32_t);
+  const size_t smem = sizeof(ColumnTile) * CNST + 2 * CHASH * sizeof(uint32_t);
   const int64_t tiles = (c->n_events + CTILE - 1) / CTILE;
   const bool wt = c->tokens_out != nullptr;
   int rc = -1;
