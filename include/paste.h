@@ -267,6 +267,17 @@ int paste_mine_expand(const paste_mine_desc* d, void* stream);
 int paste_mine_select(const paste_mine_desc* d, int64_t sigma, double tau, int64_t cap,
                       uint64_t* n_out, int64_t* out, void* stream);
 
+/* Mapping-free selection in mine()'s output order (mining.py:105-111):
+ * rows (tool, context index, support, match, follow, p as f64 bits) of the
+ * pairs with tool_count >= sigma, support >= sigma, match > 0 and
+ * p = follow / match >= tau, sorted by (-p, -len, target, context).  *n_out
+ * receives the number found (only the first `cap` are ranked and written:
+ * callers retry with a larger cap when *n_out > cap).  `scratch` is device
+ * memory of paste_mine_sort_scratch_bytes(cap) bytes.                      */
+int64_t paste_mine_sort_scratch_bytes(int64_t cap);
+int paste_mine_select_sorted(const paste_mine_desc* d, int64_t sigma, double tau, int64_t cap,
+                             uint64_t* n_out, int64_t* out, void* scratch, void* stream);
+
 /* K1 + K2 fused over a columnar trace of tool events grouped by session
  * (sessions in first-appearance order, events sorted by (t_start, seq)):
  * segments split where t_start - prev.t_end > inactivity_ms (events.py:

@@ -164,6 +164,9 @@ EXPORTS = {
     "paste_mine_expand": (c_int, [POINTER(MineDesc), c_void_p]),
     "paste_mine_select": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64, c_void_p,
                                   c_void_p, c_void_p]),
+    "paste_mine_sort_scratch_bytes": (c_int64, [c_int64]),
+    "paste_mine_select_sorted": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64,
+                                         c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 
 _lib = None

@@ -95,91 +95,188 @@ __global__ void __launch_bounds__(MT) count_grams_kernel(const uint32_t* __restr
 }
 
 // ---------------------------------------------------------------------------
-// expand: non-zero (k+1)-gram bins -> tool_count / support / match / follow
+// expand: (k+1)-gram histogram -> tool_count / support / match / follow
+//
+// One warp per *window* w = (s_k .. s_1) (the k symbols before the target),
+// lanes over the target symbol s_0: the histogram row H[w][*] is contiguous
+// (key = s_0 + base * w), so a warp reads it with one coalesced load and every
+// table update of the window is aggregated across lanes first:
+//   * support[t][c] += sum_{s_0 in tool t} H   for each distinct subsequence c
+//     of the window (or suffix, contiguous relation);
+//   * match[c]      += sum_{all s_0} H        for each context c matching at
+//     the anchor s_1 (distinct subsequence of (s_k..s_2) + s_1);
+//   * follow[c][t]  += sum_{s_0 in tool t} H   for the same contexts.
+// Distinct subsequences are enumerated as index masks and kept only in their
+// leftmost embedding (each chosen position is the first occurrence of its
+// symbol after the previous chosen one), which lists each distinct
+// subsequence exactly once without comparing masks.  Length-1 contexts and
+// tool_count (hit by every window) accumulate in shared memory per CTA.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int distinct_subseqs(const int* w, int n, int* out, int* out_len,
-                                                int max_out, bool include_empty, int maxlen) {
-  // all order-preserving subsequences of w (length n), deduplicated
-  int cnt = 0;
-  for (int mask = include_empty ? 0 : 1; mask < (1 << n); ++mask) {
-    int c[8], len = 0;
-    for (int i = 0; i < n; ++i)
-      if (mask & (1 << i)) c[len++] = w[i];
-    bool dup = false;
-    for (int q = 0; q < cnt && !dup; ++q) {
-      if (out_len[q] != len) continue;
-      bool same = true;
-      for (int i = 0; i < len; ++i) same &= out[q * maxlen + i] == c[i];
-      dup = same;
-    }
-    if (dup || cnt >= max_out) continue;
-    for (int i = 0; i < len; ++i) out[cnt * maxlen + i] = c[i];
-    out_len[cnt++] = len;
-  }
-  return cnt;
-}
+constexpr int XT = 256;                 // threads per expand CTA
+constexpr int XSMEM_CELLS = 4096;       // u64 cells for the length-1 / tool caches
 
-__global__ void expand_grams_kernel(const uint32_t* __restrict__ hist, MineGeom g, int relation,
-                                    unsigned long long* tool_count, unsigned long long* support,
-                                    unsigned long long* match, unsigned long long* follow) {
-  const int64_t key = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (key >= g.n_bins) return;
-  const uint32_t h = hist[key];
-  if (h == 0) return;
-  int sym[17];  // sym[d] = s_{j-d}
-  {
-    int64_t k2 = key;
-    for (int d = 0; d <= g.k; ++d) {
-      sym[d] = (int)(k2 % g.base);
-      k2 /= g.base;
-    }
-  }
-  const int BEGIN = g.S, END = g.S + 1;
-  const int s0 = sym[0];
-  // window before target j: (s_{j-k}..s_{j-1}) minus BEGINs, oldest first
-  int win[16], wl = 0;
-  for (int d = g.k; d >= 1; --d)
-    if (sym[d] != BEGIN) win[wl++] = sym[d];
-  int subs[64 * 6], sub_len[64];  // k <= 6: at most 2^6 subsequences
-  if (s0 != END) {  // target occurrence
-    const int tool = s0 >> 1;
-    atomicAdd(tool_count + tool, (unsigned long long)h);
-    if (relation == PASTE_REL_ANCHORED) {
-      const int ns = distinct_subseqs(win, wl, subs, sub_len, 64, false, 6);
-      for (int q = 0; q < ns; ++q)
-        atomicAdd(support + (int64_t)tool * g.n_ctx + ctx_index(g, subs + q * 6, sub_len[q]),
-                  (unsigned long long)h);
-    } else {
-      for (int st = 0; st < wl; ++st)
-        atomicAdd(support + (int64_t)tool * g.n_ctx + ctx_index(g, win + st, wl - st),
-                  (unsigned long long)h);
-    }
-  }
-  if (sym[1] == BEGIN || sym[1] == END) return;  // no anchor at j-1
-  // anchor a = j-1; previous k-1 events (s_{j-k}..s_{j-2}) minus BEGINs
-  int prev[16], pl = 0;
-  for (int d = g.k; d >= 2; --d)
-    if (sym[d] != BEGIN) prev[pl++] = sym[d];
-  const int follow_tool = s0 != END ? (s0 >> 1) : -1;
-  if (relation == PASTE_REL_ANCHORED) {
-    const int ns = distinct_subseqs(prev, pl, subs, sub_len, 64, true, 6);
-    for (int q = 0; q < ns; ++q) {
-      int c[16];
-      const int len = sub_len[q];
-      for (int i = 0; i < len; ++i) c[i] = subs[q * 6 + i];
-      c[len] = sym[1];
-      const int64_t ci = ctx_index(g, c, len + 1);
-      atomicAdd(match + ci, (unsigned long long)h);
-      if (follow_tool >= 0) atomicAdd(follow + ci * g.T + follow_tool, (unsigned long long)h);
+template <int K>
+__device__ __forceinline__ int window_contexts(const MineGeom& g, const int* w, int wl, bool anchored,
+                                               bool with_empty, int tail, int64_t* out) {
+  // contexts = (distinct subsequence | suffix of w[0..wl)) + (tail if >= 0)
+  int n = 0;
+  if (anchored) {
+#pragma unroll
+    for (int mask = 0; mask < (1 << K); ++mask) {
+      if ((mask >> wl) != 0 || (mask == 0 && !with_empty)) continue;
+      bool canon = true;
+      int prev = -1, len = 0;
+      int64_t v = 0;
+#pragma unroll
+      for (int i = 0; i < K; ++i) {
+        if (i < wl && ((mask >> i) & 1)) {
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if (q > prev && q < i && !((mask >> q) & 1) && w[q] == w[i]) canon = false;
+          prev = i;
+          v = v * g.S + w[i];
+          ++len;
+        }
+      }
+      if (!canon) continue;
+      if (tail >= 0) {
+        v = v * g.S + tail;
+        ++len;
+      }
+      out[n++] = g.ctx_off[len] + v;
     }
   } else {
-    int c[16];
-    for (int len = 1; len <= pl + 1; ++len) {  // suffixes ending at the anchor
-      for (int i = 0; i < len - 1; ++i) c[i] = prev[pl - (len - 1) + i];
-      c[len - 1] = sym[1];
-      const int64_t ci = ctx_index(g, c, len);
-      atomicAdd(match + ci, (unsigned long long)h);
-      if (follow_tool >= 0) atomicAdd(follow + ci * g.T + follow_tool, (unsigned long long)h);
+#pragma unroll
+    for (int st = 0; st <= K; ++st) {
+      if (st > wl || (st == wl && !with_empty)) continue;
+      int64_t v = 0;
+      int len = 0;
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+        if (i >= st && i < wl) {
+          v = v * g.S + w[i];
+          ++len;
+        }
+      if (tail >= 0) {
+        v = v * g.S + tail;
+        ++len;
+      }
+      out[n++] = g.ctx_off[len] + v;
+    }
+  }
+  return n;
+}
+
+template <int K>
+__global__ void __launch_bounds__(XT) expand_windows_kernel(
+    const uint32_t* __restrict__ hist, MineGeom g, int relation, unsigned long long* tool_count,
+    unsigned long long* support, unsigned long long* match, unsigned long long* follow,
+    int use_cache) {
+  // cache: tool_count[T] | support[T][S] (length-1) | match[S] | follow[S][T]
+  __shared__ unsigned long long cache[XSMEM_CELLS];
+  const int S = g.S, T = g.T, base = g.base, BEGIN = S, END = S + 1;
+  unsigned long long* c_tool = cache;
+  unsigned long long* c_sup = cache + T;
+  unsigned long long* c_match = c_sup + (int64_t)T * S;
+  unsigned long long* c_follow = c_match + S;
+  const int cells = T + 2 * T * S + S;
+  if (use_cache)
+    for (int i = threadIdx.x; i < cells; i += XT) cache[i] = 0;
+  __syncthreads();
+  const bool anchored = relation == PASTE_REL_ANCHORED;
+  const int lane = threadIdx.x & 31;
+  const int64_t n_win = g.n_bins / base;
+  const int64_t warp0 = ((int64_t)blockIdx.x * XT + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * XT) >> 5;
+  for (int64_t wi = warp0; wi < n_win; wi += n_warps) {
+    // decode the window, oldest first; BEGINs must be a prefix, no END
+    int sym[K + 1];
+    {
+      int64_t v = wi;
+#pragma unroll
+      for (int d = 1; d <= K; ++d) {
+        sym[d] = (int)(v % base);
+        v /= base;
+      }
+    }
+    int nb = 0;
+    bool valid = true;
+#pragma unroll
+    for (int d = K; d >= 1; --d) {
+      if (sym[d] == END) valid = false;
+      if (sym[d] == BEGIN) {
+        if (nb != K - d) valid = false;
+        ++nb;
+      }
+    }
+    if (!valid) continue;  // never counted (an all-BEGIN window still counts tool_count)
+    const uint32_t* row = hist + wi * base;
+    int win[K];
+    const int wl = K - nb;
+#pragma unroll
+    for (int i = 0; i < K; ++i) win[i] = i < wl ? sym[wl - i] : 0;
+    // contexts of this window (warp-uniform)
+    int64_t sup_ctx[(1 << K)];
+    int64_t mt_ctx[(1 << K)];
+    const int n_sup = wl > 0 ? window_contexts<K>(g, win, wl, anchored, false, -1, sup_ctx) : 0;
+    const bool has_anchor = wl > 0;  // s_1 is a real event
+    const int n_mt =
+        has_anchor ? window_contexts<K>(g, win, wl - 1, anchored, true, sym[1], mt_ctx) : 0;
+    unsigned long long tot = 0;
+    for (int c0 = 0; c0 < base; c0 += 32) {
+      const int s0 = c0 + lane;
+      const uint32_t h = s0 < base ? __ldg(row + s0) : 0u;
+      if (__ballot_sync(0xffffffffu, h != 0) == 0) continue;
+      tot += h;
+      // per-tool sums in the even lane of each (2t, 2t+1) pair; END excluded
+      const unsigned long long hs = s0 < S ? h : 0u;
+      const unsigned long long ht = hs + __shfl_xor_sync(0xffffffffu, hs, 1);
+      if ((s0 & 1) || ht == 0) continue;
+      const int t = s0 >> 1;
+      if (use_cache) atomicAdd(c_tool + t, ht);
+      else atomicAdd(tool_count + t, ht);
+#pragma unroll
+      for (int q = 0; q < (1 << K); ++q) {
+        if (q >= n_sup) break;
+        const int64_t c = sup_ctx[q];
+        if (use_cache && c < S) atomicAdd(c_sup + (int64_t)t * S + c, ht);
+        else atomicAdd(support + (int64_t)t * g.n_ctx + c, ht);
+      }
+#pragma unroll
+      for (int q = 0; q < (1 << K); ++q) {
+        if (q >= n_mt) break;
+        const int64_t c = mt_ctx[q];
+        if (use_cache && c < S) atomicAdd(c_follow + c * T + t, ht);
+        else atomicAdd(follow + c * T + t, ht);
+      }
+    }
+    if (n_mt == 0) continue;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (tot == 0) continue;
+    if (lane < n_mt) {
+      int64_t c = 0;
+#pragma unroll
+      for (int q = 0; q < (1 << K); ++q)
+        if (q == lane) c = mt_ctx[q];
+      if (use_cache && c < S) atomicAdd(c_match + c, tot);
+      else atomicAdd(match + c, tot);
+    }
+  }
+  if (!use_cache) return;
+  __syncthreads();
+  for (int i = threadIdx.x; i < cells; i += XT) {
+    const unsigned long long v = cache[i];
+    if (v == 0) continue;
+    if (i < T) {
+      atomicAdd(tool_count + i, v);
+    } else if (i < T + T * S) {
+      const int j = i - T, t = j / S, c = j - t * S;
+      atomicAdd(support + (int64_t)t * g.n_ctx + c, v);
+    } else if (i < T + T * S + S) {
+      atomicAdd(match + (i - T - T * S), v);
+    } else {
+      atomicAdd(follow + (i - T - T * S - S), v);  // follow[c][t], c < S
     }
   }
 }
@@ -210,6 +307,88 @@ __global__ void select_kernel(MineGeom g, const unsigned long long* tool_count,
   o[2] = (int64_t)sup;
   o[3] = (int64_t)mt;
   o[4] = (int64_t)fl;
+}
+
+// ---------------------------------------------------------------------------
+// sorted selection for mapping-free mining (columnar traces): the candidates
+// that clear sigma and p = follow / match >= tau, in mine()'s output order
+// (_sort_key, mining.py:105-111): -p, -len(context), target name, context.
+// Sig / tool ids are interned in sorted name order, so with
+//   hi = ~bits(p)                       (p > 0: bit order == numeric order)
+//   lo = (k - len) << 60 | tool << 40 | base-S digits of the context
+// the order is (hi, lo) ascending and every key is distinct ((t, c) unique).
+// The sort is a rank count: rank[i] = #{j : key_j < key_i} over tiles of keys
+// staged in shared memory (persistent CTAs over (i-tile, j-tile) pairs), then
+// a scatter.
+// ---------------------------------------------------------------------------
+struct SelRow {
+  int64_t tool, ctx, support, match, follow;
+  double p;
+};
+
+__global__ void select_keyed_kernel(MineGeom g, const unsigned long long* tool_count,
+                                    const unsigned long long* support,
+                                    const unsigned long long* match,
+                                    const unsigned long long* follow, int64_t sigma, double tau,
+                                    int64_t cap, unsigned long long* n_out, SelRow* rows,
+                                    ulonglong2* keys) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)g.T * g.n_ctx) return;
+  const int t = (int)(idx / g.n_ctx);
+  const int64_t c = idx - (int64_t)t * g.n_ctx;
+  const unsigned long long sup = support[idx];
+  if (sup < (unsigned long long)sigma || tool_count[t] < (unsigned long long)sigma) return;
+  const unsigned long long mt = match[c];
+  if (mt == 0) return;
+  const unsigned long long fl = follow[c * g.T + t];
+  const double p = __ddiv_rn((double)fl, (double)mt);  // == Python's int / int
+  if (p < tau) return;
+  const unsigned long long slot = atomicAdd(n_out, 1ull);
+  if ((int64_t)slot >= cap) return;
+  int len = 1;
+  while (len < g.k && c >= g.ctx_off[len + 1]) ++len;
+  rows[slot] = SelRow{t, c, (int64_t)sup, (int64_t)mt, (int64_t)fl, p};
+  keys[slot] = make_ulonglong2(~(unsigned long long)__double_as_longlong(p),
+                               ((unsigned long long)(g.k - len) << 60) |
+                                   ((unsigned long long)t << 40) |
+                                   (unsigned long long)(c - g.ctx_off[len]));
+}
+
+constexpr int RI = 256, RJ = 512;
+
+__global__ void __launch_bounds__(RI) rank_keys_kernel(const ulonglong2* __restrict__ keys,
+                                                       const unsigned long long* n_out,
+                                                       int64_t cap, uint32_t* rank) {
+  __shared__ ulonglong2 tile[RJ];
+  const unsigned long long nn = *n_out;
+  const int64_t n = (int64_t)nn < cap ? (int64_t)nn : cap;
+  const int64_t ni = (n + RI - 1) / RI, nj = (n + RJ - 1) / RJ;
+  for (int64_t item = blockIdx.x; item < ni * nj; item += gridDim.x) {
+    const int64_t it = item / nj, jt = item - it * nj;
+    const int64_t j0 = jt * RJ;
+    const int jn = (int)(n - j0 < RJ ? n - j0 : RJ);
+    __syncthreads();
+    for (int j = threadIdx.x; j < jn; j += RI) tile[j] = keys[j0 + j];
+    __syncthreads();
+    const int64_t i = it * RI + threadIdx.x;
+    if (i >= n) continue;
+    const ulonglong2 me = keys[i];
+    uint32_t cnt = 0;
+    for (int j = 0; j < jn; ++j) {
+      const ulonglong2 o = tile[j];
+      cnt += (o.x < me.x) | ((o.x == me.x) & (o.y < me.y));
+    }
+    if (cnt) atomicAdd(rank + i, cnt);
+  }
+}
+
+__global__ void scatter_rows_kernel(const SelRow* __restrict__ rows, const uint32_t* __restrict__ rank,
+                                    const unsigned long long* n_out, int64_t cap, SelRow* out) {
+  const unsigned long long nn = *n_out;
+  const int64_t n = (int64_t)nn < cap ? (int64_t)nn : cap;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[rank[i]] = rows[i];
 }
 
 static int make_geom(int n_sigs, int k, MineGeom* g) {
@@ -279,10 +458,28 @@ extern "C" int paste_mine_expand(const paste_mine_desc* d, void* stream) {
     set_error("mining geometry out of range (n_sigs=%d, k=%d)", d->n_sigs, d->k);
     return PASTE_ERR_UNSUPPORTED;
   }
-  const int threads = 128;
-  expand_grams_kernel<<<(unsigned)((g.n_bins + threads - 1) / threads), threads, 0,
-                        (cudaStream_t)stream>>>(d->hist, g, d->relation, U64(d->tool_count),
-                                                U64(d->support), U64(d->match), U64(d->follow));
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t n_win = g.n_bins / g.base;
+  const int64_t want = (n_win + XT / 32 - 1) / (XT / 32);
+  const int64_t cap = (int64_t)sms * 4;
+  const unsigned grid = (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
+  const int use_cache = (int64_t)g.T + 2 * (int64_t)g.T * g.S + g.S <= XSMEM_CELLS;
+  int rc = -1;
+#define PASTE_EXPAND(KV)                                                                     \
+  if (d->k == KV) {                                                                          \
+    expand_windows_kernel<KV><<<grid, XT, 0, (cudaStream_t)stream>>>(                        \
+        d->hist, g, d->relation, U64(d->tool_count), U64(d->support), U64(d->match),         \
+        U64(d->follow), use_cache);                                                          \
+    rc = 0;                                                                                  \
+  }
+  PASTE_EXPAND(1) PASTE_EXPAND(2) PASTE_EXPAND(3) PASTE_EXPAND(4) PASTE_EXPAND(5) PASTE_EXPAND(6)
+#undef PASTE_EXPAND
+  PASTE_REQUIRE(rc == 0, "k=%d outside the expand kernel's range", d->k);
   count_launch();
   PASTE_CUDA_CHECK(cudaGetLastError());
   return PASTE_OK;
@@ -592,6 +789,47 @@ extern "C" int paste_mine_ingest_count(const paste_columnar_desc* c, const paste
     return PASTE_ERR_UNSUPPORTED;
   }
   count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
+
+extern "C" int64_t paste_mine_sort_scratch_bytes(int64_t cap) {
+  return cap <= 0 ? 0 : cap * (int64_t)(sizeof(SelRow) + sizeof(ulonglong2) + sizeof(uint32_t));
+}
+
+extern "C" int paste_mine_select_sorted(const paste_mine_desc* d, int64_t sigma, double tau,
+                                        int64_t cap, uint64_t* n_out, int64_t* out, void* scratch,
+                                        void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(d != nullptr && n_out != nullptr && out != nullptr && scratch != nullptr,
+                "null argument");
+  PASTE_REQUIRE(cap > 0 && cap < ((int64_t)1 << 31), "capacity out of range");
+  MineGeom g;
+  if (make_geom(d->n_sigs, d->k, &g) != 0) {
+    set_error("mining geometry out of range (n_sigs=%d, k=%d)", d->n_sigs, d->k);
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  SelRow* rows = reinterpret_cast<SelRow*>(scratch);
+  ulonglong2* keys = reinterpret_cast<ulonglong2*>(rows + cap);
+  uint32_t* rank = reinterpret_cast<uint32_t*>(keys + cap);
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(n_out);
+  PASTE_CUDA_CHECK(cudaMemsetAsync(n_out, 0, sizeof(uint64_t), st));
+  PASTE_CUDA_CHECK(cudaMemsetAsync(rank, 0, (size_t)cap * sizeof(uint32_t), st));
+  const int64_t total = (int64_t)g.T * g.n_ctx;
+  select_keyed_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+      g, U64(d->tool_count), U64(d->support), U64(d->match), U64(d->follow), sigma, tau, cap, cnt,
+      rows, keys);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  rank_keys_kernel<<<(unsigned)(sms * 4), RI, 0, st>>>(keys, cnt, cap, rank);
+  scatter_rows_kernel<<<(unsigned)(sms * 2), 256, 0, st>>>(rows, rank, cnt, cap,
+                                                          reinterpret_cast<SelRow*>(out));
+  count_launch(3);
   PASTE_CUDA_CHECK(cudaGetLastError());
   return PASTE_OK;
 }

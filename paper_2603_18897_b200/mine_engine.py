@@ -107,12 +107,15 @@ class MineTables:
         check(lib.paste_mine_geometry(n_sigs, k, ctypes.byref(nb), ctypes.byref(nc)), lib)
         T = (n_sigs + 1) // 2
         dev = torch.device("cuda")
-        return cls(n_sigs, k, relation, nb.value, nc.value,
-                   torch.zeros(nb.value, dtype=torch.int32, device=dev),
-                   torch.zeros(T, dtype=torch.int64, device=dev),
-                   torch.zeros(T * nc.value, dtype=torch.int64, device=dev),
-                   torch.zeros(nc.value, dtype=torch.int64, device=dev),
-                   torch.zeros(nc.value * T, dtype=torch.int64, device=dev))
+        nc_ = nc.value
+        # the four u64 tables share one allocation (one memset per expand)
+        flat = torch.zeros(T + 2 * T * nc_ + nc_, dtype=torch.int64, device=dev)
+        tool_count, support, match, follow = torch.split(flat, [T, T * nc_, nc_, nc_ * T])
+        t = cls(n_sigs, k, relation, nb.value, nc_,
+                torch.zeros(nb.value, dtype=torch.int32, device=dev),
+                tool_count, support, match, follow)
+        t._flat = flat
+        return t
 
     def desc(self, tokens=None, n_tokens: int = 0) -> MineDesc:
         return MineDesc(self.n_sigs, self.k, self.relation, 0, ptr(tokens), n_tokens,
@@ -131,10 +134,43 @@ class MineTables:
         from .device_ops import stream_handle
 
         lib = _native.lib()
-        for t in (self.tool_count, self.support, self.match, self.follow):
-            t.zero_()
+        self._flat.zero_()
         d = self.desc()
         check(lib.paste_mine_expand(ctypes.byref(d), stream_handle()), lib)
+
+    def select_sorted(self, sigma: int, tau: float, cap: int | None = None) -> "MinedTable":
+        """Mapping-free patterns in mine()'s output order, selected and sorted
+        on the device (paste_mine_select_sorted) and read back as one table."""
+        from .device_ops import stream_handle
+
+        torch = _torch()
+        lib = _native.lib()
+        st = getattr(self, "_sel", None)
+        cap = cap or (st["cap"] if st else 1 << 14)
+        while True:
+            if st is None or st["cap"] < cap:
+                st = {"cap": cap,
+                      "n": torch.zeros(1, dtype=torch.int64, device="cuda"),
+                      "out": torch.empty(6 * cap, dtype=torch.int64, device="cuda"),
+                      "scratch": torch.empty(lib.paste_mine_sort_scratch_bytes(cap),
+                                             dtype=torch.uint8, device="cuda"),
+                      "n_h": torch.empty(1, dtype=torch.int64, pin_memory=True),
+                      "out_h": torch.empty(6 * cap, dtype=torch.int64, pin_memory=True)}
+                self._sel = st
+            d = self.desc()
+            check(lib.paste_mine_select_sorted(ctypes.byref(d), sigma, float(tau), st["cap"],
+                                               ptr(st["n"]), ptr(st["out"]), ptr(st["scratch"]),
+                                               stream_handle()), lib)
+            st["n_h"].copy_(st["n"], non_blocking=True)
+            stream = torch.cuda.current_stream()
+            stream.synchronize()
+            m = int(st["n_h"][0])
+            if m <= st["cap"]:
+                st["out_h"][:6 * m].copy_(st["out"][:6 * m], non_blocking=True)
+                stream.synchronize()
+                return MinedTable(st["out_h"][:6 * m].numpy().reshape(m, 6).copy(), self.n_sigs,
+                                  self.k)
+            cap = m
 
     def select(self, sigma: int, tau: float) -> np.ndarray:
         """Candidates [m, 5] = (tool, ctx index, support, match, follow)."""
@@ -403,6 +439,69 @@ def patterns_from_candidates(cands: np.ndarray, sigs: SigTable, S: int, cfg: Min
     return out
 
 
+class MinedTable:
+    """mine()'s mapping-free output as sorted columns (rows of (tool, context
+    index, support, match, follow, p)), the form the device returns and a
+    pool image is compiled from.  ``patterns()`` materialises the reference's
+    ``list[PatternTuple]`` (same order, same values)."""
+
+    __slots__ = ("rows", "n_sigs", "k")
+
+    def __init__(self, rows: np.ndarray, n_sigs: int, k: int):
+        self.rows, self.n_sigs, self.k = rows, n_sigs, k
+
+    def __len__(self) -> int:
+        return len(self.rows)
+
+    @property
+    def p(self) -> np.ndarray:
+        return self.rows[:, 5].view(np.float64)
+
+    def patterns(self, sigs: SigTable) -> list[PatternTuple]:
+        if len(self.rows) == 0:
+            return []
+        import gc
+
+        enabled = gc.isenabled()
+        gc.disable()  # thousands of small acyclic objects: skip the gen-0 scans
+        try:
+            return self._materialize(sigs)
+        finally:
+            if enabled:
+                gc.enable()
+
+    def _materialize(self, sigs: SigTable) -> list[PatternTuple]:
+        S, k = self.n_sigs, self.k
+        rows = self.rows
+        # one context tuple per distinct context index
+        uniq, inv = np.unique(rows[:, 1], return_inverse=True)
+        off = np.array(ctx_offsets(S, k), np.int64)
+        length = np.searchsorted(off[1:], uniq, side="right")
+        local = uniq - off[length]
+        sig_obj = [sigs.signature(x) for x in range(S)]
+        ctxs = []
+        for n, v in zip(length.tolist(), local.tolist()):
+            dg = []
+            for _ in range(n):
+                v, r = divmod(v, S)
+                dg.append(sig_obj[r])
+            dg.reverse()
+            ctxs.append(tuple(dg))
+        ctx_of = [ctxs[i] for i in inv.tolist()]
+        tools = [sigs.tools[t] for t in range(len(sigs.tools))]
+        # contexts are non-empty and 0 < tau <= p <= 1 by construction: fill the
+        # frozen dataclass directly (its validating __init__ would dominate)
+        new, cls = object.__new__, PatternTuple
+        out = []
+        append = out.append
+        for ctx, t, sup, pv in zip(ctx_of, rows[:, 0].tolist(), rows[:, 2].tolist(),
+                                   self.p.tolist()):
+            obj = new(cls)
+            obj.__dict__.update(context=ctx, target=tools[t], mapping=None, p=pv, support=sup)
+            append(obj)
+        return out
+
+
 def merge_shard_histograms(hist, counters, group) -> None:
     """K3: sum the per-shard (k+1)-gram histograms (and the ingest counters)
     across ranks.  Windows and matches never cross a session, so with shards
@@ -430,4 +529,4 @@ def mine_columnar(trace: dict, sigs: SigTable, cfg: MiningConfig,
         raise _native.PasteUnsupported(
             "columnar trace is not grouped by session / sorted by (t_start, seq)")
     tables.expand()
-    return patterns_from_candidates(tables.select(cfg.sigma, cfg.tau), sigs, tables.n_sigs, cfg)
+    return tables.select_sorted(cfg.sigma, cfg.tau).patterns(sigs)

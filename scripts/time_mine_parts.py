@@ -39,3 +39,8 @@ timed("expand", lambda: t.expand())
 cands = timed("select", lambda: t.select(cfg.sigma, cfg.tau))
 print("candidates", len(cands), "nonzero bins", int((t.hist != 0).sum()))
 timed("patterns (host)", lambda: patterns_from_candidates(cands, sigs, t.n_sigs, cfg))
+tab = timed("select_sorted", lambda: t.select_sorted(cfg.sigma, cfg.tau))
+print("sorted rows", len(tab))
+timed("materialize", lambda: tab.patterns(sigs))
+ref = patterns_from_candidates(cands, sigs, t.n_sigs, cfg)
+print("sorted == host", tab.patterns(sigs) == ref)

@@ -68,6 +68,31 @@ def test_count_tables_match_oracle(n_sigs, k, rel):
         assert np.array_equal(dev.cpu().numpy().astype(np.uint64), ref)
 
 
+@pytest.mark.parametrize("n_sigs,k,rel,tau", [(32, 3, 0, 0.3), (32, 3, 1, 0.1), (8, 4, 0, 0.05),
+                                              (12, 2, 1, 0.5), (6, 5, 0, 1.0), (16, 1, 0, 0.2)])
+def test_select_sorted_matches_oracle_order(n_sigs, k, rel, tau):
+    """Device selection + rank sort == the oracle's candidates in mine()'s
+    output order (mining.py:105-111), including the capacity retry."""
+    from paper_2603_18897_b200.mine_engine import patterns_from_candidates
+    from paper_2603_18897_b200.packing import SigTable
+
+    tok = _random_stream(20_000, n_sigs, seed=n_sigs * 7 + k)
+    t = MineTables.allocate(n_sigs, k, rel)
+    t.count(torch.from_numpy(tok).cuda())
+    t.expand()
+    sigs = SigTable([f"tool{i:02d}" for i in range((n_sigs + 1) // 2)])
+    cfg = MiningConfig(k=k, sigma=2, tau=tau,
+                       match_relation=MatchRelation.ANCHORED_SUBSEQUENCE if rel == 0
+                       else MatchRelation.CONTIGUOUS_SUFFIX)
+    ora = bridge.mine_counts(tok, n_sigs, k, rel)
+    cands = np.array(bridge.select_candidates(*ora, n_sigs, k, cfg.sigma, cfg.tau), np.int64)
+    exp = patterns_from_candidates(cands.reshape(-1, 5), sigs, n_sigs, cfg)
+    got = t.select_sorted(cfg.sigma, cfg.tau, cap=7)  # forces the retry path
+    assert len(got) == len(exp) > 0
+    assert got.patterns(sigs) == exp
+    assert np.array_equal(got.p, [p.p for p in exp])
+
+
 def test_count_is_additive_across_shards():
     """Shards counted into one histogram == the whole corpus (K3 merge basis)."""
     tok = _random_stream(50_000, 32, seed=5)
