@@ -297,6 +297,16 @@ typedef struct {
 } paste_columnar_desc;
 
 int paste_mine_ingest_count(const paste_columnar_desc* c, const paste_mine_desc* d, void* stream);
+/* Same, in two passes: the columnar pass writes one staged word per event
+ * (4 B) to `stage`; a second pass sends the cold grams to L2 into 8
+ * histogram replicas (a hot gram's updates spread over 8 addresses), which
+ * are then folded into d->hist.  The scattered updates no longer contend
+ * with the columnar stream.  `stage` is device memory of
+ * paste_mine_stage_bytes(n_events, n_sigs, k) bytes (16-byte aligned);
+ * NULL falls back to the single pass.                                      */
+int64_t paste_mine_stage_bytes(int64_t n_events, int32_t n_sigs, int32_t k);
+int paste_mine_ingest_count_staged(const paste_columnar_desc* c, const paste_mine_desc* d,
+                                   void* stage, int64_t stage_bytes, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* K6: admission selection (scheduling.py:59-60, 242-258)                   */

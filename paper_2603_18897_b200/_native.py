@@ -165,6 +165,9 @@ EXPORTS = {
     "paste_mine_select": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64, c_void_p,
                                   c_void_p, c_void_p]),
     "paste_mine_sort_scratch_bytes": (c_int64, [c_int64]),
+    "paste_mine_stage_bytes": (c_int64, [c_int64, c_int32, c_int32]),
+    "paste_mine_ingest_count_staged": (c_int, [POINTER(ColumnarDesc), POINTER(MineDesc), c_void_p,
+                                               c_int64, c_void_p]),
     "paste_mine_select_sorted": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64,
                                          c_void_p, c_void_p, c_void_p, c_void_p]),
 }

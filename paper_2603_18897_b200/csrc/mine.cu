@@ -25,6 +25,9 @@
 // every segment (session after gap splitting).
 #include "common.cuh"
 
+#include <mutex>
+#include <unordered_map>
+
 namespace paste {
 
 constexpr uint32_t SEG_START = 0x80000000u;
@@ -517,37 +520,26 @@ extern "C" int paste_mine_select(const paste_mine_desc* d, int64_t sigma, double
 // ---------------------------------------------------------------------------
 // Pipeline: one producer warp streams tiles of CTILE events (five columns,
 // TMA bulk copies) into CNST shared-memory stages guarded by full / empty
-// mbarriers; CW consumer warps each take 32 consecutive events at a time
-// (lane = event).  Segment flags and the (k+1)-gram window come from warp
-// shuffles (lanes 0..k-1 also compute the k events before the chunk, lane 31
-// the flag of the event after it), so consumers never wait on each other:
-// there is no __syncthreads in the steady state.
+// mbarriers.  Tiles are handed out dynamically (a global tile counter the
+// producer bumps), so SMs that see slower L2 atomics do not set the tail.
+// Each of the CW consumer warps owns 64 consecutive events of a tile (two
+// 32-lane sub-chunks): segment flags come from the staged columns, the
+// (k+1)-gram window from warp shuffles over the two sub-chunks plus one halo
+// word per lane (the k events before the span, and the event after it), so
+// consumers never wait on each other: no __syncthreads in the steady state.
+//
+// Counting: the grams of a segment's first two events, (BEGIN.., s_1, s_0),
+// are shared by every segment (1/4 of all increments at a mean length of 8)
+// and would serialise on a few L2 atomic units; they accumulate in a dense
+// per-CTA shared-memory table of base^2 counters flushed once.  Every other
+// gram is spread over ~1M bins and goes straight to L2 as a RED.
 constexpr int CW = 8;                   // consumer warps
 constexpr int CT = 32 * (CW + 1);       // + one producer warp
-constexpr int CTILE = 512;              // events per tile (= 2 chunks of 32 per consumer warp)
+constexpr int CTILE = 64 * CW;          // events per tile (64 per consumer warp)
 constexpr int CPRE = 8;                 // halo before the tile (>= k + 1, 16-B aligned)
 constexpr int CSPAN = CTILE + 16;       // staged events per tile (halo + 1 after, padded)
 constexpr int CNST = 4;                 // pipeline stages
-constexpr int CHASH = 2048;             // per-CTA heavy-hitter table (keys, counts)
-constexpr uint32_t HEMPTY = 0xffffffffu;
-
-// Per-CTA aggregation: hot grams (e.g. the (BEGIN, .., BEGIN, s) grams every
-// session starts with) would otherwise serialise on a few L2 atomic units.
-__device__ __forceinline__ void hh_add(uint32_t* hkey, uint32_t* hcnt, uint32_t* hist, uint32_t key,
-                                       uint32_t inc) {
-  const uint32_t h = (key * 2654435761u) >> (32 - 11);  // log2(CHASH) = 11
-#pragma unroll
-  for (int probe = 0; probe < 2; ++probe) {
-    const uint32_t slot = (h + probe) & (CHASH - 1);
-    uint32_t k0 = *(volatile uint32_t*)(hkey + slot);  // read first: CAS only to claim
-    if (k0 == HEMPTY) k0 = atomicCAS(hkey + slot, HEMPTY, key);
-    if (k0 == HEMPTY || k0 == key) {
-      atomicAdd(hcnt + slot, inc);
-      return;
-    }
-  }
-  atomicAdd(hist + key, inc);  // table region full: straight to L2
-}
+constexpr int CHOT_MAX = 2048;          // dense hot-gram table capacity (u32)
 
 // one stage of staged columns
 struct __align__(16) ColumnTile {
@@ -624,7 +616,7 @@ __device__ __forceinline__ void produce_tile(const paste_columnar_desc& C, int64
   }
 }
 
-// v(l) = sig | segment-start flag << 31 for staged slot l (event g0 + l).
+// v(l) = sig | segment-start flag << 31 for staged slot l (event x = g0 + l).
 // Events before the trace start or past its end read as segment starts.
 __device__ __forceinline__ uint32_t slot_word(const ColumnTile* T, int l, int64_t x, int64_t n,
                                               double gap) {
@@ -632,20 +624,107 @@ __device__ __forceinline__ uint32_t slot_word(const ColumnTile* T, int l, int64_
   const bool b = (T->sess[l] != T->sess[l - 1]) || (__dsub_rn(T->ts[l], T->te[l - 1]) > gap);
   return (uint32_t)T->sig[l] | (b ? SEG_START : 0u);
 }
+// Count the gram ending at an event (window words w[1..K], w[0] = own word)
+// and, after the segment's last event, its END gram.  Hot grams go to the
+// CTA's shared table.  Cold grams go straight to L2 (STAGE = false), or are
+// returned as a staged word for stage_hist_kernel (STAGE = true): the gram
+// key, bit 31 = already counted (hot), bit 30 = END gram still to count.
+constexpr uint32_t STG_HOT = 0x80000000u, STG_END = 0x40000000u, STG_KEY = 0x3fffffffu;
+constexpr int STG_REPS = 8;  // histogram replicas of the L2 pass
+__host__ __device__ inline int64_t stage_words(int64_t n) { return (n + 3) & ~(int64_t)3; }
 
-template <int K, bool WRITE_TOK>
+template <int K, bool STAGE>
+__device__ __forceinline__ uint32_t count_event(const uint32_t (&w)[K + 1], bool last, uint32_t S,
+                                                uint32_t base, uint32_t hot_lo, uint32_t hot_n,
+                                                uint32_t* hot, uint32_t* hist) {
+  uint32_t key = w[0] & 0x7fffffffu, mult = base, kend = S + 1, mul2 = base;
+  bool stop = w[0] >> 31, stop2 = false;
+#pragma unroll
+  for (int d = 1; d <= K; ++d) {
+    key += (stop ? S : (w[d] & 0x7fffffffu)) * mult;
+    stop = stop || (w[d] >> 31);
+    mult *= base;
+    kend += (stop2 ? S : (w[d - 1] & 0x7fffffffu)) * mul2;
+    stop2 = stop2 || (w[d - 1] >> 31);
+    mul2 *= base;
+  }
+  uint32_t word = key;
+  if (key - hot_lo < hot_n) {
+    atomicAdd(hot + (key - hot_lo), 1u);
+    word |= STG_HOT;
+  } else if (!STAGE) {
+    atomicAdd(hist + key, 1u);
+  }
+  if (last) {
+    if (kend - hot_lo < hot_n) atomicAdd(hot + (kend - hot_lo), 1u);
+    else if (!STAGE) atomicAdd(hist + kend, 1u);
+    else word |= STG_END;
+  }
+  return word;
+}
+
+// Stage 2 of the staged count: the cold grams of the staged words go to L2
+// as REDs, in a pass of their own (interleaved with the columnar stream the
+// same REDs run at well under half their standalone rate).  kend of a
+// segment's last event is END + base * (its gram mod base^K).
+__device__ __forceinline__ void stage_word(uint32_t w, uint32_t end_sym, uint32_t base,
+                                           uint32_t mod_k, uint32_t* __restrict__ hist) {
+  const uint32_t key = w & STG_KEY;
+  if (!(w & STG_HOT)) atomicAdd(hist + key, 1u);
+  if (w & STG_END) atomicAdd(hist + end_sym + base * (key % mod_k), 1u);
+}
+
+template <int V>
+__global__ void __launch_bounds__(256) stage_hist_kernel(const uint32_t* __restrict__ words,
+                                                         int64_t n, uint32_t end_sym,
+                                                         uint32_t base, uint32_t mod_k,
+                                                         uint32_t* __restrict__ reps,
+                                                         int64_t n_bins, int n_reps) {
+  // replica per CTA group: a hot bin's updates spread over n_reps addresses
+  uint32_t* __restrict__ hist = reps + (int64_t)(blockIdx.x % n_reps) * n_bins;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (V == 4) {
+    const int64_t n4 = n >> 2;
+    for (int64_t i = t0; i < n4; i += stride) {
+      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(words) + i);
+      stage_word(v.x, end_sym, base, mod_k, hist);
+      stage_word(v.y, end_sym, base, mod_k, hist);
+      stage_word(v.z, end_sym, base, mod_k, hist);
+      stage_word(v.w, end_sym, base, mod_k, hist);
+    }
+    for (int64_t i = 4 * n4 + t0; i < n; i += stride) stage_word(words[i], end_sym, base, mod_k, hist);
+  } else {
+    for (int64_t i = t0; i < n; i += stride) stage_word(__ldcs(words + i), end_sym, base, mod_k, hist);
+  }
+}
+
+// hist += sum of the replicas (one pass over n_reps * n_bins words in L2)
+__global__ void fold_replicas_kernel(const uint32_t* __restrict__ reps, int64_t n_bins, int n_reps,
+                                     uint32_t* __restrict__ hist) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_bins;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t acc = 0;
+    for (int r = 0; r < n_reps; ++r) acc += __ldcs(reps + (int64_t)r * n_bins + i);
+    if (acc) hist[i] += acc;
+  }
+}
+
+// OUT: 0 = cold grams straight to L2, 1 = same + flagged token stream,
+// 2 = staged words to `stage_out` (counted by stage_hist_kernel)
+template <int K, int OUT>
 __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar_desc C,
                                                             MineGeom g, uint32_t* __restrict__ hist,
-                                                            int32_t* __restrict__ tok_out) {
+                                                            int32_t* __restrict__ tok_out,
+                                                            uint32_t* __restrict__ stage_out,
+                                                            unsigned long long* tile_ctr,
+                                                            uint32_t hot_lo, uint32_t hot_n) {
   extern __shared__ __align__(16) uint8_t c_smem[];
   ColumnTile* tiles = reinterpret_cast<ColumnTile*>(c_smem);
-  uint32_t* hkey = reinterpret_cast<uint32_t*>(tiles + CNST);
-  uint32_t* hcnt = hkey + CHASH;
+  uint32_t* hot = reinterpret_cast<uint32_t*>(tiles + CNST);
   __shared__ uint64_t full[CNST], empty[CNST];
-  for (int i = threadIdx.x; i < CHASH; i += CT) {
-    hkey[i] = HEMPTY;
-    hcnt[i] = 0;
-  }
+  __shared__ int64_t stage_tile[CNST];
+  for (uint32_t i = threadIdx.x; i < hot_n; i += CT) hot[i] = 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < CNST; ++s) {
       mbar_init(&full[s], 1);
@@ -659,77 +738,113 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned long long segs = 0, bad = 0;
   if (warp == CW) {
-    // ---- producer ----------------------------------------------------------
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+    // ---- producer: claim tiles until the trace is exhausted -----------------
+    for (int it = 0;; ++it) {
       const int st = it % CNST;
       if (it >= CNST) mbar_wait(&empty[st], ((it / CNST) - 1) & 1);
+      int64_t t = 0;
+      if (lane == 0) t = (int64_t)atomicAdd(tile_ctr, 1ull);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= n_tiles) {
+        if (lane == 0) {
+          stage_tile[st] = -1;
+          mbar_arrive(&full[st]);  // release: consumers see the sentinel
+        }
+        break;
+      }
+      if (lane == 0) stage_tile[st] = t;
       produce_tile(C, t, &tiles[st], &full[st], lane);
     }
   } else {
-    // ---- consumers ---------------------------------------------------------
+    // ---- consumers -----------------------------------------------------------
     const uint32_t S = (uint32_t)g.S, base = (uint32_t)g.base;
     const double gap = C.inactivity_ms;
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++it) {
+    for (int it = 0;; ++it) {
       const int st = it % CNST;
-      const ColumnTile* T = &tiles[st];
       mbar_wait(&full[st], (it / CNST) & 1);
+      const int64_t t = stage_tile[st];
+      if (t < 0) break;
+      const ColumnTile* T = &tiles[st];
       const int64_t g0 = t * CTILE - CPRE;
+      const int l0 = CPRE + warp * 64;  // the warp's first slot
+      const int64_t x0 = g0 + l0;
+      // lane L owns span events e0 = 2L, e1 = 2L + 1 (slots l, l + 1): one
+      // vector load per column for both, scalar loads of the slot before
+      const int l = l0 + 2 * lane;
+      const int64_t xa = x0 + 2 * lane, xb = xa + 1;
+      const int2 sg = *reinterpret_cast<const int2*>(T->sig + l);
+      const int2 ss = *reinterpret_cast<const int2*>(T->sess + l);
+      const int2 sq = *reinterpret_cast<const int2*>(T->seq + l);
+      const double2 ts = *reinterpret_cast<const double2*>(T->ts + l);
+      const double2 te = *reinterpret_cast<const double2*>(T->te + l);
+      const int32_t ps = T->sess[l - 1], pq = T->seq[l - 1];
+      const double pts = T->ts[l - 1], pte = T->te[l - 1];
+      uint32_t v0, v1;
+      {
+        const bool b0 = (ps != ss.x) || (__dsub_rn(ts.x, pte) > gap);
+        const bool b1 = (ss.x != ss.y) || (__dsub_rn(ts.y, te.x) > gap);
+        v0 = (uint32_t)sg.x | (b0 ? SEG_START : 0u);
+        v1 = (uint32_t)sg.y | (b1 ? SEG_START : 0u);
+        if (xa <= 0 || xa >= n) v0 = (xa == 0 ? (uint32_t)sg.x : 0u) | SEG_START;
+        if (xb >= n) v1 = SEG_START;
+      }
+      // halo: lanes < K hold the word of slot l0-1-lane, the rest slot l0+64
+      const int hl = lane < K ? -1 - lane : 64;
+      const uint32_t h = slot_word(T, l0 + hl, x0 + hl, n, gap);
+      constexpr int HU = (K + 1) / 2;
+      uint32_t up0[HU + 1], up1[HU + 1], hs[K + 1];
 #pragma unroll
-      for (int j = 0; j < CTILE / (32 * CW); ++j) {
-        const int l0 = CPRE + (j * CW + warp) * 32;  // chunk's first slot
-        const int l = l0 + lane;
-        const int64_t x = g0 + l;
-        const uint32_t v = slot_word(T, l, x, n, gap);
-        // the k words before the chunk (lane d-1 holds slot l0 - d) and the
-        // flag of the slot after it (lane 31)
-        uint32_t h = 0;
-        if (lane < K) h = slot_word(T, l0 - 1 - lane, g0 + l0 - 1 - lane, n, gap);
-        if (lane == 31) h = slot_word(T, l + 1, x + 1, n, gap);
-        uint32_t w[K + 1];
-        w[0] = v;
+      for (int j = 1; j <= HU; ++j) {
+        up0[j] = __shfl_up_sync(0xffffffffu, v0, j);
+        up1[j] = __shfl_up_sync(0xffffffffu, v1, j);
+      }
 #pragma unroll
-        for (int d = 1; d <= K; ++d) {
-          const uint32_t a = __shfl_up_sync(0xffffffffu, v, d);
-          const uint32_t b = __shfl_sync(0xffffffffu, h, (d - lane - 1) & 31);
-          w[d] = lane >= d ? a : b;
-        }
-        const uint32_t nx = __shfl_down_sync(0xffffffffu, v, 1);
-        if (x >= n) continue;  // past the trace end (after the shuffles)
-        const bool last = (lane == 31 ? h : nx) >> 31;
-        // gram ending at x: BEGIN once a segment start has been passed
-        uint32_t key = w[0] & 0x7fffffffu, mult = base, kend = S + 1, mul2 = base;
-        bool stop = w[0] >> 31, stop2 = false;
+      for (int d = 1; d <= K; ++d) hs[d] = __shfl_sync(0xffffffffu, h, (d - 2 * lane - 1) & 31);
+      uint32_t w0[K + 1], w1[K + 1];
+      w0[0] = v0;
+      w1[0] = v1;
 #pragma unroll
-        for (int d = 1; d <= K; ++d) {
-          key += (stop ? S : (w[d] & 0x7fffffffu)) * mult;
-          stop = stop || (w[d] >> 31);
-          mult *= base;
-          // END gram: positions x-(d-1)
-          kend += (stop2 ? S : (w[d - 1] & 0x7fffffffu)) * mul2;
-          stop2 = stop2 || (w[d - 1] >> 31);
-          mul2 *= base;
+      for (int d = 1; d <= K; ++d) {
+        // e0 = 2L at distance d: lane L - ceil(d/2), word (d even ? v0 : v1)
+        const int c = (d + 1) / 2;
+        w0[d] = lane >= c ? ((d & 1) ? up1[c] : up0[d / 2]) : hs[d];
+        // e1 = 2L + 1 at distance d: lane L - floor(d/2), word (d odd ? v0 : v1)
+        const int f = d / 2;
+        w1[d] = d == 1 ? v0 : (lane >= f ? ((d & 1) ? up0[f] : up1[f]) : hs[d - 1]);
+      }
+      const uint32_t nx = __shfl_down_sync(0xffffffffu, v0, 1);
+      const bool last0 = v1 >> 31;
+      const bool last1 = (lane == 31 ? h : nx) >> 31;
+      constexpr bool STAGE = OUT == 2;
+      uint32_t k0 = 0, k1 = 0;
+      if (xa < n) {
+        k0 = count_event<K, STAGE>(w0, last0, S, base, hot_lo, hot_n, hot, hist);
+        segs += last0;
+        if (xa > 0) {
+          const bool back = (ts.x < pts) | ((ts.x == pts) & (sq.x <= pq));
+          bad += (ss.x < ps) | ((ss.x == ps) & back);
         }
-        hh_add(hkey, hcnt, hist, key, 1u);
-        segs += last;
-        if (last) hh_add(hkey, hcnt, hist, kend, 1u);
-        if (x > 0) {  // order check (the host rejects unsorted traces)
-          const int32_t ss = T->sess[l], ps = T->sess[l - 1];
-          const double ts = T->ts[l], pts = T->ts[l - 1];
-          const bool back = (ts < pts) | ((ts == pts) & (T->seq[l] <= T->seq[l - 1]));
-          bad += (ss < ps) | ((ss == ps) & back);
-        }
-        if (WRITE_TOK) tok_out[x] = (int32_t)v;
+        if (OUT == 1) tok_out[xa] = (int32_t)v0;
+      }
+      if (xb < n) {
+        k1 = count_event<K, STAGE>(w1, last1, S, base, hot_lo, hot_n, hot, hist);
+        segs += last1;
+        const bool back = (ts.y < ts.x) | ((ts.y == ts.x) & (sq.y <= sq.x));
+        bad += (ss.y < ss.x) | ((ss.y == ss.x) & back);
+        if (OUT == 1) tok_out[xb] = (int32_t)v1;
+      }
+      if (STAGE) {
+        if (xb < n) __stcs(reinterpret_cast<uint2*>(stage_out + xa), make_uint2(k0, k1));
+        else if (xa < n) stage_out[xa] = k0;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
     }
   }
-  // flush the heavy-hitter table
+  // flush the hot-gram table
   __syncthreads();
-  for (int i = threadIdx.x; i < CHASH; i += CT)
-    if (hkey[i] != HEMPTY) atomicAdd(hist + hkey[i], hcnt[i]);
+  for (uint32_t i = threadIdx.x; i < hot_n; i += CT)
+    if (hot[i]) atomicAdd(hist + hot_lo + i, hot[i]);
   // warp-reduce the counters
   for (int o = 16; o > 0; o >>= 1) {
     segs += __shfl_xor_sync(0xffffffffu, segs, o);
@@ -741,26 +856,62 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
   }
 }
 
-template <int K, bool WT>
+// One tile counter per stream (reset on the stream before every launch), so
+// concurrent launches on different streams never share one.
+static unsigned long long* tile_counter(cudaStream_t stream) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, unsigned long long*> ctrs;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = ctrs.find(stream);
+  if (it != ctrs.end()) return it->second;
+  unsigned long long* p = nullptr;
+  if (cudaMalloc(&p, sizeof(unsigned long long)) != cudaSuccess) return nullptr;
+  ctrs[stream] = p;
+  return p;
+}
+
+template <int K, int OUT>
 static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint32_t* hist,
-                           size_t smem, int64_t tiles, cudaStream_t stream) {
-  static int grid_cap = 0;
+                           uint32_t* stage, int64_t tiles, cudaStream_t stream) {
+  // hot grams: positions 2..K all BEGIN (a segment's first two events and
+  // the END gram of a one-event segment), dense index s_0 + base * s_1
+  uint32_t hot_lo = 0, hot_n = (uint32_t)g.base * (uint32_t)g.base;
+  uint32_t pw = hot_n;
+  for (int d = 2; d <= K; ++d, pw *= (uint32_t)g.base) hot_lo += (uint32_t)g.S * pw;
+  if (hot_n > (uint32_t)CHOT_MAX) hot_n = 0;
+  const size_t smem = sizeof(ColumnTile) * CNST + (size_t)CHOT_MAX * sizeof(uint32_t);
+  static int grid_cap = 0, sms = 0;
   if (grid_cap == 0) {
-    int dev = 0, sms = 0, occ = 0;
+    int dev = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(columnar_count_kernel<K, WT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(columnar_count_kernel<K, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, columnar_count_kernel<K, WT>, CT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, columnar_count_kernel<K, OUT>, CT, smem);
     grid_cap = sms * (occ > 0 ? occ : 1);
   }
+  unsigned long long* ctr = tile_counter(stream);
+  if (ctr == nullptr) return -2;
+  if (cudaMemsetAsync(ctr, 0, sizeof(*ctr), stream) != cudaSuccess) return -2;
   const int64_t grid = tiles < grid_cap ? tiles : grid_cap;
-  columnar_count_kernel<K, WT><<<(unsigned)grid, CT, smem, stream>>>(c, g, hist, c.tokens_out);
+  columnar_count_kernel<K, OUT><<<(unsigned)grid, CT, smem, stream>>>(c, g, hist, c.tokens_out,
+                                                                      stage, ctr, hot_lo, hot_n);
+  if (OUT == 2) {
+    uint32_t mod_k = 1;
+    for (int d = 0; d < K; ++d) mod_k *= (uint32_t)g.base;
+    uint32_t* reps = stage + stage_words(c.n_events);
+    if (cudaMemsetAsync(reps, 0, (size_t)STG_REPS * g.n_bins * sizeof(uint32_t), stream) !=
+        cudaSuccess)
+      return -2;
+    stage_hist_kernel<4><<<(unsigned)(sms * 8), 256, 0, stream>>>(
+        stage, c.n_events, (uint32_t)g.S + 1, (uint32_t)g.base, mod_k, reps, g.n_bins, STG_REPS);
+    fold_replicas_kernel<<<(unsigned)(sms * 4), 256, 0, stream>>>(reps, g.n_bins, STG_REPS, hist);
+  }
   return 0;
 }
 
-extern "C" int paste_mine_ingest_count(const paste_columnar_desc* c, const paste_mine_desc* d,
-                                       void* stream) {
+static int ingest_count_impl(const paste_columnar_desc* c, const paste_mine_desc* d,
+                             uint32_t* stage, void* stream) {
   reset_launches();
   PASTE_REQUIRE(c != nullptr && d != nullptr, "null descriptor");
   MineGeom g;
@@ -772,25 +923,54 @@ extern "C" int paste_mine_ingest_count(const paste_columnar_desc* c, const paste
   const uintptr_t mis = (uintptr_t)c->session | (uintptr_t)c->seq | (uintptr_t)c->t_start |
                         (uintptr_t)c->t_end | (uintptr_t)c->sig;
   PASTE_REQUIRE((mis & 15) == 0, "columnar arrays must be 16-byte aligned");
-  const size_t smem = sizeof(ColumnTile) * CNST + 2 * CHASH * sizeof(uint32_t);
+  PASTE_REQUIRE(stage == nullptr || ((uintptr_t)stage & 15) == 0,
+                "staging buffer must be 16-byte aligned");
   const int64_t tiles = (c->n_events + CTILE - 1) / CTILE;
-  const bool wt = c->tokens_out != nullptr;
+  // staged counting needs gram keys below 2^30 (two flag bits)
+  const int out = c->tokens_out != nullptr ? 1
+                  : (stage != nullptr && g.n_bins <= (int64_t)STG_KEY + 1) ? 2 : 0;
   int rc = -1;
-#define PASTE_COLUMNAR(KV)                                                                      \
-  if (d->k == KV) {                                                                             \
-    if (wt) rc = launch_columnar<KV, true>(*c, g, d->hist, smem, tiles, (cudaStream_t)stream);   \
-    else rc = launch_columnar<KV, false>(*c, g, d->hist, smem, tiles, (cudaStream_t)stream);     \
+#define PASTE_COLUMNAR(KV)                                                                        \
+  if (d->k == KV) {                                                                               \
+    if (out == 1) rc = launch_columnar<KV, 1>(*c, g, d->hist, stage, tiles, (cudaStream_t)stream); \
+    else if (out == 2)                                                                            \
+      rc = launch_columnar<KV, 2>(*c, g, d->hist, stage, tiles, (cudaStream_t)stream);            \
+    else rc = launch_columnar<KV, 0>(*c, g, d->hist, stage, tiles, (cudaStream_t)stream);         \
   }
   PASTE_COLUMNAR(1) PASTE_COLUMNAR(2) PASTE_COLUMNAR(3) PASTE_COLUMNAR(4) PASTE_COLUMNAR(5)
   PASTE_COLUMNAR(6)
 #undef PASTE_COLUMNAR
+  if (rc == -2) {
+    set_error("could not allocate the columnar tile counter");
+    return PASTE_ERR_CUDA;
+  }
   if (rc != 0) {
     set_error("k=%d outside the columnar kernel's range", d->k);
     return PASTE_ERR_UNSUPPORTED;
   }
-  count_launch();
+  count_launch(out == 2 ? 3 : 1);
   PASTE_CUDA_CHECK(cudaGetLastError());
   return PASTE_OK;
+}
+
+extern "C" int paste_mine_ingest_count(const paste_columnar_desc* c, const paste_mine_desc* d,
+                                       void* stream) {
+  return ingest_count_impl(c, d, nullptr, stream);
+}
+
+extern "C" int64_t paste_mine_stage_bytes(int64_t n_events, int32_t n_sigs, int32_t k) {
+  MineGeom g;
+  if (n_events <= 0 || make_geom(n_sigs, k, &g) != 0) return 0;
+  return (stage_words(n_events) + (int64_t)STG_REPS * g.n_bins) * 4;
+}
+
+extern "C" int paste_mine_ingest_count_staged(const paste_columnar_desc* c,
+                                              const paste_mine_desc* d, void* stage,
+                                              int64_t stage_bytes, void* stream) {
+  PASTE_REQUIRE(c != nullptr && d != nullptr, "null descriptor");
+  PASTE_REQUIRE(stage == nullptr || stage_bytes >= paste_mine_stage_bytes(c->n_events, d->n_sigs, d->k),
+                "staging buffer too small");
+  return ingest_count_impl(c, d, reinterpret_cast<uint32_t*>(stage), stream);
 }
 
 extern "C" int64_t paste_mine_sort_scratch_bytes(int64_t cap) {

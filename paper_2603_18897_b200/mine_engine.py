@@ -380,21 +380,35 @@ def frequent_subsequences(windows, sigma: int) -> dict:
 # ---------------------------------------------------------------------------
 
 def ingest_count(tables: MineTables, trace: dict, inactivity_ms: float = 300_000.0,
-                 tokens_out=None):
+                 tokens_out=None, staged: bool = True):
     """Fused ingest + count of a device-resident columnar trace into
-    ``tables.hist``; returns device counters (n_segments, n_unsorted)."""
+    ``tables.hist``; returns device counters (n_segments, n_unsorted).
+    ``staged`` runs the two-pass count (paste_mine_ingest_count_staged) with
+    a staging buffer cached on ``tables``."""
     from .device_ops import stream_handle
     from ._native import ColumnarDesc
 
     torch = _torch()
     lib = _native.lib()
-    counters = torch.zeros(2, dtype=torch.int64, device="cuda")
+    counters = getattr(tables, "_counters", None)
+    if counters is None:
+        counters = tables._counters = torch.zeros(2, dtype=torch.int64, device="cuda")
+    else:
+        counters.zero_()
     n = int(trace["sig"].numel())
     c = ColumnarDesc(n, ptr(trace["session"]), ptr(trace["seq"]), ptr(trace["t_start"]),
                      ptr(trace["t_end"]), ptr(trace["sig"]), float(inactivity_ms), ptr(tokens_out),
                      ptr(counters), ptr(counters) + 8)
     d = tables.desc()
-    check(lib.paste_mine_ingest_count(ctypes.byref(c), ctypes.byref(d), stream_handle()), lib)
+    if staged and tokens_out is None:
+        need = int(lib.paste_mine_stage_bytes(n, tables.n_sigs, tables.k))
+        buf = getattr(tables, "_stage", None)
+        if buf is None or buf.numel() < need:
+            buf = tables._stage = torch.empty(max(need, 16), dtype=torch.uint8, device="cuda")
+        check(lib.paste_mine_ingest_count_staged(ctypes.byref(c), ctypes.byref(d), ptr(buf),
+                                                 buf.numel(), stream_handle()), lib)
+    else:
+        check(lib.paste_mine_ingest_count(ctypes.byref(c), ctypes.byref(d), stream_handle()), lib)
     return counters
 
 

@@ -166,6 +166,26 @@ def test_columnar_ingest_count_matches_oracle():
             assert np.array_equal(dev.cpu().numpy().astype(np.uint64), ref)
 
 
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 6])
+def test_columnar_staged_count_equals_single_pass(k):
+    """Two-pass (staged words + L2 pass) histogram == the fused single pass ==
+    the oracle's tables, including a ragged tail (n not a multiple of 4)."""
+    from paper_2603_18897_b200.mine_engine import ingest_count
+    from paper_2603_18897_b200.synth import columnar_corpus
+
+    c = columnar_corpus(123_457, seed=20 + k)
+    dev = _dev(c)
+    a = MineTables.allocate(32, k, 0)
+    b = MineTables.allocate(32, k, 0)
+    ca = ingest_count(a, dev, staged=True)
+    cb = ingest_count(b, dev, staged=False)
+    assert torch.equal(a.hist, b.hist) and torch.equal(ca, cb)
+    a.expand()
+    ora = bridge.mine_counts(_host_tokens(c), 32, k, 0)
+    for dev_t, ref in zip((a.tool_count, a.support, a.match, a.follow), ora):
+        assert np.array_equal(dev_t.cpu().numpy().astype(np.uint64), ref)
+
+
 def test_mine_columnar_patterns_match_oracle_selection():
     from paper_2603_18897_b200.mine_engine import mine_columnar, patterns_from_candidates
     from paper_2603_18897_b200.packing import SigTable
