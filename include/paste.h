@@ -143,7 +143,7 @@ typedef struct {
    * (token new_tok[s]); it becomes event new_evt_base + s and its directory
    * entry is new_ref[s] with byte_base taken relative to new_byte_base.     */
   const int32_t* new_tok;      /* [n] or NULL                                 */
-  const paste_event_ref* new_ref; /* [n]                                      */
+  const paste_event_ref* new_ref; /* [n] (or NULL when new_node is given)     */
   int64_t new_evt_base;
   int64_t new_byte_base;
   /* optional stream mode (replay): windows are views into one event stream.
@@ -151,6 +151,9 @@ typedef struct {
    * length and window s = stream[stream_end[s] - count[s] .. stream_end[s]);
    * new_tok must be NULL.                                                  */
   const int64_t* stream_end;
+  /* optional narrow observe input: node_base only (byte_base = new_byte_base),
+   * 4 B/session instead of the 16-B directory entry of new_ref            */
+  const int32_t* new_node;
 } paste_windows;
 
 enum { PASTE_C_FULL = 0, PASTE_C_PARTIAL = 1, PASTE_C_TOOL_ONLY = 2 };
@@ -388,18 +391,22 @@ typedef struct {
 int paste_resolve(const paste_resolve_desc* d, void* stream);
 
 /* Live-path record compaction: the K-slot records of paste_predict_batch
- * -> CSR streams in session order (decoupled look-back scan).  Capacities:
- * pred/act/util n*K, arg n*K*B.  totals = {predictions, arguments, actions}.
- * hdr = n_pred | n_act << 8; pred = pattern | completeness << 30; arg holds
- * the n_bind references of mapped predictions only; act = slot | level << 5.
- * Requires max_candidates <= 31.                                           */
+ * -> narrow CSR streams in session order (decoupled look-back scan).
+ * Capacities: pred/act n*K, arg n*K*B.  hdr = n_pred | n_act << 8;
+ * pred = pattern | completeness << 14; arg holds the n_bind references of
+ * mapped predictions only, as region << 27 | node for a source event
+ * region * n_sessions + session (the live table's event ids; all-ones =
+ * unresolved); act = slot | level << 5.  The expected utility of an action
+ * is p(pattern) * benefit(tool) (policy.py:224-232), which the host redoes
+ * exactly, so it is not shipped.  totals = {predictions, arguments,
+ * actions, refs outside the region form (0 expected: else re-fetch the full
+ * records)}.  Requires max_candidates <= 31 and n_patterns <= 16384.      */
 typedef struct {
   uint16_t* hdr;     /* [n]                                                  */
-  uint32_t* pred;
-  int64_t* arg;
+  uint16_t* pred;
+  uint32_t* arg;
   uint8_t* act;
-  double* util;
-  int64_t* totals;   /* [3]                                                  */
+  int64_t* totals;   /* [4]                                                  */
 } paste_compact_desc;
 
 int64_t paste_compact_scratch_bytes(int64_t n_sessions);

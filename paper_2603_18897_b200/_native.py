@@ -57,7 +57,7 @@ class WindowsDesc(ctypes.Structure):
                 ("tok", c_void_p), ("evt", c_void_p), ("count", c_void_p),
                 ("nodes", c_void_p), ("bytes", c_void_p), ("refs", c_void_p),
                 ("new_tok", c_void_p), ("new_ref", c_void_p), ("new_evt_base", c_int64),
-                ("new_byte_base", c_int64), ("stream_end", c_void_p)]
+                ("new_byte_base", c_int64), ("stream_end", c_void_p), ("new_node", c_void_p)]
 
 
 class PredictOut(ctypes.Structure):
@@ -111,7 +111,7 @@ class ResolveDesc(ctypes.Structure):
 
 class CompactDesc(ctypes.Structure):
     _fields_ = [("hdr", c_void_p), ("pred", c_void_p), ("arg", c_void_p), ("act", c_void_p),
-                ("util", c_void_p), ("totals", c_void_p)]
+                ("totals", c_void_p)]
 
 
 class HoldsDesc(ctypes.Structure):

@@ -1,7 +1,7 @@
 // Record compaction for the live path: fixed K-slot predict records ->
-// CSR streams sized by what each session actually produced, so the
-// host<->device copy of a live step moves ~60 B/session instead of the
-// fixed 204 B (K = 8).
+// narrow CSR streams sized by what each session actually produced, so the
+// device->host copy of a live step moves ~24 B/session instead of the fixed
+// 204 B (K = 8).
 //
 // Single pass with a decoupled look-back scan: CTAs claim 128-session tiles
 // through a ticket counter (tiles are therefore taken in order and every
@@ -10,10 +10,15 @@
 //
 // Streams (all in session order):
 //   hdr[n]      u16  n_pred | n_act << 8
-//   pred[P]     u32  pattern id | completeness << 30
-//   arg[A]      i64  argument refs of MAPPED predictions only (n_bind each)
+//   pred[P]     u16  pattern id | completeness << 14
+//   arg[A]      u32  argument refs of MAPPED predictions only (n_bind each):
+//                    region << 27 | node, where the source event is
+//                    region * n + session (the live table's event ids); a
+//                    ref outside that form is counted in totals[3] and
+//                    written as all-ones (the caller re-fetches full records)
 //   act[Q]      u8   prediction slot | level << 5
-//   util[Q]     f64  expected utility
+// The expected utility of an action is p(pattern) * benefit(tool), one
+// IEEE multiply the host redoes exactly on decode, so it is not shipped.
 #include "common.cuh"
 
 namespace paste {
@@ -95,20 +100,32 @@ __global__ void __launch_bounds__(KT_T) compact_kernel(const paste_predict_out O
     uint64_t a0 = s_excl[1] + s_sum[1][threadIdx.x] - na;
     uint64_t q0 = s_excl[2] + s_sum[2][threadIdx.x] - nq;
     C.hdr[s] = (uint16_t)(np | (nq << 8));
+    unsigned long long wide = 0;
     for (int i = 0; i < np; ++i) {
       const int64_t o = obase + i * ostride;
       const int pid = O.pred_pat[o];
-      C.pred[p0 + i] = (uint32_t)pid | ((uint32_t)O.pred_comp[o] << 30);
+      C.pred[p0 + i] = (uint16_t)(pid | ((int)O.pred_comp[o] << 14));
       const paste_pattern pt = patterns[pid];
       if (pt.flags & PASTE_PF_HAS_MAPPING)
-        for (int b = 0; b < pt.n_bind; ++b)
-          C.arg[a0++] = O.pred_arg[abase + (int64_t)(i * B + b) * ostride];
+        for (int b = 0; b < pt.n_bind; ++b) {
+          const int64_t r = O.pred_arg[abase + (int64_t)(i * B + b) * ostride];
+          uint32_t w = 0xffffffffu;  // unresolved binding
+          if (r >= 0) {
+            const int64_t ev = r >> 32, node = r & 0xffffffffll;
+            const int64_t region = ev / n;
+            if (ev - region * n == s && region < 31 && node < (1ll << 27))
+              w = ((uint32_t)region << 27) | (uint32_t)node;
+            else
+              ++wide;
+          }
+          C.arg[a0++] = w;
+        }
     }
     for (int j = 0; j < nq; ++j) {
       const int64_t o = obase + j * ostride;
       C.act[q0 + j] = (uint8_t)(O.act_pred[o] | (O.act_level[o] << 5));
-      C.util[q0 + j] = O.act_util[o];
     }
+    if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(C.totals + 3), wide);
   }
   if (s == n - 1) {
     C.totals[0] = s_excl[0] + s_sum[0][threadIdx.x];
@@ -131,15 +148,13 @@ extern "C" int paste_compact_records(const paste_predict_out* out, int64_t n_ses
                                      void* scratch, void* stream_) {
   reset_launches();
   PASTE_REQUIRE(out && pool && c && scratch, "null argument");
-  PASTE_REQUIRE(out->max_candidates <= 31 && pool->n_patterns < (1 << 30),
-                "compaction needs max_candidates <= 31");
+  PASTE_REQUIRE(out->max_candidates <= 31 && pool->n_patterns <= (1 << 14),
+                "compaction needs max_candidates <= 31 and at most 16384 patterns");
   cudaStream_t stream = (cudaStream_t)stream_;
   const int64_t tiles = (n_sessions + KT_T - 1) / KT_T;
   PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, paste_compact_scratch_bytes(n_sessions), stream));
-  if (n_sessions == 0) {
-    PASTE_CUDA_CHECK(cudaMemsetAsync(c->totals, 0, 3 * sizeof(int64_t), stream));
-    return PASTE_OK;
-  }
+  PASTE_CUDA_CHECK(cudaMemsetAsync(c->totals, 0, 4 * sizeof(int64_t), stream));
+  if (n_sessions == 0) return PASTE_OK;
   uint64_t* ticket = static_cast<uint64_t*>(scratch);
   compact_kernel<<<(unsigned)tiles, KT_T, 0, stream>>>(*out, n_sessions, pool->patterns, *c, ticket,
                                                        ticket + 1);

@@ -85,7 +85,13 @@ __global__ void __launch_bounds__(256) predict_kernel(const PredictParams P) {
   if (P.win.new_tok != nullptr) {
     const int slot = (int)(cnt % W);
     const int64_t ev = P.win.new_evt_base + sess;
-    paste_event_ref r = P.win.new_ref[sess];
+    paste_event_ref r;
+    if (P.win.new_node != nullptr) {
+      r.node_base = P.win.new_node[sess];
+      r.byte_base = 0;
+    } else {
+      r = P.win.new_ref[sess];
+    }
     r.byte_base += P.win.new_byte_base;
     P.win.refs[ev] = r;
     P.win.tok[ring_at(P.win, sess, slot)] = P.win.new_tok[sess];

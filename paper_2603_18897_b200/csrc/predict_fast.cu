@@ -329,7 +329,13 @@ __device__ __forceinline__ void predict_session(const FastParams& P, int64_t ses
   int32_t new_t = -1;
   if (P.win.new_tok != nullptr) {  // observe (PredictionWindow.observe)
     const int64_t ev = P.win.new_evt_base + sess;
-    paste_event_ref r = P.win.new_ref[sess];
+    paste_event_ref r;
+    if (P.win.new_node != nullptr) {
+      r.node_base = P.win.new_node[sess];
+      r.byte_base = 0;
+    } else {
+      r = P.win.new_ref[sess];
+    }
     r.byte_base += P.win.new_byte_base;
     P.win.refs[ev] = r;
     new_t = P.win.new_tok[sess];

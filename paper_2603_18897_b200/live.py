@@ -36,11 +36,17 @@ class EventBatch:
     tok: object   # i32[n]      (numpy or torch, host or device)
     ref: object   # i64[n, 2]
     data: object  # u8[bytes]
+    node: object = None  # optional i32[n]: node_base only (the narrow wire form)
+
+    def wire(self, ship_bytes: bool) -> tuple:
+        """The arrays a step copies host -> device."""
+        if ship_bytes:
+            return (self.tok, self.ref, self.data)
+        return (self.tok, self.node) if self.node is not None else (self.tok, self.ref)
 
     def nbytes(self, with_data: bool = True) -> int:
-        parts = (self.tok, self.ref, self.data) if with_data else (self.tok, self.ref)
         return sum(int(x.nbytes) if isinstance(x, np.ndarray) else x.numel() * x.element_size()
-                   for x in parts)
+                   for x in self.wire(with_data))
 
 
 class LiveSessionTable:
@@ -72,7 +78,12 @@ class LiveSessionTable:
         self.refs = torch.zeros(self.regions * n * 2, dtype=torch.int64, device=dev)
         self.new_tok = torch.zeros(n, dtype=torch.int32, device=dev)
         self.new_ref = torch.zeros(n * 2, dtype=torch.int64, device=dev)
+        self.new_node = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.narrow = False  # last staged batch came in the narrow (node-only) form
+        if self.regions > 31 or len(nodes) >= (1 << 27):
+            raise ValueError("live table needs capacity <= 30 and < 2^27 template nodes")
         allow, level, bene = admit_tables(dpool.sigs, policy, estimates.duration)
+        self.benefit = np.asarray(bene, np.float64)
         self.adm_arrays = (to_dev(allow), to_dev(level), to_dev(bene))
         self.adm = AdmitDesc(1, len(allow), *[ptr(a) for a in self.adm_arrays])
         self.out = {"n_pred": torch.zeros(n, dtype=torch.int32, device=dev),
@@ -106,20 +117,27 @@ class LiveSessionTable:
         ref = batch.ref if isinstance(batch.ref, t.Tensor) else t.from_numpy(batch.ref)
         data = batch.data if isinstance(batch.data, t.Tensor) else t.from_numpy(batch.data)
         self.new_tok.copy_(tok.reshape(-1), non_blocking=non_blocking)
-        self.new_ref.copy_(ref.reshape(-1), non_blocking=non_blocking)
+        self.narrow = batch.node is not None and not self.ship_bytes
+        if self.narrow:  # node_base only: 8 B/session on the wire with the token
+            node = batch.node if isinstance(batch.node, t.Tensor) else t.from_numpy(batch.node)
+            self.new_node.copy_(node.reshape(-1), non_blocking=non_blocking)
+        else:
+            self.new_ref.copy_(ref.reshape(-1), non_blocking=non_blocking)
         if self.ship_bytes:
             if data.numel() > self.max_batch_bytes:
                 raise ValueError("event batch exceeds the arena region size")
             self.region_bytes(region)[:data.numel()].copy_(data.reshape(-1),
                                                            non_blocking=non_blocking)
 
-    def launch(self, region: int, new_tok=None, new_ref=None) -> None:
+    def launch(self, region: int, new_tok=None, new_ref=None, new_node=None) -> None:
         """observe (new event per session) + predict + admit, one kernel."""
+        if new_tok is None and new_ref is None and new_node is None and self.narrow:
+            new_node = self.new_node
+        ref = None if new_node is not None else (self.new_ref if new_ref is None else new_ref)
         win = WindowsDesc(self.n, self.W, 1, ptr(self.tok), ptr(self.evt), ptr(self.count),
                           ptr(self.nodes), ptr(self.bytes), ptr(self.refs),
-                          ptr(self.new_tok if new_tok is None else new_tok),
-                          ptr(self.new_ref if new_ref is None else new_ref),
-                          region * self.n, region * self.max_batch_bytes)
+                          ptr(self.new_tok if new_tok is None else new_tok), ptr(ref),
+                          region * self.n, region * self.max_batch_bytes, 0, ptr(new_node))
         check(self.lib.paste_predict_batch(ctypes.byref(self.pool_desc), ctypes.byref(win),
                                            ctypes.byref(self.adm), ctypes.byref(self.out_desc),
                                            stream_handle()), self.lib)
@@ -163,22 +181,24 @@ class LiveSessionTable:
 
 @dataclass
 class CompactRecords:
-    """Host copy of the CSR record streams of one live step (compact.cu)."""
+    """Host copy of the narrow CSR record streams of one live step
+    (compact.cu)."""
 
     K: int
     B: int
     hdr: np.ndarray    # u16[n]: n_pred | n_act << 8
-    pred: np.ndarray   # u32[P]: pattern | completeness << 30
-    arg: np.ndarray    # i64[A]: argument refs of mapped predictions
+    pred: np.ndarray   # u16[P]: pattern | completeness << 14
+    arg: np.ndarray    # u32[A]: region << 27 | node (all-ones = unresolved)
     act: np.ndarray    # u8[Q]:  slot | level << 5
-    util: np.ndarray   # f64[Q]
 
     @property
     def nbytes(self) -> int:
-        return 24 + sum(a.nbytes for a in (self.hdr, self.pred, self.arg, self.act, self.util))
+        return 32 + sum(a.nbytes for a in (self.hdr, self.pred, self.arg, self.act))
 
-    def expand(self, patterns: np.ndarray) -> PredictResult:
-        """Back to fixed per-session records (for decoding / comparisons)."""
+    def expand(self, patterns: np.ndarray, benefit: np.ndarray) -> PredictResult:
+        """Back to fixed per-session records (for decoding / comparisons).
+        Utilities are p(pattern) * benefit(target tool): the same IEEE
+        multiply the device did (policy.py:224-232)."""
         K, B = self.K, self.B
         hdr = self.hdr.astype(np.int64)
         n_pred, n_act = hdr & 0xFF, hdr >> 8
@@ -188,19 +208,25 @@ class CompactRecords:
         res.n_act[:] = n_act
         sess = np.repeat(np.arange(n), n_pred)
         slot = np.arange(len(sess)) - np.repeat(np.cumsum(n_pred) - n_pred, n_pred)
-        pid = (self.pred & 0x3FFFFFFF).astype(np.int64)
+        pid = (self.pred & 0x3FFF).astype(np.int64)
         res.pred_pat[sess * K + slot] = pid
-        res.pred_comp[sess * K + slot] = (self.pred >> 30).astype(np.uint8)
+        res.pred_comp[sess * K + slot] = (self.pred >> 14).astype(np.uint8)
         mapped = (patterns["flags"][pid] & 1) != 0
         nb = np.where(mapped, patterns["n_bind"][pid], 0)
         p_sess, p_slot = np.repeat(sess, nb), np.repeat(slot, nb)
         b_idx = np.arange(int(nb.sum())) - np.repeat(np.cumsum(nb) - nb, nb)
-        res.pred_arg[(p_sess * K + p_slot) * B + b_idx] = self.arg
+        a = self.arg.astype(np.int64)
+        ev = (a >> 27) * n + p_sess
+        res.pred_arg[(p_sess * K + p_slot) * B + b_idx] = np.where(
+            a == 0xFFFFFFFF, -1, (ev << 32) | (a & ((1 << 27) - 1)))
         a_sess = np.repeat(np.arange(n), n_act)
         a_slot = np.arange(len(a_sess)) - np.repeat(np.cumsum(n_act) - n_act, n_act)
-        res.act_pred[a_sess * K + a_slot] = (self.act & 31).astype(np.int16)
+        a_pred = (self.act & 31).astype(np.int64)
+        res.act_pred[a_sess * K + a_slot] = a_pred
         res.act_level[a_sess * K + a_slot] = self.act >> 5
-        res.act_util[a_sess * K + a_slot] = self.util
+        a_pid = res.pred_pat[a_sess * K + a_pred]
+        res.act_util[a_sess * K + a_slot] = (patterns["p"][a_pid]
+                                             * benefit[patterns["target_tool"][a_pid]])
         return res
 
 
@@ -209,17 +235,16 @@ def _compact_init(table: "LiveSessionTable") -> None:
     n, K, B = table.n, table.K, table.B
     dev = t.device("cuda")
     table.cbuf = {"hdr": t.zeros(n, dtype=t.int16, device=dev),
-                  "pred": t.zeros(n * K, dtype=t.int32, device=dev),
-                  "arg": t.zeros(n * K * B, dtype=t.int64, device=dev),
+                  "pred": t.zeros(n * K, dtype=t.int16, device=dev),
+                  "arg": t.zeros(n * K * B, dtype=t.int32, device=dev),
                   "act": t.zeros(n * K, dtype=t.uint8, device=dev),
-                  "util": t.zeros(n * K, dtype=t.float64, device=dev),
-                  "totals": t.zeros(3, dtype=t.int64, device=dev)}
+                  "totals": t.zeros(4, dtype=t.int64, device=dev)}
     table.cscratch = t.empty(table.lib.paste_compact_scratch_bytes(n), dtype=t.uint8, device=dev)
     c = table.cbuf
     from ._native import CompactDesc
 
     table.cdesc = CompactDesc(ptr(c["hdr"]), ptr(c["pred"]), ptr(c["arg"]), ptr(c["act"]),
-                              ptr(c["util"]), ptr(c["totals"]))
+                              ptr(c["totals"]))
 
 
 def fetch_compact(table: "LiveSessionTable", pinned: dict | None = None) -> CompactRecords:
@@ -236,14 +261,17 @@ def fetch_compact(table: "LiveSessionTable", pinned: dict | None = None) -> Comp
         pinned = {k: t.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in c.items()}
     pinned["totals"].copy_(c["totals"], non_blocking=True)
     t.cuda.current_stream().synchronize()
-    P, A, Q = (int(x) for x in pinned["totals"].tolist())
-    sizes = {"hdr": table.n, "pred": P, "arg": A, "act": Q, "util": Q}
+    P, A, Q, wide = (int(x) for x in pinned["totals"].tolist())
+    if wide:
+        raise _native.PasteError(f"{wide} argument refs outside the live table's event form: "
+                                 "use fetch()")
+    sizes = {"hdr": table.n, "pred": P, "arg": A, "act": Q}
     for k, m in sizes.items():
         pinned[k][:m].copy_(c[k][:m], non_blocking=True)
     t.cuda.current_stream().synchronize()
     h = {k: pinned[k][:m].numpy() for k, m in sizes.items()}
-    return CompactRecords(table.K, table.B, h["hdr"].view(np.uint16), h["pred"].view(np.uint32),
-                          h["arg"], h["act"], h["util"])
+    return CompactRecords(table.K, table.B, h["hdr"].view(np.uint16), h["pred"].view(np.uint16),
+                          h["arg"].view(np.uint32), h["act"])
 
 
 LiveSessionTable.fetch_compact = fetch_compact

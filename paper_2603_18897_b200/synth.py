@@ -200,7 +200,9 @@ class LiveWorkload:
         tool, ok = self.stream.step()
         kind = payload_kind(tool, ok)
         data, ref = fill_payloads(self.tmpl, kind, self.rng)
-        return EventBatch(tokens(tool, ok, self.tool_ids), ref, data)
+        # the narrow wire form (node_base only) is produced with the batch
+        return EventBatch(tokens(tool, ok, self.tool_ids), ref, data,
+                          np.ascontiguousarray(ref[:, 0], dtype=np.int32))
 
 
 def stress_pool(seed: int = 1001, n_patterns: int = 1000, n_tools: int = 20):
