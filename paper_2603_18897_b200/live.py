@@ -230,21 +230,43 @@ class CompactRecords:
         return res
 
 
-def _compact_init(table: "LiveSessionTable") -> None:
+def _compact_buffers(table: "LiveSessionTable"):
     t = table.torch
     n, K, B = table.n, table.K, table.B
     dev = t.device("cuda")
-    table.cbuf = {"hdr": t.zeros(n, dtype=t.int16, device=dev),
+    return {"hdr": t.zeros(n, dtype=t.int16, device=dev),
                   "pred": t.zeros(n * K, dtype=t.int16, device=dev),
                   "arg": t.zeros(n * K * B, dtype=t.int32, device=dev),
                   "act": t.zeros(n * K, dtype=t.uint8, device=dev),
                   "totals": t.zeros(4, dtype=t.int64, device=dev)}
-    table.cscratch = t.empty(table.lib.paste_compact_scratch_bytes(n), dtype=t.uint8, device=dev)
-    c = table.cbuf
+
+
+def _compact_desc(c: dict):
     from ._native import CompactDesc
 
-    table.cdesc = CompactDesc(ptr(c["hdr"]), ptr(c["pred"]), ptr(c["arg"]), ptr(c["act"]),
-                              ptr(c["totals"]))
+    return CompactDesc(ptr(c["hdr"]), ptr(c["pred"]), ptr(c["arg"]), ptr(c["act"]),
+                       ptr(c["totals"]))
+
+
+def _compact_init(table: "LiveSessionTable") -> None:
+    t = table.torch
+    table.cbuf = _compact_buffers(table)
+    table.cscratch = t.empty(table.lib.paste_compact_scratch_bytes(table.n), dtype=t.uint8,
+                             device="cuda")
+    table.cdesc = _compact_desc(table.cbuf)
+
+
+def _records(table, h: dict) -> CompactRecords:
+    return CompactRecords(table.K, table.B, h["hdr"].view(np.uint16), h["pred"].view(np.uint16),
+                          h["arg"].view(np.uint32), h["act"])
+
+
+def _sizes(table, totals) -> dict:
+    P, A, Q, wide = (int(x) for x in totals.tolist())
+    if wide:
+        raise _native.PasteError(f"{wide} argument refs outside the live table's event form: "
+                                 "use fetch()")
+    return {"hdr": table.n, "pred": P, "arg": A, "act": Q}
 
 
 def fetch_compact(table: "LiveSessionTable", pinned: dict | None = None) -> CompactRecords:
@@ -261,17 +283,76 @@ def fetch_compact(table: "LiveSessionTable", pinned: dict | None = None) -> Comp
         pinned = {k: t.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in c.items()}
     pinned["totals"].copy_(c["totals"], non_blocking=True)
     t.cuda.current_stream().synchronize()
-    P, A, Q, wide = (int(x) for x in pinned["totals"].tolist())
-    if wide:
-        raise _native.PasteError(f"{wide} argument refs outside the live table's event form: "
-                                 "use fetch()")
-    sizes = {"hdr": table.n, "pred": P, "arg": A, "act": Q}
+    sizes = _sizes(table, pinned["totals"])
     for k, m in sizes.items():
         pinned[k][:m].copy_(c[k][:m], non_blocking=True)
     t.cuda.current_stream().synchronize()
-    h = {k: pinned[k][:m].numpy() for k, m in sizes.items()}
-    return CompactRecords(table.K, table.B, h["hdr"].view(np.uint16), h["pred"].view(np.uint16),
-                          h["arg"].view(np.uint32), h["act"])
+    return _records(table, {k: pinned[k][:m].numpy() for k, m in sizes.items()})
 
 
+def serve(table: "LiveSessionTable", batches, depth: int = 2):
+    """Pipelined live steps (the serving loop): step i+1's upload, kernel and
+    compaction run on the compute stream while step i's records download on
+    a copy stream.  Yields each step's CompactRecords in order; a yielded
+    record's arrays are pinned-buffer views, valid until the generator has
+    advanced ``depth`` more steps."""
+    from collections import deque
+
+    t = table.torch
+    if getattr(table, "_serve", None) is None or len(table._serve["bufs"]) != depth:
+        bufs = [_compact_buffers(table) for _ in range(depth)]
+        table._serve = {
+            "bufs": bufs, "descs": [_compact_desc(c) for c in bufs],
+            "pinned": [{k: t.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in c.items()}
+                       for c in bufs],
+            "scratch": [t.empty(table.lib.paste_compact_scratch_bytes(table.n), dtype=t.uint8,
+                                device="cuda") for _ in range(depth)],
+            "copy": t.cuda.Stream(), "tot": t.cuda.Stream(), "free": [None] * depth}
+    sv = table._serve
+    # sized downloads on one copy stream, the small totals reads on another:
+    # step i's totals must not queue behind step i-1's downloads (nor the
+    # reverse), or the downloads would wait for step i's compute
+    comp, copy, tot = t.cuda.current_stream(), sv["copy"], sv["tot"]
+    pending = deque()
+
+    def finish():
+        k, tot_ev = pending.popleft()
+        tot_ev.synchronize()
+        h = sv["pinned"][k]
+        sizes = _sizes(table, h["totals"])
+        c = sv["bufs"][k]
+        with t.cuda.stream(copy):
+            copy.wait_event(tot_ev)
+            for name, m in sizes.items():
+                h[name][:m].copy_(c[name][:m], non_blocking=True)
+            done = t.cuda.Event()
+            done.record(copy)
+        sv["free"][k] = done
+        done.synchronize()
+        return _records(table, {name: h[name][:m].numpy() for name, m in sizes.items()})
+
+    for i, b in enumerate(batches):
+        k = i % depth
+        if sv["free"][k] is not None:  # the set's previous download has finished
+            comp.wait_event(sv["free"][k])
+        table.step(b)
+        check(table.lib.paste_compact_records(ctypes.byref(table.out_desc), table.n,
+                                              ctypes.byref(table.pool_desc),
+                                              ctypes.byref(sv["descs"][k]),
+                                              ptr(sv["scratch"][k]), stream_handle()), table.lib)
+        ready = t.cuda.Event()
+        ready.record(comp)
+        with t.cuda.stream(tot):
+            tot.wait_event(ready)
+            sv["pinned"][k]["totals"].copy_(sv["bufs"][k]["totals"], non_blocking=True)
+            tot_ev = t.cuda.Event()
+            tot_ev.record(tot)
+        pending.append((k, tot_ev))
+        if len(pending) == depth:
+            yield finish()
+    while pending:
+        yield finish()
+
+
+LiveSessionTable.serve = serve
 LiveSessionTable.fetch_compact = fetch_compact

@@ -203,3 +203,31 @@ def test_compact_records_expand_to_the_full_records():
         comp = table.fetch_compact()
         _compare(comp.expand(dp.image.patterns, table.benefit), full)
         assert comp.nbytes < 0.2 * table.output_nbytes()
+
+
+def test_serve_pipeline_yields_the_step_records():
+    """The pipelined serving loop (upload / kernel / compaction of step i+1
+    overlapping the download of step i) returns exactly what the sequential
+    step + fetch_compact returns."""
+    pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
+    dp = DevicePool(pool)
+    n = 30_000
+    policy = parse_policy(MOTIF_POLICY).policy
+    wl_a = LiveWorkload(dp.sigs, dp.keys, n, seed=31)
+    wl_b = LiveWorkload(dp.sigs, dp.keys, n, seed=31)
+    seq = LiveSessionTable(dp, n, wl_a.tmpl.nodes, wl_a.max_batch_bytes, policy, EstimateBook(),
+                           max_candidates=8)
+    pip = LiveSessionTable(dp, n, wl_b.tmpl.nodes, wl_b.max_batch_bytes, policy, EstimateBook(),
+                           max_candidates=8)
+    steps = 20
+    expect = []
+    for _ in range(steps):
+        seq.step(wl_a.next_batch())
+        r = seq.fetch_compact()
+        expect.append(tuple(a.copy() for a in (r.hdr, r.pred, r.arg, r.act)))
+    got = [tuple(a.copy() for a in (r.hdr, r.pred, r.arg, r.act))
+           for r in pip.serve(wl_b.next_batch() for _ in range(steps))]
+    assert len(got) == steps
+    for e, g in zip(expect, got):
+        for x, y in zip(e, g):
+            assert np.array_equal(x, y)
