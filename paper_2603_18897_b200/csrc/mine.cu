@@ -6,20 +6,22 @@
 // _collect_occurrences (mining.py:215-227).
 //
 // Reformulation (verified exact): every count mine()
-// needs is a function of one (k+1)-gram of a session's tool tokens.  For
-// position j of a stream s_0..s_{L-1} (j = L is the END position),
-// T_j = (s_{j-k} .. s_{j-1}, s_j) with BEGIN before the stream and END after
-// it:
-//   * target j (j < L): window = the non-BEGIN part of (s_{j-k}..s_{j-1});
+// needs is a function of the (k+1)-grams of a session's tool tokens.  For
+// position j of a stream s_0..s_{L-1}, T_j = (s_{j-k} .. s_{j-1}, s_j) with
+// BEGIN before the stream:
+//   * target j: window = the non-BEGIN part of (s_{j-k}..s_{j-1});
 //     support[tool(s_j)][c] += 1 for each distinct subsequence c (anchored)
 //     or suffix c (contiguous);
 //   * anchor a = j-1 (s_{j-1} != BEGIN): the contexts that match at a are
 //     u + (s_a) for each distinct subsequence u of the non-BEGIN part of
 //     (s_{j-k}..s_{j-2}) (anchored, rightmost embedding is complete) or the
-//     contiguous suffixes ending at a; match[c] += 1 and, when j < L,
-//     follow[c][tool(s_j)] += 1.
-// So the device counts one histogram H over (k+1)-grams (one warp-aggregated
-// increment per position) and expands the non-zero bins once.
+//     contiguous suffixes ending at a; follow[c][tool(s_j)] += 1.
+//   * match[c] counts every anchor, including a segment's last event (no
+//     target follows it): the anchors whose last k symbols are w number
+//     sum_x H[(x, w)] -- a marginal of the same histogram, so no END grams
+//     are counted.
+// So the device counts one histogram H over (k+1)-grams (one increment per
+// event) and expands it once.
 //
 // Token stream format: int32 sig ids with bit 31 set on the first token of
 // every segment (session after gap splitting).
@@ -51,7 +53,7 @@ __device__ __forceinline__ int64_t ctx_index(const MineGeom& g, const int* c, in
 }
 
 // ---------------------------------------------------------------------------
-// count: one (k+1)-gram per token plus one END gram per segment
+// count: one (k+1)-gram per token
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(MT) count_grams_kernel(const uint32_t* __restrict__ tok,
                                                          int64_t n, MineGeom g,
@@ -77,24 +79,6 @@ __global__ void __launch_bounds__(MT) count_grams_kernel(const uint32_t* __restr
   // warp-aggregated increment (skewed traces repeat grams within a warp)
   const unsigned peers = __match_any_sync(lanes, key);
   if ((__ffs(peers) - 1) == (int)(threadIdx.x & 31)) atomicAdd(hist + key, (uint32_t)__popc(peers));
-  // END gram after the last token of a segment
-  const bool last = (i + 1 == n) || (__ldg(tok + i + 1) & SEG_START);
-  if (last) {
-    int64_t kend = g.S + 1;  // END at d = 0
-    int64_t mul = g.base;
-    bool st = false;
-    for (int d = 1; d <= g.k; ++d) {
-      int sym = g.S;
-      if (!st) {
-        const uint32_t p = __ldg(tok + i - (d - 1));
-        sym = (int)(p & ~SEG_START);
-        st = (p & SEG_START) != 0;
-      }
-      kend += (int64_t)sym * mul;
-      mul *= g.base;
-    }
-    atomicAdd(hist + kend, 1u);
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -189,6 +173,7 @@ __global__ void __launch_bounds__(XT) expand_windows_kernel(
   const bool anchored = relation == PASTE_REL_ANCHORED;
   const int lane = threadIdx.x & 31;
   const int64_t n_win = g.n_bins / base;
+  const int64_t pw_k = n_win;  // base^K
   const int64_t warp0 = ((int64_t)blockIdx.x * XT + threadIdx.x) >> 5;
   const int64_t n_warps = ((int64_t)gridDim.x * XT) >> 5;
   for (int64_t wi = warp0; wi < n_win; wi += n_warps) {
@@ -225,13 +210,16 @@ __global__ void __launch_bounds__(XT) expand_windows_kernel(
     const bool has_anchor = wl > 0;  // s_1 is a real event
     const int n_mt =
         has_anchor ? window_contexts<K>(g, win, wl - 1, anchored, true, sym[1], mt_ctx) : 0;
+    // anchors whose last K symbols are this window: sum over the symbol
+    // before it (hist[x * base^K + wi], all x)
     unsigned long long tot = 0;
+    if (n_mt > 0)
+      for (int x = lane; x < base; x += 32) tot += __ldg(hist + (int64_t)x * pw_k + wi);
     for (int c0 = 0; c0 < base; c0 += 32) {
       const int s0 = c0 + lane;
       const uint32_t h = s0 < base ? __ldg(row + s0) : 0u;
       if (__ballot_sync(0xffffffffu, h != 0) == 0) continue;
-      tot += h;
-      // per-tool sums in the even lane of each (2t, 2t+1) pair; END excluded
+      // per-tool sums in the even lane of each (2t, 2t+1) pair
       const unsigned long long hs = s0 < S ? h : 0u;
       const unsigned long long ht = hs + __shfl_xor_sync(0xffffffffu, hs, 1);
       if ((s0 & 1) || ht == 0) continue;
@@ -624,61 +612,44 @@ __device__ __forceinline__ uint32_t slot_word(const ColumnTile* T, int l, int64_
   const bool b = (T->sess[l] != T->sess[l - 1]) || (__dsub_rn(T->ts[l], T->te[l - 1]) > gap);
   return (uint32_t)T->sig[l] | (b ? SEG_START : 0u);
 }
-// Count the gram ending at an event (window words w[1..K], w[0] = own word)
-// and, after the segment's last event, its END gram.  Hot grams go to the
-// CTA's shared table.  Cold grams go straight to L2 (STAGE = false), or are
-// returned as a staged word for stage_hist_kernel (STAGE = true): the gram
-// key, bit 31 = already counted (hot), bit 30 = END gram still to count.
-constexpr uint32_t STG_HOT = 0x80000000u, STG_END = 0x40000000u, STG_KEY = 0x3fffffffu;
+// Count the gram ending at an event (window words w[1..K], w[0] = own
+// word).  Hot grams go to the CTA's shared table.  Cold grams go straight to
+// L2 (STAGE = false), or are returned as a staged word for
+// stage_hist_kernel (STAGE = true): the gram key, bit 31 = already counted.
+constexpr uint32_t STG_HOT = 0x80000000u, STG_KEY = 0x7fffffffu;
 constexpr int STG_REPS = 8;  // histogram replicas of the L2 pass
 __host__ __device__ inline int64_t stage_words(int64_t n) { return (n + 3) & ~(int64_t)3; }
 
 template <int K, bool STAGE>
-__device__ __forceinline__ uint32_t count_event(const uint32_t (&w)[K + 1], bool last, uint32_t S,
+__device__ __forceinline__ uint32_t count_event(const uint32_t (&w)[K + 1], uint32_t S,
                                                 uint32_t base, uint32_t hot_lo, uint32_t hot_n,
                                                 uint32_t* hot, uint32_t* hist) {
-  uint32_t key = w[0] & 0x7fffffffu, mult = base, kend = S + 1, mul2 = base;
-  bool stop = w[0] >> 31, stop2 = false;
+  uint32_t key = w[0] & 0x7fffffffu, mult = base;
+  bool stop = w[0] >> 31;
 #pragma unroll
   for (int d = 1; d <= K; ++d) {
     key += (stop ? S : (w[d] & 0x7fffffffu)) * mult;
     stop = stop || (w[d] >> 31);
     mult *= base;
-    kend += (stop2 ? S : (w[d - 1] & 0x7fffffffu)) * mul2;
-    stop2 = stop2 || (w[d - 1] >> 31);
-    mul2 *= base;
   }
-  uint32_t word = key;
   if (key - hot_lo < hot_n) {
     atomicAdd(hot + (key - hot_lo), 1u);
-    word |= STG_HOT;
-  } else if (!STAGE) {
-    atomicAdd(hist + key, 1u);
+    return key | STG_HOT;
   }
-  if (last) {
-    if (kend - hot_lo < hot_n) atomicAdd(hot + (kend - hot_lo), 1u);
-    else if (!STAGE) atomicAdd(hist + kend, 1u);
-    else word |= STG_END;
-  }
-  return word;
+  if (!STAGE) atomicAdd(hist + key, 1u);
+  return key;
 }
 
 // Stage 2 of the staged count: the cold grams of the staged words go to L2
 // as REDs, in a pass of their own (interleaved with the columnar stream the
-// same REDs run at well under half their standalone rate).  kend of a
-// segment's last event is END + base * (its gram mod base^K).
-__device__ __forceinline__ void stage_word(uint32_t w, uint32_t end_sym, uint32_t base,
-                                           uint32_t mod_k, uint32_t* __restrict__ hist) {
-  const uint32_t key = w & STG_KEY;
-  if (!(w & STG_HOT)) atomicAdd(hist + key, 1u);
-  if (w & STG_END) atomicAdd(hist + end_sym + base * (key % mod_k), 1u);
+// same REDs run at well under half their standalone rate).
+__device__ __forceinline__ void stage_word(uint32_t w, uint32_t* __restrict__ hist) {
+  if (!(w & STG_HOT)) atomicAdd(hist + w, 1u);
 }
 
 template <int V>
 __global__ void __launch_bounds__(256) stage_hist_kernel(const uint32_t* __restrict__ words,
-                                                         int64_t n, uint32_t end_sym,
-                                                         uint32_t base, uint32_t mod_k,
-                                                         uint32_t* __restrict__ reps,
+                                                         int64_t n, uint32_t* __restrict__ reps,
                                                          int64_t n_bins, int n_reps) {
   // replica per CTA group: a hot bin's updates spread over n_reps addresses
   uint32_t* __restrict__ hist = reps + (int64_t)(blockIdx.x % n_reps) * n_bins;
@@ -688,14 +659,14 @@ __global__ void __launch_bounds__(256) stage_hist_kernel(const uint32_t* __restr
     const int64_t n4 = n >> 2;
     for (int64_t i = t0; i < n4; i += stride) {
       const uint4 v = __ldcs(reinterpret_cast<const uint4*>(words) + i);
-      stage_word(v.x, end_sym, base, mod_k, hist);
-      stage_word(v.y, end_sym, base, mod_k, hist);
-      stage_word(v.z, end_sym, base, mod_k, hist);
-      stage_word(v.w, end_sym, base, mod_k, hist);
+      stage_word(v.x, hist);
+      stage_word(v.y, hist);
+      stage_word(v.z, hist);
+      stage_word(v.w, hist);
     }
-    for (int64_t i = 4 * n4 + t0; i < n; i += stride) stage_word(words[i], end_sym, base, mod_k, hist);
+    for (int64_t i = 4 * n4 + t0; i < n; i += stride) stage_word(words[i], hist);
   } else {
-    for (int64_t i = t0; i < n; i += stride) stage_word(__ldcs(words + i), end_sym, base, mod_k, hist);
+    for (int64_t i = t0; i < n; i += stride) stage_word(__ldcs(words + i), hist);
   }
 }
 
@@ -788,8 +759,8 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
         if (xa <= 0 || xa >= n) v0 = (xa == 0 ? (uint32_t)sg.x : 0u) | SEG_START;
         if (xb >= n) v1 = SEG_START;
       }
-      // halo: lanes < K hold the word of slot l0-1-lane, the rest slot l0+64
-      const int hl = lane < K ? -1 - lane : 64;
+      // halo: lanes < K hold the word of slot l0-1-lane (the rest: unused)
+      const int hl = lane < K ? -1 - lane : -1;
       const uint32_t h = slot_word(T, l0 + hl, x0 + hl, n, gap);
       constexpr int HU = (K + 1) / 2;
       uint32_t up0[HU + 1], up1[HU + 1], hs[K + 1];
@@ -812,14 +783,11 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
         const int f = d / 2;
         w1[d] = d == 1 ? v0 : (lane >= f ? ((d & 1) ? up0[f] : up1[f]) : hs[d - 1]);
       }
-      const uint32_t nx = __shfl_down_sync(0xffffffffu, v0, 1);
-      const bool last0 = v1 >> 31;
-      const bool last1 = (lane == 31 ? h : nx) >> 31;
       constexpr bool STAGE = OUT == 2;
       uint32_t k0 = 0, k1 = 0;
       if (xa < n) {
-        k0 = count_event<K, STAGE>(w0, last0, S, base, hot_lo, hot_n, hot, hist);
-        segs += last0;
+        k0 = count_event<K, STAGE>(w0, S, base, hot_lo, hot_n, hot, hist);
+        segs += v0 >> 31;  // segment starts
         if (xa > 0) {
           const bool back = (ts.x < pts) | ((ts.x == pts) & (sq.x <= pq));
           bad += (ss.x < ps) | ((ss.x == ps) & back);
@@ -827,8 +795,8 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
         if (OUT == 1) tok_out[xa] = (int32_t)v0;
       }
       if (xb < n) {
-        k1 = count_event<K, STAGE>(w1, last1, S, base, hot_lo, hot_n, hot, hist);
-        segs += last1;
+        k1 = count_event<K, STAGE>(w1, S, base, hot_lo, hot_n, hot, hist);
+        segs += v1 >> 31;
         const bool back = (ts.y < ts.x) | ((ts.y == ts.x) & (sq.y <= sq.x));
         bad += (ss.y < ss.x) | ((ss.y == ss.x) & back);
         if (OUT == 1) tok_out[xb] = (int32_t)v1;
@@ -873,8 +841,8 @@ static unsigned long long* tile_counter(cudaStream_t stream) {
 template <int K, int OUT>
 static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint32_t* hist,
                            uint32_t* stage, int64_t tiles, cudaStream_t stream) {
-  // hot grams: positions 2..K all BEGIN (a segment's first two events and
-  // the END gram of a one-event segment), dense index s_0 + base * s_1
+  // hot grams: positions 2..K all BEGIN (a segment's first two events),
+  // dense index s_0 + base * s_1
   uint32_t hot_lo = 0, hot_n = (uint32_t)g.base * (uint32_t)g.base;
   uint32_t pw = hot_n;
   for (int d = 2; d <= K; ++d, pw *= (uint32_t)g.base) hot_lo += (uint32_t)g.S * pw;
@@ -897,14 +865,12 @@ static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint
   columnar_count_kernel<K, OUT><<<(unsigned)grid, CT, smem, stream>>>(c, g, hist, c.tokens_out,
                                                                       stage, ctr, hot_lo, hot_n);
   if (OUT == 2) {
-    uint32_t mod_k = 1;
-    for (int d = 0; d < K; ++d) mod_k *= (uint32_t)g.base;
     uint32_t* reps = stage + stage_words(c.n_events);
     if (cudaMemsetAsync(reps, 0, (size_t)STG_REPS * g.n_bins * sizeof(uint32_t), stream) !=
         cudaSuccess)
       return -2;
     stage_hist_kernel<4><<<(unsigned)(sms * 8), 256, 0, stream>>>(
-        stage, c.n_events, (uint32_t)g.S + 1, (uint32_t)g.base, mod_k, reps, g.n_bins, STG_REPS);
+        stage, c.n_events, reps, g.n_bins, STG_REPS);
     fold_replicas_kernel<<<(unsigned)(sms * 4), 256, 0, stream>>>(reps, g.n_bins, STG_REPS, hist);
   }
   return 0;

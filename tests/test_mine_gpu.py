@@ -166,7 +166,7 @@ def test_columnar_ingest_count_matches_oracle():
             assert np.array_equal(dev.cpu().numpy().astype(np.uint64), ref)
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 4, 6])
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
 def test_columnar_staged_count_equals_single_pass(k):
     """Two-pass (staged words + L2 pass) histogram == the fused single pass ==
     the oracle's tables, including a ragged tail (n not a multiple of 4)."""
