@@ -148,24 +148,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def algorithmic_bytes(res, n, K, B, G=3):
-    """Bytes one step must move per the algorithm (K4):
-    per session 40 + 4G read (count 8, the newest G ring tokens, new event
-    20: token + directory entry) and 44 written (count 8, ring token 4 + event
-    4, directory entry 16, n_pred / n_act / struct_err 12); per prediction 5
-    (pattern, completeness); per resolved binding 28 (source ring event 4 +
-    directory entry 16 read, argument reference 8 written); per action 11."""
-    import numpy as np
-
-    r = res.session_major()
-    n_pred = int(r.n_pred.sum())
-    n_act = int(r.n_act.sum())
-    valid = (np.arange(K)[None, :] < r.n_pred[:, None]).reshape(-1)
-    mapped = valid & (r.pred_comp != 2)
-    n_bind = int(mapped.sum()) * B
-    return n * (84 + 4 * G) + n_pred * 5 + n_bind * 28 + n_act * 11, n_pred, n_act
-
-
 def l2_flush(buf):
     """Evict L2 by streaming a 256 MB read (clean lines: no write-back lands
     inside the next timed step)."""
@@ -202,18 +184,20 @@ def run_ours(args):
     W_, S_ = args.warmup, args.steps
 
     # ---- device-resident loop: stage inputs first ----------------------------
+    # one step = observe + predict + admit for every session, one kernel
+    # (paste_predict_batch), the step's records written to HBM
+    from paper_2603_18897_b200.live import _compact_buffers, _compact_desc
+
     staged = []
-    for i in range(W_ + S_):
+    for i in range(W_ + S_ + 3):
         b = wl.next_batch()
         region = table.steps % table.regions
-        tok = torch.from_numpy(b.tok).cuda()
-        ref = torch.from_numpy(np.ascontiguousarray(b.ref).reshape(-1)).cuda()
-        staged.append((region, tok, ref))
+        staged.append((region, torch.from_numpy(b.tok).cuda(), torch.from_numpy(b.node).cuda()))
         table.steps += 1
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    for region, tok, ref in staged[:W_]:
-        table.launch(region, tok, ref)
+    for region, tok, node in staged[:W_]:
+        table.launch(region, tok, new_node=node)
     torch.cuda.synchronize()
     launches = 0
     G = min(pool.config.k, table.W)
@@ -228,10 +212,10 @@ def run_ours(args):
         t_wall = time.perf_counter()
         # everything is enqueued asynchronously; the flush between steps gives
         # the host time to run ahead, so each event pair brackets the kernel only
-        for (region, tok, ref), (e0, e1) in zip(staged[W_:], events):
+        for (region, tok, node), (e0, e1) in zip(staged[W_:W_ + S_], events):
             l2_flush(flush)
             e0.record(stream)
-            table.launch(region, tok, ref)
+            table.launch(region, tok, new_node=node)
             e1.record(stream)
             launches += lib.paste_last_launch_count()
             # per-step output statistics for the algorithmic-bytes count (async)
@@ -243,7 +227,25 @@ def run_ours(args):
         wall = time.perf_counter() - t_wall
     times = [e0.elapsed_time(e1) / 1e3 for e0, e1 in events]
     preds, n_bind, acts = (int(x) for x in stats.tolist())
-    alg = S_ * n * (84 + 4 * G) + 5 * preds + 28 * n_bind + 11 * acts
+    # DESIGN.md K4: per session 60 + 4G (count, ring tokens, new token + node
+    # read; count, ring slot, directory entry, 3 counters written), per
+    # prediction 5, per resolved binding 28, per action 11
+    alg = S_ * n * (60 + 4 * G) + 5 * preds + 28 * n_bind + 11 * acts
+    # the serving kernel (fused predict + narrow-stream compaction) for reference
+    cbuf = _compact_buffers(table)
+    cdesc = _compact_desc(cbuf)
+    cscratch = torch.empty(lib.paste_predict_compact_scratch_bytes(n), dtype=torch.uint8,
+                           device="cuda")
+    fused = []
+    for region, tok, node in staged[W_ + S_:]:
+        l2_flush(flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        table.launch_compact(region, cdesc, cscratch, new_tok=tok, new_node=node)
+        e1.record(stream)
+        fused.append((e0, e1))
+    torch.cuda.synchronize()
+    fused_ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in fused)
     dev_s = sum(times)
     if world > 1:
         t = torch.tensor([dev_s], device="cuda", dtype=torch.float64)
@@ -296,13 +298,14 @@ def run_ours(args):
                    "parallelism": f"replicas x{world}",
                    "l2": "flushed (256 MB read) between timed steps"},
         "candidates_per_s": world * preds / dev_s,
+        "fused_compact_kernel_ms_per_step": fused_ms,
         "actions_per_s": world * acts / dev_s,
         "e2e": {"value": world * n * S_ / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": h2d // S_, "d2h_bytes_per_step": d2h // S_,
                 "ms_per_step": 1e3 * e2e_s / S_},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": committed_traffic(),
-                     "kernel": "predict_kernel", "algorithmic_bytes_per_launch": alg // S_,
+                     "kernel": "predict_fast_kernel", "algorithmic_bytes_per_launch": alg // S_,
                      "peak_source": f"{peak_kind} hbm_gbs"},
         "gpu_launches": launches,
         "wall_s_timed_region": wall,

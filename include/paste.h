@@ -400,15 +400,28 @@ int paste_resolve(const paste_resolve_desc* d, void* stream);
  * is p(pattern) * benefit(tool) (policy.py:224-232), which the host redoes
  * exactly, so it is not shipped.  totals = {predictions, arguments,
  * actions, refs outside the region form (0 expected: else re-fetch the full
- * records)}.  Requires max_candidates <= 31 and n_patterns <= 16384.      */
+ * records), structural errors (Predictor diagnostics)}.  Requires
+ * max_candidates <= 31 and n_patterns <= 16384.                            */
 typedef struct {
   uint16_t* hdr;     /* [n]                                                  */
   uint16_t* pred;
   uint32_t* arg;
   uint8_t* act;
-  int64_t* totals;   /* [4]                                                  */
+  int64_t* totals;   /* [5]                                                  */
 } paste_compact_desc;
 
+/* The serving step in one kernel: paste_predict_batch (observe + predict +
+ * admit, same semantics) writing the step's records straight into the
+ * narrow streams above instead of K fixed slots per session.  Needs the
+ * match-table fast path (pool compiled with paste_build_match_table for
+ * these max_candidates / window capacity), max_candidates <= 31 and
+ * <= 16384 patterns; PASTE_ERR_UNSUPPORTED otherwise.  `scratch` is device
+ * memory of paste_predict_compact_scratch_bytes(n_sessions) bytes.        */
+int64_t paste_predict_compact_scratch_bytes(int64_t n_sessions);
+int paste_predict_compact(const paste_pool_desc* pool, paste_windows* windows,
+                          const paste_admit_desc* admit, int32_t max_candidates,
+                          int32_t max_bindings, paste_compact_desc* out, void* scratch,
+                          void* stream);
 int64_t paste_compact_scratch_bytes(int64_t n_sessions);
 int paste_compact_records(const paste_predict_out* out, int64_t n_sessions,
                           const paste_pool_desc* pool, paste_compact_desc* c, void* scratch,

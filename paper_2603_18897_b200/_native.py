@@ -152,6 +152,9 @@ EXPORTS = {
     "paste_replay_score": (c_int, [POINTER(PoolDesc), POINTER(ReplayDesc), POINTER(PredictOut),
                                    c_void_p]),
     "paste_compact_scratch_bytes": (c_int64, [c_int64]),
+    "paste_predict_compact_scratch_bytes": (c_int64, [c_int64]),
+    "paste_predict_compact": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc), POINTER(AdmitDesc),
+                                      c_int32, c_int32, POINTER(CompactDesc), c_void_p, c_void_p]),
     "paste_compact_records": (c_int, [POINTER(PredictOut), c_int64, POINTER(PoolDesc),
                                       POINTER(CompactDesc), c_void_p, c_void_p]),
     "paste_leaf_scan": (c_int, [POINTER(LeafScanDesc), c_void_p]),

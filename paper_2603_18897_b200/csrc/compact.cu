@@ -126,6 +126,9 @@ __global__ void __launch_bounds__(KT_T) compact_kernel(const paste_predict_out O
       C.act[q0 + j] = (uint8_t)(O.act_pred[o] | (O.act_level[o] << 5));
     }
     if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(C.totals + 3), wide);
+    if (O.struct_err && O.struct_err[s])
+      atomicAdd(reinterpret_cast<unsigned long long*>(C.totals + 4),
+                (unsigned long long)O.struct_err[s]);
   }
   if (s == n - 1) {
     C.totals[0] = s_excl[0] + s_sum[0][threadIdx.x];
@@ -153,7 +156,7 @@ extern "C" int paste_compact_records(const paste_predict_out* out, int64_t n_ses
   cudaStream_t stream = (cudaStream_t)stream_;
   const int64_t tiles = (n_sessions + KT_T - 1) / KT_T;
   PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, paste_compact_scratch_bytes(n_sessions), stream));
-  PASTE_CUDA_CHECK(cudaMemsetAsync(c->totals, 0, 4 * sizeof(int64_t), stream));
+  PASTE_CUDA_CHECK(cudaMemsetAsync(c->totals, 0, 5 * sizeof(int64_t), stream));
   if (n_sessions == 0) return PASTE_OK;
   uint64_t* ticket = static_cast<uint64_t*>(scratch);
   compact_kernel<<<(unsigned)tiles, KT_T, 0, stream>>>(*out, n_sessions, pool->patterns, *c, ticket,

@@ -308,22 +308,17 @@ __device__ __forceinline__ void admit_one(const FastParams& P, const OutIdx& X, 
   }
 }
 
-template <bool TABLE>
-__device__ __forceinline__ void predict_session(const FastParams& P, int64_t sess, int32_t* gt,
-                                                uint64_t* memo) {
+// observe (PredictionWindow.observe) + gather the newest G tool events of
+// session `sess` into its shared-memory row (gt: tokens by age, age 0 =
+// newest; gs: their ring slots).  Returns how many were gathered.
+__device__ __forceinline__ int observe_gather(const FastParams& P, int64_t sess, int32_t* gt,
+                                              int64_t& rbase, int64_t& rstride) {
   const int64_t n = P.win.n_sessions;
   const int W = P.win.capacity, G = P.G;
   int32_t* gs = gt + G;  // ring slots of the gathered tokens
-  const int64_t rbase = P.win.stream_end ? P.win.stream_end[sess] - P.win.count[sess]
-                                          : (P.win.slot_major ? sess : sess * W);
-  const int64_t rstride = (P.win.slot_major && !P.win.stream_end) ? n : 1;
-  const int K = P.out.max_candidates;
-  OutIdx X;
-  X.B = P.out.max_bindings;
-  X.ostride = P.out.slot_major ? n : 1;
-  X.obase = P.out.slot_major ? sess : sess * K;
-  X.abase = P.out.slot_major ? sess : sess * K * X.B;
-
+  rbase = P.win.stream_end ? P.win.stream_end[sess] - P.win.count[sess]
+                           : (P.win.slot_major ? sess : sess * W);
+  rstride = (P.win.slot_major && !P.win.stream_end) ? n : 1;
   int64_t cnt = P.win.count[sess];
   int head = (int)(cnt % W);  // next slot to write
   int32_t new_t = -1;
@@ -347,21 +342,47 @@ __device__ __forceinline__ void predict_session(const FastParams& P, int64_t ses
     head = head + 1 == W ? 0 : head + 1;
   }
   const int len = (int)(cnt < W ? cnt : W);
-
-  // ---- gather the newest G tool events (age 0 = newest) ---------------------
   int m = 0;
-  {
-    int slot = head;
-    for (int i = 0; i < len && m < G; ++i) {
-      slot = slot == 0 ? W - 1 : slot - 1;
-      const int32_t t = (i == 0 && P.win.new_tok != nullptr) ? new_t : P.win.tok[rbase + slot * rstride];
-      if (t >= 0) {
-        gt[m] = t;
-        gs[m] = slot;
-        ++m;
-      }
+  int slot = head;
+  for (int i = 0; i < len && m < G; ++i) {
+    slot = slot == 0 ? W - 1 : slot - 1;
+    const int32_t t = (i == 0 && P.win.new_tok != nullptr) ? new_t : P.win.tok[rbase + slot * rstride];
+    if (t >= 0) {
+      gt[m] = t;
+      gs[m] = slot;
+      ++m;
     }
   }
+  return m;
+}
+
+// match-table entry of the gathered tokens (the newest G tool tokens)
+__device__ __forceinline__ const uint8_t* table_entry(const FastParams& P, const int32_t* gt,
+                                                      int m) {
+  const int S = P.pool.n_bucket_sigs, G = P.G;
+  int64_t key = gt[0], mult = S;
+  for (int a = 1; a < G; ++a) {
+    const int t = a < m ? gt[a] : S;
+    key += (int64_t)(t < S ? t : S) * mult;
+    mult *= (S + 1);
+  }
+  return static_cast<const uint8_t*>(P.pool.match_table) + key * mt_stride(P.pool.mt_k);
+}
+
+template <bool TABLE>
+__device__ __forceinline__ void predict_session(const FastParams& P, int64_t sess, int32_t* gt,
+                                                uint64_t* memo) {
+  const int64_t n = P.win.n_sessions;
+  const int G = P.G;
+  int32_t* gs = gt + G;  // ring slots of the gathered tokens
+  const int K = P.out.max_candidates;
+  OutIdx X;
+  X.B = P.out.max_bindings;
+  X.ostride = P.out.slot_major ? n : 1;
+  X.obase = P.out.slot_major ? sess : sess * K;
+  X.abase = P.out.slot_major ? sess : sess * K * X.B;
+  int64_t rbase, rstride;
+  const int m = observe_gather(P, sess, gt, rbase, rstride);
 
   const paste_pool_desc& pool = P.pool;
   const bool admit = P.adm.enabled != 0;
@@ -372,13 +393,7 @@ __device__ __forceinline__ void predict_session(const FastParams& P, int64_t ses
   if (m > 0 && gt[0] < S) {
     if (TABLE) {
       // ---- table path: one entry per distinct token context ---------------
-      int64_t key = gt[0], mult = S;
-      for (int a = 1; a < G; ++a) {
-        const int t = a < m ? gt[a] : S;
-        key += (int64_t)(t < S ? t : S) * mult;
-        mult *= (S + 1);
-      }
-      const uint8_t* e = static_cast<const uint8_t*>(pool.match_table) + key * mt_stride(pool.mt_k);
+      const uint8_t* e = table_entry(P, gt, m);
       const int2 hdr = __ldg(reinterpret_cast<const int2*>(e));
       const MTRecord* recs = reinterpret_cast<const MTRecord*>(e + 16);
       n_err = hdr.y;
@@ -504,6 +519,261 @@ __global__ void __launch_bounds__(FT, 8) predict_fast_kernel(const FastParams P)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused predict + compaction (the serving path, paste_predict_compact): the
+// step's records go straight into the narrow CSR streams of
+// paste_compact_desc (compact.cu describes the format) instead of K fixed
+// slots per session that a second kernel then compacts.  Tiles of FT
+// sessions are claimed through a ticket (so every predecessor is running or
+// done) and each session runs in two phases around a decoupled look-back:
+//   1. observe + gather + match-table header: the session's prediction,
+//      argument, action and structural-error counts.  They need no
+//      resolution: one action per distinct allowed tool (admit keeps exactly
+//      one per tool, policy.py:233-236), n_bind arguments per mapped
+//      prediction.
+//   2. with the stream offsets known: resolve, write, admit.
+// ---------------------------------------------------------------------------
+// Tile state (one 128-byte line per tile): flag (0 none, 1 aggregate, 2
+// inclusive prefix), the 4 tile aggregates, the 4 inclusive prefixes.
+constexpr int LB_STRIDE = 16;  // u64 per tile record
+
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+struct CompactParams {
+  FastParams F;
+  paste_compact_desc C;
+  uint64_t* ticket;
+  uint64_t* tile_state;  // [tiles][LB_STRIDE]
+  int64_t n_tiles;
+};
+
+__device__ __forceinline__ bool allowed_tool(const paste_admit_desc& adm, int tool) {
+  return adm.enabled && tool < adm.n_tools && __ldg(adm.allow + tool);
+}
+
+// Phase 1: counts of session `sess` (after observe + gather).
+__device__ __forceinline__ void compact_counts(const FastParams& P, const int32_t* gt, int m,
+                                               const uint8_t*& e, int c[4]) {
+  c[0] = c[1] = c[2] = c[3] = 0;
+  e = nullptr;
+  if (m == 0 || gt[0] >= P.pool.n_bucket_sigs) return;
+  e = table_entry(P, gt, m);
+  const int2 hdr = __ldg(reinterpret_cast<const int2*>(e));
+  const MTRecord* recs = reinterpret_cast<const MTRecord*>(e + 16);
+  const int K = P.out.max_candidates;
+  const int nm = hdr.x < K ? hdr.x : K;
+  c[0] = nm;
+  c[3] = hdr.y;
+  uint64_t seen = 0;
+  for (int i = 0; i < nm; ++i) {
+    const int4 r0 = __ldg(reinterpret_cast<const int4*>(recs + i));
+    const int tool = r0.z, nb = r0.w & 0xffff, pflags = r0.w >> 16;
+    if (pflags & PASTE_PF_HAS_MAPPING) c[1] += nb;
+    if (!allowed_tool(P.adm, tool)) continue;
+    if (tool < 64) {
+      c[2] += !((seen >> tool) & 1ull);
+      seen |= 1ull << tool;
+    } else {
+      bool dup = false;
+      for (int j = 0; j < i && !dup; ++j) dup = __ldg(&recs[j].tool) == tool;
+      c[2] += !dup;
+    }
+  }
+}
+
+// Phase 2: resolve, write and admit session `sess` at stream offsets o[].
+__device__ __forceinline__ void compact_write(const FastParams& P, const paste_compact_desc& C,
+                                              int64_t sess, int64_t rbase, int64_t rstride,
+                                              const int32_t* gt, const uint8_t* e, const int c[4],
+                                              const uint64_t o[3], uint64_t* memo,
+                                              unsigned long long& wide) {
+  const int64_t n = P.win.n_sessions;
+  const int32_t* gs = gt + P.G;
+  const int nm = c[0];
+  C.hdr[sess] = (uint16_t)(nm | (c[2] << 8));
+  if (nm == 0) return;
+  const paste_pool_desc& pool = P.pool;
+  const MTRecord* recs = reinterpret_cast<const MTRecord*>(e + 16);
+  uint64_t a = o[1];
+  int n_act = 0;
+  uint64_t seen = 0;
+  for (int i = 0; i < nm; ++i) {
+    const int4 r0 = __ldg(reinterpret_cast<const int4*>(recs + i));
+    const int4 r1 = __ldg(reinterpret_cast<const int4*>(recs + i) + 1);
+    const int pid = r0.x, tool = r0.z, n_bind = r0.w & 0xffff, pflags = r0.w >> 16;
+    const uint32_t src = (uint32_t)r0.y;
+    const int bind_off = r1.x;
+    const double p = __hiloint2double(r1.w, r1.z);
+    int comp = PASTE_C_TOOL_ONLY;
+    if (pflags & PASTE_PF_HAS_MAPPING) {
+      comp = PASTE_C_FULL;
+      for (int b = 0; b < n_bind; ++b) {
+        const paste_binding bd = pool.bindings[bind_off + b];
+        const int age = (src >> (4 * b)) & 15;
+        const int32_t ev = P.win.evt[rbase + gs[age] * rstride];
+        const int64_t r = resolve_fast(P.win, pool.steps, bd, bind_off + b, ev, age, gt, memo);
+        uint32_t w = 0xffffffffu;  // unresolved
+        if (r < 0) {
+          comp = PASTE_C_PARTIAL;
+        } else {
+          const int64_t node = r & 0xffffffffll, region = (int64_t)ev / n;
+          if ((int64_t)ev - region * n == sess && region < 31 && node < (1ll << 27))
+            w = ((uint32_t)region << 27) | (uint32_t)node;
+          else
+            ++wide;
+        }
+        C.arg[a++] = w;
+      }
+    }
+    C.pred[o[0] + i] = (uint16_t)(pid | (comp << 14));
+    // admit (policy.py:207-236): the streamed first-candidate rule for tools
+    // with benefit >= 0 (or NaN), exact arbitration otherwise
+    if (!allowed_tool(P.adm, tool)) continue;
+    const int implied = comp == PASTE_C_FULL ? 3 : 1;
+    const int cap = __ldg(P.adm.max_level + tool);
+    const uint8_t rec = (uint8_t)(i | ((cap < implied ? cap : implied) << 5));
+    const double bene = __ldg(P.adm.benefit + tool);
+    if (!(bene < 0.0) && tool < 64) {
+      if ((seen >> tool) & 1ull) continue;
+      seen |= 1ull << tool;
+      C.act[o[2] + n_act++] = rec;
+      continue;
+    }
+    int j = 0;
+    for (; j < n_act; ++j)
+      if (__ldg(&recs[C.act[o[2] + j] & 31].tool) == tool) break;
+    if (j == n_act) {
+      C.act[o[2] + n_act++] = rec;
+      continue;
+    }
+    const int ip = C.act[o[2] + j] & 31;
+    const double ipp = __ldg(&recs[ip].p);
+    const double util = __dmul_rn(p, bene), iu = __dmul_rn(ipp, bene);
+    if ((util != iu) ? (util > iu) : (p > ipp)) C.act[o[2] + j] = rec;
+  }
+}
+
+__global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactParams Q) {
+  extern __shared__ uint64_t s_mem[];
+  __shared__ int64_t s_tile;
+  __shared__ uint64_t s_warp[FT / 32][4];
+  __shared__ uint64_t s_excl[4];
+  const FastParams& P = Q.F;
+  uint64_t* memo = s_mem;
+  for (int i = threadIdx.x; i < MEMO; i += FT) memo[i] = 0;
+  int32_t* gt = reinterpret_cast<int32_t*>(s_mem + MEMO) + threadIdx.x * P.row;
+  const int64_t n = P.win.n_sessions;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long wide = 0;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0)
+      s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(Q.ticket), 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= Q.n_tiles) break;
+    const int64_t sess = tile * FT + threadIdx.x;
+    // ---- phase 1: observe, gather, counts ---------------------------------
+    int c[4] = {0, 0, 0, 0};
+    int64_t rbase = 0, rstride = 1;
+    const uint8_t* e = nullptr;
+    if (sess < n) {
+      const int m = observe_gather(P, sess, gt, rbase, rstride);
+      compact_counts(P, gt, m, e, c);
+    }
+    // ---- block-wide exclusive scan of the 4 counters ------------------------
+    uint64_t inc[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint64_t v = (uint64_t)c[k];
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint64_t u = __shfl_up_sync(0xffffffffu, v, off);
+        if (lane >= off) v += u;
+      }
+      inc[k] = v;
+      if (lane == 31) s_warp[warp][k] = v;
+    }
+    __syncthreads();
+    // ---- decoupled look-back, one warp, 32 predecessor tiles per round --------
+    if (warp == 0) {
+      uint64_t agg[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        agg[k] = 0;
+        for (int w = 0; w < FT / 32; ++w) agg[k] += s_warp[w][k];
+      }
+      uint64_t* rec = Q.tile_state + LB_STRIDE * tile;
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) st_relaxed(rec + (tile == 0 ? 5 : 1) + k, agg[k]);
+        __threadfence();
+        st_relaxed(rec, tile == 0 ? 2 : 1);
+      }
+      uint64_t excl[4] = {0, 0, 0, 0};
+      for (int64_t w = tile - 1; w >= 0; w -= 32) {
+        const int64_t idx = w - lane;
+        uint64_t fl = 2;  // before tile 0: an inclusive prefix of 0
+        if (idx >= 0)
+          do {
+            fl = ld_relaxed(Q.tile_state + LB_STRIDE * idx);
+          } while (fl == 0);
+        __threadfence();
+        const unsigned pre = __ballot_sync(0xffffffffu, fl == 2);
+        const int stop = pre ? __ffs(pre) - 1 : 32;  // closest tile holding a prefix
+        uint64_t val[4] = {0, 0, 0, 0};
+        if (idx >= 0 && lane <= stop) {
+          const uint64_t* r = Q.tile_state + LB_STRIDE * idx + (lane == stop ? 5 : 1);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) val[k] = ld_relaxed(r + k);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) val[k] += __shfl_xor_sync(0xffffffffu, val[k], o);
+          excl[k] += val[k];
+        }
+        if (pre) break;
+      }
+      if (lane == 0) {
+        if (tile > 0) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) st_relaxed(rec + 5 + k, excl[k] + agg[k]);
+          __threadfence();
+          st_relaxed(rec, 2);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s_excl[k] = excl[k];
+        if (tile == Q.n_tiles - 1) {  // the last tile publishes the totals
+          Q.C.totals[0] = (int64_t)(excl[0] + agg[0]);
+          Q.C.totals[1] = (int64_t)(excl[1] + agg[1]);
+          Q.C.totals[2] = (int64_t)(excl[2] + agg[2]);
+          Q.C.totals[4] = (int64_t)(excl[3] + agg[3]);
+        }
+      }
+    }
+    __syncthreads();
+    if (sess < n) {
+      uint64_t o[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        uint64_t before = 0;
+        for (int w = 0; w < warp; ++w) before += s_warp[w][k];
+        o[k] = s_excl[k] + before + inc[k] - (uint64_t)c[k];
+      }
+      compact_write(P, Q.C, sess, rbase, rstride, gt, e, c, o, memo, wide);
+    }
+  }
+  if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(Q.C.totals + 3), wide);
+}
+
 // Returns true when the fast path handled the launch.
 bool predict_fast_dispatch(const paste_pool_desc* pool, const paste_windows* win,
                            const paste_admit_desc* adm, const paste_predict_out* out,
@@ -538,4 +808,66 @@ bool predict_fast_dispatch(const paste_pool_desc* pool, const paste_windows* win
   return true;
 }
 
+// Fused predict + compaction launch; false = not eligible (no match table,
+// G > 16, K > 31, ...): the caller runs paste_predict_batch + compaction.
+bool predict_compact_dispatch(const paste_pool_desc* pool, const paste_windows* win,
+                              const paste_admit_desc* adm, int K, int B,
+                              const paste_compact_desc* c, void* scratch, int G,
+                              cudaStream_t stream) {
+  if (G > 16 || K > 31 || pool->match_table == nullptr || pool->mt_k < K || pool->mt_g != G ||
+      pool->max_bindings > MT_MAX_BIND || pool->n_patterns > (1 << 14) || win->stream_end)
+    return false;
+  paste_predict_out out{};
+  out.max_candidates = K;
+  out.max_bindings = B;
+  CompactParams Q{FastParams{*pool, *win, *adm, out, G, 2 * G + 1}, *c,
+                  static_cast<uint64_t*>(scratch), static_cast<uint64_t*>(scratch) + LB_STRIDE,
+                  (win->n_sessions + FT - 1) / FT};
+  const size_t smem = sizeof(uint64_t) * MEMO + sizeof(int32_t) * FT * Q.F.row;
+  static int sms = 0, occ = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, predict_compact_kernel, FT, smem);
+    if (occ < 1) occ = 1;
+  }
+  const int64_t grid = Q.n_tiles < (int64_t)sms * occ ? Q.n_tiles : (int64_t)sms * occ;
+  predict_compact_kernel<<<(unsigned)grid, FT, smem, stream>>>(Q);
+  return true;
+}
+
 }  // namespace paste
+
+extern "C" int64_t paste_predict_compact_scratch_bytes(int64_t n_sessions) {
+  const int64_t tiles = (n_sessions + paste::FT - 1) / paste::FT;
+  return 8 * (paste::LB_STRIDE * tiles + paste::LB_STRIDE);
+}
+
+extern "C" int paste_predict_compact(const paste_pool_desc* pool, paste_windows* windows,
+                                     const paste_admit_desc* admit, int32_t max_candidates,
+                                     int32_t max_bindings, paste_compact_desc* out, void* scratch,
+                                     void* stream) {
+  using namespace paste;
+  reset_launches();
+  PASTE_REQUIRE(pool && windows && admit && out && scratch, "null argument");
+  PASTE_REQUIRE(windows->capacity >= 1 && max_candidates >= 1, "bad window / candidate count");
+  PASTE_REQUIRE(max_bindings >= pool->max_bindings, "max_bindings below pool maximum");
+  PASTE_REQUIRE(!windows->stream_end, "stream-mode windows are not live sessions");
+  cudaStream_t st = (cudaStream_t)stream;
+  PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, paste_predict_compact_scratch_bytes(windows->n_sessions), st));
+  PASTE_CUDA_CHECK(cudaMemsetAsync(out->totals, 0, 5 * sizeof(int64_t), st));
+  if (windows->n_sessions == 0) return PASTE_OK;
+  const int g = pool->relation == PASTE_REL_ANCHORED ? pool->k : pool->max_ctx;
+  const int G = g < windows->capacity ? g : windows->capacity;
+  static const bool force_generic = getenv("PASTE_FORCE_GENERIC") != nullptr;
+  if (force_generic || !predict_compact_dispatch(pool, windows, admit, max_candidates,
+                                                 max_bindings, out, scratch, G, st)) {
+    set_error("fused predict + compaction needs the match-table fast path (K <= 31, "
+              "<= 16384 patterns): use paste_predict_batch + paste_compact_records");
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}

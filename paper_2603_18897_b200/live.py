@@ -142,6 +142,27 @@ class LiveSessionTable:
                                            ctypes.byref(self.adm), ctypes.byref(self.out_desc),
                                            stream_handle()), self.lib)
 
+    def launch_compact(self, region: int, cdesc, scratch, new_tok=None, new_node=None) -> bool:
+        """observe + predict + admit writing the narrow record streams
+        directly (paste_predict_compact); False when the pool / envelope
+        needs the two-kernel path (launch + paste_compact_records)."""
+        if new_tok is None:
+            new_tok = self.new_tok
+            if self.narrow:
+                new_node = self.new_node
+        ref = None if new_node is not None else self.new_ref
+        win = WindowsDesc(self.n, self.W, 1, ptr(self.tok), ptr(self.evt), ptr(self.count),
+                          ptr(self.nodes), ptr(self.bytes), ptr(self.refs), ptr(new_tok),
+                          ptr(ref), region * self.n, region * self.max_batch_bytes, 0,
+                          ptr(new_node))
+        rc = self.lib.paste_predict_compact(ctypes.byref(self.pool_desc), ctypes.byref(win),
+                                            ctypes.byref(self.adm), self.K, self.B,
+                                            ctypes.byref(cdesc), ptr(scratch), stream_handle())
+        if rc == _native.PASTE_ERR_UNSUPPORTED:
+            return False
+        check(rc, self.lib)
+        return True
+
     def step(self, batch: EventBatch) -> None:
         """Stage one batch of new events and run the fused step (async)."""
         region = self.steps % self.regions
@@ -238,7 +259,7 @@ def _compact_buffers(table: "LiveSessionTable"):
                   "pred": t.zeros(n * K, dtype=t.int16, device=dev),
                   "arg": t.zeros(n * K * B, dtype=t.int32, device=dev),
                   "act": t.zeros(n * K, dtype=t.uint8, device=dev),
-                  "totals": t.zeros(4, dtype=t.int64, device=dev)}
+                  "totals": t.zeros(5, dtype=t.int64, device=dev)}
 
 
 def _compact_desc(c: dict):
@@ -262,7 +283,7 @@ def _records(table, h: dict) -> CompactRecords:
 
 
 def _sizes(table, totals) -> dict:
-    P, A, Q, wide = (int(x) for x in totals.tolist())
+    P, A, Q, wide, _err = (int(x) for x in totals.tolist())
     if wide:
         raise _native.PasteError(f"{wide} argument refs outside the live table's event form: "
                                  "use fetch()")
@@ -290,14 +311,18 @@ def fetch_compact(table: "LiveSessionTable", pinned: dict | None = None) -> Comp
     return _records(table, {k: pinned[k][:m].numpy() for k, m in sizes.items()})
 
 
-def serve(table: "LiveSessionTable", batches, depth: int = 2):
-    """Pipelined live steps (the serving loop): step i+1's upload, kernel and
-    compaction run on the compute stream while step i's records download on
-    a copy stream.  Yields each step's CompactRecords in order; a yielded
-    record's arrays are pinned-buffer views, valid until the generator has
-    advanced ``depth`` more steps."""
+def serve(table: "LiveSessionTable", batches, depth: int = 3):
+    """Pipelined live steps (the serving loop).  Step i's upload, fused
+    predict + compaction kernel and totals read run on the compute stream
+    while step i-1's sized record download is queued on a copy stream and
+    step i-2's records are handed out, so the copy engines never wait on the
+    host.  Yields each step's CompactRecords in order; a yielded record's
+    arrays are pinned-buffer views, valid until the generator has advanced
+    ``depth - 1`` more steps."""
     from collections import deque
 
+    if depth < 3:
+        raise ValueError("serve() needs depth >= 3 buffer sets")
     t = table.torch
     if getattr(table, "_serve", None) is None or len(table._serve["bufs"]) != depth:
         bufs = [_compact_buffers(table) for _ in range(depth)]
@@ -305,41 +330,50 @@ def serve(table: "LiveSessionTable", batches, depth: int = 2):
             "bufs": bufs, "descs": [_compact_desc(c) for c in bufs],
             "pinned": [{k: t.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in c.items()}
                        for c in bufs],
-            "scratch": [t.empty(table.lib.paste_compact_scratch_bytes(table.n), dtype=t.uint8,
-                                device="cuda") for _ in range(depth)],
+            "scratch": [t.empty(max(table.lib.paste_compact_scratch_bytes(table.n),
+                                    table.lib.paste_predict_compact_scratch_bytes(table.n)),
+                                dtype=t.uint8, device="cuda") for _ in range(depth)],
             "copy": t.cuda.Stream(), "tot": t.cuda.Stream(), "free": [None] * depth}
     sv = table._serve
     # sized downloads on one copy stream, the small totals reads on another:
     # step i's totals must not queue behind step i-1's downloads (nor the
     # reverse), or the downloads would wait for step i's compute
     comp, copy, tot = t.cuda.current_stream(), sv["copy"], sv["tot"]
-    pending = deque()
+    tot_q, copy_q = deque(), deque()
 
-    def finish():
-        k, tot_ev = pending.popleft()
+    def download(k, tot_ev):
         tot_ev.synchronize()
         h = sv["pinned"][k]
         sizes = _sizes(table, h["totals"])
         c = sv["bufs"][k]
         with t.cuda.stream(copy):
-            copy.wait_event(tot_ev)
             for name, m in sizes.items():
                 h[name][:m].copy_(c[name][:m], non_blocking=True)
             done = t.cuda.Event()
             done.record(copy)
         sv["free"][k] = done
+        copy_q.append((k, sizes, done))
+
+    def hand_out():
+        k, sizes, done = copy_q.popleft()
         done.synchronize()
+        h = sv["pinned"][k]
         return _records(table, {name: h[name][:m].numpy() for name, m in sizes.items()})
 
     for i, b in enumerate(batches):
         k = i % depth
         if sv["free"][k] is not None:  # the set's previous download has finished
             comp.wait_event(sv["free"][k])
-        table.step(b)
-        check(table.lib.paste_compact_records(ctypes.byref(table.out_desc), table.n,
-                                              ctypes.byref(table.pool_desc),
-                                              ctypes.byref(sv["descs"][k]),
-                                              ptr(sv["scratch"][k]), stream_handle()), table.lib)
+        region = table.steps % table.regions
+        table.stage(b, region)
+        if not table.launch_compact(region, sv["descs"][k], sv["scratch"][k]):
+            table.launch(region)
+            check(table.lib.paste_compact_records(ctypes.byref(table.out_desc), table.n,
+                                                  ctypes.byref(table.pool_desc),
+                                                  ctypes.byref(sv["descs"][k]),
+                                                  ptr(sv["scratch"][k]), stream_handle()),
+                  table.lib)
+        table.steps += 1
         ready = t.cuda.Event()
         ready.record(comp)
         with t.cuda.stream(tot):
@@ -347,11 +381,15 @@ def serve(table: "LiveSessionTable", batches, depth: int = 2):
             sv["pinned"][k]["totals"].copy_(sv["bufs"][k]["totals"], non_blocking=True)
             tot_ev = t.cuda.Event()
             tot_ev.record(tot)
-        pending.append((k, tot_ev))
-        if len(pending) == depth:
-            yield finish()
-    while pending:
-        yield finish()
+        tot_q.append((k, tot_ev))
+        if len(tot_q) > 1:
+            download(*tot_q.popleft())
+        if len(copy_q) > 1:
+            yield hand_out()
+    while tot_q:
+        download(*tot_q.popleft())
+    while copy_q:
+        yield hand_out()
 
 
 LiveSessionTable.serve = serve

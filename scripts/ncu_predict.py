@@ -23,3 +23,7 @@ table = LiveSessionTable(dp, n, wl.tmpl.nodes, wl.max_batch_bytes, policy, book,
 for _ in range(table.W + 3):
     table.step(wl.next_batch())
 torch.cuda.synchronize()
+# the fused serving kernel (paste_predict_compact), a few steps
+for _ in table.serve([wl.next_batch() for _ in range(4)]):
+    pass
+torch.cuda.synchronize()

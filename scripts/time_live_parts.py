@@ -62,11 +62,11 @@ bigh = torch.empty(24_000_000, dtype=torch.uint8, pin_memory=True)
 timed("D2H one 24 MB copy", lambda: bigh.copy_(big, non_blocking=True))
 timed("H2D one 24 MB copy", lambda: big.copy_(bigh, non_blocking=True))
 timed("fetch_compact (full)", lambda: table.fetch_compact(pinned), reps=5)
-batches = [wl.next_batch() for _ in range(12)]
+batches = [wl.next_batch() for _ in range(42)]
 for bb in batches:
     bb.tok = torch.from_numpy(bb.tok).pin_memory()
     bb.node = torch.from_numpy(bb.node).pin_memory()
-for depth in (2, 3):
+for depth in (3, 4):
     for _ in table.serve(batches[:2], depth=depth):
         pass
     torch.cuda.synchronize()

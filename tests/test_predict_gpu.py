@@ -205,20 +205,30 @@ def test_compact_records_expand_to_the_full_records():
         assert comp.nbytes < 0.2 * table.output_nbytes()
 
 
-def test_serve_pipeline_yields_the_step_records():
-    """The pipelined serving loop (upload / kernel / compaction of step i+1
-    overlapping the download of step i) returns exactly what the sequential
-    step + fetch_compact returns."""
+@pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3"])
+def test_serve_pipeline_yields_the_step_records(variant):
+    """The pipelined serving loop (fused predict + compaction kernel, step
+    i+1's upload / compute overlapping step i's download) returns exactly
+    what the sequential step (K-slot records) + compaction kernel returns."""
+    from paper_2603_18897_b200.policy import SpeculationPolicy
+
     pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
     dp = DevicePool(pool)
     n = 30_000
     policy = parse_policy(MOTIF_POLICY).policy
+    book = EstimateBook()
+    K = 8
+    if variant == "negative_benefit":  # exact _beats arbitration path
+        book.update("search", -700.0)
+        book.update("terminal", -5.0)
+    if variant == "allow_all_k3":
+        policy, K = SpeculationPolicy(default_allow=True), 3
     wl_a = LiveWorkload(dp.sigs, dp.keys, n, seed=31)
     wl_b = LiveWorkload(dp.sigs, dp.keys, n, seed=31)
-    seq = LiveSessionTable(dp, n, wl_a.tmpl.nodes, wl_a.max_batch_bytes, policy, EstimateBook(),
-                           max_candidates=8)
-    pip = LiveSessionTable(dp, n, wl_b.tmpl.nodes, wl_b.max_batch_bytes, policy, EstimateBook(),
-                           max_candidates=8)
+    seq = LiveSessionTable(dp, n, wl_a.tmpl.nodes, wl_a.max_batch_bytes, policy, book,
+                           max_candidates=K)
+    pip = LiveSessionTable(dp, n, wl_b.tmpl.nodes, wl_b.max_batch_bytes, policy, book,
+                           max_candidates=K)
     steps = 20
     expect = []
     for _ in range(steps):
