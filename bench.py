@@ -315,7 +315,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget_s)
     if args.mine_events > 0:
-        del table, staged, host_batches, cpinned
+        del table, staged, host_batches
         torch.cuda.empty_cache()
         out["mining"] = run_mining(args, world, rank, local)
     if args.long_sessions > 0:

@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(MT) count_grams_kernel(const uint32_t* __restr
 // subsequence exactly once without comparing masks.  Length-1 contexts and
 // tool_count (hit by every window) accumulate in shared memory per CTA.
 // ---------------------------------------------------------------------------
-constexpr int XT = 256;                 // threads per expand CTA
+constexpr int XT = 512;                 // threads per expand CTA
 constexpr int XSMEM_CELLS = 4096;       // u64 cells for the length-1 / tool caches
 
 template <int K>
@@ -345,7 +345,7 @@ __global__ void select_keyed_kernel(MineGeom g, const unsigned long long* tool_c
                                    (unsigned long long)(c - g.ctx_off[len]));
 }
 
-constexpr int RI = 256, RJ = 512;
+constexpr int RI = 256, RJ = 128;
 
 __global__ void __launch_bounds__(RI) rank_keys_kernel(const ulonglong2* __restrict__ keys,
                                                        const unsigned long long* n_out,
@@ -457,7 +457,7 @@ extern "C" int paste_mine_expand(const paste_mine_desc* d, void* stream) {
   }
   const int64_t n_win = g.n_bins / g.base;
   const int64_t want = (n_win + XT / 32 - 1) / (XT / 32);
-  const int64_t cap = (int64_t)sms * 4;
+  const int64_t cap = (int64_t)sms * 2;
   const unsigned grid = (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
   const int use_cache = (int64_t)g.T + 2 * (int64_t)g.T * g.S + g.S <= XSMEM_CELLS;
   int rc = -1;
@@ -642,32 +642,41 @@ __device__ __forceinline__ uint32_t count_event(const uint32_t (&w)[K + 1], uint
 
 // Stage 2 of the staged count: the cold grams of the staged words go to L2
 // as REDs, in a pass of their own (interleaved with the columnar stream the
-// same REDs run at well under half their standalone rate).
-__device__ __forceinline__ void stage_word(uint32_t w, uint32_t* __restrict__ hist) {
-  if (!(w & STG_HOT)) atomicAdd(hist + w, 1u);
-}
+// same REDs run at well under half their standalone rate).  The pass is
+// RED-issue bound (lg_throttle), so the third-event grams (BEGIN, s_2, s_1,
+// s_0) -- a dense base^3 block, and the most contended one -- are counted
+// in shared memory (one CTA per SM) and flushed once.
+constexpr int SH_T = 1024;
+constexpr int SH_DENSE_MAX = 40000;  // u32 counters (160 KB)
 
-template <int V>
-__global__ void __launch_bounds__(256) stage_hist_kernel(const uint32_t* __restrict__ words,
-                                                         int64_t n, uint32_t* __restrict__ reps,
-                                                         int64_t n_bins, int n_reps) {
+__global__ void __launch_bounds__(SH_T, 1) stage_hist_kernel(const uint32_t* __restrict__ words,
+                                                             int64_t n, uint32_t* __restrict__ reps,
+                                                             int64_t n_bins, int n_reps,
+                                                             uint32_t dlo, uint32_t dn) {
+  extern __shared__ uint32_t dense[];
+  for (uint32_t i = threadIdx.x; i < dn; i += SH_T) dense[i] = 0;
+  __syncthreads();
   // replica per CTA group: a hot bin's updates spread over n_reps addresses
   uint32_t* __restrict__ hist = reps + (int64_t)(blockIdx.x % n_reps) * n_bins;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (V == 4) {
-    const int64_t n4 = n >> 2;
-    for (int64_t i = t0; i < n4; i += stride) {
-      const uint4 v = __ldcs(reinterpret_cast<const uint4*>(words) + i);
-      stage_word(v.x, hist);
-      stage_word(v.y, hist);
-      stage_word(v.z, hist);
-      stage_word(v.w, hist);
-    }
-    for (int64_t i = 4 * n4 + t0; i < n; i += stride) stage_word(words[i], hist);
-  } else {
-    for (int64_t i = t0; i < n; i += stride) stage_word(__ldcs(words + i), hist);
+  const int64_t stride = (int64_t)gridDim.x * SH_T;
+  const int64_t t0 = (int64_t)blockIdx.x * SH_T + threadIdx.x;
+  const int64_t n4 = n >> 2;
+  auto one = [&](uint32_t w) {
+    if (w & STG_HOT) return;
+    if (w - dlo < dn) atomicAdd(dense + (w - dlo), 1u);
+    else atomicAdd(hist + w, 1u);
+  };
+  for (int64_t i = t0; i < n4; i += stride) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(words) + i);
+    one(v.x);
+    one(v.y);
+    one(v.z);
+    one(v.w);
   }
+  for (int64_t i = 4 * n4 + t0; i < n; i += stride) one(words[i]);
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < dn; i += SH_T)
+    if (dense[i]) atomicAdd(hist + dlo + i, dense[i]);
 }
 
 // hist += sum of the replicas (one pass over n_reps * n_bins words in L2)
@@ -869,8 +878,22 @@ static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint
     if (cudaMemsetAsync(reps, 0, (size_t)STG_REPS * g.n_bins * sizeof(uint32_t), stream) !=
         cudaSuccess)
       return -2;
-    stage_hist_kernel<4><<<(unsigned)(sms * 8), 256, 0, stream>>>(
-        stage, c.n_events, reps, g.n_bins, STG_REPS);
+    // dense block (k = 3): grams whose oldest symbol is BEGIN -- a segment's
+    // third event -- when their base^3 counters fit in shared memory
+    uint32_t dlo = 0, dn = 0;
+    const uint64_t b3 = (uint64_t)g.base * g.base * g.base;
+    if (K == 3 && b3 <= (uint64_t)SH_DENSE_MAX) {
+      dlo = (uint32_t)((uint64_t)g.S * b3);
+      dn = (uint32_t)b3;
+    }
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(stage_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           SH_DENSE_MAX * (int)sizeof(uint32_t));
+      attr = true;
+    }
+    stage_hist_kernel<<<(unsigned)sms, SH_T, dn * sizeof(uint32_t), stream>>>(
+        stage, c.n_events, reps, g.n_bins, STG_REPS, dlo, dn);
     fold_replicas_kernel<<<(unsigned)(sms * 4), 256, 0, stream>>>(reps, g.n_bins, STG_REPS, hist);
   }
   return 0;
@@ -972,7 +995,7 @@ extern "C" int paste_mine_select_sorted(const paste_mine_desc* d, int64_t sigma,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  rank_keys_kernel<<<(unsigned)(sms * 4), RI, 0, st>>>(keys, cnt, cap, rank);
+  rank_keys_kernel<<<(unsigned)(sms * 8), RI, 0, st>>>(keys, cnt, cap, rank);
   scatter_rows_kernel<<<(unsigned)(sms * 2), 256, 0, st>>>(rows, rank, cnt, cap,
                                                           reinterpret_cast<SelRow*>(out));
   count_launch(3);
