@@ -94,6 +94,38 @@ __host__ __device__ __forceinline__ int64_t arg_at(const paste_predict_out& o, i
                       : (sess * o.max_candidates + i) * o.max_bindings + b;
 }
 
+// ---------------------------------------------------------------------------
+// byte-range helpers: 32-bit word loads (2 aligned loads + funnel shift) so a
+// ~20-byte comparison is ~10 loads in flight instead of ~40 dependent byte
+// loads.  Loads never touch a 4-byte word that holds no byte of the range, so
+// they stay inside the allocation.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_part(const uint8_t* p, int r) {  // r in 1..4 bytes
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+  const uint32_t sh = (uint32_t)(a & 3);
+  const uint32_t lo = __ldg(w);
+  const uint32_t hi = (sh + r > 4) ? __ldg(w + 1) : 0u;
+  const uint32_t v = __funnelshift_r(lo, hi, sh * 8);
+  return r >= 4 ? v : (v & ((1u << (8 * r)) - 1u));
+}
+
+__device__ __forceinline__ bool bytes_eq(const uint8_t* a, const uint8_t* b, int64_t n) {
+  for (int64_t k = 0; k < n; k += 16) {
+    uint32_t diff = 0;
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+      const int64_t r = n - k - j;
+      if (r > 0) {
+        const int rr = r < 4 ? (int)r : 4;
+        diff |= ld_part(a + k + j, rr) ^ ld_part(b + k + j, rr);
+      }
+    }
+    if (diff) return false;
+  }
+  return true;
+}
+
 // K4 fast path (predict_fast.cu); false = not eligible, use the generic kernel
 bool predict_fast_dispatch(const paste_pool_desc* pool, const paste_windows* win,
                            const paste_admit_desc* adm, const paste_predict_out* out, int G,

@@ -33,45 +33,112 @@ __device__ __forceinline__ const uint8_t* canon_bytes(const uint8_t* bytes, int6
   return p;
 }
 
-__global__ void leaf_scan_kernel(const paste_leaf_scan_desc D) {
-  const int64_t q = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+// A candidate is a leaf of the target's type class with the target's
+// canonical length; only candidates need a byte comparison.  They are rare
+// per 32-node sweep (a url_list has a third of its nodes as same-length
+// strings), so each warp queues candidate node indices in shared memory (in
+// node order) and compares 32 at a time, one per lane: full lanes instead of
+// a few active lanes per sweep.  Matches are emitted in queue order = node
+// order = pre-order.
+constexpr int LS_T = 256;
+constexpr int LS_TW = 64;  // target words staged per warp (targets up to 256 bytes)
+
+// candidate bytes == the staged (zero-padded) target words, 8 bytes per check
+__device__ __forceinline__ bool eq_target(const uint8_t* a, const uint32_t* tw, int len) {
+  for (int k = 0; k < len; k += 8) {
+    const int r0 = len - k < 4 ? len - k : 4;
+    uint32_t d = ld_part(a + k, r0) ^ tw[k >> 2];
+    if (len - k > 4) {
+      const int r1 = len - k - 4 < 4 ? len - k - 4 : 4;
+      d |= ld_part(a + k + 4, r1) ^ tw[(k >> 2) + 1];
+    }
+    if (d) return false;
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(LS_T) leaf_scan_kernel(const paste_leaf_scan_desc D) {
+  __shared__ int32_t queue[LS_T / 32][64];
+  __shared__ uint32_t tword[LS_T / 32][LS_TW];
+  const int64_t q = (int64_t)blockIdx.x * (LS_T / 32) + threadIdx.x / 32;
   const int lane = threadIdx.x & 31;
+  int32_t* wq = queue[threadIdx.x / 32];
+  uint32_t* tw = tword[threadIdx.x / 32];
   if (q >= D.n_queries) return;
   const paste_event_ref ref = D.refs[D.event[q]];
   const Node root = load_node(D.nodes, ref.node_base);
   const int64_t n_nodes = root.size();
-  const int64_t limit = n_nodes < D.node_budget ? n_nodes : D.node_budget;
+  const int limit = (int)(n_nodes < D.node_budget ? n_nodes : D.node_budget);
   // target scalar
   const int tt = D.target_type[q];
   const uint8_t* tb = D.target_bytes + D.target_off[q];
   const uint32_t tl = (uint32_t)(D.target_off[q + 1] - D.target_off[q]);
   const bool tnan = D.target_nan[q] != 0;
+  const bool no_bytes = tt == PASTE_T_NULL || tt == PASTE_T_TRUE || tt == PASTE_T_FALSE;
+  const bool staged = tl <= 4 * LS_TW;
+  if (staged)
+    for (int j = lane; j < LS_TW; j += 32) {
+      const int r = (int)tl - 4 * j;
+      tw[j] = r > 0 ? ld_part(tb + 4 * j, r < 4 ? r : 4) : 0u;
+    }
+  __syncwarp();
   int64_t n_out = 0;
   const int64_t out0 = D.out_off[q], cap = D.out_off[q + 1] - out0;
-  for (int64_t base = 0; base < limit; base += 32) {
-    const int64_t i = base + lane;
-    bool eq = false;
-    if (i < limit && !tnan && tt >= 0) {
-      const Node nd = load_node(D.nodes, ref.node_base + i);
-      const int t = nd.type();
-      if (t < PASTE_T_LIST && type_class(t) == tt && !(nd.flags() & PASTE_F_NAN)) {
-        if (t == PASTE_T_NULL || t == PASTE_T_TRUE || t == PASTE_T_FALSE) {
-          eq = true;
-        } else {
-          uint32_t len;
-          const uint8_t* b = canon_bytes(D.bytes, ref.byte_base, nd, &len);
-          eq = len == tl;
-          for (uint32_t k = 0; eq && k < len; ++k) eq = b[k] == tb[k];
+  const paste_tape_node* nodes = D.nodes + ref.node_base;
+  const uint8_t* bytes = D.bytes + ref.byte_base;
+  if (tnan || tt < 0 || tt >= PASTE_T_LIST) goto done;
+  {
+    int qn = 0;  // queued candidates (warp-uniform)
+    for (int base = 0; base < limit; base += 32) {
+      const int i = base + lane;
+      bool cand = false;
+      if (i < limit) {
+        const Node nd = load_node(nodes, i);
+        const int t = nd.type();
+        if (type_class(t) == tt && !(nd.flags() & PASTE_F_NAN)) {
+          if (no_bytes) {
+            cand = true;
+          } else {
+            uint32_t len;
+            canon_bytes(bytes, 0, nd, &len);
+            cand = len == tl;
+          }
         }
       }
+      const unsigned m = __ballot_sync(0xffffffffu, cand);
+      if (cand) wq[qn + __popc(m & ((1u << lane) - 1))] = i;
+      qn += __popc(m);
+      const bool last = base + 32 >= limit;
+      while (qn >= 32 || (last && qn > 0)) {
+        __syncwarp();
+        const int k = qn < 32 ? qn : 32;
+        bool eq = false;
+        int32_t idx = 0;
+        if (lane < k) {
+          idx = wq[lane];
+          if (no_bytes) {
+            eq = true;
+          } else {
+            const Node nd = load_node(nodes, idx);
+            uint32_t len;
+            const uint8_t* bp = canon_bytes(bytes, 0, nd, &len);
+            eq = staged ? eq_target(bp, tw, (int)len) : bytes_eq(bp, tb, len);
+          }
+        }
+        const unsigned em = __ballot_sync(0xffffffffu, eq);
+        if (eq) {
+          const int64_t slot = n_out + __popc(em & ((1u << lane) - 1));
+          if (slot < cap) D.out_nodes[out0 + slot] = idx;
+        }
+        n_out += __popc(em);
+        __syncwarp();
+        if (lane + 32 < qn) wq[lane] = wq[lane + 32];
+        qn -= k;
+        __syncwarp();
+      }
     }
-    const unsigned m = __ballot_sync(0xffffffffu, eq);
-    if (eq) {
-      const int64_t slot = n_out + __popc(m & ((1u << lane) - 1));
-      if (slot < cap) D.out_nodes[out0 + slot] = (int32_t)i;
-    }
-    n_out += __popc(m);
   }
+done:
   if (lane == 0) {
     D.n_out[q] = n_out;
     D.truncated[q] = n_nodes > D.node_budget;
