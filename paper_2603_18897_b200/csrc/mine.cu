@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(MT) count_grams_kernel(const uint32_t* __restr
 // subsequence exactly once without comparing masks.  Length-1 contexts and
 // tool_count (hit by every window) accumulate in shared memory per CTA.
 // ---------------------------------------------------------------------------
-constexpr int XT = 512;                 // threads per expand CTA
+constexpr int XT = 256;                 // threads per expand CTA
 constexpr int XSMEM_CELLS = 4096;       // u64 cells for the length-1 / tool caches
 
 template <int K>
@@ -154,21 +154,32 @@ __device__ __forceinline__ int window_contexts(const MineGeom& g, const int* w, 
   return n;
 }
 
+// 64-bit add into a (lo, hi) pair of shared u32 counters with native 32-bit
+// atomics (a shared u64 atomicAdd compiles to a CAS loop)
+__device__ __forceinline__ void smem_add64(uint32_t* cell, unsigned long long v) {
+  const uint32_t lo = (uint32_t)v;
+  uint32_t hi = (uint32_t)(v >> 32);
+  const uint32_t old = atomicAdd(cell, lo);
+  hi += (uint32_t)(old + lo < old);  // carry
+  if (hi) atomicAdd(cell + 1, hi);
+}
+
 template <int K>
 __global__ void __launch_bounds__(XT) expand_windows_kernel(
     const uint32_t* __restrict__ hist, MineGeom g, int relation, unsigned long long* tool_count,
     unsigned long long* support, unsigned long long* match, unsigned long long* follow,
     int use_cache) {
-  // cache: tool_count[T] | support[T][S] (length-1) | match[S] | follow[S][T]
-  __shared__ unsigned long long cache[XSMEM_CELLS];
+  // cache (u64 as lo/hi u32 pairs): tool_count[T] | support[T][S] (length-1)
+  // | match[S] | follow[S][T]
+  __shared__ uint32_t cache[2 * XSMEM_CELLS];
   const int S = g.S, T = g.T, base = g.base, BEGIN = S, END = S + 1;
-  unsigned long long* c_tool = cache;
-  unsigned long long* c_sup = cache + T;
-  unsigned long long* c_match = c_sup + (int64_t)T * S;
-  unsigned long long* c_follow = c_match + S;
+  uint32_t* c_tool = cache;
+  uint32_t* c_sup = cache + 2 * T;
+  uint32_t* c_match = c_sup + 2 * (int64_t)T * S;
+  uint32_t* c_follow = c_match + 2 * S;
   const int cells = T + 2 * T * S + S;
   if (use_cache)
-    for (int i = threadIdx.x; i < cells; i += XT) cache[i] = 0;
+    for (int i = threadIdx.x; i < 2 * cells; i += XT) cache[i] = 0;
   __syncthreads();
   const bool anchored = relation == PASTE_REL_ANCHORED;
   const int lane = threadIdx.x & 31;
@@ -180,11 +191,11 @@ __global__ void __launch_bounds__(XT) expand_windows_kernel(
     // decode the window, oldest first; BEGINs must be a prefix, no END
     int sym[K + 1];
     {
-      int64_t v = wi;
+      uint32_t v = (uint32_t)wi;  // n_win < 2^31 (geometry check)
 #pragma unroll
       for (int d = 1; d <= K; ++d) {
-        sym[d] = (int)(v % base);
-        v /= base;
+        sym[d] = (int)(v % (uint32_t)base);
+        v /= (uint32_t)base;
       }
     }
     int nb = 0;
@@ -224,20 +235,20 @@ __global__ void __launch_bounds__(XT) expand_windows_kernel(
       const unsigned long long ht = hs + __shfl_xor_sync(0xffffffffu, hs, 1);
       if ((s0 & 1) || ht == 0) continue;
       const int t = s0 >> 1;
-      if (use_cache) atomicAdd(c_tool + t, ht);
+      if (use_cache) smem_add64(c_tool + 2 * t, ht);
       else atomicAdd(tool_count + t, ht);
 #pragma unroll
       for (int q = 0; q < (1 << K); ++q) {
         if (q >= n_sup) break;
         const int64_t c = sup_ctx[q];
-        if (use_cache && c < S) atomicAdd(c_sup + (int64_t)t * S + c, ht);
+        if (use_cache && c < S) smem_add64(c_sup + 2 * ((int64_t)t * S + c), ht);
         else atomicAdd(support + (int64_t)t * g.n_ctx + c, ht);
       }
 #pragma unroll
       for (int q = 0; q < (1 << K); ++q) {
         if (q >= n_mt) break;
         const int64_t c = mt_ctx[q];
-        if (use_cache && c < S) atomicAdd(c_follow + c * T + t, ht);
+        if (use_cache && c < S) smem_add64(c_follow + 2 * (c * T + t), ht);
         else atomicAdd(follow + c * T + t, ht);
       }
     }
@@ -250,14 +261,15 @@ __global__ void __launch_bounds__(XT) expand_windows_kernel(
 #pragma unroll
       for (int q = 0; q < (1 << K); ++q)
         if (q == lane) c = mt_ctx[q];
-      if (use_cache && c < S) atomicAdd(c_match + c, tot);
+      if (use_cache && c < S) smem_add64(c_match + 2 * c, tot);
       else atomicAdd(match + c, tot);
     }
   }
   if (!use_cache) return;
   __syncthreads();
   for (int i = threadIdx.x; i < cells; i += XT) {
-    const unsigned long long v = cache[i];
+    const unsigned long long v =
+        (unsigned long long)cache[2 * i] | ((unsigned long long)cache[2 * i + 1] << 32);
     if (v == 0) continue;
     if (i < T) {
       atomicAdd(tool_count + i, v);
@@ -457,7 +469,7 @@ extern "C" int paste_mine_expand(const paste_mine_desc* d, void* stream) {
   }
   const int64_t n_win = g.n_bins / g.base;
   const int64_t want = (n_win + XT / 32 - 1) / (XT / 32);
-  const int64_t cap = (int64_t)sms * 2;
+  const int64_t cap = (int64_t)sms * 3;
   const unsigned grid = (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
   const int use_cache = (int64_t)g.T + 2 * (int64_t)g.T * g.S + g.S <= XSMEM_CELLS;
   int rc = -1;
