@@ -233,7 +233,7 @@ def run_ours(args):
     alg = S_ * n * (60 + 4 * G) + 5 * preds + 28 * n_bind + 11 * acts
     # the serving kernel (fused predict + narrow-stream compaction) for reference
     cbuf = _compact_buffers(table)
-    cdesc = _compact_desc(cbuf)
+    cdesc = _compact_desc(cbuf, table.cformat)
     cscratch = torch.empty(lib.paste_predict_compact_scratch_bytes(n), dtype=torch.uint8,
                            device="cuda")
     fused = []

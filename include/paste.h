@@ -392,22 +392,30 @@ int paste_resolve(const paste_resolve_desc* d, void* stream);
 
 /* Live-path record compaction: the K-slot records of paste_predict_batch
  * -> narrow CSR streams in session order (decoupled look-back scan).
- * Capacities: pred/act n*K, arg n*K*B.  hdr = n_pred | n_act << 8;
- * pred = pattern | completeness << 14; arg holds the n_bind references of
- * mapped predictions only, as region << 27 | node for a source event
- * region * n_sessions + session (the live table's event ids; all-ones =
- * unresolved); act = slot | level << 5.  The expected utility of an action
- * is p(pattern) * benefit(tool) (policy.py:224-232), which the host redoes
- * exactly, so it is not shipped.  totals = {predictions, arguments,
- * actions, refs outside the region form (0 expected: else re-fetch the full
- * records), structural errors (Predictor diagnostics)}.  Requires
- * max_candidates <= 31 and n_patterns <= 16384.                            */
+ * Capacities: pred/act n*K, arg n*K*B.  Streams (element widths per
+ * `format`):
+ *   hdr  u16 n_pred | n_act << 8          (PASTE_CF_HDR8: u8 n_pred | n_act << 4)
+ *   pred u16 pattern | completeness << 14  (PASTE_CF_PRED8: u8 pattern | completeness << 6)
+ *   arg  u32 region << 27 | node           (PASTE_CF_ARG16: u16 region << 11 | node)
+ *        for the n_bind references of mapped predictions only, the source
+ *        event being region * n_sessions + session (the live table's event
+ *        ids); all-ones = unresolved
+ *   act  u8  slot | level << 5
+ * The expected utility of an action is p(pattern) * benefit(tool)
+ * (policy.py:224-232), which the host redoes exactly, so it is not shipped.
+ * totals = {predictions, arguments, actions, refs outside the chosen arg
+ * form (0 expected: else re-fetch the full records), structural errors}.
+ * Requires max_candidates <= 31 and n_patterns <= 16384; HDR8 needs
+ * max_candidates <= 15, PRED8 n_patterns <= 64.                            */
+enum { PASTE_CF_HDR8 = 1, PASTE_CF_PRED8 = 2, PASTE_CF_ARG16 = 4 };
 typedef struct {
-  uint16_t* hdr;     /* [n]                                                  */
-  uint16_t* pred;
-  uint32_t* arg;
+  void* hdr;         /* [n]                                                  */
+  void* pred;
+  void* arg;
   uint8_t* act;
   int64_t* totals;   /* [5]                                                  */
+  int32_t format;    /* PASTE_CF_* bits                                       */
+  int32_t pad;
 } paste_compact_desc;
 
 /* The serving step in one kernel: paste_predict_batch (observe + predict +

@@ -111,7 +111,10 @@ class ResolveDesc(ctypes.Structure):
 
 class CompactDesc(ctypes.Structure):
     _fields_ = [("hdr", c_void_p), ("pred", c_void_p), ("arg", c_void_p), ("act", c_void_p),
-                ("totals", c_void_p)]
+                ("totals", c_void_p), ("format", c_int32), ("pad", c_int32)]
+
+
+PASTE_CF_HDR8, PASTE_CF_PRED8, PASTE_CF_ARG16 = 1, 2, 4
 
 
 class HoldsDesc(ctypes.Structure):

@@ -126,6 +126,36 @@ __device__ __forceinline__ bool bytes_eq(const uint8_t* a, const uint8_t* b, int
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// narrow record streams (paste_compact_desc, element widths per format)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cf_hdr(const paste_compact_desc& C, int64_t s, int np, int nq) {
+  if (C.format & PASTE_CF_HDR8) static_cast<uint8_t*>(C.hdr)[s] = (uint8_t)(np | (nq << 4));
+  else static_cast<uint16_t*>(C.hdr)[s] = (uint16_t)(np | (nq << 8));
+}
+__device__ __forceinline__ void cf_pred(const paste_compact_desc& C, int64_t i, int pid, int comp) {
+  if (C.format & PASTE_CF_PRED8) static_cast<uint8_t*>(C.pred)[i] = (uint8_t)(pid | (comp << 6));
+  else static_cast<uint16_t*>(C.pred)[i] = (uint16_t)(pid | (comp << 14));
+}
+// argument ref r (event << 32 | node, < 0 = unresolved) of session s; false
+// when the ref does not fit the chosen form (written as unresolved)
+__device__ __forceinline__ bool cf_arg(const paste_compact_desc& C, int64_t i, int64_t r,
+                                       int64_t n, int64_t s) {
+  const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
+  uint32_t w = a16 ? 0xffffu : 0xffffffffu;
+  bool ok = true;
+  if (r >= 0) {
+    const int64_t ev = r >> 32, node = r & 0xffffffffll, region = ev / n;
+    if (ev - region * n == s && region < 31 && node < (a16 ? (1ll << 11) : (1ll << 27)))
+      w = a16 ? (((uint32_t)region << 11) | (uint32_t)node) : (((uint32_t)region << 27) | (uint32_t)node);
+    else
+      ok = false;
+  }
+  if (a16) static_cast<uint16_t*>(C.arg)[i] = (uint16_t)w;
+  else static_cast<uint32_t*>(C.arg)[i] = w;
+  return ok;
+}
+
 // K4 fast path (predict_fast.cu); false = not eligible, use the generic kernel
 bool predict_fast_dispatch(const paste_pool_desc* pool, const paste_windows* win,
                            const paste_admit_desc* adm, const paste_predict_out* out, int G,

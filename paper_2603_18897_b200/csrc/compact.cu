@@ -9,13 +9,14 @@
 // for the exclusive prefix, publish the inclusive prefix and scatter.
 //
 // Streams (all in session order):
-//   hdr[n]      u16  n_pred | n_act << 8
-//   pred[P]     u16  pattern id | completeness << 14
+//   hdr[n]      u16  n_pred | n_act << 8  (u8, 4 + 4 bits, with PASTE_CF_HDR8)
+//   pred[P]     u16  pattern id | completeness << 14  (u8, 6 + 2 bits: PRED8)
 //   arg[A]      u32  argument refs of MAPPED predictions only (n_bind each):
 //                    region << 27 | node, where the source event is
 //                    region * n + session (the live table's event ids); a
 //                    ref outside that form is counted in totals[3] and
 //                    written as all-ones (the caller re-fetches full records)
+//                    (u16, region << 11 | node, with PASTE_CF_ARG16)
 //   act[Q]      u8   prediction slot | level << 5
 // The expected utility of an action is p(pattern) * benefit(tool), one
 // IEEE multiply the host redoes exactly on decode, so it is not shipped.
@@ -99,27 +100,16 @@ __global__ void __launch_bounds__(KT_T) compact_kernel(const paste_predict_out O
     uint64_t p0 = s_excl[0] + s_sum[0][threadIdx.x] - np;
     uint64_t a0 = s_excl[1] + s_sum[1][threadIdx.x] - na;
     uint64_t q0 = s_excl[2] + s_sum[2][threadIdx.x] - nq;
-    C.hdr[s] = (uint16_t)(np | (nq << 8));
+    cf_hdr(C, s, np, nq);
     unsigned long long wide = 0;
     for (int i = 0; i < np; ++i) {
       const int64_t o = obase + i * ostride;
       const int pid = O.pred_pat[o];
-      C.pred[p0 + i] = (uint16_t)(pid | ((int)O.pred_comp[o] << 14));
+      cf_pred(C, p0 + i, pid, (int)O.pred_comp[o]);
       const paste_pattern pt = patterns[pid];
       if (pt.flags & PASTE_PF_HAS_MAPPING)
-        for (int b = 0; b < pt.n_bind; ++b) {
-          const int64_t r = O.pred_arg[abase + (int64_t)(i * B + b) * ostride];
-          uint32_t w = 0xffffffffu;  // unresolved binding
-          if (r >= 0) {
-            const int64_t ev = r >> 32, node = r & 0xffffffffll;
-            const int64_t region = ev / n;
-            if (ev - region * n == s && region < 31 && node < (1ll << 27))
-              w = ((uint32_t)region << 27) | (uint32_t)node;
-            else
-              ++wide;
-          }
-          C.arg[a0++] = w;
-        }
+        for (int b = 0; b < pt.n_bind; ++b)
+          wide += !cf_arg(C, a0++, O.pred_arg[abase + (int64_t)(i * B + b) * ostride], n, s);
     }
     for (int j = 0; j < nq; ++j) {
       const int64_t o = obase + j * ostride;
@@ -153,6 +143,10 @@ extern "C" int paste_compact_records(const paste_predict_out* out, int64_t n_ses
   PASTE_REQUIRE(out && pool && c && scratch, "null argument");
   PASTE_REQUIRE(out->max_candidates <= 31 && pool->n_patterns <= (1 << 14),
                 "compaction needs max_candidates <= 31 and at most 16384 patterns");
+  PASTE_REQUIRE(!(c->format & PASTE_CF_HDR8) || out->max_candidates <= 15,
+                "PASTE_CF_HDR8 needs max_candidates <= 15");
+  PASTE_REQUIRE(!(c->format & PASTE_CF_PRED8) || pool->n_patterns <= 64,
+                "PASTE_CF_PRED8 needs at most 64 patterns");
   cudaStream_t stream = (cudaStream_t)stream_;
   const int64_t tiles = (n_sessions + KT_T - 1) / KT_T;
   PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, paste_compact_scratch_bytes(n_sessions), stream));

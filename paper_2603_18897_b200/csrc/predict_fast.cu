@@ -597,7 +597,7 @@ __device__ __forceinline__ void compact_write(const FastParams& P, const paste_c
   const int64_t n = P.win.n_sessions;
   const int32_t* gs = gt + P.G;
   const int nm = c[0];
-  C.hdr[sess] = (uint16_t)(nm | (c[2] << 8));
+  cf_hdr(C, sess, nm, c[2]);
   if (nm == 0) return;
   const paste_pool_desc& pool = P.pool;
   const MTRecord* recs = reinterpret_cast<const MTRecord*>(e + 16);
@@ -619,20 +619,11 @@ __device__ __forceinline__ void compact_write(const FastParams& P, const paste_c
         const int age = (src >> (4 * b)) & 15;
         const int32_t ev = P.win.evt[rbase + gs[age] * rstride];
         const int64_t r = resolve_fast(P.win, pool.steps, bd, bind_off + b, ev, age, gt, memo);
-        uint32_t w = 0xffffffffu;  // unresolved
-        if (r < 0) {
-          comp = PASTE_C_PARTIAL;
-        } else {
-          const int64_t node = r & 0xffffffffll, region = (int64_t)ev / n;
-          if ((int64_t)ev - region * n == sess && region < 31 && node < (1ll << 27))
-            w = ((uint32_t)region << 27) | (uint32_t)node;
-          else
-            ++wide;
-        }
-        C.arg[a++] = w;
+        if (r < 0) comp = PASTE_C_PARTIAL;
+        wide += !cf_arg(C, a++, r, n, sess);
       }
     }
-    C.pred[o[0] + i] = (uint16_t)(pid | (comp << 14));
+    cf_pred(C, o[0] + i, pid, comp);
     // admit (policy.py:207-236): the streamed first-candidate rule for tools
     // with benefit >= 0 (or NaN), exact arbitration otherwise
     if (!allowed_tool(P.adm, tool)) continue;
@@ -717,22 +708,39 @@ __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactPar
         __threadfence();
         st_relaxed(rec, tile == 0 ? 2 : 1);
       }
+      // lane L checks predecessors w - 4L - j (j < 4): 128 tiles per round, so
+      // the inclusive-prefix frontier advances 128 tiles per L2 round trip
       uint64_t excl[4] = {0, 0, 0, 0};
-      for (int64_t w = tile - 1; w >= 0; w -= 32) {
-        const int64_t idx = w - lane;
-        uint64_t fl = 2;  // before tile 0: an inclusive prefix of 0
-        if (idx >= 0)
-          do {
-            fl = ld_relaxed(Q.tile_state + LB_STRIDE * idx);
-          } while (fl == 0);
-        __threadfence();
-        const unsigned pre = __ballot_sync(0xffffffffu, fl == 2);
-        const int stop = pre ? __ffs(pre) - 1 : 32;  // closest tile holding a prefix
-        uint64_t val[4] = {0, 0, 0, 0};
-        if (idx >= 0 && lane <= stop) {
-          const uint64_t* r = Q.tile_state + LB_STRIDE * idx + (lane == stop ? 5 : 1);
+      for (int64_t w = tile - 1; w >= 0; w -= 128) {
+        uint64_t fl[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) val[k] = ld_relaxed(r + k);
+        for (int j = 0; j < 4; ++j) {
+          const int64_t idx = w - 4 * lane - j;
+          fl[j] = 2;  // before tile 0: an inclusive prefix of 0
+          if (idx >= 0)
+            do {
+              fl[j] = ld_relaxed(Q.tile_state + LB_STRIDE * idx);
+            } while (fl[j] == 0);
+        }
+        __threadfence();
+        // closest predecessor holding a prefix: first (lane, j) in order
+        int first = 4;
+#pragma unroll
+        for (int j = 3; j >= 0; --j)
+          if (fl[j] == 2) first = j;
+        const unsigned pre = __ballot_sync(0xffffffffu, first < 4);
+        const int stop = pre ? __ffs(pre) - 1 : 32;
+        uint64_t val[4] = {0, 0, 0, 0};
+        if (lane <= stop) {
+          const int jmax = lane < stop ? 3 : first;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int64_t idx = w - 4 * lane - j;
+            if (j > jmax || idx < 0) continue;
+            const uint64_t* r = Q.tile_state + LB_STRIDE * idx + (fl[j] == 2 ? 5 : 1);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) val[k] += ld_relaxed(r + k);
+          }
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -815,7 +823,8 @@ bool predict_compact_dispatch(const paste_pool_desc* pool, const paste_windows* 
                               const paste_compact_desc* c, void* scratch, int G,
                               cudaStream_t stream) {
   if (G > 16 || K > 31 || pool->match_table == nullptr || pool->mt_k < K || pool->mt_g != G ||
-      pool->max_bindings > MT_MAX_BIND || pool->n_patterns > (1 << 14) || win->stream_end)
+      pool->max_bindings > MT_MAX_BIND || pool->n_patterns > (1 << 14) || win->stream_end ||
+      ((c->format & PASTE_CF_HDR8) && K > 15) || ((c->format & PASTE_CF_PRED8) && pool->n_patterns > 64))
     return false;
   paste_predict_out out{};
   out.max_candidates = K;

@@ -84,6 +84,10 @@ class LiveSessionTable:
             raise ValueError("live table needs capacity <= 30 and < 2^27 template nodes")
         allow, level, bene = admit_tables(dpool.sigs, policy, estimates.duration)
         self.benefit = np.asarray(bene, np.float64)
+        # narrowest record-stream widths this table's geometry allows
+        self.cformat = ((_native.PASTE_CF_HDR8 if max_candidates <= 15 else 0)
+                        | (_native.PASTE_CF_PRED8 if len(dpool.image.patterns) <= 64 else 0)
+                        | (_native.PASTE_CF_ARG16 if len(nodes) < (1 << 11) else 0))
         self.adm_arrays = (to_dev(allow), to_dev(level), to_dev(bene))
         self.adm = AdmitDesc(1, len(allow), *[ptr(a) for a in self.adm_arrays])
         self.out = {"n_pred": torch.zeros(n, dtype=torch.int32, device=dev),
@@ -142,7 +146,8 @@ class LiveSessionTable:
                                            ctypes.byref(self.adm), ctypes.byref(self.out_desc),
                                            stream_handle()), self.lib)
 
-    def launch_compact(self, region: int, cdesc, scratch, new_tok=None, new_node=None) -> bool:
+    def launch_compact(self, region: int, cdesc, scratch, new_tok=None, new_node=None,
+                       new_ref=None) -> bool:
         """observe + predict + admit writing the narrow record streams
         directly (paste_predict_compact); False when the pool / envelope
         needs the two-kernel path (launch + paste_compact_records)."""
@@ -150,7 +155,7 @@ class LiveSessionTable:
             new_tok = self.new_tok
             if self.narrow:
                 new_node = self.new_node
-        ref = None if new_node is not None else self.new_ref
+        ref = None if new_node is not None else (self.new_ref if new_ref is None else new_ref)
         win = WindowsDesc(self.n, self.W, 1, ptr(self.tok), ptr(self.evt), ptr(self.count),
                           ptr(self.nodes), ptr(self.bytes), ptr(self.refs), ptr(new_tok),
                           ptr(ref), region * self.n, region * self.max_batch_bytes, 0,
@@ -203,14 +208,15 @@ class LiveSessionTable:
 @dataclass
 class CompactRecords:
     """Host copy of the narrow CSR record streams of one live step
-    (compact.cu)."""
+    (compact.cu; element widths per ``fmt``, PASTE_CF_* bits)."""
 
     K: int
     B: int
-    hdr: np.ndarray    # u16[n]: n_pred | n_act << 8
-    pred: np.ndarray   # u16[P]: pattern | completeness << 14
-    arg: np.ndarray    # u32[A]: region << 27 | node (all-ones = unresolved)
-    act: np.ndarray    # u8[Q]:  slot | level << 5
+    hdr: np.ndarray    # n_pred | n_act << 8 (u16), or << 4 (u8, HDR8)
+    pred: np.ndarray   # pattern | completeness << 14 (u16), or << 6 (u8, PRED8)
+    arg: np.ndarray    # region << 27 | node (u32), or << 11 (u16, ARG16); all-ones = unresolved
+    act: np.ndarray    # u8: slot | level << 5
+    fmt: int = 0
 
     @property
     def nbytes(self) -> int:
@@ -222,24 +228,29 @@ class CompactRecords:
         multiply the device did (policy.py:224-232)."""
         K, B = self.K, self.B
         hdr = self.hdr.astype(np.int64)
-        n_pred, n_act = hdr & 0xFF, hdr >> 8
+        hshift = 4 if self.fmt & _native.PASTE_CF_HDR8 else 8
+        n_pred, n_act = hdr & ((1 << hshift) - 1), hdr >> hshift
         n = len(hdr)
         res = PredictResult.empty(n, K, B, True)
         res.n_pred[:] = n_pred
         res.n_act[:] = n_act
         sess = np.repeat(np.arange(n), n_pred)
         slot = np.arange(len(sess)) - np.repeat(np.cumsum(n_pred) - n_pred, n_pred)
-        pid = (self.pred & 0x3FFF).astype(np.int64)
+        pshift = 6 if self.fmt & _native.PASTE_CF_PRED8 else 14
+        pred = self.pred.astype(np.int64)
+        pid = pred & ((1 << pshift) - 1)
         res.pred_pat[sess * K + slot] = pid
-        res.pred_comp[sess * K + slot] = (self.pred >> 14).astype(np.uint8)
+        res.pred_comp[sess * K + slot] = (pred >> pshift).astype(np.uint8)
         mapped = (patterns["flags"][pid] & 1) != 0
         nb = np.where(mapped, patterns["n_bind"][pid], 0)
         p_sess, p_slot = np.repeat(sess, nb), np.repeat(slot, nb)
         b_idx = np.arange(int(nb.sum())) - np.repeat(np.cumsum(nb) - nb, nb)
+        a16 = bool(self.fmt & _native.PASTE_CF_ARG16)
+        ashift = 11 if a16 else 27
         a = self.arg.astype(np.int64)
-        ev = (a >> 27) * n + p_sess
+        ev = (a >> ashift) * n + p_sess
         res.pred_arg[(p_sess * K + p_slot) * B + b_idx] = np.where(
-            a == 0xFFFFFFFF, -1, (ev << 32) | (a & ((1 << 27) - 1)))
+            a == (0xFFFF if a16 else 0xFFFFFFFF), -1, (ev << 32) | (a & ((1 << ashift) - 1)))
         a_sess = np.repeat(np.arange(n), n_act)
         a_slot = np.arange(len(a_sess)) - np.repeat(np.cumsum(n_act) - n_act, n_act)
         a_pred = (self.act & 31).astype(np.int64)
@@ -254,19 +265,22 @@ class CompactRecords:
 def _compact_buffers(table: "LiveSessionTable"):
     t = table.torch
     n, K, B = table.n, table.K, table.B
+    f = table.cformat
     dev = t.device("cuda")
-    return {"hdr": t.zeros(n, dtype=t.int16, device=dev),
-                  "pred": t.zeros(n * K, dtype=t.int16, device=dev),
-                  "arg": t.zeros(n * K * B, dtype=t.int32, device=dev),
-                  "act": t.zeros(n * K, dtype=t.uint8, device=dev),
-                  "totals": t.zeros(5, dtype=t.int64, device=dev)}
+    return {"hdr": t.zeros(n, dtype=t.uint8 if f & _native.PASTE_CF_HDR8 else t.int16, device=dev),
+            "pred": t.zeros(n * K, dtype=t.uint8 if f & _native.PASTE_CF_PRED8 else t.int16,
+                            device=dev),
+            "arg": t.zeros(n * K * B, dtype=t.int16 if f & _native.PASTE_CF_ARG16 else t.int32,
+                           device=dev),
+            "act": t.zeros(n * K, dtype=t.uint8, device=dev),
+            "totals": t.zeros(5, dtype=t.int64, device=dev)}
 
 
-def _compact_desc(c: dict):
+def _compact_desc(c: dict, fmt: int = 0):
     from ._native import CompactDesc
 
     return CompactDesc(ptr(c["hdr"]), ptr(c["pred"]), ptr(c["arg"]), ptr(c["act"]),
-                       ptr(c["totals"]))
+                       ptr(c["totals"]), fmt, 0)
 
 
 def _compact_init(table: "LiveSessionTable") -> None:
@@ -274,12 +288,15 @@ def _compact_init(table: "LiveSessionTable") -> None:
     table.cbuf = _compact_buffers(table)
     table.cscratch = t.empty(table.lib.paste_compact_scratch_bytes(table.n), dtype=t.uint8,
                              device="cuda")
-    table.cdesc = _compact_desc(table.cbuf)
+    table.cdesc = _compact_desc(table.cbuf, table.cformat)
 
 
 def _records(table, h: dict) -> CompactRecords:
-    return CompactRecords(table.K, table.B, h["hdr"].view(np.uint16), h["pred"].view(np.uint16),
-                          h["arg"].view(np.uint32), h["act"])
+    f = table.cformat
+    return CompactRecords(
+        table.K, table.B, h["hdr"].view(np.uint8 if f & _native.PASTE_CF_HDR8 else np.uint16),
+        h["pred"].view(np.uint8 if f & _native.PASTE_CF_PRED8 else np.uint16),
+        h["arg"].view(np.uint16 if f & _native.PASTE_CF_ARG16 else np.uint32), h["act"], f)
 
 
 def _sizes(table, totals) -> dict:
@@ -312,13 +329,15 @@ def fetch_compact(table: "LiveSessionTable", pinned: dict | None = None) -> Comp
 
 
 def serve(table: "LiveSessionTable", batches, depth: int = 3):
-    """Pipelined live steps (the serving loop).  Step i's upload, fused
-    predict + compaction kernel and totals read run on the compute stream
-    while step i-1's sized record download is queued on a copy stream and
-    step i-2's records are handed out, so the copy engines never wait on the
-    host.  Yields each step's CompactRecords in order; a yielded record's
-    arrays are pinned-buffer views, valid until the generator has advanced
-    ``depth - 1`` more steps."""
+    """Pipelined live steps (the serving loop).  Step i's inputs upload on
+    an upload stream into their own staging set while step i-1's fused
+    predict + compaction kernel runs; the kernel and the totals read run on
+    the compute stream; step i-1's sized record download is queued on a copy
+    stream while step i-2's records are handed out -- so the two copy
+    engines and the SMs overlap and never wait on the host.  Yields each
+    step's CompactRecords in order; a yielded record's arrays are
+    pinned-buffer views, valid until the generator has advanced ``depth - 1``
+    more steps."""
     from collections import deque
 
     if depth < 3:
@@ -327,13 +346,18 @@ def serve(table: "LiveSessionTable", batches, depth: int = 3):
     if getattr(table, "_serve", None) is None or len(table._serve["bufs"]) != depth:
         bufs = [_compact_buffers(table) for _ in range(depth)]
         table._serve = {
-            "bufs": bufs, "descs": [_compact_desc(c) for c in bufs],
+            "bufs": bufs, "descs": [_compact_desc(c, table.cformat) for c in bufs],
             "pinned": [{k: t.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in c.items()}
                        for c in bufs],
             "scratch": [t.empty(max(table.lib.paste_compact_scratch_bytes(table.n),
                                     table.lib.paste_predict_compact_scratch_bytes(table.n)),
                                 dtype=t.uint8, device="cuda") for _ in range(depth)],
-            "copy": t.cuda.Stream(), "tot": t.cuda.Stream(), "free": [None] * depth}
+            "copy": t.cuda.Stream(), "tot": t.cuda.Stream(), "up": t.cuda.Stream(),
+            "free": [None] * depth, "in_free": [None] * depth,
+            "in": [{"tok": t.zeros(table.n, dtype=t.int32, device="cuda"),
+                    "node": t.zeros(table.n, dtype=t.int32, device="cuda"),
+                    "ref": t.zeros(2 * table.n, dtype=t.int64, device="cuda")}
+                   for _ in range(depth)]}
     sv = table._serve
     # sized downloads on one copy stream, the small totals reads on another:
     # step i's totals must not queue behind step i-1's downloads (nor the
@@ -360,14 +384,38 @@ def serve(table: "LiveSessionTable", batches, depth: int = 3):
         h = sv["pinned"][k]
         return _records(table, {name: h[name][:m].numpy() for name, m in sizes.items()})
 
+    up = sv["up"]
     for i, b in enumerate(batches):
         k = i % depth
+        region = table.steps % table.regions
+        # upload into staging set k once the kernel that last read it is done
+        with t.cuda.stream(up):
+            if sv["in_free"][k] is not None:
+                up.wait_event(sv["in_free"][k])
+            st = sv["in"][k]
+            narrow = b.node is not None and not table.ship_bytes
+            tok = b.tok if isinstance(b.tok, t.Tensor) else t.from_numpy(b.tok)
+            st["tok"].copy_(tok.reshape(-1), non_blocking=True)
+            if narrow:
+                node = b.node if isinstance(b.node, t.Tensor) else t.from_numpy(b.node)
+                st["node"].copy_(node.reshape(-1), non_blocking=True)
+            else:
+                ref = b.ref if isinstance(b.ref, t.Tensor) else t.from_numpy(b.ref)
+                st["ref"].copy_(ref.reshape(-1), non_blocking=True)
+            if table.ship_bytes:
+                data = b.data if isinstance(b.data, t.Tensor) else t.from_numpy(b.data)
+                table.region_bytes(region)[:data.numel()].copy_(data.reshape(-1),
+                                                                non_blocking=True)
+            uploaded = t.cuda.Event()
+            uploaded.record(up)
         if sv["free"][k] is not None:  # the set's previous download has finished
             comp.wait_event(sv["free"][k])
-        region = table.steps % table.regions
-        table.stage(b, region)
-        if not table.launch_compact(region, sv["descs"][k], sv["scratch"][k]):
-            table.launch(region)
+        comp.wait_event(uploaded)
+        node_in = st["node"] if narrow else None
+        ref_in = None if narrow else st["ref"]
+        if not table.launch_compact(region, sv["descs"][k], sv["scratch"][k], new_tok=st["tok"],
+                                    new_node=node_in, new_ref=ref_in):
+            table.launch(region, st["tok"], ref_in, node_in)
             check(table.lib.paste_compact_records(ctypes.byref(table.out_desc), table.n,
                                                   ctypes.byref(table.pool_desc),
                                                   ctypes.byref(sv["descs"][k]),
@@ -376,6 +424,7 @@ def serve(table: "LiveSessionTable", batches, depth: int = 3):
         table.steps += 1
         ready = t.cuda.Event()
         ready.record(comp)
+        sv["in_free"][k] = ready
         with t.cuda.stream(tot):
             tot.wait_event(ready)
             sv["pinned"][k]["totals"].copy_(sv["bufs"][k]["totals"], non_blocking=True)

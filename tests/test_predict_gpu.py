@@ -189,7 +189,10 @@ def test_generic_kernel_path_matches_too():
         assert proc.returncode == 0, var + proc.stdout[-3000:] + proc.stderr[-3000:]
 
 
-def test_compact_records_expand_to_the_full_records():
+@pytest.mark.parametrize("fmt", [None, 0, 1, 2, 4])
+def test_compact_records_expand_to_the_full_records(fmt):
+    """Compaction of the K-slot records into the narrow streams, at the
+    table's narrowest widths (None) and each width flag alone / none."""
     pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
     book = EstimateBook()
     dp = DevicePool(pool)
@@ -197,6 +200,8 @@ def test_compact_records_expand_to_the_full_records():
     wl = LiveWorkload(dp.sigs, dp.keys, n, seed=21)
     table = LiveSessionTable(dp, n, wl.tmpl.nodes, wl.max_batch_bytes,
                              parse_policy(MOTIF_POLICY).policy, book, max_candidates=8)
+    if fmt is not None:
+        table.cformat = fmt
     for step in range(20):
         table.step(wl.next_batch())
         full = table.fetch().session_major()
@@ -205,7 +210,7 @@ def test_compact_records_expand_to_the_full_records():
         assert comp.nbytes < 0.2 * table.output_nbytes()
 
 
-@pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3"])
+@pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3", "wide_format"])
 def test_serve_pipeline_yields_the_step_records(variant):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
@@ -229,6 +234,8 @@ def test_serve_pipeline_yields_the_step_records(variant):
                            max_candidates=K)
     pip = LiveSessionTable(dp, n, wl_b.tmpl.nodes, wl_b.max_batch_bytes, policy, book,
                            max_candidates=K)
+    if variant == "wide_format":
+        seq.cformat = pip.cformat = 0
     steps = 20
     expect = []
     for _ in range(steps):
