@@ -145,7 +145,9 @@ __device__ __forceinline__ bool cf_arg(const paste_compact_desc& C, int64_t i, i
   uint32_t w = a16 ? 0xffffu : 0xffffffffu;
   bool ok = true;
   if (r >= 0) {
-    const int64_t ev = r >> 32, node = r & 0xffffffffll, region = ev / n;
+    // event ids are int32 (the window rings), so a 32-bit division suffices
+    const int64_t ev = r >> 32, node = r & 0xffffffffll;
+    const int64_t region = n < (1ll << 31) ? (int64_t)((uint32_t)ev / (uint32_t)n) : ev / n;
     if (ev - region * n == s && region < 31 && node < (a16 ? (1ll << 11) : (1ll << 27)))
       w = a16 ? (((uint32_t)region << 11) | (uint32_t)node) : (((uint32_t)region << 27) | (uint32_t)node);
     else
@@ -154,6 +156,81 @@ __device__ __forceinline__ bool cf_arg(const paste_compact_desc& C, int64_t i, i
   if (a16) static_cast<uint16_t*>(C.arg)[i] = (uint16_t)w;
   else static_cast<uint32_t*>(C.arg)[i] = w;
   return ok;
+}
+
+// ---------------------------------------------------------------------------
+// Decoupled look-back over 4 running counters (stream compaction offsets).
+// Tile state: one 128-byte line per tile: flag (0 none, 1 aggregate, 2
+// inclusive prefix), the 4 tile aggregates, the 4 inclusive prefixes.  Call
+// with a whole warp; lane L checks predecessors w - 4L - j (j < 4), so the
+// inclusive-prefix frontier advances 128 tiles per L2 round trip.
+// ---------------------------------------------------------------------------
+constexpr int LB_STRIDE = 16;  // u64 per tile record
+
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void tile_lookback(uint64_t* tile_state, int64_t tile,
+                                              const uint64_t agg[4], uint64_t excl[4], int lane) {
+  uint64_t* rec = tile_state + LB_STRIDE * tile;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) st_relaxed(rec + (tile == 0 ? 5 : 1) + k, agg[k]);
+    __threadfence();
+    st_relaxed(rec, tile == 0 ? 2 : 1);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) excl[k] = 0;
+  for (int64_t w = tile - 1; w >= 0; w -= 128) {
+    uint64_t fl[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t idx = w - 4 * lane - j;
+      fl[j] = 2;  // before tile 0: an inclusive prefix of 0
+      if (idx >= 0)
+        do {
+          fl[j] = ld_relaxed(tile_state + LB_STRIDE * idx);
+        } while (fl[j] == 0);
+    }
+    __threadfence();
+    int first = 4;  // this lane's first predecessor holding a prefix
+#pragma unroll
+    for (int j = 3; j >= 0; --j)
+      if (fl[j] == 2) first = j;
+    const unsigned pre = __ballot_sync(0xffffffffu, first < 4);
+    const int stop = pre ? __ffs(pre) - 1 : 32;
+    uint64_t val[4] = {0, 0, 0, 0};
+    if (lane <= stop) {
+      const int jmax = lane < stop ? 3 : first;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int64_t idx = w - 4 * lane - j;
+        if (j > jmax || idx < 0) continue;
+        const uint64_t* r = tile_state + LB_STRIDE * idx + (fl[j] == 2 ? 5 : 1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) val[k] += ld_relaxed(r + k);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) val[k] += __shfl_xor_sync(0xffffffffu, val[k], o);
+      excl[k] += val[k];
+    }
+    if (pre) break;
+  }
+  if (lane == 0 && tile > 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) st_relaxed(rec + 5 + k, excl[k] + agg[k]);
+    __threadfence();
+    st_relaxed(rec, 2);
+  }
 }
 
 // K4 fast path (predict_fast.cu); false = not eligible, use the generic kernel

@@ -6,7 +6,8 @@
 // Single pass with a decoupled look-back scan: CTAs claim 128-session tiles
 // through a ticket counter (tiles are therefore taken in order and every
 // predecessor is running or done), publish their tile aggregates, look back
-// for the exclusive prefix, publish the inclusive prefix and scatter.
+// for the exclusive prefix with one warp (tile_lookback, common.cuh),
+// publish the inclusive prefix and scatter.
 //
 // Streams (all in session order):
 //   hdr[n]      u16  n_pred | n_act << 8  (u8, 4 + 4 bits, with PASTE_CF_HDR8)
@@ -25,24 +26,15 @@
 namespace paste {
 
 constexpr int KT_T = 128;  // sessions per tile / threads per CTA
-constexpr uint64_t ST_AGG = 1ull << 62, ST_PRE = 2ull << 62, ST_MASK = 3ull << 62;
-
-__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 
 __global__ void __launch_bounds__(KT_T) compact_kernel(const paste_predict_out O, int64_t n,
                                                        const paste_pattern* patterns,
                                                        paste_compact_desc C, uint64_t* ticket,
-                                                       uint64_t* tile_state) {
+                                                       uint64_t* tile_state, int64_t n_tiles) {
   __shared__ int64_t s_tile;
-  __shared__ uint64_t s_sum[3][KT_T];
-  __shared__ uint64_t s_excl[3];
+  __shared__ uint64_t s_warp[KT_T / 32][4];
+  __shared__ uint64_t s_excl[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(ticket), 1ull);
   __syncthreads();
   const int64_t tile = s_tile;
@@ -51,79 +43,75 @@ __global__ void __launch_bounds__(KT_T) compact_kernel(const paste_predict_out O
   const int64_t ostride = O.slot_major ? n : 1;
   const int64_t obase = O.slot_major ? s : s * K;
   const int64_t abase = O.slot_major ? s : s * K * B;
-  int np = 0, na = 0, nq = 0;
+  int c[4] = {0, 0, 0, 0};  // predictions, arguments, actions, structural errors
   if (s < n) {
-    np = O.n_pred[s];
-    nq = O.n_act ? O.n_act[s] : 0;
-    for (int i = 0; i < np; ++i) {
-      const int pid = O.pred_pat[obase + i * ostride];
-      const paste_pattern pt = patterns[pid];
-      if (pt.flags & PASTE_PF_HAS_MAPPING) na += pt.n_bind;
+    c[0] = O.n_pred[s];
+    c[2] = O.n_act ? O.n_act[s] : 0;
+    c[3] = O.struct_err ? O.struct_err[s] : 0;
+    for (int i = 0; i < c[0]; ++i) {
+      const paste_pattern pt = patterns[O.pred_pat[obase + i * ostride]];
+      if (pt.flags & PASTE_PF_HAS_MAPPING) c[1] += pt.n_bind;
     }
   }
-  // block-wide inclusive scans of (np, na, nq)
-  uint64_t v[3] = {(uint64_t)np, (uint64_t)na, (uint64_t)nq};
-  for (int c = 0; c < 3; ++c) s_sum[c][threadIdx.x] = v[c];
-  __syncthreads();
-  for (int off = 1; off < KT_T; off <<= 1) {
-    uint64_t add[3];
-    for (int c = 0; c < 3; ++c) add[c] = threadIdx.x >= off ? s_sum[c][threadIdx.x - off] : 0;
-    __syncthreads();
-    for (int c = 0; c < 3; ++c) s_sum[c][threadIdx.x] += add[c];
-    __syncthreads();
+  // warp inclusive scans, per-warp sums in shared memory
+  uint64_t inc[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint64_t v = (uint64_t)c[k];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint64_t u = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v += u;
+    }
+    inc[k] = v;
+    if (lane == 31) s_warp[warp][k] = v;
   }
-  // look-back (one thread per counter)
-  if (threadIdx.x < 3) {
-    const int c = threadIdx.x;
-    const uint64_t agg = s_sum[c][KT_T - 1];
-    uint64_t* st = tile_state + 3 * tile + c;
-    if (tile == 0) {
-      st_release(st, ST_PRE | agg);
-      s_excl[c] = 0;
-    } else {
-      st_release(st, ST_AGG | agg);
-      uint64_t excl = 0;
-      for (int64_t j = tile - 1; j >= 0; --j) {
-        uint64_t w;
-        do {
-          w = ld_acquire(tile_state + 3 * j + c);
-        } while ((w & ST_MASK) == 0);
-        excl += w & ~ST_MASK;
-        if ((w & ST_MASK) == ST_PRE) break;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t agg[4], excl[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      agg[k] = 0;
+      for (int w = 0; w < KT_T / 32; ++w) agg[k] += s_warp[w][k];
+    }
+    tile_lookback(tile_state, tile, agg, excl, lane);
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s_excl[k] = excl[k];
+      if (tile == n_tiles - 1) {  // the last tile publishes the totals
+        C.totals[0] = (int64_t)(excl[0] + agg[0]);
+        C.totals[1] = (int64_t)(excl[1] + agg[1]);
+        C.totals[2] = (int64_t)(excl[2] + agg[2]);
+        C.totals[4] = (int64_t)(excl[3] + agg[3]);
       }
-      st_release(st, ST_PRE | (excl + agg));
-      s_excl[c] = excl;
     }
   }
   __syncthreads();
   if (s < n) {
-    uint64_t p0 = s_excl[0] + s_sum[0][threadIdx.x] - np;
-    uint64_t a0 = s_excl[1] + s_sum[1][threadIdx.x] - na;
-    uint64_t q0 = s_excl[2] + s_sum[2][threadIdx.x] - nq;
-    cf_hdr(C, s, np, nq);
+    uint64_t o[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      uint64_t before = 0;
+      for (int w = 0; w < warp; ++w) before += s_warp[w][k];
+      o[k] = s_excl[k] + before + inc[k] - (uint64_t)c[k];
+    }
+    cf_hdr(C, s, c[0], c[2]);
     unsigned long long wide = 0;
-    for (int i = 0; i < np; ++i) {
-      const int64_t o = obase + i * ostride;
-      const int pid = O.pred_pat[o];
-      cf_pred(C, p0 + i, pid, (int)O.pred_comp[o]);
+    uint64_t a0 = o[1];
+    for (int i = 0; i < c[0]; ++i) {
+      const int64_t oi = obase + i * ostride;
+      const int pid = O.pred_pat[oi];
+      cf_pred(C, o[0] + i, pid, (int)O.pred_comp[oi]);
       const paste_pattern pt = patterns[pid];
       if (pt.flags & PASTE_PF_HAS_MAPPING)
         for (int b = 0; b < pt.n_bind; ++b)
           wide += !cf_arg(C, a0++, O.pred_arg[abase + (int64_t)(i * B + b) * ostride], n, s);
     }
-    for (int j = 0; j < nq; ++j) {
-      const int64_t o = obase + j * ostride;
-      C.act[q0 + j] = (uint8_t)(O.act_pred[o] | (O.act_level[o] << 5));
+    for (int j = 0; j < c[2]; ++j) {
+      const int64_t oj = obase + j * ostride;
+      C.act[o[2] + j] = (uint8_t)(O.act_pred[oj] | (O.act_level[oj] << 5));
     }
     if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(C.totals + 3), wide);
-    if (O.struct_err && O.struct_err[s])
-      atomicAdd(reinterpret_cast<unsigned long long*>(C.totals + 4),
-                (unsigned long long)O.struct_err[s]);
-  }
-  if (s == n - 1) {
-    C.totals[0] = s_excl[0] + s_sum[0][threadIdx.x];
-    C.totals[1] = s_excl[1] + s_sum[1][threadIdx.x];
-    C.totals[2] = s_excl[2] + s_sum[2][threadIdx.x];
   }
 }
 
@@ -133,7 +121,7 @@ using namespace paste;
 
 extern "C" int64_t paste_compact_scratch_bytes(int64_t n_sessions) {
   const int64_t tiles = (n_sessions + KT_T - 1) / KT_T;
-  return 8 * (3 * tiles + 1);
+  return 8 * (LB_STRIDE * tiles + LB_STRIDE);
 }
 
 extern "C" int paste_compact_records(const paste_predict_out* out, int64_t n_sessions,
@@ -154,7 +142,7 @@ extern "C" int paste_compact_records(const paste_predict_out* out, int64_t n_ses
   if (n_sessions == 0) return PASTE_OK;
   uint64_t* ticket = static_cast<uint64_t*>(scratch);
   compact_kernel<<<(unsigned)tiles, KT_T, 0, stream>>>(*out, n_sessions, pool->patterns, *c, ticket,
-                                                       ticket + 1);
+                                                       ticket + LB_STRIDE, tiles);
   count_launch();
   PASTE_CUDA_CHECK(cudaGetLastError());
   return PASTE_OK;

@@ -525,27 +525,12 @@ __global__ void __launch_bounds__(FT, 8) predict_fast_kernel(const FastParams P)
 // paste_compact_desc (compact.cu describes the format) instead of K fixed
 // slots per session that a second kernel then compacts.  Tiles of FT
 // sessions are claimed through a ticket (so every predecessor is running or
-// done) and each session runs in two phases around a decoupled look-back:
-//   1. observe + gather + match-table header: the session's prediction,
-//      argument, action and structural-error counts.  They need no
-//      resolution: one action per distinct allowed tool (admit keeps exactly
-//      one per tool, policy.py:233-236), n_bind arguments per mapped
-//      prediction.
-//   2. with the stream offsets known: resolve, write, admit.
+// done) and each tile runs in two phases around a decoupled look-back:
+//   1. the whole step (observe, gather, match, resolve, admit), its records
+//      staged per thread in shared memory, and its counts;
+//   2. a block scan plus a decoupled look-back give the stream offsets and
+//      the staged records are written out in the chosen widths.
 // ---------------------------------------------------------------------------
-// Tile state (one 128-byte line per tile): flag (0 none, 1 aggregate, 2
-// inclusive prefix), the 4 tile aggregates, the 4 inclusive prefixes.
-constexpr int LB_STRIDE = 16;  // u64 per tile record
-
-__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 struct CompactParams {
   FastParams F;
   paste_compact_desc C;
@@ -558,51 +543,37 @@ __device__ __forceinline__ bool allowed_tool(const paste_admit_desc& adm, int to
   return adm.enabled && tool < adm.n_tools && __ldg(adm.allow + tool);
 }
 
-// Phase 1: counts of session `sess` (after observe + gather).
-__device__ __forceinline__ void compact_counts(const FastParams& P, const int32_t* gt, int m,
-                                               const uint8_t*& e, int c[4]) {
+// Per-thread staging of one session's records in shared memory (codes in
+// the wide forms; widths are applied when the tile is flushed).
+struct Stage {
+  uint16_t* pred;  // [K] pattern | completeness << 14
+  uint32_t* arg;   // [K * B] region << 27 | node, all-ones = unresolved / not representable
+  uint8_t* act;    // [K] slot | level << 5
+};
+
+__host__ __device__ inline int stage_stride(int K, int B) {  // bytes per thread, 16-B aligned
+  return (((2 * K + 3) & ~3) + 4 * K * B + ((K + 3) & ~3) + 15) & ~15;
+}
+
+// Resolve, admit and stage session `sess` (after observe + gather);
+// c = {predictions, arguments, actions, structural errors}.
+__device__ __forceinline__ void compact_stage(const FastParams& P, int64_t sess, int64_t rbase,
+                                              int64_t rstride, const int32_t* gt, int m,
+                                              const Stage& S, int c[4], uint64_t* memo,
+                                              unsigned long long& wide) {
   c[0] = c[1] = c[2] = c[3] = 0;
-  e = nullptr;
   if (m == 0 || gt[0] >= P.pool.n_bucket_sigs) return;
-  e = table_entry(P, gt, m);
+  const int64_t n = P.win.n_sessions;
+  const int32_t* gs = gt + P.G;
+  const uint8_t* e = table_entry(P, gt, m);
   const int2 hdr = __ldg(reinterpret_cast<const int2*>(e));
   const MTRecord* recs = reinterpret_cast<const MTRecord*>(e + 16);
   const int K = P.out.max_candidates;
   const int nm = hdr.x < K ? hdr.x : K;
   c[0] = nm;
   c[3] = hdr.y;
-  uint64_t seen = 0;
-  for (int i = 0; i < nm; ++i) {
-    const int4 r0 = __ldg(reinterpret_cast<const int4*>(recs + i));
-    const int tool = r0.z, nb = r0.w & 0xffff, pflags = r0.w >> 16;
-    if (pflags & PASTE_PF_HAS_MAPPING) c[1] += nb;
-    if (!allowed_tool(P.adm, tool)) continue;
-    if (tool < 64) {
-      c[2] += !((seen >> tool) & 1ull);
-      seen |= 1ull << tool;
-    } else {
-      bool dup = false;
-      for (int j = 0; j < i && !dup; ++j) dup = __ldg(&recs[j].tool) == tool;
-      c[2] += !dup;
-    }
-  }
-}
-
-// Phase 2: resolve, write and admit session `sess` at stream offsets o[].
-__device__ __forceinline__ void compact_write(const FastParams& P, const paste_compact_desc& C,
-                                              int64_t sess, int64_t rbase, int64_t rstride,
-                                              const int32_t* gt, const uint8_t* e, const int c[4],
-                                              const uint64_t o[3], uint64_t* memo,
-                                              unsigned long long& wide) {
-  const int64_t n = P.win.n_sessions;
-  const int32_t* gs = gt + P.G;
-  const int nm = c[0];
-  cf_hdr(C, sess, nm, c[2]);
-  if (nm == 0) return;
   const paste_pool_desc& pool = P.pool;
-  const MTRecord* recs = reinterpret_cast<const MTRecord*>(e + 16);
-  uint64_t a = o[1];
-  int n_act = 0;
+  int na = 0, n_act = 0;
   uint64_t seen = 0;
   for (int i = 0; i < nm; ++i) {
     const int4 r0 = __ldg(reinterpret_cast<const int4*>(recs + i));
@@ -619,11 +590,22 @@ __device__ __forceinline__ void compact_write(const FastParams& P, const paste_c
         const int age = (src >> (4 * b)) & 15;
         const int32_t ev = P.win.evt[rbase + gs[age] * rstride];
         const int64_t r = resolve_fast(P.win, pool.steps, bd, bind_off + b, ev, age, gt, memo);
-        if (r < 0) comp = PASTE_C_PARTIAL;
-        wide += !cf_arg(C, a++, r, n, sess);
+        uint32_t w = 0xffffffffu;
+        if (r < 0) {
+          comp = PASTE_C_PARTIAL;
+        } else {
+          const int64_t node = r & 0xffffffffll;
+          const int64_t region =
+              n < (1ll << 31) ? (int64_t)((uint32_t)ev / (uint32_t)n) : (int64_t)ev / n;
+          if ((int64_t)ev - region * n == sess && region < 31 && node < (1ll << 27))
+            w = ((uint32_t)region << 27) | (uint32_t)node;
+          else
+            ++wide;
+        }
+        S.arg[na++] = w;
       }
     }
-    cf_pred(C, o[0] + i, pid, comp);
+    S.pred[i] = (uint16_t)(pid | (comp << 14));
     // admit (policy.py:207-236): the streamed first-candidate rule for tools
     // with benefit >= 0 (or NaN), exact arbitration otherwise
     if (!allowed_tool(P.adm, tool)) continue;
@@ -634,21 +616,50 @@ __device__ __forceinline__ void compact_write(const FastParams& P, const paste_c
     if (!(bene < 0.0) && tool < 64) {
       if ((seen >> tool) & 1ull) continue;
       seen |= 1ull << tool;
-      C.act[o[2] + n_act++] = rec;
+      S.act[n_act++] = rec;
       continue;
     }
     int j = 0;
     for (; j < n_act; ++j)
-      if (__ldg(&recs[C.act[o[2] + j] & 31].tool) == tool) break;
+      if (__ldg(&recs[S.act[j] & 31].tool) == tool) break;
     if (j == n_act) {
-      C.act[o[2] + n_act++] = rec;
+      S.act[n_act++] = rec;
       continue;
     }
-    const int ip = C.act[o[2] + j] & 31;
+    const int ip = S.act[j] & 31;
     const double ipp = __ldg(&recs[ip].p);
     const double util = __dmul_rn(p, bene), iu = __dmul_rn(ipp, bene);
-    if ((util != iu) ? (util > iu) : (p > ipp)) C.act[o[2] + j] = rec;
+    if ((util != iu) ? (util > iu) : (p > ipp)) S.act[j] = rec;
   }
+  c[1] = na;
+  c[2] = n_act;
+}
+
+// Write one session's staged records at its stream offsets o[].
+__device__ __forceinline__ void compact_flush(const paste_compact_desc& C, int64_t sess,
+                                              const Stage& S, const int c[4], const uint64_t o[3],
+                                              unsigned long long& wide) {
+  cf_hdr(C, sess, c[0], c[2]);
+  for (int i = 0; i < c[0]; ++i) {
+    const uint16_t v = S.pred[i];
+    cf_pred(C, o[0] + i, v & 0x3fff, v >> 14);
+  }
+  const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
+  for (int j = 0; j < c[1]; ++j) {
+    const uint32_t w = S.arg[j];
+    if (!a16) {
+      static_cast<uint32_t*>(C.arg)[o[1] + j] = w;
+      continue;
+    }
+    uint16_t h = 0xffffu;
+    if (w != 0xffffffffu) {
+      const uint32_t region = w >> 27, node = w & ((1u << 27) - 1);
+      if (node < (1u << 11)) h = (uint16_t)((region << 11) | node);
+      else ++wide;
+    }
+    static_cast<uint16_t*>(C.arg)[o[1] + j] = h;
+  }
+  for (int j = 0; j < c[2]; ++j) C.act[o[2] + j] = S.act[j];
 }
 
 __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactParams Q) {
@@ -660,6 +671,13 @@ __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactPar
   uint64_t* memo = s_mem;
   for (int i = threadIdx.x; i < MEMO; i += FT) memo[i] = 0;
   int32_t* gt = reinterpret_cast<int32_t*>(s_mem + MEMO) + threadIdx.x * P.row;
+  const int K = P.out.max_candidates, B = P.out.max_bindings;
+  uint8_t* st = reinterpret_cast<uint8_t*>(s_mem + MEMO) +
+                (((size_t)sizeof(int32_t) * FT * P.row + 15) & ~(size_t)15) +
+                (size_t)threadIdx.x * stage_stride(K, B);
+  const Stage SG{reinterpret_cast<uint16_t*>(st),
+                 reinterpret_cast<uint32_t*>(st + ((2 * K + 3) & ~3)),
+                 st + ((2 * K + 3) & ~3) + 4 * K * B};
   const int64_t n = P.win.n_sessions;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long wide = 0;
@@ -671,13 +689,12 @@ __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactPar
     const int64_t tile = s_tile;
     if (tile >= Q.n_tiles) break;
     const int64_t sess = tile * FT + threadIdx.x;
-    // ---- phase 1: observe, gather, counts ---------------------------------
+    // ---- the whole step for this session, records staged in shared memory --
     int c[4] = {0, 0, 0, 0};
-    int64_t rbase = 0, rstride = 1;
-    const uint8_t* e = nullptr;
     if (sess < n) {
+      int64_t rbase, rstride;
       const int m = observe_gather(P, sess, gt, rbase, rstride);
-      compact_counts(P, gt, m, e, c);
+      compact_stage(P, sess, rbase, rstride, gt, m, SG, c, memo, wide);
     }
     // ---- block-wide exclusive scan of the 4 counters ------------------------
     uint64_t inc[4];
@@ -693,7 +710,7 @@ __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactPar
       if (lane == 31) s_warp[warp][k] = v;
     }
     __syncthreads();
-    // ---- decoupled look-back, one warp, 32 predecessor tiles per round --------
+    // ---- decoupled look-back (warp 0, 128 predecessor tiles per round) ------
     if (warp == 0) {
       uint64_t agg[4];
 #pragma unroll
@@ -701,62 +718,9 @@ __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactPar
         agg[k] = 0;
         for (int w = 0; w < FT / 32; ++w) agg[k] += s_warp[w][k];
       }
-      uint64_t* rec = Q.tile_state + LB_STRIDE * tile;
+      uint64_t excl[4];
+      tile_lookback(Q.tile_state, tile, agg, excl, lane);
       if (lane == 0) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) st_relaxed(rec + (tile == 0 ? 5 : 1) + k, agg[k]);
-        __threadfence();
-        st_relaxed(rec, tile == 0 ? 2 : 1);
-      }
-      // lane L checks predecessors w - 4L - j (j < 4): 128 tiles per round, so
-      // the inclusive-prefix frontier advances 128 tiles per L2 round trip
-      uint64_t excl[4] = {0, 0, 0, 0};
-      for (int64_t w = tile - 1; w >= 0; w -= 128) {
-        uint64_t fl[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int64_t idx = w - 4 * lane - j;
-          fl[j] = 2;  // before tile 0: an inclusive prefix of 0
-          if (idx >= 0)
-            do {
-              fl[j] = ld_relaxed(Q.tile_state + LB_STRIDE * idx);
-            } while (fl[j] == 0);
-        }
-        __threadfence();
-        // closest predecessor holding a prefix: first (lane, j) in order
-        int first = 4;
-#pragma unroll
-        for (int j = 3; j >= 0; --j)
-          if (fl[j] == 2) first = j;
-        const unsigned pre = __ballot_sync(0xffffffffu, first < 4);
-        const int stop = pre ? __ffs(pre) - 1 : 32;
-        uint64_t val[4] = {0, 0, 0, 0};
-        if (lane <= stop) {
-          const int jmax = lane < stop ? 3 : first;
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int64_t idx = w - 4 * lane - j;
-            if (j > jmax || idx < 0) continue;
-            const uint64_t* r = Q.tile_state + LB_STRIDE * idx + (fl[j] == 2 ? 5 : 1);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) val[k] += ld_relaxed(r + k);
-          }
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) val[k] += __shfl_xor_sync(0xffffffffu, val[k], o);
-          excl[k] += val[k];
-        }
-        if (pre) break;
-      }
-      if (lane == 0) {
-        if (tile > 0) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) st_relaxed(rec + 5 + k, excl[k] + agg[k]);
-          __threadfence();
-          st_relaxed(rec, 2);
-        }
 #pragma unroll
         for (int k = 0; k < 4; ++k) s_excl[k] = excl[k];
         if (tile == Q.n_tiles - 1) {  // the last tile publishes the totals
@@ -776,7 +740,7 @@ __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactPar
         for (int w = 0; w < warp; ++w) before += s_warp[w][k];
         o[k] = s_excl[k] + before + inc[k] - (uint64_t)c[k];
       }
-      compact_write(P, Q.C, sess, rbase, rstride, gt, e, c, o, memo, wide);
+      compact_flush(Q.C, sess, SG, c, o, wide);
     }
   }
   if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(Q.C.totals + 3), wide);
@@ -832,14 +796,22 @@ bool predict_compact_dispatch(const paste_pool_desc* pool, const paste_windows* 
   CompactParams Q{FastParams{*pool, *win, *adm, out, G, 2 * G + 1}, *c,
                   static_cast<uint64_t*>(scratch), static_cast<uint64_t*>(scratch) + LB_STRIDE,
                   (win->n_sessions + FT - 1) / FT};
-  const size_t smem = sizeof(uint64_t) * MEMO + sizeof(int32_t) * FT * Q.F.row;
-  static int sms = 0, occ = 0;
+  if (K * B > 64) return false;  // staging would not fit (two-kernel path)
+  const size_t smem = sizeof(uint64_t) * MEMO +
+                      (((size_t)sizeof(int32_t) * FT * Q.F.row + 15) & ~(size_t)15) +
+                      (size_t)FT * stage_stride(K, B);
+  static int sms = 0, occ = 0, occ_smem = 0;
   if (sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(predict_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         96 * 1024);
+  }
+  if (occ_smem != (int)smem) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, predict_compact_kernel, FT, smem);
     if (occ < 1) occ = 1;
+    occ_smem = (int)smem;
   }
   const int64_t grid = Q.n_tiles < (int64_t)sms * occ ? Q.n_tiles : (int64_t)sms * occ;
   predict_compact_kernel<<<(unsigned)grid, FT, smem, stream>>>(Q);

@@ -80,6 +80,9 @@ class LiveSessionTable:
         self.new_ref = torch.zeros(n * 2, dtype=torch.int64, device=dev)
         self.new_node = torch.zeros(n, dtype=torch.int32, device=dev)
         self.narrow = False  # last staged batch came in the narrow (node-only) form
+        # serve(): one fused predict + compaction kernel (True) or the K-slot
+        # kernel + the compaction kernel (False)
+        self.serve_fused = True
         if self.regions > 31 or len(nodes) >= (1 << 27):
             raise ValueError("live table needs capacity <= 30 and < 2^27 template nodes")
         allow, level, bene = admit_tables(dpool.sigs, policy, estimates.duration)
@@ -413,8 +416,9 @@ def serve(table: "LiveSessionTable", batches, depth: int = 3):
         comp.wait_event(uploaded)
         node_in = st["node"] if narrow else None
         ref_in = None if narrow else st["ref"]
-        if not table.launch_compact(region, sv["descs"][k], sv["scratch"][k], new_tok=st["tok"],
-                                    new_node=node_in, new_ref=ref_in):
+        if not (table.serve_fused and
+                table.launch_compact(region, sv["descs"][k], sv["scratch"][k], new_tok=st["tok"],
+                                     new_node=node_in, new_ref=ref_in)):
             table.launch(region, st["tok"], ref_in, node_in)
             check(table.lib.paste_compact_records(ctypes.byref(table.out_desc), table.n,
                                                   ctypes.byref(table.pool_desc),

@@ -66,7 +66,8 @@ batches = [wl.next_batch() for _ in range(42)]
 for bb in batches:
     bb.tok = torch.from_numpy(bb.tok).pin_memory()
     bb.node = torch.from_numpy(bb.node).pin_memory()
-for depth in (3, 4):
+for depth, fused in ((3, True), (3, False), (4, False)):
+    table.serve_fused = fused
     for _ in table.serve(batches[:2], depth=depth):
         pass
     torch.cuda.synchronize()
@@ -77,4 +78,4 @@ for depth in (3, 4):
         cnt += 1
     e1.record()
     e1.synchronize()
-    print(f"serve depth {depth}: {e0.elapsed_time(e1) / cnt:.3f} ms/step over {cnt} steps")
+    print(f"serve depth {depth} fused={fused}: {e0.elapsed_time(e1) / cnt:.3f} ms/step over {cnt} steps")
