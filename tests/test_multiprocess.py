@@ -16,7 +16,8 @@ from paper_2603_18897_b200.mine_engine import merge_shard_histograms
 
 
 def gram_histogram(tok: np.ndarray, S: int, k: int) -> np.ndarray:
-    """Host restatement of the (k+1)-gram histogram (mine.cu count_grams)."""
+    """Host restatement of the (k+1)-gram histogram (mine.cu): one gram per
+    event, BEGIN (= S) before a segment's first event; base S + 2."""
     base = S + 2
     start = tok < 0
     sig = (tok & 0x7FFFFFFF).astype(np.int64)
@@ -32,14 +33,6 @@ def gram_histogram(tok: np.ndarray, S: int, k: int) -> np.ndarray:
         key += prev * mult
         mult *= base
     np.add.at(hist, key, 1)
-    last = np.append(start[1:], True)
-    kend = np.full(n, S + 1, np.int64)
-    mult = base
-    for d in range(1, k + 1):
-        prev = np.where(pos >= d - 1, sig[np.maximum(np.arange(n) - (d - 1), 0)], S)
-        kend += prev * mult
-        mult *= base
-    np.add.at(hist, kend[last], 1)
     return hist
 
 
@@ -89,9 +82,17 @@ def test_two_rank_gloo_merge_equals_whole_corpus():
     assert counters[0] == len(starts)
 
 
-def test_gram_histogram_restatement_matches_oracle_tables_shape():
-    """Sanity: the restatement counts one gram per event and one END gram per
-    segment (the identity the device kernel relies on)."""
+def test_gram_histogram_marginal_counts_every_anchor():
+    """The identity expand relies on instead of END grams: summing the
+    histogram over the oldest symbol, H[(x, w)] over x, counts the events
+    whose newest k symbols (BEGIN-padded) are w -- every anchor, including a
+    segment's last event."""
+    S, k = 10, 3
     tok, starts = _corpus(seed=3)
-    h = gram_histogram(tok, 10, 3)
-    assert h.sum() == len(tok) + len(starts)
+    h = gram_histogram(tok, S, k)
+    assert h.sum() == len(tok)
+    base = S + 2
+    marg = h.reshape(base, base ** k).sum(axis=0)  # key = w + base^k * x
+    anchors = gram_histogram(tok, S, k - 1)          # k-grams ending at each event
+    w_keys = np.arange(base ** k)
+    assert np.array_equal(marg, anchors[w_keys])
