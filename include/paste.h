@@ -312,6 +312,30 @@ int paste_mine_ingest_count_staged(const paste_columnar_desc* c, const paste_min
                                    void* stage, int64_t stage_bytes, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* canonical_arg_hash (events.py:94-122) on the device                      */
+/* ---------------------------------------------------------------------- */
+
+/* blake2b-128 of canonical_json(value) for n payload tapes (one value per
+ * directory entry).  key_bytes / key_off hold the NFC form of every interned
+ * key (UTF-8), key_rank its rank in code-point order (equal NFC forms share
+ * a rank).  unsure[i] = 1 when the value is left to the host: two keys of
+ * one dict with the same NFC form, a lone surrogate (the reference's
+ * .encode raises), nesting deeper than 32, a dict wider than 256 keys.     */
+typedef struct {
+  int64_t n;
+  const paste_tape_node* nodes;
+  const uint8_t* bytes;
+  const paste_event_ref* refs;   /* [n]                                      */
+  const uint8_t* key_bytes;
+  const int64_t* key_off;        /* [n_keys + 1]                             */
+  const int32_t* key_rank;       /* [n_keys]                                 */
+  uint8_t* digest;               /* [n][16]                                  */
+  uint8_t* unsure;               /* [n]                                      */
+} paste_hash_desc;
+
+int paste_canonical_hash(const paste_hash_desc* d, void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* K6: admission selection (scheduling.py:59-60, 242-258)                   */
 /* ---------------------------------------------------------------------- */
 

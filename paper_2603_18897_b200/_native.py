@@ -131,6 +131,11 @@ class ReplayDesc(ctypes.Structure):
                                        "fmt_bytes", "nodes", "bytes", "refs", "tallies", "unsure")]
 
 
+class HashDesc(ctypes.Structure):
+    _fields_ = [("n", c_int64)] + [(name, c_void_p) for name in (
+        "nodes", "bytes", "refs", "key_bytes", "key_off", "key_rank", "digest", "unsure")]
+
+
 # numpy mirrors of the element structs
 PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
                           ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
@@ -155,6 +160,7 @@ EXPORTS = {
     "paste_replay_score": (c_int, [POINTER(PoolDesc), POINTER(ReplayDesc), POINTER(PredictOut),
                                    c_void_p]),
     "paste_compact_scratch_bytes": (c_int64, [c_int64]),
+    "paste_canonical_hash": (c_int, [POINTER(HashDesc), c_void_p]),
     "paste_predict_compact_scratch_bytes": (c_int64, [c_int64]),
     "paste_predict_compact": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc), POINTER(AdmitDesc),
                                       c_int32, c_int32, POINTER(CompactDesc), c_void_p, c_void_p]),

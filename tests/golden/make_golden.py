@@ -457,6 +457,69 @@ def make_score():
     return {"cases": out}
 
 
+# ---------------------------------------------------------------------------
+# canonical_arg_hash (events.py:94-122)
+# ---------------------------------------------------------------------------
+
+def make_hash():
+    """Values and the reference's canonical_arg_hash of each ("error" when the
+    reference raises): key order, NFC (keys and values, incl. colliding
+    keys), JSON escapes, integral / special floats, bool vs int, deep and
+    wide containers, multi-block serialisations, lone surrogates."""
+    from spectool.events import canonical_arg_hash
+
+    rng = random.Random(7)
+    alphabet = ["a", "b", "Z", "0", " ", '"', "\\", "\n", "\t", "\x00", "\x1f", "\x7f", "é",
+                "e\u0301", "\u00c5", "A\u030a", "\u4e2d", "\U0001F600", "/", "<", "\u2028"]
+
+    def rstr(n):
+        return "".join(rng.choice(alphabet) for _ in range(n))
+
+    def rscalar():
+        r = rng.random()
+        if r < 0.3:
+            return rstr(rng.randint(0, 12))
+        if r < 0.45:
+            return rng.randint(-10 ** 6, 10 ** 6)
+        if r < 0.6:
+            return rng.choice([0.5, -1.25, 1e16, 1e-7, 3.0, -0.0, 2.5e300, 1.0 / 3.0,
+                               float("nan"), float("inf"), float("-inf"), 123456789.0])
+        if r < 0.7:
+            return rng.choice([True, False, None])
+        return rng.choice([2 ** 70, -(2 ** 64), 0, 1])
+
+    def rvalue(depth=0):
+        r = rng.random()
+        if depth > 3 or r < 0.45:
+            return rscalar()
+        if r < 0.7:
+            return [rvalue(depth + 1) for _ in range(rng.randint(0, 4))]
+        return {rstr(rng.randint(1, 6)): rvalue(depth + 1) for _ in range(rng.randint(0, 5))}
+
+    values = [
+        {}, [], "", 0, None, True, 1.0, -0.0, {"b": 1, "a": 2}, {"a": [1, 2.0, True, None]},
+        {"url": "https://example.org/a?b=c&d=\"e\""}, {"path": "C:\\tmp\\x", "n": 3},
+        {"e\u0301": 1, "\u00e9": 2}, {"\u00e9": 1, "e\u0301": 2},  # keys colliding under NFC
+        {"k": "\ud800"}, "a\udfffb",  # lone surrogates: the reference raises
+        {"x" * 60: "y" * 60}, "z" * 121, "z" * 122, "z" * 254, "z" * 500,
+        {"d%03d" % i: i for i in range(300)},  # wide dict
+        [[[[[[[[[[[[[[[[[[[[[[[[[[[[[[[[[[[[[[[["deep"]]]]]]]]]]]]]]]]]]]]]]]]]]]]]]]]]]]]]]]],
+        {"cmd": "pytest -q tests/test_x.py::test_y", "timeout": 30.0, "env": {"CI": "1"}},
+    ]
+    values += [rvalue() for _ in range(400)]
+    cases = []
+    for v in values:
+        try:
+            h = canonical_arg_hash(v)
+        except (UnicodeEncodeError, ValueError):
+            h = "error"
+        cases.append({"value": v, "hash": h})
+    path = os.path.join(OUT, "hash_golden.json")
+    with open(path, "w", encoding="utf-8") as fh:  # ASCII escapes keep lone surrogates
+        json.dump({"cases": cases}, fh, ensure_ascii=True, separators=(",", ":"))
+    print(f"hash_golden.json: {len(cases)} values", file=sys.stderr)
+
+
 def dump(name, obj):
     path = os.path.join(OUT, name)
     with open(path, "w", encoding="utf-8") as fh:
@@ -469,6 +532,8 @@ def main(which):
         make_c3_pool()
     if "c2" in which:
         make_c2()
+    if "hash" in which:
+        make_hash()
     if "fixtures" not in which:
         return
     dump("predict_golden.json", make_predict())
