@@ -165,9 +165,16 @@ def run_ours(args):
     from paper_2603_18897_b200.synth import LiveWorkload
 
     world, rank, local = dist_env()
+    # one process per GPU; PASTE_DIST_BACKEND=gloo (with ranks sharing a GPU)
+    # only exercises the multi-rank code path on a single-GPU box
+    backend = os.environ.get("PASTE_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend != "nccl" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     pool, policy, book = load_setup(args)
     dp = DevicePool(pool)
     n, K = args.sessions, args.max_candidates
