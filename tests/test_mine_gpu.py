@@ -213,3 +213,36 @@ def test_columnar_rejects_unsorted_trace():
         c[key][[i, i + 1]] = c[key][[i + 1, i]]
     with pytest.raises(PasteUnsupported):
         mine_columnar(_dev(c), SigTable(C4_TOOLS), MiningConfig())
+
+
+
+def test_sharded_mining_equals_single_device(tmp_path):
+    """mine_columnar over 2 ranks (whole-session shards, histogram merged by
+    all-reduce; gloo ranks sharing this GPU, launched by torchrun) == the
+    single-device result."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    from paper_2603_18897_b200.mine_engine import mine_columnar
+    from paper_2603_18897_b200.packing import SigTable
+    from paper_2603_18897_b200.synth import C4_TOOLS, columnar_corpus
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = tmp_path / "ranks.json"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.join(root, "tests", "sharded_mine_worker.py"), str(out)]
+    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
+    assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-3000:]
+    got = json.loads(out.read_text())
+    c = columnar_corpus(400_000, seed=31)
+    whole = mine_columnar(_dev(c), SigTable(C4_TOOLS), MiningConfig(k=3, sigma=5, tau=0.3))
+    exp = [[[[s.tool_type, s.status.value] for s in p.context], p.target, p.p, p.support]
+           for p in whole]
+    assert got["0"] == exp and got["1"] == exp and len(exp) > 0
