@@ -501,14 +501,17 @@ def run_long_outputs(args, world, rank, local):
                       "sessions_per_gpu": n, "payload_tape_nodes": len(c["nodes"]),
                       "payload_scalar_bytes": c["payload_bytes"], "node_budget": 10_000},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                        "frac": achieved / peak, "kernel": "leaf_scan_kernel",
+                        "frac": achieved / peak, "kernel": "leaf_match_kernel" if batch.shared else "leaf_scan_kernel",
                         "algorithmic_bytes_per_launch": per * n,
                         "peak_source": f"{peak_kind} hbm_gbs",
                         "note": "scalar bytes + directory + target per payload; the shared node template (3,363 x 16 B) is L2-resident"},
            "e2e": {"value": world * n * steps / t_e2e, "unit": "sessions/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                    "ms_per_step": 1e3 * t_e2e / steps},
-           "gpu_launches": steps}
+           "gpu_launches": steps * batch.launch_count()}
+    out["config"]["scan"] = ("shape-shared: candidates listed once per payload shape "
+                             f"({batch.n_groups} shapes), compared per payload"
+                             if batch.shared else "per-payload scan")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import bridge
 

@@ -394,6 +394,15 @@ typedef struct {
 } paste_leaf_scan_desc;
 
 int paste_leaf_scan(const paste_leaf_scan_desc* d, void* stream);
+/* The same for queries grouped by payload shape (shape-interned tapes):
+ * queries whose payloads share a node array and whose targets share type
+ * and canonical length form a group (group[q]; group_rep[g] = any member).
+ * The group's candidate nodes are listed once (in pre-order, within the
+ * budget), then each query compares only those with its own bytes.
+ * scratch: paste_leaf_scan_shared_bytes(n_groups, node_budget) bytes.      */
+int64_t paste_leaf_scan_shared_bytes(int64_t n_groups, int64_t node_budget);
+int paste_leaf_scan_shared(const paste_leaf_scan_desc* d, const int32_t* group, int64_t n_groups,
+                           const int32_t* group_rep, void* scratch, void* stream);
 
 /* evaluate()'s resolution (mappings.py:143-194) of one binding per query
  * against an explicit source event; for IndexedFallback the history tokens

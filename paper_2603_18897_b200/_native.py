@@ -167,6 +167,9 @@ EXPORTS = {
     "paste_compact_records": (c_int, [POINTER(PredictOut), c_int64, POINTER(PoolDesc),
                                       POINTER(CompactDesc), c_void_p, c_void_p]),
     "paste_leaf_scan": (c_int, [POINTER(LeafScanDesc), c_void_p]),
+    "paste_leaf_scan_shared_bytes": (c_int64, [c_int64, c_int64]),
+    "paste_leaf_scan_shared": (c_int, [POINTER(LeafScanDesc), c_void_p, c_int64, c_void_p,
+                                       c_void_p, c_void_p]),
     "paste_resolve": (c_int, [POINTER(ResolveDesc), c_void_p]),
     "paste_select_scratch_bytes": (c_int64, [c_int64]),
     "paste_select_greedy": (c_int, [POINTER(SelectDesc), c_int64, c_int64, c_void_p, c_int64,

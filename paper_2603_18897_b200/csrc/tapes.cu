@@ -172,9 +172,137 @@ __global__ void resolve_kernel(const paste_resolve_desc D) {
   D.result[q] = cur;
 }
 
+// ---------------------------------------------------------------------------
+// Shape-shared leaf scan.  With shape-interned tapes many payloads share one
+// node array, and which of its nodes can equal a target -- same type class,
+// same canonical length, not NaN, within the node budget, in pre-order --
+// depends only on (node array, target type, target length).  Queries are
+// grouped by that key on the host; one warp per group scans the node array
+// once and writes the group's ordered candidate list, then one warp per
+// query compares only those candidates with its own payload bytes.  Strings
+// whose NFC form differs keep their canonical length in the per-payload
+// bytes, so they stay candidates and are length-checked per payload.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(LS_T) leaf_candidates_kernel(const paste_leaf_scan_desc D,
+                                                               const int32_t* group_rep,
+                                                               int64_t n_groups, int64_t cap,
+                                                               int32_t* cand, int32_t* cand_n) {
+  const int64_t g = (int64_t)blockIdx.x * (LS_T / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (g >= n_groups) return;
+  const int64_t q = group_rep[g];
+  const paste_event_ref ref = D.refs[D.event[q]];
+  const Node root = load_node(D.nodes, ref.node_base);
+  const int64_t n_nodes = root.size();
+  const int limit = (int)(n_nodes < D.node_budget ? n_nodes : D.node_budget);
+  const int tt = D.target_type[q];
+  const uint32_t tl = (uint32_t)(D.target_off[q + 1] - D.target_off[q]);
+  const bool no_bytes = tt == PASTE_T_NULL || tt == PASTE_T_TRUE || tt == PASTE_T_FALSE;
+  const paste_tape_node* nodes = D.nodes + ref.node_base;
+  int32_t* out = cand + g * cap;
+  int n = 0;
+  const bool live = !D.target_nan[q] && tt >= 0 && tt < PASTE_T_LIST;
+  for (int base = 0; live && base < limit; base += 32) {
+    const int i = base + lane;
+    bool c = false;
+    if (i < limit) {
+      const Node nd = load_node(nodes, i);
+      const int t = nd.type();
+      if (type_class(t) == tt && !(nd.flags() & PASTE_F_NAN))
+        c = no_bytes || (nd.flags() & PASTE_F_NFC) || nd.b == tl;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, c);
+    if (c && n + __popc(m & ((1u << lane) - 1)) < cap) out[n + __popc(m & ((1u << lane) - 1))] = i;
+    n += __popc(m);
+  }
+  if (lane == 0) cand_n[g] = n < cap ? n : (int32_t)cap;
+}
+
+__global__ void __launch_bounds__(LS_T) leaf_match_kernel(const paste_leaf_scan_desc D,
+                                                          const int32_t* group, int64_t cap,
+                                                          const int32_t* cand,
+                                                          const int32_t* cand_n) {
+  __shared__ uint32_t tword[LS_T / 32][LS_TW];
+  const int64_t q = (int64_t)blockIdx.x * (LS_T / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  uint32_t* tw = tword[threadIdx.x / 32];
+  if (q >= D.n_queries) return;
+  const paste_event_ref ref = D.refs[D.event[q]];
+  const int tt = D.target_type[q];
+  const uint8_t* tb = D.target_bytes + D.target_off[q];
+  const uint32_t tl = (uint32_t)(D.target_off[q + 1] - D.target_off[q]);
+  const bool no_bytes = tt == PASTE_T_NULL || tt == PASTE_T_TRUE || tt == PASTE_T_FALSE;
+  const bool staged = tl <= 4 * LS_TW;
+  if (staged)
+    for (int j = lane; j < LS_TW; j += 32) {
+      const int r = (int)tl - 4 * j;
+      tw[j] = r > 0 ? ld_part(tb + 4 * j, r < 4 ? r : 4) : 0u;
+    }
+  __syncwarp();
+  const int64_t g = group[q];
+  const int32_t* list = cand + g * cap;
+  const int nc = cand_n[g];
+  const paste_tape_node* nodes = D.nodes + ref.node_base;
+  const uint8_t* bytes = D.bytes + ref.byte_base;
+  const int64_t out0 = D.out_off[q], ocap = D.out_off[q + 1] - out0;
+  int64_t n_out = 0;
+  for (int base = 0; base < nc; base += 32) {
+    bool eq = false;
+    int32_t idx = 0;
+    if (base + lane < nc) {
+      idx = __ldg(list + base + lane);
+      if (no_bytes) {
+        eq = true;
+      } else {
+        const Node nd = load_node(nodes, idx);
+        uint32_t len;
+        const uint8_t* bp = canon_bytes(bytes, 0, nd, &len);
+        eq = len == tl && (staged ? eq_target(bp, tw, (int)len) : bytes_eq(bp, tb, len));
+      }
+    }
+    const unsigned em = __ballot_sync(0xffffffffu, eq);
+    if (eq) {
+      const int64_t slot = n_out + __popc(em & ((1u << lane) - 1));
+      if (slot < ocap) D.out_nodes[out0 + slot] = idx;
+    }
+    n_out += __popc(em);
+  }
+  if (lane == 0) {
+    D.n_out[q] = n_out;
+    D.truncated[q] = load_node(D.nodes, ref.node_base).size() > (uint64_t)D.node_budget;
+  }
+}
+
 }  // namespace paste
 
 using namespace paste;
+
+extern "C" int64_t paste_leaf_scan_shared_bytes(int64_t n_groups, int64_t node_budget) {
+  return n_groups <= 0 ? 0 : n_groups * (node_budget + 1) * (int64_t)sizeof(int32_t);
+}
+
+extern "C" int paste_leaf_scan_shared(const paste_leaf_scan_desc* d, const int32_t* group,
+                                      int64_t n_groups, const int32_t* group_rep, void* scratch,
+                                      void* stream) {
+  using namespace paste;
+  reset_launches();
+  PASTE_REQUIRE(d != nullptr && group != nullptr && group_rep != nullptr && scratch != nullptr,
+                "null argument");
+  PASTE_REQUIRE(d->node_budget >= 0 && d->node_budget < (1ll << 30), "node budget out of range");
+  if (d->n_queries == 0) return PASTE_OK;
+  const int64_t cap = d->node_budget;
+  int32_t* cand_n = static_cast<int32_t*>(scratch);
+  int32_t* cand = cand_n + n_groups;
+  const int warps = LS_T / 32;
+  leaf_candidates_kernel<<<(unsigned)((n_groups + warps - 1) / warps), LS_T, 0,
+                           (cudaStream_t)stream>>>(*d, group_rep, n_groups, cap > 0 ? cap : 1,
+                                                   cand, cand_n);
+  leaf_match_kernel<<<(unsigned)((d->n_queries + warps - 1) / warps), LS_T, 0,
+                      (cudaStream_t)stream>>>(*d, group, cap > 0 ? cap : 1, cand, cand_n);
+  count_launch(2);
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
 
 extern "C" int paste_leaf_scan(const paste_leaf_scan_desc* d, void* stream) {
   reset_launches();

@@ -343,10 +343,15 @@ def score_replay(traces, pool, window_capacity: int, max_candidates):
 
 
 class LeafScanBatch:
-    """Device-resident K5 batch: one (payload, target) query per session."""
+    """Device-resident K5 batch: one (payload, target) query per session.
+
+    Queries whose payloads share a node array (shape-interned tapes) and
+    whose targets share type and canonical length are grouped when the batch
+    is built; when groups are few the shape-shared scan runs (candidates
+    listed once per group, compared per query), else the per-query scan."""
 
     def __init__(self, nodes, data, refs, target_off, target_bytes, node_budget: int = 10_000,
-                 target_type: int = 5, max_matches: int = 4):
+                 target_type: int = 5, max_matches: int = 4, shared: bool | None = None):
         torch = _torch()
         self.lib = _native.lib()
         n = len(refs)
@@ -361,6 +366,19 @@ class LeafScanBatch:
         self.n_out = torch.zeros(n, dtype=torch.int64, device="cuda")
         self.trunc = torch.zeros(n, dtype=torch.uint8, device="cuda")
         self.budget = node_budget
+        # shape groups: (node array, target type, target length)
+        refs_np = np.asarray(refs).reshape(-1, 2)
+        tlen = np.diff(np.asarray(target_off, np.int64))
+        keys = np.stack([refs_np[:, 0], np.full(n, target_type, np.int64), tlen], axis=1)
+        uniq, rep, inv = np.unique(keys, axis=0, return_index=True, return_inverse=True)
+        self.n_groups = len(uniq)
+        self.shared = (self.n_groups * 8 <= n) if shared is None else shared
+        if self.shared:
+            self.group = torch.from_numpy(inv.reshape(-1).astype(np.int32)).cuda()
+            self.group_rep = torch.from_numpy(rep.astype(np.int32)).cuda()
+            self.scratch = torch.empty(
+                max(self.lib.paste_leaf_scan_shared_bytes(self.n_groups, node_budget), 4),
+                dtype=torch.uint8, device="cuda")
 
     def desc(self):
         from ._native import LeafScanDesc
@@ -372,4 +390,12 @@ class LeafScanBatch:
 
     def launch(self) -> None:
         d = self.desc()
-        check(self.lib.paste_leaf_scan(ctypes.byref(d), stream_handle()), self.lib)
+        if self.shared:
+            check(self.lib.paste_leaf_scan_shared(ctypes.byref(d), ptr(self.group), self.n_groups,
+                                                  ptr(self.group_rep), ptr(self.scratch),
+                                                  stream_handle()), self.lib)
+        else:
+            check(self.lib.paste_leaf_scan(ctypes.byref(d), stream_handle()), self.lib)
+
+    def launch_count(self) -> int:
+        return 2 if self.shared else 1

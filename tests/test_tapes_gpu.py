@@ -87,8 +87,11 @@ def test_score_accuracy_matches_reference():
         assert rep.to_json() == case["expected"]
 
 
-@pytest.mark.parametrize("budget", [10_000, 2_000, 1])
-def test_long_output_leaf_scan_matches_oracle(budget):
+@pytest.mark.parametrize("shared", [True, False])
+@pytest.mark.parametrize("budget", [10_000, 2_000, 1, 0])
+def test_long_output_leaf_scan_matches_oracle(budget, shared):
+    """Both the per-query scan and the shape-shared scan (candidates listed
+    once per payload shape) against the oracle's candidate_paths."""
     import numpy as np
 
     from oracle import bridge
@@ -97,7 +100,7 @@ def test_long_output_leaf_scan_matches_oracle(budget):
 
     c = long_output_corpus(3000, seed=5)
     b = LeafScanBatch(c["nodes"], c["bytes"], c["refs"], c["target_off"], c["target_bytes"],
-                      node_budget=budget)
+                      node_budget=budget, shared=shared)
     b.launch()
     n_out, out, tr = bridge.leaf_scan(c["nodes"], c["bytes"], c["refs"], c["target_off"],
                                       c["target_bytes"], node_budget=budget, threads=8)
