@@ -501,7 +501,8 @@ def run_long_outputs(args, world, rank, local):
                       "sessions_per_gpu": n, "payload_tape_nodes": len(c["nodes"]),
                       "payload_scalar_bytes": c["payload_bytes"], "node_budget": 10_000},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                        "frac": achieved / peak, "kernel": "leaf_match_kernel" if batch.shared else "leaf_scan_kernel",
+                        "frac": achieved / peak,
+                        "kernel": "leaf_match_kernel" if batch.shared else "leaf_scan_kernel",
                         "algorithmic_bytes_per_launch": per * n,
                         "peak_source": f"{peak_kind} hbm_gbs",
                         "note": "scalar bytes + directory + target per payload; the shared node template (3,363 x 16 B) is L2-resident"},
