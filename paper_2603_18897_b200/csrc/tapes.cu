@@ -177,19 +177,23 @@ __global__ void resolve_kernel(const paste_resolve_desc D) {
 // node array, and which of its nodes can equal a target -- same type class,
 // same canonical length, not NaN, within the node budget, in pre-order --
 // depends only on (node array, target type, target length).  Queries are
-// grouped by that key on the host; one warp per group scans the node array
+// grouped by that key on the host; one CTA per group scans the node array
 // once and writes the group's ordered candidate list, then one warp per
 // query compares only those candidates with its own payload bytes.  Strings
 // whose NFC form differs keep their canonical length in the per-payload
 // bytes, so they stay candidates and are length-checked per payload.
 // ---------------------------------------------------------------------------
+// One CTA per group: the first min(n_nodes, budget) nodes are cut into
+// LS_T / 32 contiguous segments, each warp lists its segment's candidates,
+// and a block scan of the segment counts places them in pre-order.
 __global__ void __launch_bounds__(LS_T) leaf_candidates_kernel(const paste_leaf_scan_desc D,
                                                                const int32_t* group_rep,
                                                                int64_t n_groups, int64_t cap,
                                                                int32_t* cand, int32_t* cand_n) {
-  const int64_t g = (int64_t)blockIdx.x * (LS_T / 32) + threadIdx.x / 32;
-  const int lane = threadIdx.x & 31;
-  if (g >= n_groups) return;
+  constexpr int NW = LS_T / 32;
+  __shared__ int s_cnt[NW];
+  const int64_t g = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t q = group_rep[g];
   const paste_event_ref ref = D.refs[D.event[q]];
   const Node root = load_node(D.nodes, ref.node_base);
@@ -198,24 +202,37 @@ __global__ void __launch_bounds__(LS_T) leaf_candidates_kernel(const paste_leaf_
   const int tt = D.target_type[q];
   const uint32_t tl = (uint32_t)(D.target_off[q + 1] - D.target_off[q]);
   const bool no_bytes = tt == PASTE_T_NULL || tt == PASTE_T_TRUE || tt == PASTE_T_FALSE;
-  const paste_tape_node* nodes = D.nodes + ref.node_base;
-  int32_t* out = cand + g * cap;
-  int n = 0;
   const bool live = !D.target_nan[q] && tt >= 0 && tt < PASTE_T_LIST;
-  for (int base = 0; live && base < limit; base += 32) {
-    const int i = base + lane;
-    bool c = false;
-    if (i < limit) {
-      const Node nd = load_node(nodes, i);
-      const int t = nd.type();
-      if (type_class(t) == tt && !(nd.flags() & PASTE_F_NAN))
-        c = no_bytes || (nd.flags() & PASTE_F_NFC) || nd.b == tl;
-    }
-    const unsigned m = __ballot_sync(0xffffffffu, c);
-    if (c && n + __popc(m & ((1u << lane) - 1)) < cap) out[n + __popc(m & ((1u << lane) - 1))] = i;
-    n += __popc(m);
+  const paste_tape_node* nodes = D.nodes + ref.node_base;
+  const int seg = (limit + NW - 1) / NW;
+  const int lo = warp * seg, hi = lo + seg < limit ? lo + seg : limit;
+  auto is_cand = [&](int i) {
+    const Node nd = load_node(nodes, i);
+    const int t = nd.type();
+    return type_class(t) == tt && !(nd.flags() & PASTE_F_NAN) &&
+           (no_bytes || (nd.flags() & PASTE_F_NFC) || nd.b == tl);
+  };
+  // pass 1: this warp's candidate count
+  int cnt = 0;
+  for (int base = lo; live && base < hi; base += 32)
+    cnt += __popc(__ballot_sync(0xffffffffu, base + lane < hi && is_cand(base + lane)));
+  if (lane == 0) s_cnt[warp] = cnt;
+  __syncthreads();
+  int off = 0, total = 0;
+  for (int w = 0; w < NW; ++w) {
+    off += w < warp ? s_cnt[w] : 0;
+    total += s_cnt[w];
   }
-  if (lane == 0) cand_n[g] = n < cap ? n : (int32_t)cap;
+  // pass 2: write in order (L1-hot re-read of the segment)
+  int32_t* out = cand + g * cap;
+  for (int base = lo; live && base < hi; base += 32) {
+    const bool c = base + lane < hi && is_cand(base + lane);
+    const unsigned m = __ballot_sync(0xffffffffu, c);
+    const int at = off + __popc(m & ((1u << lane) - 1));
+    if (c && at < cap) out[at] = base + lane;
+    off += __popc(m);
+  }
+  if (threadIdx.x == 0) cand_n[g] = total < cap ? total : (int32_t)cap;
 }
 
 __global__ void __launch_bounds__(LS_T) leaf_match_kernel(const paste_leaf_scan_desc D,
@@ -294,9 +311,8 @@ extern "C" int paste_leaf_scan_shared(const paste_leaf_scan_desc* d, const int32
   int32_t* cand_n = static_cast<int32_t*>(scratch);
   int32_t* cand = cand_n + n_groups;
   const int warps = LS_T / 32;
-  leaf_candidates_kernel<<<(unsigned)((n_groups + warps - 1) / warps), LS_T, 0,
-                           (cudaStream_t)stream>>>(*d, group_rep, n_groups, cap > 0 ? cap : 1,
-                                                   cand, cand_n);
+  leaf_candidates_kernel<<<(unsigned)n_groups, LS_T, 0, (cudaStream_t)stream>>>(
+      *d, group_rep, n_groups, cap > 0 ? cap : 1, cand, cand_n);
   leaf_match_kernel<<<(unsigned)((d->n_queries + warps - 1) / warps), LS_T, 0,
                       (cudaStream_t)stream>>>(*d, group, cap > 0 ? cap : 1, cand, cand_n);
   count_launch(2);
