@@ -335,6 +335,35 @@ typedef struct {
 
 int paste_canonical_hash(const paste_hash_desc* d, void* stream);
 
+/* Scheduler cache keys of the admitted actions of one live step
+ * (scheduling.py:464-480: key = (tool, canonical_arg_hash(prediction.args))
+ * for every non-WARM_ONLY action).  Reads paste_predict_batch's records;
+ * writes keys[slot][16] for action slot (same addressing as act_pred) and
+ * key_state[slot]: 0 = key written, 1 = WARM_ONLY (no argument key), 2 =
+ * unsure (non-ASCII FormatTemplate text, NFC-colliding names, deep / wide
+ * values: hash the decoded arguments on the host).  Keys of the payload
+ * and the arg names come from one key table (NFC bytes + code-point ranks,
+ * as for paste_canonical_hash); bind_key / fmt / fmt_bytes as for
+ * paste_replay_score.                                                     */
+typedef struct {
+  int64_t n_sessions;
+  paste_pool_desc pool;
+  paste_predict_out out;
+  const paste_tape_node* nodes;
+  const uint8_t* bytes;
+  const paste_event_ref* refs;
+  const uint8_t* key_bytes;
+  const int64_t* key_off;
+  const int32_t* key_rank;
+  const int32_t* bind_key;   /* [n_bindings] key id of each binding's arg name */
+  const int32_t* fmt;        /* [n_bindings][5] FormatTemplate rows            */
+  const uint8_t* fmt_bytes;
+  uint8_t* keys;             /* [n * K][16]                                     */
+  uint8_t* key_state;        /* [n * K]                                         */
+} paste_action_keys_desc;
+
+int paste_action_keys(const paste_action_keys_desc* d, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* K6: admission selection (scheduling.py:59-60, 242-258)                   */
 /* ---------------------------------------------------------------------- */

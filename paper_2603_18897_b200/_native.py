@@ -136,6 +136,13 @@ class HashDesc(ctypes.Structure):
         "nodes", "bytes", "refs", "key_bytes", "key_off", "key_rank", "digest", "unsure")]
 
 
+class ActionKeysDesc(ctypes.Structure):
+    _fields_ = [("n_sessions", c_int64), ("pool", PoolDesc), ("out", PredictOut)] + \
+        [(name, c_void_p) for name in ("nodes", "bytes", "refs", "key_bytes", "key_off",
+                                       "key_rank", "bind_key", "fmt", "fmt_bytes", "keys",
+                                       "key_state")]
+
+
 # numpy mirrors of the element structs
 PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
                           ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
@@ -161,6 +168,7 @@ EXPORTS = {
                                    c_void_p]),
     "paste_compact_scratch_bytes": (c_int64, [c_int64]),
     "paste_canonical_hash": (c_int, [POINTER(HashDesc), c_void_p]),
+    "paste_action_keys": (c_int, [POINTER(ActionKeysDesc), c_void_p]),
     "paste_predict_compact_scratch_bytes": (c_int64, [c_int64]),
     "paste_predict_compact": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc), POINTER(AdmitDesc),
                                       c_int32, c_int32, POINTER(CompactDesc), c_void_p, c_void_p]),

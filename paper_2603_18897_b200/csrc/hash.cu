@@ -173,15 +173,14 @@ __device__ __forceinline__ const uint8_t* str_bytes(const uint8_t* bytes, int64_
 }
 
 // emit a scalar node; false = unsure
-__device__ bool put_scalar(Blake2b& b, const paste_hash_desc& D, int64_t byte_base,
-                           const Node& nd) {
+__device__ bool put_scalar(Blake2b& b, const uint8_t* bytes, int64_t byte_base, const Node& nd) {
   switch (nd.type()) {
     case PASTE_T_NULL: b.put_str("null"); return true;
     case PASTE_T_TRUE: b.put_str("true"); return true;
     case PASTE_T_FALSE: b.put_str("false"); return true;
-    case PASTE_T_INT: b.put_bytes(D.bytes + byte_base + nd.a, nd.b); return true;
+    case PASTE_T_INT: b.put_bytes(bytes + byte_base + nd.a, nd.b); return true;
     case PASTE_T_FLOAT: {
-      const uint8_t* p = D.bytes + byte_base + nd.a;
+      const uint8_t* p = bytes + byte_base + nd.a;
       if (nd.flags() & PASTE_F_NAN) b.put_str("NaN");
       else if (nd.b == 3 && p[0] == 'i') b.put_str("Infinity");
       else if (nd.b == 4 && p[0] == '-' && p[1] == 'i') b.put_str("-Infinity");
@@ -190,35 +189,35 @@ __device__ bool put_scalar(Blake2b& b, const paste_hash_desc& D, int64_t byte_ba
     }
     default: {
       int64_t len;
-      const uint8_t* p = str_bytes(D.bytes, byte_base, nd, &len);
+      const uint8_t* p = str_bytes(bytes, byte_base, nd, &len);
       return put_json_string(b, p, len);
     }
   }
 }
 
-__global__ void canonical_hash_kernel(const paste_hash_desc D) {
-  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= D.n) return;
-  const int64_t nb = D.refs[q].node_base, bb = D.refs[q].byte_base;
-  const paste_tape_node* nodes = D.nodes + nb;
-  Blake2b b;
-  b.init();
+struct KeyTab {  // NFC key strings and their code-point ranks (hashing.key_tables)
+  const uint8_t* bytes;
+  const int64_t* off;
+  const int32_t* rank;
+};
+
+// Emit canonical_json of the tape value rooted at `root` (nodes relative to
+// the event's node base); false = unsure (left to the host).
+__device__ bool emit_tape_value(Blake2b& b, const paste_tape_node* nodes, const uint8_t* bytes,
+                                int64_t bb, int32_t root, const KeyTab& K) {
   bool ok = true;
   HFrame st[HSTACK];
   int sp = 0;
-  int32_t cur = 0;     // node to emit next (-1: none, continue the top frame)
+  int32_t cur = root;  // node to emit next (-1: none, continue the top frame)
   bool first = true;   // inside the top frame: no separator before the next child
   while (ok) {
     if (cur >= 0) {
       const Node nd = load_node(nodes, cur);
       if (nd.type() < PASTE_T_LIST) {
-        ok = put_scalar(b, D, bb, nd);
+        ok = put_scalar(b, bytes, bb, nd);
         cur = -1;
       } else {
-        if (sp == HSTACK || (nd.type() == PASTE_T_DICT && nd.a > HDICT_SCAN)) {
-          ok = false;
-          break;
-        }
+        if (sp == HSTACK || (nd.type() == PASTE_T_DICT && nd.a > HDICT_SCAN)) return false;
         b.put(nd.type() == PASTE_T_DICT ? '{' : '[');
         st[sp++] = HFrame{cur, 0, -1, cur + 1};
         cur = -1;
@@ -249,7 +248,7 @@ __global__ void canonical_hash_kernel(const paste_hash_desc D) {
     bool tie = false;
     for (uint32_t c = 0; c < fn.a; ++c) {
       const Node cn = load_node(nodes, child);
-      const int32_t r = D.key_rank[cn.key];
+      const int32_t r = K.rank[cn.key];
       if (r > f.last_rank) {
         if (r < best_rank) {
           best_rank = r;
@@ -261,18 +260,25 @@ __global__ void canonical_hash_kernel(const paste_hash_desc D) {
       }
       child += (int32_t)node_size(cn);
     }
-    if (best < 0 || tie) {
-      ok = false;
-      break;
-    }
+    if (best < 0 || tie) return false;
     const Node kn = load_node(nodes, best);
-    ok = put_json_string(b, D.key_bytes + D.key_off[kn.key],
-                         D.key_off[kn.key + 1] - D.key_off[kn.key]);
+    ok = put_json_string(b, K.bytes + K.off[kn.key], K.off[kn.key + 1] - K.off[kn.key]);
     b.put(':');
     f.last_rank = best_rank;
     ++f.emitted;
     cur = best;
   }
+  return ok;
+}
+
+__global__ void canonical_hash_kernel(const paste_hash_desc D) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= D.n) return;
+  const int64_t nb = D.refs[q].node_base, bb = D.refs[q].byte_base;
+  Blake2b b;
+  b.init();
+  const bool ok = emit_tape_value(b, D.nodes + nb, D.bytes, bb, 0,
+                                  KeyTab{D.key_bytes, D.key_off, D.key_rank});
   uint8_t* out = D.digest + 16 * q;
   if (ok) {
     b.finish(out);
@@ -280,6 +286,132 @@ __global__ void canonical_hash_kernel(const paste_hash_desc D) {
     for (int i = 0; i < 16; ++i) out[i] = 0;
   }
   D.unsure[q] = ok ? 0 : 1;
+}
+
+// ---------------------------------------------------------------------------
+// Scheduler cache keys of admitted speculative actions (scheduling.py:464-480:
+// key = (tool, canonical_arg_hash(prediction.args)) for every non-WARM_ONLY
+// action).  A non-warm action's prediction is FULL, so every binding
+// resolved: args = {arg_name: value} with value the resolved payload node
+// (PathLookup / IndexedFallback) or prefix + norm(leaf_str(leaf)) + suffix
+// (FormatTemplate, mappings.py:197-223).  One thread per session.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool py_space_c(uint8_t c) {  // str.isspace() on ASCII
+  return c == ' ' || (c >= 9 && c <= 13) || (c >= 28 && c <= 31);
+}
+
+// FormatTemplate value as a JSON string; false = unsure (non-ASCII text:
+// Unicode strip / lower / NFC of the composed string are the host's)
+__device__ bool emit_format(Blake2b& b, const paste_action_keys_desc& D, int bind,
+                            const uint8_t* bytes, int64_t bb, const Node& leaf) {
+  const int* f = D.fmt + 5 * bind;
+  if (f[4] & PASTE_FMT_NON_ASCII) return false;
+  const uint8_t* tb = bytes + bb + leaf.a;  // leaf_str: raw text / number text
+  int64_t lo = 0, hi = leaf.b;
+  for (int64_t i = lo; i < hi; ++i)
+    if (tb[i] & 0x80) return false;
+  const int norm = f[4] & 0xff;
+  if (norm == 1) {  // str.strip()
+    while (lo < hi && py_space_c(tb[lo])) ++lo;
+    while (hi > lo && py_space_c(tb[hi - 1])) --hi;
+  }
+  const char* hex = "0123456789abcdef";
+  auto esc = [&](uint8_t c) {
+    switch (c) {
+      case '"': b.put('\\'); b.put('"'); break;
+      case '\\': b.put('\\'); b.put('\\'); break;
+      case '\n': b.put('\\'); b.put('n'); break;
+      case '\r': b.put('\\'); b.put('r'); break;
+      case '\t': b.put('\\'); b.put('t'); break;
+      case '\b': b.put('\\'); b.put('b'); break;
+      case '\f': b.put('\\'); b.put('f'); break;
+      default:
+        if (c < 0x20) {
+          b.put('\\'); b.put('u'); b.put('0'); b.put('0');
+          b.put((uint8_t)hex[c >> 4]); b.put((uint8_t)hex[c & 15]);
+        } else {
+          b.put(c);
+        }
+    }
+  };
+  b.put('"');
+  for (int i = 0; i < f[1]; ++i) esc(D.fmt_bytes[f[0] + i]);
+  for (int64_t i = lo; i < hi; ++i) {
+    uint8_t c = tb[i];
+    if (norm == 2 && c >= 'A' && c <= 'Z') c += 32;  // str.lower() on ASCII
+    esc(c);
+  }
+  for (int i = 0; i < f[3]; ++i) esc(D.fmt_bytes[f[2] + i]);
+  b.put('"');
+  return true;
+}
+
+__global__ void action_keys_kernel(const paste_action_keys_desc D) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = D.n_sessions;
+  if (s >= n) return;
+  const paste_predict_out& O = D.out;
+  const KeyTab KT{D.key_bytes, D.key_off, D.key_rank};
+  const int na = O.n_act[s];
+  for (int j = 0; j < na; ++j) {
+    const int64_t oj = out_at(O, n, s, j);
+    uint8_t* key = D.keys + 16 * oj;
+    if (O.act_level[oj] == 1) {  // WARM_ONLY: the scheduler's synthetic key
+      D.key_state[oj] = 1;
+      continue;
+    }
+    const int i = O.act_pred[oj];
+    const int64_t oi = out_at(O, n, s, i);
+    const paste_pattern pt = D.pool.patterns[O.pred_pat[oi]];
+    const int nb = (pt.flags & PASTE_PF_HAS_MAPPING) ? pt.n_bind : 0;
+    Blake2b b;
+    b.init();
+    b.put('{');
+    bool ok = O.pred_comp[oi] == PASTE_C_FULL;
+    int last = -1;
+    for (int k = 0; ok && k < nb; ++k) {
+      // bindings in the code-point order of their NFC arg names
+      int best = -1, best_rank = 0x7fffffff;
+      for (int bi = 0; bi < nb; ++bi) {
+        const int r = KT.rank[D.bind_key[pt.bind_off + bi]];
+        if (r > last && r < best_rank) {
+          best_rank = r;
+          best = bi;
+        } else if (r == best_rank) {
+          ok = false;  // two arg names with one NFC form
+        }
+      }
+      if (best < 0) {
+        ok = false;
+        break;
+      }
+      last = best_rank;
+      const int bind = pt.bind_off + best;
+      const int key_id = D.bind_key[bind];
+      if (k) b.put(',');
+      ok = ok && put_json_string(b, KT.bytes + KT.off[key_id], KT.off[key_id + 1] - KT.off[key_id]);
+      b.put(':');
+      const int64_t ref = O.pred_arg[arg_at(O, n, s, i, best)];
+      if (ref < 0) {
+        ok = false;
+        break;
+      }
+      const paste_event_ref er = D.refs[ref >> 32];
+      const int32_t node = (int32_t)(ref & 0xffffffff);
+      if (D.pool.bindings[bind].kind == PASTE_X_FORMAT)
+        ok = ok && emit_format(b, D, bind, D.bytes, er.byte_base, load_node(D.nodes + er.node_base, node));
+      else
+        ok = ok && emit_tape_value(b, D.nodes + er.node_base, D.bytes, er.byte_base, node, KT);
+    }
+    b.put('}');
+    if (ok) {
+      b.finish(key);
+      D.key_state[oj] = 0;
+    } else {
+      for (int t = 0; t < 16; ++t) key[t] = 0;
+      D.key_state[oj] = 2;
+    }
+  }
 }
 
 }  // namespace paste
@@ -294,6 +426,20 @@ extern "C" int paste_canonical_hash(const paste_hash_desc* d, void* stream) {
   const int threads = 128;
   canonical_hash_kernel<<<(unsigned)((d->n + threads - 1) / threads), threads, 0,
                           (cudaStream_t)stream>>>(*d);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
+
+extern "C" int paste_action_keys(const paste_action_keys_desc* d, void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(d != nullptr, "null descriptor");
+  if (d->n_sessions == 0) return PASTE_OK;
+  PASTE_REQUIRE(d->out.n_act && d->out.act_pred && d->out.act_level && d->keys && d->key_state,
+                "action records and key outputs are required");
+  const int threads = 128;
+  action_keys_kernel<<<(unsigned)((d->n_sessions + threads - 1) / threads), threads, 0,
+                       (cudaStream_t)stream>>>(*d);
   count_launch();
   PASTE_CUDA_CHECK(cudaGetLastError());
   return PASTE_OK;

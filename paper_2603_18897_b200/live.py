@@ -180,6 +180,34 @@ class LiveSessionTable:
 
     # -- results ----------------------------------------------------------------
 
+    def action_keys(self):
+        """Scheduler cache keys of this step's admitted actions, computed on
+        the device from the K-slot records (paste_action_keys): (keys
+        u8[n*K, 16], state u8[n*K]) device tensors in action-slot order;
+        state 0 = key, 1 = WARM_ONLY (no argument key), 2 = decide on the
+        host (``canonical_arg_hash`` of the decoded arguments)."""
+        from ._native import ActionKeysDesc
+        from .hashing import key_tables
+        from .replay import KeysetTable, pool_hit_tables
+
+        t = self.torch
+        if not self.ship_bytes:
+            raise ValueError("action keys hash argument values: build the table with "
+                             "ship_bytes=True so payload bytes live on the device")
+        if getattr(self, "_keys", None) is None:
+            _, bind_key, fmt, fbytes = pool_hit_tables(self.dpool, KeysetTable())
+            self._keys = {"bind_key": to_dev(bind_key), "fmt": to_dev(fmt), "fbytes": to_dev(fbytes),
+                          "keys": t.zeros(self.n * self.K * 16, dtype=t.uint8, device="cuda"),
+                          "state": t.zeros(self.n * self.K, dtype=t.uint8, device="cuda")}
+        k = self._keys
+        kb, ko, kr = (to_dev(a) for a in key_tables(self.dpool.keys))
+        d = ActionKeysDesc(self.n, self.pool_desc, self.out_desc, ptr(self.nodes), ptr(self.bytes),
+                           ptr(self.refs), ptr(kb), ptr(ko), ptr(kr), ptr(k["bind_key"]),
+                           ptr(k["fmt"]), ptr(k["fbytes"]), ptr(k["keys"]), ptr(k["state"]))
+        check(self.lib.paste_action_keys(ctypes.byref(d), stream_handle()), self.lib)
+        t.cuda.current_stream().synchronize()  # the key tables above are temporaries
+        return k["keys"].view(self.n * self.K, 16), k["state"]
+
     def output_nbytes(self) -> int:
         return sum(v.numel() * v.element_size() for v in self.out.values())
 

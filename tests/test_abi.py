@@ -64,7 +64,7 @@ def _c_sizeof(struct_name: str) -> int:
     ("paste_select_desc", "SelectDesc"), ("paste_columnar_desc", "ColumnarDesc"),
     ("paste_leaf_scan_desc", "LeafScanDesc"), ("paste_resolve_desc", "ResolveDesc"),
     ("paste_compact_desc", "CompactDesc"), ("paste_holds_desc", "HoldsDesc"),
-    ("paste_hash_desc", "HashDesc"),
+    ("paste_hash_desc", "HashDesc"), ("paste_action_keys_desc", "ActionKeysDesc"),
 ])
 def test_struct_layouts_match_header(cname, pyname):
     assert ctypes.sizeof(getattr(_native, pyname)) == _c_sizeof(cname)

@@ -248,3 +248,45 @@ def test_serve_pipeline_yields_the_step_records(variant):
     for e, g in zip(expect, got):
         for x, y in zip(e, g):
             assert np.array_equal(x, y)
+
+
+def test_action_keys_match_canonical_arg_hash():
+    """Device scheduler keys of admitted actions (paste_action_keys) ==
+    canonical_arg_hash of the decoded prediction arguments (the host mirror,
+    pinned to the reference's hashes in test_hash.py), for every non-warm
+    action; warm-only actions carry no argument key."""
+    from paper_2603_18897_b200.events import canonical_arg_hash
+    from paper_2603_18897_b200.packing import decode_actions, decode_predictions
+    from paper_2603_18897_b200.tape import ArrayTapes
+
+    pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
+    dp = DevicePool(pool)
+    n = 4000
+    wl = LiveWorkload(dp.sigs, dp.keys, n, seed=41)
+    table = LiveSessionTable(dp, n, wl.tmpl.nodes, wl.max_batch_bytes,
+                             parse_policy(MOTIF_POLICY).policy, EstimateBook(), max_candidates=8,
+                             ship_bytes=True)
+    checked = warm = 0
+    for step in range(20):
+        table.step(wl.next_batch())
+        if step < 16:
+            continue
+        keys, state = table.action_keys()
+        keys, state = keys.cpu().numpy(), state.cpu().numpy()
+        res = table.fetch().session_major()
+        hs = table.host_state()
+        arena = ArrayTapes(wl.tmpl.nodes, hs["bytes"], hs["refs"], dp.keys)
+        preds = decode_predictions(res, dp.image, arena, [0.0] * n, 0.0)
+        acts = decode_actions(res, preds)
+        K = table.K
+        for s in range(n):
+            for j, a in enumerate(acts[s]):
+                slot = j * n + s  # slot-major action records
+                if a.level.value == 1:
+                    assert state[slot] == 1
+                    warm += 1
+                    continue
+                assert state[slot] == 0
+                assert keys[slot].tobytes().hex() == canonical_arg_hash(a.prediction.args)
+                checked += 1
+    assert checked > 1000 and warm > 0
