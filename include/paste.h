@@ -300,6 +300,41 @@ typedef struct {
 } paste_columnar_desc;
 
 int paste_mine_ingest_count(const paste_columnar_desc* c, const paste_mine_desc* d, void* stream);
+
+/* Native (host, OpenMP) columnar ingest of a JSONL trace for mining:
+ * ingest_trace (events.py:196-252) -- group by session_id in first-
+ * appearance order, stable sort by (t_start, seq), split on gaps over all
+ * events, keep each segment's tool events (Session.tool_events) -- written
+ * as the columnar trace above with session = segment index (count it with
+ * no further gap split: inactivity_ms = +inf) and sig = 2 * tool + success,
+ * tools interned in sorted name order (tool_names: sorted, NUL-separated).
+ * Lines missing a required field are errors (error_lines, 1-based).  Input
+ * outside the parser's exact subset (escapes in ids, non-string ids,
+ * non-integral seq, NaN start times, duplicate keys, unvalidated JSON,
+ * other line separators) returns PASTE_ERR_UNSUPPORTED: use the host
+ * ingest.  Capacities too small: PASTE_ERR_INVALID with the counts set.     */
+typedef struct {
+  int64_t capacity;            /* event slots in the columns below            */
+  int32_t* session;
+  int32_t* seq;
+  double* t_start;
+  double* t_end;
+  int32_t* sig;
+  int32_t* error_lines;        /* optional [error_capacity]                   */
+  int64_t error_capacity;
+  char* tool_names;            /* optional [tool_names_capacity]              */
+  int64_t tool_names_capacity;
+  int64_t n_events;            /* out: tool events                            */
+  int64_t n_segments;          /* out                                         */
+  int64_t n_errors;            /* out                                         */
+  int64_t n_lines;             /* out                                         */
+  int64_t reordered_sessions;  /* out                                         */
+  int64_t tool_names_len;      /* out                                         */
+  int32_t n_tools;             /* out                                         */
+  int32_t pad;
+} paste_ingest_desc;
+
+int paste_ingest_jsonl(const char* text, int64_t len, double inactivity_ms, paste_ingest_desc* d);
 /* Same, in two passes: the columnar pass writes one staged word per event
  * (4 B) to `stage`; a second pass sends the cold grams to L2 into 8
  * histogram replicas (a hot gram's updates spread over 8 addresses), which

@@ -143,6 +143,15 @@ class ActionKeysDesc(ctypes.Structure):
                                        "key_state")]
 
 
+class IngestDesc(ctypes.Structure):
+    _fields_ = [("capacity", c_int64), ("session", c_void_p), ("seq", c_void_p),
+                ("t_start", c_void_p), ("t_end", c_void_p), ("sig", c_void_p),
+                ("error_lines", c_void_p), ("error_capacity", c_int64), ("tool_names", c_void_p),
+                ("tool_names_capacity", c_int64), ("n_events", c_int64), ("n_segments", c_int64),
+                ("n_errors", c_int64), ("n_lines", c_int64), ("reordered_sessions", c_int64),
+                ("tool_names_len", c_int64), ("n_tools", c_int32), ("pad", c_int32)]
+
+
 # numpy mirrors of the element structs
 PATTERN_DTYPE = np.dtype([("ctx_off", "i4"), ("ctx_len", "i4"), ("target_tool", "i4"),
                           ("bind_off", "i4"), ("n_bind", "i4"), ("flags", "i4"), ("p", "f8")])
@@ -168,6 +177,7 @@ EXPORTS = {
                                    c_void_p]),
     "paste_compact_scratch_bytes": (c_int64, [c_int64]),
     "paste_canonical_hash": (c_int, [POINTER(HashDesc), c_void_p]),
+    "paste_ingest_jsonl": (c_int, [c_char_p, c_int64, ctypes.c_double, POINTER(IngestDesc)]),
     "paste_action_keys": (c_int, [POINTER(ActionKeysDesc), c_void_p]),
     "paste_predict_compact_scratch_bytes": (c_int64, [c_int64]),
     "paste_predict_compact": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc), POINTER(AdmitDesc),

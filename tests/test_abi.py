@@ -65,6 +65,7 @@ def _c_sizeof(struct_name: str) -> int:
     ("paste_leaf_scan_desc", "LeafScanDesc"), ("paste_resolve_desc", "ResolveDesc"),
     ("paste_compact_desc", "CompactDesc"), ("paste_holds_desc", "HoldsDesc"),
     ("paste_hash_desc", "HashDesc"), ("paste_action_keys_desc", "ActionKeysDesc"),
+    ("paste_ingest_desc", "IngestDesc"),
 ])
 def test_struct_layouts_match_header(cname, pyname):
     assert ctypes.sizeof(getattr(_native, pyname)) == _c_sizeof(cname)

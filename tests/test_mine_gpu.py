@@ -246,3 +246,24 @@ def test_sharded_mining_equals_single_device(tmp_path):
     exp = [[[[s.tool_type, s.status.value] for s in p.context], p.target, p.p, p.support]
            for p in whole]
     assert got["0"] == exp and got["1"] == exp and len(exp) > 0
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_mine_jsonl_equals_mine_of_ingested_sessions(seed):
+    """JSONL -> native columnar ingest -> device counts == mine() over the
+    reference-semantics ingest_trace sessions (payload-free trace, so no
+    mapping can be inferred and p = follow / match on both paths)."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_ingest import _trace
+
+    from paper_2603_18897_b200.events import ingest_trace
+    from paper_2603_18897_b200.ingest import mine_jsonl
+
+    text = _trace(seed, n_sessions=2000, payloads=False)
+    cfg = MiningConfig(k=3, sigma=5, tau=0.3)
+    got = mine_jsonl(text, cfg)
+    exp = mine(ingest_trace(text).sessions, cfg)
+    assert got == exp and len(got) > 0
