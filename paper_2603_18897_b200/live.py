@@ -359,7 +359,7 @@ def fetch_compact(table: "LiveSessionTable", pinned: dict | None = None) -> Comp
     return _records(table, {k: pinned[k][:m].numpy() for k, m in sizes.items()})
 
 
-def serve(table: "LiveSessionTable", batches, depth: int = 3):
+def serve(table: "LiveSessionTable", batches, depth: int = 4):
     """Pipelined live steps (the serving loop).  Step i's inputs upload on
     an upload stream into their own staging set while step i-1's fused
     predict + compaction kernel runs; the kernel and the totals read run on
@@ -416,10 +416,12 @@ def serve(table: "LiveSessionTable", batches, depth: int = 3):
         return _records(table, {name: h[name][:m].numpy() for name, m in sizes.items()})
 
     up = sv["up"]
-    for i, b in enumerate(batches):
+
+    def upload(i, b):
+        """Stage step i's inputs into set i % depth on the upload stream, once
+        the kernel that last read that set is done; returns the event."""
         k = i % depth
-        region = table.steps % table.regions
-        # upload into staging set k once the kernel that last read it is done
+        region = (steps0 + i) % table.regions  # the arena region step i will use
         with t.cuda.stream(up):
             if sv["in_free"][k] is not None:
                 up.wait_event(sv["in_free"][k])
@@ -437,8 +439,20 @@ def serve(table: "LiveSessionTable", batches, depth: int = 3):
                 data = b.data if isinstance(b.data, t.Tensor) else t.from_numpy(b.data)
                 table.region_bytes(region)[:data.numel()].copy_(data.reshape(-1),
                                                                 non_blocking=True)
-            uploaded = t.cuda.Event()
-            uploaded.record(up)
+            ev = t.cuda.Event()
+            ev.record(up)
+        return ev, narrow
+
+    it = iter(batches)
+    steps0 = table.steps
+    nxt = next(it, None)
+    staged = upload(0, nxt) if nxt is not None else None
+    i = 0
+    while staged is not None:
+        k = i % depth
+        uploaded, narrow = staged
+        region = table.steps % table.regions
+        st = sv["in"][k]
         if sv["free"][k] is not None:  # the set's previous download has finished
             comp.wait_event(sv["free"][k])
         comp.wait_event(uploaded)
@@ -463,6 +477,10 @@ def serve(table: "LiveSessionTable", batches, depth: int = 3):
             tot_ev = t.cuda.Event()
             tot_ev.record(tot)
         tot_q.append((k, tot_ev))
+        # the next step's upload goes out now, before the host waits on anything
+        nxt = next(it, None)
+        staged = upload(i + 1, nxt) if nxt is not None else None
+        i += 1
         if len(tot_q) > 1:
             download(*tot_q.popleft())
         if len(copy_q) > 1:

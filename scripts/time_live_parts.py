@@ -66,7 +66,7 @@ batches = [wl.next_batch() for _ in range(42)]
 for bb in batches:
     bb.tok = torch.from_numpy(bb.tok).pin_memory()
     bb.node = torch.from_numpy(bb.node).pin_memory()
-for depth, fused in ((3, True), (3, False), (4, False)):
+for depth, fused in ((3, True), (4, True), (6, True), (3, False)):
     table.serve_fused = fused
     for _ in table.serve(batches[:2], depth=depth):
         pass

@@ -210,7 +210,8 @@ def test_compact_records_expand_to_the_full_records(fmt):
         assert comp.nbytes < 0.2 * table.output_nbytes()
 
 
-@pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3", "wide_format"])
+@pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3", "wide_format",
+                                     "ship_bytes"])
 def test_serve_pipeline_yields_the_step_records(variant):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
@@ -236,6 +237,11 @@ def test_serve_pipeline_yields_the_step_records(variant):
                            max_candidates=K)
     if variant == "wide_format":
         seq.cformat = pip.cformat = 0
+    if variant == "ship_bytes":  # payload bytes uploaded into the arena regions too
+        seq = LiveSessionTable(dp, n, wl_a.tmpl.nodes, wl_a.max_batch_bytes, policy, book,
+                               max_candidates=K, ship_bytes=True)
+        pip = LiveSessionTable(dp, n, wl_b.tmpl.nodes, wl_b.max_batch_bytes, policy, book,
+                               max_candidates=K, ship_bytes=True)
     steps = 20
     expect = []
     for _ in range(steps):
@@ -248,6 +254,8 @@ def test_serve_pipeline_yields_the_step_records(variant):
     for e, g in zip(expect, got):
         for x, y in zip(e, g):
             assert np.array_equal(x, y)
+    if variant == "ship_bytes":  # same arena contents
+        assert torch.equal(seq.bytes, pip.bytes) and torch.equal(seq.refs, pip.refs)
 
 
 def test_action_keys_match_canonical_arg_hash():
