@@ -251,15 +251,29 @@ def _occurrences(streams, sig_streams, context: tuple, target: str, cfg: MiningC
 # public entry points
 # ---------------------------------------------------------------------------
 
-def _count_corpus(streams, cfg: MiningConfig):
+def _gather(obj, group) -> list:
+    import torch.distributed as dist
+
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+def _count_corpus(streams, cfg: MiningConfig, group=None):
     torch = _torch()
-    tools = sorted({e.tool_type for st in streams for e in st})
-    sigs = SigTable(tools)
+    tools = {e.tool_type for st in streams for e in st}
+    if group is not None:  # one signature table for every shard
+        tools = set().union(*_gather(tools, group))
+    sigs = SigTable(sorted(tools))
     relation = 0 if cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE else 1
     tables = MineTables.allocate(max(sigs.n_sigs, 2), cfg.k, relation)
     tok = pack_streams(streams, sigs)
     if len(tok):
         tables.count(torch.from_numpy(tok).cuda())
+    if group is not None:  # K3: shards are whole sessions, histograms add up
+        import torch.distributed as dist
+
+        dist.all_reduce(tables.hist, group=group)
     tables.expand()
     return sigs, tables
 
@@ -282,12 +296,22 @@ def _phase2(occ, cfg: MiningConfig, hits: int):
     return mapping, phase2_device.count_mapping_hits(mapping, occs)
 
 
-def mine(traces: Sequence[Session], cfg: MiningConfig) -> list[PatternTuple]:
-    if not traces:
+def mine(traces: Sequence[Session], cfg: MiningConfig, group=None) -> list[PatternTuple]:
+    """mine() (mining.py:248-292).  With a torch.distributed ``group`` every
+    rank passes its shard -- a contiguous range of the sessions, ranks in
+    session order -- counts it on its device, and the (k+1)-gram histograms
+    are all-reduced; Phase II sees every candidate's occurrences gathered in
+    rank (= stream) order, so every rank returns the single-device result."""
+    if group is not None:
+        if not sum(_gather(len(traces), group)):
+            raise ValueError("traces must be non-empty")
+    elif not traces:
         raise ValueError("traces must be non-empty")
     streams = [s.tool_events() for s in traces]
-    sigs, tables = _count_corpus(streams, cfg)
+    sigs, tables = _count_corpus(streams, cfg, group)
     cands = tables.select(cfg.sigma, cfg.tau)
+    if group is not None:  # the select kernel compacts with atomics: fix one order for all ranks
+        cands = cands[np.lexsort((cands[:, 1], cands[:, 0]))]
     S = tables.n_sigs
     sig_streams = None
     patterns = []
@@ -300,6 +324,8 @@ def mine(traces: Sequence[Session], cfg: MiningConfig) -> list[PatternTuple]:
             if sig_streams is None:
                 sig_streams = [[signature_of(e) for e in st] for st in streams]
             occ = _occurrences(streams, sig_streams, context, target, cfg)
+            if group is not None:  # every shard's occurrences, in stream order
+                occ = [o for part in _gather(occ, group) for o in part]
             mapping, hits = _phase2(occ, cfg, hits)
         p = hits / n_match
         if p >= cfg.tau:

@@ -267,3 +267,32 @@ def test_mine_jsonl_equals_mine_of_ingested_sessions(seed):
     got = mine_jsonl(text, cfg)
     exp = mine(ingest_trace(text).sessions, cfg)
     assert got == exp and len(got) > 0
+
+
+def test_sharded_session_mining_with_mappings(tmp_path):
+    """mine(shard, cfg, group=...) over 2 ranks (contiguous session shards,
+    gloo ranks sharing this GPU): counts merged by all-reduce, Phase II over
+    the gathered occurrences -- both ranks return the reference's golden
+    patterns, mappings included."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = tmp_path / "ranks.json"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.join(root, "tests", "sharded_mine_worker.py"), str(out), "sessions"]
+    proc = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=root)
+    assert proc.returncode == 0, proc.stdout[-2000:] + proc.stderr[-3000:]
+    got = json.loads(out.read_text())
+    for i, corpus in enumerate(MINE["mapped"]):
+        exp = [[p["context"], p["target"], p["mapping"], p["p"], p["support"]]
+               for p in corpus["expected"]]
+        exp = [[[[c["tool"], c["status"]] for c in e[0]]] + e[1:] for e in exp]
+        assert got["0"][i] == exp and got["1"][i] == exp
