@@ -27,6 +27,7 @@
 // every segment (session after gap splitting).
 #include "common.cuh"
 
+#include <cooperative_groups.h>
 #include <mutex>
 #include <unordered_map>
 
@@ -628,19 +629,32 @@ __device__ __forceinline__ uint32_t slot_word(const ColumnTile* T, int l, int64_
 // word).  Hot grams go to the CTA's shared table.  Cold grams go straight to
 // L2 (STAGE = false), or are returned as a staged word for
 // stage_hist_kernel (STAGE = true): the gram key, bit 31 = already counted.
-constexpr uint32_t STG_HOT = 0x80000000u, STG_KEY = 0x7fffffffu;
+//
+// Success lattice: a gram whose K+1 events are all successful (odd
+// signatures, no BEGIN) is staged as STG_LAT | its index over the (S/2)^(K+1)
+// lattice, which stage_hist_kernel counts in shared memory.  With the usual
+// few-percent failure rate these are most full-window grams.
+constexpr uint32_t STG_HOT = 0x80000000u, STG_KEY = 0x7fffffffu, STG_LAT = 0x40000000u;
+constexpr uint32_t LAT_MAX = 65536;  // lattice cells (16-bit counters, 128 KB)
 constexpr int STG_REPS = 8;  // histogram replicas of the L2 pass
 __host__ __device__ inline int64_t stage_words(int64_t n) { return (n + 3) & ~(int64_t)3; }
 
 template <int K, bool STAGE>
 __device__ __forceinline__ uint32_t count_event(const uint32_t (&w)[K + 1], uint32_t S,
                                                 uint32_t base, uint32_t hot_lo, uint32_t hot_n,
-                                                uint32_t* hot, uint32_t* hist) {
-  uint32_t key = w[0] & 0x7fffffffu, mult = base;
+                                                uint32_t* hot, uint32_t* hist, uint32_t lat_t) {
+  const uint32_t s0 = w[0] & 0x7fffffffu;
+  uint32_t key = s0, mult = base;
+  uint32_t li = s0 >> 1, lm = lat_t;  // success-lattice index (base lat_t digits)
+  bool lat = STAGE && lat_t != 0 && (s0 & 1u);
   bool stop = w[0] >> 31;
 #pragma unroll
   for (int d = 1; d <= K; ++d) {
-    key += (stop ? S : (w[d] & 0x7fffffffu)) * mult;
+    const uint32_t sd = w[d] & 0x7fffffffu;
+    key += (stop ? S : sd) * mult;
+    lat = lat && !stop && (sd & 1u);
+    li += (sd >> 1) * lm;
+    lm *= lat_t;
     stop = stop || (w[d] >> 31);
     mult *= base;
   }
@@ -648,6 +662,7 @@ __device__ __forceinline__ uint32_t count_event(const uint32_t (&w)[K + 1], uint
     atomicAdd(hot + (key - hot_lo), 1u);
     return key | STG_HOT;
   }
+  if (STAGE && lat) return STG_LAT | li;
   if (!STAGE) atomicAdd(hist + key, 1u);
   return key;
 }
@@ -655,28 +670,65 @@ __device__ __forceinline__ uint32_t count_event(const uint32_t (&w)[K + 1], uint
 // Stage 2 of the staged count: the cold grams of the staged words go to L2
 // as REDs, in a pass of their own (interleaved with the columnar stream the
 // same REDs run at well under half their standalone rate).  The pass is
-// RED-issue bound (lg_throttle), so the third-event grams (BEGIN, s_2, s_1,
-// s_0) -- a dense base^3 block, and the most contended one -- are counted
-// in shared memory (one CTA per SM) and flushed once.
+// RED-issue bound (lg_throttle), so the two densest blocks are counted in
+// shared memory (one CTA per SM) and flushed once: the success lattice
+// (STG_LAT words) and, for k = 3, the third-event grams (BEGIN, s_2, s_1,
+// s_0), a dense base^3 block.  Both use 16-bit counters packed two per word;
+// a counter spills 2^15 to the histogram when it reaches 2^15, so bit 15 of
+// a half is a guard that never carries into its neighbour (fewer than 2^15
+// increments can land between a half reaching 2^15 and its spill).
 constexpr int SH_T = 1024;
-constexpr int SH_DENSE_MAX = 40000;  // u32 counters (160 KB)
+constexpr int SH_DENSE_MAX = 40000;  // 16-bit dense-block counters (80 KB)
+constexpr int SH_SMEM_MAX = (SH_DENSE_MAX + (int)LAT_MAX) * 2;
+
+// histogram key of success-lattice cell `li` (digits base lat_t, oldest last)
+__device__ __forceinline__ uint32_t lat_key(uint32_t li, uint32_t lat_t, uint32_t base, int k) {
+  uint32_t key = 0, mult = 1;
+  for (int d = 0; d <= k; ++d) {
+    key += (2u * (li % lat_t) + 1u) * mult;
+    li /= lat_t;
+    mult *= base;
+  }
+  return key;
+}
+
+// counter `ci` reached 2^15 (this thread's increment set the guard bit):
+// move 2^15 to the histogram (staged word `w` names the gram)
+__device__ __noinline__ void spill16(uint32_t* cells, uint32_t ci, uint32_t* hist, uint32_t w,
+                                     uint32_t lat_t, uint32_t base, int k) {
+  atomicSub(cells + (ci >> 1), 0x8000u << ((ci & 1u) << 4));
+  const uint32_t key = (w & STG_LAT) ? lat_key(w & ~STG_LAT, lat_t, base, k) : w;
+  atomicAdd(hist + key, 0x8000u);
+}
 
 __global__ void __launch_bounds__(SH_T, 1) stage_hist_kernel(const uint32_t* __restrict__ words,
                                                              int64_t n, uint32_t* __restrict__ reps,
                                                              int64_t n_bins, int n_reps,
-                                                             uint32_t dlo, uint32_t dn) {
-  extern __shared__ uint32_t dense[];
-  for (uint32_t i = threadIdx.x; i < dn; i += SH_T) dense[i] = 0;
+                                                             uint32_t dlo, uint32_t dn,
+                                                             uint32_t lat_t, uint32_t lat_n,
+                                                             uint32_t base, int k) {
+  extern __shared__ uint32_t cells[];
+  const uint32_t n_cells = ((dn + 1) >> 1) + ((lat_n + 1) >> 1);
+  for (uint32_t i = threadIdx.x; i < n_cells; i += SH_T) cells[i] = 0;
   __syncthreads();
   // replica per CTA group: a hot bin's updates spread over n_reps addresses
   uint32_t* __restrict__ hist = reps + (int64_t)(blockIdx.x % n_reps) * n_bins;
   const int64_t stride = (int64_t)gridDim.x * SH_T;
   const int64_t t0 = (int64_t)blockIdx.x * SH_T + threadIdx.x;
   const int64_t n4 = n >> 2;
+  // one counter space: dense block [0, dn), lattice from loff2 (word aligned)
+  const uint32_t loff2 = 2u * ((dn + 1) >> 1);
   auto one = [&](uint32_t w) {
     if (w & STG_HOT) return;
-    if (w - dlo < dn) atomicAdd(dense + (w - dlo), 1u);
-    else atomicAdd(hist + w, 1u);
+    const bool lw = (w & STG_LAT) != 0;
+    const uint32_t ci = lw ? loff2 + (w & ~STG_LAT) : w - dlo;
+    if (lw || ci < dn) {
+      const uint32_t sh = (ci & 1u) << 4;
+      const uint32_t old = atomicAdd(cells + (ci >> 1), 1u << sh);
+      if (((old >> sh) & 0xffffu) == 0x7fffu) spill16(cells, ci, hist, w, lat_t, base, k);
+    } else {
+      atomicAdd(hist + w, 1u);
+    }
   };
   for (int64_t i = t0; i < n4; i += stride) {
     const uint4 v = __ldcs(reinterpret_cast<const uint4*>(words) + i);
@@ -686,9 +738,34 @@ __global__ void __launch_bounds__(SH_T, 1) stage_hist_kernel(const uint32_t* __r
     one(v.w);
   }
   for (int64_t i = 4 * n4 + t0; i < n; i += stride) one(words[i]);
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < dn; i += SH_T)
-    if (dense[i]) atomicAdd(hist + dlo + i, dense[i]);
+  // flush: the CTA pair of a cluster sums its two tables over DSMEM, each
+  // CTA flushing half of the counters (half the REDs of a per-CTA flush)
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  const uint32_t cr = cl.block_rank(), cn = cl.num_blocks();
+  const uint32_t* peer = cn == 2 ? cl.map_shared_rank(cells, cr ^ 1u) : nullptr;
+  auto counter = [&](uint32_t word, uint32_t half) {
+    uint32_t v = cells[word];
+    if (peer) v += peer[word] & (0xffffu << (half << 4));  // halves stay below 2^16
+    return (v >> (half << 4)) & 0xffffu;
+  };
+  // (a half of one CTA is < 2^15 after the main loop, so the sum of the
+  // pair's halves is < 2^16 and never carries out of its half)
+  for (uint32_t i = cr * ((dn + 1) >> 1) / cn * 2 + threadIdx.x,
+                e = cr + 1 == cn ? dn : (cr + 1) * ((dn + 1) >> 1) / cn * 2;
+       i < e; i += SH_T) {
+    const uint32_t c = counter(i >> 1, i & 1u);
+    if (c) atomicAdd(hist + dlo + i, c);
+  }
+  const uint32_t loff = (dn + 1) >> 1;
+  for (uint32_t i = cr * ((lat_n + 1) >> 1) / cn * 2 + threadIdx.x,
+                e = cr + 1 == cn ? lat_n : (cr + 1) * ((lat_n + 1) >> 1) / cn * 2;
+       i < e; i += SH_T) {
+    const uint32_t c = counter(loff + (i >> 1), i & 1u);
+    if (c) atomicAdd(hist + lat_key(i, lat_t, base, k), c);
+  }
+  cl.sync();  // the peer's table stays live until both halves are flushed
 }
 
 // hist += sum of the replicas (one pass over n_reps * n_bins words in L2)
@@ -710,7 +787,8 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
                                                             int32_t* __restrict__ tok_out,
                                                             uint32_t* __restrict__ stage_out,
                                                             unsigned long long* tile_ctr,
-                                                            uint32_t hot_lo, uint32_t hot_n) {
+                                                            uint32_t hot_lo, uint32_t hot_n,
+                                                            uint32_t lat_t) {
   extern __shared__ __align__(16) uint8_t c_smem[];
   ColumnTile* tiles = reinterpret_cast<ColumnTile*>(c_smem);
   uint32_t* hot = reinterpret_cast<uint32_t*>(tiles + CNST);
@@ -807,7 +885,7 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
       constexpr bool STAGE = OUT == 2;
       uint32_t k0 = 0, k1 = 0;
       if (xa < n) {
-        k0 = count_event<K, STAGE>(w0, S, base, hot_lo, hot_n, hot, hist);
+        k0 = count_event<K, STAGE>(w0, S, base, hot_lo, hot_n, hot, hist, lat_t);
         segs += v0 >> 31;  // segment starts
         if (xa > 0) {
           const bool back = (ts.x < pts) | ((ts.x == pts) & (sq.x <= pq));
@@ -816,7 +894,7 @@ __global__ void __launch_bounds__(CT) columnar_count_kernel(const paste_columnar
         if (OUT == 1) tok_out[xa] = (int32_t)v0;
       }
       if (xb < n) {
-        k1 = count_event<K, STAGE>(w1, S, base, hot_lo, hot_n, hot, hist);
+        k1 = count_event<K, STAGE>(w1, S, base, hot_lo, hot_n, hot, hist, lat_t);
         segs += v1 >> 31;
         const bool back = (ts.y < ts.x) | ((ts.y == ts.x) & (sq.y <= sq.x));
         bad += (ss.y < ss.x) | ((ss.y == ss.x) & back);
@@ -883,8 +961,19 @@ static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint
   if (ctr == nullptr) return -2;
   if (cudaMemsetAsync(ctr, 0, sizeof(*ctr), stream) != cudaSuccess) return -2;
   const int64_t grid = tiles < grid_cap ? tiles : grid_cap;
+  // success lattice (staged counting): (S/2)^(K+1) cells, keys below 2^30
+  uint32_t lat_t = 0, lat_n = 0;
+  if (OUT == 2 && g.n_bins <= (int64_t)STG_LAT) {
+    uint64_t cells = 1;
+    for (int d = 0; d <= K; ++d) cells *= (uint64_t)(g.S / 2);
+    if (g.S >= 2 && cells <= LAT_MAX) {
+      lat_t = (uint32_t)(g.S / 2);
+      lat_n = (uint32_t)cells;
+    }
+  }
   columnar_count_kernel<K, OUT><<<(unsigned)grid, CT, smem, stream>>>(c, g, hist, c.tokens_out,
-                                                                      stage, ctr, hot_lo, hot_n);
+                                                                      stage, ctr, hot_lo, hot_n,
+                                                                      lat_t);
   if (OUT == 2) {
     uint32_t* reps = stage + stage_words(c.n_events);
     if (cudaMemsetAsync(reps, 0, (size_t)STG_REPS * g.n_bins * sizeof(uint32_t), stream) !=
@@ -901,11 +990,26 @@ static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(stage_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SH_DENSE_MAX * (int)sizeof(uint32_t));
+                           SH_SMEM_MAX);
       attr = true;
     }
-    stage_hist_kernel<<<(unsigned)sms, SH_T, dn * sizeof(uint32_t), stream>>>(
-        stage, c.n_events, reps, g.n_bins, STG_REPS, dlo, dn);
+    const size_t sh_bytes = (size_t)(((dn + 1) >> 1) + ((lat_n + 1) >> 1)) * sizeof(uint32_t);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr_c[1];
+    attr_c[0].id = cudaLaunchAttributeClusterDimension;
+    attr_c[0].val.clusterDim.x = 2;  // CTA pairs (148 SMs = 74 pairs)
+    attr_c[0].val.clusterDim.y = 1;
+    attr_c[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3((unsigned)(sms & ~1));
+    cfg.blockDim = dim3(SH_T);
+    cfg.dynamicSmemBytes = sh_bytes;
+    cfg.stream = stream;
+    cfg.attrs = attr_c;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, stage_hist_kernel, (const uint32_t*)stage, (int64_t)c.n_events,
+                           reps, (int64_t)g.n_bins, (int)STG_REPS, dlo, dn, lat_t, lat_n,
+                           (uint32_t)g.base, (int)K) != cudaSuccess)
+      return -2;
     fold_replicas_kernel<<<(unsigned)(sms * 4), 256, 0, stream>>>(reps, g.n_bins, STG_REPS, hist);
   }
   return 0;

@@ -186,6 +186,31 @@ def test_columnar_staged_count_equals_single_pass(k):
         assert np.array_equal(dev_t.cpu().numpy().astype(np.uint64), ref)
 
 
+def test_columnar_staged_count_spills_skewed_grams():
+    """A corpus dominated by one all-success gram and one third-event gram:
+    the 16-bit shared-memory counters of the staged pass (success lattice,
+    dense block) spill many times per CTA; the histogram still equals the
+    plain RED pass."""
+    from paper_2603_18897_b200.mine_engine import ingest_count
+
+    rng = np.random.default_rng(5)
+    short, long_ = 6_000_000, 14_000_000
+    sess = np.concatenate([np.arange(short) // 3, short // 3 + np.arange(long_) // 1000])
+    seq = np.concatenate([np.arange(short) % 3, np.arange(long_) % 1000]).astype(np.int32)
+    sig = np.where(rng.random(short + long_) < 0.03, rng.integers(0, 32, short + long_), 7)
+    t = seq.astype(np.float64) * 10.0
+    c = dict(session=sess.astype(np.int32), seq=seq, t_start=t, t_end=t + 1.0,
+             sig=sig.astype(np.int32))
+    dev = _dev(c)
+    for k in (3, 2):
+        a = MineTables.allocate(32, k, 0)
+        b = MineTables.allocate(32, k, 0)
+        ca = ingest_count(a, dev, staged=True)
+        cb = ingest_count(b, dev, staged=False)
+        assert torch.equal(a.hist, b.hist) and torch.equal(ca, cb)
+        assert int(a.hist.max()) > 10_000_000  # the hot cells spilled many times
+
+
 def test_mine_columnar_patterns_match_oracle_selection():
     from paper_2603_18897_b200.mine_engine import mine_columnar, patterns_from_candidates
     from paper_2603_18897_b200.packing import SigTable
