@@ -503,6 +503,164 @@ __device__ __forceinline__ void predict_session(const FastParams& P, int64_t ses
 }
 
 
+// ---------------------------------------------------------------------------
+// Warp-cooperative table path.  Lane-per-session resolution leaves most
+// lanes idle (about 7 of 32 sessions have a mapped candidate at a given rank)
+// so the argument walks -- the bulk of the instructions -- run from a
+// per-warp queue instead, one binding per lane:
+//   A. lane per session: observe, gather, table entry; per candidate rank the
+//      pattern id is written and the mapped bindings are queued (event,
+//      binding, owner lane / rank / slot / source age);
+//   B. whole warp: full rounds of 32 queued bindings are resolved (walk memo
+//      as before) and written; an unresolved one marks its candidate PARTIAL
+//      in the owner's shared-memory mask;
+//   C. lane per session: completeness codes and the streamed admit.
+// ---------------------------------------------------------------------------
+constexpr int RQ = 32 + 32 * MT_MAX_BIND;  // queue entries per warp
+constexpr int COOP_MAX_K = 64;             // candidate rank fits 6 bits
+
+struct ResolveQueue {
+  uint32_t bind[RQ];
+  uint32_t meta[RQ];   // owner lane | rank << 5 | slot << 11 | source age << 14
+  int64_t rbase[32];   // ring addressing of every lane's session
+  int64_t rstride[32];
+  unsigned long long part[32];  // ranks with an unresolved binding, per lane
+};
+
+__host__ __device__ inline size_t coop_smem_bytes(int row) {
+  return sizeof(uint64_t) * MEMO + sizeof(int32_t) * FT * row +
+         sizeof(ResolveQueue) * (FT / 32);
+}
+
+__device__ __forceinline__ OutIdx out_idx(const FastParams& P, int64_t sess) {
+  const int64_t n = P.win.n_sessions;
+  const int K = P.out.max_candidates;
+  OutIdx X;
+  X.B = P.out.max_bindings;
+  X.ostride = P.out.slot_major ? n : 1;
+  X.obase = P.out.slot_major ? sess : sess * K;
+  X.abase = P.out.slot_major ? sess : sess * K * X.B;
+  return X;
+}
+
+__device__ __forceinline__ void predict_coop(const FastParams& P, int64_t sess, bool live,
+                                             int32_t* rows, uint64_t* memo, ResolveQueue& q) {
+  const unsigned FULLM = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t warp_first = sess - lane;
+  int32_t* gt = rows + lane * P.row;
+  const paste_pool_desc& pool = P.pool;
+  const OutIdx X = out_idx(P, sess);
+  const bool admit = P.adm.enabled != 0;
+  int64_t rbase = 0, rstride = 0;
+  int nm = 0, n_err = 0, n_act = 0;
+  uint64_t seen = 0;
+  const MTRecord* recs = nullptr;
+  if (live) {
+    const int m = observe_gather(P, sess, gt, rbase, rstride);
+    if (m > 0 && gt[0] < pool.n_bucket_sigs) {
+      const uint8_t* e = table_entry(P, gt, m);
+      const int2 hdr = __ldg(reinterpret_cast<const int2*>(e));
+      recs = reinterpret_cast<const MTRecord*>(e + 16);
+      n_err = hdr.y;
+      nm = hdr.x < P.out.max_candidates ? hdr.x : P.out.max_candidates;
+    }
+  }
+  q.rbase[lane] = rbase;
+  q.rstride[lane] = rstride;
+  q.part[lane] = 0ull;
+  __syncwarp();
+  const int max_nm = (int)__reduce_max_sync(FULLM, (unsigned)nm);
+  int count = 0;
+  for (int i = 0; i < max_nm; ++i) {
+    // ---- A: rank i of every session: records, provisional completeness
+    // (FULL when mapped; B downgrades), admit, mapped bindings queued --------
+    int nb = 0, bind_off = 0;
+    uint32_t src = 0;
+    if (i < nm) {
+      const int4 r0 = __ldg(reinterpret_cast<const int4*>(recs + i));
+      const int4 r1 = __ldg(reinterpret_cast<const int4*>(recs + i) + 1);
+      const bool mapped = ((r0.w >> 16) & PASTE_PF_HAS_MAPPING) != 0;
+      const int comp = mapped ? PASTE_C_FULL : PASTE_C_TOOL_ONLY;
+      const int64_t o = X.o(i);
+      P.out.pred_pat[o] = r0.x;
+      P.out.pred_comp[o] = (uint8_t)comp;
+      if (admit) admit_one(P, X, i, r0.z, comp, __hiloint2double(r1.w, r1.z), n_act, seen);
+      if (mapped) {
+        nb = r0.w & 0xffff;
+        src = (uint32_t)r0.y;
+        bind_off = r1.x;
+      }
+    }
+    // offsets: one binding per candidate is the common case (ballot); wider
+    // candidates add a scan
+    int pos, total;
+    const unsigned any = __ballot_sync(FULLM, nb > 0);
+    if (__all_sync(FULLM, nb <= 1)) {
+      pos = count + __popc(any & lt);
+      total = __popc(any);
+    } else {
+      int incl = nb;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULLM, incl, o);
+        if (lane >= o) incl += t;
+      }
+      total = __shfl_sync(FULLM, incl, 31);
+      pos = count + incl - nb;
+    }
+    for (int b = 0; b < nb; ++b) {
+      q.bind[pos + b] = (uint32_t)(bind_off + b);
+      q.meta[pos + b] = (uint32_t)lane | ((uint32_t)i << 5) | ((uint32_t)b << 11) |
+                        (((src >> (4 * b)) & 15u) << 14);
+    }
+    count += total;
+    __syncwarp();
+    // ---- B: full rounds of 32 bindings (and the rest after the last rank) --
+    const bool last = i + 1 == max_nm;
+    while (count >= 32 || (last && count > 0)) {
+      const int take = count < 32 ? count : 32;
+      if (lane < take) {
+        const int t = count - take + lane;
+        const uint32_t meta = q.meta[t];
+        const int owner = meta & 31, ri = (meta >> 5) & 63, slot = (meta >> 11) & 7;
+        const int age = (meta >> 14) & 15;
+        const int bind = (int)q.bind[t];
+        const int32_t* ogt = rows + owner * P.row;
+        const int32_t ev = P.win.evt[q.rbase[owner] + ogt[P.G + age] * q.rstride[owner]];
+        const paste_binding bd = pool.bindings[bind];
+        const int64_t r = resolve_fast(P.win, pool.steps, bd, bind, ev, age, ogt, memo);
+        const OutIdx Y = out_idx(P, warp_first + owner);
+        P.out.pred_arg[Y.a(ri, slot)] = r;
+        if (r < 0) {
+          P.out.pred_comp[Y.o(ri)] = (uint8_t)PASTE_C_PARTIAL;
+          atomicOr(q.part + owner, 1ull << ri);
+        }
+      }
+      count -= take;
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  if (!live) return;
+  // ---- C: admitted PARTIAL candidates get level min(cap, WARM_ONLY) ---------
+  const unsigned long long pm = q.part[lane];
+  if (admit && pm) {
+    for (int j = 0; j < n_act; ++j) {
+      const int64_t o = X.o(j);
+      const int ip = P.out.act_pred[o];
+      if ((pm >> ip) & 1ull) {
+        const int cap = __ldg(P.adm.max_level + __ldg(&recs[ip].tool));
+        P.out.act_level[o] = (uint8_t)(cap < 1 ? cap : 1);
+      }
+    }
+  }
+  P.out.n_pred[sess] = nm;
+  P.out.struct_err[sess] = n_err;
+  if (admit) P.out.n_act[sess] = n_act;
+}
+
 // Persistent CTAs (grid = SMs x resident CTAs): each loops over 128-session
 // chunks so its shared-memory walk memo stays warm across chunks.
 template <bool TABLE>
@@ -511,8 +669,18 @@ __global__ void __launch_bounds__(FT, 8) predict_fast_kernel(const FastParams P)
   uint64_t* memo = s_mem;
   for (int i = threadIdx.x; i < MEMO; i += FT) memo[i] = 0;
   __syncthreads();
-  int32_t* gt = reinterpret_cast<int32_t*>(s_mem + MEMO) + threadIdx.x * P.row;
+  int32_t* rows = reinterpret_cast<int32_t*>(s_mem + MEMO);
+  int32_t* gt = rows + threadIdx.x * P.row;
   const int64_t n = P.win.n_sessions;
+  if (TABLE && P.out.max_candidates <= COOP_MAX_K) {
+    const int warp = threadIdx.x >> 5;
+    ResolveQueue* qs = reinterpret_cast<ResolveQueue*>(rows + FT * P.row);
+    for (int64_t first = (int64_t)blockIdx.x * FT; first < n; first += (int64_t)gridDim.x * FT) {
+      const int64_t sess = first + threadIdx.x;
+      predict_coop(P, sess, sess < n, rows + warp * 32 * P.row, memo, qs[warp]);
+    }
+    return;
+  }
   for (int64_t first = (int64_t)blockIdx.x * FT; first < n; first += (int64_t)gridDim.x * FT) {
     const int64_t sess = first + threadIdx.x;
     if (sess < n) predict_session<TABLE>(P, sess, gt, memo);
@@ -755,8 +923,10 @@ bool predict_fast_dispatch(const paste_pool_desc* pool, const paste_windows* win
   if (P.pool.match_table != nullptr &&
       (P.pool.mt_k < out->max_candidates || P.pool.mt_g != G || pool->max_bindings > MT_MAX_BIND))
     P.pool.match_table = nullptr;  // stale table: scan instead
-  const size_t smem = sizeof(uint64_t) * MEMO + sizeof(int32_t) * FT * P.row;
   const bool table = P.pool.match_table != nullptr;
+  const size_t smem = table && out->max_candidates <= COOP_MAX_K
+                          ? coop_smem_bytes(P.row)
+                          : sizeof(uint64_t) * MEMO + sizeof(int32_t) * FT * P.row;
   static int sms = 0, per_sm[2] = {0, 0};
   if (sms == 0) {
     int dev = 0;
