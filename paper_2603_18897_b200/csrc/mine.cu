@@ -718,24 +718,35 @@ __global__ void __launch_bounds__(SH_T, 1) stage_hist_kernel(const uint32_t* __r
   const int64_t n4 = n >> 2;
   // one counter space: dense block [0, dn), lattice from loff2 (word aligned)
   const uint32_t loff2 = 2u * ((dn + 1) >> 1);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(cells);
+  const uint32_t lat_adj = loff2 - STG_LAT;  // lattice word -> counter index
   auto one = [&](uint32_t w) {
     if (w & STG_HOT) return;
     const bool lw = (w & STG_LAT) != 0;
-    const uint32_t ci = lw ? loff2 + (w & ~STG_LAT) : w - dlo;
+    const uint32_t ci = w + (lw ? lat_adj : 0u - dlo);
     if (lw || ci < dn) {
       const uint32_t sh = (ci & 1u) << 4;
-      const uint32_t old = atomicAdd(cells + (ci >> 1), 1u << sh);
+      uint32_t old;
+      asm volatile("atom.shared.add.u32 %0, [%1], %2;"
+                   : "=r"(old)
+                   : "r"(sbase + ((ci >> 1) << 2)), "r"(1u << sh)
+                   : "memory");
       if (((old >> sh) & 0xffffu) == 0x7fffu) spill16(cells, ci, hist, w, lat_t, base, k);
     } else {
       atomicAdd(hist + w, 1u);
     }
   };
+  // software-pipelined: the next vector is in flight while this one counts
+  const uint4* wv = reinterpret_cast<const uint4*>(words);
+  uint4 v = t0 < n4 ? __ldcs(wv + t0) : make_uint4(STG_HOT, STG_HOT, STG_HOT, STG_HOT);
   for (int64_t i = t0; i < n4; i += stride) {
-    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(words) + i);
+    const uint4 nx = i + stride < n4 ? __ldcs(wv + i + stride)
+                                     : make_uint4(STG_HOT, STG_HOT, STG_HOT, STG_HOT);
     one(v.x);
     one(v.y);
     one(v.z);
     one(v.w);
+    v = nx;
   }
   for (int64_t i = 4 * n4 + t0; i < n; i += stride) one(words[i]);
   // flush: the CTA pair of a cluster sums its two tables over DSMEM, each
