@@ -986,9 +986,13 @@ static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint
                                                                       stage, ctr, hot_lo, hot_n,
                                                                       lat_t);
   if (OUT == 2) {
-    uint32_t* reps = stage + stage_words(c.n_events);
-    if (cudaMemsetAsync(reps, 0, (size_t)STG_REPS * g.n_bins * sizeof(uint32_t), stream) !=
-        cudaSuccess)
+    // with the lattice in shared memory the cold REDs are spread enough to go
+    // straight into the histogram; otherwise into STG_REPS replicas + fold
+    const int n_reps = (lat_n > 0 && getenv("PASTE_STAGE_REPS") == nullptr) ? 1 : STG_REPS;
+    uint32_t* reps = n_reps == 1 ? hist : stage + stage_words(c.n_events);
+    if (n_reps > 1 &&
+        cudaMemsetAsync(reps, 0, (size_t)n_reps * g.n_bins * sizeof(uint32_t), stream) !=
+            cudaSuccess)
       return -2;
     // dense block (k = 3): grams whose oldest symbol is BEGIN -- a segment's
     // third event -- when their base^3 counters fit in shared memory
@@ -1018,10 +1022,11 @@ static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint
     cfg.attrs = attr_c;
     cfg.numAttrs = 1;
     if (cudaLaunchKernelEx(&cfg, stage_hist_kernel, (const uint32_t*)stage, (int64_t)c.n_events,
-                           reps, (int64_t)g.n_bins, (int)STG_REPS, dlo, dn, lat_t, lat_n,
+                           reps, (int64_t)g.n_bins, n_reps, dlo, dn, lat_t, lat_n,
                            (uint32_t)g.base, (int)K) != cudaSuccess)
       return -2;
-    fold_replicas_kernel<<<(unsigned)(sms * 4), 256, 0, stream>>>(reps, g.n_bins, STG_REPS, hist);
+    if (n_reps > 1)
+      fold_replicas_kernel<<<(unsigned)(sms * 4), 256, 0, stream>>>(reps, g.n_bins, n_reps, hist);
   }
   return 0;
 }
