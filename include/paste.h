@@ -503,8 +503,14 @@ int paste_resolve(const paste_resolve_desc* d, void* stream);
  * totals = {predictions, arguments, actions, refs outside the chosen arg
  * form (0 expected: else re-fetch the full records), structural errors}.
  * Requires max_candidates <= 31 and n_patterns <= 16384; HDR8 needs
- * max_candidates <= 15, PRED8 n_patterns <= 64.                            */
-enum { PASTE_CF_HDR8 = 1, PASTE_CF_PRED8 = 2, PASTE_CF_ARG16 = 4 };
+ * max_candidates <= 15, PRED8 n_patterns <= 64.
+ * PASTE_CF_ENTRY16 (paste_predict_compact only): the pred stream instead
+ * holds one u16 per session, the session's match-table key (0xFFFF = no
+ * entry, no predictions).  The predictions are the first n_pred records of
+ * that entry (paste_build_match_table), so the host expands them from its
+ * copy of the table; completeness follows from the pattern (no mapping =
+ * TOOL_ONLY) and the arg stream (an all-ones reference = PARTIAL).        */
+enum { PASTE_CF_HDR8 = 1, PASTE_CF_PRED8 = 2, PASTE_CF_ARG16 = 4, PASTE_CF_ENTRY16 = 8 };
 typedef struct {
   void* hdr;         /* [n]                                                  */
   void* pred;
@@ -514,6 +520,14 @@ typedef struct {
   int32_t format;    /* PASTE_CF_* bits                                       */
   int32_t pad;
 } paste_compact_desc;
+
+/* 1 when paste_predict_compact runs the fused kernel for this request shape
+ * (else it returns PASTE_ERR_UNSUPPORTED and the caller runs
+ * paste_predict_batch + paste_compact_records, which cannot produce
+ * PASTE_CF_ENTRY16).  `pool` must carry its match table.                   */
+int paste_predict_compact_supported(const paste_pool_desc* pool, int32_t window_capacity,
+                                    int32_t max_candidates, int32_t max_bindings,
+                                    int32_t format);
 
 /* The serving step in one kernel: paste_predict_batch (observe + predict +
  * admit, same semantics) writing the step's records straight into the

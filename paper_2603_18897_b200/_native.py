@@ -114,7 +114,7 @@ class CompactDesc(ctypes.Structure):
                 ("totals", c_void_p), ("format", c_int32), ("pad", c_int32)]
 
 
-PASTE_CF_HDR8, PASTE_CF_PRED8, PASTE_CF_ARG16 = 1, 2, 4
+PASTE_CF_HDR8, PASTE_CF_PRED8, PASTE_CF_ARG16, PASTE_CF_ENTRY16 = 1, 2, 4, 8
 
 
 class HoldsDesc(ctypes.Structure):
@@ -180,6 +180,7 @@ EXPORTS = {
     "paste_ingest_jsonl": (c_int, [c_char_p, c_int64, ctypes.c_double, POINTER(IngestDesc)]),
     "paste_action_keys": (c_int, [POINTER(ActionKeysDesc), c_void_p]),
     "paste_predict_compact_scratch_bytes": (c_int64, [c_int64]),
+    "paste_predict_compact_supported": (c_int, [POINTER(PoolDesc), c_int, c_int, c_int, c_int]),
     "paste_predict_compact": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc), POINTER(AdmitDesc),
                                       c_int32, c_int32, POINTER(CompactDesc), c_void_p, c_void_p]),
     "paste_compact_records": (c_int, [POINTER(PredictOut), c_int64, POINTER(PoolDesc),

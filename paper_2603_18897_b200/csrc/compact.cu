@@ -135,6 +135,10 @@ extern "C" int paste_compact_records(const paste_predict_out* out, int64_t n_ses
                 "PASTE_CF_HDR8 needs max_candidates <= 15");
   PASTE_REQUIRE(!(c->format & PASTE_CF_PRED8) || pool->n_patterns <= 64,
                 "PASTE_CF_PRED8 needs at most 64 patterns");
+  if (c->format & PASTE_CF_ENTRY16) {
+    set_error("PASTE_CF_ENTRY16 is produced by paste_predict_compact only");
+    return PASTE_ERR_UNSUPPORTED;
+  }
   cudaStream_t stream = (cudaStream_t)stream_;
   const int64_t tiles = (n_sessions + KT_T - 1) / KT_T;
   PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, paste_compact_scratch_bytes(n_sessions), stream));

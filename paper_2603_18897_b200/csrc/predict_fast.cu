@@ -356,7 +356,18 @@ __device__ __forceinline__ int observe_gather(const FastParams& P, int64_t sess,
   return m;
 }
 
-// match-table entry of the gathered tokens (the newest G tool tokens)
+// match-table key / entry of the gathered tokens (the newest G tool tokens)
+__device__ __forceinline__ int64_t table_key(const FastParams& P, const int32_t* gt, int m) {
+  const int S = P.pool.n_bucket_sigs, G = P.G;
+  int64_t key = gt[0], mult = S;
+  for (int a = 1; a < G; ++a) {
+    const int t = a < m ? gt[a] : S;
+    key += (int64_t)(t < S ? t : S) * mult;
+    mult *= (S + 1);
+  }
+  return key;
+}
+
 __device__ __forceinline__ const uint8_t* table_entry(const FastParams& P, const int32_t* gt,
                                                       int m) {
   const int S = P.pool.n_bucket_sigs, G = P.G;
@@ -728,12 +739,15 @@ __host__ __device__ inline int stage_stride(int K, int B) {  // bytes per thread
 __device__ __forceinline__ void compact_stage(const FastParams& P, int64_t sess, int64_t rbase,
                                               int64_t rstride, const int32_t* gt, int m,
                                               const Stage& S, int c[4], uint64_t* memo,
-                                              unsigned long long& wide) {
+                                              unsigned long long& wide, uint32_t& key) {
   c[0] = c[1] = c[2] = c[3] = 0;
+  key = 0xffffu;
   if (m == 0 || gt[0] >= P.pool.n_bucket_sigs) return;
   const int64_t n = P.win.n_sessions;
   const int32_t* gs = gt + P.G;
-  const uint8_t* e = table_entry(P, gt, m);
+  const int64_t tk = table_key(P, gt, m);
+  key = (uint32_t)tk;
+  const uint8_t* e = static_cast<const uint8_t*>(P.pool.match_table) + tk * mt_stride(P.pool.mt_k);
   const int2 hdr = __ldg(reinterpret_cast<const int2*>(e));
   const MTRecord* recs = reinterpret_cast<const MTRecord*>(e + 16);
   const int K = P.out.max_candidates;
@@ -806,11 +820,15 @@ __device__ __forceinline__ void compact_stage(const FastParams& P, int64_t sess,
 // Write one session's staged records at its stream offsets o[].
 __device__ __forceinline__ void compact_flush(const paste_compact_desc& C, int64_t sess,
                                               const Stage& S, const int c[4], const uint64_t o[3],
-                                              unsigned long long& wide) {
+                                              unsigned long long& wide, uint32_t key) {
   cf_hdr(C, sess, c[0], c[2]);
-  for (int i = 0; i < c[0]; ++i) {
-    const uint16_t v = S.pred[i];
-    cf_pred(C, o[0] + i, v & 0x3fff, v >> 14);
+  if (C.format & PASTE_CF_ENTRY16) {  // the entry key stands for the prediction list
+    static_cast<uint16_t*>(C.pred)[sess] = (uint16_t)key;
+  } else {
+    for (int i = 0; i < c[0]; ++i) {
+      const uint16_t v = S.pred[i];
+      cf_pred(C, o[0] + i, v & 0x3fff, v >> 14);
+    }
   }
   const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
   for (int j = 0; j < c[1]; ++j) {
@@ -859,10 +877,11 @@ __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactPar
     const int64_t sess = tile * FT + threadIdx.x;
     // ---- the whole step for this session, records staged in shared memory --
     int c[4] = {0, 0, 0, 0};
+    uint32_t key = 0xffffu;
     if (sess < n) {
       int64_t rbase, rstride;
       const int m = observe_gather(P, sess, gt, rbase, rstride);
-      compact_stage(P, sess, rbase, rstride, gt, m, SG, c, memo, wide);
+      compact_stage(P, sess, rbase, rstride, gt, m, SG, c, memo, wide, key);
     }
     // ---- block-wide exclusive scan of the 4 counters ------------------------
     uint64_t inc[4];
@@ -908,7 +927,7 @@ __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactPar
         for (int w = 0; w < warp; ++w) before += s_warp[w][k];
         o[k] = s_excl[k] + before + inc[k] - (uint64_t)c[k];
       }
-      compact_flush(Q.C, sess, SG, c, o, wide);
+      compact_flush(Q.C, sess, SG, c, o, wide, key);
     }
   }
   if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(Q.C.totals + 3), wide);
@@ -952,21 +971,31 @@ bool predict_fast_dispatch(const paste_pool_desc* pool, const paste_windows* win
 
 // Fused predict + compaction launch; false = not eligible (no match table,
 // G > 16, K > 31, ...): the caller runs paste_predict_batch + compaction.
+bool compact_eligible(const paste_pool_desc* pool, int K, int B, int format, int G) {
+  static const bool force_generic = getenv("PASTE_FORCE_GENERIC") != nullptr;
+  if (force_generic || G > 16 || K > 31 || K * B > 64 || pool->match_table == nullptr ||
+      pool->mt_k < K || pool->mt_g != G || pool->max_bindings > MT_MAX_BIND ||
+      pool->n_patterns > (1 << 14) || ((format & PASTE_CF_HDR8) && K > 15) ||
+      ((format & PASTE_CF_PRED8) && pool->n_patterns > 64))
+    return false;
+  if (format & PASTE_CF_ENTRY16) {  // keys must fit u16 below the 0xFFFF marker
+    const int64_t keys = keys_for(pool, G);
+    if (keys < 0 || keys >= 0xffff) return false;
+  }
+  return true;
+}
+
 bool predict_compact_dispatch(const paste_pool_desc* pool, const paste_windows* win,
                               const paste_admit_desc* adm, int K, int B,
                               const paste_compact_desc* c, void* scratch, int G,
                               cudaStream_t stream) {
-  if (G > 16 || K > 31 || pool->match_table == nullptr || pool->mt_k < K || pool->mt_g != G ||
-      pool->max_bindings > MT_MAX_BIND || pool->n_patterns > (1 << 14) || win->stream_end ||
-      ((c->format & PASTE_CF_HDR8) && K > 15) || ((c->format & PASTE_CF_PRED8) && pool->n_patterns > 64))
-    return false;
+  if (win->stream_end || !compact_eligible(pool, K, B, c->format, G)) return false;
   paste_predict_out out{};
   out.max_candidates = K;
   out.max_bindings = B;
   CompactParams Q{FastParams{*pool, *win, *adm, out, G, 2 * G + 1}, *c,
                   static_cast<uint64_t*>(scratch), static_cast<uint64_t*>(scratch) + LB_STRIDE,
                   (win->n_sessions + FT - 1) / FT};
-  if (K * B > 64) return false;  // staging would not fit (two-kernel path)
   const size_t smem = sizeof(uint64_t) * MEMO +
                       (((size_t)sizeof(int32_t) * FT * Q.F.row + 15) & ~(size_t)15) +
                       (size_t)FT * stage_stride(K, B);
@@ -989,6 +1018,18 @@ bool predict_compact_dispatch(const paste_pool_desc* pool, const paste_windows* 
 }
 
 }  // namespace paste
+
+extern "C" int paste_predict_compact_supported(const paste_pool_desc* pool,
+                                               int32_t window_capacity, int32_t max_candidates,
+                                               int32_t max_bindings, int32_t format) {
+  using namespace paste;
+  if (!pool || window_capacity < 1 || max_candidates < 1 || max_bindings < pool->max_bindings)
+    return 0;
+  return compact_eligible(pool, max_candidates, max_bindings, format,
+                          gather_depth(pool, window_capacity))
+             ? 1
+             : 0;
+}
 
 extern "C" int64_t paste_predict_compact_scratch_bytes(int64_t n_sessions) {
   const int64_t tiles = (n_sessions + paste::FT - 1) / paste::FT;

@@ -110,6 +110,12 @@ class LiveSessionTable:
         self.pool_desc = dpool.desc(max_candidates, capacity)
         self.steps = 0
         self.lib = _native.lib()
+        # serve() format: with the fused kernel the prediction list ships as
+        # the session's match-table key (PASTE_CF_ENTRY16) when keys fit u16
+        ef = self.cformat | _native.PASTE_CF_ENTRY16
+        self.sformat = ef if self.lib.paste_predict_compact_supported(
+            ctypes.byref(self.pool_desc), capacity, K, B, ef) else self.cformat
+        self._entries = None
 
     # -- state upload ---------------------------------------------------------
 
@@ -208,6 +214,19 @@ class LiveSessionTable:
         t.cuda.current_stream().synchronize()  # the key tables above are temporaries
         return k["keys"].view(self.n * self.K, 16), k["state"]
 
+    def entries(self):
+        """Host copy of the match table's prediction lists (for
+        PASTE_CF_ENTRY16 records): (n_match[keys], pattern ids[keys, K])."""
+        if self._entries is None:
+            table, _ = self.dpool.match_table(self.pool_desc, self.K, self.W)
+            raw = table.cpu().numpy()
+            stride = 16 + 32 * self.K
+            rows = raw.reshape(-1, stride)
+            n_match = rows[:, :4].copy().view(np.int32)[:, 0]
+            recs = rows[:, 16:].copy().view(np.int32).reshape(len(rows), self.K, 8)
+            self._entries = (n_match, recs[:, :, 0].copy())
+        return self._entries
+
     def output_nbytes(self) -> int:
         return sum(v.numel() * v.element_size() for v in self.out.values())
 
@@ -248,6 +267,7 @@ class CompactRecords:
     arg: np.ndarray    # region << 27 | node (u32), or << 11 (u16, ARG16); all-ones = unresolved
     act: np.ndarray    # u8: slot | level << 5
     fmt: int = 0
+    entries: tuple | None = None  # (n_match, pattern ids [keys, K]) for PASTE_CF_ENTRY16
 
     @property
     def nbytes(self) -> int:
@@ -267,21 +287,35 @@ class CompactRecords:
         res.n_act[:] = n_act
         sess = np.repeat(np.arange(n), n_pred)
         slot = np.arange(len(sess)) - np.repeat(np.cumsum(n_pred) - n_pred, n_pred)
-        pshift = 6 if self.fmt & _native.PASTE_CF_PRED8 else 14
-        pred = self.pred.astype(np.int64)
-        pid = pred & ((1 << pshift) - 1)
-        res.pred_pat[sess * K + slot] = pid
-        res.pred_comp[sess * K + slot] = (pred >> pshift).astype(np.uint8)
-        mapped = (patterns["flags"][pid] & 1) != 0
-        nb = np.where(mapped, patterns["n_bind"][pid], 0)
-        p_sess, p_slot = np.repeat(sess, nb), np.repeat(slot, nb)
-        b_idx = np.arange(int(nb.sum())) - np.repeat(np.cumsum(nb) - nb, nb)
         a16 = bool(self.fmt & _native.PASTE_CF_ARG16)
         ashift = 11 if a16 else 27
         a = self.arg.astype(np.int64)
+        unresolved = a == (0xFFFF if a16 else 0xFFFFFFFF)
+        if self.fmt & _native.PASTE_CF_ENTRY16:
+            # the session's match-table entry lists its predictions; PARTIAL =
+            # a mapped prediction with an unresolved reference
+            pid = self.entries[1][self.pred.astype(np.int64)[sess], slot].astype(np.int64)
+            mapped = (patterns["flags"][pid] & 1) != 0
+            nb = np.where(mapped, patterns["n_bind"][pid], 0)
+            cu = np.concatenate([[0], np.cumsum(unresolved)])
+            start = np.cumsum(nb) - nb
+            partial = (cu[start + nb] - cu[start]) > 0
+            comp = np.where(mapped, np.where(partial, 1, 0), 2)
+            res.pred_pat[sess * K + slot] = pid
+            res.pred_comp[sess * K + slot] = comp.astype(np.uint8)
+        else:
+            pshift = 6 if self.fmt & _native.PASTE_CF_PRED8 else 14
+            pred = self.pred.astype(np.int64)
+            pid = pred & ((1 << pshift) - 1)
+            res.pred_pat[sess * K + slot] = pid
+            res.pred_comp[sess * K + slot] = (pred >> pshift).astype(np.uint8)
+            mapped = (patterns["flags"][pid] & 1) != 0
+            nb = np.where(mapped, patterns["n_bind"][pid], 0)
+        p_sess, p_slot = np.repeat(sess, nb), np.repeat(slot, nb)
+        b_idx = np.arange(int(nb.sum())) - np.repeat(np.cumsum(nb) - nb, nb)
         ev = (a >> ashift) * n + p_sess
         res.pred_arg[(p_sess * K + p_slot) * B + b_idx] = np.where(
-            a == (0xFFFF if a16 else 0xFFFFFFFF), -1, (ev << 32) | (a & ((1 << ashift) - 1)))
+            unresolved, -1, (ev << 32) | (a & ((1 << ashift) - 1)))
         a_sess = np.repeat(np.arange(n), n_act)
         a_slot = np.arange(len(a_sess)) - np.repeat(np.cumsum(n_act) - n_act, n_act)
         a_pred = (self.act & 31).astype(np.int64)
@@ -293,13 +327,15 @@ class CompactRecords:
         return res
 
 
-def _compact_buffers(table: "LiveSessionTable"):
+def _compact_buffers(table: "LiveSessionTable", f: int | None = None):
     t = table.torch
     n, K, B = table.n, table.K, table.B
-    f = table.cformat
+    f = table.cformat if f is None else f
     dev = t.device("cuda")
+    entry = bool(f & _native.PASTE_CF_ENTRY16)
     return {"hdr": t.zeros(n, dtype=t.uint8 if f & _native.PASTE_CF_HDR8 else t.int16, device=dev),
-            "pred": t.zeros(n * K, dtype=t.uint8 if f & _native.PASTE_CF_PRED8 else t.int16,
+            "pred": t.zeros(n if entry else n * K,
+                            dtype=t.uint8 if f & _native.PASTE_CF_PRED8 and not entry else t.int16,
                             device=dev),
             "arg": t.zeros(n * K * B, dtype=t.int16 if f & _native.PASTE_CF_ARG16 else t.int32,
                            device=dev),
@@ -322,20 +358,24 @@ def _compact_init(table: "LiveSessionTable") -> None:
     table.cdesc = _compact_desc(table.cbuf, table.cformat)
 
 
-def _records(table, h: dict) -> CompactRecords:
-    f = table.cformat
+def _records(table, h: dict, f: int | None = None) -> CompactRecords:
+    f = table.cformat if f is None else f
+    entry = bool(f & _native.PASTE_CF_ENTRY16)
     return CompactRecords(
         table.K, table.B, h["hdr"].view(np.uint8 if f & _native.PASTE_CF_HDR8 else np.uint16),
-        h["pred"].view(np.uint8 if f & _native.PASTE_CF_PRED8 else np.uint16),
-        h["arg"].view(np.uint16 if f & _native.PASTE_CF_ARG16 else np.uint32), h["act"], f)
+        h["pred"].view(np.uint8 if f & _native.PASTE_CF_PRED8 and not entry else np.uint16),
+        h["arg"].view(np.uint16 if f & _native.PASTE_CF_ARG16 else np.uint32), h["act"], f,
+        table.entries() if entry else None)
 
 
-def _sizes(table, totals) -> dict:
+def _sizes(table, totals, f: int | None = None) -> dict:
     P, A, Q, wide, _err = (int(x) for x in totals.tolist())
     if wide:
         raise _native.PasteError(f"{wide} argument refs outside the live table's event form: "
                                  "use fetch()")
-    return {"hdr": table.n, "pred": P, "arg": A, "act": Q}
+    f = table.cformat if f is None else f
+    return {"hdr": table.n, "pred": table.n if f & _native.PASTE_CF_ENTRY16 else P, "arg": A,
+            "act": Q}
 
 
 def fetch_compact(table: "LiveSessionTable", pinned: dict | None = None) -> CompactRecords:
@@ -374,10 +414,12 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
     if depth < 3:
         raise ValueError("serve() needs depth >= 3 buffer sets")
     t = table.torch
-    if getattr(table, "_serve", None) is None or len(table._serve["bufs"]) != depth:
-        bufs = [_compact_buffers(table) for _ in range(depth)]
+    fmt = table.sformat if table.serve_fused else table.cformat
+    if (getattr(table, "_serve", None) is None or len(table._serve["bufs"]) != depth
+            or table._serve["fmt"] != fmt):
+        bufs = [_compact_buffers(table, fmt) for _ in range(depth)]
         table._serve = {
-            "bufs": bufs, "descs": [_compact_desc(c, table.cformat) for c in bufs],
+            "fmt": fmt, "bufs": bufs, "descs": [_compact_desc(c, fmt) for c in bufs],
             "pinned": [{k: t.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in c.items()}
                        for c in bufs],
             "scratch": [t.empty(max(table.lib.paste_compact_scratch_bytes(table.n),
@@ -399,7 +441,7 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
     def download(k, tot_ev):
         tot_ev.synchronize()
         h = sv["pinned"][k]
-        sizes = _sizes(table, h["totals"])
+        sizes = _sizes(table, h["totals"], fmt)
         c = sv["bufs"][k]
         with t.cuda.stream(copy):
             for name, m in sizes.items():
@@ -413,7 +455,7 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         k, sizes, done = copy_q.popleft()
         done.synchronize()
         h = sv["pinned"][k]
-        return _records(table, {name: h[name][:m].numpy() for name, m in sizes.items()})
+        return _records(table, {name: h[name][:m].numpy() for name, m in sizes.items()}, fmt)
 
     up = sv["up"]
 
@@ -458,9 +500,12 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         comp.wait_event(uploaded)
         node_in = st["node"] if narrow else None
         ref_in = None if narrow else st["ref"]
-        if not (table.serve_fused and
-                table.launch_compact(region, sv["descs"][k], sv["scratch"][k], new_tok=st["tok"],
-                                     new_node=node_in, new_ref=ref_in)):
+        fused = table.serve_fused and table.launch_compact(
+            region, sv["descs"][k], sv["scratch"][k], new_tok=st["tok"], new_node=node_in,
+            new_ref=ref_in)
+        if not fused:
+            if fmt & _native.PASTE_CF_ENTRY16:
+                raise _native.PasteError("PASTE_CF_ENTRY16 needs the fused serving kernel")
             table.launch(region, st["tok"], ref_in, node_in)
             check(table.lib.paste_compact_records(ctypes.byref(table.out_desc), table.n,
                                                   ctypes.byref(table.pool_desc),

@@ -65,13 +65,19 @@ def test_serving_partial_tiles(n):
     wl_a, wl_b = (LiveWorkload(dp.sigs, dp.keys, n, seed=5) for _ in range(2))
     seq = LiveSessionTable(dp, n, wl_a.tmpl.nodes, wl_a.max_batch_bytes, policy, EstimateBook())
     pip = LiveSessionTable(dp, n, wl_b.tmpl.nodes, wl_b.max_batch_bytes, policy, EstimateBook())
-    expect = []
+    from test_predict_gpu import _compare
+
+    expect, full = [], []
     for _ in range(18):
         seq.step(wl_a.next_batch())
+        full.append(seq.fetch().session_major())
         r = seq.fetch_compact()
         expect.append([a.copy() for a in (r.hdr, r.pred, r.arg, r.act)])
-    got = [[a.copy() for a in (r.hdr, r.pred, r.arg, r.act)]
+    got = [([a.copy() for a in (r.hdr, r.pred, r.arg, r.act)],
+            r.expand(dp.image.patterns, pip.benefit))
            for r in pip.serve(wl_b.next_batch() for _ in range(18))]
-    for e, g in zip(expect, got):
-        for x, y in zip(e, g):
-            assert np.array_equal(x, y)
+    for e, f, (g, g_exp) in zip(expect, full, got):
+        _compare(g_exp, f)
+        for i, (x, y) in enumerate(zip(e, g)):
+            if i != 1 or pip.sformat == seq.cformat:  # ENTRY16 ships keys, not patterns
+                assert np.array_equal(x, y)

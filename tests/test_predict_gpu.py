@@ -14,6 +14,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
 
 from oracle import bridge  # noqa: E402
 from paper_2603_18897_b200 import admit  # noqa: E402
+from paper_2603_18897_b200._native import PASTE_CF_ENTRY16  # noqa: E402
 from paper_2603_18897_b200.device_ops import DevicePool  # noqa: E402
 from paper_2603_18897_b200.live import LiveSessionTable  # noqa: E402
 from paper_2603_18897_b200.mining import load_pool  # noqa: E402
@@ -211,11 +212,14 @@ def test_compact_records_expand_to_the_full_records(fmt):
 
 
 @pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3", "wide_format",
-                                     "ship_bytes"])
+                                     "ship_bytes", "pred_stream"])
 def test_serve_pipeline_yields_the_step_records(variant):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
-    what the sequential step (K-slot records) + compaction kernel returns."""
+    what the sequential step (K-slot records) returns: expanded records
+    equal the full records, and in the same stream format the streams equal
+    the compaction kernel's.  The serving format ships match-table keys
+    (PASTE_CF_ENTRY16) unless the variant turns it off."""
     from paper_2603_18897_b200.policy import SpeculationPolicy
 
     pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
@@ -235,25 +239,35 @@ def test_serve_pipeline_yields_the_step_records(variant):
                            max_candidates=K)
     pip = LiveSessionTable(dp, n, wl_b.tmpl.nodes, wl_b.max_batch_bytes, policy, book,
                            max_candidates=K)
-    if variant == "wide_format":
-        seq.cformat = pip.cformat = 0
     if variant == "ship_bytes":  # payload bytes uploaded into the arena regions too
         seq = LiveSessionTable(dp, n, wl_a.tmpl.nodes, wl_a.max_batch_bytes, policy, book,
                                max_candidates=K, ship_bytes=True)
         pip = LiveSessionTable(dp, n, wl_b.tmpl.nodes, wl_b.max_batch_bytes, policy, book,
                                max_candidates=K, ship_bytes=True)
+    if variant == "wide_format":
+        seq.cformat = pip.cformat = 0
+        pip.sformat = PASTE_CF_ENTRY16
+    if variant == "pred_stream":
+        pip.sformat = pip.cformat
+    else:
+        assert pip.sformat & PASTE_CF_ENTRY16
     steps = 20
-    expect = []
+    expect, full = [], []
     for _ in range(steps):
         seq.step(wl_a.next_batch())
+        full.append(seq.fetch().session_major())
         r = seq.fetch_compact()
         expect.append(tuple(a.copy() for a in (r.hdr, r.pred, r.arg, r.act)))
-    got = [tuple(a.copy() for a in (r.hdr, r.pred, r.arg, r.act))
-           for r in pip.serve(wl_b.next_batch() for _ in range(steps))]
+    got = []
+    for r in pip.serve(wl_b.next_batch() for _ in range(steps)):
+        got.append((tuple(a.copy() for a in (r.hdr, r.pred, r.arg, r.act)),
+                    r.expand(dp.image.patterns, pip.benefit)))
     assert len(got) == steps
-    for e, g in zip(expect, got):
-        for x, y in zip(e, g):
-            assert np.array_equal(x, y)
+    for e, f, (g, g_exp) in zip(expect, full, got):
+        _compare(g_exp, f)
+        for i, (x, y) in enumerate(zip(e, g)):
+            if i != 1 or pip.sformat == seq.cformat:  # pred stream: keys in ENTRY16
+                assert np.array_equal(x, y)
     if variant == "ship_bytes":  # same arena contents
         assert torch.equal(seq.bytes, pip.bytes) and torch.equal(seq.refs, pip.refs)
 
