@@ -734,85 +734,166 @@ __host__ __device__ inline int stage_stride(int K, int B) {  // bytes per thread
   return (((2 * K + 3) & ~3) + 4 * K * B + ((K + 3) & ~3) + 15) & ~15;
 }
 
-// Resolve, admit and stage session `sess` (after observe + gather);
+// Observe, gather, match, resolve, admit and stage session `sess` (all
+// lanes of the warp call this together; `live` = the lane has a session).
+// Same warp-cooperative scheme as predict_coop: lane per session for the
+// records and the admit, one queued binding per lane for the argument walks;
+// an unresolved binding marks its candidate in the owner's PARTIAL mask and
+// the owner fixes the staged completeness / action levels at the end.
 // c = {predictions, arguments, actions, structural errors}.
-__device__ __forceinline__ void compact_stage(const FastParams& P, int64_t sess, int64_t rbase,
-                                              int64_t rstride, const int32_t* gt, int m,
+__device__ __forceinline__ void compact_stage(const FastParams& P, int64_t sess, bool live,
+                                              int32_t* rows, uint8_t* stage0, int sstride,
                                               const Stage& S, int c[4], uint64_t* memo,
-                                              unsigned long long& wide, uint32_t& key) {
+                                              ResolveQueue& q, unsigned long long& wide,
+                                              uint32_t& key) {
+  const unsigned FULLM = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t warp_first = sess - lane;
+  const int64_t n = P.win.n_sessions;
+  const int K = P.out.max_candidates;
+  const paste_pool_desc& pool = P.pool;
+  int32_t* gt = rows + lane * P.row;
   c[0] = c[1] = c[2] = c[3] = 0;
   key = 0xffffu;
-  if (m == 0 || gt[0] >= P.pool.n_bucket_sigs) return;
-  const int64_t n = P.win.n_sessions;
-  const int32_t* gs = gt + P.G;
-  const int64_t tk = table_key(P, gt, m);
-  key = (uint32_t)tk;
-  const uint8_t* e = static_cast<const uint8_t*>(P.pool.match_table) + tk * mt_stride(P.pool.mt_k);
-  const int2 hdr = __ldg(reinterpret_cast<const int2*>(e));
-  const MTRecord* recs = reinterpret_cast<const MTRecord*>(e + 16);
-  const int K = P.out.max_candidates;
-  const int nm = hdr.x < K ? hdr.x : K;
-  c[0] = nm;
-  c[3] = hdr.y;
-  const paste_pool_desc& pool = P.pool;
-  int na = 0, n_act = 0;
+  int64_t rbase = 0, rstride = 0;
+  int nm = 0;
+  const MTRecord* recs = nullptr;
+  if (live) {
+    const int m = observe_gather(P, sess, gt, rbase, rstride);
+    if (m > 0 && gt[0] < pool.n_bucket_sigs) {
+      const int64_t tk = table_key(P, gt, m);
+      key = (uint32_t)tk;
+      const uint8_t* e = static_cast<const uint8_t*>(pool.match_table) + tk * mt_stride(pool.mt_k);
+      const int2 hdr = __ldg(reinterpret_cast<const int2*>(e));
+      recs = reinterpret_cast<const MTRecord*>(e + 16);
+      nm = hdr.x < K ? hdr.x : K;
+      c[3] = hdr.y;
+    }
+  }
+  q.rbase[lane] = rbase;
+  q.rstride[lane] = rstride;
+  q.part[lane] = 0ull;
+  __syncwarp();
+  const int max_nm = (int)__reduce_max_sync(FULLM, (unsigned)nm);
+  int na = 0, n_act = 0, count = 0;
   uint64_t seen = 0;
-  for (int i = 0; i < nm; ++i) {
-    const int4 r0 = __ldg(reinterpret_cast<const int4*>(recs + i));
-    const int4 r1 = __ldg(reinterpret_cast<const int4*>(recs + i) + 1);
-    const int pid = r0.x, tool = r0.z, n_bind = r0.w & 0xffff, pflags = r0.w >> 16;
-    const uint32_t src = (uint32_t)r0.y;
-    const int bind_off = r1.x;
-    const double p = __hiloint2double(r1.w, r1.z);
-    int comp = PASTE_C_TOOL_ONLY;
-    if (pflags & PASTE_PF_HAS_MAPPING) {
-      comp = PASTE_C_FULL;
-      for (int b = 0; b < n_bind; ++b) {
-        const paste_binding bd = pool.bindings[bind_off + b];
-        const int age = (src >> (4 * b)) & 15;
-        const int32_t ev = P.win.evt[rbase + gs[age] * rstride];
-        const int64_t r = resolve_fast(P.win, pool.steps, bd, bind_off + b, ev, age, gt, memo);
+  const int arg_off = (2 * K + 3) & ~3;  // Stage.arg within a thread's staging
+  for (int i = 0; i < max_nm; ++i) {
+    int nb = 0, bind_off = 0;
+    uint32_t src = 0;
+    if (i < nm) {
+      const int4 r0 = __ldg(reinterpret_cast<const int4*>(recs + i));
+      const int4 r1 = __ldg(reinterpret_cast<const int4*>(recs + i) + 1);
+      const int pid = r0.x, tool = r0.z, pflags = r0.w >> 16;
+      const double p = __hiloint2double(r1.w, r1.z);
+      const bool mapped = (pflags & PASTE_PF_HAS_MAPPING) != 0;
+      const int comp = mapped ? PASTE_C_FULL : PASTE_C_TOOL_ONLY;  // B may downgrade
+      S.pred[i] = (uint16_t)(pid | (comp << 14));
+      if (mapped) {
+        nb = r0.w & 0xffff;
+        src = (uint32_t)r0.y;
+        bind_off = r1.x;
+      }
+      // admit (policy.py:207-236): the streamed first-candidate rule for
+      // tools with benefit >= 0 (or NaN), exact arbitration otherwise
+      if (allowed_tool(P.adm, tool)) {
+        const int implied = comp == PASTE_C_FULL ? 3 : 1;
+        const int cap = __ldg(P.adm.max_level + tool);
+        const uint8_t rec = (uint8_t)(i | ((cap < implied ? cap : implied) << 5));
+        const double bene = __ldg(P.adm.benefit + tool);
+        if (!(bene < 0.0) && tool < 64) {
+          if (!((seen >> tool) & 1ull)) {
+            seen |= 1ull << tool;
+            S.act[n_act++] = rec;
+          }
+        } else {
+          int j = 0;
+          for (; j < n_act; ++j)
+            if (__ldg(&recs[S.act[j] & 31].tool) == tool) break;
+          if (j == n_act) {
+            S.act[n_act++] = rec;
+          } else {
+            const int ip = S.act[j] & 31;
+            const double ipp = __ldg(&recs[ip].p);
+            const double util = __dmul_rn(p, bene), iu = __dmul_rn(ipp, bene);
+            if ((util != iu) ? (util > iu) : (p > ipp)) S.act[j] = rec;
+          }
+        }
+      }
+    }
+    int pos, total;
+    const unsigned any = __ballot_sync(FULLM, nb > 0);
+    if (__all_sync(FULLM, nb <= 1)) {
+      pos = count + __popc(any & lt);
+      total = __popc(any);
+    } else {
+      int incl = nb;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULLM, incl, o);
+        if (lane >= o) incl += t;
+      }
+      total = __shfl_sync(FULLM, incl, 31);
+      pos = count + incl - nb;
+    }
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+      q.bind[pos + b] = (uint32_t)(bind_off + b);
+      q.meta[pos + b] = (uint32_t)lane | ((uint32_t)i << 5) | (((src >> (4 * b)) & 15u) << 14) |
+                        ((uint32_t)(na + b) << 18);
+    }
+    na += nb;
+    count += total;
+    __syncwarp();
+    const bool last = i + 1 == max_nm;
+    while (count >= 32 || (last && count > 0)) {
+      const int take = count < 32 ? count : 32;
+      if (lane < take) {
+        const int t = count - take + lane;
+        const uint32_t meta = q.meta[t];
+        const int owner = meta & 31, ri = (meta >> 5) & 63, age = (meta >> 14) & 15;
+        const int apos = (meta >> 18) & 63;
+        const int bind = (int)q.bind[t];
+        const int32_t* ogt = rows + owner * P.row;
+        const int32_t ev = P.win.evt[q.rbase[owner] + ogt[P.G + age] * q.rstride[owner]];
+        const paste_binding bd = pool.bindings[bind];
+        const int64_t r = resolve_fast(P.win, pool.steps, bd, bind, ev, age, ogt, memo);
         uint32_t w = 0xffffffffu;
         if (r < 0) {
-          comp = PASTE_C_PARTIAL;
+          atomicOr(q.part + owner, 1ull << ri);
         } else {
+          const int64_t osess = warp_first + owner;
           const int64_t node = r & 0xffffffffll;
           const int64_t region =
               n < (1ll << 31) ? (int64_t)((uint32_t)ev / (uint32_t)n) : (int64_t)ev / n;
-          if ((int64_t)ev - region * n == sess && region < 31 && node < (1ll << 27))
+          if ((int64_t)ev - region * n == osess && region < 31 && node < (1ll << 27))
             w = ((uint32_t)region << 27) | (uint32_t)node;
           else
             ++wide;
         }
-        S.arg[na++] = w;
+        reinterpret_cast<uint32_t*>(stage0 + (size_t)(threadIdx.x - lane + owner) * sstride +
+                                    arg_off)[apos] = w;
+      }
+      count -= take;
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+  if (!live) return;
+  const unsigned long long pm = q.part[lane];
+  if (pm) {  // PARTIAL: completeness code and level min(cap, WARM_ONLY)
+    for (int i = 0; i < nm; ++i)
+      if ((pm >> i) & 1ull) S.pred[i] = (uint16_t)((S.pred[i] & 0x3fff) | (PASTE_C_PARTIAL << 14));
+    for (int j = 0; j < n_act; ++j) {
+      const int ip = S.act[j] & 31;
+      if ((pm >> ip) & 1ull) {
+        const int cap = __ldg(P.adm.max_level + __ldg(&recs[ip].tool));
+        S.act[j] = (uint8_t)(ip | ((cap < 1 ? cap : 1) << 5));
       }
     }
-    S.pred[i] = (uint16_t)(pid | (comp << 14));
-    // admit (policy.py:207-236): the streamed first-candidate rule for tools
-    // with benefit >= 0 (or NaN), exact arbitration otherwise
-    if (!allowed_tool(P.adm, tool)) continue;
-    const int implied = comp == PASTE_C_FULL ? 3 : 1;
-    const int cap = __ldg(P.adm.max_level + tool);
-    const uint8_t rec = (uint8_t)(i | ((cap < implied ? cap : implied) << 5));
-    const double bene = __ldg(P.adm.benefit + tool);
-    if (!(bene < 0.0) && tool < 64) {
-      if ((seen >> tool) & 1ull) continue;
-      seen |= 1ull << tool;
-      S.act[n_act++] = rec;
-      continue;
-    }
-    int j = 0;
-    for (; j < n_act; ++j)
-      if (__ldg(&recs[S.act[j] & 31].tool) == tool) break;
-    if (j == n_act) {
-      S.act[n_act++] = rec;
-      continue;
-    }
-    const int ip = S.act[j] & 31;
-    const double ipp = __ldg(&recs[ip].p);
-    const double util = __dmul_rn(p, bene), iu = __dmul_rn(ipp, bene);
-    if ((util != iu) ? (util > iu) : (p > ipp)) S.act[j] = rec;
   }
+  c[0] = nm;
   c[1] = na;
   c[2] = n_act;
 }
@@ -866,6 +947,9 @@ __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactPar
                  st + ((2 * K + 3) & ~3) + 4 * K * B};
   const int64_t n = P.win.n_sessions;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* stage0 = st - (size_t)threadIdx.x * stage_stride(K, B);
+  ResolveQueue* qs = reinterpret_cast<ResolveQueue*>(stage0 + (size_t)FT * stage_stride(K, B));
+  int32_t* rows = reinterpret_cast<int32_t*>(s_mem + MEMO) + warp * 32 * P.row;
   unsigned long long wide = 0;
   for (;;) {
     __syncthreads();
@@ -878,11 +962,8 @@ __global__ void __launch_bounds__(FT, 8) predict_compact_kernel(const CompactPar
     // ---- the whole step for this session, records staged in shared memory --
     int c[4] = {0, 0, 0, 0};
     uint32_t key = 0xffffu;
-    if (sess < n) {
-      int64_t rbase, rstride;
-      const int m = observe_gather(P, sess, gt, rbase, rstride);
-      compact_stage(P, sess, rbase, rstride, gt, m, SG, c, memo, wide, key);
-    }
+    compact_stage(P, sess, sess < n, rows, stage0, stage_stride(K, B), SG, c, memo, qs[warp],
+                  wide, key);
     // ---- block-wide exclusive scan of the 4 counters ------------------------
     uint64_t inc[4];
 #pragma unroll
@@ -998,7 +1079,7 @@ bool predict_compact_dispatch(const paste_pool_desc* pool, const paste_windows* 
                   (win->n_sessions + FT - 1) / FT};
   const size_t smem = sizeof(uint64_t) * MEMO +
                       (((size_t)sizeof(int32_t) * FT * Q.F.row + 15) & ~(size_t)15) +
-                      (size_t)FT * stage_stride(K, B);
+                      (size_t)FT * stage_stride(K, B) + sizeof(ResolveQueue) * (FT / 32);
   static int sms = 0, occ = 0, occ_smem = 0;
   if (sms == 0) {
     int dev = 0;
