@@ -309,7 +309,10 @@ def run_ours(args):
         "actions_per_s": world * acts / dev_s,
         "e2e": {"value": world * n * S_ / e2e_s, "unit": UNIT,
                 "h2d_bytes_per_step": h2d // S_, "d2h_bytes_per_step": d2h // S_,
-                "ms_per_step": 1e3 * e2e_s / S_},
+                "ms_per_step": 1e3 * e2e_s / S_,
+                "records": "narrow CSR streams, format bits %d (%s)" % (
+                    table.sformat, "per-session match-table key + refs + actions"
+                    if table.sformat & 8 else "per-prediction codes + refs + actions")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": committed_traffic(),
                      "kernel": "predict_fast_kernel", "algorithmic_bytes_per_launch": alg // S_,
