@@ -446,7 +446,7 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         with t.cuda.stream(copy):
             for name, m in sizes.items():
                 h[name][:m].copy_(c[name][:m], non_blocking=True)
-            done = t.cuda.Event()
+            done = t.cuda.Event(enable_timing=True)
             done.record(copy)
         sv["free"][k] = done
         copy_q.append((k, sizes, done))
@@ -455,7 +455,9 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         k, sizes, done = copy_q.popleft()
         done.synchronize()
         h = sv["pinned"][k]
-        return _records(table, {name: h[name][:m].numpy() for name, m in sizes.items()}, fmt)
+        rec = _records(table, {name: h[name][:m].numpy() for name, m in sizes.items()}, fmt)
+        rec.downloaded = done  # device event: this step's records are on the host
+        return rec
 
     up = sv["up"]
 
