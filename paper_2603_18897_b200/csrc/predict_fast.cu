@@ -584,7 +584,9 @@ __device__ __forceinline__ void predict_coop(const FastParams& P, int64_t sess, 
   __syncwarp();
   const int max_nm = (int)__reduce_max_sync(FULLM, (unsigned)nm);
   int count = 0;
-  for (int i = 0; i < max_nm; ++i) {
+  int32_t* pp = P.out.pred_pat + X.obase;   // rank i's record slot, advanced per rank
+  uint8_t* pc = P.out.pred_comp + X.obase;
+  for (int i = 0; i < max_nm; ++i, pp += X.ostride, pc += X.ostride) {
     // ---- A: rank i of every session: records, provisional completeness
     // (FULL when mapped; B downgrades), admit, mapped bindings queued --------
     int nb = 0, bind_off = 0;
@@ -594,9 +596,8 @@ __device__ __forceinline__ void predict_coop(const FastParams& P, int64_t sess, 
       const int4 r1 = __ldg(reinterpret_cast<const int4*>(recs + i) + 1);
       const bool mapped = ((r0.w >> 16) & PASTE_PF_HAS_MAPPING) != 0;
       const int comp = mapped ? PASTE_C_FULL : PASTE_C_TOOL_ONLY;
-      const int64_t o = X.o(i);
-      P.out.pred_pat[o] = r0.x;
-      P.out.pred_comp[o] = (uint8_t)comp;
+      *pp = r0.x;
+      *pc = (uint8_t)comp;
       if (admit) admit_one(P, X, i, r0.z, comp, __hiloint2double(r1.w, r1.z), n_act, seen);
       if (mapped) {
         nb = r0.w & 0xffff;
@@ -621,6 +622,7 @@ __device__ __forceinline__ void predict_coop(const FastParams& P, int64_t sess, 
       total = __shfl_sync(FULLM, incl, 31);
       pos = count + incl - nb;
     }
+#pragma unroll 1
     for (int b = 0; b < nb; ++b) {
       q.bind[pos + b] = (uint32_t)(bind_off + b);
       q.meta[pos + b] = (uint32_t)lane | ((uint32_t)i << 5) | ((uint32_t)b << 11) |
