@@ -985,6 +985,7 @@ static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint
   columnar_count_kernel<K, OUT><<<(unsigned)grid, CT, smem, stream>>>(c, g, hist, c.tokens_out,
                                                                       stage, ctr, hot_lo, hot_n,
                                                                       lat_t);
+  count_launch();
   if (OUT == 2) {
     // with the lattice in shared memory the cold REDs are spread enough to go
     // straight into the histogram; otherwise into STG_REPS replicas + fold
@@ -1025,8 +1026,11 @@ static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint
                            reps, (int64_t)g.n_bins, n_reps, dlo, dn, lat_t, lat_n,
                            (uint32_t)g.base, (int)K) != cudaSuccess)
       return -2;
-    if (n_reps > 1)
+    count_launch();
+    if (n_reps > 1) {
       fold_replicas_kernel<<<(unsigned)(sms * 4), 256, 0, stream>>>(reps, g.n_bins, n_reps, hist);
+      count_launch();
+    }
   }
   return 0;
 }
@@ -1069,7 +1073,6 @@ static int ingest_count_impl(const paste_columnar_desc* c, const paste_mine_desc
     set_error("k=%d outside the columnar kernel's range", d->k);
     return PASTE_ERR_UNSUPPORTED;
   }
-  count_launch(out == 2 ? 3 : 1);
   PASTE_CUDA_CHECK(cudaGetLastError());
   return PASTE_OK;
 }
