@@ -639,6 +639,12 @@ int paste_replay_score(const paste_pool_desc* pool, const paste_replay_desc* d,
 /* Number of kernel launches the last paste_* call on this thread issued.   */
 int paste_last_launch_count(void);
 
+/* n async copies (bytes[i] <= 0 skipped) on `stream`, in order.  Used by the
+ * serving loop to issue a step's uploads / sized downloads in one call.    */
+enum { PASTE_COPY_H2D = 1, PASTE_COPY_D2H = 2, PASTE_COPY_D2D = 3 };
+int paste_memcpy_batch(int32_t n, void* const* dst, const void* const* src,
+                       const int64_t* bytes, int32_t kind, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

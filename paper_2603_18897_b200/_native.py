@@ -115,6 +115,7 @@ class CompactDesc(ctypes.Structure):
 
 
 PASTE_CF_HDR8, PASTE_CF_PRED8, PASTE_CF_ARG16, PASTE_CF_ENTRY16 = 1, 2, 4, 8
+PASTE_COPY_H2D, PASTE_COPY_D2H, PASTE_COPY_D2D = 1, 2, 3
 
 
 class HoldsDesc(ctypes.Structure):
@@ -165,6 +166,7 @@ EXPORTS = {
     "paste_last_error": (c_char_p, []),
     "paste_abi_version": (c_int, []),
     "paste_last_launch_count": (c_int, []),
+    "paste_memcpy_batch": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "paste_predict_batch": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc),
                                     POINTER(AdmitDesc), POINTER(PredictOut), c_void_p]),
     "paste_admit_lists": (c_int, [POINTER(AdmitDesc), POINTER(AdmitListsDesc), c_void_p]),

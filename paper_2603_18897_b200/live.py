@@ -399,14 +399,62 @@ def fetch_compact(table: "LiveSessionTable", pinned: dict | None = None) -> Comp
     return _records(table, {k: pinned[k][:m].numpy() for k, m in sizes.items()})
 
 
+_STREAMS = ("hdr", "pred", "arg", "act")
+
+
+def _serve_state(table, depth: int, fmt: int) -> dict:
+    """Buffer sets, pinned mirrors, numpy views, copy lists and reusable
+    events of the serving loop (built once per (depth, format))."""
+    t = table.torch
+    bufs = [_compact_buffers(table, fmt) for _ in range(depth)]
+    pinned = [{k: t.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in c.items()}
+              for c in bufs]
+    entry = bool(fmt & _native.PASTE_CF_ENTRY16)
+    vdt = {"hdr": np.uint8 if fmt & _native.PASTE_CF_HDR8 else np.uint16,
+           "pred": np.uint8 if fmt & _native.PASTE_CF_PRED8 and not entry else np.uint16,
+           "arg": np.uint16 if fmt & _native.PASTE_CF_ARG16 else np.uint32, "act": np.uint8}
+    sets = []
+    for c, h in zip(bufs, pinned):
+        sets.append({
+            "views": {k: h[k].numpy().view(vdt[k]) for k in _STREAMS},
+            "totals": h["totals"].numpy(),
+            "dst": (ctypes.c_void_p * 4)(*[h[k].data_ptr() for k in _STREAMS]),
+            "src": (ctypes.c_void_p * 4)(*[c[k].data_ptr() for k in _STREAMS]),
+            "esize": [c[k].element_size() for k in _STREAMS],
+            "tot_dst": (ctypes.c_void_p * 1)(h["totals"].data_ptr()),
+            "tot_src": (ctypes.c_void_p * 1)(c["totals"].data_ptr()),
+            "tot_bytes": (ctypes.c_int64 * 1)(5 * 8),
+            "bytes": (ctypes.c_int64 * 4)()})
+    return {
+        "fmt": fmt, "bufs": bufs, "descs": [_compact_desc(c, fmt) for c in bufs],
+        "pinned": pinned, "sets": sets,
+        "scratch": [t.empty(max(table.lib.paste_compact_scratch_bytes(table.n),
+                                table.lib.paste_predict_compact_scratch_bytes(table.n)),
+                            dtype=t.uint8, device="cuda") for _ in range(depth)],
+        "copy": t.cuda.Stream(), "tot": t.cuda.Stream(), "up": t.cuda.Stream(),
+        "free": [None] * depth, "in_free": [None] * depth,
+        "ev_ready": [t.cuda.Event() for _ in range(depth)],
+        "ev_tot": [t.cuda.Event() for _ in range(depth)],
+        "ev_up": [t.cuda.Event() for _ in range(depth)],
+        "wins": {},
+        "in": [{"tok": t.zeros(table.n, dtype=t.int32, device="cuda"),
+                "node": t.zeros(table.n, dtype=t.int32, device="cuda"),
+                "ref": t.zeros(2 * table.n, dtype=t.int64, device="cuda")}
+               for _ in range(depth)]}
+
+
 def serve(table: "LiveSessionTable", batches, depth: int = 4):
     """Pipelined live steps (the serving loop).  Step i's inputs upload on
     an upload stream into their own staging set while step i-1's fused
     predict + compaction kernel runs; the kernel and the totals read run on
     the compute stream; step i-1's sized record download is queued on a copy
     stream while step i-2's records are handed out -- so the two copy
-    engines and the SMs overlap and never wait on the host.  Yields each
-    step's CompactRecords in order; a yielded record's arrays are
+    engines and the SMs overlap and never wait on the host.  The host side
+    is kept thin (the loop is host-bound otherwise): each step's copies go
+    out as one ``paste_memcpy_batch`` call per direction, window descriptors
+    are cached per (buffer set, arena region) and events are reused.  Yields
+    each step's CompactRecords in order (``records.downloaded`` is the
+    device event of its download); a yielded record's arrays are
     pinned-buffer views, valid until the generator has advanced ``depth - 1``
     more steps."""
     from collections import deque
@@ -414,78 +462,94 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
     if depth < 3:
         raise ValueError("serve() needs depth >= 3 buffer sets")
     t = table.torch
+    lib = table.lib
     fmt = table.sformat if table.serve_fused else table.cformat
     if (getattr(table, "_serve", None) is None or len(table._serve["bufs"]) != depth
             or table._serve["fmt"] != fmt):
-        bufs = [_compact_buffers(table, fmt) for _ in range(depth)]
-        table._serve = {
-            "fmt": fmt, "bufs": bufs, "descs": [_compact_desc(c, fmt) for c in bufs],
-            "pinned": [{k: t.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in c.items()}
-                       for c in bufs],
-            "scratch": [t.empty(max(table.lib.paste_compact_scratch_bytes(table.n),
-                                    table.lib.paste_predict_compact_scratch_bytes(table.n)),
-                                dtype=t.uint8, device="cuda") for _ in range(depth)],
-            "copy": t.cuda.Stream(), "tot": t.cuda.Stream(), "up": t.cuda.Stream(),
-            "free": [None] * depth, "in_free": [None] * depth,
-            "in": [{"tok": t.zeros(table.n, dtype=t.int32, device="cuda"),
-                    "node": t.zeros(table.n, dtype=t.int32, device="cuda"),
-                    "ref": t.zeros(2 * table.n, dtype=t.int64, device="cuda")}
-                   for _ in range(depth)]}
+        table._serve = _serve_state(table, depth, fmt)
     sv = table._serve
-    # sized downloads on one copy stream, the small totals reads on another:
-    # step i's totals must not queue behind step i-1's downloads (nor the
-    # reverse), or the downloads would wait for step i's compute
-    comp, copy, tot = t.cuda.current_stream(), sv["copy"], sv["tot"]
+    comp, copy, tot, up = t.cuda.current_stream(), sv["copy"], sv["tot"], sv["up"]
+    comp_h, copy_h, tot_h, up_h = (s.cuda_stream for s in (comp, copy, tot, up))
+    entries = table.entries() if fmt & _native.PASTE_CF_ENTRY16 else None
+    n = table.n
     tot_q, copy_q = deque(), deque()
+    H2D, D2H = _native.PASTE_COPY_H2D, _native.PASTE_COPY_D2H
 
-    def download(k, tot_ev):
-        tot_ev.synchronize()
-        h = sv["pinned"][k]
-        sizes = _sizes(table, h["totals"], fmt)
-        c = sv["bufs"][k]
-        with t.cuda.stream(copy):
-            for name, m in sizes.items():
-                h[name][:m].copy_(c[name][:m], non_blocking=True)
-            done = t.cuda.Event(enable_timing=True)
-            done.record(copy)
+    def download(k):
+        sv["ev_tot"][k].synchronize()
+        st = sv["sets"][k]
+        P, A, Q, wide, _err = (int(x) for x in st["totals"])
+        if wide:
+            raise _native.PasteError(f"{wide} argument refs outside the live table's event "
+                                     "form: use fetch()")
+        sizes = (n, n if fmt & _native.PASTE_CF_ENTRY16 else P, A, Q)
+        nb = st["bytes"]
+        for j in range(4):
+            nb[j] = sizes[j] * st["esize"][j]
+        check(lib.paste_memcpy_batch(4, st["dst"], st["src"], nb, D2H, copy_h), lib)
+        done = t.cuda.Event(enable_timing=True)
+        done.record(copy)
         sv["free"][k] = done
         copy_q.append((k, sizes, done))
 
     def hand_out():
         k, sizes, done = copy_q.popleft()
         done.synchronize()
-        h = sv["pinned"][k]
-        rec = _records(table, {name: h[name][:m].numpy() for name, m in sizes.items()}, fmt)
+        v = sv["sets"][k]["views"]
+        rec = CompactRecords(table.K, table.B, v["hdr"][:sizes[0]], v["pred"][:sizes[1]],
+                             v["arg"][:sizes[2]], v["act"][:sizes[3]], fmt, entries)
         rec.downloaded = done  # device event: this step's records are on the host
         return rec
-
-    up = sv["up"]
 
     def upload(i, b):
         """Stage step i's inputs into set i % depth on the upload stream, once
         the kernel that last read that set is done; returns the event."""
         k = i % depth
         region = (steps0 + i) % table.regions  # the arena region step i will use
-        with t.cuda.stream(up):
-            if sv["in_free"][k] is not None:
-                up.wait_event(sv["in_free"][k])
-            st = sv["in"][k]
-            narrow = b.node is not None and not table.ship_bytes
-            tok = b.tok if isinstance(b.tok, t.Tensor) else t.from_numpy(b.tok)
-            st["tok"].copy_(tok.reshape(-1), non_blocking=True)
-            if narrow:
-                node = b.node if isinstance(b.node, t.Tensor) else t.from_numpy(b.node)
-                st["node"].copy_(node.reshape(-1), non_blocking=True)
-            else:
-                ref = b.ref if isinstance(b.ref, t.Tensor) else t.from_numpy(b.ref)
-                st["ref"].copy_(ref.reshape(-1), non_blocking=True)
-            if table.ship_bytes:
+        if sv["in_free"][k] is not None:
+            up.wait_event(sv["in_free"][k])
+        st = sv["in"][k]
+        narrow = b.node is not None and not table.ship_bytes
+        wire = [(st["tok"], b.tok), (st["node"], b.node) if narrow else (st["ref"], b.ref)]
+        if all(isinstance(x, t.Tensor) and not x.is_cuda and x.is_pinned() for _, x in wire):
+            nw = len(wire)
+            check(lib.paste_memcpy_batch(
+                nw, (ctypes.c_void_p * nw)(*[d.data_ptr() for d, _ in wire]),
+                (ctypes.c_void_p * nw)(*[x.data_ptr() for _, x in wire]),
+                (ctypes.c_int64 * nw)(*[x.numel() * x.element_size() for _, x in wire]),
+                H2D, up_h), lib)
+        else:
+            with t.cuda.stream(up):
+                for d, x in wire:
+                    x = x if isinstance(x, t.Tensor) else t.from_numpy(np.ascontiguousarray(x))
+                    d.copy_(x.reshape(-1), non_blocking=True)
+        if table.ship_bytes:
+            with t.cuda.stream(up):
                 data = b.data if isinstance(b.data, t.Tensor) else t.from_numpy(b.data)
                 table.region_bytes(region)[:data.numel()].copy_(data.reshape(-1),
                                                                 non_blocking=True)
-            ev = t.cuda.Event()
-            ev.record(up)
+        ev = sv["ev_up"][k]
+        ev.record(up)
         return ev, narrow
+
+    def launch_fused(k, region, st, narrow) -> bool:
+        key = (k, region, narrow)
+        win = sv["wins"].get(key)
+        if win is None:
+            win = WindowsDesc(n, table.W, 1, ptr(table.tok), ptr(table.evt), ptr(table.count),
+                              ptr(table.nodes), ptr(table.bytes), ptr(table.refs), ptr(st["tok"]),
+                              None if narrow else ptr(st["ref"]), region * n,
+                              region * table.max_batch_bytes, 0,
+                              ptr(st["node"]) if narrow else None)
+            sv["wins"][key] = win
+        rc = lib.paste_predict_compact(ctypes.byref(table.pool_desc), ctypes.byref(win),
+                                       ctypes.byref(table.adm), table.K, table.B,
+                                       ctypes.byref(sv["descs"][k]), ptr(sv["scratch"][k]),
+                                       comp_h)
+        if rc == _native.PASTE_ERR_UNSUPPORTED:
+            return False
+        check(rc, lib)
+        return True
 
     it = iter(batches)
     steps0 = table.steps
@@ -502,38 +566,35 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         comp.wait_event(uploaded)
         node_in = st["node"] if narrow else None
         ref_in = None if narrow else st["ref"]
-        fused = table.serve_fused and table.launch_compact(
-            region, sv["descs"][k], sv["scratch"][k], new_tok=st["tok"], new_node=node_in,
-            new_ref=ref_in)
+        fused = table.serve_fused and launch_fused(k, region, st, narrow)
         if not fused:
             if fmt & _native.PASTE_CF_ENTRY16:
                 raise _native.PasteError("PASTE_CF_ENTRY16 needs the fused serving kernel")
             table.launch(region, st["tok"], ref_in, node_in)
-            check(table.lib.paste_compact_records(ctypes.byref(table.out_desc), table.n,
-                                                  ctypes.byref(table.pool_desc),
-                                                  ctypes.byref(sv["descs"][k]),
-                                                  ptr(sv["scratch"][k]), stream_handle()),
-                  table.lib)
+            check(lib.paste_compact_records(ctypes.byref(table.out_desc), n,
+                                            ctypes.byref(table.pool_desc),
+                                            ctypes.byref(sv["descs"][k]),
+                                            ptr(sv["scratch"][k]), comp_h), lib)
         table.steps += 1
-        ready = t.cuda.Event()
+        ready = sv["ev_ready"][k]
         ready.record(comp)
         sv["in_free"][k] = ready
-        with t.cuda.stream(tot):
-            tot.wait_event(ready)
-            sv["pinned"][k]["totals"].copy_(sv["bufs"][k]["totals"], non_blocking=True)
-            tot_ev = t.cuda.Event()
-            tot_ev.record(tot)
-        tot_q.append((k, tot_ev))
+        tot.wait_event(ready)
+        s_k = sv["sets"][k]
+        check(lib.paste_memcpy_batch(1, s_k["tot_dst"], s_k["tot_src"], s_k["tot_bytes"], D2H,
+                                     tot_h), lib)
+        sv["ev_tot"][k].record(tot)
+        tot_q.append(k)
         # the next step's upload goes out now, before the host waits on anything
         nxt = next(it, None)
         staged = upload(i + 1, nxt) if nxt is not None else None
         i += 1
         if len(tot_q) > 1:
-            download(*tot_q.popleft())
+            download(tot_q.popleft())
         if len(copy_q) > 1:
             yield hand_out()
     while tot_q:
-        download(*tot_q.popleft())
+        download(tot_q.popleft())
     while copy_q:
         yield hand_out()
 
