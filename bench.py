@@ -117,28 +117,42 @@ class ClockSampler:
         self.proc = None
         self.path = tempfile.mktemp(suffix=".csv")
 
+    def _rows(self):
+        try:
+            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines()]
+        except OSError:
+            rows = []
+        return [r for r in rows if len(r) >= 7 and r[0].strip() == str(self.gpu)]
+
     def __enter__(self):
+        self.n0 = 0
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+                 "-lms", "50"], stdout=self.fh, stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return self
+        # the sampler must be live before the timed region starts
+        t0 = time.perf_counter()
+        while not self._rows() and time.perf_counter() - t0 < 5.0:
+            time.sleep(0.01)
+        self.n0 = len(self._rows())
         return self
 
     def __exit__(self, *exc):
         if self.proc is not None:
+            # at least one sample from the region (or its last 50 ms)
+            t0 = time.perf_counter()
+            while len(self._rows()) <= self.n0 and time.perf_counter() - t0 < 1.0:
+                time.sleep(0.005)
             self.proc.terminate()
             self.proc.wait()
             self.fh.close()
 
     def summary(self):
-        try:
-            rows = [r.split(", ") for r in open(self.path).read().strip().splitlines()]
-        except OSError:
-            rows = []
-        rows = [r for r in rows if len(r) >= 7 and r[0].strip() == str(self.gpu)]
+        rows = self._rows()[self.n0:]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[1]) for r in rows]
