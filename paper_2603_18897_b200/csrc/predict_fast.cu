@@ -598,7 +598,31 @@ __device__ __forceinline__ void predict_coop(const FastParams& P, int64_t sess, 
       const int comp = mapped ? PASTE_C_FULL : PASTE_C_TOOL_ONLY;
       *pp = r0.x;
       *pc = (uint8_t)comp;
-      if (admit) admit_one(P, X, i, r0.z, comp, __hiloint2double(r1.w, r1.z), n_act, seen);
+      if (admit) {
+        const int tool = r0.z;
+        const double p = __hiloint2double(r1.w, r1.z);
+        if (tool < 64 && tool < P.adm.n_tools) {
+          // streamed first-candidate rule inline (admit_one's fast path), with
+          // the action slot advanced by pointer
+          if (__ldg(P.adm.allow + tool) && !((seen >> tool) & 1ull)) {
+            const double bene = __ldg(P.adm.benefit + tool);
+            if (!(bene < 0.0)) {
+              seen |= 1ull << tool;
+              const int implied = comp == PASTE_C_FULL ? 3 : 1;
+              const int cap = __ldg(P.adm.max_level + tool);
+              const int64_t o = X.obase + (int64_t)n_act * X.ostride;
+              P.out.act_pred[o] = (int16_t)i;
+              P.out.act_level[o] = (uint8_t)(cap < implied ? cap : implied);
+              P.out.act_util[o] = __dmul_rn(p, bene);
+              ++n_act;
+            } else {
+              admit_one(P, X, i, tool, comp, p, n_act, seen);
+            }
+          }
+        } else {
+          admit_one(P, X, i, tool, comp, p, n_act, seen);
+        }
+      }
       if (mapped) {
         nb = r0.w & 0xffff;
         src = (uint32_t)r0.y;
