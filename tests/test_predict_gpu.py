@@ -212,7 +212,7 @@ def test_compact_records_expand_to_the_full_records(fmt):
 
 
 @pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3", "wide_format",
-                                     "ship_bytes", "pred_stream"])
+                                     "ship_bytes", "pred_stream", "pinned_inputs"])
 def test_serve_pipeline_yields_the_step_records(variant):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
@@ -258,8 +258,17 @@ def test_serve_pipeline_yields_the_step_records(variant):
         full.append(seq.fetch().session_major())
         r = seq.fetch_compact()
         expect.append(tuple(a.copy() for a in (r.hdr, r.pred, r.arg, r.act)))
+    def feed():
+        for _ in range(steps):
+            b = wl_b.next_batch()
+            if variant == "pinned_inputs":  # the batched-copy upload path
+                b.tok = torch.from_numpy(b.tok).pin_memory()
+                b.node = torch.from_numpy(b.node).pin_memory()
+                b.ref = torch.from_numpy(np.ascontiguousarray(b.ref)).pin_memory()
+            yield b
+
     got = []
-    for r in pip.serve(wl_b.next_batch() for _ in range(steps)):
+    for r in pip.serve(feed()):
         got.append((tuple(a.copy() for a in (r.hdr, r.pred, r.arg, r.act)),
                     r.expand(dp.image.patterns, pip.benefit)))
     assert len(got) == steps
