@@ -62,6 +62,8 @@ def parse_args():
     ap.add_argument("--max-candidates", type=int, default=8)
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the full-size oracle comparisons (N=1 only)")
     ap.add_argument("--mine-events", type=int, default=100_000_000,
                     help="C4 mining corpus size (0 = skip the mining measurement)")
     ap.add_argument("--long-sessions", type=int, default=100_000,
@@ -340,20 +342,81 @@ def run_ours(args):
     out["clocks"] = clk
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args, budget_s=args.cpu_budget_s)
+    del table, staged, host_batches
+    torch.cuda.empty_cache()
+    parity = {}
+    if rank == 0 and world == 1 and not args.no_parity:
+        parity["c3"] = live_full_parity(args, dp, policy, book)
     if args.mine_events > 0:
-        del table, staged, host_batches
-        torch.cuda.empty_cache()
         out["mining"] = run_mining(args, world, rank, local)
+        if "parity" in out["mining"]:
+            parity["c4"] = {"anchored": out["mining"]["parity"],
+                            "suffix": out["mining"]["suffix"].get("parity")}
     if args.long_sessions > 0:
         torch.cuda.empty_cache()
         out["long_outputs"] = run_long_outputs(args, world, rank, local)
     if args.replay_sessions > 0:
         torch.cuda.empty_cache()
         out["replay"] = run_replay(args, world, rank, local)
+    if parity:
+        out["parity"] = parity_summary(parity)
+    out["summary"] = summary(out)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out))
+
+
+def live_full_parity(args, dp, policy, book):
+    """The benchmarked C3 configuration at full size: a fresh 1M-session
+    table stepped W+2 times (every window full, several persistent-CTA
+    sweeps per launch), each step's K-slot records (predict_fast_kernel) and
+    the serving loop's expanded narrow streams (predict_compact_kernel)
+    compared record for record with the oracle over mirrored host rings."""
+    from oracle.parity import live_parity
+
+    t0 = time.perf_counter()
+    r = live_parity(dp, policy, book, args.sessions, 16 + 2, K=args.max_candidates, seed=99)
+    r["check_s"] = round(time.perf_counter() - t0, 1)
+    return r
+
+
+def parity_summary(p):
+    out = {}
+    if "c3" in p:
+        c = p["c3"]
+        out.update(c3_sessions=c["sessions"], c3_steps=c["steps"],
+                   c3_predictions=c["predictions"], c3_kslot_ok=c["kslot_ok"],
+                   c3_serve_ok=c["serve_ok"], c3_mismatch=c["mismatch"])
+    if "c4" in p:
+        a, s = p["c4"]["anchored"], p["c4"]["suffix"] or {}
+        out.update(c4_events=a["events"], c4_anchored_ok=a["ok"], c4_suffix_ok=s.get("ok"),
+                   c4_patterns=[a.get("patterns"), s.get("patterns")])
+    out["ok"] = all(v for k, v in out.items() if k.endswith("_ok"))
+    return out
+
+
+def summary(out):
+    """The headline numbers again, last on the line (the driver keeps the
+    tail of stdout)."""
+    def obj(o, key="value"):
+        if not o:
+            return None
+        r = {"value": o.get(key), "unit": o.get("unit"),
+             "frac": (o.get("roofline") or {}).get("frac"),
+             "e2e": (o.get("e2e") or {}).get("value")}
+        if o.get("cpu_baseline"):
+            r["cpu_baseline"] = o["cpu_baseline"]["value"]
+            r["cpu_cores"] = o["cpu_baseline"]["cores"]
+        return r
+
+    s = {"c3": obj(out), "c4": obj(out.get("mining")), "c5": obj(out.get("long_outputs")),
+         "c2": obj(out.get("replay"))}
+    if out.get("mining", {}).get("suffix"):
+        s["c4_suffix"] = {k: out["mining"]["suffix"][k] for k in ("value", "roofline_frac")}
+    if out.get("parity"):
+        s["parity_ok"] = out["parity"]["ok"]
+    return s
 
 
 REPLAY_METRIC = "replayed tool calls/sec (score_accuracy)"
@@ -549,6 +612,9 @@ def run_long_outputs(args, world, rank, local):
 
 
 MINE_METRIC = "mined trace events/sec"
+# 28 B columnar read + 4 B token written + 4 B token
+# re-read + ~0.5 B offsets per event (here the token is the 4-B staged word)
+MINE_ALG_BYTES = 36.5
 
 
 def run_mining(args, world, rank, local):
@@ -558,27 +624,49 @@ def run_mining(args, world, rank, local):
     One step = ingest + count (K1+K2 fused) -> merge -> expand -> select +
     sort (mine()'s output order) -> the sorted pattern table on the host.
     ``e2e`` adds the H2D of the columns and the materialised
-    list[PatternTuple]."""
-    import numpy as np
+    list[PatternTuple].  Both match relations are run (anchored = headline,
+    contiguous suffix = the ``suffix`` object); at N=1 the full-size count
+    tables and pattern lists of both are compared with the oracle."""
     import torch
     import torch.distributed as dist
 
-    from paper_2603_18897_b200 import _native
-    from paper_2603_18897_b200.mine_engine import MineTables, ingest_count
     from paper_2603_18897_b200.mining import MiningConfig
     from paper_2603_18897_b200.packing import SigTable
     from paper_2603_18897_b200.synth import C4_TOOLS, columnar_corpus
 
     n_local = args.mine_events // world
-    cfg = MiningConfig(k=3, sigma=5, tau=0.3)
     sigs = SigTable(C4_TOOLS)
     host = columnar_corpus(n_local, seed=2603 + rank)
     host_pinned = {k: torch.from_numpy(v).pin_memory() for k, v in host.items()}
     dev = {k: v.cuda() for k, v in host_pinned.items()}
-    tables = MineTables.allocate(sigs.n_sigs, cfg.k, 0)
+    group = dist.group.WORLD if world > 1 else None
+    out = mining_relation(args, world, rank, sigs, host, host_pinned, dev, group, relation=0)
+    sfx = mining_relation(args, world, rank, sigs, host, host_pinned, dev, group, relation=1)
+    out["suffix"] = {k: sfx[k] for k in ("value", "ms_per_step", "patterns", "ingest_count_ms")}
+    out["suffix"]["roofline_frac"] = sfx["roofline"]["frac"]
+    out["suffix"]["e2e"] = sfx["e2e"]["value"]
+    if "parity" in sfx:
+        out["suffix"]["parity"] = sfx["parity"]
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = mining_cpu_baseline(MiningConfig(k=3, sigma=5, tau=0.3), sigs)
+    return out
+
+
+def mining_relation(args, world, rank, sigs, host, host_pinned, dev, group, relation):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_18897_b200 import _native
+    from paper_2603_18897_b200.mine_engine import MineTables, ingest_count
+    from paper_2603_18897_b200.mining import MatchRelation, MiningConfig
+
+    n_local = int(host["sig"].shape[0])
+    cfg = MiningConfig(k=3, sigma=5, tau=0.3,
+                       match_relation=MatchRelation.CONTIGUOUS_SUFFIX if relation
+                       else MatchRelation.ANCHORED_SUBSEQUENCE)
+    tables = MineTables.allocate(sigs.n_sigs, cfg.k, relation)
     lib = _native.lib()
     stream = torch.cuda.current_stream()
-    group = dist.group.WORLD if world > 1 else None
 
     def one_step(trace):
         tables.hist.zero_()
@@ -609,7 +697,7 @@ def run_mining(args, world, rank, local):
     for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        pats = one_step(dev)
+        table = one_step(dev)
         e1.record(stream)
         e1.synchronize()
         t_dev += e0.elapsed_time(e1) / 1e3
@@ -644,11 +732,13 @@ def run_mining(args, world, rank, local):
         t_dev, t_kern, t_e2e = t.tolist()
     total = n_local * world
     peak, peak_kind = measured_peaks()
-    achieved = 28.0 * n_local / (t_kern / steps) / 1e9
+    achieved = MINE_ALG_BYTES * n_local / (t_kern / steps) / 1e9
+    traffic = committed_ncu("ncu_mine_latest.json")
+    rel = "suffix" if relation else "anchored"
     out = {"metric": MINE_METRIC, "value": total * steps / t_dev, "unit": "events/s",
            "n_gpus": world, "steps": steps, "ms_per_step": 1e3 * t_dev / steps,
            "scaling": "strong", "data": "synthetic",
-           "config": {"workload": "C4: columnar trace mining, k=3 sigma=5 tau=0.3 anchored",
+           "config": {"workload": f"C4: columnar trace mining, k=3 sigma=5 tau=0.3 {rel}",
                       "events_total": total, "events_per_gpu": n_local, "signatures": sigs.n_sigs,
                       "parallelism": f"session shards x{world} + NCCL all-reduce of the "
                                      "(k+1)-gram histogram" if world > 1 else "single GPU",
@@ -657,18 +747,44 @@ def run_mining(args, world, rank, local):
            "ingest_count_ms": 1e3 * t_kern / steps,
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak,
+                        "traffic": traffic.get("dram_bytes_per_event", 0) * n_local or None,
                         "kernel": "ingest+count: columnar_count_kernel + stage_hist_kernel",
-                        "algorithmic_bytes_per_launch": 28 * n_local,
+                        "algorithmic_bytes_per_launch": int(MINE_ALG_BYTES * n_local),
                         "peak_source": f"{peak_kind} hbm_gbs",
-                        "note": "28 B/event columnar read (session, seq, t_start, t_end, sig); "
-                                "the 4 B/event staged words (written + re-read) are not counted"},
+                        "note": "SURVEY 8(d) 36.5 B/event: 28 B columnar read + 4 B staged "
+                                "word written + 4 B re-read + 0.5 B offsets; traffic = ncu "
+                                "dram bytes of both passes scaled per event "
+                                "(profiles/ncu_mine_latest.json)"},
            "e2e": {"value": total * steps / t_e2e, "unit": "events/s", "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": 8 + 48 * len(pats), "ms_per_step": 1e3 * t_e2e / steps,
                    "includes": "H2D of the columns + step + list[PatternTuple] materialised"},
            "gpu_launches": launches}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = mining_cpu_baseline(cfg, sigs)
+    if rank == 0 and world == 1 and not args.no_parity:
+        out["parity"] = mining_full_parity(tables, host, sigs, cfg, relation, pats)
+    del tables
+    torch.cuda.empty_cache()
     return out
+
+
+def mining_full_parity(tables, host, sigs, cfg, relation, pats):
+    """The benchmarked corpus at full size: the device count tables (left by
+    the last timed step) and the pattern list against the oracle."""
+    import numpy as np
+
+    from oracle.parity import mining_parity
+    from paper_2603_18897_b200.mine_engine import patterns_from_candidates
+    from oracle import bridge
+
+    t0 = time.perf_counter()
+    r = mining_parity(tables, host, sigs.n_sigs, cfg.k, relation)
+    cands = np.array(bridge.select_candidates(*r.pop("oracle_tables"), sigs.n_sigs, cfg.k,
+                                              cfg.sigma, cfg.tau), np.int64).reshape(-1, 5)
+    exp = patterns_from_candidates(cands, sigs, sigs.n_sigs, cfg)
+    r["patterns_ok"] = exp == pats
+    r["ok"] = r["ok"] and r["patterns_ok"]
+    r["patterns"] = len(exp)
+    r["check_s"] = round(time.perf_counter() - t0, 2)
+    return r
 
 
 def mining_cpu_baseline(cfg, sigs, n_events=1_000_000):
@@ -691,14 +807,18 @@ def mining_cpu_baseline(cfg, sigs, n_events=1_000_000):
             "sample": f"{n_events} events of the C4 corpus ({dt:.1f} s)"}
 
 
+def committed_ncu(name: str) -> dict:
+    """A committed ncu summary under profiles/ ({} when absent)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
 def committed_traffic():
     """dram bytes per launch of predict_kernel from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "ncu_predict_latest.json")
-    try:
-        with open(path) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
-    except (OSError, ValueError):
-        return None
+    return committed_ncu("ncu_predict_latest.json").get("dram_bytes_per_launch")
 
 
 def oracle_live_run(args, n, threads, budget_s, max_steps=64):

@@ -308,7 +308,9 @@ int paste_mine_ingest_count(const paste_columnar_desc* c, const paste_mine_desc*
  * as the columnar trace above with session = segment index (count it with
  * no further gap split: inactivity_ms = +inf) and sig = 2 * tool + success,
  * tools interned in sorted name order (tool_names: sorted, NUL-separated).
- * Lines missing a required field are errors (error_lines, 1-based).  Input
+ * Lines missing a required field, or that Event.__post_init__ rejects
+ * (t_start > t_end; a tool_call with an empty tool), are errors
+ * (error_lines, 1-based; error_codes / error_seq give the reason).  Input
  * outside the parser's exact subset (escapes in ids, non-string ids,
  * non-integral seq, NaN start times, duplicate keys, unvalidated JSON,
  * other line separators) returns PASTE_ERR_UNSUPPORTED: use the host
@@ -332,7 +334,18 @@ typedef struct {
   int64_t tool_names_len;      /* out                                         */
   int32_t n_tools;             /* out                                         */
   int32_t pad;
+  int32_t* error_codes;        /* optional [error_capacity]: PASTE_INGEST_*   */
+  int64_t* error_seq;          /* optional [error_capacity]: the record's seq */
 } paste_ingest_desc;
+
+/* error_codes: PASTE_INGEST_MISSING | mask of the absent fields (bit i =
+ * _REQUIRED_FIELDS[i]: session_id, seq, kind, tool, status, t_start_ms,
+ * t_end_ms; "missing fields: ..."), PASTE_INGEST_T_ORDER ("event seq=N:
+ * t_start > t_end"), PASTE_INGEST_EMPTY_TOOL ("event seq=N: tool_call with
+ * empty tool_type") -- events.py:59-63,142-145.                             */
+#define PASTE_INGEST_MISSING 0x100
+#define PASTE_INGEST_T_ORDER 0x200
+#define PASTE_INGEST_EMPTY_TOOL 0x400
 
 int paste_ingest_jsonl(const char* text, int64_t len, double inactivity_ms, paste_ingest_desc* d);
 /* Same, in two passes: the columnar pass writes one staged word per event

@@ -83,13 +83,14 @@ def predict(im: PoolImage, batch: WindowBatch, K: int,
     return res
 
 
-def mine_counts(tokens: np.ndarray, n_sigs: int, k: int, relation: int):
-    """Oracle mining tables (tool_count, support, match, follow) as numpy."""
+def mine_counts(tokens: np.ndarray, n_sigs: int, k: int, relation: int, threads: int = 1):
+    """Oracle mining tables (tool_count, support, match, follow) as numpy;
+    threads > 1 counts stream-aligned chunks in parallel and sums them."""
     L = lib()
-    fn = L.oracle_mine_counts
+    fn = L.oracle_mine_counts_mt
     fn.restype = c_int
     fn.argtypes = [c_void_p, ctypes.c_int64, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
-                   c_void_p]
+                   c_void_p, c_int]
     T = (n_sigs + 1) // 2
     n_ctx = sum(n_sigs ** q for q in range(1, k + 1))
     tool_count = np.zeros(T, np.uint64)
@@ -98,7 +99,7 @@ def mine_counts(tokens: np.ndarray, n_sigs: int, k: int, relation: int):
     follow = np.zeros(n_ctx * T, np.uint64)
     tok = np.ascontiguousarray(tokens, np.int32)
     rc = fn(_p(tok), len(tok), n_sigs, k, relation, _p(tool_count), _p(support), _p(match),
-            _p(follow))
+            _p(follow), threads)
     if rc != 0:
         raise RuntimeError("oracle_mine_counts failed")
     return tool_count, support, match, follow

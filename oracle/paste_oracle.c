@@ -391,6 +391,55 @@ int oracle_mine_counts(const int32_t* tokens, int64_t n_tokens, int S, int k, in
   return PASTE_OK;
 }
 
+/* The same counts over n_threads chunks of the stream, each cut at a stream
+ * start (streams never share a window or a match, mining.py:219-226), into
+ * per-thread tables that are summed: the counting above, only partitioned. */
+int oracle_mine_counts_mt(const int32_t* tokens, int64_t n_tokens, int S, int k, int relation,
+                          uint64_t* tool_count, uint64_t* support, uint64_t* match,
+                          uint64_t* follow, int n_threads) {
+  const int T = (S + 1) / 2;
+  int64_t n_ctx = 0, p = 1, *cut;
+  int q, t, rc = PASTE_OK;
+  uint64_t* part;
+  size_t per;
+  if (n_threads < 2 || n_tokens < 2)
+    return oracle_mine_counts(tokens, n_tokens, S, k, relation, tool_count, support, match, follow);
+  for (q = 1; q <= k; ++q) { p *= S; n_ctx += p; }
+  per = (size_t)T + (size_t)T * n_ctx + (size_t)n_ctx + (size_t)n_ctx * T;
+  cut = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n_threads + 1));
+  part = (uint64_t*)calloc(per * (size_t)n_threads, sizeof(uint64_t));
+  if (!cut || !part) { free(cut); free(part); return PASTE_ERR_INVALID; }
+  for (t = 0; t <= n_threads; ++t) {
+    int64_t c = n_tokens * t / n_threads;
+    while (c > 0 && c < n_tokens && !(tokens[c] & (int32_t)0x80000000)) ++c;
+    cut[t] = t == n_threads ? n_tokens : c;
+  }
+#pragma omp parallel for num_threads(n_threads) schedule(static, 1)
+  for (t = 0; t < n_threads; ++t) {
+    uint64_t* b = part + per * (size_t)t;
+    int64_t lo = cut[t], hi = cut[t + 1];
+    if (hi <= lo) continue; /* empty chunk */
+    if (oracle_mine_counts(tokens + lo, hi - lo, S, k, relation, b, b + T, b + T + (size_t)T * n_ctx,
+                           b + T + (size_t)T * n_ctx + n_ctx) != PASTE_OK)
+      rc = PASTE_ERR_INVALID;
+  }
+  {
+    int64_t i;
+#pragma omp parallel for num_threads(n_threads) schedule(static)
+    for (i = 0; i < (int64_t)per; ++i) {
+      uint64_t s = 0;
+      for (t = 0; t < n_threads; ++t) s += part[per * (size_t)t + (size_t)i];
+      if (i < T) tool_count[i] += s;
+      else if (i < T + (int64_t)T * n_ctx) support[i - T] += s;
+      else if (i < T + (int64_t)T * n_ctx + n_ctx) match[i - T - (int64_t)T * n_ctx] += s;
+      else follow[i - T - (int64_t)T * n_ctx - n_ctx] += s;
+    }
+  }
+  free(cut);
+  free(part);
+  return rc;
+}
+
 /* ------------------------------------------------------------------------ */
 /* greedy_speculative_selection (scheduling.py:242-258): sort by            */
 /* (-U, -p, id), U = (p * benefit) / (cost * duration); take while cost fits */

@@ -116,6 +116,7 @@ class CompactDesc(ctypes.Structure):
 
 PASTE_CF_HDR8, PASTE_CF_PRED8, PASTE_CF_ARG16, PASTE_CF_ENTRY16 = 1, 2, 4, 8
 PASTE_COPY_H2D, PASTE_COPY_D2H, PASTE_COPY_D2D = 1, 2, 3
+PASTE_INGEST_MISSING, PASTE_INGEST_T_ORDER, PASTE_INGEST_EMPTY_TOOL = 0x100, 0x200, 0x400
 
 
 class HoldsDesc(ctypes.Structure):
@@ -150,7 +151,8 @@ class IngestDesc(ctypes.Structure):
                 ("error_lines", c_void_p), ("error_capacity", c_int64), ("tool_names", c_void_p),
                 ("tool_names_capacity", c_int64), ("n_events", c_int64), ("n_segments", c_int64),
                 ("n_errors", c_int64), ("n_lines", c_int64), ("reordered_sessions", c_int64),
-                ("tool_names_len", c_int64), ("n_tools", c_int32), ("pad", c_int32)]
+                ("tool_names_len", c_int64), ("n_tools", c_int32), ("pad", c_int32),
+                ("error_codes", c_void_p), ("error_seq", c_void_p)]
 
 
 # numpy mirrors of the element structs

@@ -12,14 +12,17 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libpaste.so")
 
-NVCC_FLAGS = [
+COMPILE_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "--fmad=false",            # fp64 utilities / EWMA must round like the reference
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-shared", "-lgomp",
-    "-cudart=static",
+    "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp",
     "-Xptxas", "-v",
 ]
+LINK_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-lgomp",
+              "-cudart=static", "-Xcompiler", "-fopenmp"]
+NVCC_FLAGS = COMPILE_FLAGS + LINK_FLAGS  # kept for scripts that print the recipe
+OBJ = os.path.join(ROOT, "build", "obj")
 
 
 def nvcc() -> str:
@@ -44,14 +47,37 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC, *sources(),
-           "-o", OUT + ".tmp"]
-    proc = subprocess.run(cmd, capture_output=True, text=True)
+    # one nvcc per translation unit, in parallel, then one link
+    from concurrent.futures import ThreadPoolExecutor
+
+    os.makedirs(OBJ, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(ROOT, "include", "paste.h")]
+    newest_header = max(os.path.getmtime(h) for h in headers)
+
+    def compile_one(src: str):
+        obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(src), newest_header)):
+            return obj, subprocess.CompletedProcess([], 0, "", "")
+        cmd = [nvcc(), *COMPILE_FLAGS, *inc, "-c", src, "-o", obj]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    srcs = sorted(sources(), key=lambda f: -os.path.getsize(f))  # longest first
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, srcs))
+    for obj, proc in results:
+        if proc.returncode != 0:
+            sys.stderr.write(proc.stdout + proc.stderr)
+            raise RuntimeError(f"nvcc failed building {os.path.basename(obj)}")
+        if verbose:
+            sys.stderr.write(proc.stderr)
+    proc = subprocess.run([nvcc(), *LINK_FLAGS, *[o for o, _ in results], "-o", OUT + ".tmp"],
+                          capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
-        raise RuntimeError("nvcc failed building libpaste.so")
-    if verbose:
-        sys.stderr.write(proc.stderr)
+        raise RuntimeError("nvcc failed linking libpaste.so")
     os.replace(OUT + ".tmp", OUT)
     return OUT
 

@@ -38,13 +38,16 @@ void reset_launches();
 
 namespace {
 
-enum LineKind : uint8_t { L_EMPTY, L_OK, L_MISSING, L_ODD };
+// L_MISSING: a required field is absent; L_INVALID: Event.__post_init__
+// rejects the record (events.py:59-63).  Both are tallied ingest errors.
+enum LineKind : uint8_t { L_EMPTY, L_OK, L_MISSING, L_INVALID, L_ODD };
 
 struct Rec {
   std::string_view session, tool;
   int64_t seq = 0;
   double t_start = 0, t_end = 0;
   int32_t line = 0;  // 1-based
+  int32_t reason = 0;  // error code (paste_ingest_desc.error_codes)
   uint8_t kind = L_EMPTY;
   bool tool_call = true, success = true;
 };
@@ -240,7 +243,21 @@ void parse_line(const char* b, const char* e, Rec& r) {
   }
   c.ws();
   if (c.p != c.e) { r.kind = L_ODD; return; }
-  r.kind = seen == 127 ? L_OK : L_MISSING;
+  if (seen != 127) {
+    r.kind = L_MISSING;
+    r.reason = PASTE_INGEST_MISSING | (127 & ~seen);  // the absent fields, in _REQUIRED_FIELDS order
+    return;
+  }
+  // Event.__post_init__ (events.py:59-63), in its order
+  if (r.t_start > r.t_end) {
+    r.kind = L_INVALID;
+    r.reason = PASTE_INGEST_T_ORDER;
+  } else if (r.tool_call && r.tool.empty()) {
+    r.kind = L_INVALID;
+    r.reason = PASTE_INGEST_EMPTY_TOOL;
+  } else {
+    r.kind = L_OK;
+  }
 }
 
 // bytes that make str.splitlines() split where '\n' does not
@@ -301,8 +318,14 @@ extern "C" int paste_ingest_jsonl(const char* text, int64_t len, double inactivi
   for (int64_t i = 0; i < n_lines; ++i) {
     const Rec& r = recs[i];
     if (r.kind == L_EMPTY) continue;
-    if (r.kind == L_MISSING) {
-      if (n_err < d->error_capacity && d->error_lines) d->error_lines[n_err] = r.line;
+    if (r.kind == L_MISSING || r.kind == L_INVALID) {
+      if (n_err < d->error_capacity) {
+        if (d->error_lines) d->error_lines[n_err] = r.line;
+        if (d->error_codes) {
+          d->error_codes[n_err] = r.reason;
+          if (d->error_seq) d->error_seq[n_err] = r.seq;
+        }
+      }
       ++n_err;
       continue;
     }

@@ -59,6 +59,20 @@ def _host(text: str, inactivity_ms: float) -> ColumnarTrace:
                          native=False)
 
 
+_REQUIRED_FIELDS = ("session_id", "seq", "kind", "tool", "status", "t_start_ms", "t_end_ms")
+
+
+def _error_message(code: int, seq: int) -> str:
+    """The reference's IngestError text for a native error code
+    (events.py:59-63 Event.__post_init__, :142-145 _parse_record)."""
+    if code & _native.PASTE_INGEST_MISSING:
+        missing = [f for i, f in enumerate(_REQUIRED_FIELDS) if code >> i & 1]
+        return f"missing fields: {', '.join(missing)}"
+    if code & _native.PASTE_INGEST_T_ORDER:
+        return f"event seq={seq}: t_start > t_end"
+    return f"event seq={seq}: tool_call with empty tool_type"
+
+
 def ingest_columnar(source: str | bytes,
                     inactivity_ms: float = DEFAULT_INACTIVITY_THRESHOLD_MS) -> ColumnarTrace:
     text = source.decode("utf-8") if isinstance(source, bytes) else source  # UTF-8 as the reference
@@ -69,9 +83,12 @@ def ingest_columnar(source: str | bytes,
             "t_start": np.empty(cap, np.float64), "t_end": np.empty(cap, np.float64),
             "sig": np.empty(cap, np.int32)}
     err = np.empty(cap, np.int32)
+    code = np.empty(cap, np.int32)
+    eseq = np.empty(cap, np.int64)
     names = ctypes.create_string_buffer(len(raw) + 1)
     d = IngestDesc(cap, *[c.ctypes.data for c in cols.values()], err.ctypes.data, cap,
                    ctypes.addressof(names), len(raw) + 1)
+    d.error_codes, d.error_seq = code.ctypes.data, eseq.ctypes.data
     rc = lib.paste_ingest_jsonl(raw, len(raw), float(inactivity_ms), ctypes.byref(d))
     if rc == PASTE_ERR_UNSUPPORTED:
         return _host(text, inactivity_ms)
@@ -79,7 +96,8 @@ def ingest_columnar(source: str | bytes,
     tools = names.raw[:d.tool_names_len].split(b"\0")[:d.n_tools]
     sigs = SigTable([t.decode("utf-8", "surrogatepass") for t in tools])
     n = d.n_events
-    errors = [IngestError(int(line), "missing fields") for line in err[:d.n_errors]]
+    errors = [IngestError(int(line), _error_message(int(c), int(q)))
+              for line, c, q in zip(err[:d.n_errors], code[:d.n_errors], eseq[:d.n_errors])]
     return ColumnarTrace({k: v[:n] for k, v in cols.items()}, sigs, d.n_segments,
                          d.reordered_sessions, errors)
 

@@ -61,7 +61,7 @@ def _assert_same(a, b):
         assert np.array_equal(a.columns[k], b.columns[k], equal_nan=k.startswith("t_")), k
     assert a.sigs.tools == b.sigs.tools
     assert a.n_segments == b.n_segments and a.reordered_sessions == b.reordered_sessions
-    assert [e.line for e in a.errors] == [e.line for e in b.errors]
+    assert [(e.line, e.message) for e in a.errors] == [(e.line, e.message) for e in b.errors]
 
 
 @pytest.mark.parametrize("seed", [1, 2, 3])
@@ -95,3 +95,29 @@ def test_line_separators_python_would_split():
     res = ingest.ingest_columnar(text)
     assert not res.native
     _assert_same(res, ingest._host(text, 300_000.0))
+
+
+def test_post_init_rejections_are_ingest_errors():
+    """Records Event.__post_init__ rejects (t_start > t_end; a tool_call with
+    an empty tool) are tallied errors with the reference's messages, on the
+    native path, not events (events.py:59-63)."""
+    good = _trace(5, n_sessions=30, extras=False)
+    bad = [
+        '{"session_id": "s1", "seq": 4, "kind": "tool_call", "tool": "a", "status": "success", '
+        '"t_start_ms": 5.0, "t_end_ms": 2.0}',
+        '{"session_id": "s1", "seq": 5, "kind": "tool_call", "tool": "", "status": "fail", '
+        '"t_start_ms": 1.0, "t_end_ms": 2.0}',
+        '{"session_id": "s2", "seq": 6, "kind": "llm_step", "tool": "", "status": "success", '
+        '"t_start_ms": 1.0, "t_end_ms": 2.0}',  # an LLM step may have an empty tool
+        '{"session_id": "s3", "seq": 7, "kind": "llm_step", "tool": "", "status": "success", '
+        '"t_start_ms": 9.0, "t_end_ms": 2.0}',
+        '{"seq": 8, "tool": "", "status": "success", "t_start_ms": 9.0}',
+    ]
+    text = good + "\n".join(bad) + "\n"
+    nat = ingest.ingest_columnar(text)
+    assert nat.native
+    host = ingest._host(text, 300_000.0)
+    _assert_same(nat, host)
+    msgs = [e.message for e in nat.errors]
+    assert msgs == ["event seq=4: t_start > t_end", "event seq=5: tool_call with empty tool_type",
+                    "event seq=7: t_start > t_end", "missing fields: session_id, kind, t_end_ms"]

@@ -321,3 +321,25 @@ def test_action_keys_match_canonical_arg_hash():
                 assert keys[slot].tobytes().hex() == canonical_arg_hash(a.prediction.args)
                 checked += 1
     assert checked > 1000 and warm > 0
+
+
+@pytest.mark.parametrize("n,steps", [(400_000, 6), (1_000_000, 18)])
+def test_live_beyond_one_persistent_sweep(n, steps):
+    """Sizes past one persistent-CTA sweep (grid SMs x resident CTAs x 128
+    threads = 151,552 sessions on a B200): the multi-chunk CTA loop with
+    walk-memo reuse across chunks (predict_fast_kernel) and the fused
+    serving kernel's multi-thousand-tile look-back (predict_compact_kernel),
+    every record of every step against the oracle.  The 1M x 18 case is the
+    benchmarked C3 configuration with every window full."""
+    from oracle.parity import live_parity
+
+    pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
+    book = EstimateBook()
+    for tool, ms in (("search", 700.0), ("web_fetch", 1078.8), ("file_editor", 300.0),
+                     ("terminal", 1424.2), ("grep", 400.0)):
+        book.update(tool, ms)
+    r = live_parity(DevicePool(pool), parse_policy(MOTIF_POLICY).policy, book, n, steps, K=8,
+                    seed=n + steps)
+    assert r["kslot_ok"] and r["serve_ok"], r["mismatch"]
+    assert r["serve_kernel"].startswith("fused")
+    assert r["predictions"] > n * steps
