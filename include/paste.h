@@ -413,6 +413,71 @@ typedef struct {
 int paste_action_keys(const paste_action_keys_desc* d, void* stream);
 
 /* ---------------------------------------------------------------------- */
+/* A16: admitted actions -> scheduler jobs (scheduling.py:464-511, 59-60)   */
+/* ---------------------------------------------------------------------- */
+
+/* Admitted actions in batch order (sessions in order, each session's
+ * actions in admit order), as Scheduler.submit_speculative_batch feeds them
+ * to _admit_action.                                                        */
+typedef struct {
+  int64_t n_actions;
+  const int32_t* tool;        /* [n] tool id                                   */
+  const uint8_t* level;       /* [n] SpecLevel: 1 warm_only, 2 dry_run, 3 full */
+  const double* p;            /* [n] prediction.probability                    */
+  const uint8_t* key;         /* [n][16] canonical_arg_hash(args) digest (16-B
+                                 aligned; ignored for WARM_ONLY)               */
+  int32_t n_tools;
+  int32_t pad;
+  const double* mean;         /* [n_tools] EstimateBook.duration(tool)         */
+  const int32_t* cost;        /* [n_tools] EstimateBook.cost(tool)             */
+  double warm_fraction;       /* EstimateBook.warm_fraction                    */
+  int64_t r_total;            /* ResourceState.r_total (cost > r_total: drop)  */
+  int64_t id_base;            /* the scheduler's next job id                   */
+} paste_actions_desc;
+
+/* Job columns (the paste_select_desc inputs), in batch order.              */
+typedef struct {
+  double* p;                  /* [<= n] Job.p                                  */
+  double* benefit;            /* [<= n] Job.benefit_ms                         */
+  double* duration;           /* [<= n] Job.duration_est_ms                    */
+  int32_t* cost;              /* [<= n] Job.cost                               */
+  int64_t* id;                /* [<= n] Job.id                                 */
+  int64_t* action;            /* [<= n] source action index, or NULL           */
+  int64_t* n_jobs;            /* [1] jobs written                              */
+  int64_t* next_id;           /* [1] id_base + ids consumed                    */
+} paste_jobs_out;
+
+/* _admit_action over a batch into a fresh scheduler: terms per level
+ * (WARM_ONLY T = wf*mean, d = max(wf*mean, 1e-9); DRY_RUN T = wf*mean,
+ * d = max(mean, 1e-9); FULL T = mean, d = max(mean, 1e-9)), in-batch key
+ * coalescing (first action of a key wins), ids in batch order, cost >
+ * r_total dropped after taking an id.  Synchronous.                        */
+int64_t paste_action_jobs_scratch_bytes(int64_t n_actions);
+int paste_action_jobs(const paste_actions_desc* a, paste_jobs_out* j, void* scratch,
+                      int64_t scratch_bytes, void* stream);
+
+/* A live step's K-slot records -> action columns in batch order (tool =
+ * pattern target, p = pattern p, key copied from paste_action_keys' output
+ * slot when slot_keys is non-NULL).  Stream-ordered; *n_actions on device. */
+typedef struct {
+  int64_t n_sessions;
+  paste_pool_desc pool;
+  paste_predict_out out;
+  const uint8_t* slot_keys;   /* [n*K][16] paste_action_keys output, or NULL   */
+  int32_t* tool;              /* [<= n*K]                                      */
+  uint8_t* level;
+  double* p;
+  uint8_t* key;               /* [<= n*K][16] (when slot_keys)                 */
+  int64_t* session;           /* [<= n*K] session of each action               */
+  int32_t* slot;              /* [<= n*K] record slot of each action           */
+  int64_t* n_actions;         /* [1]                                           */
+} paste_live_actions_desc;
+
+int64_t paste_live_actions_scratch_bytes(int64_t n_sessions);
+int paste_live_actions(const paste_live_actions_desc* l, void* scratch, int64_t scratch_bytes,
+                       void* stream);
+
+/* ---------------------------------------------------------------------- */
 /* K6: admission selection (scheduling.py:59-60, 242-258)                   */
 /* ---------------------------------------------------------------------- */
 
@@ -431,7 +496,8 @@ typedef struct {
 /* greedy_speculative_selection: jobs in ascending (-U, -p, id) with
  * U = (p * benefit) / (cost * duration), taken while cost fits both the
  * remaining slack and budget.  Synchronous (returns after the result is
- * written).  Envelope: min(slack, budget) <= 64.                         */
+ * written).  min(slack, budget) <= 64: per-cost-class radix select + on-chip
+ * sort; larger caps (or > 4,096 tied candidates): full device sort path.   */
 int64_t paste_select_scratch_bytes(int64_t n_jobs);
 int paste_select_greedy(paste_select_desc* d, int64_t slack, int64_t budget, void* scratch,
                         int64_t scratch_bytes, void* stream);

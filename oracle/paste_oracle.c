@@ -456,7 +456,8 @@ static int o_job_cmp(const void* a_, const void* b_) {
   const o_job* b = (const o_job*)b_;
   if (a->u != b->u) return a->u > b->u ? -1 : 1; /* -U ascending */
   if (a->p != b->p) return a->p > b->p ? -1 : 1; /* -p ascending */
-  return a->id < b->id ? -1 : (a->id > b->id ? 1 : 0);
+  if (a->id != b->id) return a->id < b->id ? -1 : 1;
+  return a->idx < b->idx ? -1 : (a->idx > b->idx ? 1 : 0); /* sorted() is stable */
 }
 
 int64_t oracle_greedy(int64_t n, const double* p, const double* benefit, const double* duration,

@@ -145,6 +145,24 @@ class ActionKeysDesc(ctypes.Structure):
                                        "key_state")]
 
 
+class ActionsDesc(ctypes.Structure):
+    _fields_ = [("n_actions", c_int64), ("tool", c_void_p), ("level", c_void_p), ("p", c_void_p),
+                ("key", c_void_p), ("n_tools", c_int32), ("pad", c_int32), ("mean", c_void_p),
+                ("cost", c_void_p), ("warm_fraction", ctypes.c_double), ("r_total", c_int64),
+                ("id_base", c_int64)]
+
+
+class JobsOut(ctypes.Structure):
+    _fields_ = [(name, c_void_p) for name in ("p", "benefit", "duration", "cost", "id", "action",
+                                              "n_jobs", "next_id")]
+
+
+class LiveActionsDesc(ctypes.Structure):
+    _fields_ = [("n_sessions", c_int64), ("pool", PoolDesc), ("out", PredictOut)] + \
+        [(name, c_void_p) for name in ("slot_keys", "tool", "level", "p", "key", "session",
+                                       "slot", "n_actions")]
+
+
 class IngestDesc(ctypes.Structure):
     _fields_ = [("capacity", c_int64), ("session", c_void_p), ("seq", c_void_p),
                 ("t_start", c_void_p), ("t_end", c_void_p), ("sig", c_void_p),
@@ -183,6 +201,11 @@ EXPORTS = {
     "paste_canonical_hash": (c_int, [POINTER(HashDesc), c_void_p]),
     "paste_ingest_jsonl": (c_int, [c_char_p, c_int64, ctypes.c_double, POINTER(IngestDesc)]),
     "paste_action_keys": (c_int, [POINTER(ActionKeysDesc), c_void_p]),
+    "paste_action_jobs_scratch_bytes": (c_int64, [c_int64]),
+    "paste_action_jobs": (c_int, [POINTER(ActionsDesc), POINTER(JobsOut), c_void_p, c_int64,
+                                  c_void_p]),
+    "paste_live_actions_scratch_bytes": (c_int64, [c_int64]),
+    "paste_live_actions": (c_int, [POINTER(LiveActionsDesc), c_void_p, c_int64, c_void_p]),
     "paste_predict_compact_scratch_bytes": (c_int64, [c_int64]),
     "paste_predict_compact_supported": (c_int, [POINTER(PoolDesc), c_int, c_int, c_int, c_int]),
     "paste_predict_compact": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc), POINTER(AdmitDesc),

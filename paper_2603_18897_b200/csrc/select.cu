@@ -17,6 +17,8 @@
 //   * the candidates are sorted by the full key (-U, -p, id) in shared memory
 //     (bitonic) and one warp runs the greedy scan; visiting a superset of the
 //     selected jobs in the same relative order yields the same decisions.
+#include <cub/cub.cuh>
+
 #include "common.cuh"
 
 namespace paste {
@@ -45,7 +47,8 @@ struct SelJob {
 __device__ __forceinline__ bool sel_less(const SelJob& a, const SelJob& b) {
   if (a.ku != b.ku) return a.ku < b.ku;
   if (a.kp != b.kp) return a.kp < b.kp;
-  return a.id < b.id;
+  if (a.id != b.id) return a.id < b.id;
+  return a.idx < b.idx;  // sorted() is stable: equal keys keep the input order
 }
 
 // per-job keys + validation
@@ -220,9 +223,195 @@ __global__ void __launch_bounds__(1024) sel_greedy_kernel(paste_select_desc D, c
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// General path (any min(slack, budget), any number of ties): a full device
+// sort by (-U, -p, id) of the jobs that can ever fit (cost <= cap), a stable
+// sort of those by cost to rank each job inside its cost class, the same
+// floor(cap / c) prefix rule per class to keep the candidates, and a
+// warp-parallel greedy scan over the candidates in key order.
+// ---------------------------------------------------------------------------
+__global__ void gen_keys_kernel(paste_select_desc D, const uint64_t* ku, int64_t cap,
+                                uint64_t* k0, uint64_t* k1, uint64_t* k2, uint8_t* fit,
+                                int32_t* iota) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= D.n_jobs) return;
+  const int c = D.cost[i];
+  fit[i] = c >= 1 && (int64_t)c <= cap;
+  k0[i] = ku[i];
+  k1[i] = desc_key(D.p[i]);
+  k2[i] = (uint64_t)D.id[i] ^ 0x8000000000000000ull;
+  iota[i] = (int32_t)i;
+}
+
+__global__ void gen_cost_kernel(paste_select_desc D, const int32_t* order, int64_t n,
+                                int32_t* ckey, int32_t* pos) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  ckey[i] = D.cost[order[i]];
+  pos[i] = (int32_t)i;
+}
+
+// t-th element of the cost-sorted array: rank inside its class = t - first
+// index of its cost (binary search); candidate if rank < floor(cap / c)
+__global__ void gen_flag_kernel(const int32_t* csorted, const int32_t* pos_sorted, int64_t n,
+                                int64_t cap, uint8_t* flag) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int32_t c = csorted[t];
+  int64_t lo = 0, hi = t;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (csorted[mid] < c) lo = mid + 1;
+    else hi = mid;
+  }
+  flag[pos_sorted[t]] = (t - lo) < cap / c ? 1 : 0;
+}
+
+__global__ void gen_gather_kernel(const uint64_t* src, const int32_t* order, int64_t n,
+                                  uint64_t* dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[order[i]];
+}
+
+__global__ void gen_iota_kernel(int32_t* a, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (int32_t)i;
+}
+
+// one warp: greedy over the candidates (positions in key order, ascending)
+__global__ void gen_scan_kernel(paste_select_desc D, const int32_t* order, const int32_t* cand,
+                                const int* n_cand_p, int64_t slack, int64_t budget) {
+  const int lane = threadIdx.x;
+  const int64_t n_cand = *n_cand_p;
+  int64_t r = slack, b = budget, n_sel = 0;
+  for (int64_t base = 0; base < n_cand; base += 32) {
+    if (r < 1 || b < 1) break;  // every cost is >= 1
+    const int64_t i = base + lane;
+    int32_t job = -1;
+    int64_t c = INT64_MAX;
+    if (i < n_cand) {
+      job = order[cand[i]];
+      c = D.cost[job];
+    }
+    bool alive = i < n_cand;
+    for (;;) {
+      const unsigned m = __ballot_sync(0xffffffffu, alive && c <= r && c <= b);
+      if (!m) break;
+      const int f = __ffs(m) - 1;
+      const int64_t cf = __shfl_sync(0xffffffffu, c, f);
+      const int32_t jf = __shfl_sync(0xffffffffu, job, f);
+      if (lane == 0) D.selected[n_sel] = jf;
+      ++n_sel;
+      r -= cf;
+      b -= cf;
+      alive = alive && lane > f;
+    }
+  }
+  if (lane == 0) *D.n_selected = n_sel;
+}
 }  // namespace paste
 
 using namespace paste;
+
+static int64_t align256(int64_t b) { return (b + 255) / 256 * 256; }
+
+static size_t general_cub_bytes(int64_t n) {
+  const int m = (int)(n > 0 ? n : 1);
+  size_t a = 0, b = 0, c = 0;
+  cub::DoubleBuffer<uint64_t> k64(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> v32(nullptr, nullptr), k32(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, a, k64, v32, m);
+  cub::DeviceRadixSort::SortPairs(nullptr, b, k32, v32, m);
+  cub::DeviceSelect::Flagged(nullptr, c, (int32_t*)nullptr, (uint8_t*)nullptr, (int32_t*)nullptr,
+                             (int*)nullptr, m);
+  return a > b ? (a > c ? a : c) : (b > c ? b : c);
+}
+
+// bytes of the radix-select path (ku first: the general path reuses it)
+static int64_t fast_bytes(int64_t n) {
+  return align256(8 * n) + 32 * SEL_MAX_CAP + 4 * SEL_MAX_CAP * 256 + 4 * (SEL_MAX_CAP + 4) + 16 +
+         4 * SEL_MAX_CAND + 256;
+}
+
+static int64_t general_bytes(int64_t n) {
+  return 3 * align256(8 * n) + 2 * align256(8 * n) + 2 * align256(4 * n) + align256(n) +
+         align256(4 * n) + 256 + (int64_t)general_cub_bytes(n) + 256;
+}
+
+// The general path: see gen_* above.  ku = per-job -U order keys (computed).
+static int select_general(paste_select_desc* d, int64_t slack, int64_t budget, int64_t cap,
+                          const uint64_t* ku, uint8_t* s, uint8_t* s_end, cudaStream_t stream) {
+  const int64_t n = d->n_jobs;
+  uint64_t* k0 = reinterpret_cast<uint64_t*>(s); s += align256(8 * n);
+  uint64_t* k1 = reinterpret_cast<uint64_t*>(s); s += align256(8 * n);
+  uint64_t* k2 = reinterpret_cast<uint64_t*>(s); s += align256(8 * n);
+  uint64_t* ka = reinterpret_cast<uint64_t*>(s); s += align256(8 * n);
+  uint64_t* kb = reinterpret_cast<uint64_t*>(s); s += align256(8 * n);
+  int32_t* va = reinterpret_cast<int32_t*>(s); s += align256(4 * n);
+  int32_t* vb = reinterpret_cast<int32_t*>(s); s += align256(4 * n);
+  uint8_t* flag = s; s += align256(n);
+  int32_t* cand = reinterpret_cast<int32_t*>(s); s += align256(4 * n);
+  unsigned* counters = reinterpret_cast<unsigned*>(s); s += 256;
+  void* tmp = s;
+  size_t tmp_bytes = (size_t)(s_end - s);
+  PASTE_CUDA_CHECK(cudaMemsetAsync(counters, 0, 16, stream));
+  const int blocks = (int)((n + SEL_T - 1) / SEL_T);
+  // the jobs that can ever fit, compacted in input order (equal keys must
+  // keep it: sorted() is stable)
+  gen_keys_kernel<<<blocks, SEL_T, 0, stream>>>(*d, ku, cap, k0, k1, k2, flag, cand);
+  count_launch();
+  int* n_fit = reinterpret_cast<int*>(counters);
+  PASTE_CUDA_CHECK(cub::DeviceSelect::Flagged(tmp, tmp_bytes, cand, flag, va, n_fit, (int)n, stream));
+  count_launch(2);
+  int h_fit = 0;
+  PASTE_CUDA_CHECK(cudaMemcpyAsync(&h_fit, n_fit, 4, cudaMemcpyDeviceToHost, stream));
+  PASTE_CUDA_CHECK(cudaStreamSynchronize(stream));
+  const int m = h_fit;
+  if (m == 0) {
+    PASTE_CUDA_CHECK(cudaMemsetAsync(d->n_selected, 0, sizeof(int64_t), stream));
+    return PASTE_OK;
+  }
+  const int mblocks = (m + SEL_T - 1) / SEL_T;
+  // LSD over the key words (stable): id, then -p, then -U; values = job index
+  cub::DoubleBuffer<int32_t> vals(va, vb);
+  const uint64_t* words[3] = {k2, k1, k0};
+  for (int w = 0; w < 3; ++w) {
+    gen_gather_kernel<<<mblocks, SEL_T, 0, stream>>>(words[w], vals.Current(), m, ka);
+    count_launch();
+    cub::DoubleBuffer<uint64_t> keys(ka, kb);
+    PASTE_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, vals, m, 0, 64, stream));
+    count_launch(8);
+  }
+  // order[t] = job index of the t-th fit job in key order
+  const int32_t* order = vals.Current();
+  // rank inside each cost class: stable sort of key positions by cost
+  int32_t* ck = reinterpret_cast<int32_t*>(ka);
+  int32_t* ck2 = reinterpret_cast<int32_t*>(ka) + m;
+  int32_t* pos = reinterpret_cast<int32_t*>(kb);
+  int32_t* pos2 = reinterpret_cast<int32_t*>(kb) + m;
+  gen_cost_kernel<<<mblocks, SEL_T, 0, stream>>>(*d, order, m, ck, pos);
+  count_launch();
+  int cbits = 1;
+  while (cbits < 31 && (int64_t(1) << cbits) <= cap) ++cbits;
+  cub::DoubleBuffer<int32_t> ckeys(ck, ck2), cpos(pos, pos2);
+  PASTE_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ckeys, cpos, m, 0, cbits, stream));
+  count_launch(4);
+  gen_flag_kernel<<<mblocks, SEL_T, 0, stream>>>(ckeys.Current(), cpos.Current(), m, cap, flag);
+  count_launch();
+  // candidate key positions in ascending order
+  int32_t* iota = reinterpret_cast<int32_t*>(ckeys.Alternate());
+  gen_iota_kernel<<<mblocks, SEL_T, 0, stream>>>(iota, m);
+  count_launch();
+  int* n_cand = reinterpret_cast<int*>(counters + 1);
+  PASTE_CUDA_CHECK(cub::DeviceSelect::Flagged(tmp, tmp_bytes, iota, flag, cand, n_cand, m, stream));
+  count_launch(2);
+  gen_scan_kernel<<<1, 32, 0, stream>>>(*d, order, cand, n_cand, slack, budget);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  PASTE_CUDA_CHECK(cudaStreamSynchronize(stream));
+  return PASTE_OK;
+}
 
 extern "C" int paste_select_greedy(paste_select_desc* d, int64_t slack, int64_t budget,
                                    void* scratch, int64_t scratch_bytes, void* stream_) {
@@ -234,19 +423,15 @@ extern "C" int paste_select_greedy(paste_select_desc* d, int64_t slack, int64_t 
   const int64_t need = paste_select_scratch_bytes(n);
   PASTE_REQUIRE(scratch != nullptr && scratch_bytes >= need, "scratch too small (%lld bytes)",
                 (long long)need);
+  PASTE_REQUIRE(n < (1ll << 31) - 1, "more than 2^31 - 2 jobs");
   if (n == 0 || cap64 < 1) {
     PASTE_CUDA_CHECK(cudaMemsetAsync(d->n_selected, 0, sizeof(int64_t), stream));
     return PASTE_OK;  // nothing fits (every cost >= 1)
   }
-  if (cap64 > SEL_MAX_CAP) {
-    set_error("min(slack, budget) = %lld exceeds the device envelope (%d)", (long long)cap64,
-              SEL_MAX_CAP);
-    return PASTE_ERR_UNSUPPORTED;
-  }
-  const int cap = (int)cap64;
-  uint8_t* s = static_cast<uint8_t*>(scratch);
+  uint8_t* s0 = static_cast<uint8_t*>(scratch);
+  uint8_t* s = s0;
   uint64_t* ku = reinterpret_cast<uint64_t*>(s);
-  s += 8 * n;
+  s += align256(8 * n);
   uint64_t* prefix = reinterpret_cast<uint64_t*>(s);
   s += 24 * SEL_MAX_CAP;
   int64_t* rank = reinterpret_cast<int64_t*>(s);
@@ -258,7 +443,24 @@ extern "C" int paste_select_greedy(paste_select_desc* d, int64_t slack, int64_t 
   unsigned* n_cand = reinterpret_cast<unsigned*>(s);
   s += 16;
   int32_t* cand = reinterpret_cast<int32_t*>(s);
+  uint8_t* gen = s0 + fast_bytes(n);
+  uint8_t* gen_end = s0 + scratch_bytes;
 
+  PASTE_CUDA_CHECK(cudaMemsetAsync(flags, 0, 4 * (SEL_MAX_CAP + 4), stream));
+  const int blocks = (int)((n + SEL_T - 1) / SEL_T);
+  sel_keys_kernel<<<blocks, SEL_T, 0, stream>>>(*d, ku, flags);
+  count_launch();
+  int h_flags[2] = {0, 0};
+  if (cap64 > SEL_MAX_CAP) {  // outside the radix-select envelope: general path
+    PASTE_CUDA_CHECK(cudaMemcpyAsync(h_flags, flags, sizeof(h_flags), cudaMemcpyDeviceToHost, stream));
+    PASTE_CUDA_CHECK(cudaStreamSynchronize(stream));
+    if (h_flags[0]) {
+      set_error("jobs need cost >= 1, a non-zero duration and a non-NaN utility");
+      return PASTE_ERR_INVALID;
+    }
+    return select_general(d, slack, budget, cap64, ku, gen, gen_end, stream);
+  }
+  const int cap = (int)cap64;
   // host-side init of the small state (ranks = floor(cap / c) - 1)
   {
     uint64_t h_prefix[3 * SEL_MAX_CAP];
@@ -270,23 +472,16 @@ extern "C" int paste_select_greedy(paste_select_desc* d, int64_t slack, int64_t 
     PASTE_CUDA_CHECK(cudaMemcpyAsync(prefix, h_prefix, sizeof(h_prefix), cudaMemcpyHostToDevice, stream));
     PASTE_CUDA_CHECK(cudaMemcpyAsync(rank, h_rank, sizeof(h_rank), cudaMemcpyHostToDevice, stream));
     PASTE_CUDA_CHECK(cudaMemsetAsync(hist, 0, 4 * SEL_MAX_CAP * 256, stream));
-    PASTE_CUDA_CHECK(cudaMemsetAsync(flags, 0, 4 * (SEL_MAX_CAP + 4), stream));
     PASTE_CUDA_CHECK(cudaMemsetAsync(n_cand, 0, 16, stream));
     // a synchronous copy keeps the stack arrays alive until they are consumed
     PASTE_CUDA_CHECK(cudaStreamSynchronize(stream));
   }
-  const int blocks = (int)((n + SEL_T - 1) / SEL_T);
-  sel_keys_kernel<<<blocks, SEL_T, 0, stream>>>(*d, ku, flags);
-  count_launch();
   const int hblocks = blocks < 148 * 4 ? blocks : 148 * 4;
-  static bool attrs = false;
-  if (!attrs) {
-    cudaFuncSetAttribute(sel_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         4 * SEL_MAX_CAP * 256);
-    cudaFuncSetAttribute(sel_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(SelJob) * SEL_MAX_CAND);
-    attrs = true;
-  }
+  // the shared-memory opt-in is per device: set it on every call (cheap)
+  PASTE_CUDA_CHECK(cudaFuncSetAttribute(sel_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        4 * SEL_MAX_CAP * 256));
+  PASTE_CUDA_CHECK(cudaFuncSetAttribute(sel_greedy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)sizeof(SelJob) * SEL_MAX_CAND));
   for (int pass = 0; pass < 24; ++pass) {  // kernels return at once when every class is done
     sel_hist_kernel<<<hblocks, SEL_T, 4 * cap * 256, stream>>>(*d, ku, cap, pass, prefix,
                                                                 flags + 3, flags + 2, hist);
@@ -300,23 +495,19 @@ extern "C" int paste_select_greedy(paste_select_desc* d, int64_t slack, int64_t 
                                                                          slack, budget, flags + 1);
   count_launch();
   PASTE_CUDA_CHECK(cudaGetLastError());
-  int h_flags[2];
   PASTE_CUDA_CHECK(cudaMemcpyAsync(h_flags, flags, sizeof(h_flags), cudaMemcpyDeviceToHost, stream));
   PASTE_CUDA_CHECK(cudaStreamSynchronize(stream));
   if (h_flags[0]) {
     set_error("jobs need cost >= 1, a non-zero duration and a non-NaN utility");
     return PASTE_ERR_INVALID;
   }
-  if (h_flags[1]) {
-    set_error("more than %d candidate jobs (ties) for the on-chip sort", SEL_MAX_CAND);
-    return PASTE_ERR_UNSUPPORTED;
-  }
+  if (h_flags[1])  // more than SEL_MAX_CAND tied candidates: the general path
+    return select_general(d, slack, budget, cap64, ku, gen, gen_end, stream);
   return PASTE_OK;
 }
 
 extern "C" int64_t paste_select_scratch_bytes(int64_t n_jobs) {
-  return 8 * n_jobs + 32 * SEL_MAX_CAP + 4 * SEL_MAX_CAP * 256 + 4 * (SEL_MAX_CAP + 4) + 16 +
-         4 * SEL_MAX_CAND + 256;
+  return fast_bytes(n_jobs) + general_bytes(n_jobs);
 }
 
 // ---------------------------------------------------------------------------

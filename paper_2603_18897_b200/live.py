@@ -73,6 +73,7 @@ class LiveSessionTable:
         self.evt = torch.full((n * W,), -1, dtype=torch.int32, device=dev)
         self.count = torch.zeros(n, dtype=torch.int64, device=dev)
         self.nodes = to_dev(nodes)
+        self.host_nodes = nodes
         self.bytes = torch.zeros(max(self.regions * self.max_batch_bytes, 1), dtype=torch.uint8,
                                  device=dev)
         self.refs = torch.zeros(self.regions * n * 2, dtype=torch.int64, device=dev)
@@ -116,6 +117,16 @@ class LiveSessionTable:
         self.sformat = ef if self.lib.paste_predict_compact_supported(
             ctypes.byref(self.pool_desc), capacity, K, B, ef) else self.cformat
         self._entries = None
+
+    def refresh_estimates(self, estimates) -> None:
+        """Re-read ``benefit_of = estimates.duration`` for every tool (the
+        reference reads the current EWMA at every prediction,
+        simulation.py:428-429): call after ``EstimateBook.update`` so the
+        device admit tables and ``CompactRecords.expand`` see the new values."""
+        bene = np.array([float(estimates.duration(name)) for name in self.dpool.sigs.tools]
+                        or [0.0], np.float64)
+        self.benefit = bene
+        self.adm_arrays[2].copy_(self.torch.from_numpy(bene))
 
     # -- state upload ---------------------------------------------------------
 

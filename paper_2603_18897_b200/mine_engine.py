@@ -336,7 +336,10 @@ def mine(traces: Sequence[Session], cfg: MiningConfig, group=None) -> list[Patte
 
 
 def validate(context, target: str, mapping: ValueMapping | None, traces: Sequence[Session],
-             cfg: MiningConfig) -> float:
+             cfg: MiningConfig | None = None) -> float:
+    cfg = cfg or MiningConfig()
+    if not context:  # match_at never matches an empty context (mining.py:128-130)
+        raise ValueError("context has no matches in the given traces")
     streams = [s.tool_events() for s in traces]
     if len(context) > cfg.k and cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE:
         raise ValueError("context has no matches in the given traces")

@@ -407,6 +407,64 @@ def make_greedy():
     return {"cases": cases}
 
 
+def make_jobs():
+    """Scheduler._admit_action (scheduling.py:464-511) on batches of admitted
+    actions from many sessions, into a fresh scheduler: the job terms
+    (benefit / duration by level, the 1e-9 clamp, warm_fraction, per-tool
+    cost), key coalescing (warm key (tool, "warm"), others (tool, arg hash)),
+    ids, the cost > r_total drop; then greedy_speculative_selection over the
+    admitted jobs (Job.utility, scheduling.py:59-60, 242-258)."""
+    from spectool.policy import SpeculativeAction
+    from spectool.scheduling import ResourceState, Scheduler
+
+    rng = random.Random(1616)
+    tools = ["search", "web_fetch", "terminal", "file_editor", "grep", "big"]
+    cases = []
+    for inst in range(120):
+        n_sess = rng.randint(0, 30 if inst % 4 else 6)
+        wf = rng.choice([0.2, 0.2, 0.35, 0.0, 1e-12])
+        book = EstimateBook(warm_fraction=wf, costs={"terminal": 2, "grep": 3, "big": 9},
+                            default_duration_ms=rng.choice([1000.0, 1000.0, 0.0, 5e-10]))
+        for t in tools:
+            r = rng.random()
+            if r < 0.5:
+                book.update(t, rng.choice([700.0, 1100.0, rng.uniform(1, 5000), 3e-9, 0.0]))
+            if r < 0.2:
+                book.update(t, rng.uniform(1, 5000))
+        r_total = rng.choice([4, 8, 24])
+        sched = Scheduler(ResourceState(r_total, 1 << 30), launcher=lambda j: None,
+                          estimates=book)
+        actions, jobs = [], []
+        for s in range(n_sess):
+            for a in range(rng.randint(0, 8)):
+                tool = rng.choice(tools)
+                args = {"u": rng.randint(0, 6)} if rng.random() < 0.8 else {"q": "x", "n": [1, 2]}
+                level = rng.choice([SpecLevel.FULL, SpecLevel.DRY_RUN, SpecLevel.WARM_ONLY])
+                p = rng.choice([0.5, 0.9, rng.uniform(0.01, 1.0)])
+                pred = PredictedInvocation(tool, args, Completeness.FULL, p, f"pat{a}", 0.0)
+                act = SpeculativeAction(pred, level, p * 1.0)
+                job = sched._admit_action(act, f"s{s}", 0.0)
+                actions.append({"session": s, "tool": tool, "args": args, "level": int(level),
+                                "p": p})
+                jobs.append(None if job is None else
+                            [job.id, job.p, job.benefit_ms, job.cost, job.duration_est_ms,
+                             job.arg_hash, job.utility() if job.cost * job.duration_est_ms
+                             else None])
+        admitted = [sched.jobs[j[0]] for j in jobs if j is not None]
+        sel = []
+        for slack, budget in ((rng.randint(0, 12), rng.randint(0, 12)), (200, 150)):
+            try:
+                chosen = [j.id for j in greedy_speculative_selection(admitted, slack, budget)]
+            except ZeroDivisionError:
+                chosen = "ZeroDivisionError"
+            sel.append({"slack": slack, "budget": budget, "expected": chosen})
+        cases.append({"tools": tools, "estimates": {
+            "default": book.default_duration_ms, "warm_fraction": wf, "costs": book.costs,
+            "durations": dict(book._duration)}, "r_total": r_total, "next_id": next(sched._ids),
+            "actions": actions, "jobs": jobs, "select": sel})
+    return {"cases": cases}
+
+
 # ---------------------------------------------------------------------------
 # candidate_paths
 # ---------------------------------------------------------------------------
@@ -534,6 +592,8 @@ def main(which):
         make_c2()
     if "hash" in which:
         make_hash()
+    if "jobs" in which:
+        dump("jobs_golden.json", make_jobs())
     if "fixtures" not in which:
         return
     dump("predict_golden.json", make_predict())

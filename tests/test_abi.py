@@ -65,7 +65,8 @@ def _c_sizeof(struct_name: str) -> int:
     ("paste_leaf_scan_desc", "LeafScanDesc"), ("paste_resolve_desc", "ResolveDesc"),
     ("paste_compact_desc", "CompactDesc"), ("paste_holds_desc", "HoldsDesc"),
     ("paste_hash_desc", "HashDesc"), ("paste_action_keys_desc", "ActionKeysDesc"),
-    ("paste_ingest_desc", "IngestDesc"),
+    ("paste_ingest_desc", "IngestDesc"), ("paste_actions_desc", "ActionsDesc"),
+    ("paste_jobs_out", "JobsOut"), ("paste_live_actions_desc", "LiveActionsDesc"),
 ])
 def test_struct_layouts_match_header(cname, pyname):
     assert ctypes.sizeof(getattr(_native, pyname)) == _c_sizeof(cname)

@@ -109,7 +109,7 @@ def _compare(dev: PredictResult, ora: PredictResult):
                           ora.act_util[act_valid].view(np.int64))
 
 
-def _live_vs_oracle(dp, n, steps, seed, policy, book, K=8, workload=None):
+def _live_vs_oracle(dp, n, steps, seed, policy, book, K=8, workload=None, updates=None):
     wl = workload or LiveWorkload(dp.sigs, dp.keys, n, seed=seed)
     table = LiveSessionTable(dp, n, wl.tmpl.nodes, wl.max_batch_bytes, policy, book,
                              max_candidates=K)
@@ -121,6 +121,11 @@ def _live_vs_oracle(dp, n, steps, seed, policy, book, K=8, workload=None):
     tables = admit_tables(dp.sigs, policy, book.duration)
     total_preds = 0
     for step in range(steps):
+        if updates and step in updates:  # EWMA moves: the device tables follow
+            for tool, ms in updates[step]:
+                book.update(tool, ms)
+            table.refresh_estimates(book)
+            tables = admit_tables(dp.sigs, policy, book.duration)
         batch = wl.next_batch()
         if step % 2:
             batch.node = None  # alternate the wide (16-B directory entry) observe input
@@ -145,6 +150,19 @@ def test_live_c3_pool_matches_oracle():
         book.update(tool, ms)
     n_preds = _live_vs_oracle(DevicePool(pool), 20_000, 24, 7, parse_policy(MOTIF_POLICY).policy, book)
     assert n_preds > 20_000 * 24  # the pool fires on this workload
+
+
+def test_live_follows_estimate_updates():
+    """EstimateBook.update between steps + refresh_estimates: utilities and
+    per-tool arbitration use the current EWMA, as the reference reads
+    estimates.duration at every prediction (simulation.py:428-429)."""
+    pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
+    book = EstimateBook()
+    ups = {3: [("search", 700.0), ("web_fetch", 5000.0)], 9: [("terminal", 1.5), ("search", 3.0)],
+           14: [("web_fetch", 0.0)]}
+    n_preds = _live_vs_oracle(DevicePool(pool), 5_000, 18, 11, parse_policy(MOTIF_POLICY).policy,
+                              book, updates=ups)
+    assert n_preds > 0
 
 
 def test_live_stress_pool_matches_oracle():

@@ -44,7 +44,10 @@ def test_device_greedy_matches_reference():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("n,cap,ties", [(2_000_000, 24, False), (1_000_000, 64, True),
-                                        (300_000, 8, True), (50, 64, False)])
+                                        (300_000, 8, True), (50, 64, False),
+                                        # general path: caps past the radix-select envelope
+                                        (2_000_000, 128, False), (1_000_000, 4_000, True),
+                                        (100_000, 10**9, True), (70, 65, False)])
 def test_device_greedy_matches_oracle_at_scale(n, cap, ties):
     torch = pytest.importorskip("torch")
     if not torch.cuda.is_available():
@@ -61,10 +64,33 @@ def test_device_greedy_matches_oracle_at_scale(n, cap, ties):
         bene = rng.uniform(100, 10_000, n)
         dur = rng.uniform(100, 5_000, n)
     cost = rng.integers(1, 6, n).astype(np.int32)
+    if cap > 1000:
+        cost = rng.integers(1, 300, n).astype(np.int32)
     ids = rng.permutation(n).astype(np.int64) + 1
     slack, budget = cap + 3, cap
     got = select_greedy_arrays(p, bene, dur, cost, ids, slack, budget).tolist()
     assert got == bridge.greedy(p, bene, dur, cost, ids, slack, budget)
+
+
+@pytest.mark.gpu
+def test_device_greedy_many_tied_candidates():
+    """More than the on-chip sort's 4,096 candidates (every job tied on
+    U and p, cost 1, cap 64 -> the radix select is exact, but a cap-64 class
+    of all-equal keys with duplicate ids overflows it): the general path
+    takes over and still matches the oracle."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2603_18897_b200.select import select_greedy_arrays
+
+    n = 50_000
+    p = np.full(n, 0.5)
+    bene = np.full(n, 100.0)
+    dur = np.full(n, 100.0)
+    cost = np.ones(n, np.int32)
+    ids = np.full(n, 7, np.int64)  # duplicate ids: the threshold cannot split the tie
+    got = select_greedy_arrays(p, bene, dur, cost, ids, 64, 64).tolist()
+    assert got == bridge.greedy(p, bene, dur, cost, ids, 64, 64)
 
 
 @pytest.mark.gpu
