@@ -620,6 +620,51 @@ int paste_predict_compact(const paste_pool_desc* pool, paste_windows* windows,
                           const paste_admit_desc* admit, int32_t max_candidates,
                           int32_t max_bindings, paste_compact_desc* out, void* scratch,
                           void* stream);
+/* ---------------------------------------------------------------------- */
+/* Live plan: the live step with its key-only work compiled (live_plan.cu)  */
+/* ---------------------------------------------------------------------- */
+
+/* Which patterns match, their rank order, the bindings to resolve and the
+ * admit decisions (winner per tool, level if complete, utility) depend only
+ * on the match-table key and the admit tables (policy.py:207-244: admission
+ * does not depend on completeness, only the level does).  The plan holds
+ * them per key; the walk table holds, per (binding, node), the node a
+ * PathLookup / FormatTemplate binding resolves to in the tape starting at
+ * that node (mappings.py:143-223; IndexedFallback is resolved at run time).
+ * Rebuild the plan when the admit tables change (policy, EWMA estimates).  */
+typedef struct {
+  const void* plan;           /* paste_live_plan_bytes() bytes                */
+  int32_t max_candidates;     /* K the plan was built for                     */
+  int32_t max_bindings;       /* pool->max_bindings at build                  */
+  const int32_t* walk;        /* [n_bindings][walk_nodes] or NULL             */
+  int64_t walk_nodes;
+} paste_live_plan;
+
+/* -1 when outside the envelope: needs the pool's match table for (K, W),
+ * K <= 31, gather depth <= 4, window capacity <= 16.                       */
+int64_t paste_live_plan_bytes(const paste_pool_desc* pool, int32_t max_candidates,
+                              int32_t window_capacity);
+int paste_build_live_plan(const paste_pool_desc* pool, const paste_admit_desc* admit,
+                          int32_t max_candidates, int32_t window_capacity, void* plan,
+                          void* stream);
+/* -1 above 2^24 entries.                                                    */
+int64_t paste_live_walk_bytes(int32_t n_bindings, int64_t n_nodes);
+int paste_build_live_walk(const paste_pool_desc* pool, int32_t n_bindings,
+                          const paste_tape_node* nodes, int64_t n_nodes, int32_t* walk,
+                          void* stream);
+
+/* paste_predict_batch (observe + predict + admit, same records) from a live
+ * plan: windows must observe (new_tok and new_ref / new_node set).          */
+int paste_predict_live(const paste_pool_desc* pool, paste_windows* windows,
+                       const paste_admit_desc* admit, const paste_live_plan* plan,
+                       paste_predict_out* out, void* stream);
+/* paste_predict_compact from a live plan (same streams and totals).         */
+int64_t paste_predict_live_compact_scratch_bytes(int64_t n_sessions);
+int paste_predict_live_compact(const paste_pool_desc* pool, paste_windows* windows,
+                               const paste_admit_desc* admit, const paste_live_plan* plan,
+                               int32_t max_bindings, paste_compact_desc* out, void* scratch,
+                               void* stream);
+
 int64_t paste_compact_scratch_bytes(int64_t n_sessions);
 int paste_compact_records(const paste_predict_out* out, int64_t n_sessions,
                           const paste_pool_desc* pool, paste_compact_desc* c, void* scratch,

@@ -163,6 +163,11 @@ class LiveActionsDesc(ctypes.Structure):
                                        "slot", "n_actions")]
 
 
+class LivePlan(ctypes.Structure):
+    _fields_ = [("plan", c_void_p), ("max_candidates", c_int32), ("max_bindings", c_int32),
+                ("walk", c_void_p), ("walk_nodes", c_int64)]
+
+
 class IngestDesc(ctypes.Structure):
     _fields_ = [("capacity", c_int64), ("session", c_void_p), ("seq", c_void_p),
                 ("t_start", c_void_p), ("t_end", c_void_p), ("sig", c_void_p),
@@ -198,6 +203,18 @@ EXPORTS = {
     "paste_replay_score": (c_int, [POINTER(PoolDesc), POINTER(ReplayDesc), POINTER(PredictOut),
                                    c_void_p]),
     "paste_compact_scratch_bytes": (c_int64, [c_int64]),
+    "paste_live_plan_bytes": (c_int64, [POINTER(PoolDesc), c_int32, c_int32]),
+    "paste_build_live_plan": (c_int, [POINTER(PoolDesc), POINTER(AdmitDesc), c_int32, c_int32,
+                                      c_void_p, c_void_p]),
+    "paste_live_walk_bytes": (c_int64, [c_int32, c_int64]),
+    "paste_build_live_walk": (c_int, [POINTER(PoolDesc), c_int32, c_void_p, c_int64, c_void_p,
+                                      c_void_p]),
+    "paste_predict_live": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc), POINTER(AdmitDesc),
+                                   POINTER(LivePlan), POINTER(PredictOut), c_void_p]),
+    "paste_predict_live_compact_scratch_bytes": (c_int64, [c_int64]),
+    "paste_predict_live_compact": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc),
+                                           POINTER(AdmitDesc), POINTER(LivePlan), c_int32,
+                                           POINTER(CompactDesc), c_void_p, c_void_p]),
     "paste_canonical_hash": (c_int, [POINTER(HashDesc), c_void_p]),
     "paste_ingest_jsonl": (c_int, [c_char_p, c_int64, ctypes.c_double, POINTER(IngestDesc)]),
     "paste_action_keys": (c_int, [POINTER(ActionKeysDesc), c_void_p]),

@@ -1,0 +1,904 @@
+// Live plan: the live step (K4 / the serving step) with everything that
+// depends only on the match-table key precomputed.
+//
+// Reference: PredictionWindow.observe + Predictor.predict + admit
+// (prediction.py:40-118, mining.py:119-156, mappings.py:143-223,
+// policy.py:207-244), one session per tool completion (simulation.py:402-442).
+//
+// Which patterns match, their rank order, which bindings must be resolved
+// (and against which matched event), and the admit decisions -- which
+// candidate wins each tool, its level when the prediction is complete, its
+// utility p * benefit -- all depend only on the newest G tool tokens (the
+// match-table key) and the per-tool admit tables: admission does not depend
+// on completeness, only the level does (a PARTIAL prediction is admitted at
+// min(cap, WARM_ONLY)).  paste_build_live_plan therefore compiles, per key,
+// the step's records; the live kernel per session is
+//
+//   observe (ring write, directory entry)  ->  newest G-1 older tool tokens
+//   (one batch of independent loads)  ->  key  ->  plan entry (L1/L2)  ->
+//   copy the records, resolve the entry's bindings (walk table: the resolved
+//   node of a PathLookup / FormatTemplate binding depends only on (binding,
+//   node array), one L1/L2 load), downgrade PARTIAL predictions.
+//
+// Each thread runs SPT sessions (j * FT + thread of a tile) with their loads
+// interleaved, for memory-level parallelism.  The serving form writes the
+// narrow streams directly: stream counts depend only on the key, so a tile
+// publishes its aggregate (decoupled look-back) before any binding is
+// resolved, and every record is written once at its final offset -- no
+// staging.
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace paste {
+
+constexpr int LT = 128;  // threads per CTA
+
+__host__ __device__ inline int plan_align(int x, int a) { return (x + a - 1) / a * a; }
+
+struct PlanLayout {
+  int K, M;                  // candidate slots, binding slots (K * max_bindings)
+  int off_pid, off_comp, off_act, off_util, off_map;
+  int64_t stride;
+};
+
+__host__ __device__ inline PlanLayout plan_layout(int K, int max_bind) {
+  PlanLayout L;
+  L.K = K;
+  L.M = K * (max_bind > 0 ? max_bind : 1);
+  L.off_pid = 16;
+  L.off_comp = L.off_pid + 4 * K;
+  L.off_act = plan_align(L.off_comp + K, 16);
+  L.off_util = plan_align(L.off_act + 2 * K, 8);
+  L.off_map = L.off_util + 8 * K;
+  L.stride = plan_align(L.off_map + 8 * L.M, 16);
+  return L;
+}
+
+struct MTRec {  // the match-table record (predict_fast.cu, 32 bytes)
+  int32_t pid;
+  uint32_t src;
+  int32_t tool;
+  int32_t nb_flags;
+  int32_t bind_off;
+  int32_t pad;
+  double p;
+};
+
+// one thread per key: admit the key's first K matches exactly as admit()
+// does (policy.py:207-244) and lay the records out
+__global__ void build_live_plan_kernel(const paste_pool_desc pool, const paste_admit_desc adm,
+                                       const uint8_t* table, int64_t mt_stride, int64_t n_keys,
+                                       PlanLayout L, uint8_t* plan) {
+  const int64_t key = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (key >= n_keys) return;
+  const uint8_t* e = table + key * mt_stride;
+  const int32_t* hdr = reinterpret_cast<const int32_t*>(e);
+  const MTRec* rec = reinterpret_cast<const MTRec*>(e + 16);
+  uint8_t* P = plan + key * L.stride;
+  const int nm = hdr[0] < L.K ? hdr[0] : L.K;
+  int32_t* pid = reinterpret_cast<int32_t*>(P + L.off_pid);
+  uint8_t* comp = P + L.off_comp;
+  uint16_t* act = reinterpret_cast<uint16_t*>(P + L.off_act);
+  double* util = reinterpret_cast<double*>(P + L.off_util);
+  uint64_t* map = reinterpret_cast<uint64_t*>(P + L.off_map);
+  int n_act = 0, n_map = 0;
+  for (int i = 0; i < nm; ++i) {
+    const MTRec r = rec[i];
+    const int flags = r.nb_flags >> 16, nb = r.nb_flags & 0xffff;
+    const bool mapped = (flags & PASTE_PF_HAS_MAPPING) != 0;
+    const int c = mapped ? PASTE_C_FULL : PASTE_C_TOOL_ONLY;
+    pid[i] = r.pid;
+    comp[i] = (uint8_t)c;
+    if (mapped)
+      for (int b = 0; b < nb && n_map < L.M; ++b)
+        map[n_map++] = (uint64_t)(uint32_t)(r.bind_off + b) | ((uint64_t)i << 32) |
+                       ((uint64_t)b << 40) | ((uint64_t)((r.src >> (4 * b)) & 15u) << 48);
+    if (!adm.enabled || r.tool >= adm.n_tools || !adm.allow[r.tool]) continue;
+    const int cap = adm.max_level[r.tool];
+    const int implied = c == PASTE_C_FULL ? 3 : 1;
+    const int lv_full = cap < implied ? cap : implied, lv_part = cap < 1 ? cap : 1;
+    const uint16_t a = (uint16_t)(i | (lv_full << 8) | (lv_part << 12));
+    const double u = __dmul_rn(r.p, adm.benefit[r.tool]);
+    int j = 0;  // the tool's incumbent (first-appearance order is kept)
+    for (; j < n_act; ++j)
+      if (rec[act[j] & 0xff].tool == r.tool) break;
+    if (j == n_act) {
+      act[n_act] = a;
+      util[n_act] = u;
+      ++n_act;
+      continue;
+    }
+    const double iu = util[j], ip = rec[act[j] & 0xff].p;
+    if ((u != iu) ? (u > iu) : (r.p > ip)) {  // _beats: (utility, p, -created_at)
+      act[j] = a;
+      util[j] = u;
+    }
+  }
+  P[0] = (uint8_t)nm;
+  P[1] = (uint8_t)n_act;
+  P[2] = (uint8_t)n_map;
+  P[3] = 0;
+  reinterpret_cast<int32_t*>(P)[1] = hdr[1];
+}
+
+// one thread per (binding, node): the node a PathLookup / FormatTemplate
+// binding resolves to in the payload whose tape starts at `node`; -1 =
+// unresolved, -2 = resolve at run time (IndexedFallback counts failures)
+__global__ void build_walk_kernel(const paste_pool_desc pool, int32_t n_bind,
+                                  const paste_tape_node* nodes, int64_t n_nodes, int32_t* walk) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n_bind * n_nodes) return;
+  const int64_t bind = i / n_nodes, base = i - bind * n_nodes;
+  const paste_binding bd = pool.bindings[bind];
+  if (bd.kind == PASTE_X_FALLBACK) {
+    walk[i] = -2;
+    return;
+  }
+  int64_t cur = 0;
+  const int2* st = reinterpret_cast<const int2*>(pool.steps);
+  for (int s = 0; s < bd.step_cnt && cur >= 0; ++s) {
+    const int2 k = st[bd.step_off + s];
+    cur = step_child(nodes, base, cur, k.x, k.y);
+  }
+  if (bd.kind == PASTE_X_FORMAT && cur >= 0) {  // _leaf_str holes (mappings.py:197-204)
+    const int t = load_node(nodes, base + cur).type();
+    if (t != PASTE_T_STR && t != PASTE_T_INT && t != PASTE_T_FLOAT) cur = -1;
+  }
+  walk[i] = cur >= 0 && cur < (1ll << 31) ? (int32_t)cur : -1;
+}
+
+
+// ---------------------------------------------------------------------------
+// the live kernel
+// ---------------------------------------------------------------------------
+struct LiveParams {
+  paste_pool_desc pool;
+  paste_windows win;
+  paste_predict_out out;  // K-slot records (predict form)
+  paste_compact_desc C;   // narrow streams (serving form)
+  const uint8_t* plan;
+  PlanLayout L;
+  const int32_t* walk;
+  int64_t walk_nodes;
+  int admit;
+  int S;                  // n_bucket_sigs
+  int fast8;              // K = 8, slot-major, n * K * B < 2^31 (kslot_write8)
+  uint64_t* ticket;
+  uint64_t* tile_state;
+  int64_t n_tiles;
+};
+
+template <int G>
+struct Sess {
+  int64_t s;
+  int64_t rbase, rstride;
+  int32_t ev0;             // the observed event
+  int64_t node0;           // its node base
+  int newest;              // ring slot of the observed event, -1 = it is not a tool event
+  uint64_t slots;          // ring slot of the tool event of age a at bits 4a
+  int32_t tk[G];           // newest tool tokens by age
+  int m;
+  const uint8_t* e;        // plan entry (nullptr = no predictions)
+  int nm, n_act, n_map, n_err;
+};
+
+// newest G tool tokens: the G-1 older ring slots in one batch of loads; an
+// LLM step (-1) among them falls back to the slot-by-slot scan
+template <int G>
+__device__ __forceinline__ void gather_slow(const LiveParams& P, Sess<G>& x, int32_t t_new,
+                                            int len, int head) {
+  const int W = P.win.capacity;
+  x.m = 0;
+  x.slots = 0;
+  int slot = head;
+  for (int i = 0; i < len && x.m < G; ++i) {
+    const int32_t t = i == 0 ? t_new : P.win.tok[x.rbase + slot * x.rstride];
+    if (t >= 0) {
+#pragma unroll
+      for (int q = 0; q < G; ++q)
+        if (q == x.m) x.tk[q] = t;
+      x.slots |= (uint64_t)slot << (4 * x.m);
+      ++x.m;
+    }
+    slot = slot == 0 ? W - 1 : slot - 1;
+  }
+}
+
+// stage 1: the session's inputs (independent loads; the values are not
+// consumed here, so the loads stay in flight across a pipelined round)
+struct FrontIn {
+  int64_t s, cnt;
+  paste_event_ref ref;  // new_ref form
+  int32_t node;         // new_node form
+  int32_t t;
+};
+
+__device__ __forceinline__ void front_load(const LiveParams& P, int64_t s, FrontIn& f) {
+  f.s = s;
+  if (s >= P.win.n_sessions) return;
+  f.cnt = P.win.count[s];
+  f.t = P.win.new_tok[s];
+  if (P.win.new_node != nullptr)
+    f.node = P.win.new_node[s];
+  else
+    f.ref = P.win.new_ref[s];
+}
+
+__device__ __forceinline__ int wrap_sub(int a, int b, int W) {  // (a - b) mod W, 0 <= a, b < W
+  const int d = a - b;
+  return d < 0 ? d + W : d;
+}
+
+// stage 2: observe (ring slot, directory entry, count) and issue the loads of
+// the G-1 older ring slots
+template <int G>
+struct FrontMid {
+  int32_t ot[G > 1 ? G - 1 : 1];
+  int32_t t_new;
+  int len;
+};
+
+template <int G>
+__device__ __forceinline__ void front_observe(const LiveParams& P, const FrontIn& f, Sess<G>& y,
+                                              FrontMid<G>& m) {
+  const int64_t n = P.win.n_sessions;
+  const int W = P.win.capacity;
+  y.s = f.s;
+  y.e = nullptr;
+  y.nm = y.n_act = y.n_map = y.n_err = 0;
+  if (f.s >= n) return;
+  const bool slot_major = P.win.slot_major != 0;
+  y.rbase = slot_major ? f.s : f.s * W;
+  y.rstride = slot_major ? n : 1;
+  const int head = (W & (W - 1)) == 0 ? (int)(f.cnt & (W - 1))
+                   : f.cnt < (1ll << 31) ? (int)((uint32_t)f.cnt % (uint32_t)W)
+                                         : (int)(f.cnt % W);
+  y.ev0 = (int32_t)(P.win.new_evt_base + f.s);
+  const bool narrow = P.win.new_node != nullptr;
+  y.node0 = narrow ? (int64_t)f.node : f.ref.node_base;
+  P.win.refs[y.ev0] =
+      paste_event_ref{y.node0, (narrow ? 0 : f.ref.byte_base) + P.win.new_byte_base};
+  P.win.tok[y.rbase + head * y.rstride] = f.t;
+  P.win.evt[y.rbase + head * y.rstride] = y.ev0;
+  const int64_t c1 = f.cnt + 1;
+  P.win.count[f.s] = c1;
+  y.newest = head;
+  m.t_new = f.t;
+  m.len = (int)(c1 < W ? c1 : W);
+#pragma unroll
+  for (int a = 1; a < G; ++a) {
+    m.ot[a - 1] = -1;
+    if (a < m.len) m.ot[a - 1] = P.win.tok[y.rbase + wrap_sub(head, a, W) * y.rstride];
+  }
+}
+
+// stage 3: the newest G tool tokens, the key and the plan entry header
+template <int G, bool COMPACT>
+__device__ __forceinline__ void front_key(const LiveParams& P, Sess<G>& y, const FrontMid<G>& m) {
+  if (y.s >= P.win.n_sessions) return;
+  const int W = P.win.capacity;
+  bool fast = m.t_new >= 0;
+  y.tk[0] = m.t_new;
+  y.slots = (uint64_t)y.newest;
+  y.m = 1;
+#pragma unroll
+  for (int a = 1; a < G; ++a) {
+    if (a < m.len) {
+      fast = fast && m.ot[a - 1] >= 0;
+      y.tk[a] = m.ot[a - 1];
+      y.slots |= (uint64_t)wrap_sub(y.newest, a, W) << (4 * a);
+      y.m = a + 1;
+    }
+  }
+  if (!fast) {
+    gather_slow<G>(P, y, m.t_new, m.len, y.newest);
+    if (m.t_new < 0) y.newest = -1;
+  }
+  if (y.m > 0 && y.tk[0] < P.S) {
+    int key = y.tk[0], mult = P.S;  // keys < 2^31 (paste_live_plan_bytes)
+#pragma unroll
+    for (int a = 1; a < G; ++a) {
+      const int t = a < y.m ? y.tk[a] : P.S;
+      key += (t < P.S ? t : P.S) * mult;
+      mult *= P.S + 1;
+    }
+    y.e = P.plan + (int64_t)key * P.L.stride;
+    const int2 h = *reinterpret_cast<const int2*>(y.e);
+    y.nm = h.x & 0xff;
+    y.n_act = (h.x >> 8) & 0xff;
+    y.n_map = (h.x >> 16) & 0xff;
+    y.n_err = h.y;
+    if (COMPACT) y.slots |= (uint64_t)key << 48;  // ENTRY16 key rides along (<= 0xfffe)
+  }
+}
+
+template <int G, int SPT, bool COMPACT>
+__device__ __forceinline__ void live_front(const LiveParams& P, int64_t base, Sess<G> (&x)[SPT]) {
+  FrontIn f[SPT];
+  FrontMid<G> m[SPT];
+#pragma unroll
+  for (int j = 0; j < SPT; ++j) front_load(P, base + j * LT + threadIdx.x, f[j]);
+#pragma unroll
+  for (int j = 0; j < SPT; ++j) front_observe<G>(P, f[j], x[j], m[j]);
+#pragma unroll
+  for (int j = 0; j < SPT; ++j) front_key<G, COMPACT>(P, x[j], m[j]);
+}
+
+// resolve the entry's bindings for session y; returns the PARTIAL mask and
+// calls emit(q, rank, bslot, ev, node) for every binding (node < 0 = unresolved)
+template <int G, typename F>
+__device__ __forceinline__ uint32_t live_resolve(const LiveParams& P, const Sess<G>& y, F emit) {
+  uint32_t part = 0;
+  const uint64_t* map = reinterpret_cast<const uint64_t*>(y.e + P.L.off_map);
+  for (int q = 0; q < y.n_map; ++q) {
+    const uint64_t w = map[q];
+    const int bind = (int)(uint32_t)w, rank = (int)((w >> 32) & 0xff), bslot = (int)((w >> 40) & 0xff);
+    const int age = (int)((w >> 48) & 0xff);
+    const int slot = (int)((y.slots >> (4 * age)) & 15);
+    int32_t ev;
+    int64_t nb;
+    if (slot == y.newest) {
+      ev = y.ev0;
+      nb = y.node0;
+    } else {
+      ev = P.win.evt[y.rbase + slot * y.rstride];
+      nb = P.win.refs[ev].node_base;
+    }
+    int64_t cur = -2;
+    if (P.walk != nullptr && nb >= 0 && nb < P.walk_nodes) cur = P.walk[(int64_t)bind * P.walk_nodes + nb];
+    if (cur == -2) {  // IndexedFallback, or outside the walk table
+      const paste_binding bd = P.pool.bindings[bind];
+      int fails = 0;  // FAIL events of fail_tool after the source (mappings.py:185-194)
+      if (bd.kind == PASTE_X_FALLBACK) {
+#pragma unroll
+        for (int a = 0; a < G; ++a)
+          if (a < age) fails += ((y.tk[a] >> 1) == bd.fail_tool) && ((y.tk[a] & 1) == 0);
+      }
+      cur = walk_binding(P.win, P.pool.steps, bd, nb, fails);
+    }
+    if (cur < 0) part |= 1u << rank;
+    emit(rank, bslot, ev, cur);
+  }
+  return part;
+}
+
+// true when any lane of this lane's aligned group of g lanes has its bit in
+// `mask` (g = 32-byte sector / element size): a store that only some lanes
+// of a sector make is a partial-sector write, which L2 completes with a DRAM
+// read; filling the sector's other slots with don't-care values avoids it
+__device__ __forceinline__ bool group_any(unsigned mask, int g) {
+  const int lane = threadIdx.x & 31;
+  if (g >= 32) return mask != 0;
+  const unsigned gm = ((1u << g) - 1u) << (lane & ~(g - 1));
+  return (mask & gm) != 0;
+}
+
+// K-slot records of one session from its plan entry (called by every active
+// lane of the warp together).  Slots past n_pred / n_act (and unmapped
+// argument slots) are don't-care; in slot-major layout the lanes write them
+// wherever a neighbour's record shares the 32-byte sector, so every sector is
+// written whole.
+template <int G>
+__device__ __forceinline__ void kslot_write(const LiveParams& P, const Sess<G>& y) {
+  const int64_t n = P.win.n_sessions;
+  const int K = P.out.max_candidates, B = P.out.max_bindings;
+  const bool sm = P.out.slot_major != 0;
+  const int64_t ostride = sm ? n : 1;
+  const int64_t obase = sm ? y.s : y.s * K;
+  const int64_t abase = sm ? y.s : y.s * K * B;
+  const unsigned act_m = __activemask();
+  uint32_t part = 0;
+  uint64_t mapped = 0;  // (rank * B + bslot) bits of the written arguments
+  if (y.n_map > 0)
+    part = live_resolve<G>(P, y, [&](int rank, int bslot, int32_t ev, int64_t cur) {
+      P.out.pred_arg[abase + (int64_t)(rank * B + bslot) * ostride] =
+          cur < 0 ? -1 : (((int64_t)ev << 32) | cur);
+      mapped |= 1ull << ((rank * B + bslot) & 63);
+    });
+  const int max_nm = (int)__reduce_max_sync(act_m, (unsigned)y.nm);
+  const int max_na = (int)__reduce_max_sync(act_m, (unsigned)y.n_act);
+  const int4* pid4 = reinterpret_cast<const int4*>(y.e + P.L.off_pid);
+  const uint32_t* comp4 = reinterpret_cast<const uint32_t*>(y.e + P.L.off_comp);
+  int32_t* pp = P.out.pred_pat + obase;
+  uint8_t* pc = P.out.pred_comp + obase;
+  for (int i0 = 0; i0 < max_nm; i0 += 4) {
+    int4 v = make_int4(-1, -1, -1, -1);
+    uint32_t cw = 0;
+    if (i0 < y.nm) {
+      v = pid4[i0 >> 2];
+      cw = comp4[i0 >> 2];
+    }
+    const int pv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u;
+      if (i >= max_nm) break;
+      const bool mine = i < y.nm;
+      const unsigned have = __ballot_sync(act_m, mine);
+      if (mine || (sm && group_any(have, 8))) pp[i * ostride] = mine ? pv[u] : -1;
+      if (mine || (sm && have)) {
+        const uint8_t c = ((part >> i) & 1u) ? (uint8_t)PASTE_C_PARTIAL : (uint8_t)(cw >> (8 * u));
+        pc[i * ostride] = mine ? c : (uint8_t)PASTE_C_TOOL_ONLY;
+      }
+    }
+  }
+  if (sm && K * B <= 64) {  // unmapped argument slots that share a sector with a written one
+    uint64_t pairs = mapped;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) pairs |= __shfl_xor_sync(act_m, pairs, o);
+    while (pairs) {
+      const int bit = __ffsll((long long)pairs) - 1;
+      pairs &= pairs - 1;
+      const unsigned have = __ballot_sync(act_m, (mapped >> bit) & 1ull);
+      if (!((mapped >> bit) & 1ull) && group_any(have, 4))
+        P.out.pred_arg[abase + (int64_t)bit * ostride] = -1;
+    }
+  }
+  if (max_na > 0) {
+    const uint16_t* act = reinterpret_cast<const uint16_t*>(y.e + P.L.off_act);
+    const double* util = reinterpret_cast<const double*>(y.e + P.L.off_util);
+    for (int a = 0; a < max_na; ++a) {
+      const bool mine = a < y.n_act;
+      const unsigned have = __ballot_sync(act_m, mine);
+      const int64_t o = obase + a * ostride;
+      uint16_t v = 0;
+      double u = 0.0;
+      if (mine) {
+        v = act[a];
+        u = util[a];
+      }
+      const int slot = v & 0xff;
+      if (mine || (sm && group_any(have, 16))) P.out.act_pred[o] = (int16_t)(mine ? slot : -1);
+      if (mine || (sm && have))
+        P.out.act_level[o] = (uint8_t)(((part >> slot) & 1u) ? (v >> 12) & 15 : (v >> 8) & 15);
+      if (mine || (sm && group_any(have, 4))) P.out.act_util[o] = u;
+    }
+  }
+  P.out.n_pred[y.s] = y.nm;
+  P.out.struct_err[y.s] = y.n_err;
+  if (P.admit) P.out.n_act[y.s] = y.n_act;
+}
+
+// max of v over this lane's aligned group of g lanes (full warp only)
+template <int g>
+__device__ __forceinline__ int group_max(int v) {
+#pragma unroll
+  for (int o = 1; o < g; o <<= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// K = 8, slot-major, full warp: the same records with the sector fill
+// computed once per quantity (group maxima over the 8 / 16 / 4 / 32 lanes
+// that share a 32-byte sector of a 4 / 2 / 8 / 1-byte array) and 32-bit
+// record offsets.  Argument slots are written only where resolved.
+template <int G>
+__device__ __forceinline__ void kslot_write8(const LiveParams& P, const Sess<G>& y) {
+  const uint32_t n = (uint32_t)P.win.n_sessions;
+  const uint32_t s = (uint32_t)y.s;
+  const int B = P.out.max_bindings;
+  uint32_t part = 0;
+  if (y.n_map > 0)
+    part = live_resolve<G>(P, y, [&](int rank, int bslot, int32_t ev, int64_t cur) {
+      P.out.pred_arg[(uint32_t)(rank * B + bslot) * n + s] =
+          cur < 0 ? -1 : (((int64_t)ev << 32) | cur);
+    });
+  const int nm = y.nm, na = y.n_act;
+  const int nm8 = group_max<8>(nm);
+  const int nm32 = max(nm8, __shfl_xor_sync(0xffffffffu, max(nm8, __shfl_xor_sync(0xffffffffu, nm8, 8)), 16));
+  const int na4 = group_max<4>(na);
+  int na_16 = max(na4, __shfl_xor_sync(0xffffffffu, na4, 4));
+  na_16 = max(na_16, __shfl_xor_sync(0xffffffffu, na_16, 8));
+  const int na32 = max(na_16, __shfl_xor_sync(0xffffffffu, na_16, 16));
+  int4 p0 = make_int4(-1, -1, -1, -1), p1 = p0;
+  uint64_t cw = 0x0202020202020202ull;  // TOOL_ONLY
+  uint4 av = make_uint4(0, 0, 0, 0);
+  if (y.e) {
+    p0 = *reinterpret_cast<const int4*>(y.e + P.L.off_pid);
+    p1 = *reinterpret_cast<const int4*>(y.e + P.L.off_pid + 16);
+    cw = *reinterpret_cast<const uint64_t*>(y.e + P.L.off_comp);
+    av = *reinterpret_cast<const uint4*>(y.e + P.L.off_act);
+  }
+  const int pv[8] = {p0.x, p0.y, p0.z, p0.w, p1.x, p1.y, p1.z, p1.w};
+  const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+  const double* util = reinterpret_cast<const double*>(y.e + P.L.off_util);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t o = (uint32_t)i * n + s;
+    const bool mine = i < nm;
+    if (i < nm8) P.out.pred_pat[o] = mine ? pv[i] : -1;
+    if (i < nm32)
+      P.out.pred_comp[o] = !mine ? (uint8_t)PASTE_C_TOOL_ONLY
+                           : ((part >> i) & 1u) ? (uint8_t)PASTE_C_PARTIAL
+                                                : (uint8_t)(cw >> (8 * i));
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    if (a >= na32) break;
+    const uint32_t o = (uint32_t)a * n + s;
+    const bool mine = a < na;
+    const uint32_t v = (aw[a >> 1] >> (16 * (a & 1))) & 0xffffu;
+    const int slot = (int)(v & 0xff);
+    if (a < na_16) P.out.act_pred[o] = (int16_t)(mine ? slot : -1);
+    P.out.act_level[o] = (uint8_t)(((part >> slot) & 1u) ? (v >> 12) & 15 : (v >> 8) & 15);
+    if (a < na4) P.out.act_util[o] = mine ? util[a] : 0.0;
+  }
+  P.out.n_pred[s] = nm;
+  P.out.struct_err[s] = y.n_err;
+  if (P.admit) P.out.n_act[s] = na;
+}
+
+// Persistent CTAs, one session per thread per round, software-pipelined over
+// rounds: round r+2's inputs and round r+1's older ring slots are in flight
+// while round r is keyed and written, so the count -> ring -> plan chain
+// costs one memory round trip per round instead of three.
+template <int G>
+__global__ void __launch_bounds__(LT) predict_live_kernel(const LiveParams P) {
+  const int64_t n = P.win.n_sessions;
+  const int64_t stride = (int64_t)gridDim.x * LT;
+  const int64_t s0 = (int64_t)blockIdx.x * LT + threadIdx.x;
+  FrontIn f1, f2;
+  Sess<G> y0, y1;
+  FrontMid<G> m0, m1;
+  front_load(P, s0, f1);
+  front_load(P, s0 + stride, f2);
+  front_observe<G>(P, f1, y1, m1);
+  for (int64_t s = s0; s < n; s += stride) {
+    y0 = y1;
+    m0 = m1;
+    f1 = f2;
+    front_load(P, s + 2 * stride, f2);
+    front_observe<G>(P, f1, y1, m1);
+    front_key<G, false>(P, y0, m0);
+    if (P.fast8 && __activemask() == 0xffffffffu)
+      kslot_write8<G>(P, y0);
+    else
+      kslot_write<G>(P, y0);
+  }
+}
+
+// block-wide exclusive offsets of the 4 stream counters in session order
+// (j-major within the tile), with a decoupled look-back across tiles
+template <int SPT>
+__device__ __forceinline__ void live_offsets(const LiveParams& P, int64_t tile, const int c[SPT][4],
+                                             uint64_t off[SPT][4]) {
+  __shared__ uint32_t s_w[SPT][LT / 32][4];
+  __shared__ uint64_t s_ex[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc[SPT][4];
+#pragma unroll
+  for (int j = 0; j < SPT; ++j)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t v = (uint32_t)c[j][k];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      inc[j][k] = v;
+      if (lane == 31) s_w[j][warp][k] = v;
+    }
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t agg[4], ex[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      agg[k] = 0;
+      for (int j = 0; j < SPT; ++j)
+        for (int w = 0; w < LT / 32; ++w) agg[k] += s_w[j][w][k];
+    }
+    tile_lookback(P.tile_state, tile, agg, ex, lane);
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s_ex[k] = ex[k];
+      if (tile == P.n_tiles - 1) {
+        P.C.totals[0] = (int64_t)(ex[0] + agg[0]);
+        P.C.totals[1] = (int64_t)(ex[1] + agg[1]);
+        P.C.totals[2] = (int64_t)(ex[2] + agg[2]);
+        P.C.totals[4] = (int64_t)(ex[3] + agg[3]);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint64_t run = s_ex[k];
+#pragma unroll
+    for (int j = 0; j < SPT; ++j) {
+      uint64_t before = 0, all = 0;
+      for (int w = 0; w < LT / 32; ++w) {
+        all += s_w[j][w][k];
+        if (w < warp) before += s_w[j][w][k];
+      }
+      off[j][k] = run + before + inc[j][k] - (uint32_t)c[j][k];
+      run += all;
+    }
+  }
+}
+
+template <int G, int SPT>
+__global__ void __launch_bounds__(LT) predict_live_compact_kernel(const LiveParams P) {
+  __shared__ int64_t s_tile;
+  const int64_t n = P.win.n_sessions;
+  const paste_compact_desc& C = P.C;
+  const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
+  const bool entry = (C.format & PASTE_CF_ENTRY16) != 0;
+  unsigned long long wide = 0;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0)
+      s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(P.ticket), 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= P.n_tiles) break;
+    Sess<G> x[SPT];
+    live_front<G, SPT, true>(P, tile * LT * SPT, x);
+    int c[SPT][4];
+#pragma unroll
+    for (int j = 0; j < SPT; ++j) {
+      c[j][0] = x[j].nm;
+      c[j][1] = x[j].n_map;
+      c[j][2] = x[j].n_act;
+      c[j][3] = x[j].n_err;
+    }
+    uint64_t off[SPT][4];
+    live_offsets<SPT>(P, tile, c, off);
+#pragma unroll
+    for (int j = 0; j < SPT; ++j) {
+      const Sess<G>& y = x[j];
+      if (y.s >= n) continue;
+      cf_hdr(C, y.s, y.nm, y.n_act);
+      uint32_t part = 0;
+      if (y.nm > 0 && y.n_map > 0) {
+        int q = 0;
+        const uint64_t oa = off[j][1];
+        part = live_resolve<G>(P, y, [&](int, int, int32_t ev, int64_t cur) {
+          uint32_t w = a16 ? 0xffffu : 0xffffffffu;
+          if (cur >= 0) {
+            const int64_t region =
+                n < (1ll << 31) ? (int64_t)((uint32_t)ev / (uint32_t)n) : (int64_t)ev / n;
+            if ((int64_t)ev - region * n == y.s && region < 31 && cur < (a16 ? (1ll << 11) : (1ll << 27)))
+              w = a16 ? (((uint32_t)region << 11) | (uint32_t)cur)
+                      : (((uint32_t)region << 27) | (uint32_t)cur);
+            else
+              ++wide;
+          }
+          if (a16) static_cast<uint16_t*>(C.arg)[oa + q] = (uint16_t)w;
+          else static_cast<uint32_t*>(C.arg)[oa + q] = w;
+          ++q;
+        });
+      }
+      if (entry) {
+        static_cast<uint16_t*>(C.pred)[y.s] = y.e ? (uint16_t)(y.slots >> 48) : (uint16_t)0xffffu;
+      } else if (y.nm > 0) {
+        const int32_t* pid = reinterpret_cast<const int32_t*>(y.e + P.L.off_pid);
+        const uint8_t* comp = y.e + P.L.off_comp;
+        for (int i = 0; i < y.nm; ++i)
+          cf_pred(C, off[j][0] + i, pid[i], ((part >> i) & 1u) ? PASTE_C_PARTIAL : comp[i]);
+      }
+      if (y.n_act > 0) {
+        const uint16_t* act = reinterpret_cast<const uint16_t*>(y.e + P.L.off_act);
+        for (int a = 0; a < y.n_act; ++a) {
+          const uint16_t v = act[a];
+          const int slot = v & 0xff;
+          const int lv = ((part >> slot) & 1u) ? (v >> 12) & 15 : (v >> 8) & 15;
+          C.act[off[j][2] + a] = (uint8_t)(slot | (lv << 5));
+        }
+      }
+    }
+  }
+  if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(P.C.totals + 3), wide);
+}
+
+}  // namespace paste
+
+using namespace paste;
+
+static int live_gather_depth(const paste_pool_desc* pool, int W) {
+  const int g = pool->relation == PASTE_REL_ANCHORED ? pool->k : pool->max_ctx;
+  return g < W ? g : W;
+}
+
+static int64_t live_keys(const paste_pool_desc* pool, int G) {
+  int64_t keys = pool->n_bucket_sigs;
+  for (int a = 1; a < G; ++a) keys *= (int64_t)pool->n_bucket_sigs + 1;
+  return keys;
+}
+
+extern "C" int64_t paste_live_plan_bytes(const paste_pool_desc* pool, int32_t max_candidates,
+                                         int32_t window_capacity) {
+  if (!pool || !pool->match_table || max_candidates < 1 || max_candidates > 31 ||
+      pool->mt_k < max_candidates || window_capacity < 1 || window_capacity > 16)
+    return -1;
+  const int G = live_gather_depth(pool, window_capacity);
+  if (G < 1 || G > 4 || pool->mt_g != G) return -1;
+  const PlanLayout L = plan_layout(max_candidates, pool->max_bindings);
+  if (L.M > 255) return -1;
+  return live_keys(pool, G) * L.stride;
+}
+
+extern "C" int paste_build_live_plan(const paste_pool_desc* pool, const paste_admit_desc* admit,
+                                     int32_t max_candidates, int32_t window_capacity, void* plan,
+                                     void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(pool && admit && plan, "null argument");
+  const int64_t bytes = paste_live_plan_bytes(pool, max_candidates, window_capacity);
+  if (bytes < 0) {
+    set_error("pool / request shape outside the live-plan envelope (match table, K <= 31, G <= 4)");
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  const int G = live_gather_depth(pool, window_capacity);
+  const int64_t keys = live_keys(pool, G);
+  const PlanLayout L = plan_layout(max_candidates, pool->max_bindings);
+  const int64_t mt_stride = 16 + 32 * (int64_t)pool->mt_k;
+  cudaStream_t st = (cudaStream_t)stream;
+  PASTE_CUDA_CHECK(cudaMemsetAsync(plan, 0, bytes, st));
+  build_live_plan_kernel<<<(unsigned)((keys + 127) / 128), 128, 0, st>>>(
+      *pool, *admit, static_cast<const uint8_t*>(pool->match_table), mt_stride, keys, L,
+      static_cast<uint8_t*>(plan));
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
+
+extern "C" int64_t paste_live_walk_bytes(int32_t n_bindings, int64_t n_nodes) {
+  if (n_bindings < 1 || n_nodes < 1) return -1;
+  const int64_t entries = (int64_t)n_bindings * n_nodes;
+  return entries > (1ll << 24) ? -1 : 4 * entries;
+}
+
+extern "C" int paste_build_live_walk(const paste_pool_desc* pool, int32_t n_bindings,
+                                     const paste_tape_node* nodes, int64_t n_nodes, int32_t* walk,
+                                     void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(pool && nodes && walk, "null argument");
+  if (paste_live_walk_bytes(n_bindings, n_nodes) < 0) {
+    set_error("walk table over 2^24 entries");
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  const int64_t total = (int64_t)n_bindings * n_nodes;
+  build_walk_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      *pool, n_bindings, nodes, n_nodes, walk);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
+
+template <int G, int SPT>
+static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
+  static int sms = 0;
+  static int occ[2] = {0, 0};
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int& o = occ[compact ? 1 : 0];
+  if (o == 0) {
+    if (compact)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_compact_kernel<G, SPT>, LT, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G>, LT, 0);
+    if (o < 1) o = 1;
+  }
+  const int spt = compact ? SPT : 1;
+  const int64_t groups = (P.win.n_sessions + LT * spt - 1) / (LT * spt);
+  const int64_t grid = groups < (int64_t)sms * o ? groups : (int64_t)sms * o;
+  if (compact)
+    predict_live_compact_kernel<G, SPT><<<(unsigned)grid, LT, 0, st>>>(P);
+  else
+    predict_live_kernel<G><<<(unsigned)grid, LT, 0, st>>>(P);
+}
+
+static int live_spt() {
+  static int spt = 0;
+  if (spt == 0) {
+    const char* e = getenv("PASTE_LIVE_SPT");
+    spt = e ? atoi(e) : 2;
+    if (spt != 1 && spt != 2 && spt != 4) spt = 2;
+  }
+  return spt;
+}
+
+template <int G>
+static void launch_live_g(const LiveParams& P, bool compact, cudaStream_t st) {
+  switch (live_spt()) {
+    case 1: launch_live<G, 1>(P, compact, st); break;
+    case 4: launch_live<G, 4>(P, compact, st); break;
+    default: launch_live<G, 2>(P, compact, st); break;
+  }
+}
+
+static int live_prepare(const paste_pool_desc* pool, paste_windows* w, const paste_admit_desc* adm,
+                        const paste_live_plan* plan, int K, LiveParams& P) {
+  PASTE_REQUIRE(pool && w && adm && plan && plan->plan, "null argument");
+  PASTE_REQUIRE(w->new_tok != nullptr && (w->new_ref || w->new_node),
+                "the live kernel observes one new event per session");
+  PASTE_REQUIRE(!w->stream_end, "stream-mode windows are not live sessions");
+  PASTE_REQUIRE(w->capacity >= 1 && w->capacity <= 16, "live plan needs window capacity <= 16");
+  PASTE_REQUIRE(plan->max_candidates == K, "plan built for another max_candidates");
+  PASTE_REQUIRE(plan->max_bindings == pool->max_bindings, "plan built for another pool");
+  const int G = live_gather_depth(pool, w->capacity);
+  PASTE_REQUIRE(G >= 1 && G <= 4 && pool->mt_g == G, "plan / window depth mismatch");
+  memset(&P, 0, sizeof(P));
+  P.pool = *pool;
+  P.win = *w;
+  P.plan = static_cast<const uint8_t*>(plan->plan);
+  P.L = plan_layout(K, pool->max_bindings);
+  P.walk = plan->walk;
+  P.walk_nodes = plan->walk ? plan->walk_nodes : 0;
+  P.admit = adm->enabled;
+  P.S = pool->n_bucket_sigs;
+  return PASTE_OK;
+}
+
+template <typename F>
+static void by_depth(int G, F f) {
+  switch (G) {
+    case 1: f(std::integral_constant<int, 1>()); break;
+    case 2: f(std::integral_constant<int, 2>()); break;
+    case 3: f(std::integral_constant<int, 3>()); break;
+    default: f(std::integral_constant<int, 4>()); break;
+  }
+}
+
+extern "C" int paste_predict_live(const paste_pool_desc* pool, paste_windows* windows,
+                                  const paste_admit_desc* admit, const paste_live_plan* plan,
+                                  paste_predict_out* out, void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(out != nullptr, "null output");
+  PASTE_REQUIRE(out->max_bindings >= pool->max_bindings, "max_bindings below pool maximum");
+  LiveParams P;
+  const int rc = live_prepare(pool, windows, admit, plan, out->max_candidates, P);
+  if (rc != PASTE_OK) return rc;
+  P.out = *out;
+  P.fast8 = out->max_candidates == 8 && out->slot_major &&
+            windows->n_sessions * 8 * (int64_t)out->max_bindings < (1ll << 31);
+  if (windows->n_sessions == 0) return PASTE_OK;
+  const int G = live_gather_depth(pool, windows->capacity);
+  cudaStream_t st = (cudaStream_t)stream;
+  by_depth(G, [&](auto g) { launch_live_g<decltype(g)::value>(P, false, st); });
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
+
+extern "C" int64_t paste_predict_live_compact_scratch_bytes(int64_t n_sessions) {
+  const int64_t tiles = (n_sessions + LT - 1) / LT;  // SPT >= 1
+  return 8 * (LB_STRIDE * tiles + LB_STRIDE);
+}
+
+extern "C" int paste_predict_live_compact(const paste_pool_desc* pool, paste_windows* windows,
+                                          const paste_admit_desc* admit,
+                                          const paste_live_plan* plan, int32_t max_bindings,
+                                          paste_compact_desc* c, void* scratch, void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(c != nullptr && scratch != nullptr, "null argument");
+  PASTE_REQUIRE(max_bindings >= pool->max_bindings, "max_bindings below pool maximum");
+  LiveParams P;
+  const int rc = live_prepare(pool, windows, admit, plan, plan->max_candidates, P);
+  if (rc != PASTE_OK) return rc;
+  const int K = plan->max_candidates;
+  if (((c->format & PASTE_CF_HDR8) && K > 15) ||
+      ((c->format & PASTE_CF_PRED8) && pool->n_patterns > 64) || pool->n_patterns > (1 << 14) ||
+      ((c->format & PASTE_CF_ENTRY16) &&
+       live_keys(pool, live_gather_depth(pool, windows->capacity)) >= 0xffff)) {
+    set_error("stream format outside the live plan's envelope");
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  P.C = *c;
+  const int spt = live_spt();
+  P.n_tiles = (windows->n_sessions + LT * spt - 1) / (LT * spt);
+  P.ticket = static_cast<uint64_t*>(scratch);
+  P.tile_state = static_cast<uint64_t*>(scratch) + LB_STRIDE;
+  cudaStream_t st = (cudaStream_t)stream;
+  PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, 8 * (LB_STRIDE * P.n_tiles + LB_STRIDE), st));
+  PASTE_CUDA_CHECK(cudaMemsetAsync(c->totals, 0, 5 * sizeof(int64_t), st));
+  if (windows->n_sessions == 0) return PASTE_OK;
+  const int G = live_gather_depth(pool, windows->capacity);
+  by_depth(G, [&](auto g) { launch_live_g<decltype(g)::value>(P, true, st); });
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}

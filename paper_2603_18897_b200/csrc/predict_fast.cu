@@ -199,30 +199,6 @@ __device__ __forceinline__ int memo_slot(uint64_t key) {
   return (int)((key * 0x9E3779B97F4A7C15ull) >> 57);  // 7 bits -> 128 slots
 }
 
-// Walk `bd`'s path (plus the fallback index) from the root of event `ev`.
-__device__ __forceinline__ int64_t walk_binding(const paste_windows& win, const int32_t* steps,
-                                                const paste_binding& bd, int64_t nb, int fails) {
-  int64_t cur = 0;
-  const int2* st = reinterpret_cast<const int2*>(steps);
-  for (int s = 0; s < bd.step_cnt && cur >= 0; ++s) {
-    const int2 k = __ldg(st + bd.step_off + s);
-    cur = step_child(win.nodes, nb, cur, k.x, k.y);
-  }
-  if (bd.kind == PASTE_X_FALLBACK) {
-    if (cur >= 0)
-      cur = bd.start_index < 0 ? -1 : step_child(win.nodes, nb, cur, 1, bd.start_index + fails);
-    for (int s = 0; s < bd.suf_cnt && cur >= 0; ++s) {
-      const int2 k = __ldg(st + bd.suf_off + s);
-      cur = step_child(win.nodes, nb, cur, k.x, k.y);
-    }
-  } else if (bd.kind == PASTE_X_FORMAT && cur >= 0) {
-    // _leaf_str: only str / number leaves fill the hole (mappings.py:197-204)
-    const int t = load_node(win.nodes, nb + cur).type();
-    if (t != PASTE_T_STR && t != PASTE_T_INT && t != PASTE_T_FLOAT) cur = -1;
-  }
-  return cur;
-}
-
 // Resolve binding `bind` (global index) against source event `ev` at age
 // `src_age`; `gt` holds the gathered tokens by age for the failure count.
 __device__ __forceinline__ int64_t resolve_fast(const paste_windows& win, const int32_t* steps,

@@ -18,12 +18,13 @@ bytes only.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
 
 from . import _native
-from ._native import AdmitDesc, PredictOut, WindowsDesc, check, ptr
+from ._native import AdmitDesc, LivePlan, PredictOut, WindowsDesc, check, ptr
 from .device_ops import DevicePool, stream_handle, to_dev
 from .packing import PredictResult, admit_tables
 
@@ -117,6 +118,35 @@ class LiveSessionTable:
         self.sformat = ef if self.lib.paste_predict_compact_supported(
             ctypes.byref(self.pool_desc), capacity, K, B, ef) else self.cformat
         self._entries = None
+        self.plan = None
+        self._build_plan()
+
+    def _build_plan(self) -> None:
+        """Compile the live plan (paste_build_live_plan: per match-table key,
+        the step's records and admit decisions) and the walk table (per
+        (binding, template node): the resolved argument node).  None when the
+        request shape is outside the plan's envelope (the step then runs the
+        general kernel)."""
+        t = self.torch
+        lib = self.lib
+        if os.environ.get("PASTE_NO_LIVE_PLAN"):
+            return
+        nbytes = lib.paste_live_plan_bytes(ctypes.byref(self.pool_desc), self.K, self.W)
+        if nbytes <= 0:
+            return
+        buf = t.empty(nbytes, dtype=t.uint8, device="cuda")
+        check(lib.paste_build_live_plan(ctypes.byref(self.pool_desc), ctypes.byref(self.adm),
+                                        self.K, self.W, ptr(buf), stream_handle()), lib)
+        walk = None
+        n_bind = len(self.dpool.image.bindings)
+        wbytes = lib.paste_live_walk_bytes(n_bind, len(self.host_nodes)) if n_bind else -1
+        if wbytes > 0:
+            walk = t.empty(wbytes // 4, dtype=t.int32, device="cuda")
+            check(lib.paste_build_live_walk(ctypes.byref(self.pool_desc), n_bind, ptr(self.nodes),
+                                            len(self.host_nodes), ptr(walk), stream_handle()), lib)
+        self._plan_bufs = (buf, walk)
+        self.plan = LivePlan(ptr(buf), self.K, self.dpool.image.max_bindings, ptr(walk),
+                             len(self.host_nodes) if walk is not None else 0)
 
     def refresh_estimates(self, estimates) -> None:
         """Re-read ``benefit_of = estimates.duration`` for every tool (the
@@ -127,6 +157,10 @@ class LiveSessionTable:
                         or [0.0], np.float64)
         self.benefit = bene
         self.adm_arrays[2].copy_(self.torch.from_numpy(bene))
+        if self.plan is not None:  # utilities / per-tool winners live in the plan
+            check(self.lib.paste_build_live_plan(ctypes.byref(self.pool_desc),
+                                                 ctypes.byref(self.adm), self.K, self.W,
+                                                 self.plan.plan, stream_handle()), self.lib)
 
     # -- state upload ---------------------------------------------------------
 
@@ -162,6 +196,12 @@ class LiveSessionTable:
                           ptr(self.nodes), ptr(self.bytes), ptr(self.refs),
                           ptr(self.new_tok if new_tok is None else new_tok), ptr(ref),
                           region * self.n, region * self.max_batch_bytes, 0, ptr(new_node))
+        if self.plan is not None:
+            check(self.lib.paste_predict_live(ctypes.byref(self.pool_desc), ctypes.byref(win),
+                                              ctypes.byref(self.adm), ctypes.byref(self.plan),
+                                              ctypes.byref(self.out_desc), stream_handle()),
+                  self.lib)
+            return
         check(self.lib.paste_predict_batch(ctypes.byref(self.pool_desc), ctypes.byref(win),
                                            ctypes.byref(self.adm), ctypes.byref(self.out_desc),
                                            stream_handle()), self.lib)
@@ -180,6 +220,14 @@ class LiveSessionTable:
                           ptr(self.nodes), ptr(self.bytes), ptr(self.refs), ptr(new_tok),
                           ptr(ref), region * self.n, region * self.max_batch_bytes, 0,
                           ptr(new_node))
+        if self.plan is not None:
+            rc = self.lib.paste_predict_live_compact(
+                ctypes.byref(self.pool_desc), ctypes.byref(win), ctypes.byref(self.adm),
+                ctypes.byref(self.plan), self.B, ctypes.byref(cdesc), ptr(scratch),
+                stream_handle())
+            if rc != _native.PASTE_ERR_UNSUPPORTED:
+                check(rc, self.lib)
+                return True
         rc = self.lib.paste_predict_compact(ctypes.byref(self.pool_desc), ctypes.byref(win),
                                             ctypes.byref(self.adm), self.K, self.B,
                                             ctypes.byref(cdesc), ptr(scratch), stream_handle())

@@ -142,7 +142,11 @@ def _live_vs_oracle(dp, n, steps, seed, policy, book, K=8, workload=None, update
     return total_preds
 
 
-def test_live_c3_pool_matches_oracle():
+@pytest.mark.parametrize("plan", [True, False])
+def test_live_c3_pool_matches_oracle(plan, monkeypatch):
+    """The live-plan kernel (default) and the general match-table kernel."""
+    if not plan:
+        monkeypatch.setenv("PASTE_NO_LIVE_PLAN", "1")
     pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
     book = EstimateBook()
     for tool, ms in (("search", 700.0), ("web_fetch", 1080.0), ("file_editor", 300.0),
@@ -165,11 +169,14 @@ def test_live_follows_estimate_updates():
     assert n_preds > 0
 
 
-def test_live_stress_pool_matches_oracle():
+@pytest.mark.parametrize("plan", [True, False])
+def test_live_stress_pool_matches_oracle(plan, monkeypatch):
     """1,000-pattern pool; the synthetic tools are renamed onto the pool's tools."""
     from paper_2603_18897_b200 import synth
     from paper_2603_18897_b200.policy import SpeculationPolicy
 
+    if not plan:
+        monkeypatch.setenv("PASTE_NO_LIVE_PLAN", "1")
     pool = stress_pool()
     dp = DevicePool(pool)
 
@@ -230,8 +237,9 @@ def test_compact_records_expand_to_the_full_records(fmt):
 
 
 @pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3", "wide_format",
-                                     "ship_bytes", "pred_stream", "pinned_inputs"])
-def test_serve_pipeline_yields_the_step_records(variant):
+                                     "ship_bytes", "pred_stream", "pinned_inputs", "no_plan",
+                                     "no_plan_pred_stream"])
+def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
     what the sequential step (K-slot records) returns: expanded records
@@ -240,6 +248,9 @@ def test_serve_pipeline_yields_the_step_records(variant):
     (PASTE_CF_ENTRY16) unless the variant turns it off."""
     from paper_2603_18897_b200.policy import SpeculationPolicy
 
+    if variant.startswith("no_plan"):  # the general fused kernel
+        monkeypatch.setenv("PASTE_NO_LIVE_PLAN", "1")
+        variant = variant[len("no_plan_"):] or "motif"
     pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
     dp = DevicePool(pool)
     n = 30_000
