@@ -257,8 +257,7 @@ def run_ours(args):
     # the serving kernel (fused predict + narrow-stream compaction) for reference
     cbuf = _compact_buffers(table)
     cdesc = _compact_desc(cbuf, table.cformat)
-    cscratch = torch.empty(lib.paste_predict_compact_scratch_bytes(n), dtype=torch.uint8,
-                           device="cuda")
+    cscratch = torch.empty(table.compact_scratch_bytes(), dtype=torch.uint8, device="cuda")
     fused = []
     for region, tok, node in staged[W_ + S_:]:
         l2_flush(flush)
@@ -279,7 +278,10 @@ def run_ours(args):
     # two batches past the timed ones keep the pipeline full at the end
     host_batches = []
     for i in range(W_ + S_ + 2):
-        b = wl.next_batch()
+        b = wl.next_batch().narrowed()  # u8 token + u16 node_base on the wire when they fit
+        if b.tok8 is not None:
+            b.tok8 = torch.from_numpy(b.tok8).pin_memory()
+            b.node16 = torch.from_numpy(b.node16.view(np.int16)).pin_memory()
         b.tok = torch.from_numpy(b.tok).pin_memory()
         b.ref = torch.from_numpy(np.ascontiguousarray(b.ref)).pin_memory()
         b.data = torch.from_numpy(b.data).pin_memory()
@@ -294,7 +296,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    h2d = sum(b.nbytes(with_data=table.ship_bytes) for b in host_batches[max(W_, 1):max(W_, 1) + S_])
+    h2d = sum(b.nbytes(with_data=table.ship_bytes, narrow8=table.narrow8)
+              for b in host_batches[max(W_, 1):max(W_, 1) + S_])
     d2h = 0
     marks = {}
     we = max(W_, 1)  # the mark before the first timed step
@@ -329,8 +332,12 @@ def run_ours(args):
                 "h2d_bytes_per_step": h2d // S_, "d2h_bytes_per_step": d2h // S_,
                 "ms_per_step": 1e3 * e2e_s / S_,
                 "records": "narrow CSR streams, format bits %d (%s)" % (
-                    table.sformat, "per-session match-table key + refs + actions"
-                    if table.sformat & 8 else "per-prediction codes + refs + actions")},
+                    table.sformat, "per-session match-table key + refs; counts and actions "
+                    "from the key's live-plan entry" if table.sformat & 16 else
+                    "per-session match-table key + refs + actions"
+                    if table.sformat & 8 else "per-prediction codes + refs + actions"),
+                "inputs": "u8 token + u16 node_base per session" if table.narrow8
+                else "i32 token + i32 node_base per session"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": committed_traffic(),
                      "kernel": "predict_fast_kernel", "algorithmic_bytes_per_launch": alg // S_,

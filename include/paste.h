@@ -154,6 +154,11 @@ typedef struct {
   /* optional narrow observe input: node_base only (byte_base = new_byte_base),
    * 4 B/session instead of the 16-B directory entry of new_ref            */
   const int32_t* new_node;
+  /* optional narrow wire form of the observe input (live-plan kernels only):
+   * token u8 (255 = LLM step) and node_base u16 (byte_base = new_byte_base);
+   * when set they replace new_tok / new_node                               */
+  const uint8_t* new_tok8;
+  const uint16_t* new_node16;
 } paste_windows;
 
 enum { PASTE_C_FULL = 0, PASTE_C_PARTIAL = 1, PASTE_C_TOOL_ONLY = 2 };
@@ -588,8 +593,15 @@ int paste_resolve(const paste_resolve_desc* d, void* stream);
  * entry, no predictions).  The predictions are the first n_pred records of
  * that entry (paste_build_match_table), so the host expands them from its
  * copy of the table; completeness follows from the pattern (no mapping =
- * TOOL_ONLY) and the arg stream (an all-ones reference = PARTIAL).        */
-enum { PASTE_CF_HDR8 = 1, PASTE_CF_PRED8 = 2, PASTE_CF_ARG16 = 4, PASTE_CF_ENTRY16 = 8 };
+ * TOOL_ONLY) and the arg stream (an all-ones reference = PARTIAL).
+ * PASTE_CF_KEYS (with PASTE_CF_ENTRY16, paste_predict_live_compact only):
+ * the hdr and act streams are not written either -- a session's counts and
+ * actions follow from its key's live-plan entry (paste_build_live_plan: the
+ * same admit decisions) and its arg stream (an unresolved reference makes
+ * the prediction PARTIAL, which admits it at the entry's partial level); the
+ * host expands them from its copy of the plan.  Streams: key + arg.       */
+enum { PASTE_CF_HDR8 = 1, PASTE_CF_PRED8 = 2, PASTE_CF_ARG16 = 4, PASTE_CF_ENTRY16 = 8,
+       PASTE_CF_KEYS = 16 };
 typedef struct {
   void* hdr;         /* [n]                                                  */
   void* pred;
@@ -658,12 +670,17 @@ int paste_build_live_walk(const paste_pool_desc* pool, int32_t n_bindings,
 int paste_predict_live(const paste_pool_desc* pool, paste_windows* windows,
                        const paste_admit_desc* admit, const paste_live_plan* plan,
                        paste_predict_out* out, void* stream);
-/* paste_predict_compact from a live plan (same streams and totals).         */
-int64_t paste_predict_live_compact_scratch_bytes(int64_t n_sessions);
+/* paste_predict_compact from a live plan (same streams and totals): the
+ * pipelined step writes the fixed-position streams and an L2-resident
+ * per-session staging record, then a scatter pass places the variable-length
+ * streams (two launches).  scratch: device memory of
+ * paste_predict_live_compact_scratch_bytes(n, K, max_bindings) bytes.     */
+int64_t paste_predict_live_compact_scratch_bytes(int64_t n_sessions, int32_t max_candidates,
+                                                 int32_t max_bindings);
 int paste_predict_live_compact(const paste_pool_desc* pool, paste_windows* windows,
                                const paste_admit_desc* admit, const paste_live_plan* plan,
                                int32_t max_bindings, paste_compact_desc* out, void* scratch,
-                               void* stream);
+                               int64_t scratch_bytes, void* stream);
 
 int64_t paste_compact_scratch_bytes(int64_t n_sessions);
 int paste_compact_records(const paste_predict_out* out, int64_t n_sessions,

@@ -57,7 +57,8 @@ class WindowsDesc(ctypes.Structure):
                 ("tok", c_void_p), ("evt", c_void_p), ("count", c_void_p),
                 ("nodes", c_void_p), ("bytes", c_void_p), ("refs", c_void_p),
                 ("new_tok", c_void_p), ("new_ref", c_void_p), ("new_evt_base", c_int64),
-                ("new_byte_base", c_int64), ("stream_end", c_void_p), ("new_node", c_void_p)]
+                ("new_byte_base", c_int64), ("stream_end", c_void_p), ("new_node", c_void_p),
+                ("new_tok8", c_void_p), ("new_node16", c_void_p)]
 
 
 class PredictOut(ctypes.Structure):
@@ -114,7 +115,7 @@ class CompactDesc(ctypes.Structure):
                 ("totals", c_void_p), ("format", c_int32), ("pad", c_int32)]
 
 
-PASTE_CF_HDR8, PASTE_CF_PRED8, PASTE_CF_ARG16, PASTE_CF_ENTRY16 = 1, 2, 4, 8
+PASTE_CF_HDR8, PASTE_CF_PRED8, PASTE_CF_ARG16, PASTE_CF_ENTRY16, PASTE_CF_KEYS = 1, 2, 4, 8, 16
 PASTE_COPY_H2D, PASTE_COPY_D2H, PASTE_COPY_D2D = 1, 2, 3
 PASTE_INGEST_MISSING, PASTE_INGEST_T_ORDER, PASTE_INGEST_EMPTY_TOOL = 0x100, 0x200, 0x400
 
@@ -211,10 +212,10 @@ EXPORTS = {
                                       c_void_p]),
     "paste_predict_live": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc), POINTER(AdmitDesc),
                                    POINTER(LivePlan), POINTER(PredictOut), c_void_p]),
-    "paste_predict_live_compact_scratch_bytes": (c_int64, [c_int64]),
+    "paste_predict_live_compact_scratch_bytes": (c_int64, [c_int64, c_int32, c_int32]),
     "paste_predict_live_compact": (c_int, [POINTER(PoolDesc), POINTER(WindowsDesc),
                                            POINTER(AdmitDesc), POINTER(LivePlan), c_int32,
-                                           POINTER(CompactDesc), c_void_p, c_void_p]),
+                                           POINTER(CompactDesc), c_void_p, c_int64, c_void_p]),
     "paste_canonical_hash": (c_int, [POINTER(HashDesc), c_void_p]),
     "paste_ingest_jsonl": (c_int, [c_char_p, c_int64, ctypes.c_double, POINTER(IngestDesc)]),
     "paste_action_keys": (c_int, [POINTER(ActionKeysDesc), c_void_p]),

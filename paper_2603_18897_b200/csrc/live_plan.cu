@@ -26,6 +26,8 @@
 // publishes its aggregate (decoupled look-back) before any binding is
 // resolved, and every record is written once at its final offset -- no
 // staging.
+#include <string.h>
+
 #include <type_traits>
 
 #include "common.cuh"
@@ -164,6 +166,12 @@ struct LiveParams {
   int admit;
   int S;                  // n_bucket_sigs
   int fast8;              // K = 8, slot-major, n * K * B < 2^31 (kslot_write8)
+  // two-pass serving form: per-session staging (session-major, L2-resident)
+  int32_t* st_key;        // [n] match-table key, -1 = none
+  uint32_t* st_cnt;       // [n] nm | n_act << 5 | n_map << 10 | n_err << 18
+  uint32_t* st_part;      // [n] PARTIAL mask
+  uint32_t* st_arg;       // [n][M] encoded argument words (stream width applied later)
+  int M;
   uint64_t* ticket;
   uint64_t* tile_state;
   int64_t n_tiles;
@@ -180,6 +188,7 @@ struct Sess {
   int32_t tk[G];           // newest tool tokens by age
   int m;
   const uint8_t* e;        // plan entry (nullptr = no predictions)
+  int32_t key;             // match-table key, -1 = none
   int nm, n_act, n_map, n_err;
 };
 
@@ -218,6 +227,11 @@ __device__ __forceinline__ void front_load(const LiveParams& P, int64_t s, Front
   f.s = s;
   if (s >= P.win.n_sessions) return;
   f.cnt = P.win.count[s];
+  if (P.win.new_tok8 != nullptr) {  // narrow wire form: u8 token, u16 node
+    f.t = P.win.new_tok8[s];
+    f.node = P.win.new_node16[s];
+    return;
+  }
   f.t = P.win.new_tok[s];
   if (P.win.new_node != nullptr)
     f.node = P.win.new_node[s];
@@ -246,25 +260,27 @@ __device__ __forceinline__ void front_observe(const LiveParams& P, const FrontIn
   const int W = P.win.capacity;
   y.s = f.s;
   y.e = nullptr;
+  y.key = -1;
   y.nm = y.n_act = y.n_map = y.n_err = 0;
   if (f.s >= n) return;
   const bool slot_major = P.win.slot_major != 0;
   y.rbase = slot_major ? f.s : f.s * W;
   y.rstride = slot_major ? n : 1;
+  const int32_t t_in = (P.win.new_tok8 != nullptr && f.t == 255) ? -1 : f.t;
   const int head = (W & (W - 1)) == 0 ? (int)(f.cnt & (W - 1))
                    : f.cnt < (1ll << 31) ? (int)((uint32_t)f.cnt % (uint32_t)W)
                                          : (int)(f.cnt % W);
   y.ev0 = (int32_t)(P.win.new_evt_base + f.s);
-  const bool narrow = P.win.new_node != nullptr;
+  const bool narrow = P.win.new_node != nullptr || P.win.new_tok8 != nullptr;
   y.node0 = narrow ? (int64_t)f.node : f.ref.node_base;
   P.win.refs[y.ev0] =
       paste_event_ref{y.node0, (narrow ? 0 : f.ref.byte_base) + P.win.new_byte_base};
-  P.win.tok[y.rbase + head * y.rstride] = f.t;
+  P.win.tok[y.rbase + head * y.rstride] = t_in;
   P.win.evt[y.rbase + head * y.rstride] = y.ev0;
   const int64_t c1 = f.cnt + 1;
   P.win.count[f.s] = c1;
   y.newest = head;
-  m.t_new = f.t;
+  m.t_new = t_in;
   m.len = (int)(c1 < W ? c1 : W);
 #pragma unroll
   for (int a = 1; a < G; ++a) {
@@ -304,6 +320,7 @@ __device__ __forceinline__ void front_key(const LiveParams& P, Sess<G>& y, const
       mult *= P.S + 1;
     }
     y.e = P.plan + (int64_t)key * P.L.stride;
+    y.key = key;
     const int2 h = *reinterpret_cast<const int2*>(y.e);
     y.nm = h.x & 0xff;
     y.n_act = (h.x >> 8) & 0xff;
@@ -617,13 +634,59 @@ __device__ __forceinline__ void live_offsets(const LiveParams& P, int64_t tile, 
   }
 }
 
+// one session's records in the narrow streams at its offsets off[4]
+template <int G>
+__device__ __forceinline__ void compact_write(const LiveParams& P, const Sess<G>& y,
+                                              const uint64_t off[4], unsigned long long& wide) {
+  const int64_t n = P.win.n_sessions;
+  const paste_compact_desc& C = P.C;
+  const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
+  const bool keys = (C.format & PASTE_CF_KEYS) != 0;
+  if (!keys) cf_hdr(C, y.s, y.nm, y.n_act);
+  uint32_t part = 0;
+  if (y.nm > 0 && y.n_map > 0) {
+    int q = 0;
+    const uint64_t oa = off[1];
+    part = live_resolve<G>(P, y, [&](int, int, int32_t ev, int64_t cur) {
+      uint32_t w = a16 ? 0xffffu : 0xffffffffu;
+      if (cur >= 0) {
+        const int64_t region =
+            n < (1ll << 31) ? (int64_t)((uint32_t)ev / (uint32_t)n) : (int64_t)ev / n;
+        if ((int64_t)ev - region * n == y.s && region < 31 && cur < (a16 ? (1ll << 11) : (1ll << 27)))
+          w = a16 ? (((uint32_t)region << 11) | (uint32_t)cur)
+                  : (((uint32_t)region << 27) | (uint32_t)cur);
+        else
+          ++wide;
+      }
+      if (a16) static_cast<uint16_t*>(C.arg)[oa + q] = (uint16_t)w;
+      else static_cast<uint32_t*>(C.arg)[oa + q] = w;
+      ++q;
+    });
+  }
+  if (C.format & PASTE_CF_ENTRY16) {
+    static_cast<uint16_t*>(C.pred)[y.s] = y.e ? (uint16_t)(y.slots >> 48) : (uint16_t)0xffffu;
+  } else if (y.nm > 0) {
+    const int32_t* pid = reinterpret_cast<const int32_t*>(y.e + P.L.off_pid);
+    const uint8_t* comp = y.e + P.L.off_comp;
+    for (int i = 0; i < y.nm; ++i)
+      cf_pred(C, off[0] + i, pid[i], ((part >> i) & 1u) ? PASTE_C_PARTIAL : comp[i]);
+  }
+  if (y.n_act > 0 && !keys) {
+    const uint16_t* act = reinterpret_cast<const uint16_t*>(y.e + P.L.off_act);
+    for (int a = 0; a < y.n_act; ++a) {
+      const uint16_t v = act[a];
+      const int slot = v & 0xff;
+      const int lv = ((part >> slot) & 1u) ? (v >> 12) & 15 : (v >> 8) & 15;
+      C.act[off[2] + a] = (uint8_t)(slot | (lv << 5));
+    }
+  }
+}
+
+// tiles claimed through a ticket (SPT sessions per thread)
 template <int G, int SPT>
 __global__ void __launch_bounds__(LT) predict_live_compact_kernel(const LiveParams P) {
   __shared__ int64_t s_tile;
   const int64_t n = P.win.n_sessions;
-  const paste_compact_desc& C = P.C;
-  const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
-  const bool entry = (C.format & PASTE_CF_ENTRY16) != 0;
   unsigned long long wide = 0;
   for (;;) {
     __syncthreads();
@@ -645,48 +708,163 @@ __global__ void __launch_bounds__(LT) predict_live_compact_kernel(const LivePara
     uint64_t off[SPT][4];
     live_offsets<SPT>(P, tile, c, off);
 #pragma unroll
-    for (int j = 0; j < SPT; ++j) {
-      const Sess<G>& y = x[j];
-      if (y.s >= n) continue;
-      cf_hdr(C, y.s, y.nm, y.n_act);
-      uint32_t part = 0;
-      if (y.nm > 0 && y.n_map > 0) {
-        int q = 0;
-        const uint64_t oa = off[j][1];
-        part = live_resolve<G>(P, y, [&](int, int, int32_t ev, int64_t cur) {
-          uint32_t w = a16 ? 0xffffu : 0xffffffffu;
-          if (cur >= 0) {
-            const int64_t region =
-                n < (1ll << 31) ? (int64_t)((uint32_t)ev / (uint32_t)n) : (int64_t)ev / n;
-            if ((int64_t)ev - region * n == y.s && region < 31 && cur < (a16 ? (1ll << 11) : (1ll << 27)))
-              w = a16 ? (((uint32_t)region << 11) | (uint32_t)cur)
-                      : (((uint32_t)region << 27) | (uint32_t)cur);
-            else
-              ++wide;
-          }
-          if (a16) static_cast<uint16_t*>(C.arg)[oa + q] = (uint16_t)w;
-          else static_cast<uint32_t*>(C.arg)[oa + q] = w;
-          ++q;
-        });
+    for (int j = 0; j < SPT; ++j)
+      if (x[j].s < n) compact_write<G>(P, x[j], off[j], wide);
+  }
+  if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(P.C.totals + 3), wide);
+}
+
+// ---- two-pass serving form ---------------------------------------------
+// Pass 1 is predict_live_kernel's pipelined step writing, per session, the
+// fixed-position streams (hdr, and the ENTRY16 key) plus a staging record
+// (key, counts, PARTIAL mask, resolved argument words) that stays in L2.
+// Pass 2 scans the counts (decoupled look-back over light tiles) and
+// scatters the variable-length streams.  The step itself thus runs without
+// any cross-CTA wait; only the light scatter does.
+template <int G>
+__device__ __forceinline__ void stage_write(const LiveParams& P, const Sess<G>& y,
+                                            unsigned long long& wide) {
+  const int64_t n = P.win.n_sessions;
+  const paste_compact_desc& C = P.C;
+  const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
+  uint32_t part = 0;
+  if (y.nm > 0 && y.n_map > 0) {
+    int q = 0;
+    uint32_t* sa = P.st_arg + y.s * P.M;
+    part = live_resolve<G>(P, y, [&](int, int, int32_t ev, int64_t cur) {
+      uint32_t w = a16 ? 0xffffu : 0xffffffffu;
+      if (cur >= 0) {
+        const int64_t region =
+            n < (1ll << 31) ? (int64_t)((uint32_t)ev / (uint32_t)n) : (int64_t)ev / n;
+        if ((int64_t)ev - region * n == y.s && region < 31 && cur < (a16 ? (1ll << 11) : (1ll << 27)))
+          w = a16 ? (((uint32_t)region << 11) | (uint32_t)cur)
+                  : (((uint32_t)region << 27) | (uint32_t)cur);
+        else
+          ++wide;
       }
-      if (entry) {
-        static_cast<uint16_t*>(C.pred)[y.s] = y.e ? (uint16_t)(y.slots >> 48) : (uint16_t)0xffffu;
-      } else if (y.nm > 0) {
-        const int32_t* pid = reinterpret_cast<const int32_t*>(y.e + P.L.off_pid);
-        const uint8_t* comp = y.e + P.L.off_comp;
-        for (int i = 0; i < y.nm; ++i)
+      sa[q++] = w;
+    });
+  }
+  if (!(C.format & PASTE_CF_KEYS)) cf_hdr(C, y.s, y.nm, y.n_act);
+  if (C.format & PASTE_CF_ENTRY16)
+    static_cast<uint16_t*>(C.pred)[y.s] = y.key >= 0 ? (uint16_t)y.key : (uint16_t)0xffffu;
+  P.st_key[y.s] = y.key;
+  P.st_cnt[y.s] = (uint32_t)y.nm | ((uint32_t)y.n_act << 5) | ((uint32_t)y.n_map << 10) |
+                  ((uint32_t)y.n_err << 18);
+  P.st_part[y.s] = part;
+}
+
+template <int G>
+__global__ void __launch_bounds__(LT) predict_live_stage_kernel(const LiveParams P) {
+  const int64_t n = P.win.n_sessions;
+  const int64_t stride = (int64_t)gridDim.x * LT;
+  const int64_t s0 = (int64_t)blockIdx.x * LT + threadIdx.x;
+  unsigned long long wide = 0;
+  FrontIn f1, f2;
+  Sess<G> y0, y1;
+  FrontMid<G> m0, m1;
+  front_load(P, s0, f1);
+  front_load(P, s0 + stride, f2);
+  front_observe<G>(P, f1, y1, m1);
+  for (int64_t s = s0; s < n; s += stride) {
+    y0 = y1;
+    m0 = m1;
+    f1 = f2;
+    front_load(P, s + 2 * stride, f2);
+    front_observe<G>(P, f1, y1, m1);
+    front_key<G, false>(P, y0, m0);
+    stage_write<G>(P, y0, wide);
+  }
+  if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(P.C.totals + 3), wide);
+}
+
+constexpr int SCAT_SPT = 4;
+
+__global__ void __launch_bounds__(LT) live_scatter_kernel(const LiveParams P) {
+  __shared__ int64_t s_tile;
+  const int64_t n = P.win.n_sessions;
+  const paste_compact_desc& C = P.C;
+  const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
+  const bool entry = (C.format & PASTE_CF_ENTRY16) != 0;
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0)
+      s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(P.ticket), 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= P.n_tiles) break;
+    int64_t sj[SCAT_SPT];
+    uint32_t cj[SCAT_SPT];
+    int c[SCAT_SPT][4];
+#pragma unroll
+    for (int j = 0; j < SCAT_SPT; ++j) {
+      sj[j] = tile * LT * SCAT_SPT + j * LT + threadIdx.x;
+      cj[j] = sj[j] < n ? P.st_cnt[sj[j]] : 0u;
+      c[j][0] = cj[j] & 31;
+      c[j][1] = (cj[j] >> 10) & 0xff;
+      c[j][2] = (cj[j] >> 5) & 31;
+      c[j][3] = (int)(cj[j] >> 18);
+    }
+    uint64_t off[SCAT_SPT][4];
+    live_offsets<SCAT_SPT>(P, tile, c, off);
+#pragma unroll
+    for (int j = 0; j < SCAT_SPT; ++j) {
+      if (sj[j] >= n || (c[j][0] == 0 && c[j][2] == 0)) continue;
+      if ((C.format & PASTE_CF_KEYS) && c[j][1] == 0) continue;
+      const int64_t s = sj[j];
+      const uint32_t part = c[j][1] > 0 || c[j][2] > 0 ? P.st_part[s] : 0u;
+      const uint32_t* sa = P.st_arg + s * P.M;
+      for (int q = 0; q < c[j][1]; ++q) {
+        const uint32_t w = sa[q];
+        if (a16) static_cast<uint16_t*>(C.arg)[off[j][1] + q] = (uint16_t)w;
+        else static_cast<uint32_t*>(C.arg)[off[j][1] + q] = w;
+      }
+      const uint8_t* e = P.plan + (int64_t)P.st_key[s] * P.L.stride;
+      if (!entry) {
+        const int32_t* pid = reinterpret_cast<const int32_t*>(e + P.L.off_pid);
+        const uint8_t* comp = e + P.L.off_comp;
+        for (int i = 0; i < c[j][0]; ++i)
           cf_pred(C, off[j][0] + i, pid[i], ((part >> i) & 1u) ? PASTE_C_PARTIAL : comp[i]);
       }
-      if (y.n_act > 0) {
-        const uint16_t* act = reinterpret_cast<const uint16_t*>(y.e + P.L.off_act);
-        for (int a = 0; a < y.n_act; ++a) {
-          const uint16_t v = act[a];
-          const int slot = v & 0xff;
-          const int lv = ((part >> slot) & 1u) ? (v >> 12) & 15 : (v >> 8) & 15;
-          C.act[off[j][2] + a] = (uint8_t)(slot | (lv << 5));
-        }
+      if (C.format & PASTE_CF_KEYS) continue;  // actions follow from the key
+      const uint16_t* act = reinterpret_cast<const uint16_t*>(e + P.L.off_act);
+      for (int a = 0; a < c[j][2]; ++a) {
+        const uint16_t v = act[a];
+        const int slot = v & 0xff;
+        const int lv = ((part >> slot) & 1u) ? (v >> 12) & 15 : (v >> 8) & 15;
+        C.act[off[j][2] + a] = (uint8_t)(slot | (lv << 5));
       }
     }
+  }
+}
+
+// Static tiles (tile = CTA + round * grid, every CTA resident, so each
+// tile's predecessors are running or done) and the same three-round software
+// pipeline as predict_live_kernel: round r+2's inputs and round r+1's older
+// ring slots load while round r is keyed, scanned and written.
+template <int G>
+__global__ void __launch_bounds__(LT) predict_live_compact_pipe_kernel(const LiveParams P) {
+  const int64_t n = P.win.n_sessions;
+  const int64_t G64 = gridDim.x;
+  unsigned long long wide = 0;
+  const int64_t t0 = blockIdx.x;
+  FrontIn f1, f2;
+  Sess<G> y0, y1;
+  FrontMid<G> m0, m1;
+  front_load(P, t0 * LT + threadIdx.x, f1);
+  front_load(P, (t0 + G64) * LT + threadIdx.x, f2);
+  front_observe<G>(P, f1, y1, m1);
+  for (int64_t tile = t0; tile < P.n_tiles; tile += G64) {
+    y0 = y1;
+    m0 = m1;
+    f1 = f2;
+    front_load(P, (tile + 2 * G64) * LT + threadIdx.x, f2);
+    front_observe<G>(P, f1, y1, m1);
+    front_key<G, true>(P, y0, m0);
+    int c[1][4] = {{y0.nm, y0.n_map, y0.n_act, y0.n_err}};
+    uint64_t off[1][4];
+    live_offsets<1>(P, tile, c, off);
+    if (y0.s < n) compact_write<G>(P, y0, off[0], wide);
   }
   if (wide) atomicAdd(reinterpret_cast<unsigned long long*>(P.C.totals + 3), wide);
 }
@@ -694,6 +872,8 @@ __global__ void __launch_bounds__(LT) predict_live_compact_kernel(const LivePara
 }  // namespace paste
 
 using namespace paste;
+
+static int live_mode();
 
 static int live_gather_depth(const paste_pool_desc* pool, int W) {
   const int g = pool->relation == PASTE_REL_ANCHORED ? pool->k : pool->max_ctx;
@@ -765,30 +945,41 @@ extern "C" int paste_build_live_walk(const paste_pool_desc* pool, int32_t n_bind
   return PASTE_OK;
 }
 
+static bool live_ticket() {
+  static int t = -1;
+  if (t < 0) t = getenv("PASTE_LIVE_TICKET") != nullptr ? 1 : 0;
+  return t == 1;
+}
+
 template <int G, int SPT>
 static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
   static int sms = 0;
-  static int occ[2] = {0, 0};
+  static int occ[3] = {0, 0, 0};
   if (sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  int& o = occ[compact ? 1 : 0];
+  const int which = !compact ? 0 : live_mode() == 1 ? 1 : 2;
+  int& o = occ[which];
   if (o == 0) {
-    if (compact)
+    if (which == 0)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G>, LT, 0);
+    else if (which == 1)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_compact_kernel<G, SPT>, LT, 0);
     else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G>, LT, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_compact_pipe_kernel<G>, LT, 0);
     if (o < 1) o = 1;
   }
-  const int spt = compact ? SPT : 1;
+  const int spt = which == 1 ? SPT : 1;
   const int64_t groups = (P.win.n_sessions + LT * spt - 1) / (LT * spt);
   const int64_t grid = groups < (int64_t)sms * o ? groups : (int64_t)sms * o;
-  if (compact)
+  if (which == 0)
+    predict_live_kernel<G><<<(unsigned)grid, LT, 0, st>>>(P);
+  else if (which == 1)
     predict_live_compact_kernel<G, SPT><<<(unsigned)grid, LT, 0, st>>>(P);
   else
-    predict_live_kernel<G><<<(unsigned)grid, LT, 0, st>>>(P);
+    predict_live_compact_pipe_kernel<G><<<(unsigned)grid, LT, 0, st>>>(P);
 }
 
 static int live_spt() {
@@ -813,7 +1004,8 @@ static void launch_live_g(const LiveParams& P, bool compact, cudaStream_t st) {
 static int live_prepare(const paste_pool_desc* pool, paste_windows* w, const paste_admit_desc* adm,
                         const paste_live_plan* plan, int K, LiveParams& P) {
   PASTE_REQUIRE(pool && w && adm && plan && plan->plan, "null argument");
-  PASTE_REQUIRE(w->new_tok != nullptr && (w->new_ref || w->new_node),
+  PASTE_REQUIRE((w->new_tok != nullptr && (w->new_ref || w->new_node)) ||
+                    (w->new_tok8 != nullptr && w->new_node16 != nullptr),
                 "the live kernel observes one new event per session");
   PASTE_REQUIRE(!w->stream_end, "stream-mode windows are not live sessions");
   PASTE_REQUIRE(w->capacity >= 1 && w->capacity <= 16, "live plan needs window capacity <= 16");
@@ -864,15 +1056,56 @@ extern "C" int paste_predict_live(const paste_pool_desc* pool, paste_windows* wi
   return PASTE_OK;
 }
 
-extern "C" int64_t paste_predict_live_compact_scratch_bytes(int64_t n_sessions) {
-  const int64_t tiles = (n_sessions + LT - 1) / LT;  // SPT >= 1
-  return 8 * (LB_STRIDE * tiles + LB_STRIDE);
+static int64_t live_state_bytes(int64_t n) {
+  const int64_t tiles = (n + LT - 1) / LT;  // the most tiles any mode uses
+  return (8 * (LB_STRIDE * tiles + LB_STRIDE) + 255) / 256 * 256;
+}
+
+extern "C" int64_t paste_predict_live_compact_scratch_bytes(int64_t n_sessions,
+                                                            int32_t max_candidates,
+                                                            int32_t max_bindings) {
+  const int64_t M = (int64_t)max_candidates * (max_bindings > 0 ? max_bindings : 1);
+  const int64_t n = n_sessions;
+  return live_state_bytes(n) + 3 * ((4 * n + 255) / 256 * 256) + (4 * n * M + 255) / 256 * 256;
+}
+
+static int live_mode_impl() {  // 0 two-pass (default), 1 ticket tiles, 2 pipelined static tiles
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("PASTE_LIVE_MODE");
+    m = !e ? 0 : !strcmp(e, "ticket") ? 1 : !strcmp(e, "pipe") ? 2 : 0;
+    if (live_ticket()) m = 1;
+  }
+  return m;
+}
+
+static int live_mode() { return live_mode_impl(); }
+
+template <int G>
+static void launch_two_pass(const LiveParams& P, cudaStream_t st) {
+  static int sms = 0, o1 = 0, o2 = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, predict_live_stage_kernel<G>, LT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, live_scatter_kernel, LT, 0);
+    if (o1 < 1) o1 = 1;
+    if (o2 < 1) o2 = 1;
+  }
+  const int64_t n = P.win.n_sessions;
+  const int64_t g1 = (n + LT - 1) / LT;
+  predict_live_stage_kernel<G><<<(unsigned)(g1 < (int64_t)sms * o1 ? g1 : (int64_t)sms * o1), LT,
+                                 0, st>>>(P);
+  const int64_t g2 = P.n_tiles < (int64_t)sms * o2 ? P.n_tiles : (int64_t)sms * o2;
+  live_scatter_kernel<<<(unsigned)g2, LT, 0, st>>>(P);
 }
 
 extern "C" int paste_predict_live_compact(const paste_pool_desc* pool, paste_windows* windows,
                                           const paste_admit_desc* admit,
                                           const paste_live_plan* plan, int32_t max_bindings,
-                                          paste_compact_desc* c, void* scratch, void* stream) {
+                                          paste_compact_desc* c, void* scratch,
+                                          int64_t scratch_bytes, void* stream) {
   reset_launches();
   PASTE_REQUIRE(c != nullptr && scratch != nullptr, "null argument");
   PASTE_REQUIRE(max_bindings >= pool->max_bindings, "max_bindings below pool maximum");
@@ -883,22 +1116,39 @@ extern "C" int paste_predict_live_compact(const paste_pool_desc* pool, paste_win
   if (((c->format & PASTE_CF_HDR8) && K > 15) ||
       ((c->format & PASTE_CF_PRED8) && pool->n_patterns > 64) || pool->n_patterns > (1 << 14) ||
       ((c->format & PASTE_CF_ENTRY16) &&
-       live_keys(pool, live_gather_depth(pool, windows->capacity)) >= 0xffff)) {
+       live_keys(pool, live_gather_depth(pool, windows->capacity)) >= 0xffff) ||
+      ((c->format & PASTE_CF_KEYS) && !(c->format & PASTE_CF_ENTRY16))) {
     set_error("stream format outside the live plan's envelope");
     return PASTE_ERR_UNSUPPORTED;
   }
+  const int64_t n = windows->n_sessions;
+  const int64_t need = paste_predict_live_compact_scratch_bytes(n, K, max_bindings);
+  PASTE_REQUIRE(scratch_bytes >= need, "scratch too small (%lld bytes)", (long long)need);
   P.C = *c;
-  const int spt = live_spt();
-  P.n_tiles = (windows->n_sessions + LT * spt - 1) / (LT * spt);
+  const int mode = live_mode();
+  const int spt = mode == 1 ? live_spt() : mode == 0 ? SCAT_SPT : 1;
+  P.n_tiles = (n + LT * spt - 1) / (LT * spt);
   P.ticket = static_cast<uint64_t*>(scratch);
   P.tile_state = static_cast<uint64_t*>(scratch) + LB_STRIDE;
+  uint8_t* stg = static_cast<uint8_t*>(scratch) + live_state_bytes(n);
+  const int64_t a4 = (4 * n + 255) / 256 * 256;
+  P.st_key = reinterpret_cast<int32_t*>(stg);
+  P.st_cnt = reinterpret_cast<uint32_t*>(stg + a4);
+  P.st_part = reinterpret_cast<uint32_t*>(stg + 2 * a4);
+  P.st_arg = reinterpret_cast<uint32_t*>(stg + 3 * a4);
+  P.M = K * (max_bindings > 0 ? max_bindings : 1);
   cudaStream_t st = (cudaStream_t)stream;
   PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, 8 * (LB_STRIDE * P.n_tiles + LB_STRIDE), st));
   PASTE_CUDA_CHECK(cudaMemsetAsync(c->totals, 0, 5 * sizeof(int64_t), st));
-  if (windows->n_sessions == 0) return PASTE_OK;
+  if (n == 0) return PASTE_OK;
   const int G = live_gather_depth(pool, windows->capacity);
-  by_depth(G, [&](auto g) { launch_live_g<decltype(g)::value>(P, true, st); });
-  count_launch();
+  if (mode == 0) {
+    by_depth(G, [&](auto g) { launch_two_pass<decltype(g)::value>(P, st); });
+    count_launch(2);
+  } else {
+    by_depth(G, [&](auto g) { launch_live_g<decltype(g)::value>(P, true, st); });
+    count_launch();
+  }
   PASTE_CUDA_CHECK(cudaGetLastError());
   return PASTE_OK;
 }

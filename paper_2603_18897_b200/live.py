@@ -38,16 +38,31 @@ class EventBatch:
     ref: object   # i64[n, 2]
     data: object  # u8[bytes]
     node: object = None  # optional i32[n]: node_base only (the narrow wire form)
+    tok8: object = None    # optional u8[n]: token, 255 = LLM step (the 3-byte wire form)
+    node16: object = None  # optional u16[n]: node_base
 
-    def wire(self, ship_bytes: bool) -> tuple:
+    def narrowed(self) -> "EventBatch":
+        """The 3-byte wire form (u8 token + u16 node_base) alongside the
+        others, when the values fit (signature ids < 255, node bases < 2^16)."""
+        tok = np.asarray(self.tok)
+        node = np.asarray(self.node if self.node is not None else np.asarray(self.ref)[:, 0])
+        if tok.size and (tok.max() >= 255 or node.max() >= (1 << 16) or node.min() < 0):
+            return self
+        return EventBatch(self.tok, self.ref, self.data, self.node,
+                          np.where(tok < 0, 255, tok).astype(np.uint8),
+                          node.astype(np.uint16))
+
+    def wire(self, ship_bytes: bool, narrow8: bool = False) -> tuple:
         """The arrays a step copies host -> device."""
         if ship_bytes:
             return (self.tok, self.ref, self.data)
+        if narrow8 and self.tok8 is not None:
+            return (self.tok8, self.node16)
         return (self.tok, self.node) if self.node is not None else (self.tok, self.ref)
 
-    def nbytes(self, with_data: bool = True) -> int:
+    def nbytes(self, with_data: bool = True, narrow8: bool = False) -> int:
         return sum(int(x.nbytes) if isinstance(x, np.ndarray) else x.numel() * x.element_size()
-                   for x in self.wire(with_data))
+                   for x in self.wire(with_data, narrow8))
 
 
 class LiveSessionTable:
@@ -119,7 +134,17 @@ class LiveSessionTable:
             ctypes.byref(self.pool_desc), capacity, K, B, ef) else self.cformat
         self._entries = None
         self.plan = None
+        self._plan_host = None
         self._build_plan()
+        # the 3-byte observe input and the key + argument serving streams
+        # need the live-plan kernels
+        self.narrow8 = (self.plan is not None and not ship_bytes and len(nodes) < (1 << 16)
+                        and 2 * len(dpool.sigs) < 255)
+        self.new_tok8 = torch.zeros(n, dtype=torch.uint8, device=dev)
+        self.new_node16 = torch.zeros(n, dtype=torch.int16, device=dev)
+        self.staged8 = False
+        if self.plan is not None and self.sformat & _native.PASTE_CF_ENTRY16:
+            self.sformat |= _native.PASTE_CF_KEYS
 
     def _build_plan(self) -> None:
         """Compile the live plan (paste_build_live_plan: per match-table key,
@@ -174,6 +199,12 @@ class LiveSessionTable:
         tok = batch.tok if isinstance(batch.tok, t.Tensor) else t.from_numpy(batch.tok)
         ref = batch.ref if isinstance(batch.ref, t.Tensor) else t.from_numpy(batch.ref)
         data = batch.data if isinstance(batch.data, t.Tensor) else t.from_numpy(batch.data)
+        self.staged8 = self.narrow8 and batch.tok8 is not None
+        if self.staged8:
+            for d, x in ((self.new_tok8, batch.tok8), (self.new_node16, batch.node16)):
+                x = x if isinstance(x, t.Tensor) else t.from_numpy(np.ascontiguousarray(x))
+                d.copy_(x.reshape(-1).view(d.dtype), non_blocking=non_blocking)
+            return
         self.new_tok.copy_(tok.reshape(-1), non_blocking=non_blocking)
         self.narrow = batch.node is not None and not self.ship_bytes
         if self.narrow:  # node_base only: 8 B/session on the wire with the token
@@ -189,6 +220,7 @@ class LiveSessionTable:
 
     def launch(self, region: int, new_tok=None, new_ref=None, new_node=None) -> None:
         """observe (new event per session) + predict + admit, one kernel."""
+        staged8 = new_tok is None and new_ref is None and new_node is None and self.staged8
         if new_tok is None and new_ref is None and new_node is None and self.narrow:
             new_node = self.new_node
         ref = None if new_node is not None else (self.new_ref if new_ref is None else new_ref)
@@ -196,6 +228,9 @@ class LiveSessionTable:
                           ptr(self.nodes), ptr(self.bytes), ptr(self.refs),
                           ptr(self.new_tok if new_tok is None else new_tok), ptr(ref),
                           region * self.n, region * self.max_batch_bytes, 0, ptr(new_node))
+        if staged8:
+            win.new_tok, win.new_ref, win.new_node = None, None, None
+            win.new_tok8, win.new_node16 = ptr(self.new_tok8), ptr(self.new_node16)
         if self.plan is not None:
             check(self.lib.paste_predict_live(ctypes.byref(self.pool_desc), ctypes.byref(win),
                                               ctypes.byref(self.adm), ctypes.byref(self.plan),
@@ -205,6 +240,13 @@ class LiveSessionTable:
         check(self.lib.paste_predict_batch(ctypes.byref(self.pool_desc), ctypes.byref(win),
                                            ctypes.byref(self.adm), ctypes.byref(self.out_desc),
                                            stream_handle()), self.lib)
+
+    def compact_scratch_bytes(self) -> int:
+        """Scratch for launch_compact (either serving kernel) and the
+        compaction kernel."""
+        return max(self.lib.paste_compact_scratch_bytes(self.n),
+                   self.lib.paste_predict_compact_scratch_bytes(self.n),
+                   self.lib.paste_predict_live_compact_scratch_bytes(self.n, self.K, self.B))
 
     def launch_compact(self, region: int, cdesc, scratch, new_tok=None, new_node=None,
                        new_ref=None) -> bool:
@@ -224,7 +266,7 @@ class LiveSessionTable:
             rc = self.lib.paste_predict_live_compact(
                 ctypes.byref(self.pool_desc), ctypes.byref(win), ctypes.byref(self.adm),
                 ctypes.byref(self.plan), self.B, ctypes.byref(cdesc), ptr(scratch),
-                stream_handle())
+                scratch.numel(), stream_handle())
             if rc != _native.PASTE_ERR_UNSUPPORTED:
                 check(rc, self.lib)
                 return True
@@ -286,6 +328,23 @@ class LiveSessionTable:
             self._entries = (n_match, recs[:, :, 0].copy())
         return self._entries
 
+    def plan_host(self):
+        """Host copy of the live plan for expanding PASTE_CF_KEYS streams:
+        per key (n_pred, n_act, action codes [keys, K] = slot | level if
+        complete << 8 | level if PARTIAL << 12)."""
+        if self._plan_host is None:
+            buf = self._plan_bufs[0].cpu().numpy()
+            K, M = self.K, self.K * max(self.dpool.image.max_bindings, 1)
+            al = lambda x, a: (x + a - 1) // a * a  # noqa: E731  (live_plan.cu plan_layout)
+            off_comp = 16 + 4 * K
+            off_act = al(off_comp + K, 16)
+            off_util = al(off_act + 2 * K, 8)
+            stride = al(off_util + 8 * K + 8 * M, 16)
+            rows = buf.reshape(-1, stride)
+            self._plan_host = (rows[:, 0].astype(np.int64), rows[:, 1].astype(np.int64),
+                               rows[:, off_act:off_act + 2 * K].copy().view(np.uint16))
+        return self._plan_host
+
     def output_nbytes(self) -> int:
         return sum(v.numel() * v.element_size() for v in self.out.values())
 
@@ -327,6 +386,7 @@ class CompactRecords:
     act: np.ndarray    # u8: slot | level << 5
     fmt: int = 0
     entries: tuple | None = None  # (n_match, pattern ids [keys, K]) for PASTE_CF_ENTRY16
+    plan: tuple | None = None     # LiveSessionTable.plan_host() for PASTE_CF_KEYS
 
     @property
     def nbytes(self) -> int:
@@ -337,10 +397,18 @@ class CompactRecords:
         Utilities are p(pattern) * benefit(target tool): the same IEEE
         multiply the device did (policy.py:224-232)."""
         K, B = self.K, self.B
-        hdr = self.hdr.astype(np.int64)
-        hshift = 4 if self.fmt & _native.PASTE_CF_HDR8 else 8
-        n_pred, n_act = hdr & ((1 << hshift) - 1), hdr >> hshift
-        n = len(hdr)
+        keys = bool(self.fmt & _native.PASTE_CF_KEYS)
+        if keys:  # counts from the key's live-plan entry
+            key = self.pred.astype(np.int64)
+            valid = key != 0xFFFF
+            kk = np.where(valid, key, 0)
+            n_pred = np.where(valid, self.plan[0][kk], 0)
+            n_act = np.where(valid, self.plan[1][kk], 0)
+        else:
+            hdr = self.hdr.astype(np.int64)
+            hshift = 4 if self.fmt & _native.PASTE_CF_HDR8 else 8
+            n_pred, n_act = hdr & ((1 << hshift) - 1), hdr >> hshift
+        n = len(n_pred)
         res = PredictResult.empty(n, K, B, True)
         res.n_pred[:] = n_pred
         res.n_act[:] = n_act
@@ -362,6 +430,8 @@ class CompactRecords:
             comp = np.where(mapped, np.where(partial, 1, 0), 2)
             res.pred_pat[sess * K + slot] = pid
             res.pred_comp[sess * K + slot] = comp.astype(np.uint8)
+            part_at = np.zeros(n * K, bool)
+            part_at[sess * K + slot] = mapped & partial
         else:
             pshift = 6 if self.fmt & _native.PASTE_CF_PRED8 else 14
             pred = self.pred.astype(np.int64)
@@ -377,9 +447,16 @@ class CompactRecords:
             unresolved, -1, (ev << 32) | (a & ((1 << ashift) - 1)))
         a_sess = np.repeat(np.arange(n), n_act)
         a_slot = np.arange(len(a_sess)) - np.repeat(np.cumsum(n_act) - n_act, n_act)
-        a_pred = (self.act & 31).astype(np.int64)
-        res.act_pred[a_sess * K + a_slot] = a_pred
-        res.act_level[a_sess * K + a_slot] = self.act >> 5
+        if keys:  # the entry's admit decisions; PARTIAL predictions at their partial level
+            code = self.plan[2][kk[a_sess], a_slot].astype(np.int64)
+            a_pred = code & 0xFF
+            lv = np.where(part_at[a_sess * K + a_pred], (code >> 12) & 15, (code >> 8) & 15)
+            res.act_pred[a_sess * K + a_slot] = a_pred
+            res.act_level[a_sess * K + a_slot] = lv.astype(np.uint8)
+        else:
+            a_pred = (self.act & 31).astype(np.int64)
+            res.act_pred[a_sess * K + a_slot] = a_pred
+            res.act_level[a_sess * K + a_slot] = self.act >> 5
         a_pid = res.pred_pat[a_sess * K + a_pred]
         res.act_util[a_sess * K + a_slot] = (patterns["p"][a_pid]
                                              * benefit[patterns["target_tool"][a_pid]])
@@ -487,8 +564,7 @@ def _serve_state(table, depth: int, fmt: int) -> dict:
     return {
         "fmt": fmt, "bufs": bufs, "descs": [_compact_desc(c, fmt) for c in bufs],
         "pinned": pinned, "sets": sets,
-        "scratch": [t.empty(max(table.lib.paste_compact_scratch_bytes(table.n),
-                                table.lib.paste_predict_compact_scratch_bytes(table.n)),
+        "scratch": [t.empty(table.compact_scratch_bytes(),
                             dtype=t.uint8, device="cuda") for _ in range(depth)],
         "copy": t.cuda.Stream(), "tot": t.cuda.Stream(), "up": t.cuda.Stream(),
         "free": [None] * depth, "in_free": [None] * depth,
@@ -496,7 +572,9 @@ def _serve_state(table, depth: int, fmt: int) -> dict:
         "ev_tot": [t.cuda.Event() for _ in range(depth)],
         "ev_up": [t.cuda.Event() for _ in range(depth)],
         "wins": {},
-        "in": [{"tok": t.zeros(table.n, dtype=t.int32, device="cuda"),
+        "in": [{"tok8": t.zeros(table.n, dtype=t.uint8, device="cuda"),
+                "node16": t.zeros(table.n, dtype=t.int16, device="cuda"),
+                "tok": t.zeros(table.n, dtype=t.int32, device="cuda"),
                 "node": t.zeros(table.n, dtype=t.int32, device="cuda"),
                 "ref": t.zeros(2 * table.n, dtype=t.int64, device="cuda")}
                for _ in range(depth)]}
@@ -530,6 +608,7 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
     comp, copy, tot, up = t.cuda.current_stream(), sv["copy"], sv["tot"], sv["up"]
     comp_h, copy_h, tot_h, up_h = (s.cuda_stream for s in (comp, copy, tot, up))
     entries = table.entries() if fmt & _native.PASTE_CF_ENTRY16 else None
+    plan = table.plan_host() if fmt & _native.PASTE_CF_KEYS else None
     n = table.n
     tot_q, copy_q = deque(), deque()
     H2D, D2H = _native.PASTE_COPY_H2D, _native.PASTE_COPY_D2H
@@ -541,7 +620,9 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         if wide:
             raise _native.PasteError(f"{wide} argument refs outside the live table's event "
                                      "form: use fetch()")
-        sizes = (n, n if fmt & _native.PASTE_CF_ENTRY16 else P, A, Q)
+        keys = bool(fmt & _native.PASTE_CF_KEYS)  # counts / actions follow from the key
+        sizes = (0 if keys else n, n if fmt & _native.PASTE_CF_ENTRY16 else P, A,
+                 0 if keys else Q)
         nb = st["bytes"]
         for j in range(4):
             nb[j] = sizes[j] * st["esize"][j]
@@ -556,7 +637,7 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         done.synchronize()
         v = sv["sets"][k]["views"]
         rec = CompactRecords(table.K, table.B, v["hdr"][:sizes[0]], v["pred"][:sizes[1]],
-                             v["arg"][:sizes[2]], v["act"][:sizes[3]], fmt, entries)
+                             v["arg"][:sizes[2]], v["act"][:sizes[3]], fmt, entries, plan)
         rec.downloaded = done  # device event: this step's records are on the host
         return rec
 
@@ -569,7 +650,11 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
             up.wait_event(sv["in_free"][k])
         st = sv["in"][k]
         narrow = b.node is not None and not table.ship_bytes
-        wire = [(st["tok"], b.tok), (st["node"], b.node) if narrow else (st["ref"], b.ref)]
+        if table.narrow8 and table.serve_fused and b.tok8 is not None:  # 3 B per session
+            narrow = 8
+            wire = [(st["tok8"], b.tok8), (st["node16"], b.node16)]
+        else:
+            wire = [(st["tok"], b.tok), (st["node"], b.node) if narrow else (st["ref"], b.ref)]
         if all(isinstance(x, t.Tensor) and not x.is_cuda and x.is_pinned() for _, x in wire):
             nw = len(wire)
             check(lib.paste_memcpy_batch(
@@ -581,7 +666,7 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
             with t.cuda.stream(up):
                 for d, x in wire:
                     x = x if isinstance(x, t.Tensor) else t.from_numpy(np.ascontiguousarray(x))
-                    d.copy_(x.reshape(-1), non_blocking=True)
+                    d.copy_(x.reshape(-1).view(d.dtype), non_blocking=True)
         if table.ship_bytes:
             with t.cuda.stream(up):
                 data = b.data if isinstance(b.data, t.Tensor) else t.from_numpy(b.data)
@@ -600,7 +685,19 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
                               None if narrow else ptr(st["ref"]), region * n,
                               region * table.max_batch_bytes, 0,
                               ptr(st["node"]) if narrow else None)
+            if narrow == 8:
+                win.new_tok, win.new_node = None, None
+                win.new_tok8, win.new_node16 = ptr(st["tok8"]), ptr(st["node16"])
             sv["wins"][key] = win
+        if table.plan is not None:
+            scr = sv["scratch"][k]
+            rc = lib.paste_predict_live_compact(ctypes.byref(table.pool_desc), ctypes.byref(win),
+                                                ctypes.byref(table.adm), ctypes.byref(table.plan),
+                                                table.B, ctypes.byref(sv["descs"][k]), ptr(scr),
+                                                scr.numel(), comp_h)
+            if rc != _native.PASTE_ERR_UNSUPPORTED:
+                check(rc, lib)
+                return True
         rc = lib.paste_predict_compact(ctypes.byref(table.pool_desc), ctypes.byref(win),
                                        ctypes.byref(table.adm), table.K, table.B,
                                        ctypes.byref(sv["descs"][k]), ptr(sv["scratch"][k]),

@@ -14,7 +14,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
 
 from oracle import bridge  # noqa: E402
 from paper_2603_18897_b200 import admit  # noqa: E402
-from paper_2603_18897_b200._native import PASTE_CF_ENTRY16  # noqa: E402
+from paper_2603_18897_b200._native import PASTE_CF_ENTRY16, PASTE_CF_KEYS  # noqa: E402
 from paper_2603_18897_b200.device_ops import DevicePool  # noqa: E402
 from paper_2603_18897_b200.live import LiveSessionTable  # noqa: E402
 from paper_2603_18897_b200.mining import load_pool  # noqa: E402
@@ -238,7 +238,8 @@ def test_compact_records_expand_to_the_full_records(fmt):
 
 @pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3", "wide_format",
                                      "ship_bytes", "pred_stream", "pinned_inputs", "no_plan",
-                                     "no_plan_pred_stream"])
+                                     "no_plan_pred_stream", "narrow8", "narrow8_pinned",
+                                     "no_keys"])
 def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
@@ -280,6 +281,8 @@ def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
         pip.sformat = pip.cformat
     else:
         assert pip.sformat & PASTE_CF_ENTRY16
+    if variant == "no_keys":
+        pip.sformat &= ~PASTE_CF_KEYS
     steps = 20
     expect, full = [], []
     for _ in range(steps):
@@ -290,10 +293,16 @@ def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     def feed():
         for _ in range(steps):
             b = wl_b.next_batch()
-            if variant == "pinned_inputs":  # the batched-copy upload path
+            if variant.startswith("narrow8"):  # u8 token + u16 node on the wire
+                b = b.narrowed()
+                assert b.tok8 is not None and pip.narrow8
+            if variant in ("pinned_inputs", "narrow8_pinned"):  # the batched-copy upload path
                 b.tok = torch.from_numpy(b.tok).pin_memory()
                 b.node = torch.from_numpy(b.node).pin_memory()
                 b.ref = torch.from_numpy(np.ascontiguousarray(b.ref)).pin_memory()
+                if b.tok8 is not None:
+                    b.tok8 = torch.from_numpy(b.tok8).pin_memory()
+                    b.node16 = torch.from_numpy(b.node16.view(np.int16)).pin_memory()
             yield b
 
     got = []
@@ -304,8 +313,12 @@ def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     for e, f, (g, g_exp) in zip(expect, full, got):
         _compare(g_exp, f)
         for i, (x, y) in enumerate(zip(e, g)):
-            if i != 1 or pip.sformat == seq.cformat:  # pred stream: keys in ENTRY16
-                assert np.array_equal(x, y)
+            if i == 1 and pip.sformat != seq.cformat:  # pred stream: keys in ENTRY16
+                continue
+            if i in (0, 3) and pip.sformat & PASTE_CF_KEYS:  # no hdr / act streams
+                assert len(y) == 0
+                continue
+            assert np.array_equal(x, y)
     if variant == "ship_bytes":  # same arena contents
         assert torch.equal(seq.bytes, pip.bytes) and torch.equal(seq.refs, pip.refs)
 
