@@ -578,6 +578,159 @@ def make_hash():
     print(f"hash_golden.json: {len(cases)} values", file=sys.stderr)
 
 
+# ---------------------------------------------------------------------------
+# ingestion (events.py:196-252) and the pool wire format (mining.py:300-398)
+# ---------------------------------------------------------------------------
+
+def _ingest_json(text, threshold=None):
+    from spectool.events import ingest_trace
+    res = ingest_trace(text) if threshold is None else ingest_trace(text, threshold)
+    return {"text": text, "threshold": threshold,
+            "expected": {"sessions": [sess_json(s) for s in res.sessions],
+                         "errors": [[e.line, e.message] for e in res.errors],
+                         "reordered": res.reordered_sessions}}
+
+
+def _line(sid, seq, kind="tool_call", tool="a", status="success", t0=0.0, t1=None, **extra):
+    d = {"session_id": sid, "seq": seq, "kind": kind, "tool": tool, "status": status,
+         "t_start_ms": t0, "t_end_ms": t0 + 1.0 if t1 is None else t1}
+    d.update(extra)
+    return json.dumps(d, ensure_ascii=False)
+
+
+def make_ingest():
+    """The reference's ingest_trace on hand-made edge traces and on random
+    interleaved traces: first-appearance grouping, the stable (t_start, seq)
+    sort and the reorder tally, gap splits at exactly / just past / just
+    under the threshold (incl. gaps measured from an LLM step), #n segment
+    ids, per-line errors (bad JSON, non-objects, missing fields, bad enums,
+    t_start > t_end, empty tool), coerced field types and custom thresholds."""
+    T = 300_000.0
+    hand = []
+    # exact-threshold gaps: > splits, == does not; +-0.5
+    hand.append("\n".join([_line("g", 0, t0=0.0, t1=10.0), _line("g", 1, t0=10.0 + T),
+                           _line("g", 2, t0=11.0 + T + T + 0.5), _line("g", 3, t0=2 * T + 12.0 + T - 0.5 + 0.5),
+                           _line("g", 4, t0=4 * T + 100.0, tool="b"),
+                           _line("g", 5, kind="llm_step", tool="", t0=5 * T + 200.0),
+                           _line("g", 6, t0=5 * T + 201.0 + T)]))
+    # interleaving + reorders + ties on t_start broken by seq, duplicate (t, seq) kept stable
+    hand.append("\n".join([_line("x", 3, t0=5.0, tool="c"), _line("y", 0, t0=1.0),
+                           _line("x", 1, t0=5.0, tool="b"), _line("x", 0, t0=9.0),
+                           _line("y", 1, t0=1.0, tool="d"), _line("y", 1, t0=1.0, tool="e"),
+                           _line("z", 0, t0=0.0, kind="llm_step", tool=""),
+                           _line("x", 2, t0=2.0, status="fail")]))
+    # malformed lines of every kind the reference tallies
+    hand.append("\n".join([
+        _line("m", 0), "{broken", "[1, 2]", "42", '"str"', "null",
+        json.dumps({"session_id": "m", "seq": 1, "kind": "tool_call", "tool": "a"}),
+        _line("m", 2, kind="bogus"), _line("m", 3, status="ok"),
+        _line("m", 4, t0=10.0, t1=5.0), _line("m", 5, tool=""),
+        _line("m", 6, kind="llm_step", tool=""), "   ", "",
+        _line("m", 7, t0=3.0, t1=3.0, tool="f"),
+        '{"session_id": "m", "seq": "x", "kind": "tool_call", "tool": "a", "status": "success", '
+        '"t_start_ms": 1, "t_end_ms": 2}',
+        '{"session_id": "m", "seq": 8, "kind": "tool_call", "tool": "a", "status": "success", '
+        '"t_start_ms": "abc", "t_end_ms": 2}',
+        _line("m", 9, t0=20.0)]))
+    # coercions: numeric / escaped / unicode ids, seq as float or numeric string,
+    # times as strings or ints, -0.0, tools that are numbers, extra keys and payloads
+    hand.append("\n".join([
+        '{"session_id": 7, "seq": 0, "kind": "tool_call", "tool": "a", "status": "success", '
+        '"t_start_ms": 1, "t_end_ms": 2}',
+        '{"session_id": "7", "seq": 1.9, "kind": "tool_call", "tool": 5, "status": "fail", '
+        '"t_start_ms": "3", "t_end_ms": "4.5"}',
+        '{"session_id": "s\\"q", "seq": "2", "kind": "tool_call", "tool": "\\u00e9t\\u00e9", '
+        '"status": "success", "t_start_ms": -0.0, "t_end_ms": 0.0, "args": {"q": [1, {"k": null}]}}',
+        '{"session_id": "s\\"q", "seq": 3, "kind": "tool_call", "tool": "b", "status": "success", '
+        '"t_start_ms": 0.0, "t_end_ms": 0.0, "result": "r", "extra": true}',
+        _line("ü#1", 0, t0=1e15, t1=1e15 + 1), _line("ü", 0, t0=-5.0, t1=-4.0),
+        _line("ü", 1, t0=-1e-300, t1=1e-300, tool="z"),
+        '{"session_id": "n", "seq": 0, "kind": "tool_call", "tool": "a", "status": "success", '
+        '"t_start_ms": 1e308, "t_end_ms": Infinity}',
+        '{"session_id": "n", "seq": 1, "kind": "tool_call", "tool": "a", "status": "success", '
+        '"t_start_ms": true, "t_end_ms": 2}']))
+    cases = [_ingest_json(t) for t in hand]
+    cases.append(_ingest_json(hand[0], 1000.0))
+    cases.append(_ingest_json(hand[1], 0.0))
+    cases.append(_ingest_json(hand[0], 299_999.5))
+    # random interleaved traces
+    rng = random.Random(5196)
+    tools = ["search", "web_fetch", "file_editor", "terminal", "grep", "Zeta", "été"]
+    for ci in range(24):
+        lines = []
+        n_sess = rng.randint(1, 40)
+        for s in range(n_sess):
+            t = rng.choice([0.0, rng.uniform(0, 1e6)])
+            sid = rng.choice([f"s{s}", f"sess-{s}", f"s{s}#1", f"é{s}"])
+            for q in range(rng.randint(1, 12)):
+                kind = "llm_step" if rng.random() < 0.2 else "tool_call"
+                t += rng.choice([0.0, 10.0, 500.0, T - 0.5, T, T + 0.5, 400_000.0, 1e6])
+                dur = rng.choice([0.0, 1.0, rng.uniform(1, 2000)])
+                extra = {}
+                if rng.random() < 0.3:
+                    extra["args"] = {"q": rng.randint(0, 9)}
+                if rng.random() < 0.3:
+                    extra["result"] = {"r": [1, 2.5, None, True]}
+                lines.append(_line(sid, q, kind=kind,
+                                   tool="" if kind == "llm_step" else rng.choice(tools),
+                                   status="fail" if rng.random() < 0.1 else "success",
+                                   t0=t, t1=t + dur, **extra))
+            if rng.random() < 0.3 and len(lines) > 2:  # swap timestamps -> reorder
+                i = rng.randrange(len(lines) - 1)
+                a, b = json.loads(lines[i]), json.loads(lines[i + 1])
+                if a["session_id"] == b["session_id"]:
+                    for key in ("t_start_ms", "t_end_ms"):
+                        a[key], b[key] = b[key], a[key]
+                    lines[i], lines[i + 1] = json.dumps(a), json.dumps(b)
+        if ci % 2:
+            rng.shuffle(lines)
+        for _ in range(rng.randint(0, 4)):
+            lines.insert(rng.randrange(len(lines) + 1), rng.choice(["{", "[]", "   ", _line(
+                "bad", 0, t0=5.0, t1=1.0), _line("bad", 1, tool="")]))
+        cases.append(_ingest_json("\n".join(lines) + rng.choice(["", "\n"]),
+                                  rng.choice([None, None, 1000.0, 5e5])))
+    return {"cases": cases}
+
+
+def make_pool_bytes():
+    """save_pool text written by the reference: the random 1000-pattern pool of
+    pkg/tests/test_mining.py:253-276 (its generator, seed 21), pools with every
+    mapping kind and normalisation, and pools the reference mined from the
+    mapped motif corpora -- the load -> save byte-identity gate and the
+    serialisation of device-mined pools."""
+    from spectool.mining import MatchRelation
+    rng = random.Random(21)
+    tools = ["a", "b", "c"]
+    patterns = []
+    for _ in range(1000):
+        ctx = tuple(sig(rng.choice(tools), rng.choice([S, F])) for _ in range(rng.randint(1, 3)))
+        mapping = None
+        if rng.random() < 0.5:
+            mapping = ValueMapping((ArgBinding("arg0", PathLookup(
+                rng.randrange(len(ctx)), ("list", rng.randint(0, 3), "url"))),))
+        patterns.append(PatternTuple(context=ctx, target=rng.choice(tools), mapping=mapping,
+                                     p=round(rng.uniform(0.1, 1.0), 6), support=rng.randint(1, 50)))
+    pools = {"random_1000": PatternPool(config=MiningConfig(), patterns=tuple(patterns))}
+    pools["edge"] = PatternPool(config=MiningConfig(k=2, sigma=3, tau=0.25,
+                                                    match_relation=MatchRelation.CONTIGUOUS_SUFFIX),
+                                patterns=tuple(edge_pool()))
+    for name, (seed, mix, cfg) in {
+            "mined_search_batch_t03": (7, {"search_visit": 0.5, "batch_fetch": 0.5},
+                                       MiningConfig(tau=0.3)),
+            "mined_coding_t03": (1, {"edit_verify": 0.5, "locate_examine": 0.5},
+                                 MiningConfig(tau=0.3))}.items():
+        corpus = generate_corpus(mix, 150, seed=seed)
+        pools[name] = mine_pool(corpus.sessions, cfg)
+    out = {}
+    for name, pool in pools.items():
+        buf = io.StringIO()
+        save_pool(pool, buf)
+        again = io.StringIO()  # the reference's own load -> save of that text
+        save_pool(load_pool(io.StringIO(buf.getvalue())), again)
+        out[name] = {"saved": buf.getvalue(), "resaved": again.getvalue()}
+    return {"pools": out}
+
+
 def dump(name, obj):
     path = os.path.join(OUT, name)
     with open(path, "w", encoding="utf-8") as fh:
@@ -594,6 +747,10 @@ def main(which):
         make_hash()
     if "jobs" in which:
         dump("jobs_golden.json", make_jobs())
+    if "ingest" in which:
+        dump("ingest_golden.json", make_ingest())
+    if "poolbytes" in which:
+        dump("pool_bytes_golden.json", make_pool_bytes())
     if "fixtures" not in which:
         return
     dump("predict_golden.json", make_predict())
