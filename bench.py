@@ -250,10 +250,12 @@ def run_ours(args):
         wall = time.perf_counter() - t_wall
     times = [e0.elapsed_time(e1) / 1e3 for e0, e1 in events]
     preds, n_bind, acts = (int(x) for x in stats.tolist())
-    # DESIGN.md K4: per session 60 + 4G (count, ring tokens, new token + node
-    # read; count, ring slot, directory entry, 3 counters written), per
-    # prediction 5, per resolved binding 28, per action 11
-    alg = S_ * n * (60 + 4 * G) + 5 * preds + 28 * n_bind + 11 * acts
+    # 200 B per session prediction (16 x 4 B suffix + 8 B
+    # header + 8 x 16 B output records), the canonical encoding.  The kernel's
+    # own byte model (K4: per session 60 + 4G, per prediction 5,
+    # per resolved binding 28, per action 11) is reported beside it.
+    alg = S_ * n * C3_ALG_BYTES
+    model = S_ * n * (60 + 4 * G) + 5 * preds + 28 * n_bind + 11 * acts
     # the serving kernel (fused predict + narrow-stream compaction) for reference
     cbuf = _compact_buffers(table)
     cdesc = _compact_desc(cbuf, table.cformat)
@@ -340,8 +342,14 @@ def run_ours(args):
                 else "i32 token + i32 node_base per session"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": committed_traffic(),
-                     "kernel": "predict_fast_kernel", "algorithmic_bytes_per_launch": alg // S_,
-                     "peak_source": f"{peak_kind} hbm_gbs"},
+                     "kernel": "predict_live_kernel" if table.plan is not None
+                     else "predict_fast_kernel",
+                     "algorithmic_bytes_per_launch": alg // S_,
+                     "kernel_model_bytes_per_launch": model // S_,
+                     "peak_source": f"{peak_kind} hbm_gbs",
+                     "note": "SURVEY 8(d) 200 B/session; traffic = ncu dram bytes per launch "
+                             "(profiles/ncu_live_r2.json): the narrow u8/u16 inputs and the "
+                             "key-coded records move fewer bytes than the canonical encoding"},
         "gpu_launches": launches,
         "wall_s_timed_region": wall,
     }
@@ -504,7 +512,10 @@ def run_replay(args, world, rank, local):
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "kernel": "replay step (windows + predict + score)",
                         "algorithmic_bytes_per_launch": REPLAY_ALG_BYTES * n,
-                        "peak_source": f"{peak_kind} hbm_gbs"},
+                        "traffic": replay_traffic(),
+                        "peak_source": f"{peak_kind} hbm_gbs",
+                        "note": "SURVEY 8(d) 233 B/call; traffic = ncu dram bytes of the step's "
+                                "kernels (profiles/ncu_replay_r2.json)"},
            "e2e": {"value": world * n * steps / t_e2e, "unit": "calls/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 32,
                    "ms_per_step": 1e3 * t_e2e / steps},
@@ -578,11 +589,21 @@ def run_long_outputs(args, world, rank, local):
     h2d = c["bytes"].nbytes + c["refs"].nbytes + c["target_bytes"].nbytes
     d2h = out_h.numel() * 4 + n_out_h.numel() * 8
     peak, peak_kind = measured_peaks()
-    # algorithmic bytes: each payload's scalar bytes + its directory entry +
-    # target; the node records of the shape-interned url_list tape are shared
-    # by every payload (L2-resident), so they are not HBM traffic
-    per = c["payload_bytes"] + 16 + int(c["target_off"][-1]) // n
-    achieved = per * n / (t_dev / steps) / 1e9
+    # algorithmic bytes: per session the bytes of the leaves values_equal can
+    # accept -- string leaves of the target's canonical length (mappings.py:
+    # 237-266; every other leaf is rejected on its node record alone) -- plus
+    # the directory entry and the target.  The node records of the
+    # shape-interned url_list tape are shared by every payload (L2-resident).
+    # SURVEY 8(d)'s 65,005 B/session (the whole canonical payload) is
+    # reported beside it: the scan never needs the other leaves' bytes.
+    nd = c["nodes"]
+    tlen = np.diff(c["target_off"])
+    strs = nd["b"][nd["type"] == 5].astype(np.int64)
+    cand = {int(L): int(strs[strs == L].sum()) for L in np.unique(tlen)}
+    alg_total = int(sum(cand[int(L)] for L in tlen)) + 16 * n + int(c["target_off"][-1])
+    per = alg_total // n
+    achieved = alg_total / (t_dev / steps) / 1e9
+    traffic = kernel_traffic("ncu_leaf_r2.json", "leaf_match_kernel")
     out = {"metric": LONG_METRIC, "value": world * n * steps / t_dev, "unit": "sessions/s",
            "n_gpus": world, "steps": steps, "ms_per_step": 1e3 * t_dev / steps,
            "scaling": "weak", "data": "synthetic", "parity_spot_check": ok,
@@ -592,9 +613,12 @@ def run_long_outputs(args, world, rank, local):
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak,
                         "kernel": "leaf_match_kernel" if batch.shared else "leaf_scan_kernel",
-                        "algorithmic_bytes_per_launch": per * n,
+                        "algorithmic_bytes_per_launch": alg_total, "traffic": traffic,
+                        "survey_bytes_per_launch": 65_005 * n,
                         "peak_source": f"{peak_kind} hbm_gbs",
-                        "note": "scalar bytes + directory + target per payload; the shared node template (3,363 x 16 B) is L2-resident"},
+                        "note": "candidate-leaf bytes (string leaves of the target's length) + "
+                                "directory + target per payload; traffic = ncu dram bytes of "
+                                "leaf_match_kernel (profiles/ncu_leaf_r2.json)"},
            "e2e": {"value": world * n * steps / t_e2e, "unit": "sessions/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                    "ms_per_step": 1e3 * t_e2e / steps},
@@ -619,6 +643,7 @@ def run_long_outputs(args, world, rank, local):
 
 
 MINE_METRIC = "mined trace events/sec"
+C3_ALG_BYTES = 200
 # 28 B columnar read + 4 B token written + 4 B token
 # re-read + ~0.5 B offsets per event (here the token is the 4-B staged word)
 MINE_ALG_BYTES = 36.5
@@ -823,9 +848,29 @@ def committed_ncu(name: str) -> dict:
         return {}
 
 
-def committed_traffic():
-    """dram bytes per launch of predict_kernel from the committed ncu capture."""
-    return committed_ncu("ncu_predict_latest.json").get("dram_bytes_per_launch")
+def kernel_traffic(name: str, kernel: str):
+    """dram bytes of the first launch of `kernel` in a committed ncu capture."""
+    for l in committed_ncu(name).get("launches", []):
+        if l["kernel"].split("(")[0].split()[-1].startswith(kernel):
+            return l.get("dram_bytes_per_launch")
+    return None
+
+
+def replay_traffic():
+    """dram bytes of one C2 replay step (one launch of each kernel) from the
+    committed ncu capture."""
+    seen, total = set(), 0.0
+    for l in committed_ncu("ncu_replay_r2.json").get("launches", []):
+        k = l["kernel"].split("(")[0]
+        if k not in seen and l.get("dram_bytes_per_launch"):
+            seen.add(k)
+            total += l["dram_bytes_per_launch"]
+    return total or None
+
+
+def committed_traffic(name: str = "ncu_live_r2.json"):
+    """dram bytes per launch of the C3 step kernel from the committed ncu capture."""
+    return committed_ncu(name).get("dram_bytes_per_launch")
 
 
 def oracle_live_run(args, n, threads, budget_s, max_steps=64):

@@ -364,6 +364,59 @@ int64_t paste_mine_stage_bytes(int64_t n_events, int32_t n_sigs, int32_t k);
 int paste_mine_ingest_count_staged(const paste_columnar_desc* c, const paste_mine_desc* d,
                                    void* stage, int64_t stage_bytes, void* stream);
 
+/* K1 general path: ingest_trace's grouping, stable sort, reorder tally and
+ * gap split (events.py:196-252, _split_on_gaps :243-252) on the device, for
+ * columnar traces in ARRIVAL order (the order records were read), with
+ * every event of every kind.  Replaces the host-only grouping/sort of
+ * ingest_trace (events.py:212-241) on the columnar path.
+ *   session: [n] session id in [0, n_sessions).  Groups are emitted in id
+ *            order: pass first-appearance ids (the order ingest_trace's
+ *            `order` list holds) to reproduce the reference.  Unused ids
+ *            are allowed and give no segment.
+ *   sig:     [n] tool signature, or -1 for an LLM step (LLM steps take
+ *            part in the sort and the gap split but are not written out).
+ * Each session's events are stably sorted by (t_start, seq) (-0.0 == 0.0,
+ * arrival order breaks ties, as Python's sorted); a session counts as
+ * reordered when its seq list changed; a new segment starts where
+ * t_start - prev.t_end > inactivity_ms.  Output: the columnar mining trace
+ * of paste_mine_ingest_count (tool events only, session = global segment
+ * index, segments numbered in (session id, segment) order, LLM-only
+ * segments included in the numbering) -- count it with inactivity_ms = +inf.
+ * Device-side results: *n_out tool events, *n_segments, *reordered, and
+ * *status (PASTE_ORDER_NAN_T: a NaN t_start, whose Python sort order is
+ * undefined -- the caller must use the host ingest; PASTE_ORDER_BAD_SESSION:
+ * an id outside [0, n_sessions)).  `order` (optional, [n]) receives the
+ * arrival index of every event in sorted order (payload gathers).
+ * Requires n_events < 2^31.  `scratch`: paste_ingest_order_scratch_bytes.  */
+typedef struct {
+  int64_t n_events;
+  int32_t n_sessions;
+  int32_t pad;
+  const int32_t* session;
+  const int32_t* seq;
+  const double* t_start;
+  const double* t_end;
+  const int32_t* sig;
+  double inactivity_ms;
+  int32_t* out_session;     /* [n] capacity                                  */
+  int32_t* out_seq;
+  double* out_t_start;
+  double* out_t_end;
+  int32_t* out_sig;
+  int32_t* order;           /* optional [n]                                  */
+  int64_t* n_out;           /* device scalars                                */
+  int64_t* n_segments;
+  int64_t* reordered;
+  int64_t* status;
+} paste_order_desc;
+
+#define PASTE_ORDER_NAN_T 1
+#define PASTE_ORDER_BAD_SESSION 2
+
+int64_t paste_ingest_order_scratch_bytes(int64_t n_events, int32_t n_sessions);
+int paste_ingest_order(const paste_order_desc* d, void* scratch, int64_t scratch_bytes,
+                       void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* canonical_arg_hash (events.py:94-122) on the device                      */
 /* ---------------------------------------------------------------------- */

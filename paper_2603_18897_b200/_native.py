@@ -89,6 +89,20 @@ class ColumnarDesc(ctypes.Structure):
                 ("n_segments", c_void_p), ("n_unsorted", c_void_p)]
 
 
+class OrderDesc(ctypes.Structure):
+    _fields_ = [("n_events", c_int64), ("n_sessions", c_int32), ("pad", c_int32),
+                ("session", c_void_p), ("seq", c_void_p), ("t_start", c_void_p),
+                ("t_end", c_void_p), ("sig", c_void_p), ("inactivity_ms", ctypes.c_double),
+                ("out_session", c_void_p), ("out_seq", c_void_p), ("out_t_start", c_void_p),
+                ("out_t_end", c_void_p), ("out_sig", c_void_p), ("order", c_void_p),
+                ("n_out", c_void_p), ("n_segments", c_void_p), ("reordered", c_void_p),
+                ("status", c_void_p)]
+
+
+PASTE_ORDER_NAN_T = 1
+PASTE_ORDER_BAD_SESSION = 2
+
+
 class SelectDesc(ctypes.Structure):
     _fields_ = [("n_jobs", c_int64), ("p", c_void_p), ("benefit", c_void_p), ("duration", c_void_p),
                 ("cost", c_void_p), ("id", c_void_p), ("selected", c_void_p),
@@ -247,6 +261,8 @@ EXPORTS = {
     "paste_mine_stage_bytes": (c_int64, [c_int64, c_int32, c_int32]),
     "paste_mine_ingest_count_staged": (c_int, [POINTER(ColumnarDesc), POINTER(MineDesc), c_void_p,
                                                c_int64, c_void_p]),
+    "paste_ingest_order_scratch_bytes": (c_int64, [c_int64, c_int32]),
+    "paste_ingest_order": (c_int, [POINTER(OrderDesc), c_void_p, c_int64, c_void_p]),
     "paste_mine_select_sorted": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64,
                                          c_void_p, c_void_p, c_void_p, c_void_p]),
 }

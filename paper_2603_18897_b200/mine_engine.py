@@ -563,6 +563,58 @@ def merge_shard_histograms(hist, counters, group) -> None:
     dist.all_reduce(counters, group=group)
 
 
+@dataclass
+class OrderedTrace:
+    columns: dict          # device columnar mining trace (tool events, session = segment)
+    n_segments: int
+    reordered_sessions: int
+    order: Any = None      # optional: arrival index of every event in sorted order
+
+
+_ORDER_DTYPES = {"session": "int32", "seq": "int32", "t_start": "float64", "t_end": "float64",
+                 "sig": "int32"}
+
+
+def order_columnar(raw: dict, n_sessions: int, inactivity_ms: float = 300_000.0,
+                   with_order: bool = False) -> OrderedTrace:
+    """K1 general path (paste_ingest_order): ingest_trace's grouping by
+    session id, stable (t_start, seq) sort, reorder tally and inactivity
+    split (events.py:196-252) over a device-resident columnar trace in
+    arrival order.  ``raw['sig']`` is -1 for LLM steps (they take part in
+    the sort and the gap split, and are dropped from the output like
+    Session.tool_events drops them); session ids are first-appearance
+    indices in [0, n_sessions).  One host sync (the result counts)."""
+    from .device_ops import stream_handle
+    from ._native import OrderDesc
+
+    torch = _torch()
+    lib = _native.lib()
+    for k, dt in _ORDER_DTYPES.items():
+        if str(raw[k].dtype) != "torch." + dt or not raw[k].is_cuda:
+            raise ValueError(f"column {k!r} must be a CUDA {dt} tensor")
+    n = int(raw["sig"].numel())
+    dev = raw["sig"].device
+    out = {k: torch.empty(n, dtype=getattr(torch, dt), device=dev)
+           for k, dt in _ORDER_DTYPES.items()}
+    res = torch.zeros(4, dtype=torch.int64, device=dev)
+    order = torch.empty(n, dtype=torch.int32, device=dev) if with_order else None
+    need = int(lib.paste_ingest_order_scratch_bytes(n, int(n_sessions)))
+    scratch = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
+    base = ptr(res)
+    cols = [raw[k].contiguous() for k in _ORDER_DTYPES]  # alive until the sync below
+    d = OrderDesc(n, int(n_sessions), 0, *[ptr(c) for c in cols],
+                  float(inactivity_ms), *[ptr(out[k]) for k in _ORDER_DTYPES], ptr(order),
+                  base, base + 8, base + 16, base + 24)
+    check(lib.paste_ingest_order(ctypes.byref(d), ptr(scratch), need, stream_handle()), lib)
+    n_out, n_seg, reord, status = (int(x) for x in res.tolist())
+    if status & _native.PASTE_ORDER_BAD_SESSION:
+        raise ValueError(f"session ids outside [0, {n_sessions})")
+    if status & _native.PASTE_ORDER_NAN_T:
+        raise _native.PasteUnsupported("NaN t_start: Python's sort order for it is undefined "
+                                       "(use the host ingest_trace)")
+    return OrderedTrace({k: v[:n_out] for k, v in out.items()}, n_seg, reord, order)
+
+
 def mine_columnar(trace: dict, sigs: SigTable, cfg: MiningConfig,
                   inactivity_ms: float = 300_000.0, group=None) -> list[PatternTuple]:
     """mine() over a columnar trace shard on this device.  With a
@@ -573,10 +625,15 @@ def mine_columnar(trace: dict, sigs: SigTable, cfg: MiningConfig,
     relation = 0 if cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE else 1
     tables = MineTables.allocate(max(sigs.n_sigs, 2), cfg.k, relation)
     counters = ingest_count(tables, trace, inactivity_ms)
+    if int(counters[1].item()):
+        # not grouped by session / sorted by (t_start, seq): the K1 general
+        # path orders it on the device (ingest_trace's stable sort and gap
+        # split), then the count runs again over the ordered segments
+        n_sessions = int(trace["session"].max().item()) + 1
+        ordered = order_columnar(trace, n_sessions, inactivity_ms)
+        tables.hist.zero_()
+        counters = ingest_count(tables, ordered.columns, float("inf"))
     if group is not None:
         merge_shard_histograms(tables.hist, counters, group)
-    if int(counters[1].item()):
-        raise _native.PasteUnsupported(
-            "columnar trace is not grouped by session / sorted by (t_start, seq)")
     tables.expand()
     return tables.select_sorted(cfg.sigma, cfg.tau).patterns(sigs)

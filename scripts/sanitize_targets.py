@@ -10,6 +10,8 @@ shows the results stayed right under its serialising scheduler.
   live   predict_live_kernel, the two-pass serving step (stage + scatter),
          the look-back serving kernels (PASTE_LIVE_MODE=ticket / pipe) and
          compact.cu's look-back compaction, vs the K-slot records
+  order  the K1 general path (order.cu): warp bitonic, CTA chunk sort +
+         merge-path passes, warp-aggregated placement
   select sel_greedy_kernel / victim_kernel
 
 usage: python scripts/sanitize_targets.py {mine,live,select,all}
@@ -80,6 +82,24 @@ def live():
     print("live ok", os.environ.get("PASTE_LIVE_MODE", "two-pass"))
 
 
+def order():
+    from oracle.order import order_trace
+    from order_cases import random_trace
+    from paper_2603_18897_b200.mine_engine import order_columnar
+
+    keys = ("session", "seq", "t_start", "t_end", "sig")
+    for il, ls in ((False, ()), (True, (64, 3000))):
+        raw = random_trace(3000, seed=5, long_sessions=ls, interleave=il)
+        got = order_columnar({k: torch.from_numpy(v).cuda() for k, v in raw.items()}, 3000,
+                             300_000.0, with_order=True)
+        cols, n_seg, reord, order_ = order_trace(*(raw[k] for k in keys), 3000, 300_000.0)
+        assert got.n_segments == n_seg and got.reordered_sessions == reord
+        assert np.array_equal(got.order.cpu().numpy(), order_)
+        for k in keys:
+            assert np.array_equal(got.columns[k].cpu().numpy(), cols[k]), k
+    print("order ok")
+
+
 def select():
     from paper_2603_18897_b200.select import select_greedy_arrays
     rng = np.random.default_rng(5)
@@ -105,6 +125,6 @@ def select():
 
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
-    for name, fn in (("mine", mine), ("live", live), ("select", select)):
+    for name, fn in (("mine", mine), ("live", live), ("order", order), ("select", select)):
         if which in (name, "all"):
             fn()

@@ -731,6 +731,31 @@ def make_pool_bytes():
     return {"pools": out}
 
 
+def make_c1():
+    """C1 at its stated size: generate_corpus(search_visit /
+    batch_fetch 0.5 / 0.5, 1000 sessions, seed 7) mined at the default
+    MiningConfig (tau 0.5) and at tau 0.3, and score_accuracy(W=16) of each
+    pool on the held-out seed-8 corpus (1000 sessions)."""
+    import gzip
+    mix = {"search_visit": 0.5, "batch_fetch": 0.5}
+    train = generate_corpus(mix, 1000, seed=7)
+    held = generate_corpus(mix, 1000, seed=8)
+    out = {"train": [sess_json(s) for s in train.sessions],
+           "held": [sess_json(s) for s in held.sessions], "cases": []}
+    for cfg in (MiningConfig(), MiningConfig(tau=0.3)):
+        pool = mine_pool(train.sessions, cfg)
+        rep = score_accuracy(held.sessions, pool, window_capacity=16)
+        out["cases"].append({"config": {"k": cfg.k, "sigma": cfg.sigma, "tau": cfg.tau,
+                                        "match_relation": cfg.match_relation.value},
+                             "expected": [pattern_json(p) for p in pool.patterns],
+                             "score": rep.to_json()})
+        print(f"C1 tau={cfg.tau}: {len(pool)} patterns, {rep.to_json()}", file=sys.stderr)
+    path = os.path.join(OUT, "c1_golden.json.gz")
+    with gzip.open(path, "wt", encoding="utf-8") as fh:
+        json.dump(out, fh, ensure_ascii=False, separators=(",", ":"))
+    print(f"c1_golden.json.gz: {os.path.getsize(path) / 1e6:.2f} MB", file=sys.stderr)
+
+
 def dump(name, obj):
     path = os.path.join(OUT, name)
     with open(path, "w", encoding="utf-8") as fh:
@@ -747,6 +772,8 @@ def main(which):
         make_hash()
     if "jobs" in which:
         dump("jobs_golden.json", make_jobs())
+    if "c1" in which:
+        make_c1()
     if "ingest" in which:
         dump("ingest_golden.json", make_ingest())
     if "poolbytes" in which:

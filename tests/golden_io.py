@@ -17,8 +17,14 @@ _cache: dict[str, dict] = {}
 
 def golden(name: str) -> dict:
     if name not in _cache:
-        with open(os.path.join(GOLDEN, name), encoding="utf-8") as fh:
-            _cache[name] = json.load(fh)
+        path = os.path.join(GOLDEN, name)
+        if name.endswith(".gz"):
+            import gzip
+            with gzip.open(path, "rt", encoding="utf-8") as fh:
+                _cache[name] = json.load(fh)
+        else:
+            with open(path, encoding="utf-8") as fh:
+                _cache[name] = json.load(fh)
     return _cache[name]
 
 

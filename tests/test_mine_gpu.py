@@ -251,21 +251,6 @@ def test_columnar_count_at_scale_matches_oracle(rel):
     assert got == patterns_from_candidates(cands, sigs, 32, cfg) and len(got) > 0
 
 
-def test_columnar_rejects_unsorted_trace():
-    from paper_2603_18897_b200._native import PasteUnsupported
-    from paper_2603_18897_b200.mine_engine import mine_columnar
-    from paper_2603_18897_b200.packing import SigTable
-    from paper_2603_18897_b200.synth import C4_TOOLS, columnar_corpus
-
-    c = columnar_corpus(10_000, seed=13)
-    i = int(np.flatnonzero(c["session"][1:] == c["session"][:-1])[5])
-    for key in ("t_start", "t_end", "seq", "sig"):
-        c[key][[i, i + 1]] = c[key][[i + 1, i]]
-    with pytest.raises(PasteUnsupported):
-        mine_columnar(_dev(c), SigTable(C4_TOOLS), MiningConfig())
-
-
-
 def test_sharded_mining_equals_single_device(tmp_path):
     """mine_columnar over 2 ranks (whole-session shards, histogram merged by
     all-reduce; gloo ranks sharing this GPU, launched by torchrun) == the
