@@ -417,6 +417,48 @@ int64_t paste_ingest_order_scratch_bytes(int64_t n_events, int32_t n_sessions);
 int paste_ingest_order(const paste_order_desc* d, void* scratch, int64_t scratch_bytes,
                        void* stream);
 
+/* Phase II occurrence collection: _collect_occurrences (mining.py:215-227)
+ * for many candidates in one pass, keeping the followed occurrences whose
+ * next event has the candidate's target tool -- the `occ` list mine()
+ * hands to infer_mapping / mapping_holds (:277-285).  Replaces the host's
+ * per-candidate rescan of every stream.
+ * For every anchor a of the flagged token stream (bit 31 = first event of a
+ * session stream, token = 2 * tool + success) whose next token is in the
+ * same stream, the candidates of bucket (sig(a), tool(a + 1)) are matched
+ * with match_at (:119-156: last context sig == the anchor's; anchored
+ * rightmost embedding inside the k events ending at a, or the contiguous
+ * suffix slice), never across a stream boundary.  Candidate c's
+ * occurrences land in slots [off[c], off[c+1]) -- off is the exclusive scan
+ * of the candidates' follow counts from the mining tables, which count
+ * exactly these occurrences -- in no particular order: anchor[slot] = a,
+ * picked[slot * kmax + j] = stream position of matched event j (the
+ * history is [picked[slot * kmax], a]).  `cursor` ([n_cand], zeroed by the
+ * caller) and *overflow (emissions past a candidate's range; must stay 0)
+ * are device memory.  Sort slots by (candidate, anchor) with
+ * paste_ingest_order (session = candidate, t_start = anchor) for stream
+ * order.                                                                   */
+typedef struct {
+  int64_t n_tokens;
+  const int32_t* tok;
+  int32_t n_cand;
+  int32_t k;                /* MiningConfig.k                                */
+  int32_t relation;         /* 0 anchored subsequence, 1 contiguous suffix   */
+  int32_t kmax;             /* row width of ctx / picked (>= every ctx_len)  */
+  int32_t n_sigs;
+  int32_t n_tools;
+  const int32_t* ctx;       /* [n_cand * kmax] context sigs                  */
+  const int32_t* ctx_len;   /* [n_cand]                                      */
+  const int32_t* bucket_off;/* [n_sigs * n_tools + 1] by (last sig, target)  */
+  const int32_t* bucket;    /* candidate ids                                 */
+  const int64_t* off;       /* [n_cand + 1]                                  */
+  int64_t* cursor;          /* [n_cand]                                      */
+  int64_t* anchor;          /* [off[n_cand]]                                 */
+  int32_t* picked;          /* [off[n_cand] * kmax]                          */
+  uint64_t* overflow;
+} paste_occ_desc;
+
+int paste_mine_occurrences(const paste_occ_desc* d, void* stream);
+
 /* ---------------------------------------------------------------------- */
 /* canonical_arg_hash (events.py:94-122) on the device                      */
 /* ---------------------------------------------------------------------- */

@@ -99,6 +99,15 @@ class OrderDesc(ctypes.Structure):
                 ("status", c_void_p)]
 
 
+class OccDesc(ctypes.Structure):
+    _fields_ = [("n_tokens", c_int64), ("tok", c_void_p), ("n_cand", c_int32), ("k", c_int32),
+                ("relation", c_int32), ("kmax", c_int32), ("n_sigs", c_int32),
+                ("n_tools", c_int32), ("ctx", c_void_p), ("ctx_len", c_void_p),
+                ("bucket_off", c_void_p), ("bucket", c_void_p), ("off", c_void_p),
+                ("cursor", c_void_p), ("anchor", c_void_p), ("picked", c_void_p),
+                ("overflow", c_void_p)]
+
+
 PASTE_ORDER_NAN_T = 1
 PASTE_ORDER_BAD_SESSION = 2
 
@@ -261,6 +270,7 @@ EXPORTS = {
     "paste_mine_stage_bytes": (c_int64, [c_int64, c_int32, c_int32]),
     "paste_mine_ingest_count_staged": (c_int, [POINTER(ColumnarDesc), POINTER(MineDesc), c_void_p,
                                                c_int64, c_void_p]),
+    "paste_mine_occurrences": (c_int, [POINTER(OccDesc), c_void_p]),
     "paste_ingest_order_scratch_bytes": (c_int64, [c_int64, c_int32]),
     "paste_ingest_order": (c_int, [POINTER(OrderDesc), c_void_p, c_int64, c_void_p]),
     "paste_mine_select_sorted": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64,

@@ -234,6 +234,83 @@ def match_at(stream, anchor, context, k, relation):
     return match_events(stream, sig_stream, anchor, context, k, relation)
 
 
+def device_occurrences(tok_dev, flat_events: Sequence[Event], sigs: SigTable, cands: list,
+                       cfg: MiningConfig) -> list[list]:
+    """Phase II occurrence lists for many candidates at once on the device
+    (paste_mine_occurrences + the K1 sort for stream order): for every
+    (context sig tuple, target tool id, follow count) in ``cands`` the
+    (MatchedContext, next event) pairs of _collect_occurrences whose next
+    event is the target (mining.py:215-227,277-279), in stream order.  The
+    host only wraps the device's positions in the reference's objects."""
+    from .device_ops import stream_handle
+    from ._native import OccDesc
+
+    torch = _torch()
+    lib = _native.lib()
+    C = len(cands)
+    if C == 0:
+        return []
+    kmax = max(len(c[0]) for c in cands)
+    n_tools = (sigs.n_sigs + 1) // 2
+    ctx = np.zeros((C, kmax), np.int32)
+    ctx_len = np.zeros(C, np.int32)
+    follow = np.zeros(C, np.int64)
+    keys = np.zeros(C, np.int64)
+    for i, (cs, tool, f) in enumerate(cands):
+        ctx[i, :len(cs)] = cs
+        ctx_len[i] = len(cs)
+        follow[i] = f
+        keys[i] = cs[-1] * n_tools + tool
+    order = np.argsort(keys, kind="stable")
+    bucket_off = np.zeros(sigs.n_sigs * n_tools + 1, np.int32)
+    np.add.at(bucket_off, keys + 1, 1)
+    bucket_off = np.cumsum(bucket_off).astype(np.int32)
+    off = np.zeros(C + 1, np.int64)
+    off[1:] = np.cumsum(follow)
+    total = int(off[-1])
+    dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in dict(
+        ctx=ctx.reshape(-1), ctx_len=ctx_len, bucket_off=bucket_off,
+        bucket=order.astype(np.int32), off=off).items()}
+    cursor = torch.zeros(C, dtype=torch.int64, device="cuda")
+    anchor = torch.empty(max(total, 1), dtype=torch.int64, device="cuda")
+    picked = torch.empty(max(total, 1) * kmax, dtype=torch.int32, device="cuda")
+    overflow = torch.zeros(1, dtype=torch.int64, device="cuda")
+    rel = 0 if cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE else 1
+    d = OccDesc(int(tok_dev.numel()), ptr(tok_dev), C, cfg.k, rel, kmax, sigs.n_sigs, n_tools,
+                ptr(dev["ctx"]), ptr(dev["ctx_len"]), ptr(dev["bucket_off"]), ptr(dev["bucket"]),
+                ptr(dev["off"]), ptr(cursor), ptr(anchor), ptr(picked), ptr(overflow))
+    check(lib.paste_mine_occurrences(ctypes.byref(d), stream_handle()), lib)
+    # stream order inside every candidate's range: the K1 sort, candidate =
+    # session, anchor = t_start (slots are grouped by candidate already)
+    slot_cand = torch.repeat_interleave(torch.arange(C, dtype=torch.int32, device="cuda"),
+                                        torch.from_numpy(follow).cuda())
+    t = anchor[:total].to(torch.float64)
+    zeros = torch.zeros(total, dtype=torch.int32, device="cuda")
+    srt = order_columnar({"session": slot_cand, "seq": zeros, "t_start": t, "t_end": t,
+                          "sig": zeros}, C, float("inf"), with_order=True)
+    if int(overflow.item()) or int(cursor.sum().item()) != total:
+        raise _native.PasteError("occurrence counts disagree with the follow table")
+    perm = srt.order.long()
+    anc = anchor[:total][perm].cpu().numpy()
+    pk = picked.view(-1, kmax)[:total][perm].cpu().numpy()
+    out = []
+    for i, (cs, _tool, f) in enumerate(cands):
+        L = len(cs)
+        occ = []
+        for r in range(int(off[i]), int(off[i + 1])):
+            a = int(anc[r])
+            pos = pk[r, :L]
+            if rel:
+                sl = tuple(flat_events[a - L + 1:a + 1])
+                m = MatchedContext(events=sl, history=sl)
+            else:
+                m = MatchedContext(events=tuple(flat_events[p] for p in pos.tolist()),
+                                   history=tuple(flat_events[int(pos[0]):a + 1]))
+            occ.append((m, flat_events[a + 1]))
+        out.append(occ)
+    return out
+
+
 def _occurrences(streams, sig_streams, context: tuple, target: str, cfg: MiningConfig):
     """(matched, next) pairs whose next event is ``target``, in stream order."""
     occ = []
@@ -268,14 +345,29 @@ def _count_corpus(streams, cfg: MiningConfig, group=None):
     relation = 0 if cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE else 1
     tables = MineTables.allocate(max(sigs.n_sigs, 2), cfg.k, relation)
     tok = pack_streams(streams, sigs)
+    tok_dev = None
     if len(tok):
-        tables.count(torch.from_numpy(tok).cuda())
+        tok_dev = torch.from_numpy(tok).cuda()
+        tables.count(tok_dev)
     if group is not None:  # K3: shards are whole sessions, histograms add up
         import torch.distributed as dist
 
         dist.all_reduce(tables.hist, group=group)
     tables.expand()
-    return sigs, tables
+    return sigs, tables, tok_dev
+
+
+def _local_follow(tables: "MineTables", tok_dev, rows: list, S: int, cfg: MiningConfig) -> list:
+    """This shard's follow counts of the given candidates (the merged tables
+    hold the corpus totals): a count pass over the shard alone."""
+    if tok_dev is None:
+        return [0] * len(rows)
+    local = MineTables.allocate(tables.n_sigs, tables.k, tables.relation)
+    local.count(tok_dev)
+    local.expand()
+    T = (local.n_sigs + 1) // 2
+    fol = local.follow.cpu().numpy()
+    return [int(fol[cidx * T + tool]) for tool, cidx, *_ in rows]
 
 
 def _phase2(occ, cfg: MiningConfig, hits: int):
@@ -308,25 +400,39 @@ def mine(traces: Sequence[Session], cfg: MiningConfig, group=None) -> list[Patte
     elif not traces:
         raise ValueError("traces must be non-empty")
     streams = [s.tool_events() for s in traces]
-    sigs, tables = _count_corpus(streams, cfg, group)
+    sigs, tables, tok_dev = _count_corpus(streams, cfg, group)
     cands = tables.select(cfg.sigma, cfg.tau)
     if group is not None:  # the select kernel compacts with atomics: fix one order for all ranks
         cands = cands[np.lexsort((cands[:, 1], cands[:, 0]))]
     S = tables.n_sigs
-    sig_streams = None
+    rows = cands.tolist()
+    # Phase II occurrences of every candidate that can carry a mapping, from
+    # one device pass; under sharding each rank collects its shard (its own
+    # follow counts) and the lists are gathered in rank = stream order
+    need = [i for i, r in enumerate(rows) if r[4] >= 2]
+    occ_of: dict[int, list] = {}
+    if need:
+        if group is not None:  # this shard's follow counts size the slots
+            local = _local_follow(tables, tok_dev, [rows[i] for i in need], S, cfg)
+        else:
+            local = [rows[i][4] for i in need]
+        flat = [e for st in streams for e in st]
+        lists = device_occurrences(
+            tok_dev, flat, sigs, [(decode_context(rows[i][1], S, cfg.k), rows[i][0], f)
+                                  for i, f in zip(need, local)], cfg) if tok_dev is not None \
+            else [[] for _ in need]
+        for i, occ in zip(need, lists):
+            if group is not None:
+                occ = [o for part in _gather(occ, group) for o in part]
+            occ_of[i] = occ
     patterns = []
-    for tool, cidx, support, n_match, follow in cands.tolist():
+    for i, (tool, cidx, support, n_match, follow) in enumerate(rows):
         context = tuple(sigs.signature(x) for x in decode_context(cidx, S, cfg.k))
         target = sigs.tools[tool]
         mapping = None
         hits = follow
         if follow >= 2:
-            if sig_streams is None:
-                sig_streams = [[signature_of(e) for e in st] for st in streams]
-            occ = _occurrences(streams, sig_streams, context, target, cfg)
-            if group is not None:  # every shard's occurrences, in stream order
-                occ = [o for part in _gather(occ, group) for o in part]
-            mapping, hits = _phase2(occ, cfg, hits)
+            mapping, hits = _phase2(occ_of[i], cfg, hits)
         p = hits / n_match
         if p >= cfg.tau:
             patterns.append(PatternTuple(context=context, target=target, mapping=mapping, p=p,
@@ -351,11 +457,10 @@ def validate(context, target: str, mapping: ValueMapping | None, traces: Sequenc
     tables = MineTables.allocate(max(sigs.n_sigs, 2), k, relation)
     torch = _torch()
     tok = pack_streams(streams, sigs)
-    if len(tok):
-        tables.count(torch.from_numpy(tok).cuda())
+    tok_dev = torch.from_numpy(tok).cuda() if len(tok) else None
+    if tok_dev is not None:
+        tables.count(tok_dev)
     tables.expand()
-    if k != cfg.k:  # contexts longer than k only exist under the suffix relation
-        pass
     cidx = encode_context([sigs.sig_of(s) for s in context], tables.n_sigs, k)
     n_match = int(tables.match[cidx].item())
     if n_match == 0:
@@ -363,8 +468,9 @@ def validate(context, target: str, mapping: ValueMapping | None, traces: Sequenc
     follow = int(tables.follow[cidx * ((tables.n_sigs + 1) // 2) + sigs.tool(target)].item())
     if mapping is None:
         return follow / n_match
-    sig_streams = [[signature_of(e) for e in st] for st in streams]
-    occ = _occurrences(streams, sig_streams, tuple(context), target, cfg)
+    ctx_sigs = tuple(sigs.sig_of(s) for s in context)
+    occ = device_occurrences(tok_dev, [e for st in streams for e in st], sigs,
+                             [(ctx_sigs, sigs.tool(target), follow)], cfg)[0] if follow else []
     if not occ:
         return 0.0
     from . import phase2_device

@@ -331,3 +331,46 @@ def test_sharded_session_mining_with_mappings(tmp_path):
                for p in corpus["expected"]]
         exp = [[[[c["tool"], c["status"]] for c in e[0]]] + e[1:] for e in exp]
         assert got["0"][i] == exp and got["1"][i] == exp
+
+
+@pytest.mark.parametrize("rel,k", [(MatchRelation.ANCHORED_SUBSEQUENCE, 3),
+                                   (MatchRelation.ANCHORED_SUBSEQUENCE, 4),
+                                   (MatchRelation.CONTIGUOUS_SUFFIX, 3)])
+def test_device_occurrences_equal_host_rescan(rel, k):
+    """paste_mine_occurrences + the K1 sort == the host rescan of every
+    stream (_collect_occurrences filtered to the target, mining.py:215-227,
+    277-279) for every selected candidate: same occurrences, stream order,
+    matched events and histories."""
+    from paper_2603_18897_b200.events import Event, EventKind, Session, signature_of
+    from paper_2603_18897_b200.mine_engine import (_count_corpus, _occurrences, decode_context,
+                                                   device_occurrences)
+
+    rng = np.random.default_rng(k + 10 * rel.value.__len__())
+    tools = ["a", "b", "c", "d"]
+    sessions = []
+    for i in range(400):
+        evs = []
+        for j in range(int(rng.integers(1, 14))):
+            evs.append(Event(f"s{i}", j, EventKind.TOOL_CALL, tools[int(rng.integers(0, 4))],
+                             Status.FAIL if rng.random() < 0.2 else Status.SUCCESS, None, None,
+                             float(j), float(j) + 0.5))
+        sessions.append(Session(f"s{i}", tuple(evs)))
+    cfg = MiningConfig(k=k, sigma=2, tau=0.0, match_relation=rel)
+    streams = [s.tool_events() for s in sessions]
+    sigs, tables, tok_dev = _count_corpus(streams, cfg)
+    rows = [r for r in tables.select(cfg.sigma, cfg.tau).tolist() if r[4] >= 2]
+    assert len(rows) > 50
+    S = tables.n_sigs
+    cands = [(decode_context(r[1], S, cfg.k), r[0], r[4]) for r in rows]
+    flat = [e for st in streams for e in st]
+    got = device_occurrences(tok_dev, flat, sigs, cands, cfg)
+    sig_streams = [[signature_of(e) for e in st] for st in streams]
+    for (cs, tool, f), occ in zip(cands, got):
+        ctx = tuple(sigs.signature(x) for x in cs)
+        exp = _occurrences(streams, sig_streams, ctx, sigs.tools[tool], cfg)
+        assert len(occ) == len(exp) == f
+        for (m1, n1), (m2, n2) in zip(occ, exp):
+            assert n1 is n2
+            assert all(x is y for x, y in zip(m1.events, m2.events))
+            assert len(m1.history) == len(m2.history)
+            assert all(x is y for x, y in zip(m1.history, m2.history))
