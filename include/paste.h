@@ -819,9 +819,38 @@ typedef struct {
   int64_t* hits;             /* [n_hyp]                                       */
   int64_t* unsure;           /* [n_hyp]                                       */
   uint8_t* eq;               /* optional [n_hyp * n_occ]                      */
+  /* corpus mode (mine() over one corpus tape): when
+   * hist_end is set, occurrence m's history is hist_tok[hist_off[m],
+   * hist_end[m]) -- overlapping ranges of the corpus token stream (bit 31 =
+   * stream start) -- instead of the CSR hist_off[m], hist_off[m + 1]; when
+   * act_event is set, the actual argument is node act_node[m] of tape
+   * act_event[m] (-1: absent; containers never compare equal) instead of
+   * act_type / act_nan / act_off / act_bytes.                               */
+  const int32_t* hist_end;   /* optional [n_occ]                              */
+  const int32_t* act_event;  /* optional [n_occ]                              */
+  const int32_t* act_node;   /* [n_occ] with act_event                        */
 } paste_holds_desc;
 
 int paste_holds(const paste_holds_desc* d, void* stream);
+
+/* Key lookup over many payload tapes: out_node[i] = the child of tape
+ * tape[i]'s root dict whose key is `key` (node index inside the tape), -1
+ * when the root is not a dict or has no such key; *n_scalar (device,
+ * accumulated) += the number of found values that are scalars -- the
+ * "present and not a container in every occurrence" test of
+ * _common_scalar_args (mappings.py:299-315).                                */
+typedef struct {
+  int64_t n;
+  const paste_tape_node* nodes;
+  const paste_event_ref* refs;
+  const int32_t* tape;
+  int32_t key;
+  int32_t pad;
+  int32_t* out_node;
+  uint64_t* n_scalar;
+} paste_key_lookup_desc;
+
+int paste_tape_key_lookup(const paste_key_lookup_desc* d, void* stream);
 
 /* ---------------------------------------------------------------------- */
 /* C2 replay: score_accuracy (prediction.py:133-169)                        */

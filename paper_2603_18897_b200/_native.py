@@ -147,7 +147,14 @@ class HoldsDesc(ctypes.Structure):
     _fields_ = [("n_hyp", c_int64), ("n_occ", c_int64), ("n_ctx", c_int32), ("pad", c_int32)] + \
         [(name, c_void_p) for name in ("hyp", "steps", "fmt", "fmt_bytes", "nodes", "bytes", "refs",
                                        "occ_event", "src_pos", "hist_off", "hist_tok", "act_type",
-                                       "act_nan", "act_off", "act_bytes", "hits", "unsure", "eq")]
+                                       "act_nan", "act_off", "act_bytes", "hits", "unsure", "eq",
+                                       "hist_end", "act_event", "act_node")]
+
+
+class KeyLookupDesc(ctypes.Structure):
+    _fields_ = [("n", c_int64), ("nodes", c_void_p), ("refs", c_void_p), ("tape", c_void_p),
+                ("key", c_int32), ("pad", c_int32), ("out_node", c_void_p),
+                ("n_scalar", c_void_p)]
 
 
 class ReplayDesc(ctypes.Structure):
@@ -271,6 +278,7 @@ EXPORTS = {
     "paste_mine_ingest_count_staged": (c_int, [POINTER(ColumnarDesc), POINTER(MineDesc), c_void_p,
                                                c_int64, c_void_p]),
     "paste_mine_occurrences": (c_int, [POINTER(OccDesc), c_void_p]),
+    "paste_tape_key_lookup": (c_int, [POINTER(KeyLookupDesc), c_void_p]),
     "paste_ingest_order_scratch_bytes": (c_int64, [c_int64, c_int32]),
     "paste_ingest_order": (c_int, [POINTER(OrderDesc), c_void_p, c_int64, c_void_p]),
     "paste_mine_select_sorted": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64,

@@ -34,6 +34,7 @@ __global__ void holds_kernel(const paste_holds_desc D) {
     const paste_binding bd = D.hyp[h];
     bool eq = false, unsure = false;
     // resolve (mappings.py:162-194)
+    const int32_t h_lo = D.hist_off[m], h_hi = D.hist_end ? D.hist_end[m] : D.hist_off[m + 1];
     const int32_t ev = D.occ_event[m * D.n_ctx + bd.ctx_pos];
     const paste_event_ref ref = D.refs[ev];
     int64_t cur = 0;
@@ -44,7 +45,7 @@ __global__ void holds_kernel(const paste_holds_desc D) {
       int fails = 0;
       const int32_t sp = D.src_pos[m * D.n_ctx + bd.ctx_pos];
       if (sp >= 0)
-        for (int32_t q = D.hist_off[m] + sp + 1; q < D.hist_off[m + 1]; ++q) {
+        for (int32_t q = h_lo + sp + 1; q < h_hi; ++q) {
           const int32_t tk = D.hist_tok[q];
           fails += tk >= 0 && (tk >> 1) == bd.fail_tool && (tk & 1) == 0;
         }
@@ -55,14 +56,43 @@ __global__ void holds_kernel(const paste_holds_desc D) {
         cur = step_child(D.nodes, ref.node_base, cur, D.steps[2 * (bd.suf_off + s)],
                          D.steps[2 * (bd.suf_off + s) + 1]);
     }
-    const int at = D.act_type[m];
-    const uint8_t* ab = D.act_bytes + D.act_off[m];
-    const int64_t al = D.act_off[m + 1] - D.act_off[m];
+    int at;
+    bool anan;
+    const uint8_t* ab;
+    int64_t al;
+    if (D.act_event) {  // corpus mode: the actual is a node of the argument tape
+      const int32_t an = D.act_node[m];
+      at = -1;
+      anan = false;
+      ab = D.bytes;
+      al = 0;
+      if (an >= 0) {
+        const paste_event_ref aref = D.refs[D.act_event[m]];
+        const Node a = load_node(D.nodes, aref.node_base + an);
+        if (a.type() < PASTE_T_LIST) {
+          at = a.type();
+          anan = (a.flags() & PASTE_F_NAN) != 0;
+          ab = D.bytes + aref.byte_base + a.a;
+          al = a.b;
+          if (at == PASTE_T_STR && (a.flags() & PASTE_F_NFC)) {  // canonical: the NFC bytes
+            const uint8_t* x = ab + a.b;
+            al = (int64_t)x[0] | ((int64_t)x[1] << 8) | ((int64_t)x[2] << 16) |
+                 ((int64_t)x[3] << 24);
+            ab = x + 4;
+          }
+        }
+      }
+    } else {
+      at = D.act_type[m];
+      anan = D.act_nan[m] != 0;
+      ab = D.act_bytes + D.act_off[m];
+      al = D.act_off[m + 1] - D.act_off[m];
+    }
     if (cur >= 0) {
       const Node nd = load_node(D.nodes, ref.node_base + cur);
       const int nt = nd.type();
       if (bd.kind != PASTE_X_FORMAT) {
-        if (nt < PASTE_T_LIST && nt == at && !(nd.flags() & PASTE_F_NAN) && !D.act_nan[m]) {
+        if (nt < PASTE_T_LIST && nt == at && !(nd.flags() & PASTE_F_NAN) && !anan) {
           if (nt <= PASTE_T_TRUE) {
             eq = true;
           } else {
@@ -116,9 +146,35 @@ __global__ void holds_kernel(const paste_holds_desc D) {
   }
 }
 
+__global__ void key_lookup_kernel(const paste_key_lookup_desc D) {
+  unsigned long long scal = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < D.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const paste_event_ref ref = D.refs[D.tape[i]];
+    const int64_t c = step_child(D.nodes, ref.node_base, 0, 0, D.key);  // -1: no dict / key
+    D.out_node[i] = (int32_t)c;
+    if (c >= 0 && load_node(D.nodes, ref.node_base + c).type() < PASTE_T_LIST) ++scal;
+  }
+  for (int o = 16; o; o >>= 1) scal += __shfl_down_sync(0xffffffffu, scal, o);
+  if ((threadIdx.x & 31) == 0 && scal) atomicAdd(reinterpret_cast<unsigned long long*>(D.n_scalar), scal);
+}
+
 }  // namespace paste
 
 using namespace paste;
+
+extern "C" int paste_tape_key_lookup(const paste_key_lookup_desc* d, void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(d != nullptr, "null descriptor");
+  if (d->n == 0) return PASTE_OK;
+  PASTE_REQUIRE(d->nodes && d->refs && d->tape && d->out_node && d->n_scalar, "null array");
+  int64_t blocks = (d->n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  key_lookup_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(*d);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
 
 extern "C" int paste_holds(const paste_holds_desc* d, void* stream) {
   reset_launches();

@@ -242,6 +242,29 @@ def device_occurrences(tok_dev, flat_events: Sequence[Event], sigs: SigTable, ca
     (MatchedContext, next event) pairs of _collect_occurrences whose next
     event is the target (mining.py:215-227,277-279), in stream order.  The
     host only wraps the device's positions in the reference's objects."""
+    rel = cfg.match_relation is MatchRelation.CONTIGUOUS_SUFFIX
+    out = []
+    for (cs, _tool, _f), (anc, pk) in zip(cands, occurrence_positions(tok_dev, sigs, cands, cfg)):
+        L = len(cs)
+        occ = []
+        for r in range(len(anc)):
+            a = int(anc[r])
+            if rel:
+                sl = tuple(flat_events[a - L + 1:a + 1])
+                m = MatchedContext(events=sl, history=sl)
+            else:
+                pos = pk[r].tolist()
+                m = MatchedContext(events=tuple(flat_events[p] for p in pos),
+                                   history=tuple(flat_events[pos[0]:a + 1]))
+            occ.append((m, flat_events[a + 1]))
+        out.append(occ)
+    return out
+
+
+def occurrence_positions(tok_dev, sigs: SigTable, cands: list, cfg: MiningConfig) -> list:
+    """Per candidate (anchors int64[M], matched positions int32[M, len(ctx)])
+    in stream order, from one device pass (paste_mine_occurrences) and the K1
+    sort (candidate = session, anchor = t_start)."""
     from .device_ops import stream_handle
     from ._native import OccDesc
 
@@ -251,6 +274,8 @@ def device_occurrences(tok_dev, flat_events: Sequence[Event], sigs: SigTable, ca
     if C == 0:
         return []
     kmax = max(len(c[0]) for c in cands)
+    if tok_dev is None:
+        return [(np.zeros(0, np.int64), np.zeros((0, len(c[0])), np.int32)) for c in cands]
     n_tools = (sigs.n_sigs + 1) // 2
     ctx = np.zeros((C, kmax), np.int32)
     ctx_len = np.zeros(C, np.int32)
@@ -293,22 +318,8 @@ def device_occurrences(tok_dev, flat_events: Sequence[Event], sigs: SigTable, ca
     perm = srt.order.long()
     anc = anchor[:total][perm].cpu().numpy()
     pk = picked.view(-1, kmax)[:total][perm].cpu().numpy()
-    out = []
-    for i, (cs, _tool, f) in enumerate(cands):
-        L = len(cs)
-        occ = []
-        for r in range(int(off[i]), int(off[i + 1])):
-            a = int(anc[r])
-            pos = pk[r, :L]
-            if rel:
-                sl = tuple(flat_events[a - L + 1:a + 1])
-                m = MatchedContext(events=sl, history=sl)
-            else:
-                m = MatchedContext(events=tuple(flat_events[p] for p in pos.tolist()),
-                                   history=tuple(flat_events[int(pos[0]):a + 1]))
-            occ.append((m, flat_events[a + 1]))
-        out.append(occ)
-    return out
+    return [(anc[off[i]:off[i + 1]], pk[off[i]:off[i + 1], :len(cands[i][0])])
+            for i in range(C)]
 
 
 def _occurrences(streams, sig_streams, context: tuple, target: str, cfg: MiningConfig):
@@ -388,6 +399,31 @@ def _phase2(occ, cfg: MiningConfig, hits: int):
     return mapping, phase2_device.count_mapping_hits(mapping, occs)
 
 
+def _phase2_corpus(tok_dev, flat, sigs: SigTable, rows: list, idx: list, S: int,
+                   cfg: MiningConfig) -> dict:
+    """Phase II of every candidate over one corpus tape (phase2_corpus.py):
+    occurrence positions from the device pass, the argument test, hypothesis
+    scoring and mapping_holds counts on the device."""
+    from . import phase2_corpus as pc
+
+    cands = [(decode_context(r[1], S, cfg.k), r[0], r[4]) for r in rows]
+    positions = occurrence_positions(tok_dev, sigs, cands, cfg)
+    tok_host = tok_dev.cpu().numpy() if tok_dev is not None else np.zeros(0, np.int32)
+    ct = None
+    out = {}
+    for i, r, (anc, pk) in zip(idx, rows, positions):
+        first = flat[int(anc[0]) + 1].args if len(anc) else None
+        if len(anc) < 2 or not isinstance(first, dict) or not first:
+            out[i] = (None, r[4])
+            continue
+        if ct is None:
+            ct = pc.CorpusTapes.from_events(flat, tok_host, tok_dev, sigs)
+        co = pc.CorpusOccurrences(ct, anc, pk, sigs.tools[r[0]])
+        mapping = pc.infer_mapping(co, cfg.validation_fraction)
+        out[i] = (None, r[4]) if mapping is None else (mapping, pc.count_mapping_hits(mapping, co))
+    return out
+
+
 def mine(traces: Sequence[Session], cfg: MiningConfig, group=None) -> list[PatternTuple]:
     """mine() (mining.py:248-292).  With a torch.distributed ``group`` every
     rank passes its shard -- a contiguous range of the sessions, ranks in
@@ -410,21 +446,20 @@ def mine(traces: Sequence[Session], cfg: MiningConfig, group=None) -> list[Patte
     # one device pass; under sharding each rank collects its shard (its own
     # follow counts) and the lists are gathered in rank = stream order
     need = [i for i, r in enumerate(rows) if r[4] >= 2]
-    occ_of: dict[int, list] = {}
+    phase2_of: dict[int, tuple] = {}
     if need:
+        flat = [e for st in streams for e in st]
         if group is not None:  # this shard's follow counts size the slots
             local = _local_follow(tables, tok_dev, [rows[i] for i in need], S, cfg)
-        else:
-            local = [rows[i][4] for i in need]
-        flat = [e for st in streams for e in st]
-        lists = device_occurrences(
-            tok_dev, flat, sigs, [(decode_context(rows[i][1], S, cfg.k), rows[i][0], f)
-                                  for i, f in zip(need, local)], cfg) if tok_dev is not None \
-            else [[] for _ in need]
-        for i, occ in zip(need, lists):
-            if group is not None:
+            lists = device_occurrences(
+                tok_dev, flat, sigs, [(decode_context(rows[i][1], S, cfg.k), rows[i][0], f)
+                                      for i, f in zip(need, local)], cfg)
+            for i, occ in zip(need, lists):
                 occ = [o for part in _gather(occ, group) for o in part]
-            occ_of[i] = occ
+                phase2_of[i] = _phase2(occ, cfg, rows[i][4])
+        else:
+            phase2_of = _phase2_corpus(tok_dev, flat, sigs, [rows[i] for i in need], need, S,
+                                       cfg)
     patterns = []
     for i, (tool, cidx, support, n_match, follow) in enumerate(rows):
         context = tuple(sigs.signature(x) for x in decode_context(cidx, S, cfg.k))
@@ -432,7 +467,7 @@ def mine(traces: Sequence[Session], cfg: MiningConfig, group=None) -> list[Patte
         mapping = None
         hits = follow
         if follow >= 2:
-            mapping, hits = _phase2(occ_of[i], cfg, hits)
+            mapping, hits = phase2_of[i]
         p = hits / n_match
         if p >= cfg.tau:
             patterns.append(PatternTuple(context=context, target=target, mapping=mapping, p=p,

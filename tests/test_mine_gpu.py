@@ -355,7 +355,7 @@ def test_device_occurrences_equal_host_rescan(rel, k):
                              Status.FAIL if rng.random() < 0.2 else Status.SUCCESS, None, None,
                              float(j), float(j) + 0.5))
         sessions.append(Session(f"s{i}", tuple(evs)))
-    cfg = MiningConfig(k=k, sigma=2, tau=0.0, match_relation=rel)
+    cfg = MiningConfig(k=k, sigma=2, tau=1e-9, match_relation=rel)
     streams = [s.tool_events() for s in sessions]
     sigs, tables, tok_dev = _count_corpus(streams, cfg)
     rows = [r for r in tables.select(cfg.sigma, cfg.tau).tolist() if r[4] >= 2]
