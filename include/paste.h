@@ -353,6 +353,59 @@ typedef struct {
 #define PASTE_INGEST_EMPTY_TOOL 0x400
 
 int paste_ingest_jsonl(const char* text, int64_t len, double inactivity_ms, paste_ingest_desc* d);
+
+/* Native JSONL parse feeding the DEVICE ingest (K1 general path,
+ * paste_ingest_order) and device Phase II: _parse_record (events.py:
+ * 165-184) for every line in parallel, with the records' payloads.
+ * Output, in FILE order, one row per valid record (errors as above):
+ * session = first-appearance index of session_id, sig = 2 * tool + success
+ * (tools in sorted name order) or -1 for an LLM step; and, with
+ * want_payloads, the record's `result` and `args` (record.get: absent =
+ * null) as payload tapes (tape.py layout, canonical scalar bytes of
+ * events.py:94-130: ints as digits, integral floats as int digits with
+ * FLOATSRC, other floats as Python's repr, strings as UTF-8): tape 2r =
+ * result of row r, 2r + 1 = its args; dict keys interned in first-seen
+ * order (key_names: NUL-separated, id = position).  The grouping, sort and
+ * gap split are left to the device.  Input outside the parser's exact
+ * subset (see paste_ingest_jsonl, plus: payload strings with a lone
+ * surrogate or a code point >= U+0300 whose NFC form needs the Unicode
+ * database, duplicate keys inside a payload, nesting deeper than 512)
+ * returns PASTE_ERR_UNSUPPORTED: use the host ingest.  The result is an
+ * opaque host handle: query sizes, copy into caller buffers, destroy.     */
+typedef struct paste_jsonl paste_jsonl;
+typedef struct {
+  int64_t n_rows;
+  int64_t n_sessions;
+  int64_t n_errors;
+  int64_t n_lines;
+  int64_t n_nodes;
+  int64_t n_bytes;
+  int64_t n_keys;
+  int64_t key_names_len;
+  int64_t tool_names_len;
+  int32_t n_tools;
+  int32_t pad;
+} paste_jsonl_sizes;
+typedef struct {             /* host buffers sized by paste_jsonl_sizes      */
+  int32_t* session;          /* [n_rows]                                     */
+  int32_t* seq;
+  double* t_start;
+  double* t_end;
+  int32_t* sig;
+  int32_t* error_lines;      /* [n_errors]                                   */
+  int32_t* error_codes;
+  int64_t* error_seq;
+  char* tool_names;          /* [tool_names_len]                             */
+  paste_tape_node* nodes;    /* [n_nodes]      (payloads only)               */
+  uint8_t* bytes;            /* [n_bytes]                                    */
+  paste_event_ref* refs;     /* [2 * n_rows]                                 */
+  char* key_names;           /* [key_names_len]                              */
+} paste_jsonl_out;
+
+int paste_jsonl_parse(const char* text, int64_t len, int32_t want_payloads, paste_jsonl** out);
+int paste_jsonl_sizes_of(const paste_jsonl* h, paste_jsonl_sizes* s);
+int paste_jsonl_copy(const paste_jsonl* h, const paste_jsonl_out* o);
+void paste_jsonl_destroy(paste_jsonl* h);
 /* Same, in two passes: the columnar pass writes one staged word per event
  * (4 B) to `stage`; a second pass sends the cold grams to L2 into 8
  * histogram replicas (a hot gram's updates spread over 8 addresses), which
@@ -404,6 +457,9 @@ typedef struct {
   double* out_t_end;
   int32_t* out_sig;
   int32_t* order;           /* optional [n]                                  */
+  int32_t* out_tok;         /* optional [n]: flagged token stream of the
+                               output (sig, bit 31 on a segment's first tool
+                               event) for paste_mine_count / occurrences     */
   int64_t* n_out;           /* device scalars                                */
   int64_t* n_segments;
   int64_t* reordered;

@@ -95,8 +95,20 @@ class OrderDesc(ctypes.Structure):
                 ("t_end", c_void_p), ("sig", c_void_p), ("inactivity_ms", ctypes.c_double),
                 ("out_session", c_void_p), ("out_seq", c_void_p), ("out_t_start", c_void_p),
                 ("out_t_end", c_void_p), ("out_sig", c_void_p), ("order", c_void_p),
-                ("n_out", c_void_p), ("n_segments", c_void_p), ("reordered", c_void_p),
+                ("out_tok", c_void_p), ("n_out", c_void_p), ("n_segments", c_void_p), ("reordered", c_void_p),
                 ("status", c_void_p)]
+
+
+class JsonlSizes(ctypes.Structure):
+    _fields_ = [(n, c_int64) for n in ("n_rows", "n_sessions", "n_errors", "n_lines", "n_nodes",
+                                       "n_bytes", "n_keys", "key_names_len", "tool_names_len")] + \
+        [("n_tools", c_int32), ("pad", c_int32)]
+
+
+class JsonlOut(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in ("session", "seq", "t_start", "t_end", "sig",
+                                        "error_lines", "error_codes", "error_seq", "tool_names",
+                                        "nodes", "bytes", "refs", "key_names")]
 
 
 class OccDesc(ctypes.Structure):
@@ -248,6 +260,10 @@ EXPORTS = {
                                            POINTER(CompactDesc), c_void_p, c_int64, c_void_p]),
     "paste_canonical_hash": (c_int, [POINTER(HashDesc), c_void_p]),
     "paste_ingest_jsonl": (c_int, [c_char_p, c_int64, ctypes.c_double, POINTER(IngestDesc)]),
+    "paste_jsonl_parse": (c_int, [c_char_p, c_int64, c_int32, POINTER(c_void_p)]),
+    "paste_jsonl_sizes_of": (c_int, [c_void_p, POINTER(JsonlSizes)]),
+    "paste_jsonl_copy": (c_int, [c_void_p, POINTER(JsonlOut)]),
+    "paste_jsonl_destroy": (None, [c_void_p]),
     "paste_action_keys": (c_int, [POINTER(ActionKeysDesc), c_void_p]),
     "paste_action_jobs_scratch_bytes": (c_int64, [c_int64]),
     "paste_action_jobs": (c_int, [POINTER(ActionsDesc), POINTER(JobsOut), c_void_p, c_int64,

@@ -165,8 +165,269 @@ void skip_value(Cursor& c, int depth) {
   parse_number(c, &integral);
 }
 
+// ---------------------------------------------------------------------------
+// payload tapes (tape.py layout) for _parse_record's args / result
+// ---------------------------------------------------------------------------
+struct TNode {
+  uint8_t type, flags;
+  uint16_t pad;
+  int32_t key;
+  uint32_t a, b;
+};
+static_assert(sizeof(TNode) == 16, "tape node is 16 bytes");
+
+enum { T_NULL = 0, T_FALSE, T_TRUE, T_INT, T_FLOAT, T_STR, T_LIST, T_DICT };
+enum { F_FLOATSRC = 2, F_NAN = 4, F_ASCII = 8 };
+
+struct Tape {
+  std::vector<TNode> nodes;
+  std::vector<uint8_t> bytes;
+};
+
+struct LineTapes {
+  Tape result, args;
+  bool has_result = false, has_args = false;
+  std::vector<std::string> keys;  // line-local key ids
+  std::unordered_map<std::string, int32_t> key_id;
+  int32_t intern(const std::string& k) {
+    auto it = key_id.find(k);
+    if (it != key_id.end()) return it->second;
+    const int32_t id = (int32_t)keys.size();
+    keys.push_back(k);
+    key_id.emplace(k, id);
+    return id;
+  }
+};
+
+void put_utf8(std::string& out, uint32_t cp) {
+  if (cp < 0x80) {
+    out += (char)cp;
+  } else if (cp < 0x800) {
+    out += (char)(0xC0 | (cp >> 6));
+    out += (char)(0x80 | (cp & 0x3F));
+  } else if (cp < 0x10000) {
+    out += (char)(0xE0 | (cp >> 12));
+    out += (char)(0x80 | ((cp >> 6) & 0x3F));
+    out += (char)(0x80 | (cp & 0x3F));
+  } else {
+    out += (char)(0xF0 | (cp >> 18));
+    out += (char)(0x80 | ((cp >> 12) & 0x3F));
+    out += (char)(0x80 | ((cp >> 6) & 0x3F));
+    out += (char)(0x80 | (cp & 0x3F));
+  }
+}
+
+// JSON string -> UTF-8 text (json.loads).  `nfc_safe` is cleared when the
+// text holds a lone surrogate or a code point >= U+0300 (its NFC form then
+// needs the Unicode database: the caller hands the trace to the host);
+// `ascii` tells whether every byte is < 0x80.
+bool unescape(Cursor& c, std::string& out, bool* ascii, bool* nfc_safe) {
+  bool esc;
+  const std::string_view raw = parse_string(c, &esc);
+  if (!c.ok) return false;
+  out.clear();
+  *ascii = true;
+  *nfc_safe = true;
+  for (size_t i = 0; i < raw.size();) {
+    const unsigned char ch = (unsigned char)raw[i];
+    if (ch == '\\') {
+      const char x = raw[i + 1];
+      if (x != 'u') {
+        const char* m = "\"\\/bfnrt";
+        const char* r = "\"\\/\b\f\n\r\t";
+        out += r[strchr(m, x) - m];
+        i += 2;
+        continue;
+      }
+      uint32_t cp = (uint32_t)strtoul(std::string(raw.substr(i + 2, 4)).c_str(), nullptr, 16);
+      i += 6;
+      if (cp >= 0xD800 && cp < 0xDC00 && i + 6 <= raw.size() && raw[i] == '\\' &&
+          raw[i + 1] == 'u') {
+        const uint32_t lo =
+            (uint32_t)strtoul(std::string(raw.substr(i + 2, 4)).c_str(), nullptr, 16);
+        if (lo >= 0xDC00 && lo < 0xE000) {
+          cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+          i += 6;
+        }
+      }
+      if (cp >= 0xD800 && cp < 0xE000) *nfc_safe = false;  // lone surrogate
+      if (cp >= 0x80) *ascii = false;
+      if (cp >= 0x300) *nfc_safe = false;
+      put_utf8(out, cp);
+      continue;
+    }
+    if (ch >= 0x80) {  // raw UTF-8 (valid: Python decoded the text)
+      *ascii = false;
+      uint32_t cp;
+      int n;
+      if (ch >= 0xF0) { cp = ch & 7; n = 3; }
+      else if (ch >= 0xE0) { cp = ch & 15; n = 2; }
+      else { cp = ch & 31; n = 1; }
+      for (int k = 1; k <= n && i + k < raw.size(); ++k) cp = (cp << 6) | (raw[i + k] & 0x3F);
+      if (cp >= 0x300) *nfc_safe = false;
+      out.append(raw.data() + i, (size_t)n + 1);
+      i += (size_t)n + 1;
+      continue;
+    }
+    out += (char)ch;
+    ++i;
+  }
+  return true;
+}
+
+// str(int(x)) of an integral double (exact, any magnitude)
+std::string int_digits(double x) {
+  const bool neg = x < 0;
+  double ax = std::fabs(x);
+  if (ax < 9.0e18) {
+    const unsigned long long v = (unsigned long long)ax;
+    std::string s = std::to_string(v);
+    return (neg && v) ? "-" + s : s;
+  }
+  int e;
+  const double f = std::frexp(ax, &e);                 // ax = f * 2^e, f in [0.5, 1)
+  uint64_t m = (uint64_t)std::ldexp(f, 53);            // ax = m * 2^(e - 53)
+  int shift = e - 53;
+  std::vector<uint32_t> big;                           // base 1e9, little endian
+  while (m) { big.push_back((uint32_t)(m % 1000000000ull)); m /= 1000000000ull; }
+  while (shift > 0) {
+    const int k = shift > 28 ? 28 : shift;
+    uint64_t carry = 0;
+    for (auto& d : big) {
+      const uint64_t v = ((uint64_t)d << k) + carry;
+      d = (uint32_t)(v % 1000000000ull);
+      carry = v / 1000000000ull;
+    }
+    while (carry) { big.push_back((uint32_t)(carry % 1000000000ull)); carry /= 1000000000ull; }
+    shift -= k;
+  }
+  std::string s = std::to_string(big.back());
+  char buf[16];
+  for (size_t i = big.size() - 1; i-- > 0;) {
+    snprintf(buf, sizeof buf, "%09u", big[i]);
+    s += buf;
+  }
+  return neg ? "-" + s : s;
+}
+
+// repr(x) of a finite non-integral double: the shortest digits that round
+// trip (the correctly rounded p-digit form for the least p that does), in
+// Python's float_repr_style layout (exponent when decpt <= -4 or > 16).
+std::string py_repr(double x) {
+  char buf[40];
+  int p = 1;
+  for (; p <= 17; ++p) {
+    snprintf(buf, sizeof buf, "%.*e", p - 1, x);
+    if (strtod(buf, nullptr) == x) break;
+  }
+  std::string t(buf);
+  const bool neg = t[0] == '-';
+  if (neg) t.erase(0, 1);
+  const size_t epos = t.find('e');
+  const int exp10 = atoi(t.c_str() + epos + 1);
+  std::string digits;
+  for (size_t i = 0; i < epos; ++i)
+    if (t[i] != '.') digits += t[i];
+  while (digits.size() > 1 && digits.back() == '0') digits.pop_back();
+  const int decpt = exp10 + 1;
+  std::string out;
+  if (decpt <= -4 || decpt > 16) {
+    out = digits.substr(0, 1);
+    if (digits.size() > 1) out += "." + digits.substr(1);
+    const int ex = decpt - 1;
+    snprintf(buf, sizeof buf, "e%c%02d", ex < 0 ? '-' : '+', ex < 0 ? -ex : ex);
+    out += buf;
+  } else if (decpt <= 0) {
+    out = "0." + std::string((size_t)-decpt, '0') + digits;
+  } else if ((size_t)decpt >= digits.size()) {
+    out = digits + std::string((size_t)decpt - digits.size(), '0') + ".0";
+  } else {
+    out = digits.substr(0, (size_t)decpt) + "." + digits.substr((size_t)decpt);
+  }
+  return neg ? "-" + out : out;
+}
+
+void push_scalar(Tape& t, int32_t key, uint8_t type, uint8_t flags, const std::string& data) {
+  TNode nd{type, flags, 0, key, (uint32_t)t.bytes.size(), (uint32_t)data.size()};
+  t.bytes.insert(t.bytes.end(), data.begin(), data.end());
+  t.nodes.push_back(nd);
+}
+
+// one JSON value -> tape nodes (pre-order; dict children in document order,
+// which is json.loads' insertion order when no key repeats)
+bool emit_value(Cursor& c, int32_t key, Tape& t, LineTapes& lt, int depth) {
+  c.ws();
+  if (!c.ok || c.p >= c.e || depth > 512) return c.ok = false;
+  const char ch = *c.p;
+  if (ch == '{' || ch == '[') {
+    const bool dict = ch == '{';
+    const size_t idx = t.nodes.size();
+    t.nodes.push_back(TNode{(uint8_t)(dict ? T_DICT : T_LIST), 0, 0, key, 0, 0});
+    ++c.p;
+    c.ws();
+    uint32_t n = 0;
+    std::vector<int32_t> seen;
+    if (c.p < c.e && *c.p == (dict ? '}' : ']')) {
+      ++c.p;
+    } else {
+      while (true) {
+        int32_t ck = -1;
+        if (dict) {
+          c.ws();
+          std::string k;
+          bool ascii, safe;
+          if (!unescape(c, k, &ascii, &safe) || !safe) return c.ok = false;
+          ck = lt.intern(k);
+          if (std::find(seen.begin(), seen.end(), ck) != seen.end()) return c.ok = false;
+          seen.push_back(ck);
+          c.ws();
+          if (c.p >= c.e || *c.p != ':') return c.ok = false;
+          ++c.p;
+        }
+        if (!emit_value(c, ck, t, lt, depth + 1)) return false;
+        ++n;
+        c.ws();
+        if (c.p < c.e && *c.p == ',') { ++c.p; continue; }
+        if (c.p < c.e && *c.p == (dict ? '}' : ']')) { ++c.p; break; }
+        return c.ok = false;
+      }
+    }
+    t.nodes[idx].a = n;
+    t.nodes[idx].b = (uint32_t)(t.nodes.size() - idx);
+    return true;
+  }
+  if (ch == '"') {
+    std::string v;
+    bool ascii, safe;
+    if (!unescape(c, v, &ascii, &safe) || !safe) return c.ok = false;
+    push_scalar(t, key, T_STR, ascii ? F_ASCII : 0, v);
+    return true;
+  }
+  if (ch == 't') { if (!c.lit("true")) return false; push_scalar(t, key, T_TRUE, 0, ""); return true; }
+  if (ch == 'f') { if (!c.lit("false")) return false; push_scalar(t, key, T_FALSE, 0, ""); return true; }
+  if (ch == 'n') { if (!c.lit("null")) return false; push_scalar(t, key, T_NULL, 0, ""); return true; }
+  bool integral;
+  const std::string_view v = parse_number(c, &integral);
+  if (!c.ok || v.empty()) return c.ok = false;
+  if (integral) {  // int(literal): "-0" is 0
+    push_scalar(t, key, T_INT, F_ASCII, v == "-0" ? std::string("0") : std::string(v));
+    return true;
+  }
+  double x;
+  if (v == "NaN") x = NAN;
+  else if (v == "Infinity") x = INFINITY;
+  else if (v == "-Infinity") x = -INFINITY;
+  else x = strtod(std::string(v).c_str(), nullptr);
+  if (std::isnan(x)) push_scalar(t, key, T_FLOAT, F_NAN | F_ASCII, "nan");
+  else if (std::isinf(x)) push_scalar(t, key, T_FLOAT, F_ASCII, x > 0 ? "inf" : "-inf");
+  else if (x == std::floor(x)) push_scalar(t, key, T_INT, F_FLOATSRC | F_ASCII, int_digits(x));
+  else push_scalar(t, key, T_FLOAT, F_ASCII, py_repr(x));
+  return true;
+}
+
 // One line -> record.  L_ODD = outside what this parser reproduces exactly.
-void parse_line(const char* b, const char* e, Rec& r) {
+// With `lt`, the record's `result` / `args` values become payload tapes.
+void parse_line(const char* b, const char* e, Rec& r, LineTapes* lt = nullptr) {
   Cursor c{b, e};
   c.ws();
   if (c.p == c.e) { r.kind = L_EMPTY; return; }
@@ -231,6 +492,11 @@ void parse_line(const char* b, const char* e, Rec& r) {
           r.t_end = x;
         }
       }
+    } else if (lt && (key == "result" || key == "args")) {
+      const bool res = key == "result";
+      if (res ? lt->has_result : lt->has_args) { r.kind = L_ODD; return; }  // last wins in Python
+      (res ? lt->has_result : lt->has_args) = true;
+      if (!emit_value(c, -1, res ? lt->result : lt->args, *lt, 1)) { r.kind = L_ODD; return; }
     } else {
       skip_value(c, 1);
       if (!c.ok) { r.kind = L_ODD; return; }
@@ -400,3 +666,174 @@ extern "C" int paste_ingest_jsonl(const char* text, int64_t len, double inactivi
   }
   return PASTE_OK;
 }
+
+
+// ---------------------------------------------------------------------------
+// raw parse for the device ingest path (paste_jsonl_*)
+// ---------------------------------------------------------------------------
+struct paste_jsonl {
+  std::vector<int32_t> session, seq, sig, err_line, err_code;
+  std::vector<int64_t> err_seq;
+  std::vector<double> t_start, t_end;
+  std::string tool_names, key_names;
+  std::vector<TNode> nodes;
+  std::vector<uint8_t> bytes;
+  std::vector<paste_event_ref> refs;
+  int64_t n_sessions = 0, n_lines = 0, n_keys = 0;
+  int32_t n_tools = 0;
+};
+
+extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_payloads,
+                                 paste_jsonl** out) {
+  paste::reset_launches();
+  if (!text || !out || len < 0) {
+    set_error("null argument");
+    return PASTE_ERR_INVALID;
+  }
+  *out = nullptr;
+  if (odd_line_breaks(text, len)) {
+    set_error("line separators other than '\\n': host ingest");
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  std::vector<int64_t> starts{0};
+  for (int64_t i = 0; i < len; ++i)
+    if (text[i] == '\n' && i + 1 < len) starts.push_back(i + 1);
+  const int64_t n_lines = len == 0 ? 0 : (int64_t)starts.size();
+  std::vector<Rec> recs(n_lines);
+  std::vector<LineTapes> tapes(want_payloads ? n_lines : 0);
+  bool odd = false;
+#pragma omp parallel for schedule(dynamic, 1024) reduction(|| : odd)
+  for (int64_t i = 0; i < n_lines; ++i) {
+    const char* b = text + starts[i];
+    const char* e = i + 1 < n_lines ? text + starts[i + 1] - 1 : text + len;
+    if (e > b && e[-1] == '\n') --e;
+    recs[i].line = (int32_t)(i + 1);
+    parse_line(b, e, recs[i], want_payloads ? &tapes[i] : nullptr);
+    odd = odd || recs[i].kind == L_ODD;
+  }
+  if (odd) {
+    set_error("records outside the native parser's exact subset: host ingest");
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  auto* h = new paste_jsonl();
+  h->n_lines = n_lines;
+  std::unordered_map<std::string_view, int32_t> sid, tool_id;
+  std::vector<std::string_view> tools;
+  std::unordered_map<std::string, int32_t> key_id;
+  std::vector<int32_t> remap;
+  int64_t n_rows = 0;
+  for (int64_t i = 0; i < n_lines; ++i) {
+    const Rec& r = recs[i];
+    if (r.kind == L_EMPTY) continue;
+    if (r.kind == L_MISSING || r.kind == L_INVALID) {
+      h->err_line.push_back(r.line);
+      h->err_code.push_back(r.reason);
+      h->err_seq.push_back(r.seq);
+      continue;
+    }
+    auto it = sid.find(r.session);
+    if (it == sid.end()) it = sid.emplace(r.session, (int32_t)sid.size()).first;
+    h->session.push_back(it->second);
+    h->seq.push_back((int32_t)r.seq);
+    h->t_start.push_back(r.t_start);
+    h->t_end.push_back(r.t_end);
+    int32_t tid = -1;
+    if (r.tool_call) {
+      auto t = tool_id.find(r.tool);
+      if (t == tool_id.end()) {
+        t = tool_id.emplace(r.tool, (int32_t)tools.size()).first;
+        tools.push_back(r.tool);
+      }
+      tid = t->second;
+    }
+    h->sig.push_back(tid < 0 ? -1 : (tid << 1) | (r.success ? 1 : 0));  // tool rank applied below
+    ++n_rows;
+    if (!want_payloads) continue;
+    LineTapes& lt = tapes[i];
+    remap.assign(lt.keys.size(), -1);
+    for (size_t k = 0; k < lt.keys.size(); ++k) {
+      auto g = key_id.find(lt.keys[k]);
+      if (g == key_id.end()) {
+        g = key_id.emplace(lt.keys[k], (int32_t)key_id.size()).first;
+        h->key_names.append(lt.keys[k]);
+        h->key_names.push_back('\0');
+      }
+      remap[k] = g->second;
+    }
+    for (Tape* t : {&lt.result, &lt.args}) {
+      h->refs.push_back(paste_event_ref{(int64_t)h->nodes.size(), (int64_t)h->bytes.size()});
+      if (t->nodes.empty()) t->nodes.push_back(TNode{T_NULL, 0, 0, -1, 0, 0});  // absent: None
+      for (TNode nd : t->nodes) {
+        if (nd.key >= 0) nd.key = remap[nd.key];
+        h->nodes.push_back(nd);
+      }
+      h->bytes.insert(h->bytes.end(), t->bytes.begin(), t->bytes.end());
+    }
+    LineTapes().keys.swap(lt.keys);  // release the line's memory early
+    lt.result = Tape();
+    lt.args = Tape();
+  }
+  h->n_keys = (int64_t)key_id.size();
+  h->n_sessions = (int64_t)sid.size();
+  // tools in sorted name order: sig = 2 * rank + success
+  std::vector<int32_t> order(tools.size());
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return tools[a] < tools[b]; });
+  std::vector<int32_t> rank(tools.size());
+  for (size_t r = 0; r < order.size(); ++r) {
+    rank[order[r]] = (int32_t)r;
+    h->tool_names.append(tools[order[r]].data(), tools[order[r]].size());
+    h->tool_names.push_back('\0');
+  }
+  for (auto& sg : h->sig)
+    if (sg >= 0) sg = 2 * rank[sg >> 1] + (sg & 1);
+  h->n_tools = (int32_t)tools.size();
+  *out = h;
+  return PASTE_OK;
+}
+
+extern "C" int paste_jsonl_sizes_of(const paste_jsonl* h, paste_jsonl_sizes* s) {
+  if (!h || !s) {
+    set_error("null argument");
+    return PASTE_ERR_INVALID;
+  }
+  s->n_rows = (int64_t)h->session.size();
+  s->n_sessions = h->n_sessions;
+  s->n_errors = (int64_t)h->err_line.size();
+  s->n_lines = h->n_lines;
+  s->n_nodes = (int64_t)h->nodes.size();
+  s->n_bytes = (int64_t)h->bytes.size();
+  s->n_keys = h->n_keys;
+  s->key_names_len = (int64_t)h->key_names.size();
+  s->tool_names_len = (int64_t)h->tool_names.size();
+  s->n_tools = h->n_tools;
+  s->pad = 0;
+  return PASTE_OK;
+}
+
+extern "C" int paste_jsonl_copy(const paste_jsonl* h, const paste_jsonl_out* o) {
+  if (!h || !o) {
+    set_error("null argument");
+    return PASTE_ERR_INVALID;
+  }
+  auto cp = [](void* dst, const void* src, size_t n) {
+    if (dst && n) memcpy(dst, src, n);
+  };
+  const size_t n = h->session.size();
+  cp(o->session, h->session.data(), 4 * n);
+  cp(o->seq, h->seq.data(), 4 * n);
+  cp(o->t_start, h->t_start.data(), 8 * n);
+  cp(o->t_end, h->t_end.data(), 8 * n);
+  cp(o->sig, h->sig.data(), 4 * n);
+  cp(o->error_lines, h->err_line.data(), 4 * h->err_line.size());
+  cp(o->error_codes, h->err_code.data(), 4 * h->err_code.size());
+  cp(o->error_seq, h->err_seq.data(), 8 * h->err_seq.size());
+  cp(o->tool_names, h->tool_names.data(), h->tool_names.size());
+  cp(o->nodes, h->nodes.data(), sizeof(TNode) * h->nodes.size());
+  cp(o->bytes, h->bytes.data(), h->bytes.size());
+  cp(o->refs, h->refs.data(), sizeof(paste_event_ref) * h->refs.size());
+  cp(o->key_names, h->key_names.data(), h->key_names.size());
+  return PASTE_OK;
+}
+
+extern "C" void paste_jsonl_destroy(paste_jsonl* h) { delete h; }

@@ -512,6 +512,18 @@ __global__ void __launch_bounds__(OT) order_number_kernel(const paste_order_desc
   }
 }
 
+__global__ void __launch_bounds__(OT) order_tok_kernel(const paste_order_desc d,
+                                                       const int64_t* tbase,
+                                                       const OrderCounters* c) {
+  if (c->bad_session != 0) return;
+  const int64_t n_out = tbase[d.n_sessions];
+  for (int64_t p = (int64_t)blockIdx.x * OT + threadIdx.x; p < n_out;
+       p += (int64_t)gridDim.x * OT) {
+    const bool first = p == 0 || d.out_session[p] != d.out_session[p - 1];
+    d.out_tok[p] = d.out_sig[p] | (first ? (int32_t)0x80000000 : 0);
+  }
+}
+
 __global__ void order_finish_kernel(const paste_order_desc d, const int64_t* tbase,
                                     const int64_t* sbase, const OrderCounters* c) {
   const bool bad = c->bad_session != 0;
@@ -624,6 +636,10 @@ extern "C" int paste_ingest_order(const paste_order_desc* d, void* scratch, int6
   if (rc) return rc;
   if (S > 0) {
     order_number_kernel<<<grid_ss, OT, 0, st>>>(D, sc.tbase, sc.sbase, sc.counters);
+    ++launches;
+  }
+  if (d->out_tok && n > 0) {
+    order_tok_kernel<<<grid_ev, OT, 0, st>>>(D, sc.tbase, sc.counters);
     ++launches;
   }
   order_finish_kernel<<<1, 1, 0, st>>>(D, sc.tbase, sc.sbase, sc.counters);

@@ -102,19 +102,110 @@ def ingest_columnar(source: str | bytes,
                          d.reordered_sessions, errors)
 
 
+@dataclass
+class RawTrace:
+    """paste_jsonl_parse output: valid records in FILE order (the input of the
+    device K1 path) and, optionally, their payload tapes."""
+    columns: dict[str, np.ndarray]   # session (first-appearance id), seq, t_start, t_end, sig
+    n_sessions: int
+    sigs: SigTable
+    errors: list[IngestError]
+    tapes: tuple | None = None       # (nodes, data, refs): tape 2r = result, 2r + 1 = args
+    keys: Any = None                 # KeyTable of the tapes
+
+
+def parse_jsonl_raw(source: str | bytes, payloads: bool = True) -> RawTrace | None:
+    """Native parallel parse (paste_jsonl_parse) of a JSONL trace; None when
+    the input is outside the parser's exact subset (use the host ingest)."""
+    from ._native import JsonlOut, JsonlSizes
+    from .tape import NODE_DTYPE, KeyTable
+
+    text = source.decode("utf-8") if isinstance(source, bytes) else source
+    raw = text.encode("utf-8", "surrogatepass")
+    lib = _native.load_library()
+    h = ctypes.c_void_p()
+    rc = lib.paste_jsonl_parse(raw, len(raw), 1 if payloads else 0, ctypes.byref(h))
+    if rc == PASTE_ERR_UNSUPPORTED:
+        return None
+    check(rc, lib)
+    try:
+        z = JsonlSizes()
+        check(lib.paste_jsonl_sizes_of(h, ctypes.byref(z)), lib)
+        n = z.n_rows
+        cols = {"session": np.empty(n, np.int32), "seq": np.empty(n, np.int32),
+                "t_start": np.empty(n, np.float64), "t_end": np.empty(n, np.float64),
+                "sig": np.empty(n, np.int32)}
+        err = [np.empty(z.n_errors, np.int32), np.empty(z.n_errors, np.int32),
+               np.empty(z.n_errors, np.int64)]
+        tools = ctypes.create_string_buffer(max(z.tool_names_len, 1))
+        nodes = np.empty(z.n_nodes, NODE_DTYPE)
+        data = np.empty(max(z.n_bytes, 1), np.uint8)
+        refs = np.empty((2 * n if payloads else 0, 2), np.int64)
+        knames = ctypes.create_string_buffer(max(z.key_names_len, 1))
+        o = JsonlOut(*[c.ctypes.data for c in cols.values()], *[e.ctypes.data for e in err],
+                     ctypes.addressof(tools), nodes.ctypes.data, data.ctypes.data,
+                     refs.ctypes.data, ctypes.addressof(knames))
+        check(lib.paste_jsonl_copy(h, ctypes.byref(o)), lib)
+    finally:
+        lib.paste_jsonl_destroy(h)
+    names = tools.raw[:z.tool_names_len].split(b"\0")[:z.n_tools]
+    sigs = SigTable([t.decode("utf-8", "surrogatepass") for t in names])
+    errors = [IngestError(int(line), _error_message(int(c), int(q))) for line, c, q in zip(*err)]
+    tr = RawTrace(cols, int(z.n_sessions), sigs, errors)
+    if payloads:
+        keys = KeyTable()
+        for k in knames.raw[:z.key_names_len].split(b"\0")[:z.n_keys]:
+            keys.intern(k.decode("utf-8", "surrogatepass"))
+        tr.tapes, tr.keys = (nodes, data, refs), keys
+    return tr
+
+
 def mine_jsonl(source: str | bytes, cfg: Any = None,
                inactivity_ms: float = DEFAULT_INACTIVITY_THRESHOLD_MS, group=None):
-    """mine(ingest_trace(source).sessions, cfg) through the columnar path:
-    native ingest, then the device count / expand / select."""
+    """mine(ingest_trace(source).sessions, cfg) with the trace never
+    materialised as Python sessions: native parallel parse of the records
+    and their payload tapes (paste_jsonl_parse), then on the device the K1
+    grouping / stable sort / gap split (paste_ingest_order), the count,
+    selection and Phase II over the corpus tapes (mappings included).
+    Input outside the native parser's exact subset goes through the host
+    ingest_trace and the device mine() of its sessions: same result."""
     import torch
 
-    from .mine_engine import mine_columnar
-    from .mining import MiningConfig
+    from . import phase2_corpus as pc
+    from .mine_engine import MineTables, _select_patterns, mine, order_columnar
+    from .mining import MatchRelation, MiningConfig
 
-    tr = ingest_columnar(source, inactivity_ms)
-    if tr.n_events == 0:
-        raise ValueError("traces must be non-empty")
+    cfg = cfg or MiningConfig()
+    tr = parse_jsonl_raw(source, payloads=group is None)
+    if tr is None or group is not None:
+        text = source.decode("utf-8") if isinstance(source, bytes) else source
+        if group is not None:  # sharded: every rank mines its sessions, merged on device
+            res = ingest_trace(text, inactivity_ms)
+            return mine(res.sessions, cfg, group)
+        return mine(ingest_trace(text, inactivity_ms).sessions, cfg)
+    sig_raw = tr.columns["sig"]
     dev = {k: torch.from_numpy(np.ascontiguousarray(v)).cuda() for k, v in tr.columns.items()}
-    # segments are already split: the count pass only follows the segment ids
-    return mine_columnar(dev, tr.sigs, cfg or MiningConfig(), inactivity_ms=float("inf"),
-                         group=group)
+    ordered = order_columnar(dev, tr.n_sessions, inactivity_ms, with_order=True,
+                             with_tokens=True)
+    if ordered.n_segments == 0:
+        raise ValueError("traces must be non-empty")
+    rel = 0 if cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE else 1
+    tables = MineTables.allocate(max(tr.sigs.n_sigs, 2), cfg.k, rel)
+    tok_dev = ordered.tokens
+    if tok_dev.numel():
+        tables.count(tok_dev)
+    tables.expand()
+    order = ordered.order.cpu().numpy()
+    rows = order[sig_raw[order] >= 0]          # arrival row of every tool event, stream order
+    tok_host = tok_dev.cpu().numpy()
+    cols = {k: tr.columns[k][rows] for k in ("seq", "t_start", "t_end")}
+    res_tape, args_tape = 2 * rows.astype(np.int64), 2 * rows.astype(np.int64) + 1
+    events = pc.TapeEvents(tr.tapes, tr.keys, tr.sigs, tok_host, res_tape, args_tape, cols)
+
+    def corpus():
+        nodes, data, refs = tr.tapes
+        return pc.CorpusTapes(nodes, data, refs, tr.keys, tok_host, tok_dev if tok_dev.numel()
+                              else None, tr.sigs, events, res_tape, args_tape)
+
+    return _select_patterns(tables, tr.sigs, tok_dev if tok_dev.numel() else None, events, cfg,
+                            corpus=corpus)

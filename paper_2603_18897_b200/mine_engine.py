@@ -400,7 +400,7 @@ def _phase2(occ, cfg: MiningConfig, hits: int):
 
 
 def _phase2_corpus(tok_dev, flat, sigs: SigTable, rows: list, idx: list, S: int,
-                   cfg: MiningConfig) -> dict:
+                   cfg: MiningConfig, corpus=None) -> dict:
     """Phase II of every candidate over one corpus tape (phase2_corpus.py):
     occurrence positions from the device pass, the argument test, hypothesis
     scoring and mapping_holds counts on the device."""
@@ -417,7 +417,8 @@ def _phase2_corpus(tok_dev, flat, sigs: SigTable, rows: list, idx: list, S: int,
             out[i] = (None, r[4])
             continue
         if ct is None:
-            ct = pc.CorpusTapes.from_events(flat, tok_host, tok_dev, sigs)
+            ct = corpus() if corpus is not None else \
+                pc.CorpusTapes.from_events(flat, tok_host, tok_dev, sigs)
         co = pc.CorpusOccurrences(ct, anc, pk, sigs.tools[r[0]])
         mapping = pc.infer_mapping(co, cfg.validation_fraction)
         out[i] = (None, r[4]) if mapping is None else (mapping, pc.count_mapping_hits(mapping, co))
@@ -437,6 +438,15 @@ def mine(traces: Sequence[Session], cfg: MiningConfig, group=None) -> list[Patte
         raise ValueError("traces must be non-empty")
     streams = [s.tool_events() for s in traces]
     sigs, tables, tok_dev = _count_corpus(streams, cfg, group)
+    flat = [e for st in streams for e in st]
+    return _select_patterns(tables, sigs, tok_dev, flat, cfg, group)
+
+
+def _select_patterns(tables: "MineTables", sigs: SigTable, tok_dev, flat: Sequence, cfg,
+                     group=None, corpus=None) -> list[PatternTuple]:
+    """Selection + Phase II + the reference's order (mining.py:264-292) over a
+    counted corpus: ``flat`` maps stream positions to events (a list, or a
+    lazy view over tapes); ``corpus`` builds the CorpusTapes on first need."""
     cands = tables.select(cfg.sigma, cfg.tau)
     if group is not None:  # the select kernel compacts with atomics: fix one order for all ranks
         cands = cands[np.lexsort((cands[:, 1], cands[:, 0]))]
@@ -448,7 +458,6 @@ def mine(traces: Sequence[Session], cfg: MiningConfig, group=None) -> list[Patte
     need = [i for i, r in enumerate(rows) if r[4] >= 2]
     phase2_of: dict[int, tuple] = {}
     if need:
-        flat = [e for st in streams for e in st]
         if group is not None:  # this shard's follow counts size the slots
             local = _local_follow(tables, tok_dev, [rows[i] for i in need], S, cfg)
             lists = device_occurrences(
@@ -459,7 +468,7 @@ def mine(traces: Sequence[Session], cfg: MiningConfig, group=None) -> list[Patte
                 phase2_of[i] = _phase2(occ, cfg, rows[i][4])
         else:
             phase2_of = _phase2_corpus(tok_dev, flat, sigs, [rows[i] for i in need], need, S,
-                                       cfg)
+                                       cfg, corpus)
     patterns = []
     for i, (tool, cidx, support, n_match, follow) in enumerate(rows):
         context = tuple(sigs.signature(x) for x in decode_context(cidx, S, cfg.k))
@@ -710,6 +719,7 @@ class OrderedTrace:
     n_segments: int
     reordered_sessions: int
     order: Any = None      # optional: arrival index of every event in sorted order
+    tokens: Any = None     # optional: flagged token stream of the output
 
 
 _ORDER_DTYPES = {"session": "int32", "seq": "int32", "t_start": "float64", "t_end": "float64",
@@ -717,7 +727,7 @@ _ORDER_DTYPES = {"session": "int32", "seq": "int32", "t_start": "float64", "t_en
 
 
 def order_columnar(raw: dict, n_sessions: int, inactivity_ms: float = 300_000.0,
-                   with_order: bool = False) -> OrderedTrace:
+                   with_order: bool = False, with_tokens: bool = False) -> OrderedTrace:
     """K1 general path (paste_ingest_order): ingest_trace's grouping by
     session id, stable (t_start, seq) sort, reorder tally and inactivity
     split (events.py:196-252) over a device-resident columnar trace in
@@ -739,13 +749,14 @@ def order_columnar(raw: dict, n_sessions: int, inactivity_ms: float = 300_000.0,
            for k, dt in _ORDER_DTYPES.items()}
     res = torch.zeros(4, dtype=torch.int64, device=dev)
     order = torch.empty(n, dtype=torch.int32, device=dev) if with_order else None
+    tok = torch.empty(n, dtype=torch.int32, device=dev) if with_tokens else None
     need = int(lib.paste_ingest_order_scratch_bytes(n, int(n_sessions)))
     scratch = torch.empty(max(need, 16), dtype=torch.uint8, device=dev)
     base = ptr(res)
     cols = [raw[k].contiguous() for k in _ORDER_DTYPES]  # alive until the sync below
     d = OrderDesc(n, int(n_sessions), 0, *[ptr(c) for c in cols],
                   float(inactivity_ms), *[ptr(out[k]) for k in _ORDER_DTYPES], ptr(order),
-                  base, base + 8, base + 16, base + 24)
+                  ptr(tok), base, base + 8, base + 16, base + 24)
     check(lib.paste_ingest_order(ctypes.byref(d), ptr(scratch), need, stream_handle()), lib)
     n_out, n_seg, reord, status = (int(x) for x in res.tolist())
     if status & _native.PASTE_ORDER_BAD_SESSION:
@@ -753,7 +764,8 @@ def order_columnar(raw: dict, n_sessions: int, inactivity_ms: float = 300_000.0,
     if status & _native.PASTE_ORDER_NAN_T:
         raise _native.PasteUnsupported("NaN t_start: Python's sort order for it is undefined "
                                        "(use the host ingest_trace)")
-    return OrderedTrace({k: v[:n_out] for k, v in out.items()}, n_seg, reord, order)
+    return OrderedTrace({k: v[:n_out] for k, v in out.items()}, n_seg, reord, order,
+                        tok[:n_out] if with_tokens else None)
 
 
 def mine_columnar(trace: dict, sigs: SigTable, cfg: MiningConfig,

@@ -57,12 +57,17 @@ class CorpusTapes:
     """The corpus in HBM for Phase II: token stream + result / args tapes."""
 
     def __init__(self, nodes, data, refs, keys: KeyTable, tok_host: np.ndarray, tok_dev,
-                 sigs: SigTable, events: Sequence):
+                 sigs: SigTable, events: Sequence, res_tape=None, args_tape=None):
         from .device_ops import to_dev
 
         self.keys, self.sigs, self.events = keys, sigs, events
         self.tok, self.tok_dev = tok_host, tok_dev
         self.dev = {"nodes": to_dev(nodes), "data": to_dev(data), "refs": to_dev(refs)}
+        n = len(tok_host)
+        # tape of stream position p's result / args (default: 2p, 2p + 1)
+        self.res_tape = (2 * np.arange(n, dtype=np.int64) if res_tape is None
+                         else np.asarray(res_tape, np.int64))
+        self.args_tape = self.res_tape + 1 if args_tape is None else np.asarray(args_tape, np.int64)
         self._fail_prefix: dict[int, np.ndarray] = {}
 
     @classmethod
@@ -88,6 +93,41 @@ class CorpusTapes:
         return f
 
 
+class TapeEvents:
+    """Stream position -> Event decoded from the corpus tapes (the JSONL path
+    has no Python events): built once per position, so histories keep the
+    identity _failures_after relies on (mappings.py:197-206)."""
+
+    def __init__(self, ct_arrays: tuple, keys: KeyTable, sigs: SigTable, tok: np.ndarray,
+                 res_tape: np.ndarray, args_tape: np.ndarray, cols: dict):
+        self.nodes, self.data, self.refs = ct_arrays
+        self.keys, self.sigs, self.tok = keys, sigs, tok
+        self.res_tape, self.args_tape, self.cols = res_tape, args_tape, cols
+        self._cache: dict[int, Any] = {}
+
+    def __len__(self) -> int:
+        return len(self.tok)
+
+    def _decode(self, tape: int) -> Any:
+        from .tape import decode_node
+
+        return decode_node(self.nodes, self.data, int(self.refs[tape, 0]),
+                           int(self.refs[tape, 1]), 0, self.keys)
+
+    def __getitem__(self, p: int):
+        ev = self._cache.get(p)
+        if ev is None:
+            from .events import Event, EventKind, Status
+
+            t = int(self.tok[p]) & 0x7fffffff
+            ev = Event("", int(self.cols["seq"][p]), EventKind.TOOL_CALL, self.sigs.tools[t >> 1],
+                       Status.SUCCESS if t & 1 else Status.FAIL,
+                       self._decode(int(self.args_tape[p])), self._decode(int(self.res_tape[p])),
+                       float(self.cols["t_start"][p]), float(self.cols["t_end"][p]))
+            self._cache[p] = ev
+        return ev
+
+
 class CorpusOccurrences:
     """One candidate's occurrences as stream positions (anchors [M], matched
     event positions [M, n_ctx]) over a CorpusTapes."""
@@ -101,9 +141,9 @@ class CorpusOccurrences:
         self.picked = np.asarray(picked, np.int32)
         self.M, self.n_ctx = self.picked.shape
         self.target_tool = target_tool
-        self.act_tape = (2 * (self.anchors + 1) + 1).astype(np.int32)
+        self.act_tape = ct.args_tape[self.anchors + 1].astype(np.int32)
         self.dev = {k: to_dev(v) for k, v in dict(
-            occ_event=(2 * self.picked).reshape(-1).astype(np.int32),
+            occ_event=ct.res_tape[self.picked].reshape(-1).astype(np.int32),
             src_pos=(self.picked - self.picked[:, :1]).reshape(-1).astype(np.int32),
             hist_off=self.picked[:, 0].astype(np.int32),
             hist_end=(self.anchors + 1).astype(np.int32), act_tape=self.act_tape).items()}

@@ -69,6 +69,7 @@ def _c_sizeof(struct_name: str) -> int:
     ("paste_jobs_out", "JobsOut"), ("paste_live_actions_desc", "LiveActionsDesc"),
     ("paste_live_plan", "LivePlan"), ("paste_order_desc", "OrderDesc"),
     ("paste_occ_desc", "OccDesc"), ("paste_key_lookup_desc", "KeyLookupDesc"),
+    ("paste_jsonl_sizes", "JsonlSizes"), ("paste_jsonl_out", "JsonlOut"),
 ])
 def test_struct_layouts_match_header(cname, pyname):
     assert ctypes.sizeof(getattr(_native, pyname)) == _c_sizeof(cname)
