@@ -462,21 +462,34 @@ def run_replay(args, world, rank, local):
     rb = ReplayBatch(dp, c, W, K, ks)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    # the two-kernel replay (K4 records + replay_score_kernel): its tallies are
+    # the parity reference of the fused kernel, its time is reported beside it
+    rb.launch()
+    two_kernel = rb.tallies.cpu().numpy().tolist()
+    fused = rb.launch_fused()
+    step = rb.launch_fused if fused else rb.launch
     for _ in range(args.warmup):
-        rb.launch()
+        step()
     torch.cuda.synchronize()
     steps = max(1, min(args.steps, 10))
-    t_dev = 0.0
-    for _ in range(steps):
-        l2_flush(flush)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        rb.launch()
-        e1.record(stream)
-        e1.synchronize()
-        t_dev += e0.elapsed_time(e1) / 1e3
+
+    def timed(fn):
+        t = 0.0
+        for _ in range(steps):
+            l2_flush(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            e1.synchronize()
+            t += e0.elapsed_time(e1) / 1e3
+        return t
+
+    t_two = timed(rb.launch) if fused else None
+    t_dev = timed(step)
     launches = rb.launch_count() * steps
     tallies = rb.tallies.cpu().numpy().tolist()
+    fused_parity = tallies == two_kernel
     # end to end: the corpus arrays from pinned host memory, tallies (+ the
     # unsure flags when any) back, every step
     host = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.uint8).reshape(-1)).pin_memory()
@@ -490,7 +503,8 @@ def run_replay(args, world, rank, local):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         h2d = rb_e2e.upload_from(host)
-        rb_e2e.launch()
+        if not (fused and rb_e2e.launch_fused()):
+            rb_e2e.launch()
         tal_h.copy_(rb_e2e.tallies, non_blocking=True)
         e1.record(stream)
         e1.synchronize()
@@ -502,6 +516,8 @@ def run_replay(args, world, rank, local):
     out = {"metric": REPLAY_METRIC, "value": world * n * steps / t_dev, "unit": "calls/s",
            "n_gpus": world, "steps": steps, "ms_per_step": 1e3 * t_dev / steps,
            "scaling": "weak", "data": "synthetic", "consistent_e2e_tallies": ok,
+           "fused_equals_two_kernel_tallies": fused_parity,
+           "two_kernel_ms_per_step": 1e3 * t_two / steps if t_two else None,
            "rates": {"top1": tallies[0] / n, "top3": tallies[1] / n, "hit_rate": tallies[2] / n},
            "config": {"workload": "C2: score_accuracy replay of 100k coding sessions "
                                   "(edit_verify + locate_examine), window 16, top-8",
@@ -510,12 +526,15 @@ def run_replay(args, world, rank, local):
                       "pool": f"coding tau=0.3 ({len(pool.patterns)} patterns, reference-mined)",
                       "l2": "256 MB read flush between steps"},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                        "frac": achieved / peak, "kernel": "replay step (windows + predict + score)",
+                        "frac": achieved / peak,
+                        "kernel": "replay_fused_kernel" if fused
+                        else "replay step (windows + predict + score)",
                         "algorithmic_bytes_per_launch": REPLAY_ALG_BYTES * n,
-                        "traffic": replay_traffic(),
+                        "traffic": kernel_traffic("ncu_replay_fused_r2.json", "replay_fused_kernel")
+                        if fused else replay_traffic(),
                         "peak_source": f"{peak_kind} hbm_gbs",
                         "note": "SURVEY 8(d) 233 B/call; traffic = ncu dram bytes of the step's "
-                                "kernels (profiles/ncu_replay_r2.json)"},
+                                "kernel(s) (profiles/ncu_replay_fused_r2.json, ncu_replay_r2.json)"},
            "e2e": {"value": world * n * steps / t_e2e, "unit": "calls/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 32,
                    "ms_per_step": 1e3 * t_e2e / steps},

@@ -957,6 +957,17 @@ typedef struct {
 int paste_replay_score(const paste_pool_desc* pool, const paste_replay_desc* d,
                        paste_predict_out* out, void* stream);
 
+/* The same replay as ONE kernel without prediction records (SURVEY 8(f)
+ * row 3): per call the window's newest G tool events select a match-table
+ * entry, top1 / top3 come from its records' tools, and only the FULL-
+ * candidate-of-the-call's-tool bindings are resolved and compared.
+ * tallies / unsure as paste_replay_score; the caller re-checks unsure calls
+ * with paste_replay_score's records.  Requires pool->match_table valid for
+ * max_candidates (mt_k >= max_candidates) with mt_g <= 8; else
+ * PASTE_ERR_UNSUPPORTED.                                                   */
+int paste_replay_fused(const paste_pool_desc* pool, const paste_replay_desc* d,
+                       int32_t max_candidates, void* stream);
+
 /* Number of kernel launches the last paste_* call on this thread issued.   */
 int paste_last_launch_count(void);
 

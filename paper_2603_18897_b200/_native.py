@@ -245,6 +245,7 @@ EXPORTS = {
     "paste_holds": (c_int, [POINTER(HoldsDesc), c_void_p]),
     "paste_replay_score": (c_int, [POINTER(PoolDesc), POINTER(ReplayDesc), POINTER(PredictOut),
                                    c_void_p]),
+    "paste_replay_fused": (c_int, [POINTER(PoolDesc), POINTER(ReplayDesc), c_int32, c_void_p]),
     "paste_compact_scratch_bytes": (c_int64, [c_int64]),
     "paste_live_plan_bytes": (c_int64, [POINTER(PoolDesc), c_int32, c_int32]),
     "paste_build_live_plan": (c_int, [POINTER(PoolDesc), POINTER(AdmitDesc), c_int32, c_int32,

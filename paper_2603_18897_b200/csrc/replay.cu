@@ -17,6 +17,7 @@
 // surrogates (json.dumps(...).encode raises on them) -- make the call
 // "unsure"; the host re-checks those calls with the reference semantics.
 #include "common.cuh"
+#include "fast.cuh"
 
 namespace paste {
 
@@ -272,9 +273,223 @@ __global__ void __launch_bounds__(RS_THREADS, 4) replay_score_kernel(const paste
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused replay: windows -> match-table candidates -> score, one kernel, no
+// prediction records.  Scoring needs far less than the records: top1 / top3
+// are the target tools of the first three table records; a hit needs a FULL
+// candidate of the call's tool with the call's key set, so only those
+// candidates' bindings are resolved (resolve_fast, the K4 walk) and compared
+// (compare_binding) -- every other candidate is never resolved.  FULL = every
+// binding resolves; a candidate with an unresolved binding cannot hit.
+// Calls the device cannot decide (Unicode / containers / key sets the host
+// interns as -1) are flagged exactly as replay_score_kernel flags them.
+// ---------------------------------------------------------------------------
+constexpr int RF_THREADS = 256;
+constexpr int RF_WARPS = RF_THREADS / 32;
+constexpr int RF_GMAX = 8;
+constexpr int RF_CHUNK = 8;
+
+__global__ void __launch_bounds__(RF_THREADS, 4) replay_fused_kernel(const paste_pool_desc pool,
+                                                                   const paste_replay_desc D,
+                                                                   int K, int G) {
+  __shared__ int32_t gts[RF_WARPS][32][2 * RF_GMAX];  // gathered tokens, then event ids
+  __shared__ const uint8_t* ents[RF_WARPS][32];
+  __shared__ uint32_t queue[RF_WARPS][32 + RF_CHUNK * 32];
+  __shared__ unsigned hit_mask[RF_WARPS], unsure_mask[RF_WARPS];
+  __shared__ uint64_t memo[MEMO];
+  for (int i = threadIdx.x; i < MEMO; i += RF_THREADS) memo[i] = 0;
+  __syncthreads();
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t n = D.n_calls;
+  const int S = pool.n_bucket_sigs;
+  const int64_t stride = (int64_t)gridDim.x * RF_WARPS * 32;
+  const int64_t mts = mt_stride(pool.mt_k);
+  paste_windows win{};
+  win.nodes = D.nodes;
+  win.bytes = D.bytes;
+  win.refs = const_cast<paste_event_ref*>(D.refs);
+  unsigned long long c1 = 0, c3 = 0, ch = 0, cu = 0;
+  for (int64_t base = ((int64_t)blockIdx.x * RF_WARPS + w) * 32; base < n; base += stride) {
+    const int64_t c = base + lane;
+    const bool live = c < n;
+    int32_t* gt = gts[w][lane];
+    int32_t* ge = gt + RF_GMAX;
+    // ---- gather the newest G tool events of the call's window ---------------
+    int m = 0;
+    int32_t tool = -1, cks = -2;
+    if (live) {
+      const int64_t end = D.call_pos[c];
+      const int64_t len = D.call_len[c];
+      for (int64_t q = end - 1; q >= end - len && m < G; --q) {
+        const int32_t t = __ldg(D.ev_tok + q);
+        if (t >= 0) {
+          gt[m] = t;
+          ge[m] = __ldg(D.ev_evt + q);
+          ++m;
+        }
+      }
+      tool = D.call_tool[c];
+      cks = D.call_keyset[c];
+    }
+    const uint8_t* e = nullptr;
+    int np = 0;
+    if (live && m > 0 && gt[0] < S) {
+      int64_t key = gt[0], mult = S;
+      for (int a = 1; a < G; ++a) {
+        const int t = a < m ? gt[a] : S;
+        key += (int64_t)(t < S ? t : S) * mult;
+        mult *= (S + 1);
+      }
+      e = static_cast<const uint8_t*>(pool.match_table) + key * mts;
+      const int nm0 = __ldg(reinterpret_cast<const int*>(e));
+      const int nm = nm0 < K ? nm0 : K;
+      const int lim = D.cand_limit;
+      np = lim >= 0 ? (nm < lim ? nm : lim) : (nm + lim > 0 ? nm + lim : 0);
+    }
+    ents[w][lane] = e;
+    if (lane == 0) {
+      hit_mask[w] = 0u;
+      unsure_mask[w] = 0u;
+    }
+    __syncwarp();
+    bool top1 = false, top3 = false;
+    int count = 0;
+    const int max_np = __reduce_max_sync(FULL, (unsigned)np);
+    for (int i0 = 0; i0 < max_np; i0 += RF_CHUNK) {
+      int4 rv[RF_CHUNK];
+#pragma unroll
+      for (int j = 0; j < RF_CHUNK; ++j)
+        rv[j] = i0 + j < np ? __ldg(reinterpret_cast<const int4*>(e + 16 + 32 * (i0 + j)))
+                            : make_int4(0, 0, -1, 0);
+#pragma unroll
+      for (int j = 0; j < RF_CHUNK; ++j) {
+        const int i = i0 + j;
+        uint32_t item = 0;
+        bool need = false;
+        if (i < np) {
+          const bool same = rv[j].z == tool;
+          if (i == 0) top1 = same;
+          if (i < 3) top3 |= same;
+          if (same && ((rv[j].w >> 16) & PASTE_PF_HAS_MAPPING) && cks != -2) {
+            const int32_t pks = __ldg(D.pat_keyset + rv[j].x);
+            if (pks < 0 || cks < 0) {
+              need = true;  // undecided key sets: unsure iff the candidate is FULL
+              item = 1u << 15;
+            } else {
+              need = pks == cks;
+            }
+          }
+        }
+        const unsigned msk = __ballot_sync(FULL, need);
+        if (need) queue[w][count + __popc(msk & lt)] = ((uint32_t)lane << 16) | item | (uint32_t)i;
+        count += __popc(msk);
+      }
+      __syncwarp();
+      const bool last = i0 + RF_CHUNK >= max_np;
+      while (count >= 32 || (last && count > 0)) {
+        const int take = count < 32 ? count : 32;
+        if (lane < take) {
+          const uint32_t it = queue[w][count - take + lane];
+          const int src = it >> 16, i = it & 0x7fff;
+          const bool ks_unsure = (it >> 15) & 1u;
+          const int64_t cc = base + src;
+          const int4 r0 = __ldg(reinterpret_cast<const int4*>(ents[w][src] + 16 + 32 * i));
+          const int4 r1 = __ldg(reinterpret_cast<const int4*>(ents[w][src] + 16 + 32 * i) + 1);
+          const uint32_t ages = (uint32_t)r0.y;
+          const int n_bind = r0.w & 0xffff, bind_off = r1.x;
+          const int32_t* ogt = gts[w][src];
+          const int32_t* oge = ogt + RF_GMAX;
+          const int32_t aev = D.call_args[cc];
+          const int64_t abase = D.refs[aev].node_base;
+          int verdict = CMP_EQ;
+          for (int b = 0; b < n_bind; ++b) {
+            const int bind = bind_off + b;
+            const paste_binding bd = pool.bindings[bind];
+            const int age = (ages >> (4 * b)) & 15;
+            const int64_t r = resolve_fast(win, pool.steps, bd, bind, oge[age], age, ogt, memo);
+            if (r < 0) {  // PARTIAL: not a hit candidate
+              verdict = CMP_NE;
+              break;
+            }
+            if (ks_unsure) {
+              verdict = CMP_UNSURE;
+              continue;
+            }
+            const int64_t an = lookup_key(D.nodes, abase, D.bind_key[bind]);
+            const int v = an < 0 ? CMP_UNSURE : compare_binding(D, bind, bd.kind, r, aev, an);
+            if (v == CMP_NE) {
+              verdict = CMP_NE;
+              break;
+            }
+            if (v == CMP_UNSURE) verdict = CMP_UNSURE;
+          }
+          if (verdict == CMP_EQ) atomicOr(&hit_mask[w], 1u << src);
+          else if (verdict == CMP_UNSURE) atomicOr(&unsure_mask[w], 1u << src);
+        }
+        count -= take;
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+    if (live) {
+      const bool hit = (hit_mask[w] >> lane) & 1u;
+      const bool unsure = ((unsure_mask[w] >> lane) & 1u) && !hit;
+      D.unsure[c] = unsure;
+      c1 += top1;
+      c3 += top3;
+      ch += hit;
+      cu += unsure;
+    }
+    __syncwarp();
+  }
+  __shared__ unsigned long long red[4][RF_WARPS];
+  for (int off = 16; off; off >>= 1) {
+    c1 += __shfl_down_sync(FULL, c1, off);
+    c3 += __shfl_down_sync(FULL, c3, off);
+    ch += __shfl_down_sync(FULL, ch, off);
+    cu += __shfl_down_sync(FULL, cu, off);
+  }
+  if (lane == 0) {
+    red[0][w] = c1;
+    red[1][w] = c3;
+    red[2][w] = ch;
+    red[3][w] = cu;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    unsigned long long s = 0;
+    for (int k = 0; k < RF_WARPS; ++k) s += red[threadIdx.x][k];
+    if (s) atomicAdd(reinterpret_cast<unsigned long long*>(D.tallies) + threadIdx.x, s);
+  }
+}
+
 }  // namespace paste
 
 using namespace paste;
+
+extern "C" int paste_replay_fused(const paste_pool_desc* pool, const paste_replay_desc* d,
+                                  int32_t max_candidates, void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(pool && d, "null descriptor");
+  PASTE_REQUIRE(d->capacity >= 1, "window capacity must be >= 1");
+  PASTE_REQUIRE(max_candidates >= 1, "max_candidates must be >= 1");
+  const int G = pool->mt_g;
+  if (!pool->match_table || pool->mt_k < max_candidates || G < 1 || G > RF_GMAX ||
+      pool->max_bindings > 8) {
+    set_error("pool / window outside the fused replay envelope (needs a match table)");
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  if (d->n_calls == 0) return PASTE_OK;
+  int64_t blocks = (d->n_calls + RF_THREADS - 1) / RF_THREADS;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  replay_fused_kernel<<<(unsigned)blocks, RF_THREADS, 0, (cudaStream_t)stream>>>(
+      *pool, *d, max_candidates, G);
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  count_launch(1);
+  return PASTE_OK;
+}
 
 extern "C" int paste_replay_score(const paste_pool_desc* pool, const paste_replay_desc* d,
                                   paste_predict_out* out, void* stream) {

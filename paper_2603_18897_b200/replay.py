@@ -199,6 +199,20 @@ class ReplayBatch:
         check(self.lib.paste_replay_score(ctypes.byref(self.pool_desc), ctypes.byref(self.desc),
                                           ctypes.byref(self.out), stream_handle() if stream is None else stream), self.lib)
 
+    def launch_fused(self, stream: int | None = None) -> bool:
+        """The fused replay (paste_replay_fused: one kernel, no prediction
+        records); False when the pool is outside its envelope (no match
+        table for this window / K) -- use launch()."""
+        from .device_ops import stream_handle
+
+        self.tallies.zero_()
+        rc = self.lib.paste_replay_fused(ctypes.byref(self.pool_desc), ctypes.byref(self.desc),
+                                         self.K, stream_handle() if stream is None else stream)
+        if rc == _native.PASTE_ERR_UNSUPPORTED:
+            return False
+        check(rc, self.lib)
+        return True
+
     def launch_count(self) -> int:
         return int(self.lib.paste_last_launch_count())
 
@@ -244,8 +258,11 @@ def score_replay(traces, pool, window_capacity: int, max_candidates):
     if scored == 0:
         return AccuracyReport(0.0, 0.0, 0.0, 0)
     rb = ReplayBatch(dp, corpus, window_capacity, max_candidates, ksets)
-    rb.launch()
+    fused = rb.launch_fused()
     top1, top3, hits, unsure = (int(x) for x in rb.tallies.cpu().numpy())
-    if unsure:
-        hits += rb.host_recheck(actual, arena)
+    if unsure or not fused:  # undecided calls need the prediction records
+        rb.launch()
+        top1, top3, hits, unsure = (int(x) for x in rb.tallies.cpu().numpy())
+        if unsure:
+            hits += rb.host_recheck(actual, arena)
     return AccuracyReport(top1 / scored, top3 / scored, hits / scored, scored)

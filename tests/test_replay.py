@@ -95,8 +95,11 @@ def test_device_replay_matches_oracle(pool_file, W, K):
     rb.launch()
     top1, top3, hits, unsure = rb.tallies.cpu().numpy().tolist()
     assert unsure == 0  # ASCII corpus: every hit decided on the device
-    assert (top1, top3, hits, c.n_calls) == bridge.score_corpus(dp.image, c, dp.keys, W, K,
-                                                                threads=8)
+    exp = bridge.score_corpus(dp.image, c, dp.keys, W, K, threads=8)
+    assert (top1, top3, hits, c.n_calls) == exp
+    # the fused replay (one kernel, no records) gives the same tallies
+    assert rb.launch_fused()
+    assert rb.tallies.cpu().numpy().tolist() == [top1, top3, hits, 0]
 
 
 @pytest.mark.gpu
