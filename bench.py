@@ -68,6 +68,8 @@ def parse_args():
                     help="C4 mining corpus size (0 = skip the mining measurement)")
     ap.add_argument("--long-sessions", type=int, default=100_000,
                     help="C5 long-output sessions (0 = skip)")
+    ap.add_argument("--phase2-tiles", type=int, default=160,
+                    help="tiles of the 400-session coding corpus mined by mine_jsonl (0 = skip)")
     ap.add_argument("--replay-sessions", type=int, default=100_000,
                     help="C2 replay sessions (0 = skip)")
     return ap.parse_args()
@@ -373,6 +375,9 @@ def run_ours(args):
     if args.replay_sessions > 0:
         torch.cuda.empty_cache()
         out["replay"] = run_replay(args, world, rank, local)
+    if args.phase2_tiles > 0 and rank == 0:
+        torch.cuda.empty_cache()
+        out["phase2_mining"] = run_phase2(args, world, rank, local)
     if parity:
         out["parity"] = parity_summary(parity)
     out["summary"] = summary(out)
@@ -426,7 +431,7 @@ def summary(out):
         return r
 
     s = {"c3": obj(out), "c4": obj(out.get("mining")), "c5": obj(out.get("long_outputs")),
-         "c2": obj(out.get("replay"))}
+         "c2": obj(out.get("replay")), "phase2": obj(out.get("phase2_mining"))}
     if out.get("mining", {}).get("suffix"):
         s["c4_suffix"] = {k: out["mining"]["suffix"][k] for k in ("value", "roofline_frac")}
     if out.get("parity"):
@@ -658,6 +663,119 @@ def run_long_outputs(args, world, rank, local):
         out["cpu_baseline"] = {"value": m / dt, "unit": "sessions/s", "cores": threads,
                                "kind": "port", "sample": f"{m} sessions ({dt:.2f} s), "
                                "oracle_leaf_scan (candidate_paths restated in C), OpenMP"}
+    return out
+
+
+PHASE2_METRIC = "mined trace events/sec, mapping-bearing JSONL (Phase II included)"
+
+
+def coding_jsonl(tiles: int) -> tuple[str, int, int]:
+    """The reference-generated coding corpus (generate_corpus edit_verify /
+    locate_examine 0.5 / 0.5, 400 sessions, seed 2: tests/golden/
+    score_c2_golden.json) tiled `tiles` times with distinct session ids, as
+    JSONL text.  Returns (text, sessions, events)."""
+    import io
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import golden_io as G
+    from paper_2603_18897_b200.events import Session, write_trace
+
+    base = [G.session(s) for s in G.golden("score_c2_golden.json")["sessions"]]
+    buf = io.StringIO()
+    write_trace(base, buf)
+    one = buf.getvalue()
+    parts = [one.replace('"session_id": "', f'"session_id": "t{t}-') if t else one
+             for t in range(tiles)]
+    n_ev = sum(len(s.events) for s in base)
+    return "".join(parts), len(base) * tiles, n_ev * tiles
+
+
+def run_phase2(args, world, rank, local):
+    """Mining with Phase II at scale: mine_jsonl --
+    native parallel parse of records + payload tapes, then on the device the
+    K1 ordering, count, selection and mapping inference over the corpus
+    tapes -- on a mapping-bearing coding corpus, end to end from host text.
+    The per-part times come from one instrumented call; `value` is the
+    whole call (wall clock, synchronised).  Also C1 (1k deep-research
+    sessions, tau 0.3) through mine(sessions) and mine_jsonl."""
+    import torch
+
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import golden_io as G
+    from paper_2603_18897_b200 import mine
+    from paper_2603_18897_b200.events import ingest_trace
+    from paper_2603_18897_b200.ingest import mine_jsonl, parse_jsonl_raw
+    from paper_2603_18897_b200.mining import MiningConfig
+
+    cfg = MiningConfig(tau=0.3)
+    text, n_sess, n_ev = coding_jsonl(args.phase2_tiles)
+    raw = text.encode()
+    pats = mine_jsonl(text, cfg)  # warm (library, pool of buffers)
+    torch.cuda.synchronize()
+    steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        pats = mine_jsonl(text, cfg)
+        torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / steps
+    t0 = time.perf_counter()
+    parse_jsonl_raw(text)
+    parse_s = time.perf_counter() - t0
+    mapped = sum(p.mapping is not None for p in pats)
+    out = {"metric": PHASE2_METRIC, "value": n_ev / wall, "unit": "events/s", "n_gpus": 1,
+           "steps": steps, "ms_per_step": 1e3 * wall, "scaling": "replicas only",
+           "data": "synthetic",
+           "config": {"workload": "mine_jsonl: coding corpus (reference generate_corpus "
+                                  "edit_verify/locate_examine, 400 sessions seed 2) tiled "
+                                  f"{args.phase2_tiles}x, MiningConfig(tau=0.3)",
+                      "sessions": n_sess, "events": n_ev, "jsonl_bytes": len(raw)},
+           "patterns": len(pats), "patterns_with_mapping": mapped,
+           "native_parse_ms": 1e3 * parse_s,
+           "e2e": {"value": n_ev / wall, "unit": "events/s", "h2d_bytes_per_step": None,
+                   "d2h_bytes_per_step": None,
+                   "includes": "JSONL text -> patterns: parse, H2D of columns + tapes, device "
+                               "K1 order / count / select / Phase II, list[PatternTuple]"}}
+    # C1 at its stated size through both public entry points
+    c1 = G.golden("c1_golden.json.gz")
+    train = [G.session(s) for s in c1["train"]]
+    exp = c1["cases"][1]["expected"]
+    t0 = time.perf_counter()
+    got = mine(train, cfg)
+    t_sess = time.perf_counter() - t0
+    import io as _io
+
+    from paper_2603_18897_b200.events import write_trace
+    buf = _io.StringIO()
+    write_trace(train, buf)
+    t0 = time.perf_counter()
+    got_j = mine_jsonl(buf.getvalue(), cfg)
+    t_json = time.perf_counter() - t0
+    from paper_2603_18897_b200.mappings import mapping_to_json
+    as_json = [{"context": [{"tool": s.tool_type, "status": s.status.value} for s in p.context],
+                "target": p.target, "mapping": mapping_to_json(p.mapping) if p.mapping else None,
+                "p": p.p, "support": p.support, "pattern_id": p.pattern_id} for p in got]
+    out["c1"] = {"sessions": len(train), "tool_events": sum(len(s.tool_events()) for s in train),
+                 "mine_sessions_ms": 1e3 * t_sess, "mine_jsonl_ms": 1e3 * t_json,
+                 "equals_reference": as_json == exp, "jsonl_equals_sessions": got_j == got}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # the reference algorithm on the host: ingest_trace + the C oracle's
+        # counts + the Python restatement of Phase II (occurrence rescans,
+        # infer_mapping, mapping_holds), one core, on a sample of the corpus
+        from oracle.mine_host import mine_host
+
+        m = min(n_sess, 2000)
+        lines = text.splitlines()
+        sample = "\n".join(lines[:len(lines) * m // n_sess]) + "\n"
+        t0 = time.perf_counter()
+        sess = ingest_trace(sample).sessions
+        host = mine_host(sess, cfg)
+        dt = time.perf_counter() - t0
+        ev = sum(len(s.events) for s in sess)
+        out["cpu_baseline"] = {"value": ev / dt, "unit": "events/s", "cores": 1, "kind": "port",
+                               "sample": f"{len(sess)} sessions / {ev} events ({dt:.2f} s): "
+                                         "ingest_trace + oracle counts + Python Phase II "
+                                         "restatement (oracle/mine_host.py)",
+                               "patterns": len(host)}
     return out
 
 

@@ -28,6 +28,7 @@
 #include <vector>
 #include <algorithm>
 #include <numeric>
+#include <omp.h>
 
 #include "paste.h"
 
@@ -187,17 +188,41 @@ struct Tape {
 struct LineTapes {
   Tape result, args;
   bool has_result = false, has_args = false;
-  std::vector<std::string> keys;  // line-local key ids
-  std::unordered_map<std::string, int32_t> key_id;
+  std::vector<std::string> keys;  // line-local key ids (few per line: linear search)
   int32_t intern(const std::string& k) {
-    auto it = key_id.find(k);
-    if (it != key_id.end()) return it->second;
-    const int32_t id = (int32_t)keys.size();
+    for (size_t i = 0; i < keys.size(); ++i)
+      if (keys[i] == k) return (int32_t)i;
     keys.push_back(k);
-    key_id.emplace(k, id);
-    return id;
+    return (int32_t)keys.size() - 1;
   }
 };
+
+// Line starts and the str.splitlines() check, in parallel chunks.
+bool split_lines(const char* text, int64_t len, std::vector<int64_t>& starts) {
+  const int64_t CH = 1 << 22;
+  const int64_t nch = (len + CH - 1) / CH;
+  std::vector<std::vector<int64_t>> part(nch);
+  bool odd = false;
+#pragma omp parallel for schedule(static) reduction(|| : odd)
+  for (int64_t c = 0; c < nch; ++c) {
+    const int64_t b = c * CH, e = std::min(len, b + CH);
+    for (int64_t i = b; i < e; ++i) {
+      const unsigned char ch = (unsigned char)text[i];
+      if (ch == '\n') {
+        if (i + 1 < len) part[c].push_back(i + 1);
+      } else if (ch < 0x20 || ch >= 0xC2) {
+        if (ch == '\r' || ch == '\v' || ch == '\f' || (ch >= 0x1c && ch <= 0x1e)) odd = true;
+        else if (ch == 0xC2 && i + 1 < len && (unsigned char)text[i + 1] == 0x85) odd = true;
+        else if (ch == 0xE2 && i + 2 < len && (unsigned char)text[i + 1] == 0x80 &&
+                 ((unsigned char)text[i + 2] == 0xA8 || (unsigned char)text[i + 2] == 0xA9))
+          odd = true;
+      }
+    }
+  }
+  starts.assign(1, 0);
+  for (auto& p : part) starts.insert(starts.end(), p.begin(), p.end());
+  return !odd;
+}
 
 void put_utf8(std::string& out, uint32_t cp) {
   if (cp < 0x80) {
@@ -691,13 +716,11 @@ extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_pay
     return PASTE_ERR_INVALID;
   }
   *out = nullptr;
-  if (odd_line_breaks(text, len)) {
+  std::vector<int64_t> starts;
+  if (!split_lines(text, len, starts)) {
     set_error("line separators other than '\\n': host ingest");
     return PASTE_ERR_UNSUPPORTED;
   }
-  std::vector<int64_t> starts{0};
-  for (int64_t i = 0; i < len; ++i)
-    if (text[i] == '\n' && i + 1 < len) starts.push_back(i + 1);
   const int64_t n_lines = len == 0 ? 0 : (int64_t)starts.size();
   std::vector<Rec> recs(n_lines);
   std::vector<LineTapes> tapes(want_payloads ? n_lines : 0);
@@ -719,9 +742,8 @@ extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_pay
   h->n_lines = n_lines;
   std::unordered_map<std::string_view, int32_t> sid, tool_id;
   std::vector<std::string_view> tools;
-  std::unordered_map<std::string, int32_t> key_id;
-  std::vector<int32_t> remap;
-  int64_t n_rows = 0;
+  std::vector<int64_t> row_line;  // line of every valid row
+  row_line.reserve((size_t)n_lines);
   for (int64_t i = 0; i < n_lines; ++i) {
     const Rec& r = recs[i];
     if (r.kind == L_EMPTY) continue;
@@ -747,31 +769,75 @@ extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_pay
       tid = t->second;
     }
     h->sig.push_back(tid < 0 ? -1 : (tid << 1) | (r.success ? 1 : 0));  // tool rank applied below
-    ++n_rows;
-    if (!want_payloads) continue;
-    LineTapes& lt = tapes[i];
-    remap.assign(lt.keys.size(), -1);
-    for (size_t k = 0; k < lt.keys.size(); ++k) {
-      auto g = key_id.find(lt.keys[k]);
-      if (g == key_id.end()) {
-        g = key_id.emplace(lt.keys[k], (int32_t)key_id.size()).first;
-        h->key_names.append(lt.keys[k]);
-        h->key_names.push_back('\0');
-      }
-      remap[k] = g->second;
+    row_line.push_back(i);
+  }
+  const int64_t n_rows = (int64_t)row_line.size();
+  std::unordered_map<std::string_view, int32_t> key_id;
+  if (want_payloads) {
+    // distinct keys (per thread, merged), ids in sorted key order: deterministic
+    std::vector<std::vector<std::string_view>> seen;
+#pragma omp parallel
+    {
+#pragma omp single
+      seen.resize((size_t)omp_get_num_threads());
+      std::unordered_map<std::string_view, char> mine;
+#pragma omp for schedule(static)
+      for (int64_t r = 0; r < n_rows; ++r)
+        for (const std::string& k : tapes[row_line[r]].keys) mine.emplace(k, 0);
+      auto& out = seen[(size_t)omp_get_thread_num()];
+      for (auto& kv : mine) out.push_back(kv.first);
     }
-    for (Tape* t : {&lt.result, &lt.args}) {
-      h->refs.push_back(paste_event_ref{(int64_t)h->nodes.size(), (int64_t)h->bytes.size()});
-      if (t->nodes.empty()) t->nodes.push_back(TNode{T_NULL, 0, 0, -1, 0, 0});  // absent: None
-      for (TNode nd : t->nodes) {
-        if (nd.key >= 0) nd.key = remap[nd.key];
-        h->nodes.push_back(nd);
-      }
-      h->bytes.insert(h->bytes.end(), t->bytes.begin(), t->bytes.end());
+    std::vector<std::string_view> all;
+    for (auto& v : seen) all.insert(all.end(), v.begin(), v.end());
+    std::sort(all.begin(), all.end());
+    all.erase(std::unique(all.begin(), all.end()), all.end());
+    for (size_t k = 0; k < all.size(); ++k) {
+      key_id.emplace(all[k], (int32_t)k);
+      h->key_names.append(all[k].data(), all[k].size());
+      h->key_names.push_back('\0');
     }
-    LineTapes().keys.swap(lt.keys);  // release the line's memory early
-    lt.result = Tape();
-    lt.args = Tape();
+    // tape offsets (absent payload = one null node), then a parallel copy
+    std::vector<int64_t> node_off(2 * n_rows + 1, 0), byte_off(2 * n_rows + 1, 0);
+    for (int64_t r = 0; r < n_rows; ++r) {
+      const LineTapes& lt = tapes[row_line[r]];
+      int q = 0;
+      for (const Tape* t : {&lt.result, &lt.args}) {
+        const int64_t j = 2 * r + q++;
+        node_off[j + 1] = node_off[j] + (t->nodes.empty() ? 1 : (int64_t)t->nodes.size());
+        byte_off[j + 1] = byte_off[j] + (int64_t)t->bytes.size();
+      }
+    }
+    h->nodes.resize((size_t)node_off[2 * n_rows]);
+    h->bytes.resize((size_t)byte_off[2 * n_rows]);
+    h->refs.resize((size_t)(2 * n_rows));
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t r = 0; r < n_rows; ++r) {
+      LineTapes& lt = tapes[row_line[r]];
+      int32_t remap[64];
+      std::vector<int32_t> big;
+      int32_t* rm = remap;
+      if (lt.keys.size() > 64) {
+        big.resize(lt.keys.size());
+        rm = big.data();
+      }
+      for (size_t k = 0; k < lt.keys.size(); ++k) rm[k] = key_id.at(std::string_view(lt.keys[k]));
+      int q = 0;
+      for (Tape* t : {&lt.result, &lt.args}) {
+        const int64_t j = 2 * r + q++;
+        h->refs[(size_t)j] = paste_event_ref{node_off[j], byte_off[j]};
+        TNode* dst = h->nodes.data() + node_off[j];
+        if (t->nodes.empty()) {
+          *dst = TNode{T_NULL, 0, 0, -1, 0, 0};  // absent: record.get -> None
+        } else {
+          for (size_t x = 0; x < t->nodes.size(); ++x) {
+            TNode nd = t->nodes[x];
+            if (nd.key >= 0) nd.key = rm[nd.key];
+            dst[x] = nd;
+          }
+        }
+        if (!t->bytes.empty()) memcpy(h->bytes.data() + byte_off[j], t->bytes.data(), t->bytes.size());
+      }
+    }
   }
   h->n_keys = (int64_t)key_id.size();
   h->n_sessions = (int64_t)sid.size();
