@@ -719,8 +719,9 @@ def run_phase2(args, world, rank, local):
         torch.cuda.synchronize()
     wall = (time.perf_counter() - t0) / steps
     t0 = time.perf_counter()
-    parse_jsonl_raw(text)
+    tr = parse_jsonl_raw(text)
     parse_s = time.perf_counter() - t0
+    h2d = sum(v.nbytes for v in tr.columns.values()) + sum(a.nbytes for a in tr.tapes)
     mapped = sum(p.mapping is not None for p in pats)
     out = {"metric": PHASE2_METRIC, "value": n_ev / wall, "unit": "events/s", "n_gpus": 1,
            "steps": steps, "ms_per_step": 1e3 * wall, "scaling": "replicas only",
@@ -731,7 +732,7 @@ def run_phase2(args, world, rank, local):
                       "sessions": n_sess, "events": n_ev, "jsonl_bytes": len(raw)},
            "patterns": len(pats), "patterns_with_mapping": mapped,
            "native_parse_ms": 1e3 * parse_s,
-           "e2e": {"value": n_ev / wall, "unit": "events/s", "h2d_bytes_per_step": None,
+           "e2e": {"value": n_ev / wall, "unit": "events/s", "h2d_bytes_per_step": h2d,
                    "d2h_bytes_per_step": None,
                    "includes": "JSONL text -> patterns: parse, H2D of columns + tapes, device "
                                "K1 order / count / select / Phase II, list[PatternTuple]"}}
