@@ -549,8 +549,8 @@ __device__ __forceinline__ void kslot_write8(const LiveParams& P, const Sess<G>&
 // rounds: round r+2's inputs and round r+1's older ring slots are in flight
 // while round r is keyed and written, so the count -> ring -> plan chain
 // costs one memory round trip per round instead of three.
-template <int G>
-__global__ void __launch_bounds__(LT) predict_live_kernel(const LiveParams P) {
+template <int G, int MINB = 6>
+__global__ void __launch_bounds__(LT, MINB) predict_live_kernel(const LiveParams P) {
   const int64_t n = P.win.n_sessions;
   const int64_t stride = (int64_t)gridDim.x * LT;
   const int64_t s0 = (int64_t)blockIdx.x * LT + threadIdx.x;
@@ -951,20 +951,43 @@ static bool live_ticket() {
   return t == 1;
 }
 
+// min resident CTAs per SM of the K-slot live kernel, i.e. its register
+// cap: 6 -> 80 registers and no spills, the default (measured: 57.9 us per
+// 1M sessions vs 69.4 us at 8 -> 64 registers with spills, 64.4 us at 4 ->
+// 106 registers); PASTE_LIVE_MINB = 4 / 8 / 10 / 12 selects another build
+static int live_minb() {
+  static int m = -1;
+  if (m < 0) {
+    const char* e = getenv("PASTE_LIVE_MINB");
+    m = e ? atoi(e) : 6;
+  }
+  return m;
+}
+
 template <int G, int SPT>
 static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
   static int sms = 0;
-  static int occ[3] = {0, 0, 0};
+  static int occ[7] = {0, 0, 0, 0, 0, 0, 0};
   if (sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const int which = !compact ? 0 : live_mode() == 1 ? 1 : 2;
+  const int minb = live_minb();
+  const int which = !compact ? (minb == 12 ? 4 : minb == 10 ? 3 : minb == 8 ? 5 : minb == 4 ? 6 : 0)
+                             : live_mode() == 1 ? 1 : 2;
   int& o = occ[which];
   if (o == 0) {
     if (which == 0)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G>, LT, 0);
+    else if (which == 3)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 10>, LT, 0);
+    else if (which == 4)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 12>, LT, 0);
+    else if (which == 5)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 8>, LT, 0);
+    else if (which == 6)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 4>, LT, 0);
     else if (which == 1)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_compact_kernel<G, SPT>, LT, 0);
     else
@@ -976,6 +999,14 @@ static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
   const int64_t grid = groups < (int64_t)sms * o ? groups : (int64_t)sms * o;
   if (which == 0)
     predict_live_kernel<G><<<(unsigned)grid, LT, 0, st>>>(P);
+  else if (which == 3)
+    predict_live_kernel<G, 10><<<(unsigned)grid, LT, 0, st>>>(P);
+  else if (which == 4)
+    predict_live_kernel<G, 12><<<(unsigned)grid, LT, 0, st>>>(P);
+  else if (which == 5)
+    predict_live_kernel<G, 8><<<(unsigned)grid, LT, 0, st>>>(P);
+  else if (which == 6)
+    predict_live_kernel<G, 4><<<(unsigned)grid, LT, 0, st>>>(P);
   else if (which == 1)
     predict_live_compact_kernel<G, SPT><<<(unsigned)grid, LT, 0, st>>>(P);
   else
