@@ -350,7 +350,7 @@ def run_ours(args):
                      "kernel_model_bytes_per_launch": model // S_,
                      "peak_source": f"{peak_kind} hbm_gbs",
                      "note": "SURVEY 8(d) 200 B/session; traffic = ncu dram bytes per launch "
-                             "(profiles/ncu_live_r2.json): the narrow u8/u16 inputs and the "
+                             "(profiles/ncu_live_r2b.json): the narrow u8/u16 inputs and the "
                              "key-coded records move fewer bytes than the canonical encoding"},
         "gpu_launches": launches,
         "wall_s_timed_region": wall,
@@ -1006,7 +1006,7 @@ def replay_traffic():
     return total or None
 
 
-def committed_traffic(name: str = "ncu_live_r2.json"):
+def committed_traffic(name: str = "ncu_live_r2b.json"):
     """dram bytes per launch of the C3 step kernel from the committed ncu capture."""
     return committed_ncu(name).get("dram_bytes_per_launch")
 

@@ -954,7 +954,8 @@ static bool live_ticket() {
 // min resident CTAs per SM of the K-slot live kernel, i.e. its register
 // cap: 6 -> 80 registers and no spills, the default (measured: 57.9 us per
 // 1M sessions vs 69.4 us at 8 -> 64 registers with spills, 64.4 us at 4 ->
-// 106 registers); PASTE_LIVE_MINB = 4 / 8 / 10 / 12 selects another build
+// 106 registers, 77.2 us at 10 -> 48, 87.4 us at 12 -> 40); PASTE_LIVE_MINB =
+// 4 / 5 / 7 / 8 selects another build
 static int live_minb() {
   static int m = -1;
   if (m < 0) {
@@ -974,16 +975,16 @@ static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int minb = live_minb();
-  const int which = !compact ? (minb == 12 ? 4 : minb == 10 ? 3 : minb == 8 ? 5 : minb == 4 ? 6 : 0)
+  const int which = !compact ? (minb == 7 ? 4 : minb == 5 ? 3 : minb == 8 ? 5 : minb == 4 ? 6 : 0)
                              : live_mode() == 1 ? 1 : 2;
   int& o = occ[which];
   if (o == 0) {
     if (which == 0)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G>, LT, 0);
     else if (which == 3)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 10>, LT, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 5>, LT, 0);
     else if (which == 4)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 12>, LT, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 7>, LT, 0);
     else if (which == 5)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 8>, LT, 0);
     else if (which == 6)
@@ -1000,9 +1001,9 @@ static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
   if (which == 0)
     predict_live_kernel<G><<<(unsigned)grid, LT, 0, st>>>(P);
   else if (which == 3)
-    predict_live_kernel<G, 10><<<(unsigned)grid, LT, 0, st>>>(P);
+    predict_live_kernel<G, 5><<<(unsigned)grid, LT, 0, st>>>(P);
   else if (which == 4)
-    predict_live_kernel<G, 12><<<(unsigned)grid, LT, 0, st>>>(P);
+    predict_live_kernel<G, 7><<<(unsigned)grid, LT, 0, st>>>(P);
   else if (which == 5)
     predict_live_kernel<G, 8><<<(unsigned)grid, LT, 0, st>>>(P);
   else if (which == 6)
