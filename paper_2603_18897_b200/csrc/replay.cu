@@ -324,22 +324,14 @@ __global__ void __launch_bounds__(RF_THREADS, 4) replay_fused_kernel(const paste
       const int64_t lo = end - D.call_len[c];
       tool = D.call_tool[c];
       cks = D.call_keyset[c];
-      // newest G tool events: tokens in independent batches of 8 (LLM steps
-      // interleave), their stream offsets from `lo` parked in ge[], then the
-      // G event ids loaded together
-      for (int64_t q = end - 1; m < G && q >= lo; q -= 8) {
-        int32_t tb[8];
-#pragma unroll
-        for (int b = 0; b < 8; ++b) tb[b] = q - b >= lo ? __ldg(D.ev_tok + q - b) : -1;
-#pragma unroll
-        for (int b = 0; b < 8; ++b)
-          if (tb[b] >= 0 && m < G) {
-            gt[m] = tb[b];
-            ge[m] = (int32_t)(q - b - lo);  // < call_len <= capacity
-            ++m;
-          }
+      for (int64_t q = end - 1; q >= lo && m < G; --q) {  // newest G tool events
+        const int32_t t = __ldg(D.ev_tok + q);
+        if (t >= 0) {
+          gt[m] = t;
+          ge[m] = __ldg(D.ev_evt + q);
+          ++m;
+        }
       }
-      for (int i = 0; i < m; ++i) ge[i] = __ldg(D.ev_evt + lo + ge[i]);
     }
     const uint8_t* e = nullptr;
     int np = 0;
