@@ -958,13 +958,15 @@ static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint
   for (int d = 2; d <= K; ++d, pw *= (uint32_t)g.base) hot_lo += (uint32_t)g.S * pw;
   if (hot_n > (uint32_t)CHOT_MAX) hot_n = 0;
   const size_t smem = sizeof(ColumnTile) * CNST + (size_t)CHOT_MAX * sizeof(uint32_t);
+  // the attribute is per device context: set it on every call (cheap), so a
+  // second GPU in the same process launches too
+  cudaFuncSetAttribute(columnar_count_kernel<K, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
   static int grid_cap = 0, sms = 0;
   if (grid_cap == 0) {
     int dev = 0, occ = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(columnar_count_kernel<K, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, columnar_count_kernel<K, OUT>, CT, smem);
     grid_cap = sms * (occ > 0 ? occ : 1);
   }
@@ -1003,12 +1005,8 @@ static int launch_columnar(const paste_columnar_desc& c, const MineGeom& g, uint
       dlo = (uint32_t)((uint64_t)g.S * b3);
       dn = (uint32_t)b3;
     }
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(stage_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           SH_SMEM_MAX);
-      attr = true;
-    }
+    cudaFuncSetAttribute(stage_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         SH_SMEM_MAX);  // per device context: every call
     const size_t sh_bytes = (size_t)(((dn + 1) >> 1) + ((lat_n + 1) >> 1)) * sizeof(uint32_t);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr_c[1];

@@ -1022,12 +1022,12 @@ bool predict_compact_dispatch(const paste_pool_desc* pool, const paste_windows* 
                       (((size_t)sizeof(int32_t) * FT * Q.F.row + 15) & ~(size_t)15) +
                       (size_t)FT * stage_stride(K, B) + sizeof(ResolveQueue) * (FT / 32);
   static int sms = 0, occ = 0, occ_smem = 0;
+  cudaFuncSetAttribute(predict_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       96 * 1024);  // per device context: every call
   if (sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(predict_compact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         96 * 1024);
   }
   if (occ_smem != (int)smem) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, predict_compact_kernel, FT, smem);
