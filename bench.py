@@ -190,6 +190,10 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         if backend == "nccl":
+            # NCCL's init lines (ranks, NVLink / NVLS transport) go to stderr so
+            # a multi-GPU run shows how the ranks were connected
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
