@@ -29,6 +29,8 @@
 #include <algorithm>
 #include <numeric>
 #include <omp.h>
+#include <memory>
+#include <chrono>
 
 #include "paste.h"
 
@@ -45,6 +47,7 @@ enum LineKind : uint8_t { L_EMPTY, L_OK, L_MISSING, L_INVALID, L_ODD };
 
 struct Rec {
   std::string_view session, tool;
+  uint64_t sid_hash = 0, tool_hash = 0;  // computed in the parallel parse
   int64_t seq = 0;
   double t_start = 0, t_end = 0;
   int32_t line = 0;  // 1-based
@@ -180,21 +183,30 @@ static_assert(sizeof(TNode) == 16, "tape node is 16 bytes");
 enum { T_NULL = 0, T_FALSE, T_TRUE, T_INT, T_FLOAT, T_STR, T_LIST, T_DICT };
 enum { F_FLOATSRC = 2, F_NAN = 4, F_ASCII = 8 };
 
-struct Tape {
+// Payload tapes land in per-thread arenas (no allocation per line); keys
+// are interned per thread and renumbered globally after the parse.
+struct Arena {
   std::vector<TNode> nodes;
   std::vector<uint8_t> bytes;
+  std::unordered_map<std::string, int32_t> key_id;
+  std::vector<const std::string*> key_name;  // id -> name (map nodes are stable)
+  std::string scratch;
+  int64_t byte_base = 0;  // byte offset of the tape being written
+  int32_t intern(const std::string& k) {
+    auto it = key_id.find(k);
+    if (it != key_id.end()) return it->second;
+    const int32_t id = (int32_t)key_name.size();
+    it = key_id.emplace(k, id).first;
+    key_name.push_back(&it->first);
+    return id;
+  }
 };
 
+// where one line's two tapes (result, args) live in its thread's arena
 struct LineTapes {
-  Tape result, args;
-  bool has_result = false, has_args = false;
-  std::vector<std::string> keys;  // line-local key ids (few per line: linear search)
-  int32_t intern(const std::string& k) {
-    for (size_t i = 0; i < keys.size(); ++i)
-      if (keys[i] == k) return (int32_t)i;
-    keys.push_back(k);
-    return (int32_t)keys.size() - 1;
-  }
+  Arena* arena = nullptr;
+  int64_t node0[2] = {0, 0}, nnode[2] = {0, 0}, byte0[2] = {0, 0}, nbyte[2] = {0, 0};
+  bool has[2] = {false, false};
 };
 
 // Line starts and the str.splitlines() check, in parallel chunks.
@@ -372,15 +384,21 @@ std::string py_repr(double x) {
   return neg ? "-" + out : out;
 }
 
-void push_scalar(Tape& t, int32_t key, uint8_t type, uint8_t flags, const std::string& data) {
-  TNode nd{type, flags, 0, key, (uint32_t)t.bytes.size(), (uint32_t)data.size()};
-  t.bytes.insert(t.bytes.end(), data.begin(), data.end());
+void push_scalar(Arena& t, int32_t key, uint8_t type, uint8_t flags, const char* data,
+                 size_t len) {
+  TNode nd{type, flags, 0, key, (uint32_t)((int64_t)t.bytes.size() - t.byte_base),
+           (uint32_t)len};
+  t.bytes.insert(t.bytes.end(), data, data + len);
   t.nodes.push_back(nd);
+}
+
+void push_scalar(Arena& t, int32_t key, uint8_t type, uint8_t flags, const std::string& v) {
+  push_scalar(t, key, type, flags, v.data(), v.size());
 }
 
 // one JSON value -> tape nodes (pre-order; dict children in document order,
 // which is json.loads' insertion order when no key repeats)
-bool emit_value(Cursor& c, int32_t key, Tape& t, LineTapes& lt, int depth) {
+bool emit_value(Cursor& c, int32_t key, Arena& t, int depth) {
   c.ws();
   if (!c.ok || c.p >= c.e || depth > 512) return c.ok = false;
   const char ch = *c.p;
@@ -391,7 +409,8 @@ bool emit_value(Cursor& c, int32_t key, Tape& t, LineTapes& lt, int depth) {
     ++c.p;
     c.ws();
     uint32_t n = 0;
-    std::vector<int32_t> seen;
+    int32_t seen_small[16];
+    std::vector<int32_t> seen_big;
     if (c.p < c.e && *c.p == (dict ? '}' : ']')) {
       ++c.p;
     } else {
@@ -399,17 +418,21 @@ bool emit_value(Cursor& c, int32_t key, Tape& t, LineTapes& lt, int depth) {
         int32_t ck = -1;
         if (dict) {
           c.ws();
-          std::string k;
           bool ascii, safe;
-          if (!unescape(c, k, &ascii, &safe) || !safe) return c.ok = false;
-          ck = lt.intern(k);
-          if (std::find(seen.begin(), seen.end(), ck) != seen.end()) return c.ok = false;
-          seen.push_back(ck);
+          if (!unescape(c, t.scratch, &ascii, &safe) || !safe) return c.ok = false;
+          ck = t.intern(t.scratch);
+          // duplicate key (json.loads keeps the last value): host ingest
+          for (uint32_t q = 0; q < n && q < 16; ++q)
+            if (seen_small[q] == ck) return c.ok = false;
+          if (n >= 16 && std::find(seen_big.begin(), seen_big.end(), ck) != seen_big.end())
+            return c.ok = false;
+          if (n < 16) seen_small[n] = ck;
+          else seen_big.push_back(ck);
           c.ws();
           if (c.p >= c.e || *c.p != ':') return c.ok = false;
           ++c.p;
         }
-        if (!emit_value(c, ck, t, lt, depth + 1)) return false;
+        if (!emit_value(c, ck, t, depth + 1)) return false;
         ++n;
         c.ws();
         if (c.p < c.e && *c.p == ',') { ++c.p; continue; }
@@ -422,20 +445,20 @@ bool emit_value(Cursor& c, int32_t key, Tape& t, LineTapes& lt, int depth) {
     return true;
   }
   if (ch == '"') {
-    std::string v;
     bool ascii, safe;
-    if (!unescape(c, v, &ascii, &safe) || !safe) return c.ok = false;
-    push_scalar(t, key, T_STR, ascii ? F_ASCII : 0, v);
+    if (!unescape(c, t.scratch, &ascii, &safe) || !safe) return c.ok = false;
+    push_scalar(t, key, T_STR, ascii ? F_ASCII : 0, t.scratch);
     return true;
   }
-  if (ch == 't') { if (!c.lit("true")) return false; push_scalar(t, key, T_TRUE, 0, ""); return true; }
-  if (ch == 'f') { if (!c.lit("false")) return false; push_scalar(t, key, T_FALSE, 0, ""); return true; }
-  if (ch == 'n') { if (!c.lit("null")) return false; push_scalar(t, key, T_NULL, 0, ""); return true; }
+  if (ch == 't') { if (!c.lit("true")) return false; push_scalar(t, key, T_TRUE, 0, "", 0); return true; }
+  if (ch == 'f') { if (!c.lit("false")) return false; push_scalar(t, key, T_FALSE, 0, "", 0); return true; }
+  if (ch == 'n') { if (!c.lit("null")) return false; push_scalar(t, key, T_NULL, 0, "", 0); return true; }
   bool integral;
   const std::string_view v = parse_number(c, &integral);
   if (!c.ok || v.empty()) return c.ok = false;
   if (integral) {  // int(literal): "-0" is 0
-    push_scalar(t, key, T_INT, F_ASCII, v == "-0" ? std::string("0") : std::string(v));
+    if (v == "-0") push_scalar(t, key, T_INT, F_ASCII, "0", 1);
+    else push_scalar(t, key, T_INT, F_ASCII, v.data(), v.size());
     return true;
   }
   double x;
@@ -443,8 +466,8 @@ bool emit_value(Cursor& c, int32_t key, Tape& t, LineTapes& lt, int depth) {
   else if (v == "Infinity") x = INFINITY;
   else if (v == "-Infinity") x = -INFINITY;
   else x = strtod(std::string(v).c_str(), nullptr);
-  if (std::isnan(x)) push_scalar(t, key, T_FLOAT, F_NAN | F_ASCII, "nan");
-  else if (std::isinf(x)) push_scalar(t, key, T_FLOAT, F_ASCII, x > 0 ? "inf" : "-inf");
+  if (std::isnan(x)) push_scalar(t, key, T_FLOAT, F_NAN | F_ASCII, "nan", 3);
+  else if (std::isinf(x)) push_scalar(t, key, T_FLOAT, F_ASCII, x > 0 ? "inf" : "-inf", x > 0 ? 3 : 4);
   else if (x == std::floor(x)) push_scalar(t, key, T_INT, F_FLOATSRC | F_ASCII, int_digits(x));
   else push_scalar(t, key, T_FLOAT, F_ASCII, py_repr(x));
   return true;
@@ -518,10 +541,16 @@ void parse_line(const char* b, const char* e, Rec& r, LineTapes* lt = nullptr) {
         }
       }
     } else if (lt && (key == "result" || key == "args")) {
-      const bool res = key == "result";
-      if (res ? lt->has_result : lt->has_args) { r.kind = L_ODD; return; }  // last wins in Python
-      (res ? lt->has_result : lt->has_args) = true;
-      if (!emit_value(c, -1, res ? lt->result : lt->args, *lt, 1)) { r.kind = L_ODD; return; }
+      const int q = key == "result" ? 0 : 1;
+      if (lt->has[q]) { r.kind = L_ODD; return; }  // duplicate field: last wins in Python
+      lt->has[q] = true;
+      Arena& a = *lt->arena;
+      a.byte_base = (int64_t)a.bytes.size();
+      lt->node0[q] = (int64_t)a.nodes.size();
+      lt->byte0[q] = a.byte_base;
+      if (!emit_value(c, -1, a, 1)) { r.kind = L_ODD; return; }
+      lt->nnode[q] = (int64_t)a.nodes.size() - lt->node0[q];
+      lt->nbyte[q] = (int64_t)a.bytes.size() - lt->byte0[q];
     } else {
       skip_value(c, 1);
       if (!c.ok) { r.kind = L_ODD; return; }
@@ -701,12 +730,24 @@ struct paste_jsonl {
   std::vector<int64_t> err_seq;
   std::vector<double> t_start, t_end;
   std::string tool_names, key_names;
-  std::vector<TNode> nodes;
-  std::vector<uint8_t> bytes;
-  std::vector<paste_event_ref> refs;
+  std::unique_ptr<TNode[]> nodes;  // default-initialised (no zero fill): written in parallel
+  std::unique_ptr<uint8_t[]> bytes;
+  std::unique_ptr<paste_event_ref[]> refs;
+  int64_t n_nodes = 0, n_bytes = 0, n_refs = 0;
   int64_t n_sessions = 0, n_lines = 0, n_keys = 0;
   int32_t n_tools = 0;
 };
+
+namespace {
+struct HashedView {  // a string view with its hash computed once
+  std::string_view s;
+  uint64_t h;
+  bool operator==(const HashedView& o) const { return h == o.h && s == o.s; }
+};
+struct HashedViewHash {
+  size_t operator()(const HashedView& v) const { return (size_t)v.h; }
+};
+}  // namespace
 
 extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_payloads,
                                  paste_jsonl** out) {
@@ -716,14 +757,27 @@ extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_pay
     return PASTE_ERR_INVALID;
   }
   *out = nullptr;
+  const bool prof = getenv("PASTE_JSONL_PROF") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t0 = now();
+  auto lap = [&](const char* what) {
+    if (!prof) return;
+    const auto t1 = now();
+    fprintf(stderr, "jsonl %-10s %.1f ms\n", what,
+            std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
   std::vector<int64_t> starts;
   if (!split_lines(text, len, starts)) {
     set_error("line separators other than '\\n': host ingest");
     return PASTE_ERR_UNSUPPORTED;
   }
   const int64_t n_lines = len == 0 ? 0 : (int64_t)starts.size();
+  lap("split");
   std::vector<Rec> recs(n_lines);
   std::vector<LineTapes> tapes(want_payloads ? n_lines : 0);
+  std::vector<std::unique_ptr<Arena>> arenas((size_t)omp_get_max_threads());
+  for (auto& a : arenas) a.reset(new Arena());
   bool odd = false;
 #pragma omp parallel for schedule(dynamic, 1024) reduction(|| : odd)
   for (int64_t i = 0; i < n_lines; ++i) {
@@ -731,17 +785,33 @@ extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_pay
     const char* e = i + 1 < n_lines ? text + starts[i + 1] - 1 : text + len;
     if (e > b && e[-1] == '\n') --e;
     recs[i].line = (int32_t)(i + 1);
-    parse_line(b, e, recs[i], want_payloads ? &tapes[i] : nullptr);
+    LineTapes* lt = nullptr;
+    if (want_payloads) {
+      lt = &tapes[i];
+      lt->arena = arenas[(size_t)omp_get_thread_num()].get();
+    }
+    parse_line(b, e, recs[i], lt);
+    if (recs[i].kind == L_OK) {
+      recs[i].sid_hash = std::hash<std::string_view>()(recs[i].session);
+      recs[i].tool_hash = std::hash<std::string_view>()(recs[i].tool);
+    }
     odd = odd || recs[i].kind == L_ODD;
   }
+  lap("parse");
   if (odd) {
     set_error("records outside the native parser's exact subset: host ingest");
     return PASTE_ERR_UNSUPPORTED;
   }
   auto* h = new paste_jsonl();
   h->n_lines = n_lines;
-  std::unordered_map<std::string_view, int32_t> sid, tool_id;
+  std::unordered_map<HashedView, int32_t, HashedViewHash> sid, tool_id;
+  sid.reserve((size_t)n_lines / 8 + 16);
+  for (auto* v : {&h->session, &h->seq, &h->sig}) v->reserve((size_t)n_lines);
+  h->t_start.reserve((size_t)n_lines);
+  h->t_end.reserve((size_t)n_lines);
   std::vector<std::string_view> tools;
+  HashedView last_hv{};
+  int32_t last_sid = -1;
   std::vector<int64_t> row_line;  // line of every valid row
   row_line.reserve((size_t)n_lines);
   for (int64_t i = 0; i < n_lines; ++i) {
@@ -753,17 +823,23 @@ extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_pay
       h->err_seq.push_back(r.seq);
       continue;
     }
-    auto it = sid.find(r.session);
-    if (it == sid.end()) it = sid.emplace(r.session, (int32_t)sid.size()).first;
-    h->session.push_back(it->second);
+    const HashedView hv{r.session, r.sid_hash};
+    if (!(last_sid >= 0 && hv == last_hv)) {  // records of a session mostly arrive together
+      auto it = sid.find(hv);
+      if (it == sid.end()) it = sid.emplace(hv, (int32_t)sid.size()).first;
+      last_hv = hv;
+      last_sid = it->second;
+    }
+    h->session.push_back(last_sid);
     h->seq.push_back((int32_t)r.seq);
     h->t_start.push_back(r.t_start);
     h->t_end.push_back(r.t_end);
     int32_t tid = -1;
     if (r.tool_call) {
-      auto t = tool_id.find(r.tool);
+      const HashedView tv{r.tool, r.tool_hash};
+      auto t = tool_id.find(tv);
       if (t == tool_id.end()) {
-        t = tool_id.emplace(r.tool, (int32_t)tools.size()).first;
+        t = tool_id.emplace(tv, (int32_t)tools.size()).first;
         tools.push_back(r.tool);
       }
       tid = t->second;
@@ -772,74 +848,70 @@ extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_pay
     row_line.push_back(i);
   }
   const int64_t n_rows = (int64_t)row_line.size();
-  std::unordered_map<std::string_view, int32_t> key_id;
+  lap("rows");
+  int64_t n_keys = 0;
   if (want_payloads) {
-    // distinct keys (per thread, merged), ids in sorted key order: deterministic
-    std::vector<std::vector<std::string_view>> seen;
-#pragma omp parallel
-    {
-#pragma omp single
-      seen.resize((size_t)omp_get_num_threads());
-      std::unordered_map<std::string_view, char> mine;
-#pragma omp for schedule(static)
-      for (int64_t r = 0; r < n_rows; ++r)
-        for (const std::string& k : tapes[row_line[r]].keys) mine.emplace(k, 0);
-      auto& out = seen[(size_t)omp_get_thread_num()];
-      for (auto& kv : mine) out.push_back(kv.first);
-    }
+    // global key ids in sorted key order (deterministic), a remap per arena
     std::vector<std::string_view> all;
-    for (auto& v : seen) all.insert(all.end(), v.begin(), v.end());
+    for (auto& a : arenas)
+      for (const std::string* k : a->key_name) all.push_back(*k);
     std::sort(all.begin(), all.end());
     all.erase(std::unique(all.begin(), all.end()), all.end());
+    std::unordered_map<std::string_view, int32_t> key_id;
     for (size_t k = 0; k < all.size(); ++k) {
       key_id.emplace(all[k], (int32_t)k);
       h->key_names.append(all[k].data(), all[k].size());
       h->key_names.push_back('\0');
     }
+    n_keys = (int64_t)all.size();
+    std::unordered_map<const Arena*, std::vector<int32_t>> remap;
+    for (auto& a : arenas) {
+      std::vector<int32_t>& rm = remap[a.get()];
+      rm.resize(a->key_name.size());
+      for (size_t k = 0; k < rm.size(); ++k) rm[k] = key_id.at(std::string_view(*a->key_name[k]));
+    }
     // tape offsets (absent payload = one null node), then a parallel copy
     std::vector<int64_t> node_off(2 * n_rows + 1, 0), byte_off(2 * n_rows + 1, 0);
     for (int64_t r = 0; r < n_rows; ++r) {
       const LineTapes& lt = tapes[row_line[r]];
-      int q = 0;
-      for (const Tape* t : {&lt.result, &lt.args}) {
-        const int64_t j = 2 * r + q++;
-        node_off[j + 1] = node_off[j] + (t->nodes.empty() ? 1 : (int64_t)t->nodes.size());
-        byte_off[j + 1] = byte_off[j] + (int64_t)t->bytes.size();
+      for (int q = 0; q < 2; ++q) {
+        const int64_t j = 2 * r + q;
+        node_off[j + 1] = node_off[j] + (lt.nnode[q] ? lt.nnode[q] : 1);
+        byte_off[j + 1] = byte_off[j] + lt.nbyte[q];
       }
     }
-    h->nodes.resize((size_t)node_off[2 * n_rows]);
-    h->bytes.resize((size_t)byte_off[2 * n_rows]);
-    h->refs.resize((size_t)(2 * n_rows));
+    h->n_nodes = node_off[2 * n_rows];
+    h->n_bytes = byte_off[2 * n_rows];
+    h->n_refs = 2 * n_rows;
+    h->nodes.reset(new TNode[(size_t)h->n_nodes + 1]);
+    h->bytes.reset(new uint8_t[(size_t)h->n_bytes + 1]);
+    h->refs.reset(new paste_event_ref[(size_t)h->n_refs + 1]);
 #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t r = 0; r < n_rows; ++r) {
-      LineTapes& lt = tapes[row_line[r]];
-      int32_t remap[64];
-      std::vector<int32_t> big;
-      int32_t* rm = remap;
-      if (lt.keys.size() > 64) {
-        big.resize(lt.keys.size());
-        rm = big.data();
-      }
-      for (size_t k = 0; k < lt.keys.size(); ++k) rm[k] = key_id.at(std::string_view(lt.keys[k]));
-      int q = 0;
-      for (Tape* t : {&lt.result, &lt.args}) {
-        const int64_t j = 2 * r + q++;
+      const LineTapes& lt = tapes[row_line[r]];
+      const std::vector<int32_t>& rm = remap.at(lt.arena);
+      for (int q = 0; q < 2; ++q) {
+        const int64_t j = 2 * r + q;
         h->refs[(size_t)j] = paste_event_ref{node_off[j], byte_off[j]};
-        TNode* dst = h->nodes.data() + node_off[j];
-        if (t->nodes.empty()) {
+        TNode* dst = h->nodes.get() + node_off[j];
+        if (lt.nnode[q] == 0) {
           *dst = TNode{T_NULL, 0, 0, -1, 0, 0};  // absent: record.get -> None
-        } else {
-          for (size_t x = 0; x < t->nodes.size(); ++x) {
-            TNode nd = t->nodes[x];
-            if (nd.key >= 0) nd.key = rm[nd.key];
-            dst[x] = nd;
-          }
+          continue;
         }
-        if (!t->bytes.empty()) memcpy(h->bytes.data() + byte_off[j], t->bytes.data(), t->bytes.size());
+        const TNode* src = lt.arena->nodes.data() + lt.node0[q];
+        for (int64_t x = 0; x < lt.nnode[q]; ++x) {
+          TNode nd = src[x];
+          if (nd.key >= 0) nd.key = rm[(size_t)nd.key];
+          dst[x] = nd;
+        }
+        if (lt.nbyte[q])
+          memcpy(h->bytes.get() + byte_off[j], lt.arena->bytes.data() + lt.byte0[q],
+                 (size_t)lt.nbyte[q]);
       }
     }
   }
-  h->n_keys = (int64_t)key_id.size();
+  lap("tapes");
+  h->n_keys = n_keys;
   h->n_sessions = (int64_t)sid.size();
   // tools in sorted name order: sig = 2 * rank + success
   std::vector<int32_t> order(tools.size());
@@ -867,8 +939,8 @@ extern "C" int paste_jsonl_sizes_of(const paste_jsonl* h, paste_jsonl_sizes* s) 
   s->n_sessions = h->n_sessions;
   s->n_errors = (int64_t)h->err_line.size();
   s->n_lines = h->n_lines;
-  s->n_nodes = (int64_t)h->nodes.size();
-  s->n_bytes = (int64_t)h->bytes.size();
+  s->n_nodes = h->n_nodes;
+  s->n_bytes = h->n_bytes;
   s->n_keys = h->n_keys;
   s->key_names_len = (int64_t)h->key_names.size();
   s->tool_names_len = (int64_t)h->tool_names.size();
@@ -895,9 +967,9 @@ extern "C" int paste_jsonl_copy(const paste_jsonl* h, const paste_jsonl_out* o) 
   cp(o->error_codes, h->err_code.data(), 4 * h->err_code.size());
   cp(o->error_seq, h->err_seq.data(), 8 * h->err_seq.size());
   cp(o->tool_names, h->tool_names.data(), h->tool_names.size());
-  cp(o->nodes, h->nodes.data(), sizeof(TNode) * h->nodes.size());
-  cp(o->bytes, h->bytes.data(), h->bytes.size());
-  cp(o->refs, h->refs.data(), sizeof(paste_event_ref) * h->refs.size());
+  cp(o->nodes, h->nodes.get(), sizeof(TNode) * (size_t)h->n_nodes);
+  cp(o->bytes, h->bytes.get(), (size_t)h->n_bytes);
+  cp(o->refs, h->refs.get(), sizeof(paste_event_ref) * (size_t)h->n_refs);
   cp(o->key_names, h->key_names.data(), h->key_names.size());
   return PASTE_OK;
 }
