@@ -417,8 +417,17 @@ def _phase2_corpus(tok_dev, flat, sigs: SigTable, rows: list, idx: list, S: int,
             out[i] = (None, r[4])
             continue
         if ct is None:
-            ct = corpus() if corpus is not None else \
-                pc.CorpusTapes.from_events(flat, tok_host, tok_dev, sigs)
+            try:
+                ct = corpus() if corpus is not None else \
+                    pc.CorpusTapes.from_events(flat, tok_host, tok_dev, sigs)
+            except TypeError:
+                # a payload the tape cannot hold (not JSON-like) somewhere in the
+                # corpus: per-candidate occurrence sets, as in the sharded path
+                ct = False
+        if ct is False:
+            occ = device_occurrences(tok_dev, flat, sigs, [cands[idx.index(i)]], cfg)[0]
+            out[i] = _phase2(occ, cfg, r[4])
+            continue
         co = pc.CorpusOccurrences(ct, anc, pk, sigs.tools[r[0]])
         mapping = pc.infer_mapping(co, cfg.validation_fraction)
         out[i] = (None, r[4]) if mapping is None else (mapping, pc.count_mapping_hits(mapping, co))

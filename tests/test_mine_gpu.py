@@ -374,3 +374,24 @@ def test_device_occurrences_equal_host_rescan(rel, k):
             assert all(x is y for x, y in zip(m1.events, m2.events))
             assert len(m1.history) == len(m2.history)
             assert all(x is y for x, y in zip(m1.history, m2.history))
+
+
+def test_mine_with_non_json_payload_outside_mappings():
+    """A payload the tape cannot hold (a tuple) on an event no mapping needs:
+    mine() still equals the reference semantics (per-candidate occurrence
+    sets instead of the corpus tape)."""
+    from paper_2603_18897_b200.events import Event, EventKind, Session
+
+    sessions = []
+    for i in range(20):
+        url = f"https://x{i}.example"
+        evs = (Event(f"s{i}", 0, EventKind.TOOL_CALL, "search", Status.SUCCESS, {"q": str(i)},
+                     {"list": [{"url": url}]}, 0.0, 1.0),
+               Event(f"s{i}", 1, EventKind.TOOL_CALL, "web_fetch", Status.SUCCESS, {"url": url},
+                     {"ok": 1}, 2.0, 3.0),
+               Event(f"s{i}", 2, EventKind.TOOL_CALL, "note", Status.SUCCESS, None,
+                     ("opaque", i), 4.0, 5.0))
+        sessions.append(Session(f"s{i}", evs))
+    pats = mine(sessions, MiningConfig(k=1, sigma=5, tau=0.5))
+    m = [p for p in pats if p.target == "web_fetch"]
+    assert m and m[0].mapping is not None and m[0].p == 1.0
