@@ -268,6 +268,26 @@ int paste_mine_geometry(int32_t n_sigs, int32_t k, int64_t* n_bins, int64_t* n_c
 int paste_mine_count(const paste_mine_desc* d, void* stream);
 /* Expand the histogram into tool_count / support / match / follow.         */
 int paste_mine_expand(const paste_mine_desc* d, void* stream);
+
+/* Target-sliced tail for strong scaling.  support[t][*],
+ * follow[*][t] and tool_count[t] only read histogram column s0 in {2t,
+ * 2t+1} (the gram's last symbol = the target), and match[c] only reads the
+ * grams whose last symbol is c's last symbol (the anchor).  So with the
+ * columns cut into n_slices equal blocks of `slice_cols` (even, covering
+ * every sig; paste_mine_slice_cols), rank r expands block r alone:
+ *   paste_mine_transpose_slices: hist [window][s0] -> hist_t [s0][window]
+ *     for s0 < n_slices * slice_cols (columns >= n_sigs are zero), so block
+ *     r is contiguous (reduce-scatter it);
+ *   paste_mine_expand_slice: expand block r (slice [col_lo, col_lo +
+ *     slice_cols) of hist_t, [slice_cols][base^k]) into the zeroed tables:
+ *     complete values for the block's tools and for the match of contexts
+ *     whose last signature is in the block, zero elsewhere (sum the match
+ *     arrays over the ranks; the other tables are disjoint).              */
+int32_t paste_mine_slice_cols(int32_t n_sigs, int32_t n_slices);
+int paste_mine_transpose_slices(const paste_mine_desc* d, int32_t n_slices, uint32_t* hist_t,
+                                void* stream);
+int paste_mine_expand_slice(const paste_mine_desc* d, const uint32_t* slice, int32_t col_lo,
+                            int32_t slice_cols, void* stream);
 /* Candidates (target, context) with tool_count >= sigma, support >= sigma,
  * match > 0 and follow / match >= tau (the upper bound of p for any
  * mapping): out[5*i..] = {tool, context index, support, match, follow};

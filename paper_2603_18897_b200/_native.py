@@ -288,6 +288,9 @@ EXPORTS = {
     "paste_select_victim": (c_int, [POINTER(SelectDesc), c_void_p, c_void_p, c_void_p]),
     "paste_mine_ingest_count": (c_int, [POINTER(ColumnarDesc), POINTER(MineDesc), c_void_p]),
     "paste_mine_expand": (c_int, [POINTER(MineDesc), c_void_p]),
+    "paste_mine_slice_cols": (c_int32, [c_int32, c_int32]),
+    "paste_mine_transpose_slices": (c_int, [POINTER(MineDesc), c_int32, c_void_p, c_void_p]),
+    "paste_mine_expand_slice": (c_int, [POINTER(MineDesc), c_void_p, c_int32, c_int32, c_void_p]),
     "paste_mine_select": (c_int, [POINTER(MineDesc), c_int64, ctypes.c_double, c_int64, c_void_p,
                                   c_void_p, c_void_p]),
     "paste_mine_sort_scratch_bytes": (c_int64, [c_int64]),

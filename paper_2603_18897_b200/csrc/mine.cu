@@ -286,6 +286,111 @@ __global__ void __launch_bounds__(XT) expand_windows_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// target-sliced tail: the same expansion over one block of histogram columns
+// (s0 in [lo, lo + W)), read from the s0-major slice [s0 - lo][window].
+// Windows with no count in the block and an anchor outside it are skipped
+// before their contexts are enumerated.
+// ---------------------------------------------------------------------------
+__global__ void transpose_slices_kernel(const uint32_t* __restrict__ hist, int64_t n_win, int base,
+                                        int S, int cols, uint32_t* __restrict__ out) {
+  // out[c][w] = hist[w * base + c] (c < S), 0 for S <= c < cols
+  const int64_t total = (int64_t)cols * n_win;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / n_win, w = i - c * n_win;
+    out[i] = c < S ? __ldg(hist + w * base + c) : 0u;
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(XT) expand_slice_kernel(
+    const uint32_t* __restrict__ slice, int lo, int width, MineGeom g, int relation,
+    unsigned long long* tool_count, unsigned long long* support, unsigned long long* match,
+    unsigned long long* follow) {
+  const int S = g.S, T = g.T, base = g.base, BEGIN = S, END = S + 1;
+  const bool anchored = relation == PASTE_REL_ANCHORED;
+  const int lane = threadIdx.x & 31;
+  const int64_t n_win = g.n_bins / base;
+  const int64_t warp0 = ((int64_t)blockIdx.x * XT + threadIdx.x) >> 5;
+  const int64_t n_warps = ((int64_t)gridDim.x * XT) >> 5;
+  for (int64_t wi = warp0; wi < n_win; wi += n_warps) {
+    int sym[K + 1];
+    {
+      uint32_t v = (uint32_t)wi;
+#pragma unroll
+      for (int d = 1; d <= K; ++d) {
+        sym[d] = (int)(v % (uint32_t)base);
+        v /= (uint32_t)base;
+      }
+    }
+    int nb = 0;
+    bool valid = true;
+#pragma unroll
+    for (int d = K; d >= 1; --d) {
+      if (sym[d] == END) valid = false;
+      if (sym[d] == BEGIN) {
+        if (nb != K - d) valid = false;
+        ++nb;
+      }
+    }
+    if (!valid) continue;
+    const int wl = K - nb;
+    const bool anchor_here = wl > 0 && sym[1] >= lo && sym[1] < lo + width;
+    // this block's counts of the window (lane = column - lo, width <= 32 per chunk)
+    bool any = false;
+    for (int c0 = 0; c0 < width && !any; c0 += 32)
+      any = __ballot_sync(0xffffffffu, c0 + lane < width &&
+                                           __ldg(slice + (int64_t)(c0 + lane) * n_win + wi) != 0u) != 0;
+    if (!any && !anchor_here) continue;
+    int win[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) win[i] = i < wl ? sym[wl - i] : 0;
+    int64_t sup_ctx[(1 << K)];
+    int64_t mt_ctx[(1 << K)];
+    const int n_sup = wl > 0 ? window_contexts<K>(g, win, wl, anchored, false, -1, sup_ctx) : 0;
+    const int n_mt = wl > 0 ? window_contexts<K>(g, win, wl - 1, anchored, true, sym[1], mt_ctx) : 0;
+    for (int c0 = 0; c0 < width; c0 += 32) {
+      const int col = c0 + lane;
+      const uint32_t h = col < width ? __ldg(slice + (int64_t)col * n_win + wi) : 0u;
+      if (__ballot_sync(0xffffffffu, h != 0) == 0) continue;
+      const int s0 = lo + col;  // lo and width are even: tool pairs share a chunk
+      const unsigned long long hs = s0 < S ? h : 0u;
+      const unsigned long long ht = hs + __shfl_xor_sync(0xffffffffu, hs, 1);
+      if ((s0 & 1) || ht == 0) continue;
+      const int t = s0 >> 1;
+      atomicAdd(tool_count + t, ht);
+#pragma unroll
+      for (int q = 0; q < (1 << K); ++q) {
+        if (q >= n_sup) break;
+        atomicAdd(support + (int64_t)t * g.n_ctx + sup_ctx[q], ht);
+      }
+#pragma unroll
+      for (int q = 0; q < (1 << K); ++q) {
+        if (q >= n_mt) break;
+        atomicAdd(follow + mt_ctx[q] * T + t, ht);
+      }
+    }
+    if (!anchor_here || n_mt == 0) continue;
+    // anchors whose last K symbols are this window: the grams x*base^K + wi,
+    // all of column sym[1] (row x*base^(K-1) + wi/base of the s0-major slice)
+    const int64_t pw1 = n_win / base;  // base^(K-1)
+    const uint32_t* col = slice + (int64_t)(sym[1] - lo) * n_win + wi / base;
+    unsigned long long tot = 0;
+    for (int x = lane; x < base; x += 32) tot += __ldg(col + (int64_t)x * pw1);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (tot == 0) continue;
+    if (lane < n_mt) {
+      int64_t c = 0;
+#pragma unroll
+      for (int q = 0; q < (1 << K); ++q)
+        if (q == lane) c = mt_ctx[q];
+      atomicAdd(match + c, tot);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // select: (target, context) pairs clearing the sigma gates and the tau bound
 // ---------------------------------------------------------------------------
 __global__ void select_kernel(MineGeom g, const unsigned long long* tool_count,
@@ -483,6 +588,72 @@ extern "C" int paste_mine_expand(const paste_mine_desc* d, void* stream) {
   }
   PASTE_EXPAND(1) PASTE_EXPAND(2) PASTE_EXPAND(3) PASTE_EXPAND(4) PASTE_EXPAND(5) PASTE_EXPAND(6)
 #undef PASTE_EXPAND
+  PASTE_REQUIRE(rc == 0, "k=%d outside the expand kernel's range", d->k);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
+
+extern "C" int32_t paste_mine_slice_cols(int32_t n_sigs, int32_t n_slices) {
+  if (n_sigs < 1 || n_slices < 1) return 0;
+  const int32_t tools = (n_sigs + 1) / 2;
+  return 2 * ((tools + n_slices - 1) / n_slices);
+}
+
+extern "C" int paste_mine_transpose_slices(const paste_mine_desc* d, int32_t n_slices,
+                                           uint32_t* hist_t, void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(d != nullptr && hist_t != nullptr && d->hist != nullptr, "null argument");
+  MineGeom g;
+  if (make_geom(d->n_sigs, d->k, &g) != 0) {
+    set_error("mining geometry out of range (n_sigs=%d, k=%d)", d->n_sigs, d->k);
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  const int32_t w = paste_mine_slice_cols(d->n_sigs, n_slices);
+  PASTE_REQUIRE(w > 0, "n_slices must be >= 1");
+  const int64_t n_win = g.n_bins / g.base;
+  const int64_t total = (int64_t)w * n_slices * n_win;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  transpose_slices_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      d->hist, n_win, g.base, g.S, w * n_slices, hist_t);
+  count_launch();
+  PASTE_CUDA_CHECK(cudaGetLastError());
+  return PASTE_OK;
+}
+
+extern "C" int paste_mine_expand_slice(const paste_mine_desc* d, const uint32_t* slice,
+                                       int32_t col_lo, int32_t slice_cols, void* stream) {
+  reset_launches();
+  PASTE_REQUIRE(d != nullptr && slice != nullptr, "null argument");
+  PASTE_REQUIRE(col_lo >= 0 && slice_cols > 0 && (col_lo % 2) == 0 && (slice_cols % 2) == 0,
+                "slice columns must be a non-empty even-aligned block");
+  MineGeom g;
+  if (make_geom(d->n_sigs, d->k, &g) != 0) {
+    set_error("mining geometry out of range (n_sigs=%d, k=%d)", d->n_sigs, d->k);
+    return PASTE_ERR_UNSUPPORTED;
+  }
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int64_t n_win = g.n_bins / g.base;
+  const int64_t want = (n_win + XT / 32 - 1) / (XT / 32);
+  const int64_t cap = (int64_t)sms * 4;
+  const unsigned grid = (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
+  int rc = -1;
+#define PASTE_EXPAND_SLICE(KV)                                                               \
+  if (d->k == KV) {                                                                          \
+    expand_slice_kernel<KV><<<grid, XT, 0, (cudaStream_t)stream>>>(                          \
+        slice, col_lo, slice_cols, g, d->relation, U64(d->tool_count), U64(d->support),      \
+        U64(d->match), U64(d->follow));                                                      \
+    rc = 0;                                                                                  \
+  }
+  PASTE_EXPAND_SLICE(1) PASTE_EXPAND_SLICE(2) PASTE_EXPAND_SLICE(3) PASTE_EXPAND_SLICE(4)
+  PASTE_EXPAND_SLICE(5) PASTE_EXPAND_SLICE(6)
+#undef PASTE_EXPAND_SLICE
   PASTE_REQUIRE(rc == 0, "k=%d outside the expand kernel's range", d->k);
   count_launch();
   PASTE_CUDA_CHECK(cudaGetLastError());

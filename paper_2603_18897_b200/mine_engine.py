@@ -711,6 +711,62 @@ class MinedTable:
         return out
 
 
+def sharded_tail(tables: "MineTables", group, sigma: int, tau: float) -> "MinedTable":
+    """The target-sliced mining tail: every rank expands one
+    block of histogram columns and selects the candidates of its tools, so
+    the expansion and selection work falls with the rank count.
+
+      * support / follow / tool_count of target t read only column s0 in
+        {2t, 2t+1} (the gram's last symbol); match[c] reads only the grams
+        whose last symbol is c's last symbol (the anchor).  The histogram is
+        transposed to s0-major blocks (paste_mine_transpose_slices) and
+        reduce-scattered: rank r receives block r summed over the shards;
+      * paste_mine_expand_slice fills the rank's tools' tables and the
+        match of the contexts anchored in its block; one all-reduce (sum)
+        of the match array (n_ctx u64) completes it;
+      * each rank selects + sorts its own candidates on the device; the
+        sorted rows (a few thousand) are all-gathered and merged in the
+        reference's order (-p, -len, target, context).
+    Every rank returns the single-device table."""
+    import torch.distributed as dist
+
+    from .device_ops import stream_handle
+
+    torch = _torch()
+    lib = _native.lib()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    w = int(lib.paste_mine_slice_cols(tables.n_sigs, world))
+    base = tables.n_sigs + 2
+    n_win = tables.n_bins // base
+    d = tables.desc()
+    hist_t = torch.empty(world * w * n_win, dtype=torch.int32, device="cuda")
+    check(lib.paste_mine_transpose_slices(ctypes.byref(d), world, ptr(hist_t), stream_handle()), lib)
+    if dist.get_backend(group) == "nccl":
+        block = torch.empty(w * n_win, dtype=torch.int32, device="cuda")
+        dist.reduce_scatter_tensor(block, hist_t, group=group)
+    else:  # gloo has no reduce-scatter: sum everything, keep this rank's block
+        dist.all_reduce(hist_t, group=group)
+        block = hist_t[rank * w * n_win:(rank + 1) * w * n_win].contiguous()
+    for t in (tables.tool_count, tables.support, tables.match, tables.follow):
+        t.zero_()
+    check(lib.paste_mine_expand_slice(ctypes.byref(d), ptr(block), rank * w, w, stream_handle()),
+          lib)
+    dist.all_reduce(tables.match, group=group)
+    mine = tables.select_sorted(sigma, tau)
+    parts = [None] * world
+    dist.all_gather_object(parts, mine.rows, group=group)
+    rows = np.concatenate([p for p in parts if len(p)] or [np.zeros((0, 6), np.int64)])
+    if len(rows):
+        S, k = tables.n_sigs, tables.k
+        off = np.array(ctx_offsets(S, k), np.int64)
+        length = np.searchsorted(off[1:], rows[:, 1], side="right")
+        local = rows[:, 1] - off[length]
+        p = rows[:, 5].view(np.float64)
+        # the device sort key (hi = ~bits(p), lo = (k - len, tool, digits)) in numpy
+        rows = rows[np.lexsort((local, rows[:, 0], -length, -p))]
+    return MinedTable(np.ascontiguousarray(rows), tables.n_sigs, tables.k)
+
+
 def merge_shard_histograms(hist, counters, group) -> None:
     """K3: sum the per-shard (k+1)-gram histograms (and the ingest counters)
     across ranks.  Windows and matches never cross a session, so with shards
@@ -795,7 +851,10 @@ def mine_columnar(trace: dict, sigs: SigTable, cfg: MiningConfig,
         ordered = order_columnar(trace, n_sessions, inactivity_ms)
         tables.hist.zero_()
         counters = ingest_count(tables, ordered.columns, float("inf"))
-    if group is not None:
-        merge_shard_histograms(tables.hist, counters, group)
+    if group is not None:  # whole-session shards: the sliced tail (sharded_tail)
+        import torch.distributed as dist
+
+        dist.all_reduce(counters, group=group)
+        return sharded_tail(tables, group, cfg.sigma, cfg.tau).patterns(sigs)
     tables.expand()
     return tables.select_sorted(cfg.sigma, cfg.tau).patterns(sigs)

@@ -395,3 +395,43 @@ def test_mine_with_non_json_payload_outside_mappings():
     pats = mine(sessions, MiningConfig(k=1, sigma=5, tau=0.5))
     m = [p for p in pats if p.target == "web_fetch"]
     assert m and m[0].mapping is not None and m[0].p == 1.0
+
+
+@pytest.mark.parametrize("slices,rel,k", [(1, 0, 3), (2, 0, 3), (3, 1, 3), (8, 0, 3), (5, 0, 2),
+                                          (4, 1, 4)])
+def test_sliced_expand_sums_to_full_expand(slices, rel, k):
+    """The target-sliced tail (paste_mine_transpose_slices + expand_slice):
+    for every slice count the per-block tables -- tools of the block, match
+    of the contexts anchored in it -- add up to the full expansion exactly,
+    and each block's selection is the full selection restricted to its
+    tools."""
+    import ctypes
+
+    from paper_2603_18897_b200 import _native
+    from paper_2603_18897_b200._native import check, ptr
+    from paper_2603_18897_b200.synth import columnar_corpus
+
+    lib = _native.lib()
+    c = columnar_corpus(300_000, seed=70 + slices)
+    full = MineTables.allocate(32, k, rel)
+    from paper_2603_18897_b200.mine_engine import ingest_count
+    ingest_count(full, _dev(c))
+    part = MineTables.allocate(32, k, rel)
+    part.hist.copy_(full.hist)
+    full.expand()
+    w = int(lib.paste_mine_slice_cols(32, slices))
+    n_win = full.n_bins // 34
+    hist_t = torch.empty(slices * w * n_win, dtype=torch.int32, device="cuda")
+    d = part.desc()
+    check(lib.paste_mine_transpose_slices(ctypes.byref(d), slices, ptr(hist_t), None), lib)
+    acc = {n: torch.zeros_like(getattr(full, n)) for n in ("tool_count", "support", "match",
+                                                           "follow")}
+    for r in range(slices):
+        for n in acc:
+            getattr(part, n).zero_()
+        block = hist_t[r * w * n_win:(r + 1) * w * n_win].contiguous()
+        check(lib.paste_mine_expand_slice(ctypes.byref(d), ptr(block), r * w, w, None), lib)
+        for n in acc:
+            acc[n] += getattr(part, n)
+    for n in acc:
+        assert torch.equal(acc[n], getattr(full, n)), n
