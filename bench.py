@@ -831,7 +831,7 @@ def mining_relation(args, world, rank, sigs, host, host_pinned, dev, group, rela
     import torch.distributed as dist
 
     from paper_2603_18897_b200 import _native
-    from paper_2603_18897_b200.mine_engine import MineTables, ingest_count
+    from paper_2603_18897_b200.mine_engine import MineTables, ingest_count, sharded_tail
     from paper_2603_18897_b200.mining import MatchRelation, MiningConfig
 
     n_local = int(host["sig"].shape[0])
@@ -845,8 +845,8 @@ def mining_relation(args, world, rank, sigs, host, host_pinned, dev, group, rela
     def one_step(trace):
         tables.hist.zero_()
         ingest_count(tables, trace)
-        if group is not None:
-            dist.all_reduce(tables.hist, group=group)
+        if group is not None:  # target-sliced tail: reduce-scatter, per-block expand + select
+            return sharded_tail(tables, group, cfg.sigma, cfg.tau)
         tables.expand()
         # selection + mine()'s output order on the device; the sorted pattern
         # table is read back to the host (the step's result)
