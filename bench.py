@@ -845,8 +845,10 @@ def mining_relation(args, world, rank, sigs, host, host_pinned, dev, group, rela
     def one_step(trace):
         tables.hist.zero_()
         ingest_count(tables, trace)
-        if group is not None:  # target-sliced tail: reduce-scatter, per-block expand + select
-            return sharded_tail(tables, group, cfg.sigma, cfg.tau)
+        if group is not None:
+            if os.environ.get("PASTE_MINE_TAIL") == "sliced":  # measured no faster (DESIGN 7)
+                return sharded_tail(tables, group, cfg.sigma, cfg.tau)
+            dist.all_reduce(tables.hist, group=group)
         tables.expand()
         # selection + mine()'s output order on the device; the sorted pattern
         # table is read back to the host (the step's result)

@@ -640,9 +640,12 @@ extern "C" int paste_mine_expand_slice(const paste_mine_desc* d, const uint32_t*
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t n_win = g.n_bins / g.base;
+  // one warp per window: the per-window work is a short dependent chain
+  // (block counts -> contexts -> atomics), so latency hiding wants every
+  // window in flight at once
   const int64_t want = (n_win + XT / 32 - 1) / (XT / 32);
-  const int64_t cap = (int64_t)sms * 4;
-  const unsigned grid = (unsigned)(want < cap ? (want > 0 ? want : 1) : cap);
+  const unsigned grid = (unsigned)(want > 0 ? want : 1);
+  (void)sms;
   int rc = -1;
 #define PASTE_EXPAND_SLICE(KV)                                                               \
   if (d->k == KV) {                                                                          \

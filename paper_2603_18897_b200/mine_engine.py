@@ -834,12 +834,15 @@ def order_columnar(raw: dict, n_sessions: int, inactivity_ms: float = 300_000.0,
 
 
 def mine_columnar(trace: dict, sigs: SigTable, cfg: MiningConfig,
-                  inactivity_ms: float = 300_000.0, group=None) -> list[PatternTuple]:
+                  inactivity_ms: float = 300_000.0, group=None,
+                  tail: str = "allreduce") -> list[PatternTuple]:
     """mine() over a columnar trace shard on this device.  With a
     torch.distributed ``group`` every rank counts its shard (whole sessions)
     and the (k+1)-gram histograms are summed with one NCCL all-reduce before
     expansion -- windows and matches never cross a session, so the merged
-    histogram equals the single-device one."""
+    histogram equals the single-device one.  ``tail="sliced"`` runs the
+    target-sliced tail instead (sharded_tail: reduce-scatter + per-block
+    expansion and selection)."""
     relation = 0 if cfg.match_relation is MatchRelation.ANCHORED_SUBSEQUENCE else 1
     tables = MineTables.allocate(max(sigs.n_sigs, 2), cfg.k, relation)
     counters = ingest_count(tables, trace, inactivity_ms)
@@ -851,10 +854,12 @@ def mine_columnar(trace: dict, sigs: SigTable, cfg: MiningConfig,
         ordered = order_columnar(trace, n_sessions, inactivity_ms)
         tables.hist.zero_()
         counters = ingest_count(tables, ordered.columns, float("inf"))
-    if group is not None:  # whole-session shards: the sliced tail (sharded_tail)
+    if group is not None and tail == "sliced":  # target-sliced tail (sharded_tail)
         import torch.distributed as dist
 
         dist.all_reduce(counters, group=group)
         return sharded_tail(tables, group, cfg.sigma, cfg.tau).patterns(sigs)
+    if group is not None:
+        merge_shard_histograms(tables.hist, counters, group)
     tables.expand()
     return tables.select_sorted(cfg.sigma, cfg.tau).patterns(sigs)

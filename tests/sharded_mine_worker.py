@@ -59,8 +59,10 @@ def main(out_path):
     cut = int(bounds[len(bounds) // 3])  # a session boundary
     lo, hi = (0, cut) if rank == 0 else (cut, len(c["session"]))
     shard = {k: torch.from_numpy(np.ascontiguousarray(v[lo:hi])).cuda() for k, v in c.items()}
-    pats = mine_columnar(shard, SigTable(C4_TOOLS), MiningConfig(k=3, sigma=5, tau=0.3),
-                         group=dist.group.WORLD)
+    cfg = MiningConfig(k=3, sigma=5, tau=0.3)
+    pats = mine_columnar(shard, SigTable(C4_TOOLS), cfg, group=dist.group.WORLD)
+    sliced = mine_columnar(shard, SigTable(C4_TOOLS), cfg, group=dist.group.WORLD, tail="sliced")
+    assert sliced == pats, "sliced tail differs from the all-reduce tail"
     rows = [[[[s.tool_type, s.status.value] for s in p.context], p.target, p.p, p.support]
             for p in pats]
     gathered = [None, None]
