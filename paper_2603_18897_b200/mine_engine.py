@@ -753,18 +753,26 @@ def sharded_tail(tables: "MineTables", group, sigma: int, tau: float) -> "MinedT
           lib)
     dist.all_reduce(tables.match, group=group)
     mine = tables.select_sorted(sigma, tau)
-    parts = [None] * world
-    dist.all_gather_object(parts, mine.rows, group=group)
+    return merge_sorted_tables(mine.rows, tables.n_sigs, tables.k, group)
+
+
+def merge_sorted_tables(rows: np.ndarray, n_sigs: int, k: int, group) -> "MinedTable":
+    """All-gather every rank's sorted selection rows (tool, context, support,
+    match, follow, p bits) and merge them in mine()'s order (-p, -len,
+    target, context): the device sort key (hi = ~bits(p), lo = (k - len,
+    tool, context digits)) restated in numpy."""
+    import torch.distributed as dist
+
+    parts = [None] * dist.get_world_size(group)
+    dist.all_gather_object(parts, np.asarray(rows, np.int64), group=group)
     rows = np.concatenate([p for p in parts if len(p)] or [np.zeros((0, 6), np.int64)])
     if len(rows):
-        S, k = tables.n_sigs, tables.k
-        off = np.array(ctx_offsets(S, k), np.int64)
+        off = np.array(ctx_offsets(n_sigs, k), np.int64)
         length = np.searchsorted(off[1:], rows[:, 1], side="right")
         local = rows[:, 1] - off[length]
         p = rows[:, 5].view(np.float64)
-        # the device sort key (hi = ~bits(p), lo = (k - len, tool, digits)) in numpy
         rows = rows[np.lexsort((local, rows[:, 0], -length, -p))]
-    return MinedTable(np.ascontiguousarray(rows), tables.n_sigs, tables.k)
+    return MinedTable(np.ascontiguousarray(rows), n_sigs, k)
 
 
 def merge_shard_histograms(hist, counters, group) -> None:

@@ -96,3 +96,55 @@ def test_gram_histogram_marginal_counts_every_anchor():
     anchors = gram_histogram(tok, S, k - 1)          # k-grams ending at each event
     w_keys = np.arange(base ** k)
     assert np.array_equal(marg, anchors[w_keys])
+
+
+def _merge_worker(rank, world, port, out_q):
+    """The sliced tail's row merge (mine_engine.merge_sorted_tables) over two
+    gloo ranks, each holding the sorted rows of its own tools."""
+    from paper_2603_18897_b200.mine_engine import merge_sorted_tables
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rows = _sorted_rows()
+    mine = rows[(rows[:, 0] % world) == rank]  # a rank's tools, still in order
+    merged = merge_sorted_tables(mine, 10, 3, dist.group.WORLD)
+    if rank == 0:
+        out_q.put(merged.rows)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _sorted_rows():
+    """Random selection rows in mine()'s order: (-p, -len, tool, context)."""
+    from paper_2603_18897_b200.mine_engine import ctx_offsets
+
+    rng = np.random.default_rng(3)
+    S, k = 10, 3
+    off = ctx_offsets(S, k)
+    n = 400
+    length = rng.integers(1, k + 1, n)
+    local = np.array([rng.integers(0, S ** int(L)) for L in length])
+    ctx = np.array(off)[length] + local
+    tool = rng.integers(0, S // 2, n)
+    p = rng.choice([0.25, 0.5, 0.75, 1.0, 1 / 3], n)
+    rows = np.stack([tool, ctx, rng.integers(5, 50, n), rng.integers(1, 9, n),
+                     rng.integers(1, 9, n), p.view(np.int64)], axis=1).astype(np.int64)
+    keep = np.unique(rows[:, :2], axis=0, return_index=True)[1]  # (tool, ctx) unique
+    rows = rows[np.sort(keep)]
+    L = np.searchsorted(np.array(off)[1:], rows[:, 1], side="right")
+    return rows[np.lexsort((rows[:, 1] - np.array(off)[L], rows[:, 0], -L,
+                            -rows[:, 5].view(np.float64)))]
+
+
+def test_sliced_tail_row_merge_two_gloo_ranks():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_merge_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    merged = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert np.array_equal(merged, _sorted_rows())
