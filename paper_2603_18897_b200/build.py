@@ -32,8 +32,36 @@ def nvcc() -> str:
     return "nvcc"
 
 
+PYEXT_SRC = os.path.join(CSRC, "tapes_py.cpp")  # CPython extension, built apart
+
+
 def sources() -> list[str]:
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
+    return sorted(f for f in glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp"))
+                  if f != PYEXT_SRC)
+
+
+def pyext_path() -> str:
+    import sysconfig
+
+    return os.path.join(HERE, "_tapes" + sysconfig.get_config_var("EXT_SUFFIX"))
+
+
+def build_pyext(force: bool = False) -> str:
+    """The native payload-tape encoder (csrc/tapes_py.cpp) as an in-tree
+    CPython extension module (host code: g++)."""
+    import sysconfig
+
+    out = pyext_path()
+    if not force and os.path.exists(out) and os.path.getmtime(out) > os.path.getmtime(PYEXT_SRC):
+        return out
+    cmd = [os.environ.get("CXX", "g++"), "-O3", "-std=c++17", "-shared", "-fPIC",
+           "-I", sysconfig.get_paths()["include"], PYEXT_SRC, "-o", out + ".tmp"]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        sys.stderr.write(proc.stdout + proc.stderr)
+        raise RuntimeError("g++ failed building the tape encoder extension")
+    os.replace(out + ".tmp", out)
+    return out
 
 
 def needs_build() -> bool:
@@ -45,6 +73,7 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    build_pyext(force)
     if not force and not needs_build():
         return OUT
     # one nvcc per translation unit, in parallel, then one link

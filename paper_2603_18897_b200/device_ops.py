@@ -239,7 +239,7 @@ def candidate_paths_batch(payloads: Sequence[Any], targets: Sequence[Any], node_
     torch = _torch()
     lib = _native.lib()
     arena = TapeArena(keep_objects=False)
-    events = np.array([arena.add(p) for p in payloads] or [0], np.int32)
+    events = np.array(arena.add_many(payloads) or [0], np.int32)
     nodes, data, refs = arena.arrays()
     n = len(payloads)
     sizes = []

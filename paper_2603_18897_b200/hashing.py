@@ -45,8 +45,7 @@ def canonical_arg_hash_batch(values: Sequence[Any]) -> list[str]:
         return []
     keys = KeyTable()
     arena = TapeArena(keys, keep_objects=False)
-    for v in values:
-        arena.add(v)
+    arena.add_many(values)
     nodes, data, refs = arena.arrays()
     kb, ko, kr = key_tables(keys)
     dev = {name: torch.from_numpy(np.ascontiguousarray(a)).cuda()

@@ -221,15 +221,18 @@ def pack_windows(windows: Sequence[Sequence[Event]], sigs: SigTable, keys: KeyTa
     count = np.zeros(n, np.int64)
     arena = TapeArena(keys)
     created: list[float | None] = []
+    payloads: list = []  # tape i = payloads[i], encoded in one batch below
     for s, events in enumerate(windows):
         last_tool = None
         for i, ev in enumerate(events):
             if ev.kind is EventKind.TOOL_CALL:
                 tok[s * W + i] = sigs.sig(ev.tool_type, ev.status)
-                evt[s * W + i] = arena.add(ev.result)
+                evt[s * W + i] = len(payloads)
+                payloads.append(ev.result)
                 last_tool = ev
         count[s] = len(events)
         created.append(last_tool.t_end if last_tool is not None else None)
+    arena.add_many(payloads)
     return WindowBatch(W, tok, evt, count, arena, created)
 
 

@@ -75,9 +75,10 @@ class CorpusTapes:
                     ) -> "CorpusTapes":
         keys = KeyTable()
         arena = TapeArena(keys, keep_objects=False)
-        for ev in flat:
-            arena.add(ev.result)
-            arena.add(ev.args)
+        payloads = [None] * (2 * len(flat))
+        payloads[0::2] = [ev.result for ev in flat]
+        payloads[1::2] = [ev.args for ev in flat]
+        arena.add_many(payloads)
         nodes, data, refs = arena.arrays()
         return cls(nodes, data, refs, keys, tok_host, tok_dev, sigs, flat)
 

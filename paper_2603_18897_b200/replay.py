@@ -108,6 +108,7 @@ def corpus_from_traces(traces, dp, window_capacity: int, ksets: KeysetTable):
     from .tape import TapeArena
 
     arena = TapeArena(dp.keys)
+    payloads: list = []  # tape i = payloads[i], encoded in one batch below
     ev_tok, ev_evt, calls, call_len, actual = [], [], [], [], []
     call_args, call_ks = [], []
     g = 0
@@ -120,15 +121,18 @@ def corpus_from_traces(traces, dp, window_capacity: int, ksets: KeysetTable):
                     calls.append(g)
                     call_len.append(min(window_capacity, g - start))
                     actual.append(ev)
-                    call_args.append(arena.add(ev.args))
+                    call_args.append(len(payloads))
+                    payloads.append(ev.args)
                     call_ks.append(ksets.of_args(ev.args))
                 seen_tool = True
                 ev_tok.append(dp.sigs.sig(ev.tool_type, ev.status))
-                ev_evt.append(arena.add(ev.result))
+                ev_evt.append(len(payloads))
+                payloads.append(ev.result)
             else:
                 ev_tok.append(-1)
                 ev_evt.append(-1)
             g += 1
+    arena.add_many(payloads)
     nodes, data, refs = arena.arrays()
     corpus = ReplayCorpus(
         np.array(ev_tok or [-1], np.int32), np.array(ev_evt or [-1], np.int32),

@@ -92,57 +92,93 @@ def scalar_bytes(value: Any) -> tuple[int, int, bytes]:
     raise TypeError(f"payload leaf of type {type(value).__name__} is not JSON-like")
 
 
+_NODE = struct.Struct("<BBHiII")
+try:  # the native encoder (csrc/tapes_py.cpp): exact JSON types, ~20x faster
+    from . import _tapes as _native_tapes
+except ImportError:  # pragma: no cover - built by build(); the Python path is exact
+    _native_tapes = None
+
+
 class TapeArena:
     """Append-only arena of payload tapes (one tape per event payload).
 
     ``keep_objects`` keeps the Python object of every node so that values the
     device resolves can be handed back by identity (the reference returns the
-    payload's own leaf object from ``_walk``)."""
+    payload's own leaf object from ``_walk``).  Nodes are kept packed
+    (NODE_DTYPE bytes); ``add_many`` encodes a batch natively."""
 
     def __init__(self, keys: KeyTable | None = None, keep_objects: bool = True) -> None:
         self.keys = KeyTable() if keys is None else keys
         self.keep_objects = keep_objects
-        self._nodes: list[tuple[int, int, int, int, int, int]] = []
+        self._nodes = bytearray()
         self._data = bytearray()
         self._refs: list[tuple[int, int]] = []
         self._objs: list[Any] = []
         self._frozen: tuple[np.ndarray, np.ndarray, np.ndarray] | None = None
 
+    @property
+    def n_nodes(self) -> int:
+        return len(self._nodes) // 16
+
     # -- building -----------------------------------------------------------
 
     def add(self, payload: Any) -> int:
         """Encode one payload; returns its event-tape index."""
-        node_base = len(self._nodes)
+        node_base = self.n_nodes
         byte_base = len(self._data)
         self._emit(payload, -1, node_base, byte_base)
         self._refs.append((node_base, byte_base))
         self._frozen = None
         return len(self._refs) - 1
 
+    def add_many(self, payloads) -> list[int]:
+        """Encode a batch of payloads (native encoder for the exact JSON
+        types; any payload it does not take goes through ``add``)."""
+        payloads = list(payloads)
+        if _native_tapes is None:
+            return [self.add(p) for p in payloads]
+        first = len(self._refs)
+        i = 0
+        while i < len(payloads):
+            nodes, data, refs = _native_tapes.encode(
+                payloads[i:] if i else payloads, self.keys.ids, self.keys.names, self.n_nodes,
+                len(self._data), self._objs if self.keep_objects else None)
+            self._nodes += nodes
+            self._data += data
+            self._refs.extend(refs)
+            i += len(refs)
+            if i < len(payloads):  # outside the native subset: the exact Python encoder
+                self.add(payloads[i])
+                i += 1
+        self._frozen = None
+        return list(range(first, len(self._refs)))
+
     def _emit(self, value: Any, key: int, node_base: int, byte_base: int) -> None:
-        idx = len(self._nodes)
+        idx = self.n_nodes
         if isinstance(value, dict):
-            self._nodes.append((T_DICT, 0, 0, key, len(value), 0))
+            self._nodes += _NODE.pack(T_DICT, 0, 0, key, len(value), 0)
             if self.keep_objects:
                 self._objs.append(value)
             for k, v in value.items():
                 if not isinstance(k, str):
                     raise TypeError("payload dict keys must be strings (JSON objects)")
                 self._emit(v, self.keys.intern(k), node_base, byte_base)
-            self._nodes[idx] = (T_DICT, 0, 0, key, len(value), len(self._nodes) - idx)
+            _NODE.pack_into(self._nodes, 16 * idx, T_DICT, 0, 0, key, len(value),
+                            self.n_nodes - idx)
         elif isinstance(value, list):
-            self._nodes.append((T_LIST, 0, 0, key, len(value), 0))
+            self._nodes += _NODE.pack(T_LIST, 0, 0, key, len(value), 0)
             if self.keep_objects:
                 self._objs.append(value)
             for v in value:
                 self._emit(v, -1, node_base, byte_base)
-            self._nodes[idx] = (T_LIST, 0, 0, key, len(value), len(self._nodes) - idx)
+            _NODE.pack_into(self._nodes, 16 * idx, T_LIST, 0, 0, key, len(value),
+                            self.n_nodes - idx)
         else:
             typ, flags, data = scalar_bytes(value)
             off = len(self._data) - byte_base
             self._data += data
             nbytes = len(data) if not flags & F_NFC else len(value.encode("utf-8", "surrogatepass"))
-            self._nodes.append((typ, flags, 0, key, off, nbytes))
+            self._nodes += _NODE.pack(typ, flags, 0, key, off, nbytes)
             if self.keep_objects:
                 self._objs.append(value)
 
@@ -151,7 +187,7 @@ class TapeArena:
     def arrays(self) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
         """(nodes[N] NODE_DTYPE, data u8[B], refs i64[E,2] = (node_base, byte_base))."""
         if self._frozen is None:
-            nodes = np.array(self._nodes, dtype=NODE_DTYPE) if self._nodes \
+            nodes = np.frombuffer(bytes(self._nodes), dtype=NODE_DTYPE).copy() if self._nodes \
                 else np.zeros(1, NODE_DTYPE)
             data = np.frombuffer(bytes(self._data) or b"\0", dtype=np.uint8).copy()
             refs = np.array(self._refs, dtype=np.int64).reshape(-1, 2)
@@ -171,7 +207,7 @@ class TapeArena:
         return decode_node(nodes, data, int(refs[event, 0]), int(refs[event, 1]), node, self.keys)
 
     def node_type(self, event: int, node: int) -> int:
-        return self._nodes[self._refs[event][0] + node][0]
+        return self._nodes[16 * (self._refs[event][0] + node)]
 
     def path_of(self, event: int, node: int) -> tuple:
         nodes, _, refs = self.arrays()
