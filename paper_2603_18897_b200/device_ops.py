@@ -27,6 +27,32 @@ def _torch():
     return torch
 
 
+def to_dev_many(arrays: dict) -> dict:
+    """Several small numpy arrays -> CUDA tensors in ONE host-to-device copy:
+    packed at 16-byte aligned offsets of one buffer; every result is a view
+    of it with the array's dtype (structured arrays as uint8 bytes)."""
+    torch = _torch()
+    parts, off = [], 0
+    for k, arr in arrays.items():
+        a = np.ascontiguousarray(arr)
+        raw = a.view(np.uint8).reshape(-1) if a.size else np.zeros(0, np.uint8)
+        parts.append((k, a, off, raw.nbytes))
+        off = (off + raw.nbytes + 15) & ~15
+    host = np.zeros(max(off, 16), np.uint8)
+    for k, a, o, nb in parts:
+        if nb:
+            host[o:o + nb] = a.view(np.uint8).reshape(-1)
+    dev = torch.from_numpy(host).to("cuda", non_blocking=False)
+    out = {}
+    for k, a, o, nb in parts:
+        view = dev[o:o + nb]
+        if a.dtype.names is not None or a.dtype == np.uint8:
+            out[k] = view
+        else:
+            out[k] = view.view(getattr(torch, a.dtype.name))
+    return out
+
+
 def to_dev(arr: np.ndarray):
     """numpy (incl. structured) -> contiguous CUDA tensor with the same bytes."""
     torch = _torch()

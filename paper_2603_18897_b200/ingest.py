@@ -114,6 +114,25 @@ class RawTrace:
     keys: Any = None                 # KeyTable of the tapes
 
 
+_as_utf8 = ctypes.pythonapi.PyUnicode_AsUTF8AndSize
+_as_utf8.restype = ctypes.c_void_p
+_as_utf8.argtypes = [ctypes.py_object, ctypes.POINTER(ctypes.c_ssize_t)]
+
+
+def _utf8_view(text: str):
+    """The UTF-8 bytes of `text` without a copy when CPython can lend them (an
+    ASCII str's own buffer; otherwise its cached UTF-8 form), else encoded."""
+    n = ctypes.c_ssize_t()
+    try:
+        p = _as_utf8(text, ctypes.byref(n))
+    except UnicodeEncodeError:  # lone surrogates: the reference's text never has them
+        p = None
+    if not p:
+        raw = text.encode("utf-8", "surrogatepass")
+        return raw, len(raw)
+    return ctypes.cast(p, ctypes.c_char_p), n.value
+
+
 def parse_jsonl_raw(source: str | bytes, payloads: bool = True) -> RawTrace | None:
     """Native parallel parse (paste_jsonl_parse) of a JSONL trace; None when
     the input is outside the parser's exact subset (use the host ingest)."""
@@ -121,10 +140,10 @@ def parse_jsonl_raw(source: str | bytes, payloads: bool = True) -> RawTrace | No
     from .tape import NODE_DTYPE, KeyTable
 
     text = source.decode("utf-8") if isinstance(source, bytes) else source
-    raw = text.encode("utf-8", "surrogatepass")
+    raw, n_raw = _utf8_view(text)
     lib = _native.load_library()
     h = ctypes.c_void_p()
-    rc = lib.paste_jsonl_parse(raw, len(raw), 1 if payloads else 0, ctypes.byref(h))
+    rc = lib.paste_jsonl_parse(raw, n_raw, 1 if payloads else 0, ctypes.byref(h))
     if rc == PASTE_ERR_UNSUPPORTED:
         return None
     check(rc, lib)

@@ -135,7 +135,7 @@ class CorpusOccurrences:
 
     def __init__(self, ct: CorpusTapes, anchors: np.ndarray, picked: np.ndarray,
                  target_tool: str):
-        from .device_ops import to_dev
+        from .device_ops import to_dev_many
 
         self.ct = ct
         self.anchors = np.asarray(anchors, np.int64)
@@ -143,11 +143,11 @@ class CorpusOccurrences:
         self.M, self.n_ctx = self.picked.shape
         self.target_tool = target_tool
         self.act_tape = ct.args_tape[self.anchors + 1].astype(np.int32)
-        self.dev = {k: to_dev(v) for k, v in dict(
+        self.dev = to_dev_many(dict(
             occ_event=ct.res_tape[self.picked].reshape(-1).astype(np.int32),
             src_pos=(self.picked - self.picked[:, :1]).reshape(-1).astype(np.int32),
             hist_off=self.picked[:, 0].astype(np.int32),
-            hist_end=(self.anchors + 1).astype(np.int32), act_tape=self.act_tape).items()}
+            hist_end=(self.anchors + 1).astype(np.int32), act_tape=self.act_tape))
         self._objs: dict[int, tuple] = {}
         self._act: dict[str, tuple] = {}
 
@@ -193,7 +193,7 @@ class CorpusOccurrences:
 
     def holds(self, exprs: Sequence, name: str, want_eq: bool = False):
         """(hits[H], unsure[H], eq[H, M] or None) of hypotheses over every occurrence."""
-        from .device_ops import stream_handle, to_dev
+        from .device_ops import stream_handle, to_dev_many
 
         torch = _torch()
         lib = _native.lib()
@@ -211,10 +211,10 @@ class CorpusOccurrences:
             else:
                 fmt += [0, 0, 0, 0, 0]
         node, _ = self.actual(name)
-        d = {k: to_dev(v) for k, v in dict(
+        d = to_dev_many(dict(
             hyp=np.array(rows, dtype=BINDING_DTYPE), steps=np.array(steps or [0, 0], np.int32),
             fmt=np.array(fmt, np.int32),
-            fbytes=np.frombuffer(bytes(fbytes) + b"\0", np.uint8)).items()}
+            fbytes=np.frombuffer(bytes(fbytes) + b"\0", np.uint8)))
         hits = torch.zeros(H, dtype=torch.int64, device="cuda")
         unsure = torch.zeros(H, dtype=torch.int64, device="cuda")
         eq = torch.zeros(H * self.M, dtype=torch.uint8, device="cuda") if want_eq else None
