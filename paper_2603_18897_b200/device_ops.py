@@ -43,7 +43,7 @@ def to_dev_many(arrays: dict) -> dict:
         if nb:
             host[o:o + nb] = a.view(np.uint8).reshape(-1)
     dev = torch.from_numpy(host).to("cuda", non_blocking=False)
-    out = {}
+    out = {"__buf__": dev, "__span__": {k: (o, nb) for k, _a, o, nb in parts}}
     for k, a, o, nb in parts:
         view = dev[o:o + nb]
         if a.dtype.names is not None or a.dtype == np.uint8:
@@ -279,19 +279,28 @@ def candidate_paths_batch(payloads: Sequence[Any], targets: Sequence[Any], node_
     target_off = np.zeros(n + 1, np.int64)
     target_off[1:] = np.cumsum([len(b) for b in tb])
     tbytes = np.frombuffer(b"".join(tb) + b"\0", np.uint8)
-    d = {k: to_dev(v) for k, v in dict(
+    d = to_dev_many(dict(
         nodes=nodes, data=data, refs=refs, events=events,
         tt=np.array(list(tt) or [0], np.int32), tn=np.array(list(tn) or [0], np.uint8),
-        toff=target_off, tbytes=tbytes, out_off=out_off).items()}
-    dev = torch.device("cuda")
-    out_nodes = torch.zeros(max(int(out_off[-1]), 1), dtype=torch.int32, device=dev)
-    n_out = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
-    trunc = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)
+        toff=target_off, tbytes=tbytes, out_off=out_off,
+        out_nodes=np.zeros(max(int(out_off[-1]), 1), np.int32),
+        n_out=np.zeros(max(n, 1), np.int64), trunc=np.zeros(max(n, 1), np.uint8)))
+    out_nodes, n_out, trunc = d["out_nodes"], d["n_out"], d["trunc"]
     desc = LeafScanDesc(n, int(node_budget), ptr(d["nodes"]), ptr(d["data"]), ptr(d["refs"]),
                         ptr(d["events"]), ptr(d["tt"]), ptr(d["tn"]), ptr(d["toff"]),
                         ptr(d["tbytes"]), ptr(d["out_off"]), ptr(out_nodes), ptr(n_out), ptr(trunc))
     check(lib.paste_leaf_scan(ctypes.byref(desc), stream_handle()), lib)
-    out_nodes, n_out, trunc = out_nodes.cpu().numpy(), n_out.cpu().numpy(), trunc.cpu().numpy()
+    # the three results are the tail of the packed buffer: one device-to-host copy
+    span = d["__span__"]
+    lo = span["out_nodes"][0]
+    hi = span["trunc"][0] + span["trunc"][1]
+    back = d["__buf__"][lo:hi].cpu().numpy()
+    o, nb = span["out_nodes"]
+    out_nodes = back[o - lo:o - lo + nb].view(np.int32)
+    o, nb = span["n_out"]
+    n_out = back[o - lo:o - lo + nb].view(np.int64)
+    o, nb = span["trunc"]
+    trunc = back[o - lo:o - lo + nb]
     res = []
     for q in range(n):
         found = out_nodes[out_off[q]:out_off[q] + min(int(n_out[q]), int(cap[q]))]
