@@ -804,16 +804,18 @@ extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_pay
   }
   auto* h = new paste_jsonl();
   h->n_lines = n_lines;
+  // rows in file order: the ids need one sequential pass (first appearance),
+  // everything else is filled in parallel afterwards
   std::unordered_map<HashedView, int32_t, HashedViewHash> sid, tool_id;
   sid.reserve((size_t)n_lines / 8 + 16);
-  for (auto* v : {&h->session, &h->seq, &h->sig}) v->reserve((size_t)n_lines);
-  h->t_start.reserve((size_t)n_lines);
-  h->t_end.reserve((size_t)n_lines);
   std::vector<std::string_view> tools;
-  HashedView last_hv{};
-  int32_t last_sid = -1;
+  HashedView last_hv{}, last_tv{};
+  int32_t last_sid = -1, last_tid = -1;
   std::vector<int64_t> row_line;  // line of every valid row
+  std::vector<int32_t> row_sid, row_tid;
   row_line.reserve((size_t)n_lines);
+  row_sid.reserve((size_t)n_lines);
+  row_tid.reserve((size_t)n_lines);
   for (int64_t i = 0; i < n_lines; ++i) {
     const Rec& r = recs[i];
     if (r.kind == L_EMPTY) continue;
@@ -830,22 +832,41 @@ extern "C" int paste_jsonl_parse(const char* text, int64_t len, int32_t want_pay
       last_hv = hv;
       last_sid = it->second;
     }
-    h->session.push_back(last_sid);
-    h->seq.push_back((int32_t)r.seq);
-    h->t_start.push_back(r.t_start);
-    h->t_end.push_back(r.t_end);
     int32_t tid = -1;
     if (r.tool_call) {
       const HashedView tv{r.tool, r.tool_hash};
-      auto t = tool_id.find(tv);
-      if (t == tool_id.end()) {
-        t = tool_id.emplace(tv, (int32_t)tools.size()).first;
-        tools.push_back(r.tool);
+      if (!(last_tid >= 0 && tv == last_tv)) {
+        auto t = tool_id.find(tv);
+        if (t == tool_id.end()) {
+          t = tool_id.emplace(tv, (int32_t)tools.size()).first;
+          tools.push_back(r.tool);
+        }
+        last_tv = tv;
+        last_tid = t->second;
       }
-      tid = t->second;
+      tid = last_tid;
     }
-    h->sig.push_back(tid < 0 ? -1 : (tid << 1) | (r.success ? 1 : 0));  // tool rank applied below
     row_line.push_back(i);
+    row_sid.push_back(last_sid);
+    row_tid.push_back(tid);
+  }
+  {
+    const int64_t nr = (int64_t)row_line.size();
+    h->session.resize((size_t)nr);
+    h->seq.resize((size_t)nr);
+    h->sig.resize((size_t)nr);
+    h->t_start.resize((size_t)nr);
+    h->t_end.resize((size_t)nr);
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < nr; ++q) {
+      const Rec& r = recs[row_line[q]];
+      h->session[q] = row_sid[q];
+      h->seq[q] = (int32_t)r.seq;
+      h->t_start[q] = r.t_start;
+      h->t_end[q] = r.t_end;
+      const int32_t tid = row_tid[q];
+      h->sig[q] = tid < 0 ? -1 : (tid << 1) | (r.success ? 1 : 0);  // tool rank applied below
+    }
   }
   const int64_t n_rows = (int64_t)row_line.size();
   lap("rows");
