@@ -180,17 +180,24 @@ struct LiveParams {
 template <int G>
 struct Sess {
   int64_t s;
-  int64_t rbase, rstride;
   int32_t ev0;             // the observed event
   int64_t node0;           // its node base
   int newest;              // ring slot of the observed event, -1 = it is not a tool event
-  uint64_t slots;          // ring slot of the tool event of age a at bits 4a
+  uint32_t slots;          // ring slot (< 16) of the tool event of age a at bits 4a
   int32_t tk[G];           // newest tool tokens by age
   int m;
   const uint8_t* e;        // plan entry (nullptr = no predictions)
   int32_t key;             // match-table key, -1 = none
   int nm, n_act, n_map, n_err;
 };
+
+// ring addressing of session s (derived, not kept per session: registers)
+__device__ __forceinline__ int64_t ring_base(const LiveParams& P, int64_t s) {
+  return P.win.slot_major ? s : s * P.win.capacity;
+}
+__device__ __forceinline__ int64_t ring_stride(const LiveParams& P) {
+  return P.win.slot_major ? P.win.n_sessions : 1;
+}
 
 // newest G tool tokens: the G-1 older ring slots in one batch of loads; an
 // LLM step (-1) among them falls back to the slot-by-slot scan
@@ -202,12 +209,12 @@ __device__ __forceinline__ void gather_slow(const LiveParams& P, Sess<G>& x, int
   x.slots = 0;
   int slot = head;
   for (int i = 0; i < len && x.m < G; ++i) {
-    const int32_t t = i == 0 ? t_new : P.win.tok[x.rbase + slot * x.rstride];
+    const int32_t t = i == 0 ? t_new : P.win.tok[ring_base(P, x.s) + slot * ring_stride(P)];
     if (t >= 0) {
 #pragma unroll
       for (int q = 0; q < G; ++q)
         if (q == x.m) x.tk[q] = t;
-      x.slots |= (uint64_t)slot << (4 * x.m);
+      x.slots |= (uint32_t)slot << (4 * x.m);
       ++x.m;
     }
     slot = slot == 0 ? W - 1 : slot - 1;
@@ -263,9 +270,7 @@ __device__ __forceinline__ void front_observe(const LiveParams& P, const FrontIn
   y.key = -1;
   y.nm = y.n_act = y.n_map = y.n_err = 0;
   if (f.s >= n) return;
-  const bool slot_major = P.win.slot_major != 0;
-  y.rbase = slot_major ? f.s : f.s * W;
-  y.rstride = slot_major ? n : 1;
+  const int64_t rbase = ring_base(P, f.s), rstride = ring_stride(P);
   const int32_t t_in = (P.win.new_tok8 != nullptr && f.t == 255) ? -1 : f.t;
   const int head = (W & (W - 1)) == 0 ? (int)(f.cnt & (W - 1))
                    : f.cnt < (1ll << 31) ? (int)((uint32_t)f.cnt % (uint32_t)W)
@@ -275,8 +280,8 @@ __device__ __forceinline__ void front_observe(const LiveParams& P, const FrontIn
   y.node0 = narrow ? (int64_t)f.node : f.ref.node_base;
   P.win.refs[y.ev0] =
       paste_event_ref{y.node0, (narrow ? 0 : f.ref.byte_base) + P.win.new_byte_base};
-  P.win.tok[y.rbase + head * y.rstride] = t_in;
-  P.win.evt[y.rbase + head * y.rstride] = y.ev0;
+  P.win.tok[rbase + head * rstride] = t_in;
+  P.win.evt[rbase + head * rstride] = y.ev0;
   const int64_t c1 = f.cnt + 1;
   P.win.count[f.s] = c1;
   y.newest = head;
@@ -285,7 +290,7 @@ __device__ __forceinline__ void front_observe(const LiveParams& P, const FrontIn
 #pragma unroll
   for (int a = 1; a < G; ++a) {
     m.ot[a - 1] = -1;
-    if (a < m.len) m.ot[a - 1] = P.win.tok[y.rbase + wrap_sub(head, a, W) * y.rstride];
+    if (a < m.len) m.ot[a - 1] = P.win.tok[rbase + wrap_sub(head, a, W) * rstride];
   }
 }
 
@@ -296,14 +301,14 @@ __device__ __forceinline__ void front_key(const LiveParams& P, Sess<G>& y, const
   const int W = P.win.capacity;
   bool fast = m.t_new >= 0;
   y.tk[0] = m.t_new;
-  y.slots = (uint64_t)y.newest;
+  y.slots = (uint32_t)y.newest;
   y.m = 1;
 #pragma unroll
   for (int a = 1; a < G; ++a) {
     if (a < m.len) {
       fast = fast && m.ot[a - 1] >= 0;
       y.tk[a] = m.ot[a - 1];
-      y.slots |= (uint64_t)wrap_sub(y.newest, a, W) << (4 * a);
+      y.slots |= (uint32_t)wrap_sub(y.newest, a, W) << (4 * a);
       y.m = a + 1;
     }
   }
@@ -326,7 +331,6 @@ __device__ __forceinline__ void front_key(const LiveParams& P, Sess<G>& y, const
     y.n_act = (h.x >> 8) & 0xff;
     y.n_map = (h.x >> 16) & 0xff;
     y.n_err = h.y;
-    if (COMPACT) y.slots |= (uint64_t)key << 48;  // ENTRY16 key rides along (<= 0xfffe)
   }
 }
 
@@ -359,7 +363,7 @@ __device__ __forceinline__ uint32_t live_resolve(const LiveParams& P, const Sess
       ev = y.ev0;
       nb = y.node0;
     } else {
-      ev = P.win.evt[y.rbase + slot * y.rstride];
+      ev = P.win.evt[ring_base(P, y.s) + slot * ring_stride(P)];
       nb = P.win.refs[ev].node_base;
     }
     int64_t cur = -2;
@@ -549,7 +553,7 @@ __device__ __forceinline__ void kslot_write8(const LiveParams& P, const Sess<G>&
 // rounds: round r+2's inputs and round r+1's older ring slots are in flight
 // while round r is keyed and written, so the count -> ring -> plan chain
 // costs one memory round trip per round instead of three.
-template <int G, int MINB = 6>
+template <int G, int MINB = 7>
 __global__ void __launch_bounds__(LT, MINB) predict_live_kernel(const LiveParams P) {
   const int64_t n = P.win.n_sessions;
   const int64_t stride = (int64_t)gridDim.x * LT;
@@ -664,7 +668,7 @@ __device__ __forceinline__ void compact_write(const LiveParams& P, const Sess<G>
     });
   }
   if (C.format & PASTE_CF_ENTRY16) {
-    static_cast<uint16_t*>(C.pred)[y.s] = y.e ? (uint16_t)(y.slots >> 48) : (uint16_t)0xffffu;
+    static_cast<uint16_t*>(C.pred)[y.s] = y.e ? (uint16_t)y.key : (uint16_t)0xffffu;
   } else if (y.nm > 0) {
     const int32_t* pid = reinterpret_cast<const int32_t*>(y.e + P.L.off_pid);
     const uint8_t* comp = y.e + P.L.off_comp;
@@ -952,15 +956,15 @@ static bool live_ticket() {
 }
 
 // min resident CTAs per SM of the K-slot live kernel, i.e. its register
-// cap: 6 -> 80 registers and no spills, the default (measured: 57.9 us per
-// 1M sessions vs 69.4 us at 8 -> 64 registers with spills, 64.4 us at 4 ->
-// 106 registers, 77.2 us at 10 -> 48, 87.4 us at 12 -> 40); PASTE_LIVE_MINB =
-// 4 / 5 / 7 / 8 selects another build
+// cap: 7 -> 72 registers and no spills, the default (per 1M-session step:
+// 56 us; 6 -> 80 registers 58 us; 8 -> 64 registers with spills 59 us; 4 ->
+// 96 registers 64 us; 10 / 12 -> 48 / 40 registers 77 / 87 us);
+// PASTE_LIVE_MINB = 4 / 5 / 6 / 8 selects another build
 static int live_minb() {
   static int m = -1;
   if (m < 0) {
     const char* e = getenv("PASTE_LIVE_MINB");
-    m = e ? atoi(e) : 6;
+    m = e ? atoi(e) : 7;
   }
   return m;
 }
@@ -975,7 +979,7 @@ static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int minb = live_minb();
-  const int which = !compact ? (minb == 7 ? 4 : minb == 5 ? 3 : minb == 8 ? 5 : minb == 4 ? 6 : 0)
+  const int which = !compact ? (minb == 6 ? 4 : minb == 5 ? 3 : minb == 8 ? 5 : minb == 4 ? 6 : 0)
                              : live_mode() == 1 ? 1 : 2;
   int& o = occ[which];
   if (o == 0) {
@@ -984,7 +988,7 @@ static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
     else if (which == 3)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 5>, LT, 0);
     else if (which == 4)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 7>, LT, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 6>, LT, 0);
     else if (which == 5)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 8>, LT, 0);
     else if (which == 6)
@@ -1003,7 +1007,7 @@ static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
   else if (which == 3)
     predict_live_kernel<G, 5><<<(unsigned)grid, LT, 0, st>>>(P);
   else if (which == 4)
-    predict_live_kernel<G, 7><<<(unsigned)grid, LT, 0, st>>>(P);
+    predict_live_kernel<G, 6><<<(unsigned)grid, LT, 0, st>>>(P);
   else if (which == 5)
     predict_live_kernel<G, 8><<<(unsigned)grid, LT, 0, st>>>(P);
   else if (which == 6)
