@@ -364,6 +364,14 @@ def test_device_occurrences_equal_host_rescan(rel, k):
     cands = [(decode_context(r[1], S, cfg.k), r[0], r[4]) for r in rows]
     flat = [e for st in streams for e in st]
     got = device_occurrences(tok_dev, flat, sigs, cands, cfg)
+    # positions against the oracle restatement (oracle/occurrences.py)
+    from oracle.occurrences import occurrences as oracle_occurrences
+    from paper_2603_18897_b200.mine_engine import occurrence_positions
+    tok_host = tok_dev.cpu().numpy()
+    for (cs, tool, f), (anc, pk) in zip(cands, occurrence_positions(tok_dev, sigs, cands, cfg)):
+        exp = oracle_occurrences(tok_host, cs, tool, cfg.k,
+                                 rel is MatchRelation.CONTIGUOUS_SUFFIX)
+        assert [(int(a), tuple(int(x) for x in p)) for a, p in zip(anc, pk)] == exp
     sig_streams = [[signature_of(e) for e in st] for st in streams]
     for (cs, tool, f), occ in zip(cands, got):
         ctx = tuple(sigs.signature(x) for x in cs)
