@@ -578,39 +578,6 @@ __global__ void __launch_bounds__(LT, MINB) predict_live_kernel(const LiveParams
   }
 }
 
-// One round deeper: round r+1's key and plan-entry header are issued while
-// round r's records are written, so the header load (L2) is off the chain
-// count -> ring -> key -> header -> records of the round being written.
-template <int G, int MINB = 6>
-__global__ void __launch_bounds__(LT, MINB) predict_live_deep_kernel(const LiveParams P) {
-  const int64_t n = P.win.n_sessions;
-  const int64_t stride = (int64_t)gridDim.x * LT;
-  const int64_t s0 = (int64_t)blockIdx.x * LT + threadIdx.x;
-  FrontIn f1, f2;
-  Sess<G> y0, y1, y2;
-  FrontMid<G> m1, m2;
-  front_load(P, s0, f1);
-  front_load(P, s0 + stride, f2);
-  front_observe<G>(P, f1, y1, m1);
-  front_key<G, false>(P, y1, m1);
-  f1 = f2;
-  front_load(P, s0 + 2 * stride, f2);
-  front_observe<G>(P, f1, y2, m2);
-  for (int64_t s = s0; s < n; s += stride) {
-    y0 = y1;
-    y1 = y2;
-    m1 = m2;
-    f1 = f2;
-    front_load(P, s + 3 * stride, f2);
-    front_observe<G>(P, f1, y2, m2);
-    front_key<G, false>(P, y1, m1);
-    if (P.fast8 && __activemask() == 0xffffffffu)
-      kslot_write8<G>(P, y0);
-    else
-      kslot_write<G>(P, y0);
-  }
-}
-
 // block-wide exclusive offsets of the 4 stream counters in session order
 // (j-major within the tile), with a decoupled look-back across tiles
 template <int SPT>
@@ -991,14 +958,10 @@ static bool live_ticket() {
 // min resident CTAs per SM of the K-slot live kernel, i.e. its register
 // cap: 7 -> 72 registers and no spills, the default (per 1M-session step:
 // 56 us; 6 -> 80 registers 58 us; 8 -> 64 registers with spills 59 us; 4 ->
-// 96 registers 64 us; 10 / 12 -> 48 / 40 registers 77 / 87 us);
+// 96 registers 64 us; 10 / 12 -> 48 / 40 registers 77 / 87 us; a pipeline
+// one round deeper -- the next round's plan header loaded while this round
+// writes -- ran at 60 us with 96 registers and 74 us with spills at 80);
 // PASTE_LIVE_MINB = 4 / 5 / 6 / 8 selects another build
-static bool live_deep() {  // PASTE_LIVE_DEEP=1: the one-round-deeper pipeline
-  static int d = -1;
-  if (d < 0) d = getenv("PASTE_LIVE_DEEP") != nullptr && atoi(getenv("PASTE_LIVE_DEEP")) == 1;
-  return d == 1;
-}
-
 static int live_minb() {
   static int m = -1;
   if (m < 0) {
@@ -1011,16 +974,14 @@ static int live_minb() {
 template <int G, int SPT>
 static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
   static int sms = 0;
-  static int occ[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  static int occ[7] = {0, 0, 0, 0, 0, 0, 0};
   if (sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int minb = live_minb();
-  const int which = !compact ? (live_deep() ? (minb == 5 ? 8 : 7)
-                                            : minb == 6 ? 4 : minb == 5 ? 3 : minb == 8 ? 5
-                                            : minb == 4 ? 6 : 0)
+  const int which = !compact ? (minb == 6 ? 4 : minb == 5 ? 3 : minb == 8 ? 5 : minb == 4 ? 6 : 0)
                              : live_mode() == 1 ? 1 : 2;
   int& o = occ[which];
   if (o == 0) {
@@ -1034,10 +995,7 @@ static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 8>, LT, 0);
     else if (which == 6)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_kernel<G, 4>, LT, 0);
-    else if (which == 7)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_deep_kernel<G, 6>, LT, 0);
-    else if (which == 8)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_deep_kernel<G, 5>, LT, 0);
+
     else if (which == 1)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, predict_live_compact_kernel<G, SPT>, LT, 0);
     else
@@ -1057,10 +1015,7 @@ static void launch_live(const LiveParams& P, bool compact, cudaStream_t st) {
     predict_live_kernel<G, 8><<<(unsigned)grid, LT, 0, st>>>(P);
   else if (which == 6)
     predict_live_kernel<G, 4><<<(unsigned)grid, LT, 0, st>>>(P);
-  else if (which == 7)
-    predict_live_deep_kernel<G, 6><<<(unsigned)grid, LT, 0, st>>>(P);
-  else if (which == 8)
-    predict_live_deep_kernel<G, 5><<<(unsigned)grid, LT, 0, st>>>(P);
+
   else if (which == 1)
     predict_live_compact_kernel<G, SPT><<<(unsigned)grid, LT, 0, st>>>(P);
   else
