@@ -134,18 +134,21 @@ __device__ __forceinline__ uint32_t ld_part(const uint8_t* p, int r) {  // r in 
   return r >= 4 ? v : (v & ((1u << (8 * r)) - 1u));
 }
 
+// r in 1..8 bytes at p, from aligned 8-byte words that each hold a byte of
+// the range (device allocations are at least 8-byte granular)
+__device__ __forceinline__ uint64_t ld_part8(const uint8_t* p, int r) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(a & ~uintptr_t(7));
+  const uint32_t o = (uint32_t)(a & 7);
+  uint64_t v = __ldg(w) >> (8 * o);
+  if (o + r > 8) v |= __ldg(w + 1) << (64 - 8 * o);  // o > 0 here
+  return r >= 8 ? v : (v & ((1ull << (8 * r)) - 1ull));
+}
+
 __device__ __forceinline__ bool bytes_eq(const uint8_t* a, const uint8_t* b, int64_t n) {
-  for (int64_t k = 0; k < n; k += 16) {
-    uint32_t diff = 0;
-#pragma unroll
-    for (int j = 0; j < 16; j += 4) {
-      const int64_t r = n - k - j;
-      if (r > 0) {
-        const int rr = r < 4 ? (int)r : 4;
-        diff |= ld_part(a + k + j, rr) ^ ld_part(b + k + j, rr);
-      }
-    }
-    if (diff) return false;
+  for (int64_t k = 0; k < n; k += 8) {
+    const int r = n - k < 8 ? (int)(n - k) : 8;
+    if (ld_part8(a + k, r) != ld_part8(b + k, r)) return false;
   }
   return true;
 }

@@ -21,26 +21,26 @@
 
 namespace paste {
 
-// a == lower(b) over n ASCII bytes (str.lower on ASCII text)
+__device__ __forceinline__ uint32_t lower4(uint32_t y) {  // ASCII A-Z -> a-z, bytewise
+  const uint32_t up = __vcmpgeu4(y, 0x41414141u) & __vcmpleu4(y, 0x5a5a5a5au);
+  return y + (up & 0x20202020u);
+}
+
+// a == lower(b) over n ASCII bytes (str.lower on ASCII text), 8 bytes a step
 __device__ __forceinline__ bool bytes_eq_lower(const uint8_t* a, const uint8_t* b, int64_t n) {
-  for (int64_t k = 0; k < n; k += 4) {
-    const int64_t r = n - k;
-    const int rr = r < 4 ? (int)r : 4;
-    uint32_t y = ld_part(b + k, rr);
-    const uint32_t up = __vcmpgeu4(y, 0x41414141u) & __vcmpleu4(y, 0x5a5a5a5au);
-    y += up & 0x20202020u;
-    if (ld_part(a + k, rr) != y) return false;
+  for (int64_t k = 0; k < n; k += 8) {
+    const int r = n - k < 8 ? (int)(n - k) : 8;
+    const uint64_t y = ld_part8(b + k, r);
+    const uint64_t ly = (uint64_t)lower4((uint32_t)y) | ((uint64_t)lower4((uint32_t)(y >> 32)) << 32);
+    if (ld_part8(a + k, r) != ly) return false;
   }
   return true;
 }
 
 __device__ __forceinline__ bool bytes_ascii(const uint8_t* a, int64_t n) {
-  uint32_t acc = 0;
-  for (int64_t k = 0; k < n; k += 4) {
-    const int64_t r = n - k;
-    acc |= ld_part(a + k, r < 4 ? (int)r : 4);
-  }
-  return (acc & 0x80808080u) == 0;
+  uint64_t acc = 0;
+  for (int64_t k = 0; k < n; k += 8) acc |= ld_part8(a + k, n - k < 8 ? (int)(n - k) : 8);
+  return (acc & 0x8080808080808080ull) == 0;
 }
 
 __device__ __forceinline__ bool node_ascii(const Node& nd, const uint8_t* b, int64_t n) {
