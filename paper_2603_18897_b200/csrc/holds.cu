@@ -103,8 +103,7 @@ __global__ void holds_kernel(const paste_holds_desc D) {
               len = (int64_t)x[0] | ((int64_t)x[1] << 8) | ((int64_t)x[2] << 16) | ((int64_t)x[3] << 24);
               b = x + 4;
             }
-            eq = len == al;
-            for (int64_t k = 0; eq && k < len; ++k) eq = b[k] == ab[k];
+            eq = len == al && bytes_eq(b, ab, len);
           }
         }
       } else if ((nt == PASTE_T_STR || nt == PASTE_T_INT || nt == PASTE_T_FLOAT) &&
