@@ -45,14 +45,11 @@ constexpr int LS_TW = 64;  // target words staged per warp (targets up to 256 by
 
 // candidate bytes == the staged (zero-padded) target words, 8 bytes per check
 __device__ __forceinline__ bool eq_target(const uint8_t* a, const uint32_t* tw, int len) {
+  // 8 bytes a step; the staged target words are zero past its end
   for (int k = 0; k < len; k += 8) {
-    const int r0 = len - k < 4 ? len - k : 4;
-    uint32_t d = ld_part(a + k, r0) ^ tw[k >> 2];
-    if (len - k > 4) {
-      const int r1 = len - k - 4 < 4 ? len - k - 4 : 4;
-      d |= ld_part(a + k + 4, r1) ^ tw[(k >> 2) + 1];
-    }
-    if (d) return false;
+    const int r = len - k < 8 ? len - k : 8;
+    const uint64_t t = (uint64_t)tw[k >> 2] | ((uint64_t)tw[(k >> 2) + 1] << 32);
+    if (ld_part8(a + k, r) != t) return false;
   }
   return true;
 }
