@@ -354,7 +354,7 @@ def run_ours(args):
                      "kernel_model_bytes_per_launch": model // S_,
                      "peak_source": f"{peak_kind} hbm_gbs",
                      "note": "SURVEY 8(d) 200 B/session; traffic = ncu dram bytes per launch "
-                             "(profiles/ncu_live_r2b.json): the narrow u8/u16 inputs and the "
+                             "(profiles/ncu_live_r2c.json): the narrow u8/u16 inputs and the "
                              "key-coded records move fewer bytes than the canonical encoding"},
         "gpu_launches": launches,
         "wall_s_timed_region": wall,
@@ -539,11 +539,11 @@ def run_replay(args, world, rank, local):
                         "kernel": "replay_fused_kernel" if fused
                         else "replay step (windows + predict + score)",
                         "algorithmic_bytes_per_launch": REPLAY_ALG_BYTES * n,
-                        "traffic": kernel_traffic("ncu_replay_fused_r2.json", "replay_fused_kernel")
+                        "traffic": kernel_traffic("ncu_replay_fused_r2b.json", "replay_fused_kernel")
                         if fused else replay_traffic(),
                         "peak_source": f"{peak_kind} hbm_gbs",
                         "note": "SURVEY 8(d) 233 B/call; traffic = ncu dram bytes of the step's "
-                                "kernel(s) (profiles/ncu_replay_fused_r2.json, ncu_replay_r2.json)"},
+                                "kernel(s) (profiles/ncu_replay_fused_r2b.json, ncu_replay_r2.json)"},
            "e2e": {"value": world * n * steps / t_e2e, "unit": "calls/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 32,
                    "ms_per_step": 1e3 * t_e2e / steps},
@@ -631,7 +631,7 @@ def run_long_outputs(args, world, rank, local):
     alg_total = int(sum(cand[int(L)] for L in tlen)) + 16 * n + int(c["target_off"][-1])
     per = alg_total // n
     achieved = alg_total / (t_dev / steps) / 1e9
-    traffic = kernel_traffic("ncu_leaf_r2.json", "leaf_match_kernel")
+    traffic = kernel_traffic("ncu_leaf_r2b.json", "leaf_match_kernel")
     out = {"metric": LONG_METRIC, "value": world * n * steps / t_dev, "unit": "sessions/s",
            "n_gpus": world, "steps": steps, "ms_per_step": 1e3 * t_dev / steps,
            "scaling": "weak", "data": "synthetic", "parity_spot_check": ok,
@@ -646,7 +646,7 @@ def run_long_outputs(args, world, rank, local):
                         "peak_source": f"{peak_kind} hbm_gbs",
                         "note": "candidate-leaf bytes (string leaves of the target's length) + "
                                 "directory + target per payload; traffic = ncu dram bytes of "
-                                "leaf_match_kernel (profiles/ncu_leaf_r2.json)"},
+                                "leaf_match_kernel (profiles/ncu_leaf_r2b.json)"},
            "e2e": {"value": world * n * steps / t_e2e, "unit": "sessions/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                    "ms_per_step": 1e3 * t_e2e / steps},
@@ -1012,7 +1012,7 @@ def replay_traffic():
     return total or None
 
 
-def committed_traffic(name: str = "ncu_live_r2b.json"):
+def committed_traffic(name: str = "ncu_live_r2c.json"):
     """dram bytes per launch of the C3 step kernel from the committed ncu capture."""
     return committed_ncu(name).get("dram_bytes_per_launch")
 
