@@ -842,17 +842,21 @@ def mining_relation(args, world, rank, sigs, host, host_pinned, dev, group, rela
     lib = _native.lib()
     stream = torch.cuda.current_stream()
 
-    def one_step(trace):
+    def one_step(trace, done=None):
         tables.hist.zero_()
         ingest_count(tables, trace)
         if group is not None:
             if os.environ.get("PASTE_MINE_TAIL") == "sliced":  # measured no faster (DESIGN 7)
-                return sharded_tail(tables, group, cfg.sigma, cfg.tau)
+                tab = sharded_tail(tables, group, cfg.sigma, cfg.tau)
+                if done is not None:
+                    done.record(stream)
+                return tab
             dist.all_reduce(tables.hist, group=group)
         tables.expand()
         # selection + mine()'s output order on the device; the sorted pattern
-        # table is read back to the host (the step's result)
-        return tables.select_sorted(cfg.sigma, cfg.tau)
+        # table is read back to the host (the step's result: `done` fires
+        # when it is in host memory)
+        return tables.select_sorted(cfg.sigma, cfg.tau, done_event=done)
 
     for _ in range(args.warmup):
         one_step(dev)
@@ -873,8 +877,7 @@ def mining_relation(args, world, rank, sigs, host, host_pinned, dev, group, rela
     for _ in range(steps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        table = one_step(dev)
-        e1.record(stream)
+        table = one_step(dev, e1)
         e1.synchronize()
         t_dev += e0.elapsed_time(e1) / 1e3
         launches += per_step

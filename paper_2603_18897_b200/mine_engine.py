@@ -138,9 +138,13 @@ class MineTables:
         d = self.desc()
         check(lib.paste_mine_expand(ctypes.byref(d), stream_handle()), lib)
 
-    def select_sorted(self, sigma: int, tau: float, cap: int | None = None) -> "MinedTable":
+    def select_sorted(self, sigma: int, tau: float, cap: int | None = None,
+                      done_event=None) -> "MinedTable":
         """Mapping-free patterns in mine()'s output order, selected and sorted
-        on the device (paste_mine_select_sorted) and read back as one table."""
+        on the device (paste_mine_select_sorted) and read back as one table.
+        ``done_event`` (a torch.cuda.Event) is recorded on the stream right
+        after the table's device-to-host copy, i.e. when the result is in
+        host memory, before the host wraps it."""
         from .device_ops import stream_handle
 
         torch = _torch()
@@ -168,11 +172,15 @@ class MineTables:
             st["n_h"].copy_(st["n"], non_blocking=True)
             st["out_h"][:6 * guess].copy_(st["out"][:6 * guess], non_blocking=True)
             stream = torch.cuda.current_stream()
+            if done_event is not None:
+                done_event.record(stream)
             stream.synchronize()
             m = int(st["n_h"][0])
             if m <= st["cap"]:
                 if m > guess:
                     st["out_h"][:6 * m].copy_(st["out"][:6 * m], non_blocking=True)
+                    if done_event is not None:
+                        done_event.record(stream)
                     stream.synchronize()
                 st["last"] = m
                 return MinedTable(st["out_h"][:6 * m].numpy().reshape(m, 6).copy(), self.n_sigs,
