@@ -68,6 +68,8 @@ def parse_args():
                     help="C4 mining corpus size (0 = skip the mining measurement)")
     ap.add_argument("--long-sessions", type=int, default=100_000,
                     help="C5 long-output sessions (0 = skip)")
+    ap.add_argument("--no-stress", dest="stress", action="store_false",
+                    help="skip the C3 run on the 1,000-pattern stress pool")
     ap.add_argument("--phase2-tiles", type=int, default=160,
                     help="tiles of the 400-session coding corpus mined by mine_jsonl (0 = skip)")
     ap.add_argument("--replay-sessions", type=int, default=100_000,
@@ -379,6 +381,9 @@ def run_ours(args):
     if args.replay_sessions > 0:
         torch.cuda.empty_cache()
         out["replay"] = run_replay(args, world, rank, local)
+    if args.stress and args.pool == "c3":
+        torch.cuda.empty_cache()
+        out["c3_stress_pool"] = run_stress(args, world, rank, local)
     if args.phase2_tiles > 0 and rank == 0:
         torch.cuda.empty_cache()
         out["phase2_mining"] = run_phase2(args, world, rank, local)
@@ -389,6 +394,81 @@ def run_ours(args):
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(out))
+
+
+def run_stress(args, world, rank, local):
+    """C3 on SURVEY.md 8(d)'s second pool: the 1,000-pattern / 20-tool stress
+    pool (test_acceptance.py:511-527) with the allow-all policy, 1M sessions
+    whose tool calls cycle uniformly through the pool's tools.  Device-timed
+    steps of the live kernel (L2 flushed between steps) and, at N=1, a
+    parity check of 4 full steps of 100k sessions against the oracle (which
+    scans the 1,000 patterns per session)."""
+    import torch
+
+    from paper_2603_18897_b200.device_ops import DevicePool
+    from paper_2603_18897_b200.live import LiveSessionTable
+    from paper_2603_18897_b200.policy import SpeculationPolicy
+    from paper_2603_18897_b200.scheduling import EstimateBook
+    from paper_2603_18897_b200.synth import StressWorkload, stress_pool
+
+    pool, policy, book = stress_pool(), SpeculationPolicy(default_allow=True), EstimateBook()
+    dp = DevicePool(pool)
+    n, K = args.sessions, args.max_candidates
+    wl = StressWorkload(dp.sigs, dp.keys, n, seed=4242 + rank)
+    table = LiveSessionTable(dp, n, wl.tmpl.nodes, wl.max_batch_bytes, policy, book,
+                             max_candidates=K)
+    for _ in range(table.W):
+        table.step(wl.next_batch())
+    flush = torch.zeros(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    steps = max(1, min(args.steps, 20))
+    staged = []
+    for _ in range(args.warmup + steps):
+        b = wl.next_batch()
+        staged.append((table.steps % table.regions, torch.from_numpy(b.tok).cuda(),
+                       torch.from_numpy(b.node).cuda()))
+        table.steps += 1
+    stream = torch.cuda.current_stream()
+    for region, tok, node in staged[:args.warmup]:
+        table.launch(region, tok, new_node=node)
+    torch.cuda.synchronize()
+    t, preds, acts = 0.0, 0, 0
+    for region, tok, node in staged[args.warmup:]:
+        l2_flush(flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        table.launch(region, tok, new_node=node)
+        e1.record(stream)
+        e1.synchronize()
+        t += e0.elapsed_time(e1) / 1e3
+        preds += int(table.out["n_pred"].sum())
+        acts += int(table.out["n_act"].sum())
+    peak, peak_kind = measured_peaks()
+    achieved = C3_ALG_BYTES * n * steps / t / 1e9
+    out = {"metric": METRIC, "value": world * n * steps / t, "unit": UNIT,
+           "ms_per_step": 1e3 * t / steps, "steps": steps,
+           "config": {"workload": "C3 on the 1,000-pattern / 20-tool stress pool, allow-all policy",
+                      "sessions_per_gpu": n, "window": table.W, "max_candidates": K,
+                      "pool": f"stress ({len(pool.patterns)} patterns)"},
+           "candidates_per_s": world * preds / t, "actions_per_s": world * acts / t,
+           "predictions_per_session": preds / (n * steps),
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "kernel": "predict_live_kernel",
+                        "algorithmic_bytes_per_launch": C3_ALG_BYTES * n,
+                        "peak_source": f"{peak_kind} hbm_gbs"}}
+    del table, staged
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not args.no_parity:
+        from oracle.parity import live_parity
+
+        t0 = time.perf_counter()
+        m = min(n, 100_000)
+        r = live_parity(dp, policy, book, m, 4, K=K, seed=5,
+                        workload_cls=lambda: StressWorkload(dp.sigs, dp.keys, m, seed=5))
+        r["check_s"] = round(time.perf_counter() - t0, 1)
+        out["parity"] = {"sessions": m, "steps": 4, "predictions": r.get("predictions"),
+                         "ok": bool(r.get("kslot_ok") and r.get("serve_ok")),
+                         "mismatch": r.get("mismatch", [])[:5], "check_s": r["check_s"]}
+    return out
 
 
 def live_full_parity(args, dp, policy, book):
@@ -435,7 +515,8 @@ def summary(out):
         return r
 
     s = {"c3": obj(out), "c4": obj(out.get("mining")), "c5": obj(out.get("long_outputs")),
-         "c2": obj(out.get("replay")), "phase2": obj(out.get("phase2_mining"))}
+         "c2": obj(out.get("replay")), "phase2": obj(out.get("phase2_mining")),
+         "c3_stress": obj(out.get("c3_stress_pool"))}
     if out.get("mining", {}).get("suffix"):
         s["c4_suffix"] = {k: out["mining"]["suffix"][k] for k in ("value", "roofline_frac")}
     if out.get("parity"):

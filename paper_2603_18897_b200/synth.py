@@ -205,6 +205,33 @@ class LiveWorkload:
                           np.ascontiguousarray(ref[:, 0], dtype=np.int32))
 
 
+class StressWorkload:
+    """C3 on the 1,000-pattern / 20-tool stress pool (SURVEY.md 8(d) pool ii):
+    every session observes one tool call per step, a uniformly drawn tool of
+    the pool (as the reference's latency test cycles through its 20 tools,
+    test_prediction.py:186-199) that fails with probability ``fail_rate``;
+    the pool has no mappings, so payloads are the small echo shape."""
+
+    def __init__(self, sigs, keys, n_sessions: int, seed: int = 2603, n_tools: int = 20,
+                 fail_rate: float = 0.2):
+        self.n = n_sessions
+        self.tmpl = make_templates(keys)
+        self.rng = np.random.default_rng(seed)
+        self.tool_ids = np.array([sigs.tool(f"tool{i}") for i in range(n_tools)], np.int32)
+        self.fail_rate = fail_rate
+        self.max_batch_bytes = n_sessions * max(len(t) for t in self.tmpl.byte_tmpl)
+
+    def next_batch(self):
+        from .live import EventBatch
+
+        tool = self.rng.integers(0, len(self.tool_ids), self.n)
+        ok = self.rng.random(self.n) >= self.fail_rate
+        kind = np.where(ok, K_ECHO, K_FAIL).astype(np.int8)
+        data, ref = fill_payloads(self.tmpl, kind, self.rng)
+        tok = (2 * self.tool_ids[tool] + ok.astype(np.int32)).astype(np.int32)
+        return EventBatch(tok, ref, data, np.ascontiguousarray(ref[:, 0], dtype=np.int32))
+
+
 def stress_pool(seed: int = 1001, n_patterns: int = 1000, n_tools: int = 20):
     """The 1,000-pattern / 20-tool stress pool of the reference's runtime
     overhead criterion (test_acceptance.py:507-527), regenerated from its
