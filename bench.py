@@ -384,6 +384,8 @@ def run_ours(args):
     if args.stress and args.pool == "c3":
         torch.cuda.empty_cache()
         out["c3_stress_pool"] = run_stress(args, world, rank, local)
+        if out["c3_stress_pool"].get("parity"):
+            parity["c3_stress"] = out["c3_stress_pool"]["parity"]
     if args.phase2_tiles > 0 and rank == 0:
         torch.cuda.empty_cache()
         out["phase2_mining"] = run_phase2(args, world, rank, local)
@@ -496,6 +498,10 @@ def parity_summary(p):
         a, s = p["c4"]["anchored"], p["c4"]["suffix"] or {}
         out.update(c4_events=a["events"], c4_anchored_ok=a["ok"], c4_suffix_ok=s.get("ok"),
                    c4_patterns=[a.get("patterns"), s.get("patterns")])
+    if p.get("c3_stress"):
+        c = p["c3_stress"]
+        out.update(c3_stress_sessions=c["sessions"], c3_stress_predictions=c["predictions"],
+                   c3_stress_ok=c["ok"])
     out["ok"] = all(v for k, v in out.items() if k.endswith("_ok"))
     return out
 
