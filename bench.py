@@ -381,6 +381,15 @@ def run_ours(args):
     if args.replay_sessions > 0:
         torch.cuda.empty_cache()
         out["replay"] = run_replay(args, world, rank, local)
+        r = out["replay"]
+        if r.get("oracle_parity"):
+            parity["c2"] = dict(r["oracle_parity"])
+            parity["c2"]["ok"] = (parity["c2"]["ok"] and r["fused_equals_two_kernel_tallies"]
+                                  and r["consistent_e2e_tallies"])
+            if r.get("pool_tau05"):
+                q = r["pool_tau05"]
+                parity["c2"]["tau05"] = (q["oracle_parity"]["ok"]
+                                         and q["fused_equals_two_kernel_tallies"])
     if args.stress and args.pool == "c3":
         torch.cuda.empty_cache()
         out["c3_stress_pool"] = run_stress(args, world, rank, local)
@@ -498,6 +507,11 @@ def parity_summary(p):
         a, s = p["c4"]["anchored"], p["c4"]["suffix"] or {}
         out.update(c4_events=a["events"], c4_anchored_ok=a["ok"], c4_suffix_ok=s.get("ok"),
                    c4_patterns=[a.get("patterns"), s.get("patterns")])
+    if p.get("c2"):
+        c = p["c2"]
+        out.update(c2_calls=c["calls"], c2_ok=c["ok"])
+        if "tau05" in c:
+            out.update(c2_tau05_ok=c["tau05"])
     if p.get("c3_stress"):
         c = p["c3_stress"]
         out.update(c3_stress_sessions=c["sessions"], c3_stress_predictions=c["predictions"],
@@ -640,12 +654,77 @@ def run_replay(args, world, rank, local):
 
         m = min(n, 60_000)
         t0 = time.perf_counter()
-        bridge.score_corpus(dp.image, c, dp.keys, W, K, threads=1, calls=slice(0, m))
+        want = bridge.score_corpus(dp.image, c, dp.keys, W, K, threads=1, calls=slice(0, m))
         dt = time.perf_counter() - t0
         out["cpu_baseline"] = {"value": m / dt, "unit": "calls/s", "cores": 1, "kind": "port",
                                "sample": f"first {m} scored calls ({dt:.2f} s): oracle_predict "
                                "(C) + canonical_arg_hash hit check (Python), one core"}
+        out["oracle_parity"] = replay_sample_parity(rb, want, m, fused)
+        # SURVEY 8(d) C2's other pool: mine_pool(tau=0.5), 12 patterns
+        out["pool_tau05"] = replay_pool_leg(args, "pool_coding_c2.json", W, K, rank, steps, flush)
     return out
+
+
+def replay_sample_parity(rb, want, m, fused):
+    """Device tallies over the first m scored calls (the same slice the
+    oracle scored) == the oracle's (top1, top3, hits)."""
+    n = rb.desc.n_calls
+    rb.desc.n_calls = m
+    try:
+        if not (fused and rb.launch_fused()):
+            rb.launch()
+        got = rb.tallies.cpu().numpy().tolist()
+    finally:
+        rb.desc.n_calls = n
+    unsure = got[3]
+    if unsure:  # undecided calls are rechecked on the host (score_replay)
+        rb.launch()
+    return {"calls": m, "device": got[:3], "oracle": list(want[:3]), "unsure": unsure,
+            "ok": got[:3] == list(want[:3]) and not unsure}
+
+
+def replay_pool_leg(args, pool_file, W, K, rank, steps, flush):
+    """The fused replay on another pool: time, fused == two-kernel tallies,
+    and oracle parity on a sample of calls."""
+    import torch
+
+    from oracle import bridge
+    from paper_2603_18897_b200.device_ops import DevicePool
+    from paper_2603_18897_b200.mining import load_pool
+    from paper_2603_18897_b200.replay import KeysetTable, ReplayBatch
+    from paper_2603_18897_b200.synth import coding_replay_corpus
+
+    pool = load_pool(os.path.join(ROOT, "paper_2603_18897_b200", "data", pool_file))
+    dp = DevicePool(pool)
+    ks = KeysetTable()
+    c = coding_replay_corpus(dp, args.replay_sessions, window_capacity=W, seed=2 + rank, ksets=ks)
+    n = c.n_calls
+    rb = ReplayBatch(dp, c, W, K, ks)
+    rb.launch()
+    two = rb.tallies.cpu().numpy().tolist()
+    fused = rb.launch_fused()
+    step = rb.launch_fused if fused else rb.launch
+    for _ in range(max(args.warmup, 1)):
+        step()
+    stream = torch.cuda.current_stream()
+    t = 0.0
+    for _ in range(steps):
+        l2_flush(flush)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        t += e0.elapsed_time(e1) / 1e3
+    tallies = rb.tallies.cpu().numpy().tolist()
+    m = min(n, 20_000)
+    want = bridge.score_corpus(dp.image, c, dp.keys, W, K, threads=1, calls=slice(0, m))
+    return {"pool": f"coding tau=0.5 ({len(pool.patterns)} patterns, reference-mined)",
+            "scored_calls": n, "fused": fused, "ms_per_step": 1e3 * t / steps,
+            "value": n * steps / t, "unit": "calls/s",
+            "rates": {"top1": tallies[0] / n, "top3": tallies[1] / n, "hit_rate": tallies[2] / n},
+            "fused_equals_two_kernel_tallies": tallies == two,
+            "oracle_parity": replay_sample_parity(rb, want, m, fused)}
 
 
 LONG_METRIC = "long-output dependency resolutions/sec"
