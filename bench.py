@@ -57,6 +57,8 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-python-reference", action="store_true",
+                    help="skip timing the unmodified Python reference (baseline/_ref)")
     ap.add_argument("--sessions", type=int, default=1_000_000)
     ap.add_argument("--pool", default="c3", choices=["c3", "stress"])
     ap.add_argument("--max-candidates", type=int, default=8)
@@ -398,6 +400,11 @@ def run_ours(args):
     if args.phase2_tiles > 0 and rank == 0:
         torch.cuda.empty_cache()
         out["phase2_mining"] = run_phase2(args, world, rank, local)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.no_python_reference:
+        out["python_reference"] = python_reference_c3(args, check=True)
+        pr = out["python_reference"].get("parity")
+        if pr:
+            parity["c3_reference"] = pr
     if parity:
         out["parity"] = parity_summary(parity)
     out["summary"] = summary(out)
@@ -512,6 +519,10 @@ def parity_summary(p):
         out.update(c2_calls=c["calls"], c2_ok=c["ok"])
         if "tau05" in c:
             out.update(c2_tau05_ok=c["tau05"])
+    if p.get("c3_reference"):
+        c = p["c3_reference"]
+        out.update(c3_reference_session_steps=c["sessions"] * c["steps"],
+                   c3_reference_predictions=c["predictions"], c3_reference_ok=c["ok"])
     if p.get("c3_stress"):
         c = p["c3_stress"]
         out.update(c3_stress_sessions=c["sessions"], c3_stress_predictions=c["predictions"],
@@ -539,9 +550,52 @@ def summary(out):
          "c3_stress": obj(out.get("c3_stress_pool"))}
     if out.get("mining", {}).get("suffix"):
         s["c4_suffix"] = {k: out["mining"]["suffix"][k] for k in ("value", "roofline_frac")}
+    pr = out.get("python_reference") or {}
+    if pr.get("all_cores"):
+        s["python_reference"] = {"one_core": pr["one_core"]["value"],
+                                 "all_cores": pr["all_cores"]["value"],
+                                 "cores": pr["all_cores"]["cores"], "unit": UNIT}
     if out.get("parity"):
         s["parity_ok"] = out["parity"]["ok"]
     return s
+
+
+def python_reference_c3(args, check=False):
+    """The unmodified reference (spectool from baseline/_ref) on a bounded
+    sample of the C3 workload, timed on this host's cores: one core, then
+    all cores as session-sharded processes.  With
+    ``check``, our live step runs the same batches on the device and every
+    decoded prediction / admitted action is compared with the reference's."""
+    import spectool_ref as R
+
+    why = R.available()
+    if why:
+        return {"unavailable": why}
+    if args.pool != "c3":
+        return {"unavailable": "sampled on the C3 motif pool only"}
+    pf = os.path.join(ROOT, "paper_2603_18897_b200", "data", "pool_motif_c3.json")
+    m, timed = 2000, 8
+    n_steps = R.W + timed
+    t0 = time.perf_counter()
+    dp, wl, batches, events = R.c3_sample(m, n_steps, 2603, pf)
+    gen = time.perf_counter() - t0
+    done, spent, outs = R.run_c3(events, pf, MOTIF_POLICY, DURATIONS, args.max_candidates,
+                                 record=check)
+    out = {"impl": "reference: unmodified spectool (baseline/_ref), Python",
+           "one_core": {"value": done / spent, "unit": UNIT, "cores": 1,
+                        "sample": f"{m} sessions x {timed} steps after a {R.W}-event fill "
+                                  f"({spent:.2f} s): observe + predict(max_candidates="
+                                  f"{args.max_candidates}) + admit per session-step"},
+           "sample_build_s": round(gen, 2)}
+    procs = os.cpu_count() or 1
+    v, d, slowest = R.c3_all_cores(procs, m, n_steps, pf, MOTIF_POLICY, DURATIONS)
+    out["all_cores"] = {"value": v, "unit": UNIT, "cores": procs,
+                        "sample": f"{procs} processes x {m} sessions x {timed} steps, each its "
+                                  f"own shard; {d} session-steps / slowest worker {slowest:.2f} s"}
+    if check:
+        _, policy, book = load_setup(args)
+        out["parity"] = R.c3_parity(dp, wl, batches, outs, policy, book, args.max_candidates)
+    return out
 
 
 REPLAY_METRIC = "replayed tool calls/sec (score_accuracy)"
@@ -1258,6 +1312,8 @@ def run_reference(args):
                                       "oracle/paste_oracle.c with all host threads"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
+    if not args.no_python_reference:
+        out["python_reference"] = python_reference_c3(args)
     print(json.dumps(out))
 
 
