@@ -377,9 +377,14 @@ def run_ours(args):
         if "parity" in out["mining"]:
             parity["c4"] = {"anchored": out["mining"]["parity"],
                             "suffix": out["mining"]["suffix"].get("parity")}
+        if "ok" in (out["mining"].get("python_reference") or {}):
+            parity["c4_reference"] = out["mining"]["python_reference"]["ok"]
     if args.long_sessions > 0:
         torch.cuda.empty_cache()
         out["long_outputs"] = run_long_outputs(args, world, rank, local)
+        lr = out["long_outputs"].get("python_reference") or {}
+        if "ours_equals_reference" in lr:
+            parity["c5_reference"] = lr["ours_equals_reference"]
     if args.replay_sessions > 0:
         torch.cuda.empty_cache()
         out["replay"] = run_replay(args, world, rank, local)
@@ -388,6 +393,8 @@ def run_ours(args):
             parity["c2"] = dict(r["oracle_parity"])
             parity["c2"]["ok"] = (parity["c2"]["ok"] and r["fused_equals_two_kernel_tallies"]
                                   and r["consistent_e2e_tallies"])
+            if (r.get("python_reference") or {}).get("ok") is not None:
+                parity["c2"]["reference"] = r["python_reference"]["ok"]
             if r.get("pool_tau05"):
                 q = r["pool_tau05"]
                 parity["c2"]["tau05"] = (q["oracle_parity"]["ok"]
@@ -400,6 +407,9 @@ def run_ours(args):
     if args.phase2_tiles > 0 and rank == 0:
         torch.cuda.empty_cache()
         out["phase2_mining"] = run_phase2(args, world, rank, local)
+        pr = out["phase2_mining"].get("python_reference") or {}
+        if "mine_jsonl_equals_reference" in pr:
+            parity["phase2_reference"] = pr
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.no_python_reference:
         out["python_reference"] = python_reference_c3(args, check=True)
         pr = out["python_reference"].get("parity")
@@ -519,10 +529,20 @@ def parity_summary(p):
         out.update(c2_calls=c["calls"], c2_ok=c["ok"])
         if "tau05" in c:
             out.update(c2_tau05_ok=c["tau05"])
+        if "reference" in c:
+            out.update(c2_reference_ok=c["reference"])
     if p.get("c3_reference"):
         c = p["c3_reference"]
         out.update(c3_reference_session_steps=c["sessions"] * c["steps"],
                    c3_reference_predictions=c["predictions"], c3_reference_ok=c["ok"])
+    if p.get("c4_reference") is not None:
+        out.update(c4_reference_ok=p["c4_reference"])
+    if p.get("c5_reference") is not None:
+        out.update(c5_reference_ok=p["c5_reference"])
+    if p.get("phase2_reference"):
+        c = p["phase2_reference"]
+        out.update(phase2_reference_ok=c["mine_jsonl_equals_reference"],
+                   c1_reference_ok=c["c1"]["ours_equals_reference"])
     if p.get("c3_stress"):
         c = p["c3_stress"]
         out.update(c3_stress_sessions=c["sessions"], c3_stress_predictions=c["predictions"],
@@ -543,6 +563,8 @@ def summary(out):
         if o.get("cpu_baseline"):
             r["cpu_baseline"] = o["cpu_baseline"]["value"]
             r["cpu_cores"] = o["cpu_baseline"]["cores"]
+        if (o.get("python_reference") or {}).get("value"):
+            r["python_reference_1core"] = o["python_reference"]["value"]
         return r
 
     s = {"c3": obj(out), "c4": obj(out.get("mining")), "c5": obj(out.get("long_outputs")),
@@ -555,6 +577,9 @@ def summary(out):
         s["python_reference"] = {"one_core": pr["one_core"]["value"],
                                  "all_cores": pr["all_cores"]["value"],
                                  "cores": pr["all_cores"]["cores"], "unit": UNIT}
+    pm = (out.get("phase2_mining") or {}).get("python_reference") or {}
+    if pm.get("value"):
+        s["phase2_python_reference"] = {"value": pm["value"], "unit": pm["unit"], "cores": 1}
     if out.get("parity"):
         s["parity_ok"] = out["parity"]["ok"]
     return s
@@ -716,6 +741,44 @@ def run_replay(args, world, rank, local):
         out["oracle_parity"] = replay_sample_parity(rb, want, m, fused)
         # SURVEY 8(d) C2's other pool: mine_pool(tau=0.5), 12 patterns
         out["pool_tau05"] = replay_pool_leg(args, "pool_coding_c2.json", W, K, rank, steps, flush)
+        out["python_reference"] = replay_python_reference(W, K)
+    return out
+
+
+def replay_python_reference(W, K, tiles=20):
+    """The unmodified reference's score_accuracy on the reference-generated
+    coding corpus (400 sessions, tiled), both C2 pools, one core, timed on
+    this host; our score_accuracy (the public API: one device batch) on the
+    same sessions must report the same top1 / top3 / hit_rate / scored."""
+    import spectool_ref as R
+
+    from paper_2603_18897_b200.events import ingest_trace
+    from paper_2603_18897_b200.mining import load_pool
+    from paper_2603_18897_b200.prediction import score_accuracy
+
+    why = R.available()
+    if why:
+        return {"unavailable": why}
+    text, n_sess, _ = coding_jsonl(tiles)
+    sessions = ingest_trace(text).sessions
+    out = {"impl": "reference: unmodified spectool (baseline/_ref), Python", "cores": 1,
+           "unit": "calls/s", "sessions": n_sess}
+    ok = True
+    for name in ("pool_coding_c2_t03.json", "pool_coding_c2.json"):
+        pf = os.path.join(ROOT, "paper_2603_18897_b200", "data", name)
+        ref, scored, dt = R.score_text(text, pf, W, K)
+        t0 = time.perf_counter()
+        ours = score_accuracy(sessions, load_pool(pf), W, K).to_json()
+        t_ours = time.perf_counter() - t0
+        same = ours == ref
+        ok = ok and same
+        out[name] = {"value": scored / dt, "scored_calls": scored, "seconds": dt,
+                     "report": ref, "ours_equals_reference": same,
+                     "ours_public_api_seconds": t_ours}
+    out["value"] = out["pool_coding_c2_t03.json"]["value"]
+    out["ok"] = ok
+    out["sample"] = (f"{n_sess} sessions (the reference-generated coding corpus tiled {tiles}x): "
+                     f"score_accuracy(W={W}, max_candidates={K})")
     return out
 
 
@@ -887,7 +950,30 @@ def run_long_outputs(args, world, rank, local):
         out["cpu_baseline"] = {"value": m / dt, "unit": "sessions/s", "cores": threads,
                                "kind": "port", "sample": f"{m} sessions ({dt:.2f} s), "
                                "oracle_leaf_scan (candidate_paths restated in C), OpenMP"}
+        out["python_reference"] = leaf_python_reference(c, batch, n)
     return out
+
+
+def leaf_python_reference(c, batch, n, m=300):
+    """The unmodified reference's candidate_paths on the first m C5 payloads,
+    one core, timed on this host; every session's path list compared with
+    the device's match nodes (as key/index paths)."""
+    import spectool_ref as R
+
+    from paper_2603_18897_b200.tape import path_to_node
+
+    why = R.available()
+    if why:
+        return {"unavailable": why}
+    paths, trunc, dt = R.candidate_paths_sample(c, m)
+    n_out = batch.n_out.cpu().numpy()
+    nodes = batch.out_nodes.view(n, -1).cpu().numpy()
+    same = all(tuple(path_to_node(c["nodes"], 0, int(x), c["keys"]) for x in nodes[s, :n_out[s]])
+               == paths[s] for s in range(m)) and not any(trunc)
+    return {"impl": "reference: unmodified spectool (baseline/_ref), Python",
+            "value": m / dt, "unit": "sessions/s", "cores": 1,
+            "sample": f"first {m} sessions ({dt:.2f} s): candidate_paths(payload, next url)",
+            "paths": sum(len(p) for p in paths), "ours_equals_reference": same}
 
 
 PHASE2_METRIC = "mined trace events/sec, mapping-bearing JSONL (Phase II included)"
@@ -1001,7 +1087,34 @@ def run_phase2(args, world, rank, local):
                                          "ingest_trace + oracle counts + Python Phase II "
                                          "restatement (oracle/mine_host.py)",
                                "patterns": len(host)}
+        out["python_reference"] = phase2_python_reference(sample, buf.getvalue(), cfg, got)
     return out
+
+
+def phase2_python_reference(sample, c1_text, cfg, c1_ours):
+    """The unmodified reference's ingest_trace + mine() on the same corpus
+    sample and on C1, one core, timed on this host; its pattern lists
+    (contexts, targets, mappings, p, support, pattern ids) compared with
+    mine_jsonl's on the same text."""
+    import spectool_ref as R
+
+    from paper_2603_18897_b200.ingest import mine_jsonl
+
+    why = R.available()
+    if why:
+        return {"unavailable": why}
+    ref, n_sess, n_ev, dt = R.mine_text(sample, cfg.tau)
+    ours = R.ours_as_json(mine_jsonl(sample, cfg))
+    ref_c1, _, c1_ev, dt_c1 = R.mine_text(c1_text, cfg.tau)
+    return {"impl": "reference: unmodified spectool (baseline/_ref), Python",
+            "value": n_ev / dt, "unit": "events/s", "cores": 1,
+            "sample": f"{n_sess} sessions / {n_ev} events of the corpus ({dt:.2f} s): "
+                      "ingest_trace + mine(MiningConfig(tau=0.3))",
+            "patterns": len(ref), "patterns_with_mapping": sum(p["mapping"] is not None
+                                                               for p in ref),
+            "mine_jsonl_equals_reference": ours == ref,
+            "c1": {"events": c1_ev, "seconds": dt_c1, "events_per_s": c1_ev / dt_c1,
+                   "ours_equals_reference": R.ours_as_json(c1_ours) == ref_c1}}
 
 
 MINE_METRIC = "mined trace events/sec"
@@ -1043,6 +1156,7 @@ def run_mining(args, world, rank, local):
         out["suffix"]["parity"] = sfx["parity"]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = mining_cpu_baseline(MiningConfig(k=3, sigma=5, tau=0.3), sigs)
+        out["python_reference"] = mining_python_reference()
     return out
 
 
@@ -1204,6 +1318,40 @@ def mining_cpu_baseline(cfg, sigs, n_events=1_000_000):
     dt = time.perf_counter() - t0
     return {"value": n_events / dt, "unit": "events/s", "cores": 1, "kind": "port",
             "sample": f"{n_events} events of the C4 corpus ({dt:.1f} s)"}
+
+
+def mining_python_reference(n_events=5000):
+    """The unmodified reference's ingest_trace + mine() (k=3, sigma=5,
+    tau=0.3, both relations) on a small sample of the C4 corpus as JSONL,
+    one core, timed on this host; its pattern lists compared with mine_jsonl
+    on the same text.  The reference's Phase II rescans every stream for
+    every candidate (mining.py:215-227), so its cost grows faster than the
+    sample: the per-event rate holds for this sample size only."""
+    import spectool_ref as R
+
+    from paper_2603_18897_b200.ingest import mine_jsonl
+    from paper_2603_18897_b200.mining import MatchRelation, MiningConfig
+    from paper_2603_18897_b200.synth import C4_TOOLS, columnar_corpus
+
+    why = R.available()
+    if why:
+        return {"unavailable": why}
+    text = R.columnar_to_jsonl(columnar_corpus(n_events, seed=7), C4_TOOLS)
+    out = {"impl": "reference: unmodified spectool (baseline/_ref), Python", "cores": 1,
+           "unit": "events/s", "events": n_events}
+    ok = True
+    for rel in MatchRelation:
+        ref, n_sess, n_ev, dt = R.mine_text(text, 0.3, 3, 5, rel.value)
+        cfg = MiningConfig(k=3, sigma=5, tau=0.3, match_relation=rel)
+        same = R.ours_as_json(mine_jsonl(text, cfg)) == ref
+        ok = ok and same
+        out[rel.value] = {"value": n_ev / dt, "seconds": dt, "sessions": n_sess,
+                          "patterns": len(ref), "ours_equals_reference": same}
+    out["value"] = out[MatchRelation.ANCHORED_SUBSEQUENCE.value]["value"]
+    out["ok"] = ok
+    out["sample"] = (f"{n_events} events of the C4 generator (seed 7) as JSONL: ingest_trace + "
+                     "mine(); Phase II rescans make the rate fall as the sample grows")
+    return out
 
 
 def committed_ncu(name: str) -> dict:

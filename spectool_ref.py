@@ -190,3 +190,78 @@ def c3_parity(dp, wl, batches, ref_outs, policy, book, max_candidates=8):
                              "reference": [_pred_key(p) for p in rp]}
     return {"sessions": m, "steps": len(batches) - W, "predictions": n_pred, "actions": n_act,
             "mismatched_session_steps": bad, "first_mismatch": first, "ok": bad == 0}
+
+
+def mine_text(text: str, tau: float, k: int = 3, sigma: int = 5, relation: str | None = None):
+    """The reference end to end on JSONL text: ingest_trace (events.py:196)
+    + mine (mining.py:248) with MiningConfig(k, sigma, tau, relation).
+    Returns (patterns as pool JSON, sessions, events, seconds)."""
+    from spectool.events import ingest_trace
+    from spectool.mining import MatchRelation, MiningConfig, _pattern_to_json, mine
+
+    cfg = MiningConfig(k=k, sigma=sigma, tau=tau)
+    if relation is not None:
+        cfg = MiningConfig(k=k, sigma=sigma, tau=tau, match_relation=MatchRelation(relation))
+    t0 = time.perf_counter()
+    sessions = ingest_trace(text).sessions
+    pats = mine(sessions, cfg)
+    dt = time.perf_counter() - t0
+    return ([_pattern_to_json(p) for p in pats], len(sessions),
+            sum(len(s.events) for s in sessions), dt)
+
+
+def ours_as_json(patterns):
+    from paper_2603_18897_b200.mining import _pattern_to_json
+
+    return [_pattern_to_json(p) for p in patterns]
+
+
+def score_text(text: str, pool_file: str, window: int, max_candidates):
+    """The reference's score_accuracy (prediction.py:133-169) over the
+    sessions of JSONL text, with a reference-format pool file.  Returns
+    (report dict, scored calls, seconds of score_accuracy alone)."""
+    from spectool.events import ingest_trace
+    from spectool.mining import load_pool
+    from spectool.prediction import score_accuracy
+
+    sessions = ingest_trace(text).sessions
+    pool = load_pool(pool_file)
+    t0 = time.perf_counter()
+    rep = score_accuracy(sessions, pool, window, max_candidates)
+    dt = time.perf_counter() - t0
+    return rep.to_json(), rep.scored_calls, dt
+
+
+def candidate_paths_sample(c: dict, m: int):
+    """The reference's candidate_paths (mappings.py:237-266, default node
+    budget) over the first m C5 payloads (synth.long_output_corpus),
+    decoded to Python objects; the target is the next call's argument
+    string.  Returns (paths per session, truncated flags, seconds of the
+    candidate_paths calls alone)."""
+    from spectool.mappings import candidate_paths
+
+    from paper_2603_18897_b200.tape import decode_node
+
+    payloads, targets = [], []
+    for s in range(m):
+        payloads.append(decode_node(c["nodes"], c["bytes"], int(c["refs"][s, 0]),
+                                    int(c["refs"][s, 1]), 0, c["keys"]))
+        t0, t1 = int(c["target_off"][s]), int(c["target_off"][s + 1])
+        targets.append(bytes(c["target_bytes"][t0:t1]).decode("utf-8"))
+    t0 = time.perf_counter()
+    res = [candidate_paths(p, t) for p, t in zip(payloads, targets)]
+    dt = time.perf_counter() - t0
+    return [r.paths for r in res], [r.truncated for r in res], dt
+
+
+def columnar_to_jsonl(c: dict, tools) -> str:
+    """A columnar corpus (synth.columnar_corpus) as the reference's JSONL
+    records (events.py:162-184: session_id, seq, kind, tool, status,
+    t_start_ms, t_end_ms), one line per event in file order."""
+    sess, seq, sig = c["session"].tolist(), c["seq"].tolist(), c["sig"].tolist()
+    ts, te = c["t_start"].tolist(), c["t_end"].tolist()
+    return "".join(
+        '{"session_id": "c%d", "seq": %d, "kind": "tool_call", "tool": "%s", "status": "%s", '
+        '"t_start_ms": %r, "t_end_ms": %r}\n'
+        % (a, q, tools[g >> 1], "success" if g & 1 else "fail", x, y)
+        for a, q, g, x, y in zip(sess, seq, sig, ts, te))
