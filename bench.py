@@ -344,8 +344,10 @@ def run_ours(args):
                 "h2d_bytes_per_step": h2d // S_, "d2h_bytes_per_step": d2h // S_,
                 "ms_per_step": 1e3 * e2e_s / S_,
                 "records": "narrow CSR streams, format bits %d (%s)" % (
-                    table.sformat, "per-session match-table key + refs; counts and actions "
-                    "from the key's live-plan entry" if table.sformat & 16 else
+                    table.sformat, "per-session match-table key + refs%s; counts and actions "
+                    "from the key's live-plan entry" % (
+                        " (one per distinct resolution)" if table.sformat & 32 else "")
+                    if table.sformat & 16 else
                     "per-session match-table key + refs + actions"
                     if table.sformat & 8 else "per-prediction codes + refs + actions"),
                 "inputs": "u8 token + u16 node_base per session" if table.narrow8

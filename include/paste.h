@@ -770,9 +770,16 @@ int paste_resolve(const paste_resolve_desc* d, void* stream);
  * actions follow from its key's live-plan entry (paste_build_live_plan: the
  * same admit decisions) and its arg stream (an unresolved reference makes
  * the prediction PARTIAL, which admits it at the entry's partial level); the
- * host expands them from its copy of the plan.  Streams: key + arg.       */
+ * host expands them from its copy of the plan.  Streams: key + arg.
+ * PASTE_CF_UNIQ (with PASTE_CF_KEYS): the arg stream holds one reference
+ * per distinct resolution of the entry instead of one per binding --
+ * bindings with the same expression (kind, path steps; fallback suffix,
+ * start index and fail tool) on the same source event resolve to the same
+ * node, so the plan numbers them as units in first-use order (map word bits
+ * 56-63, the count in header byte 3) and the host maps each binding to its
+ * unit's reference.                                                        */
 enum { PASTE_CF_HDR8 = 1, PASTE_CF_PRED8 = 2, PASTE_CF_ARG16 = 4, PASTE_CF_ENTRY16 = 8,
-       PASTE_CF_KEYS = 16 };
+       PASTE_CF_KEYS = 16, PASTE_CF_UNIQ = 32 };
 typedef struct {
   void* hdr;         /* [n]                                                  */
   void* pred;

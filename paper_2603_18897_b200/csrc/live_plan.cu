@@ -67,8 +67,36 @@ struct MTRec {  // the match-table record (predict_fast.cu, 32 bytes)
   double p;
 };
 
+// true when bindings a and b resolve to the same node of the same source
+// payload (the caller compares the source ages): same expression kind and
+// the same path steps (and, for IndexedFallback, the same suffix, start
+// index and fail tool).  ctx_pos is not compared -- the age stands for it.
+__device__ inline bool same_resolution(const paste_pool_desc& pool, int a, int b) {
+  if (a == b) return true;
+  const paste_binding x = pool.bindings[a], y = pool.bindings[b];
+  if (x.kind != y.kind || x.step_cnt != y.step_cnt) return false;
+  const bool fb = x.kind == PASTE_X_FALLBACK;
+  if (fb && (x.suf_cnt != y.suf_cnt || x.start_index != y.start_index ||
+             x.fail_tool != y.fail_tool))
+    return false;
+  const int2* st = reinterpret_cast<const int2*>(pool.steps);
+  for (int i = 0; i < x.step_cnt; ++i) {
+    const int2 u = st[x.step_off + i], v = st[y.step_off + i];
+    if (u.x != v.x || u.y != v.y) return false;
+  }
+  if (fb)
+    for (int i = 0; i < x.suf_cnt; ++i) {
+      const int2 u = st[x.suf_off + i], v = st[y.suf_off + i];
+      if (u.x != v.x || u.y != v.y) return false;
+    }
+  return true;
+}
+
 // one thread per key: admit the key's first K matches exactly as admit()
-// does (policy.py:207-244) and lay the records out
+// does (policy.py:207-244) and lay the records out.  Map word q:
+// binding | rank << 32 | bslot << 40 | source age << 48 | unit << 56, where
+// the units number the entry's distinct resolutions (same_resolution at the
+// same age) in first-use order; duplicates only ever point at units < 64.
 __global__ void build_live_plan_kernel(const paste_pool_desc pool, const paste_admit_desc adm,
                                        const uint8_t* table, int64_t mt_stride, int64_t n_keys,
                                        PlanLayout L, uint8_t* plan) {
@@ -117,10 +145,22 @@ __global__ void build_live_plan_kernel(const paste_pool_desc pool, const paste_a
       util[j] = u;
     }
   }
+  int n_unit = 0;
+  for (int q = 0; q < n_map; ++q) {
+    const int bq = (int)(uint32_t)map[q], aq = (int)((map[q] >> 48) & 0xff);
+    int u = -1;
+    for (int p = 0; p < q && u < 0; ++p) {
+      const int up = (int)(map[p] >> 56);
+      if (up < 64 && (int)((map[p] >> 48) & 0xff) == aq && same_resolution(pool, (int)(uint32_t)map[p], bq))
+        u = up;
+    }
+    if (u < 0) u = n_unit++;
+    map[q] |= (uint64_t)u << 56;
+  }
   P[0] = (uint8_t)nm;
   P[1] = (uint8_t)n_act;
   P[2] = (uint8_t)n_map;
-  P[3] = 0;
+  P[3] = (uint8_t)n_unit;
   reinterpret_cast<int32_t*>(P)[1] = hdr[1];
 }
 
@@ -188,7 +228,8 @@ struct Sess {
   int m;
   const uint8_t* e;        // plan entry (nullptr = no predictions)
   int32_t key;             // match-table key, -1 = none
-  int nm, n_act, n_map, n_err;
+  int nm, n_act, n_err;
+  int n_map;               // map entries | distinct units << 8 (the plan header)
 };
 
 // ring addressing of session s (derived, not kept per session: registers)
@@ -329,7 +370,7 @@ __device__ __forceinline__ void front_key(const LiveParams& P, Sess<G>& y, const
     const int2 h = *reinterpret_cast<const int2*>(y.e);
     y.nm = h.x & 0xff;
     y.n_act = (h.x >> 8) & 0xff;
-    y.n_map = (h.x >> 16) & 0xff;
+    y.n_map = (h.x >> 16) & 0xffff;
     y.n_err = h.y;
   }
 }
@@ -347,15 +388,29 @@ __device__ __forceinline__ void live_front(const LiveParams& P, int64_t base, Se
 }
 
 // resolve the entry's bindings for session y; returns the PARTIAL mask and
-// calls emit(q, rank, bslot, ev, node) for every binding (node < 0 = unresolved)
+// calls emit(rank, bslot, ev, node) for every binding (node < 0 =
+// unresolved).  With `units` (PASTE_CF_UNIQ) a binding whose resolution
+// unit was already resolved is not resolved or emitted again: it takes the
+// unit's outcome for the PARTIAL mask, and emit runs once per unit.
 template <int G, typename F>
-__device__ __forceinline__ uint32_t live_resolve(const LiveParams& P, const Sess<G>& y, F emit) {
+__device__ __forceinline__ uint32_t live_resolve(const LiveParams& P, const Sess<G>& y, F emit,
+                                                 bool units = false) {
   uint32_t part = 0;
+  uint64_t bad = 0;  // unresolved units (< 64)
+  int nu = 0;
   const uint64_t* map = reinterpret_cast<const uint64_t*>(y.e + P.L.off_map);
-  for (int q = 0; q < y.n_map; ++q) {
+  const int n_map = y.n_map & 0xff;
+  for (int q = 0; q < n_map; ++q) {
     const uint64_t w = map[q];
     const int bind = (int)(uint32_t)w, rank = (int)((w >> 32) & 0xff), bslot = (int)((w >> 40) & 0xff);
-    const int age = (int)((w >> 48) & 0xff);
+    const int age = (int)((w >> 48) & 0xff), unit = (int)(w >> 56);
+    if (units) {
+      if (unit < nu) {  // a repeat of an earlier unit
+        if (unit < 64 && ((bad >> unit) & 1ull)) part |= 1u << rank;
+        continue;
+      }
+      ++nu;
+    }
     const int slot = (int)((y.slots >> (4 * age)) & 15);
     int32_t ev;
     int64_t nb;
@@ -378,7 +433,10 @@ __device__ __forceinline__ uint32_t live_resolve(const LiveParams& P, const Sess
       }
       cur = walk_binding(P.win, P.pool.steps, bd, nb, fails);
     }
-    if (cur < 0) part |= 1u << rank;
+    if (cur < 0) {
+      part |= 1u << rank;
+      if (units && unit < 64) bad |= 1ull << unit;
+    }
     emit(rank, bslot, ev, cur);
   }
   return part;
@@ -638,6 +696,14 @@ __device__ __forceinline__ void live_offsets(const LiveParams& P, int64_t tile, 
   }
 }
 
+// argument words a session writes: one per binding, or one per resolution
+// unit (PASTE_CF_UNIQ); none without predictions
+template <int G>
+__device__ __forceinline__ int arg_count(const LiveParams& P, const Sess<G>& y) {
+  if (y.nm == 0) return 0;
+  return (P.C.format & PASTE_CF_UNIQ) ? (y.n_map >> 8) & 0xff : y.n_map & 0xff;
+}
+
 // one session's records in the narrow streams at its offsets off[4]
 template <int G>
 __device__ __forceinline__ void compact_write(const LiveParams& P, const Sess<G>& y,
@@ -646,6 +712,7 @@ __device__ __forceinline__ void compact_write(const LiveParams& P, const Sess<G>
   const paste_compact_desc& C = P.C;
   const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
   const bool keys = (C.format & PASTE_CF_KEYS) != 0;
+  const bool units = (C.format & PASTE_CF_UNIQ) != 0;
   if (!keys) cf_hdr(C, y.s, y.nm, y.n_act);
   uint32_t part = 0;
   if (y.nm > 0 && y.n_map > 0) {
@@ -665,7 +732,7 @@ __device__ __forceinline__ void compact_write(const LiveParams& P, const Sess<G>
       if (a16) static_cast<uint16_t*>(C.arg)[oa + q] = (uint16_t)w;
       else static_cast<uint32_t*>(C.arg)[oa + q] = w;
       ++q;
-    });
+    }, units);
   }
   if (C.format & PASTE_CF_ENTRY16) {
     static_cast<uint16_t*>(C.pred)[y.s] = y.e ? (uint16_t)y.key : (uint16_t)0xffffu;
@@ -705,7 +772,7 @@ __global__ void __launch_bounds__(LT) predict_live_compact_kernel(const LivePara
 #pragma unroll
     for (int j = 0; j < SPT; ++j) {
       c[j][0] = x[j].nm;
-      c[j][1] = x[j].n_map;
+      c[j][1] = arg_count(P, x[j]);
       c[j][2] = x[j].n_act;
       c[j][3] = x[j].n_err;
     }
@@ -732,8 +799,8 @@ __device__ __forceinline__ void stage_write(const LiveParams& P, const Sess<G>& 
   const paste_compact_desc& C = P.C;
   const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
   uint32_t part = 0;
+  int q = 0;  // argument words staged
   if (y.nm > 0 && y.n_map > 0) {
-    int q = 0;
     uint32_t* sa = P.st_arg + y.s * P.M;
     part = live_resolve<G>(P, y, [&](int, int, int32_t ev, int64_t cur) {
       uint32_t w = a16 ? 0xffffu : 0xffffffffu;
@@ -747,13 +814,13 @@ __device__ __forceinline__ void stage_write(const LiveParams& P, const Sess<G>& 
           ++wide;
       }
       sa[q++] = w;
-    });
+    }, (C.format & PASTE_CF_UNIQ) != 0);
   }
   if (!(C.format & PASTE_CF_KEYS)) cf_hdr(C, y.s, y.nm, y.n_act);
   if (C.format & PASTE_CF_ENTRY16)
     static_cast<uint16_t*>(C.pred)[y.s] = y.key >= 0 ? (uint16_t)y.key : (uint16_t)0xffffu;
   P.st_key[y.s] = y.key;
-  P.st_cnt[y.s] = (uint32_t)y.nm | ((uint32_t)y.n_act << 5) | ((uint32_t)y.n_map << 10) |
+  P.st_cnt[y.s] = (uint32_t)y.nm | ((uint32_t)y.n_act << 5) | ((uint32_t)q << 10) |
                   ((uint32_t)y.n_err << 18);
   P.st_part[y.s] = part;
 }
@@ -865,7 +932,7 @@ __global__ void __launch_bounds__(LT) predict_live_compact_pipe_kernel(const Liv
     front_load(P, (tile + 2 * G64) * LT + threadIdx.x, f2);
     front_observe<G>(P, f1, y1, m1);
     front_key<G, true>(P, y0, m0);
-    int c[1][4] = {{y0.nm, y0.n_map, y0.n_act, y0.n_err}};
+    int c[1][4] = {{y0.nm, arg_count(P, y0), y0.n_act, y0.n_err}};
     uint64_t off[1][4];
     live_offsets<1>(P, tile, c, off);
     if (y0.s < n) compact_write<G>(P, y0, off[0], wide);
@@ -1157,7 +1224,8 @@ extern "C" int paste_predict_live_compact(const paste_pool_desc* pool, paste_win
       ((c->format & PASTE_CF_PRED8) && pool->n_patterns > 64) || pool->n_patterns > (1 << 14) ||
       ((c->format & PASTE_CF_ENTRY16) &&
        live_keys(pool, live_gather_depth(pool, windows->capacity)) >= 0xffff) ||
-      ((c->format & PASTE_CF_KEYS) && !(c->format & PASTE_CF_ENTRY16))) {
+      ((c->format & PASTE_CF_KEYS) && !(c->format & PASTE_CF_ENTRY16)) ||
+      ((c->format & PASTE_CF_UNIQ) && !(c->format & PASTE_CF_KEYS))) {
     set_error("stream format outside the live plan's envelope");
     return PASTE_ERR_UNSUPPORTED;
   }

@@ -145,6 +145,9 @@ class LiveSessionTable:
         self.staged8 = False
         if self.plan is not None and self.sformat & _native.PASTE_CF_ENTRY16:
             self.sformat |= _native.PASTE_CF_KEYS
+            # one reference per distinct resolution (PASTE_CF_UNIQ)
+            if os.environ.get("PASTE_NO_UNIQ") != "1":
+                self.sformat |= _native.PASTE_CF_UNIQ
 
     def _build_plan(self) -> None:
         """Compile the live plan (paste_build_live_plan: per match-table key,
@@ -331,7 +334,9 @@ class LiveSessionTable:
     def plan_host(self):
         """Host copy of the live plan for expanding PASTE_CF_KEYS streams:
         per key (n_pred, n_act, action codes [keys, K] = slot | level if
-        complete << 8 | level if PARTIAL << 12)."""
+        complete << 8 | level if PARTIAL << 12, n_map, n_units, map words
+        [keys, M] = binding | rank << 32 | bslot << 40 | age << 48 | unit
+        << 56)."""
         if self._plan_host is None:
             buf = self._plan_bufs[0].cpu().numpy()
             K, M = self.K, self.K * max(self.dpool.image.max_bindings, 1)
@@ -339,10 +344,13 @@ class LiveSessionTable:
             off_comp = 16 + 4 * K
             off_act = al(off_comp + K, 16)
             off_util = al(off_act + 2 * K, 8)
-            stride = al(off_util + 8 * K + 8 * M, 16)
+            off_map = off_util + 8 * K
+            stride = al(off_map + 8 * M, 16)
             rows = buf.reshape(-1, stride)
             self._plan_host = (rows[:, 0].astype(np.int64), rows[:, 1].astype(np.int64),
-                               rows[:, off_act:off_act + 2 * K].copy().view(np.uint16))
+                               rows[:, off_act:off_act + 2 * K].copy().view(np.uint16),
+                               rows[:, 2].astype(np.int64), rows[:, 3].astype(np.int64),
+                               rows[:, off_map:off_map + 8 * M].copy().view(np.uint64))
         return self._plan_host
 
     def output_nbytes(self) -> int:
@@ -424,14 +432,15 @@ class CompactRecords:
             pid = self.entries[1][self.pred.astype(np.int64)[sess], slot].astype(np.int64)
             mapped = (patterns["flags"][pid] & 1) != 0
             nb = np.where(mapped, patterns["n_bind"][pid], 0)
-            cu = np.concatenate([[0], np.cumsum(unresolved)])
-            start = np.cumsum(nb) - nb
-            partial = (cu[start + nb] - cu[start]) > 0
-            comp = np.where(mapped, np.where(partial, 1, 0), 2)
             res.pred_pat[sess * K + slot] = pid
-            res.pred_comp[sess * K + slot] = comp.astype(np.uint8)
-            part_at = np.zeros(n * K, bool)
-            part_at[sess * K + slot] = mapped & partial
+            if not self.fmt & _native.PASTE_CF_UNIQ:  # (else from the units, below)
+                cu = np.concatenate([[0], np.cumsum(unresolved)])
+                start = np.cumsum(nb) - nb
+                partial = (cu[start + nb] - cu[start]) > 0
+                comp = np.where(mapped, np.where(partial, 1, 0), 2)
+                res.pred_comp[sess * K + slot] = comp.astype(np.uint8)
+                part_at = np.zeros(n * K, bool)
+                part_at[sess * K + slot] = mapped & partial
         else:
             pshift = 6 if self.fmt & _native.PASTE_CF_PRED8 else 14
             pred = self.pred.astype(np.int64)
@@ -440,11 +449,33 @@ class CompactRecords:
             res.pred_comp[sess * K + slot] = (pred >> pshift).astype(np.uint8)
             mapped = (patterns["flags"][pid] & 1) != 0
             nb = np.where(mapped, patterns["n_bind"][pid], 0)
-        p_sess, p_slot = np.repeat(sess, nb), np.repeat(slot, nb)
-        b_idx = np.arange(int(nb.sum())) - np.repeat(np.cumsum(nb) - nb, nb)
-        ev = (a >> ashift) * n + p_sess
-        res.pred_arg[(p_sess * K + p_slot) * B + b_idx] = np.where(
-            unresolved, -1, (ev << 32) | (a & ((1 << ashift) - 1)))
+        if self.fmt & _native.PASTE_CF_UNIQ:
+            # one reference per resolution unit: binding q of the entry reads
+            # its unit's reference (map word bits 56-63)
+            nmap = np.where(valid, self.plan[3][kk], 0)
+            nu = np.where(valid, self.plan[4][kk], 0)
+            q_sess = np.repeat(np.arange(n), nmap)
+            q_idx = np.arange(len(q_sess)) - np.repeat(np.cumsum(nmap) - nmap, nmap)
+            w = self.plan[5][kk[q_sess], q_idx]
+            rank = ((w >> np.uint64(32)) & np.uint64(0xFF)).astype(np.int64)
+            bslot = ((w >> np.uint64(40)) & np.uint64(0xFF)).astype(np.int64)
+            unit = (w >> np.uint64(56)).astype(np.int64)
+            word = a[(np.cumsum(nu) - nu)[q_sess] + unit]
+            bad = word == (0xFFFF if a16 else 0xFFFFFFFF)
+            part_q = np.zeros(n * K, bool)
+            part_q[(q_sess * K + rank)[bad]] = True
+            comp = np.where(mapped, np.where(part_q[sess * K + slot], 1, 0), 2)
+            res.pred_comp[sess * K + slot] = comp.astype(np.uint8)
+            part_at = part_q
+            ev = (word >> ashift) * n + q_sess
+            res.pred_arg[(q_sess * K + rank) * B + bslot] = np.where(
+                bad, -1, (ev << 32) | (word & ((1 << ashift) - 1)))
+        else:
+            p_sess, p_slot = np.repeat(sess, nb), np.repeat(slot, nb)
+            b_idx = np.arange(int(nb.sum())) - np.repeat(np.cumsum(nb) - nb, nb)
+            ev = (a >> ashift) * n + p_sess
+            res.pred_arg[(p_sess * K + p_slot) * B + b_idx] = np.where(
+                unresolved, -1, (ev << 32) | (a & ((1 << ashift) - 1)))
         a_sess = np.repeat(np.arange(n), n_act)
         a_slot = np.arange(len(a_sess)) - np.repeat(np.cumsum(n_act) - n_act, n_act)
         if keys:  # the entry's admit decisions; PARTIAL predictions at their partial level

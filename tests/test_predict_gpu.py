@@ -14,7 +14,7 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
 
 from oracle import bridge  # noqa: E402
 from paper_2603_18897_b200 import admit  # noqa: E402
-from paper_2603_18897_b200._native import PASTE_CF_ENTRY16, PASTE_CF_KEYS  # noqa: E402
+from paper_2603_18897_b200._native import PASTE_CF_ENTRY16, PASTE_CF_KEYS, PASTE_CF_UNIQ  # noqa: E402
 from paper_2603_18897_b200.device_ops import DevicePool  # noqa: E402
 from paper_2603_18897_b200.live import LiveSessionTable  # noqa: E402
 from paper_2603_18897_b200.mining import load_pool  # noqa: E402
@@ -239,7 +239,7 @@ def test_compact_records_expand_to_the_full_records(fmt):
 @pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3", "wide_format",
                                      "ship_bytes", "pred_stream", "pinned_inputs", "no_plan",
                                      "no_plan_pred_stream", "narrow8", "narrow8_pinned",
-                                     "no_keys"])
+                                     "no_keys", "no_uniq"])
 def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
@@ -282,7 +282,9 @@ def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     else:
         assert pip.sformat & PASTE_CF_ENTRY16
     if variant == "no_keys":
-        pip.sformat &= ~PASTE_CF_KEYS
+        pip.sformat &= ~(PASTE_CF_KEYS | PASTE_CF_UNIQ)
+    if variant == "no_uniq":
+        pip.sformat &= ~PASTE_CF_UNIQ
     steps = 20
     expect, full = [], []
     for _ in range(steps):
@@ -317,6 +319,9 @@ def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
                 continue
             if i in (0, 3) and pip.sformat & PASTE_CF_KEYS:  # no hdr / act streams
                 assert len(y) == 0
+                continue
+            if i == 2 and pip.sformat & PASTE_CF_UNIQ:  # one reference per unit
+                assert len(y) <= len(x)
                 continue
             assert np.array_equal(x, y)
     if variant == "ship_bytes":  # same arena contents
