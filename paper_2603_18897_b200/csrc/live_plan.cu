@@ -212,6 +212,9 @@ struct LiveParams {
   uint32_t* st_part;      // [n] PARTIAL mask
   uint32_t* st_arg;       // [n][M] encoded argument words (stream width applied later)
   int M;
+  // key-stream form: per-warp argument counts and exclusive offsets
+  uint32_t* w_cnt;
+  uint32_t* w_off;
   uint64_t* ticket;
   uint64_t* tile_state;
   int64_t n_tiles;
@@ -851,6 +854,174 @@ __global__ void __launch_bounds__(LT) predict_live_stage_kernel(const LiveParams
 
 constexpr int SCAT_SPT = 4;
 
+// ---- key-stream serving form (PASTE_CF_KEYS) ----------------------------
+// With the key stream only the argument stream has a variable length, and a
+// session's argument count follows from its key.  The step writes each
+// warp's argument words (32 consecutive sessions) contiguously into the
+// warp's staging slot (capacity 32 * M) at the warp-exclusive offsets, and
+// the warp's total; one CTA scans the warp totals (31k per 1M sessions); a
+// copy kernel moves every warp's words to their final offset.  No tile
+// look-back, no CTA-wide barrier in the step.
+struct KeyTotals {
+  unsigned long long nm, na, ne, wide;
+};
+
+template <int G>
+__device__ __forceinline__ void keys_write(const LiveParams& P, const Sess<G>& y, KeyTotals& t) {
+  const int64_t n = P.win.n_sessions;
+  const paste_compact_desc& C = P.C;
+  const int lane = threadIdx.x & 31;
+  const bool live = y.s < n;
+  const int cnt = live ? arg_count(P, y) : 0;
+  int inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  const int64_t w = (y.s - lane) >> 5;  // warp base is a multiple of 32
+  if (lane == 31) P.w_cnt[w] = (uint32_t)inc;
+  if (!live) return;
+  const bool a16 = (C.format & PASTE_CF_ARG16) != 0;
+  if (cnt > 0) {
+    const int64_t at = w * 32 * P.M + (inc - cnt);
+    int q = 0;
+    live_resolve<G>(P, y, [&](int, int, int32_t ev, int64_t cur) {
+      uint32_t wd = a16 ? 0xffffu : 0xffffffffu;
+      if (cur >= 0) {
+        const int64_t region =
+            n < (1ll << 31) ? (int64_t)((uint32_t)ev / (uint32_t)n) : (int64_t)ev / n;
+        if ((int64_t)ev - region * n == y.s && region < 31 && cur < (a16 ? (1ll << 11) : (1ll << 27)))
+          wd = a16 ? (((uint32_t)region << 11) | (uint32_t)cur)
+                   : (((uint32_t)region << 27) | (uint32_t)cur);
+        else
+          ++t.wide;
+      }
+      if (a16) reinterpret_cast<uint16_t*>(P.st_arg)[at + q] = (uint16_t)wd;
+      else P.st_arg[at + q] = wd;
+      ++q;
+    }, (C.format & PASTE_CF_UNIQ) != 0);
+  }
+  static_cast<uint16_t*>(C.pred)[y.s] = y.key >= 0 ? (uint16_t)y.key : (uint16_t)0xffffu;
+  t.nm += (unsigned)y.nm;
+  t.na += (unsigned)y.n_act;
+  t.ne += (unsigned)y.n_err;
+}
+
+template <int G, int MINB>
+__global__ void __launch_bounds__(LT, MINB) predict_live_keys_kernel(const LiveParams P) {
+  const int64_t n = P.win.n_sessions;
+  const int64_t stride = (int64_t)gridDim.x * LT;
+  const int64_t s0 = (int64_t)blockIdx.x * LT + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  KeyTotals t{0, 0, 0, 0};
+  FrontIn f1, f2;
+  Sess<G> y0, y1;
+  FrontMid<G> m0, m1;
+  front_load(P, s0, f1);
+  front_load(P, s0 + stride, f2);
+  front_observe<G>(P, f1, y1, m1);
+  for (int64_t s = s0; s - lane < n; s += stride) {  // warp-uniform: whole warps
+    y0 = y1;
+    m0 = m1;
+    f1 = f2;
+    front_load(P, s + 2 * stride, f2);
+    front_observe<G>(P, f1, y1, m1);
+    front_key<G, false>(P, y0, m0);
+    keys_write<G>(P, y0, t);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t.nm += __shfl_xor_sync(0xffffffffu, t.nm, o);
+    t.na += __shfl_xor_sync(0xffffffffu, t.na, o);
+    t.ne += __shfl_xor_sync(0xffffffffu, t.ne, o);
+    t.wide += __shfl_xor_sync(0xffffffffu, t.wide, o);
+  }
+  if (lane == 0) {
+    unsigned long long* tot = reinterpret_cast<unsigned long long*>(P.C.totals);
+    if (t.nm) atomicAdd(tot + 0, t.nm);
+    if (t.na) atomicAdd(tot + 2, t.na);
+    if (t.wide) atomicAdd(tot + 3, t.wide);
+    if (t.ne) atomicAdd(tot + 4, t.ne);
+  }
+}
+
+// exclusive offsets of the warp totals, one CTA of 1024 threads; each pass
+// covers 32 warps x 1024 values: a warp holds its 1024 values in registers
+// (32 coalesced loads per lane), the CTA scans the 32 warp sums, then each
+// warp scans its values 32 at a time and stores the offsets coalesced
+constexpr int WSCAN_T = 1024, WSCAN_V = 32;
+
+__global__ void __launch_bounds__(WSCAN_T) warp_scan_kernel(const uint32_t* cnt, uint32_t* off,
+                                                            int64_t nw, int64_t* total) {
+  __shared__ uint32_t s_warp[WSCAN_T / 32];
+  __shared__ uint64_t s_carry;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nw; base += (int64_t)WSCAN_T * WSCAN_V) {
+    const int64_t chunk = base + (int64_t)warp * (32 * WSCAN_V);
+    uint32_t v[WSCAN_V];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < WSCAN_V; ++i) {
+      const int64_t at = chunk + i * 32 + lane;
+      v[i] = at < nw ? cnt[at] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < WSCAN_V; ++i) sum += v[i];
+    const uint32_t wsum = __reduce_add_sync(0xffffffffu, sum);
+    if (lane == 0) s_warp[warp] = wsum;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t x = s_warp[lane];
+      uint32_t xi = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, xi, o);
+        if (lane >= o) xi += u;
+      }
+      s_warp[lane] = xi - x;
+    }
+    __syncthreads();
+    uint32_t run = (uint32_t)s_carry + s_warp[warp];
+#pragma unroll
+    for (int i = 0; i < WSCAN_V; ++i) {
+      uint32_t inc = v[i];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      const int64_t at = chunk + i * 32 + lane;
+      if (at < nw) off[at] = run + inc - v[i];
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    __syncthreads();
+    if (threadIdx.x == WSCAN_T - 1) s_carry = run;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) total[1] = (int64_t)s_carry;
+}
+
+// every staged warp's words to their final offset (one warp per staged warp)
+__global__ void __launch_bounds__(LT) warp_copy_kernel(const LiveParams P, int64_t nw) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * LT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * LT) >> 5;
+  const bool a16 = (P.C.format & PASTE_CF_ARG16) != 0;
+  for (int64_t w = gw; w < nw; w += nwarps) {
+    const uint32_t c = P.w_cnt[w], o = P.w_off[w];
+    const int64_t src = w * 32 * P.M;
+    for (uint32_t i = lane; i < c; i += 32) {
+      if (a16)
+        static_cast<uint16_t*>(P.C.arg)[o + i] = reinterpret_cast<const uint16_t*>(P.st_arg)[src + i];
+      else
+        static_cast<uint32_t*>(P.C.arg)[o + i] = P.st_arg[src + i];
+    }
+  }
+}
+
 __global__ void __launch_bounds__(LT) live_scatter_kernel(const LiveParams P) {
   __shared__ int64_t s_tile;
   const int64_t n = P.win.n_sessions;
@@ -1172,18 +1343,42 @@ extern "C" int64_t paste_predict_live_compact_scratch_bytes(int64_t n_sessions,
                                                             int32_t max_candidates,
                                                             int32_t max_bindings) {
   const int64_t M = (int64_t)max_candidates * (max_bindings > 0 ? max_bindings : 1);
-  const int64_t n = n_sessions;
-  return live_state_bytes(n) + 3 * ((4 * n + 255) / 256 * 256) + (4 * n * M + 255) / 256 * 256;
+  const int64_t n = n_sessions, n32 = (n + 31) / 32 * 32;  // warp staging slots: whole warps
+  return live_state_bytes(n) + 3 * ((4 * n + 255) / 256 * 256) + (4 * n32 * M + 255) / 256 * 256;
 }
 
-static int live_mode_impl() {  // 0 two-pass (default), 1 ticket tiles, 2 pipelined static tiles
+// 0 two-pass (default; the key-stream form runs the warp-staged kernels),
+// 1 ticket tiles, 2 pipelined static tiles, 3 two-pass with the tile
+// look-back scatter for the key-stream form too
+static int live_mode_impl() {
   static int m = -1;
   if (m < 0) {
     const char* e = getenv("PASTE_LIVE_MODE");
-    m = !e ? 0 : !strcmp(e, "ticket") ? 1 : !strcmp(e, "pipe") ? 2 : 0;
+    m = !e ? 0 : !strcmp(e, "ticket") ? 1 : !strcmp(e, "pipe") ? 2 : !strcmp(e, "scatter") ? 3 : 0;
     if (live_ticket()) m = 1;
   }
   return m;
+}
+
+template <int G>
+static void launch_keys(const LiveParams& P, cudaStream_t st) {
+  static int sms = 0, o1 = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, predict_live_keys_kernel<G, 7>, LT, 0);
+    if (o1 < 1) o1 = 1;
+  }
+  const int64_t n = P.win.n_sessions;
+  const int64_t nw = (n + 31) / 32;
+  const int64_t g1 = (n + LT - 1) / LT;
+  predict_live_keys_kernel<G, 7><<<(unsigned)(g1 < (int64_t)sms * o1 ? g1 : (int64_t)sms * o1), LT,
+                                   0, st>>>(P);
+  warp_scan_kernel<<<1, WSCAN_T, 0, st>>>(P.w_cnt, P.w_off, nw, P.C.totals);
+  // one warp per staged warp: every copy's loads are in flight at once
+  const int64_t g3 = (nw * 32 + LT - 1) / LT;
+  warp_copy_kernel<<<(unsigned)(g3 < (1ll << 31) - 1 ? g3 : (1ll << 31) - 1), LT, 0, st>>>(P, nw);
 }
 
 static int live_mode() { return live_mode_impl(); }
@@ -1234,7 +1429,7 @@ extern "C" int paste_predict_live_compact(const paste_pool_desc* pool, paste_win
   PASTE_REQUIRE(scratch_bytes >= need, "scratch too small (%lld bytes)", (long long)need);
   P.C = *c;
   const int mode = live_mode();
-  const int spt = mode == 1 ? live_spt() : mode == 0 ? SCAT_SPT : 1;
+  const int spt = mode == 1 ? live_spt() : (mode == 0 || mode == 3) ? SCAT_SPT : 1;
   P.n_tiles = (n + LT * spt - 1) / (LT * spt);
   P.ticket = static_cast<uint64_t*>(scratch);
   P.tile_state = static_cast<uint64_t*>(scratch) + LB_STRIDE;
@@ -1245,12 +1440,20 @@ extern "C" int paste_predict_live_compact(const paste_pool_desc* pool, paste_win
   P.st_part = reinterpret_cast<uint32_t*>(stg + 2 * a4);
   P.st_arg = reinterpret_cast<uint32_t*>(stg + 3 * a4);
   P.M = K * (max_bindings > 0 ? max_bindings : 1);
+  P.w_cnt = reinterpret_cast<uint32_t*>(stg);        // key-stream form: [n / 32]
+  P.w_off = reinterpret_cast<uint32_t*>(stg + a4);
   cudaStream_t st = (cudaStream_t)stream;
-  PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, 8 * (LB_STRIDE * P.n_tiles + LB_STRIDE), st));
+  const bool keys_form = mode == 0 && (c->format & PASTE_CF_KEYS) &&
+                         ((n + 31) / 32) * 32 * (int64_t)P.M < (1ll << 32);
+  if (!keys_form)
+    PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, 8 * (LB_STRIDE * P.n_tiles + LB_STRIDE), st));
   PASTE_CUDA_CHECK(cudaMemsetAsync(c->totals, 0, 5 * sizeof(int64_t), st));
   if (n == 0) return PASTE_OK;
   const int G = live_gather_depth(pool, windows->capacity);
-  if (mode == 0) {
+  if (keys_form) {
+    by_depth(G, [&](auto g) { launch_keys<decltype(g)::value>(P, st); });
+    count_launch(3);
+  } else if (mode == 0 || mode == 3) {
     by_depth(G, [&](auto g) { launch_two_pass<decltype(g)::value>(P, st); });
     count_launch(2);
   } else {

@@ -29,6 +29,13 @@ from .device_ops import DevicePool, stream_handle, to_dev
 from .packing import PredictResult, admit_tables
 
 
+def wire8_layout(n: int) -> tuple[int, int]:
+    """(byte offset of node16, total bytes) of the packed 3-byte wire form:
+    tok8 [n] | pad to 16 | node16 [n]."""
+    off = (n + 15) // 16 * 16
+    return off, off + 2 * n
+
+
 @dataclass
 class EventBatch:
     """One new tool event per session: tokens, batch-relative directory
@@ -40,22 +47,45 @@ class EventBatch:
     node: object = None  # optional i32[n]: node_base only (the narrow wire form)
     tok8: object = None    # optional u8[n]: token, 255 = LLM step (the 3-byte wire form)
     node16: object = None  # optional u16[n]: node_base
+    packed: object = None  # optional u8: tok8 and node16 in one buffer (wire8_layout)
 
     def narrowed(self) -> "EventBatch":
         """The 3-byte wire form (u8 token + u16 node_base) alongside the
-        others, when the values fit (signature ids < 255, node bases < 2^16)."""
+        others, when the values fit (signature ids < 255, node bases < 2^16):
+        both in one buffer (`packed`, wire8_layout), so a step uploads them
+        with one copy."""
         tok = np.asarray(self.tok)
         node = np.asarray(self.node if self.node is not None else np.asarray(self.ref)[:, 0])
         if tok.size and (tok.max() >= 255 or node.max() >= (1 << 16) or node.min() < 0):
             return self
-        return EventBatch(self.tok, self.ref, self.data, self.node,
-                          np.where(tok < 0, 255, tok).astype(np.uint8),
-                          node.astype(np.uint16))
+        n = len(tok)
+        off, size = wire8_layout(n)
+        packed = np.zeros(size, np.uint8)
+        tok8 = packed[:n]
+        node16 = packed[off:off + 2 * n].view(np.uint16)
+        tok8[:] = np.where(tok < 0, 255, tok)
+        node16[:] = node
+        return EventBatch(self.tok, self.ref, self.data, self.node, tok8, node16, packed)
+
+    def pin(self) -> "EventBatch":
+        """Move the 3-byte wire form into pinned host memory (one buffer, with
+        tok8 / node16 as views), for the asynchronous single-copy upload."""
+        import torch
+
+        if self.packed is not None and isinstance(self.packed, np.ndarray):
+            n = len(self.tok8)
+            off, _ = wire8_layout(n)
+            self.packed = torch.from_numpy(self.packed).pin_memory()
+            self.tok8 = self.packed[:n]
+            self.node16 = self.packed[off:off + 2 * n].view(torch.int16)
+        return self
 
     def wire(self, ship_bytes: bool, narrow8: bool = False) -> tuple:
         """The arrays a step copies host -> device."""
         if ship_bytes:
             return (self.tok, self.ref, self.data)
+        if narrow8 and self.packed is not None:
+            return (self.packed,)
         if narrow8 and self.tok8 is not None:
             return (self.tok8, self.node16)
         return (self.tok, self.node) if self.node is not None else (self.tok, self.ref)
@@ -500,6 +530,8 @@ def _compact_buffers(table: "LiveSessionTable", f: int | None = None):
     f = table.cformat if f is None else f
     dev = t.device("cuda")
     entry = bool(f & _native.PASTE_CF_ENTRY16)
+    if f & _native.PASTE_CF_KEYS:  # totals | keys | args in one buffer: one download copy
+        return _keys_buffers(t, n * K * B, n, bool(f & _native.PASTE_CF_ARG16), dev)
     return {"hdr": t.zeros(n, dtype=t.uint8 if f & _native.PASTE_CF_HDR8 else t.int16, device=dev),
             "pred": t.zeros(n if entry else n * K,
                             dtype=t.uint8 if f & _native.PASTE_CF_PRED8 and not entry else t.int16,
@@ -508,6 +540,26 @@ def _compact_buffers(table: "LiveSessionTable", f: int | None = None):
                            device=dev),
             "act": t.zeros(n * K, dtype=t.uint8, device=dev),
             "totals": t.zeros(5, dtype=t.int64, device=dev)}
+
+
+def keys_layout(n: int, arg_cap: int, a16: bool) -> tuple[int, int, int]:
+    """Byte offsets of the key-stream buffer: totals (5 x i64) at 0, the
+    u16 keys at `k_off`, the argument words at `a_off`; `size` in total."""
+    k_off = 64
+    a_off = (k_off + 2 * n + 63) // 64 * 64
+    return k_off, a_off, a_off + arg_cap * (2 if a16 else 4)
+
+
+def _keys_buffers(t, arg_cap: int, n: int, a16: bool, dev, pinned: bool = False) -> dict:
+    k_off, a_off, size = keys_layout(n, arg_cap, a16)
+    blob = (t.empty(size, dtype=t.uint8, pin_memory=True) if pinned
+            else t.zeros(size, dtype=t.uint8, device=dev))
+    z = (lambda m, dt: t.empty(m, dtype=dt, pin_memory=True)) if pinned else \
+        (lambda m, dt: t.zeros(m, dtype=dt, device=dev))
+    return {"blob": blob, "totals": blob[:40].view(t.int64),
+            "pred": blob[k_off:k_off + 2 * n].view(t.int16),
+            "arg": blob[a_off:a_off + arg_cap * (2 if a16 else 4)].view(t.int16 if a16 else t.int32),
+            "hdr": z(16, t.int16), "act": z(16, t.uint8)}  # not written in this form
 
 
 def _compact_desc(c: dict, fmt: int = 0):
@@ -571,60 +623,78 @@ _STREAMS = ("hdr", "pred", "arg", "act")
 
 def _serve_state(table, depth: int, fmt: int) -> dict:
     """Buffer sets, pinned mirrors, numpy views, copy lists and reusable
-    events of the serving loop (built once per (depth, format))."""
+    events of the serving loop (built once per (depth, format)): `depth`
+    device sets, `2 * depth` pinned host sets (records are handed out
+    depth - 1 steps behind the launches, and a yielded record's pinned set
+    is not overwritten until the generator has advanced depth - 1 more
+    steps)."""
     t = table.torch
     bufs = [_compact_buffers(table, fmt) for _ in range(depth)]
-    pinned = [{k: t.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in c.items()}
-              for c in bufs]
+    keys = bool(fmt & _native.PASTE_CF_KEYS)
+    if keys:
+        pinned = [_keys_buffers(t, bufs[0]["arg"].numel(), table.n,
+                                bool(fmt & _native.PASTE_CF_ARG16), None, pinned=True)
+                  for _ in range(2 * depth)]
+    else:
+        pinned = [{k: t.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                   for k, v in bufs[0].items()} for _ in range(2 * depth)]
     entry = bool(fmt & _native.PASTE_CF_ENTRY16)
     vdt = {"hdr": np.uint8 if fmt & _native.PASTE_CF_HDR8 else np.uint16,
            "pred": np.uint8 if fmt & _native.PASTE_CF_PRED8 and not entry else np.uint16,
            "arg": np.uint16 if fmt & _native.PASTE_CF_ARG16 else np.uint32, "act": np.uint8}
-    sets = []
-    for c, h in zip(bufs, pinned):
-        sets.append({
-            "views": {k: h[k].numpy().view(vdt[k]) for k in _STREAMS},
-            "totals": h["totals"].numpy(),
-            "dst": (ctypes.c_void_p * 4)(*[h[k].data_ptr() for k in _STREAMS]),
-            "src": (ctypes.c_void_p * 4)(*[c[k].data_ptr() for k in _STREAMS]),
-            "esize": [c[k].element_size() for k in _STREAMS],
-            "tot_dst": (ctypes.c_void_p * 1)(h["totals"].data_ptr()),
-            "tot_src": (ctypes.c_void_p * 1)(c["totals"].data_ptr()),
-            "tot_bytes": (ctypes.c_int64 * 1)(5 * 8),
-            "bytes": (ctypes.c_int64 * 4)()})
+    names = ("totals",) + _STREAMS
+    hsets = [{"views": {k: h[k].numpy().view(vdt[k]) for k in _STREAMS},
+              "totals": h["totals"].numpy(),
+              "dst": (ctypes.c_void_p * 5)(*[h[k].data_ptr() for k in names]),
+              "ptr": {k: h[k].data_ptr() for k in names},
+              "base": h["blob"].data_ptr() if keys else None}
+             for h in pinned]
+    dsets = [{"src": (ctypes.c_void_p * 5)(*[c[k].data_ptr() for k in names]),
+              "ptr": {k: c[k].data_ptr() for k in names},
+              "esize": [c[k].element_size() for k in _STREAMS],
+              "cap": [c[k].numel() for k in _STREAMS],
+              "base": c["blob"].data_ptr() if keys else None}
+             for c in bufs]
     return {
         "fmt": fmt, "bufs": bufs, "descs": [_compact_desc(c, fmt) for c in bufs],
-        "pinned": pinned, "sets": sets,
+        "pinned": pinned, "hsets": hsets, "dsets": dsets,
+        "bytes": (ctypes.c_int64 * 5)(),
+        "bound": [None] * 4,  # per variable stream: elements the async download copies
         "scratch": [t.empty(table.compact_scratch_bytes(),
                             dtype=t.uint8, device="cuda") for _ in range(depth)],
-        "copy": t.cuda.Stream(), "tot": t.cuda.Stream(), "up": t.cuda.Stream(),
+        "copy": t.cuda.Stream(), "up": t.cuda.Stream(), "sup": t.cuda.Stream(),
         "free": [None] * depth, "in_free": [None] * depth,
         "ev_ready": [t.cuda.Event() for _ in range(depth)],
-        "ev_tot": [t.cuda.Event() for _ in range(depth)],
         "ev_up": [t.cuda.Event() for _ in range(depth)],
         "wins": {},
-        "in": [{"tok8": t.zeros(table.n, dtype=t.uint8, device="cuda"),
-                "node16": t.zeros(table.n, dtype=t.int16, device="cuda"),
-                "tok": t.zeros(table.n, dtype=t.int32, device="cuda"),
-                "node": t.zeros(table.n, dtype=t.int32, device="cuda"),
-                "ref": t.zeros(2 * table.n, dtype=t.int64, device="cuda")}
-               for _ in range(depth)]}
+        "in": [_in_set(t, table.n) for _ in range(depth)]}
+
+
+def _in_set(t, n: int) -> dict:
+    off, size = wire8_layout(n)
+    packed = t.zeros(size, dtype=t.uint8, device="cuda")
+    return {"packed": packed, "tok8": packed[:n], "node16": packed[off:off + 2 * n].view(t.int16),
+            "tok": t.zeros(n, dtype=t.int32, device="cuda"),
+            "node": t.zeros(n, dtype=t.int32, device="cuda"),
+            "ref": t.zeros(2 * n, dtype=t.int64, device="cuda")}
 
 
 def serve(table: "LiveSessionTable", batches, depth: int = 4):
-    """Pipelined live steps (the serving loop).  Step i's inputs upload on
-    an upload stream into their own staging set while step i-1's fused
-    predict + compaction kernel runs; the kernel and the totals read run on
-    the compute stream; step i-1's sized record download is queued on a copy
-    stream while step i-2's records are handed out -- so the two copy
-    engines and the SMs overlap and never wait on the host.  The host side
-    is kept thin (the loop is host-bound otherwise): each step's copies go
-    out as one ``paste_memcpy_batch`` call per direction, window descriptors
-    are cached per (buffer set, arena region) and events are reused.  Yields
-    each step's CompactRecords in order (``records.downloaded`` is the
-    device event of its download); a yielded record's arrays are
-    pinned-buffer views, valid until the generator has advanced ``depth - 1``
-    more steps."""
+    """Pipelined live steps (the serving loop).  Step i+1's inputs upload on
+    an upload stream into their own staging set while step i's fused
+    predict + compaction kernel runs on the compute stream; step i's
+    download is queued on a copy stream right behind its kernel, with no
+    host round trip: the variable-length streams are copied up to a bound
+    (the largest recent count plus a margin) together with the step's
+    totals, and the rare step that outgrows its bound fetches the rest when
+    it is handed out.  So the two copy engines and the SMs overlap and the
+    host only waits for records it hands out.  The host side is kept thin:
+    each step's copies go out as one ``paste_memcpy_batch`` call per
+    direction, window descriptors are cached per (buffer set, arena region)
+    and events are reused.  Yields each step's CompactRecords in order
+    (``records.downloaded`` is the device event of its download); a yielded
+    record's arrays are pinned-buffer views, valid until the generator has
+    advanced ``depth - 1`` more steps."""
     from collections import deque
 
     if depth < 3:
@@ -636,40 +706,93 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
             or table._serve["fmt"] != fmt):
         table._serve = _serve_state(table, depth, fmt)
     sv = table._serve
-    comp, copy, tot, up = t.cuda.current_stream(), sv["copy"], sv["tot"], sv["up"]
-    comp_h, copy_h, tot_h, up_h = (s.cuda_stream for s in (comp, copy, tot, up))
+    comp, copy, up = t.cuda.current_stream(), sv["copy"], sv["up"]
+    comp_h, copy_h, up_h = (s.cuda_stream for s in (comp, copy, up))
     entries = table.entries() if fmt & _native.PASTE_CF_ENTRY16 else None
     plan = table.plan_host() if fmt & _native.PASTE_CF_KEYS else None
     n = table.n
-    tot_q, copy_q = deque(), deque()
+    keys = bool(fmt & _native.PASTE_CF_KEYS)  # counts / actions follow from the key
+    # stream sizes fixed by the format (None = variable, from the totals)
+    fixed = (0 if keys else n, n if fmt & _native.PASTE_CF_ENTRY16 else None, None,
+             0 if keys else None)
+    bound = sv["bound"]
+    margin = getattr(table, "serve_bound_margin", None)
+    copy_q = deque()
     H2D, D2H = _native.PASTE_COPY_H2D, _native.PASTE_COPY_D2H
+    nh = 2 * depth  # pinned sets: a handed-out record outlives depth - 1 more steps
+    a_off = keys_layout(n, 0, True)[1] if keys else 0
 
-    def download(k):
-        sv["ev_tot"][k].synchronize()
-        st = sv["sets"][k]
-        P, A, Q, wide, _err = (int(x) for x in st["totals"])
-        if wide:
-            raise _native.PasteError(f"{wide} argument refs outside the live table's event "
-                                     "form: use fetch()")
-        keys = bool(fmt & _native.PASTE_CF_KEYS)  # counts / actions follow from the key
-        sizes = (0 if keys else n, n if fmt & _native.PASTE_CF_ENTRY16 else P, A,
-                 0 if keys else Q)
-        nb = st["bytes"]
+    def actual_sizes(tot):
+        P, A, Q = int(tot[0]), int(tot[1]), int(tot[2])
+        return [fixed[0], fixed[1] if fixed[1] is not None else P, A,
+                fixed[3] if fixed[3] is not None else Q]
+
+    def download(k, h, step):
+        """Queue step's download (device set k -> pinned set h) behind its
+        kernel on the copy stream."""
+        ds, hs = sv["dsets"][k], sv["hsets"][h]
+        copy.wait_event(sv["ev_ready"][k])
+        nb = sv["bytes"]
+        nb[0] = 5 * 8
+        if any(bound[j] is None for j in range(4) if fixed[j] is None):
+            # no bound yet: the sizes come from this step's totals (host round trip)
+            check(lib.paste_memcpy_batch(1, hs["dst"], ds["src"], nb, D2H, copy_h), lib)
+            copy.synchronize()
+            sizes = actual_sizes(hs["totals"])
+        else:
+            sizes = [fixed[j] if fixed[j] is not None else min(bound[j], ds["cap"][j])
+                     for j in range(4)]
         for j in range(4):
-            nb[j] = sizes[j] * st["esize"][j]
-        check(lib.paste_memcpy_batch(4, st["dst"], st["src"], nb, D2H, copy_h), lib)
+            nb[1 + j] = sizes[j] * ds["esize"][j]
+        if trace is not None:
+            trace[step]["d0"] = _tev(t, copy)
+        if keys:  # totals | keys | args[:bound]: one contiguous copy
+            one = (ctypes.c_int64 * 1)(a_off + nb[3])
+            copied = int(one[0])
+            check(lib.paste_memcpy_batch(1, (ctypes.c_void_p * 1)(hs["base"]),
+                                         (ctypes.c_void_p * 1)(ds["base"]), one, D2H, copy_h), lib)
+        else:
+            check(lib.paste_memcpy_batch(5, hs["dst"], ds["src"], nb, D2H, copy_h), lib)
+            copied = sum(int(nb[j]) for j in range(5))
         done = t.cuda.Event(enable_timing=True)
         done.record(copy)
+        if trace is not None:
+            trace[step]["d1"] = done
         sv["free"][k] = done
-        copy_q.append((k, sizes, done))
+        copy_q.append((k, h, sizes, done, copied))
 
     def hand_out():
-        k, sizes, done = copy_q.popleft()
+        k, h, sizes, done, copied = copy_q.popleft()
         done.synchronize()
-        v = sv["sets"][k]["views"]
-        rec = CompactRecords(table.K, table.B, v["hdr"][:sizes[0]], v["pred"][:sizes[1]],
-                             v["arg"][:sizes[2]], v["act"][:sizes[3]], fmt, entries, plan)
+        hs, ds = sv["hsets"][h], sv["dsets"][k]
+        tot = hs["totals"]
+        if int(tot[3]):
+            raise _native.PasteError(f"{int(tot[3])} argument refs outside the live table's "
+                                     "event form: use fetch()")
+        need = actual_sizes(tot)
+        for j, name in enumerate(_STREAMS):
+            if fixed[j] is not None:
+                continue
+            if need[j] > sizes[j]:  # outgrew the bound: fetch the rest (device set k is
+                es = ds["esize"][j]  # not reused before this step's download is done)
+                nb1 = (ctypes.c_int64 * 1)((need[j] - sizes[j]) * es)
+                sup = sv["sup"]  # its own stream: not behind later steps' downloads
+                check(lib.paste_memcpy_batch(
+                    1, (ctypes.c_void_p * 1)(hs["ptr"][name] + sizes[j] * es),
+                    (ctypes.c_void_p * 1)(ds["ptr"][name] + sizes[j] * es), nb1, D2H,
+                    sup.cuda_stream), lib)
+                sup.synchronize()
+                copied += int(nb1[0])
+                sv["supplements"] = sv.get("supplements", 0) + 1
+            # the bound follows the largest recent count with 1/8 headroom
+            # (a step past it costs a synchronous fetch of the rest)
+            grow = need[j] + (need[j] >> 3) + 4096 if margin is None else int(margin)
+            bound[j] = grow if bound[j] is None else max(grow, (bound[j] * 63) // 64)
+        v = hs["views"]
+        rec = CompactRecords(table.K, table.B, v["hdr"][:need[0]], v["pred"][:need[1]],
+                             v["arg"][:need[2]], v["act"][:need[3]], fmt, entries, plan)
         rec.downloaded = done  # device event: this step's records are on the host
+        rec.wire_bytes = copied  # bytes this step's download moved (bound slack included)
         return rec
 
     def upload(i, b):
@@ -679,11 +802,15 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         region = (steps0 + i) % table.regions  # the arena region step i will use
         if sv["in_free"][k] is not None:
             up.wait_event(sv["in_free"][k])
+        if trace is not None:
+            trace.append({"u0": _tev(t, up)})
         st = sv["in"][k]
         narrow = b.node is not None and not table.ship_bytes
         if table.narrow8 and table.serve_fused and b.tok8 is not None:  # 3 B per session
             narrow = 8
-            wire = [(st["tok8"], b.tok8), (st["node16"], b.node16)]
+            wire = ([(st["packed"], b.packed)]
+                    if isinstance(b.packed, t.Tensor) and b.packed.numel() == st["packed"].numel()
+                    else [(st["tok8"], b.tok8), (st["node16"], b.node16)])
         else:
             wire = [(st["tok"], b.tok), (st["node"], b.node) if narrow else (st["ref"], b.ref)]
         if all(isinstance(x, t.Tensor) and not x.is_cuda and x.is_pinned() for _, x in wire):
@@ -705,6 +832,8 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
                                                                 non_blocking=True)
         ev = sv["ev_up"][k]
         ev.record(up)
+        if trace is not None:
+            trace[-1]["u1"] = _tev(t, up)
         return ev, narrow
 
     def launch_fused(k, region, st, narrow) -> bool:
@@ -738,6 +867,7 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         check(rc, lib)
         return True
 
+    trace = getattr(table, "serve_trace", None)  # development: per-step timing events
     it = iter(batches)
     steps0 = table.steps
     nxt = next(it, None)
@@ -745,6 +875,8 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
     i = 0
     while staged is not None:
         k = i % depth
+        h = sv.setdefault("hnext", 0)  # pinned sets rotate across serve() calls
+        sv["hnext"] = (h + 1) % nh
         uploaded, narrow = staged
         region = table.steps % table.regions
         st = sv["in"][k]
@@ -753,6 +885,8 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         comp.wait_event(uploaded)
         node_in = st["node"] if narrow else None
         ref_in = None if narrow else st["ref"]
+        if trace is not None:
+            trace[i]["k0"] = _tev(t, comp)
         fused = table.serve_fused and launch_fused(k, region, st, narrow)
         if not fused:
             if fmt & _native.PASTE_CF_ENTRY16:
@@ -763,27 +897,26 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
                                             ctypes.byref(sv["descs"][k]),
                                             ptr(sv["scratch"][k]), comp_h), lib)
         table.steps += 1
+        if trace is not None:
+            trace[i]["k1"] = _tev(t, comp)
         ready = sv["ev_ready"][k]
         ready.record(comp)
         sv["in_free"][k] = ready
-        tot.wait_event(ready)
-        s_k = sv["sets"][k]
-        check(lib.paste_memcpy_batch(1, s_k["tot_dst"], s_k["tot_src"], s_k["tot_bytes"], D2H,
-                                     tot_h), lib)
-        sv["ev_tot"][k].record(tot)
-        tot_q.append(k)
+        download(k, h, i)
         # the next step's upload goes out now, before the host waits on anything
         nxt = next(it, None)
         staged = upload(i + 1, nxt) if nxt is not None else None
         i += 1
-        if len(tot_q) > 1:
-            download(tot_q.popleft())
-        if len(copy_q) > 1:
+        if len(copy_q) > depth - 1:  # hand out step i - depth + 1
             yield hand_out()
-    while tot_q:
-        download(tot_q.popleft())
     while copy_q:
         yield hand_out()
+
+
+def _tev(t, stream):
+    e = t.cuda.Event(enable_timing=True)
+    e.record(stream)
+    return e
 
 
 LiveSessionTable.serve = serve

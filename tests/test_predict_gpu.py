@@ -239,7 +239,7 @@ def test_compact_records_expand_to_the_full_records(fmt):
 @pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3", "wide_format",
                                      "ship_bytes", "pred_stream", "pinned_inputs", "no_plan",
                                      "no_plan_pred_stream", "narrow8", "narrow8_pinned",
-                                     "no_keys", "no_uniq"])
+                                     "no_keys", "no_uniq", "tight_bound"])
 def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
@@ -285,6 +285,8 @@ def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
         pip.sformat &= ~(PASTE_CF_KEYS | PASTE_CF_UNIQ)
     if variant == "no_uniq":
         pip.sformat &= ~PASTE_CF_UNIQ
+    if variant == "tight_bound":  # every step outgrows its download bound: the rest is fetched
+        pip.serve_bound_margin = 64
     steps = 20
     expect, full = [], []
     for _ in range(steps):
@@ -303,8 +305,7 @@ def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
                 b.node = torch.from_numpy(b.node).pin_memory()
                 b.ref = torch.from_numpy(np.ascontiguousarray(b.ref)).pin_memory()
                 if b.tok8 is not None:
-                    b.tok8 = torch.from_numpy(b.tok8).pin_memory()
-                    b.node16 = torch.from_numpy(b.node16.view(np.int16)).pin_memory()
+                    b.pin()
             yield b
 
     got = []
