@@ -290,8 +290,10 @@ def run_ours(args):
     # two batches past the timed ones keep the pipeline full at the end
     host_batches = []
     for i in range(W_ + S_ + 2):
-        b = wl.next_batch().narrowed()  # u8 token + u16 node_base on the wire when they fit
-        b.pin()  # ... in one pinned buffer: one upload copy per step
+        # u8 token + u8 node code (the table's NodeCodes) on the wire when they
+        # fit, in one pinned buffer: one upload copy per step
+        b = wl.next_batch().narrowed(table.codes)
+        b.pin()
         b.tok = torch.from_numpy(b.tok).pin_memory()
         b.ref = torch.from_numpy(np.ascontiguousarray(b.ref)).pin_memory()
         b.data = torch.from_numpy(b.data).pin_memory()
@@ -348,7 +350,8 @@ def run_ours(args):
                     if table.sformat & 16 else
                     "per-session match-table key + refs + actions"
                     if table.sformat & 8 else "per-prediction codes + refs + actions"),
-                "inputs": "u8 token + u16 node_base per session" if table.narrow8
+                "inputs": ("u8 token + u8 node code per session" if host_batches[-1].node8 is not None
+                           else "u8 token + u16 node_base per session") if table.narrow8
                 else "i32 token + i32 node_base per session"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": committed_traffic(),

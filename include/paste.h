@@ -159,6 +159,11 @@ typedef struct {
    * when set they replace new_tok / new_node                               */
   const uint8_t* new_tok8;
   const uint16_t* new_node16;
+  /* optional 2-byte wire form (with new_tok8, instead of new_node16): a u8
+   * node code per session and the code -> node_base table [256]; the caller
+   * assigns codes to the node arrays (payload shapes) it has seen          */
+  const uint8_t* new_node8;
+  const int32_t* node_codes;
 } paste_windows;
 
 enum { PASTE_C_FULL = 0, PASTE_C_PARTIAL = 1, PASTE_C_TOOL_ONLY = 2 };

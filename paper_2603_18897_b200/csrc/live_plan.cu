@@ -278,9 +278,9 @@ __device__ __forceinline__ void front_load(const LiveParams& P, int64_t s, Front
   f.s = s;
   if (s >= P.win.n_sessions) return;
   f.cnt = P.win.count[s];
-  if (P.win.new_tok8 != nullptr) {  // narrow wire form: u8 token, u16 node
+  if (P.win.new_tok8 != nullptr) {  // narrow wire form: u8 token, u16 node or u8 node code
     f.t = P.win.new_tok8[s];
-    f.node = P.win.new_node16[s];
+    f.node = P.win.new_node8 != nullptr ? (int32_t)P.win.new_node8[s] : (int32_t)P.win.new_node16[s];
     return;
   }
   f.t = P.win.new_tok[s];
@@ -321,7 +321,8 @@ __device__ __forceinline__ void front_observe(const LiveParams& P, const FrontIn
                                          : (int)(f.cnt % W);
   y.ev0 = (int32_t)(P.win.new_evt_base + f.s);
   const bool narrow = P.win.new_node != nullptr || P.win.new_tok8 != nullptr;
-  y.node0 = narrow ? (int64_t)f.node : f.ref.node_base;
+  y.node0 = narrow ? (int64_t)(P.win.new_node8 != nullptr ? __ldg(P.win.node_codes + f.node) : f.node)
+                   : f.ref.node_base;
   P.win.refs[y.ev0] =
       paste_event_ref{y.node0, (narrow ? 0 : f.ref.byte_base) + P.win.new_byte_base};
   P.win.tok[rbase + head * rstride] = t_in;
@@ -1283,7 +1284,8 @@ static int live_prepare(const paste_pool_desc* pool, paste_windows* w, const pas
                         const paste_live_plan* plan, int K, LiveParams& P) {
   PASTE_REQUIRE(pool && w && adm && plan && plan->plan, "null argument");
   PASTE_REQUIRE((w->new_tok != nullptr && (w->new_ref || w->new_node)) ||
-                    (w->new_tok8 != nullptr && w->new_node16 != nullptr),
+                    (w->new_tok8 != nullptr &&
+                     (w->new_node16 != nullptr || (w->new_node8 != nullptr && w->node_codes != nullptr))),
                 "the live kernel observes one new event per session");
   PASTE_REQUIRE(!w->stream_end, "stream-mode windows are not live sessions");
   PASTE_REQUIRE(w->capacity >= 1 && w->capacity <= 16, "live plan needs window capacity <= 16");

@@ -252,7 +252,7 @@ extern "C" int paste_predict_batch(const paste_pool_desc* pool, paste_windows* w
   PASTE_REQUIRE(out->max_bindings >= pool->max_bindings, "max_bindings below pool maximum");
   PASTE_REQUIRE(pool->k >= 1, "k must be >= 1");
   PASTE_REQUIRE(!(windows->stream_end && windows->new_tok), "stream-mode windows cannot observe");
-  PASTE_REQUIRE(!windows->new_tok8 && !windows->new_node16,
+  PASTE_REQUIRE(!windows->new_tok8 && !windows->new_node16 && !windows->new_node8,
                 "the narrow observe form needs the live-plan kernel (paste_predict_live)");
   {
     const int g = pool->relation == PASTE_REL_ANCHORED ? pool->k : pool->max_ctx;

@@ -1068,7 +1068,7 @@ extern "C" int paste_predict_compact(const paste_pool_desc* pool, paste_windows*
   PASTE_REQUIRE(windows->capacity >= 1 && max_candidates >= 1, "bad window / candidate count");
   PASTE_REQUIRE(max_bindings >= pool->max_bindings, "max_bindings below pool maximum");
   PASTE_REQUIRE(!windows->stream_end, "stream-mode windows are not live sessions");
-  PASTE_REQUIRE(!windows->new_tok8 && !windows->new_node16 && !(out->format & PASTE_CF_KEYS),
+  PASTE_REQUIRE(!windows->new_tok8 && !windows->new_node16 && !windows->new_node8 && !(out->format & PASTE_CF_KEYS),
                 "narrow observe form / PASTE_CF_KEYS need paste_predict_live_compact");
   cudaStream_t st = (cudaStream_t)stream;
   PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, paste_predict_compact_scratch_bytes(windows->n_sessions), st));

@@ -29,11 +29,50 @@ from .device_ops import DevicePool, stream_handle, to_dev
 from .packing import PredictResult, admit_tables
 
 
-def wire8_layout(n: int) -> tuple[int, int]:
-    """(byte offset of node16, total bytes) of the packed 3-byte wire form:
-    tok8 [n] | pad to 16 | node16 [n]."""
+def wire8_layout(n: int, node_bytes: int = 2) -> tuple[int, int]:
+    """(byte offset of the node half, total bytes) of the packed narrow wire
+    form: tok8 [n] | pad to 16 | node16 [n] (node_bytes 2) or node8 [n] (1)."""
     off = (n + 15) // 16 * 16
-    return off, off + 2 * n
+    return off, off + node_bytes * n
+
+
+class NodeCodes:
+    """u8 codes for the node arrays (payload shapes) of a live table's
+    events: the 2-byte wire form (u8 token + u8 node code), decoded on the
+    device through a 256-entry code -> node_base table.  Codes are only ever
+    appended, so steps in flight keep their meaning; past 256 node arrays
+    encode() returns None and batches keep the 3-byte form."""
+
+    def __init__(self):
+        import torch
+
+        self.lut = np.full(1 << 16, -1, np.int16)  # node_base -> code
+        self.host = torch.zeros(256, dtype=torch.int32).pin_memory()
+        self.dev = torch.zeros(256, dtype=torch.int32, device="cuda")
+        self.n = 0
+        self.uploaded = 0
+
+    def encode(self, node: np.ndarray) -> np.ndarray | None:
+        code = self.lut[node]
+        missing = code < 0
+        if missing.any():
+            new = np.unique(node[missing])
+            if self.n + len(new) > 256:
+                return None
+            self.lut[new] = np.arange(self.n, self.n + len(new), dtype=np.int16)
+            self.host.numpy()[self.n:self.n + len(new)] = new
+            self.n += len(new)
+            code = self.lut[node]
+        return code.astype(np.uint8)
+
+    def upload(self, stream) -> None:
+        """Queue the table's new entries host -> device on `stream`."""
+        import torch
+
+        if self.n > self.uploaded:
+            with torch.cuda.stream(stream):
+                self.dev[:self.n].copy_(self.host[:self.n], non_blocking=True)
+            self.uploaded = self.n
 
 
 @dataclass
@@ -45,31 +84,40 @@ class EventBatch:
     ref: object   # i64[n, 2]
     data: object  # u8[bytes]
     node: object = None  # optional i32[n]: node_base only (the narrow wire form)
-    tok8: object = None    # optional u8[n]: token, 255 = LLM step (the 3-byte wire form)
-    node16: object = None  # optional u16[n]: node_base
-    packed: object = None  # optional u8: tok8 and node16 in one buffer (wire8_layout)
+    tok8: object = None    # optional u8[n]: token, 255 = LLM step (the narrow wire forms)
+    node16: object = None  # optional u16[n]: node_base (3-byte form)
+    packed: object = None  # optional u8: tok8 and node16 / node8 in one buffer (wire8_layout)
+    node8: object = None   # optional u8[n]: node code (2-byte form, NodeCodes of the table)
 
-    def narrowed(self) -> "EventBatch":
-        """The 3-byte wire form (u8 token + u16 node_base) alongside the
-        others, when the values fit (signature ids < 255, node bases < 2^16):
-        both in one buffer (`packed`, wire8_layout), so a step uploads them
-        with one copy."""
+    def narrowed(self, codes: "NodeCodes | None" = None) -> "EventBatch":
+        """The narrow wire form alongside the others, when the values fit
+        (signature ids < 255, node bases < 2^16): u8 token + u16 node_base
+        (3 bytes), or with a live table's ``codes`` u8 token + u8 node code
+        (2 bytes) while the table has seen at most 256 node arrays.  Both
+        halves sit in one buffer (`packed`, wire8_layout), so a step uploads
+        them with one copy."""
         tok = np.asarray(self.tok)
         node = np.asarray(self.node if self.node is not None else np.asarray(self.ref)[:, 0])
         if tok.size and (tok.max() >= 255 or node.max() >= (1 << 16) or node.min() < 0):
             return self
         n = len(tok)
-        off, size = wire8_layout(n)
+        code = codes.encode(node) if codes is not None else None
+        off, size = wire8_layout(n, 1 if code is not None else 2)
         packed = np.zeros(size, np.uint8)
         tok8 = packed[:n]
-        node16 = packed[off:off + 2 * n].view(np.uint16)
         tok8[:] = np.where(tok < 0, 255, tok)
+        if code is not None:
+            node8 = packed[off:off + n]
+            node8[:] = code
+            return EventBatch(self.tok, self.ref, self.data, self.node, tok8, None, packed, node8)
+        node16 = packed[off:off + 2 * n].view(np.uint16)
         node16[:] = node
         return EventBatch(self.tok, self.ref, self.data, self.node, tok8, node16, packed)
 
     def pin(self) -> "EventBatch":
-        """Move the 3-byte wire form into pinned host memory (one buffer, with
-        tok8 / node16 as views), for the asynchronous single-copy upload."""
+        """Move the narrow wire form into pinned host memory (one buffer, with
+        tok8 / node16 / node8 as views), for the asynchronous single-copy
+        upload."""
         import torch
 
         if self.packed is not None and isinstance(self.packed, np.ndarray):
@@ -77,7 +125,10 @@ class EventBatch:
             off, _ = wire8_layout(n)
             self.packed = torch.from_numpy(self.packed).pin_memory()
             self.tok8 = self.packed[:n]
-            self.node16 = self.packed[off:off + 2 * n].view(torch.int16)
+            if self.node8 is not None:
+                self.node8 = self.packed[off:off + n]
+            else:
+                self.node16 = self.packed[off:off + 2 * n].view(torch.int16)
         return self
 
     def wire(self, ship_bytes: bool, narrow8: bool = False) -> tuple:
@@ -170,6 +221,7 @@ class LiveSessionTable:
         # need the live-plan kernels
         self.narrow8 = (self.plan is not None and not ship_bytes and len(nodes) < (1 << 16)
                         and 2 * len(dpool.sigs) < 255)
+        self.codes = NodeCodes() if self.narrow8 else None  # the 2-byte wire form
         self.new_tok8 = torch.zeros(n, dtype=torch.uint8, device=dev)
         self.new_node16 = torch.zeros(n, dtype=torch.int16, device=dev)
         self.staged8 = False
@@ -234,7 +286,12 @@ class LiveSessionTable:
         data = batch.data if isinstance(batch.data, t.Tensor) else t.from_numpy(batch.data)
         self.staged8 = self.narrow8 and batch.tok8 is not None
         if self.staged8:
-            for d, x in ((self.new_tok8, batch.tok8), (self.new_node16, batch.node16)):
+            node16 = batch.node16
+            if batch.node8 is not None:  # the 2-byte form: node codes -> node_base here
+                code = batch.node8.cpu().numpy() if isinstance(batch.node8, t.Tensor) \
+                    else np.asarray(batch.node8)
+                node16 = self.codes.host.numpy()[code.astype(np.int64)].astype(np.uint16)
+            for d, x in ((self.new_tok8, batch.tok8), (self.new_node16, node16)):
                 x = x if isinstance(x, t.Tensor) else t.from_numpy(np.ascontiguousarray(x))
                 d.copy_(x.reshape(-1).view(d.dtype), non_blocking=non_blocking)
             return
@@ -674,6 +731,7 @@ def _in_set(t, n: int) -> dict:
     off, size = wire8_layout(n)
     packed = t.zeros(size, dtype=t.uint8, device="cuda")
     return {"packed": packed, "tok8": packed[:n], "node16": packed[off:off + 2 * n].view(t.int16),
+            "node8": packed[off:off + n], "n2": wire8_layout(n, 1)[1],
             "tok": t.zeros(n, dtype=t.int32, device="cuda"),
             "node": t.zeros(n, dtype=t.int32, device="cuda"),
             "ref": t.zeros(2 * n, dtype=t.int64, device="cuda")}
@@ -806,7 +864,14 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
             trace.append({"u0": _tev(t, up)})
         st = sv["in"][k]
         narrow = b.node is not None and not table.ship_bytes
-        if table.narrow8 and table.serve_fused and b.tok8 is not None:  # 3 B per session
+        if (table.narrow8 and table.serve_fused and b.tok8 is not None
+                and b.node8 is not None):  # 2 B per session: token + node code
+            narrow = 2
+            table.codes.upload(up)
+            wire = ([(st["packed"][:b.packed.numel()], b.packed)]
+                    if isinstance(b.packed, t.Tensor) and b.packed.numel() == st["n2"]
+                    else [(st["tok8"], b.tok8), (st["node8"], b.node8)])
+        elif table.narrow8 and table.serve_fused and b.tok8 is not None:  # 3 B per session
             narrow = 8
             wire = ([(st["packed"], b.packed)]
                     if isinstance(b.packed, t.Tensor) and b.packed.numel() == st["packed"].numel()
@@ -848,6 +913,10 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
             if narrow == 8:
                 win.new_tok, win.new_node = None, None
                 win.new_tok8, win.new_node16 = ptr(st["tok8"]), ptr(st["node16"])
+            elif narrow == 2:
+                win.new_tok, win.new_node = None, None
+                win.new_tok8, win.new_node16 = ptr(st["tok8"]), None
+                win.new_node8, win.node_codes = ptr(st["node8"]), ptr(table.codes.dev)
             sv["wins"][key] = win
         if table.plan is not None:
             scr = sv["scratch"][k]

@@ -51,3 +51,24 @@ for name, a, b in (("H2D 3 MB x1", (up_h, up_d), None), ("H2D 1+2 MB", (up2_h, u
                    ("both split", (up2_h, up2_d), (dn3_h, dn3_d))):
     u, d = run(a, b)
     print(f"{name:20s} up-stream {u:7.1f} us  down-stream {d:7.1f} us")
+
+# the same copies while a memory-bound kernel stream runs beside them
+big = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+s3 = torch.cuda.Stream()
+
+
+def busy(reps):
+    with torch.cuda.stream(s3):
+        for _ in range(reps):
+            big.add_(1)
+
+
+torch.cuda.synchronize()
+busy(400)
+u, d = run((up_h, up_d), (dn_h, dn_d), reps=100)
+print(f"{'both x1 + kernel':20s} up-stream {u:7.1f} us  down-stream {d:7.1f} us")
+torch.cuda.synchronize()
+up2m_h, up2m_d = bufs([2 * MB])
+dn35_h, dn35_d = bufs([3_500_000])
+u, d = run((up2m_h, up2m_d), (dn35_h, dn35_d))
+print(f"{'up 2 MB, down 3.5 MB':20s} up-stream {u:7.1f} us  down-stream {d:7.1f} us")

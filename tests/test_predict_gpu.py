@@ -239,7 +239,8 @@ def test_compact_records_expand_to_the_full_records(fmt):
 @pytest.mark.parametrize("variant", ["motif", "negative_benefit", "allow_all_k3", "wide_format",
                                      "ship_bytes", "pred_stream", "pinned_inputs", "no_plan",
                                      "no_plan_pred_stream", "narrow8", "narrow8_pinned",
-                                     "no_keys", "no_uniq", "tight_bound"])
+                                     "no_keys", "no_uniq", "tight_bound", "narrow2",
+                                     "narrow2_pinned"])
 def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
@@ -300,7 +301,10 @@ def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
             if variant.startswith("narrow8"):  # u8 token + u16 node on the wire
                 b = b.narrowed()
                 assert b.tok8 is not None and pip.narrow8
-            if variant in ("pinned_inputs", "narrow8_pinned"):  # the batched-copy upload path
+            if variant.startswith("narrow2"):  # u8 token + u8 node code on the wire
+                b = b.narrowed(pip.codes)
+                assert b.node8 is not None and pip.narrow8
+            if variant in ("pinned_inputs", "narrow8_pinned", "narrow2_pinned"):  # batched copies
                 b.tok = torch.from_numpy(b.tok).pin_memory()
                 b.node = torch.from_numpy(b.node).pin_memory()
                 b.ref = torch.from_numpy(np.ascontiguousarray(b.ref)).pin_memory()
@@ -391,3 +395,18 @@ def test_live_beyond_one_persistent_sweep(n, steps):
     assert r["kslot_ok"] and r["serve_ok"], r["mismatch"]
     assert r["serve_kernel"].startswith("fused")
     assert r["predictions"] > n * steps
+
+
+def test_node_codes_append_only_and_bounded():
+    """NodeCodes: new node arrays get the next codes (in sorted order within a
+    batch) and codes never change;
+    past 256 node arrays encode() declines (the 3-byte form is kept)."""
+    from paper_2603_18897_b200.live import NodeCodes
+
+    c = NodeCodes()
+    a = c.encode(np.array([700, 5, 700, 9], np.int64))
+    assert a.tolist() == [2, 0, 2, 1] and c.n == 3
+    b = c.encode(np.array([9, 11, 5], np.int64))
+    assert b.tolist() == [1, 3, 0] and c.host.numpy()[:4].tolist() == [5, 9, 700, 11]
+    assert c.encode(np.arange(1000, 1300)) is None and c.n == 4
+    assert c.encode(np.arange(1000, 1252)).max() == 255 and c.n == 256
