@@ -288,6 +288,7 @@ constexpr int RF_THREADS = 256;
 constexpr int RF_WARPS = RF_THREADS / 32;
 constexpr int RF_GMAX = 8;
 constexpr int RF_CHUNK = 8;
+constexpr int RF_PEEK = 6;  // window events gathered in one batch
 
 __global__ void __launch_bounds__(RF_THREADS, 4) replay_fused_kernel(const paste_pool_desc pool,
                                                                    const paste_replay_desc D,
@@ -296,6 +297,8 @@ __global__ void __launch_bounds__(RF_THREADS, 4) replay_fused_kernel(const paste
   __shared__ const uint8_t* ents[RF_WARPS][32];
   __shared__ uint32_t queue[RF_WARPS][32 + RF_CHUNK * 32];
   __shared__ unsigned hit_mask[RF_WARPS], unsure_mask[RF_WARPS];
+  __shared__ int32_t s_aev[RF_WARPS][32];   // the call's actual-argument payload
+  __shared__ int64_t s_abase[RF_WARPS][32];  // and its node base
   __shared__ uint64_t memo[MEMO];
   for (int i = threadIdx.x; i < MEMO; i += RF_THREADS) memo[i] = 0;
   __syncthreads();
@@ -324,7 +327,26 @@ __global__ void __launch_bounds__(RF_THREADS, 4) replay_fused_kernel(const paste
       const int64_t lo = end - D.call_len[c];
       tool = D.call_tool[c];
       cks = D.call_keyset[c];
-      for (int64_t q = end - 1; q >= lo && m < G; --q) {  // newest G tool events
+      const int32_t aev = D.call_args[c];
+      s_aev[w][lane] = aev;
+      // the newest RF_PEEK events in one batch of independent loads (a
+      // window's newest G tool events are almost always among them)
+      const int span = end - lo < RF_PEEK ? (int)(end - lo) : RF_PEEK;
+      int32_t tk[RF_PEEK], ev[RF_PEEK];
+#pragma unroll
+      for (int j = 0; j < RF_PEEK; ++j) {
+        tk[j] = j < span ? __ldg(D.ev_tok + end - 1 - j) : -1;
+        ev[j] = j < span ? __ldg(D.ev_evt + end - 1 - j) : -1;
+      }
+      s_abase[w][lane] = aev >= 0 ? D.refs[aev].node_base : 0;
+#pragma unroll
+      for (int j = 0; j < RF_PEEK; ++j)
+        if (tk[j] >= 0 && m < G) {
+          gt[m] = tk[j];
+          ge[m] = ev[j];
+          ++m;
+        }
+      for (int64_t q = end - 1 - span; q >= lo && m < G; --q) {  // longer LLM runs
         const int32_t t = __ldg(D.ev_tok + q);
         if (t >= 0) {
           gt[m] = t;
@@ -394,15 +416,14 @@ __global__ void __launch_bounds__(RF_THREADS, 4) replay_fused_kernel(const paste
           const uint32_t it = queue[w][count - take + lane];
           const int src = it >> 16, i = it & 0x7fff;
           const bool ks_unsure = (it >> 15) & 1u;
-          const int64_t cc = base + src;
           const int4 r0 = __ldg(reinterpret_cast<const int4*>(ents[w][src] + 16 + 32 * i));
           const int4 r1 = __ldg(reinterpret_cast<const int4*>(ents[w][src] + 16 + 32 * i) + 1);
           const uint32_t ages = (uint32_t)r0.y;
           const int n_bind = r0.w & 0xffff, bind_off = r1.x;
           const int32_t* ogt = gts[w][src];
           const int32_t* oge = ogt + RF_GMAX;
-          const int32_t aev = D.call_args[cc];
-          const int64_t abase = D.refs[aev].node_base;
+          const int32_t aev = s_aev[w][src];
+          const int64_t abase = s_abase[w][src];
           int verdict = CMP_EQ;
           for (int b = 0; b < n_bind; ++b) {
             const int bind = bind_off + b;
@@ -482,8 +503,17 @@ extern "C" int paste_replay_fused(const paste_pool_desc* pool, const paste_repla
     return PASTE_ERR_UNSUPPORTED;
   }
   if (d->n_calls == 0) return PASTE_OK;
+  // one resident wave (a second partial wave left most warps idle at the end)
+  static int resident = 0;
+  if (resident == 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, replay_fused_kernel, RF_THREADS, 0);
+    resident = sms * (occ > 0 ? occ : 1);
+  }
   int64_t blocks = (d->n_calls + RF_THREADS - 1) / RF_THREADS;
-  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks > resident) blocks = resident;
   replay_fused_kernel<<<(unsigned)blocks, RF_THREADS, 0, (cudaStream_t)stream>>>(
       *pool, *d, max_candidates, G);
   PASTE_CUDA_CHECK(cudaGetLastError());
