@@ -52,14 +52,18 @@ __device__ __forceinline__ int64_t resolve_fast(const paste_windows& win, const 
   int64_t cur;
   if (cacheable) {
     const int h = memo_slot(key);
-    const uint64_t e = memo[h];
+    // a lock-free cache shared by the CTA's warps: each entry is one 64-bit
+    // word (valid bit, tag, value) read and written with shared-memory
+    // atomics, so a reader sees an old or a new entry whole and checks the tag
+    unsigned long long* slot = reinterpret_cast<unsigned long long*>(memo + h);
+    const uint64_t e = atomicAdd(slot, 0ull);
     if ((e >> 63) && ((e >> 23) & ((1ull << 40) - 1)) == key) {
       const uint64_t v = e & MEMO_NONE;
       cur = v == MEMO_NONE ? -1 : (int64_t)v;
     } else {
       cur = walk_binding(win, steps, bd, nb, 0);
       if (cur < (int64_t)MEMO_NONE)
-        memo[h] = (1ull << 63) | (key << 23) | (cur < 0 ? MEMO_NONE : (uint64_t)cur);
+        atomicExch(slot, (1ull << 63) | (key << 23) | (cur < 0 ? MEMO_NONE : (uint64_t)cur));
     }
   } else {
     cur = walk_binding(win, steps, bd, nb, 0);

@@ -75,11 +75,32 @@ def live():
         seq.step(wl_a.next_batch())
         full.append(seq.fetch().session_major())
         seq.fetch_compact()  # compact.cu look-back compaction
-    got = [r.expand(dp.image.patterns, pip.benefit)
-           for r in pip.serve(wl_b.next_batch() for _ in range(steps))]
+    wire2 = os.environ.get("SAN_WIRE2") == "1"  # the 2-byte input (node codes), pinned
+    batches = (wl_b.next_batch().narrowed(pip.codes).pin() if wire2 else wl_b.next_batch()
+               for _ in range(steps))
+    got = [r.expand(dp.image.patterns, pip.benefit) for r in pip.serve(batches)]
     for g, f in zip(got, full):
         _compare(g, f)
     print("live ok", os.environ.get("PASTE_LIVE_MODE", "two-pass"))
+
+
+def replay():
+    from paper_2603_18897_b200.device_ops import DevicePool
+    from paper_2603_18897_b200.mining import load_pool
+    from paper_2603_18897_b200.replay import KeysetTable, ReplayBatch
+    from paper_2603_18897_b200.synth import coding_replay_corpus
+
+    pool = load_pool(os.path.join(ROOT, "paper_2603_18897_b200", "data", "pool_coding_c2_t03.json"))
+    dp = DevicePool(pool)
+    ks = KeysetTable()
+    c = coding_replay_corpus(dp, int(os.environ.get("SAN_SESSIONS", "3000")), window_capacity=16,
+                             seed=2, ksets=ks)
+    rb = ReplayBatch(dp, c, 16, 8, ks)
+    rb.launch()
+    two = rb.tallies.cpu().tolist()
+    assert rb.launch_fused()
+    assert rb.tallies.cpu().tolist() == two
+    print("replay ok", two)
 
 
 def order():
@@ -125,6 +146,7 @@ def select():
 
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
-    for name, fn in (("mine", mine), ("live", live), ("order", order), ("select", select)):
+    for name, fn in (("mine", mine), ("live", live), ("order", order), ("select", select),
+                     ("replay", replay)):
         if which in (name, "all"):
             fn()
