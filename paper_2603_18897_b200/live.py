@@ -821,7 +821,11 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
 
     def hand_out():
         k, h, sizes, done, copied = copy_q.popleft()
-        done.synchronize()
+        if spin:  # poll: a sleeping wait wakes tens of microseconds late
+            while not done.query():
+                pass
+        else:
+            done.synchronize()
         hs, ds = sv["hsets"][h], sv["dsets"][k]
         tot = hs["totals"]
         if int(tot[3]):
@@ -937,6 +941,7 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         return True
 
     trace = getattr(table, "serve_trace", None)  # development: per-step timing events
+    spin = os.environ.get("PASTE_SERVE_SPIN", "0") == "1"  # measured no faster
     it = iter(batches)
     steps0 = table.steps
     nxt = next(it, None)
