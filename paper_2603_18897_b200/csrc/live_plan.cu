@@ -26,6 +26,7 @@
 // publishes its aggregate (decoupled look-back) before any binding is
 // resolved, and every record is written once at its final offset -- no
 // staging.
+#include <cooperative_groups.h>
 #include <string.h>
 
 #include <type_traits>
@@ -214,7 +215,6 @@ struct LiveParams {
   int M;
   // key-stream form: per-warp argument counts and exclusive offsets
   uint32_t* w_cnt;
-  uint32_t* w_off;
   uint64_t* ticket;
   uint64_t* tile_state;
   int64_t n_tiles;
@@ -860,9 +860,9 @@ constexpr int SCAT_SPT = 4;
 // session's argument count follows from its key.  The step writes each
 // warp's argument words (32 consecutive sessions) contiguously into the
 // warp's staging slot (capacity 32 * M) at the warp-exclusive offsets, and
-// the warp's total; one CTA scans the warp totals (31k per 1M sessions); a
-// copy kernel moves every warp's words to their final offset.  No tile
-// look-back, no CTA-wide barrier in the step.
+// the warp's total; a copy kernel scans the warp totals (tiles of 256
+// warps, decoupled look-back over ~120 tiles per 1M sessions) and moves
+// every warp's words to their final offset.  No barrier in the step.
 struct KeyTotals {
   unsigned long long nm, na, ne, wide;
 };
@@ -915,6 +915,11 @@ __global__ void __launch_bounds__(LT, MINB) predict_live_keys_kernel(const LiveP
   const int64_t stride = (int64_t)gridDim.x * LT;
   const int64_t s0 = (int64_t)blockIdx.x * LT + threadIdx.x;
   const int lane = threadIdx.x & 31;
+  {  // the copy kernel's ticket and tile records (it runs after this kernel)
+    const int64_t words = LB_STRIDE * (P.n_tiles + 1);
+    for (int64_t i = (int64_t)blockIdx.x * LT + threadIdx.x; i < words; i += stride)
+      P.ticket[i] = 0;
+  }
   KeyTotals t{0, 0, 0, 0};
   FrontIn f1, f2;
   Sess<G> y0, y1;
@@ -947,78 +952,183 @@ __global__ void __launch_bounds__(LT, MINB) predict_live_keys_kernel(const LiveP
   }
 }
 
-// exclusive offsets of the warp totals, one CTA of 1024 threads; each pass
-// covers 32 warps x 1024 values: a warp holds its 1024 values in registers
-// (32 coalesced loads per lane), the CTA scans the 32 warp sums, then each
-// warp scans its values 32 at a time and stores the offsets coalesced
-constexpr int WSCAN_T = 1024, WSCAN_V = 32;
-
-__global__ void __launch_bounds__(WSCAN_T) warp_scan_kernel(const uint32_t* cnt, uint32_t* off,
-                                                            int64_t nw, int64_t* total) {
-  __shared__ uint32_t s_warp[WSCAN_T / 32];
-  __shared__ uint64_t s_carry;
+// The key-stream step, the warp-total scan and the copy in ONE cooperative
+// kernel (every CTA resident): after the pipelined step a grid barrier; CTA
+// b then sums the warp totals of its contiguous range of staged warps; a
+// second barrier; each CTA adds up the sums of the CTAs before it, scans its
+// range and copies those warps' words to their final offset.  Two grid
+// barriers instead of two more launches.
+template <int G, int MINB>
+__global__ void __launch_bounds__(LT, MINB) predict_live_keys_coop_kernel(const LiveParams P) {
+  namespace cg = cooperative_groups;
+  const int64_t n = P.win.n_sessions;
+  const int64_t stride = (int64_t)gridDim.x * LT;
+  const int64_t s0 = (int64_t)blockIdx.x * LT + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = 0;
+  KeyTotals t{0, 0, 0, 0};
+  {
+    FrontIn f1, f2;
+    Sess<G> y0, y1;
+    FrontMid<G> m0, m1;
+    front_load(P, s0, f1);
+    front_load(P, s0 + stride, f2);
+    front_observe<G>(P, f1, y1, m1);
+    for (int64_t s = s0; s - lane < n; s += stride) {  // warp-uniform: whole warps
+      y0 = y1;
+      m0 = m1;
+      f1 = f2;
+      front_load(P, s + 2 * stride, f2);
+      front_observe<G>(P, f1, y1, m1);
+      front_key<G, false>(P, y0, m0);
+      keys_write<G>(P, y0, t);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    t.nm += __shfl_xor_sync(0xffffffffu, t.nm, o);
+    t.na += __shfl_xor_sync(0xffffffffu, t.na, o);
+    t.ne += __shfl_xor_sync(0xffffffffu, t.ne, o);
+    t.wide += __shfl_xor_sync(0xffffffffu, t.wide, o);
+  }
+  if (lane == 0) {
+    unsigned long long* tot = reinterpret_cast<unsigned long long*>(P.C.totals);
+    if (t.nm) atomicAdd(tot + 0, t.nm);
+    if (t.na) atomicAdd(tot + 2, t.na);
+    if (t.wide) atomicAdd(tot + 3, t.wide);
+    if (t.ne) atomicAdd(tot + 4, t.ne);
+  }
+  cg::grid_group grid = cg::this_grid();
+  __threadfence();
+  grid.sync();  // every warp total is written
+  __shared__ uint64_t s_red[LT / 32];
+  __shared__ uint64_t s_base;
+  const int64_t nw = (n + 31) / 32;
+  const int64_t per = (nw + gridDim.x - 1) / gridDim.x;
+  const int64_t w0 = (int64_t)blockIdx.x * per;
+  const int64_t w1 = w0 + per < nw ? w0 + per : nw;
+  uint64_t* cta_sum = P.tile_state;  // [gridDim.x]
+  uint64_t part = 0;
+  for (int64_t w = w0 + threadIdx.x; w < w1; w += LT) part += P.w_cnt[w];
+  part = __reduce_add_sync(0xffffffffu, (unsigned)part);
+  if (lane == 0) s_red[warp] = part;
   __syncthreads();
-  for (int64_t base = 0; base < nw; base += (int64_t)WSCAN_T * WSCAN_V) {
-    const int64_t chunk = base + (int64_t)warp * (32 * WSCAN_V);
-    uint32_t v[WSCAN_V];
-    uint32_t sum = 0;
+  if (threadIdx.x == 0) {
+    uint64_t v = 0;
+    for (int k = 0; k < LT / 32; ++k) v += s_red[k];
+    cta_sum[blockIdx.x] = v;
+  }
+  __threadfence();
+  grid.sync();  // every CTA's sum is written
+  uint64_t before = 0;
+  for (int64_t b = threadIdx.x; b < blockIdx.x; b += LT) before += cta_sum[b];
 #pragma unroll
-    for (int i = 0; i < WSCAN_V; ++i) {
-      const int64_t at = chunk + i * 32 + lane;
-      v[i] = at < nw ? cnt[at] : 0u;
+  for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+  __syncthreads();
+  if (lane == 0) s_red[warp] = before;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t v = 0;
+    for (int k = 0; k < LT / 32; ++k) v += s_red[k];
+    s_base = v;
+    if (blockIdx.x == gridDim.x - 1) P.C.totals[1] = (int64_t)(v + cta_sum[blockIdx.x]);
+  }
+  __syncthreads();
+  // scan the range LT warps at a time, then copy: staged warp w goes to warp
+  // (w - chunk) % (LT / 32) of this CTA, lanes copy its words
+  __shared__ uint32_t s_c[LT], s_o[LT];
+  uint64_t run = s_base;
+  const bool a16 = (P.C.format & PASTE_CF_ARG16) != 0;
+  for (int64_t c0 = w0; c0 < w1; c0 += LT) {
+    const int64_t w = c0 + threadIdx.x;
+    const uint32_t c = w < w1 ? P.w_cnt[w] : 0u;
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
     }
-#pragma unroll
-    for (int i = 0; i < WSCAN_V; ++i) sum += v[i];
-    const uint32_t wsum = __reduce_add_sync(0xffffffffu, sum);
-    if (lane == 0) s_warp[warp] = wsum;
+    if (lane == 31) s_red[warp] = inc;
     __syncthreads();
-    if (warp == 0) {
-      const uint32_t x = s_warp[lane];
-      uint32_t xi = x;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, xi, o);
-        if (lane >= o) xi += u;
+    uint64_t wb = 0, all = 0;
+    for (int k = 0; k < LT / 32; ++k) {
+      if (k < warp) wb += s_red[k];
+      all += s_red[k];
+    }
+    s_c[threadIdx.x] = c;
+    s_o[threadIdx.x] = (uint32_t)(run + wb + inc - c);
+    __syncthreads();
+    const int nk = (int)(w1 - c0 < LT ? w1 - c0 : LT);
+    for (int j = warp; j < nk; j += LT / 32) {
+      const uint32_t cj = s_c[j], oj = s_o[j];
+      const int64_t src = (c0 + j) * 32 * P.M;
+      for (uint32_t i = lane; i < cj; i += 32) {
+        if (a16)
+          static_cast<uint16_t*>(P.C.arg)[oj + i] = reinterpret_cast<const uint16_t*>(P.st_arg)[src + i];
+        else
+          static_cast<uint32_t*>(P.C.arg)[oj + i] = P.st_arg[src + i];
       }
-      s_warp[lane] = xi - x;
     }
-    __syncthreads();
-    uint32_t run = (uint32_t)s_carry + s_warp[warp];
-#pragma unroll
-    for (int i = 0; i < WSCAN_V; ++i) {
-      uint32_t inc = v[i];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += u;
-      }
-      const int64_t at = chunk + i * 32 + lane;
-      if (at < nw) off[at] = run + inc - v[i];
-      run += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    __syncthreads();
-    if (threadIdx.x == WSCAN_T - 1) s_carry = run;
+    run += all;
     __syncthreads();
   }
-  if (threadIdx.x == 0) total[1] = (int64_t)s_carry;
 }
 
-// every staged warp's words to their final offset (one warp per staged warp)
-__global__ void __launch_bounds__(LT) warp_copy_kernel(const LiveParams P, int64_t nw) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * LT + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * LT) >> 5;
+// every staged warp's words to their final offset: tiles of WC_T staged
+// warps (one per thread) claimed through a ticket, a block scan of their
+// counts and a decoupled look-back across the tiles (tile_lookback) for the
+// tile's offset; each warp then copies its 32 staged warps, coalesced
+constexpr int WC_T = 256;
+
+__global__ void __launch_bounds__(WC_T) warp_copy_kernel(const LiveParams P, int64_t nw,
+                                                         int64_t n_tiles) {
+  __shared__ int64_t s_tile;
+  __shared__ uint32_t s_w[WC_T / 32];
+  __shared__ uint64_t s_ex;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0)
+    s_tile = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(P.ticket), 1ull);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t w = tile * WC_T + threadIdx.x;
+  const uint32_t c = w < nw ? P.w_cnt[w] : 0u;
+  uint32_t inc = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t x = lane < WC_T / 32 ? s_w[lane] : 0u;
+    uint32_t xi = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xffffffffu, xi, o);
+      if (lane >= o) xi += u;
+    }
+    const uint64_t agg = __shfl_sync(0xffffffffu, xi, WC_T / 32 - 1);
+    const uint64_t a4[4] = {agg, 0, 0, 0};
+    uint64_t e4[4];
+    tile_lookback(P.tile_state, tile, a4, e4, lane);
+    if (lane < WC_T / 32) s_w[lane] = xi - x;
+    if (lane == 0) {
+      s_ex = e4[0];
+      if (tile == n_tiles - 1) P.C.totals[1] = (int64_t)(e4[0] + agg);
+    }
+  }
+  __syncthreads();
+  const uint32_t off = (uint32_t)s_ex + s_w[warp] + inc - c;
   const bool a16 = (P.C.format & PASTE_CF_ARG16) != 0;
-  for (int64_t w = gw; w < nw; w += nwarps) {
-    const uint32_t c = P.w_cnt[w], o = P.w_off[w];
-    const int64_t src = w * 32 * P.M;
-    for (uint32_t i = lane; i < c; i += 32) {
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t cj = __shfl_sync(0xffffffffu, c, j), oj = __shfl_sync(0xffffffffu, off, j);
+    if (cj == 0) continue;
+    const int64_t src = (tile * WC_T + warp * 32 + j) * 32 * P.M;
+    for (uint32_t i = lane; i < cj; i += 32) {
       if (a16)
-        static_cast<uint16_t*>(P.C.arg)[o + i] = reinterpret_cast<const uint16_t*>(P.st_arg)[src + i];
+        static_cast<uint16_t*>(P.C.arg)[oj + i] = reinterpret_cast<const uint16_t*>(P.st_arg)[src + i];
       else
-        static_cast<uint32_t*>(P.C.arg)[o + i] = P.st_arg[src + i];
+        static_cast<uint32_t*>(P.C.arg)[oj + i] = P.st_arg[src + i];
     }
   }
 }
@@ -1362,8 +1472,34 @@ static int live_mode_impl() {
   return m;
 }
 
+static bool live_coop() {  // PASTE_LIVE_COOP=0: step + look-back copy as two launches
+  static int c = -1;
+  if (c < 0) {
+    const char* e = getenv("PASTE_LIVE_COOP");
+    c = e && !strcmp(e, "0") ? 0 : 1;
+  }
+  return c == 1;
+}
+
 template <int G>
 static void launch_keys(const LiveParams& P, cudaStream_t st) {
+  if (live_coop()) {
+    static int sms = 0, oc = 0;
+    if (sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, predict_live_keys_coop_kernel<G, 7>, LT, 0);
+      if (oc < 1) oc = 1;
+    }
+    const int64_t g1 = (P.win.n_sessions + LT - 1) / LT;
+    const unsigned grid = (unsigned)(g1 < (int64_t)sms * oc ? g1 : (int64_t)sms * oc);
+    LiveParams Q = P;
+    void* args[] = {&Q};
+    cudaLaunchCooperativeKernel((const void*)predict_live_keys_coop_kernel<G, 7>, dim3(grid),
+                                dim3(LT), args, 0, st);
+    return;
+  }
   static int sms = 0, o1 = 0;
   if (sms == 0) {
     int dev = 0;
@@ -1377,10 +1513,7 @@ static void launch_keys(const LiveParams& P, cudaStream_t st) {
   const int64_t g1 = (n + LT - 1) / LT;
   predict_live_keys_kernel<G, 7><<<(unsigned)(g1 < (int64_t)sms * o1 ? g1 : (int64_t)sms * o1), LT,
                                    0, st>>>(P);
-  warp_scan_kernel<<<1, WSCAN_T, 0, st>>>(P.w_cnt, P.w_off, nw, P.C.totals);
-  // one warp per staged warp: every copy's loads are in flight at once
-  const int64_t g3 = (nw * 32 + LT - 1) / LT;
-  warp_copy_kernel<<<(unsigned)(g3 < (1ll << 31) - 1 ? g3 : (1ll << 31) - 1), LT, 0, st>>>(P, nw);
+  warp_copy_kernel<<<(unsigned)P.n_tiles, WC_T, 0, st>>>(P, nw, P.n_tiles);
 }
 
 static int live_mode() { return live_mode_impl(); }
@@ -1443,10 +1576,10 @@ extern "C" int paste_predict_live_compact(const paste_pool_desc* pool, paste_win
   P.st_arg = reinterpret_cast<uint32_t*>(stg + 3 * a4);
   P.M = K * (max_bindings > 0 ? max_bindings : 1);
   P.w_cnt = reinterpret_cast<uint32_t*>(stg);        // key-stream form: [n / 32]
-  P.w_off = reinterpret_cast<uint32_t*>(stg + a4);
   cudaStream_t st = (cudaStream_t)stream;
   const bool keys_form = mode == 0 && (c->format & PASTE_CF_KEYS) &&
                          ((n + 31) / 32) * 32 * (int64_t)P.M < (1ll << 32);
+  if (keys_form) P.n_tiles = ((n + 31) / 32 + WC_T - 1) / WC_T;  // warp_copy_kernel tiles
   if (!keys_form)
     PASTE_CUDA_CHECK(cudaMemsetAsync(scratch, 0, 8 * (LB_STRIDE * P.n_tiles + LB_STRIDE), st));
   PASTE_CUDA_CHECK(cudaMemsetAsync(c->totals, 0, 5 * sizeof(int64_t), st));
@@ -1454,7 +1587,7 @@ extern "C" int paste_predict_live_compact(const paste_pool_desc* pool, paste_win
   const int G = live_gather_depth(pool, windows->capacity);
   if (keys_form) {
     by_depth(G, [&](auto g) { launch_keys<decltype(g)::value>(P, st); });
-    count_launch(3);
+    count_launch(live_coop() ? 1 : 2);
   } else if (mode == 0 || mode == 3) {
     by_depth(G, [&](auto g) { launch_two_pass<decltype(g)::value>(P, st); });
     count_launch(2);

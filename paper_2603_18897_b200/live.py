@@ -846,10 +846,11 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
                 sup.synchronize()
                 copied += int(nb1[0])
                 sv["supplements"] = sv.get("supplements", 0) + 1
-            # the bound follows the largest recent count with 1/8 headroom
-            # (a step past it costs a synchronous fetch of the rest)
-            grow = need[j] + (need[j] >> 3) + 4096 if margin is None else int(margin)
-            bound[j] = grow if bound[j] is None else max(grow, (bound[j] * 63) // 64)
+            # the bound follows the largest recent count with 1/32 headroom
+            # (a step past it costs a synchronous fetch of the rest, on a
+            # side stream; the headroom is D2H bytes every step)
+            grow = need[j] + (need[j] >> 5) + 1024 if margin is None else int(margin)
+            bound[j] = grow if bound[j] is None else max(grow, (bound[j] * 127) // 128)
         v = hs["views"]
         rec = CompactRecords(table.K, table.B, v["hdr"][:need[0]], v["pred"][:need[1]],
                              v["arg"][:need[2]], v["act"][:need[3]], fmt, entries, plan)
@@ -944,14 +945,23 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
     spin = os.environ.get("PASTE_SERVE_SPIN", "0") == "1"  # measured no faster
     it = iter(batches)
     steps0 = table.steps
-    nxt = next(it, None)
-    staged = upload(0, nxt) if nxt is not None else None
+    # uploads run `ahead` steps in front of the kernels, so the H2D engine
+    # always has queued work whatever the host is doing
+    ahead = max(1, min(int(os.environ.get("PASTE_SERVE_AHEAD", "2")), depth - 2))
+    staged = deque()
+    n_up = 0
+    while len(staged) < ahead:
+        nxt = next(it, None)
+        if nxt is None:
+            break
+        staged.append(upload(n_up, nxt))
+        n_up += 1
     i = 0
-    while staged is not None:
+    while staged:
         k = i % depth
         h = sv.setdefault("hnext", 0)  # pinned sets rotate across serve() calls
         sv["hnext"] = (h + 1) % nh
-        uploaded, narrow = staged
+        uploaded, narrow = staged.popleft()
         region = table.steps % table.regions
         st = sv["in"][k]
         if sv["free"][k] is not None:  # the set's previous download has finished
@@ -977,9 +987,11 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
         ready.record(comp)
         sv["in_free"][k] = ready
         download(k, h, i)
-        # the next step's upload goes out now, before the host waits on anything
+        # the next upload goes out now, before the host waits on anything
         nxt = next(it, None)
-        staged = upload(i + 1, nxt) if nxt is not None else None
+        if nxt is not None:
+            staged.append(upload(n_up, nxt))
+            n_up += 1
         i += 1
         if len(copy_q) > depth - 1:  # hand out step i - depth + 1
             yield hand_out()
