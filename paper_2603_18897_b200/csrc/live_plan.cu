@@ -863,8 +863,8 @@ constexpr int SCAT_SPT = 4;
 // the warp's total; a copy kernel scans the warp totals (tiles of 256
 // warps, decoupled look-back over ~120 tiles per 1M sessions) and moves
 // every warp's words to their final offset.  No barrier in the step.
-struct KeyTotals {
-  unsigned long long nm, na, ne, wide;
+struct KeyTotals {  // per thread (32-bit: a thread runs few sessions; registers are tight)
+  uint32_t nm, na, ne, wide;
 };
 
 template <int G>
@@ -936,19 +936,18 @@ __global__ void __launch_bounds__(LT, MINB) predict_live_keys_kernel(const LiveP
     front_key<G, false>(P, y0, m0);
     keys_write<G>(P, y0, t);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    t.nm += __shfl_xor_sync(0xffffffffu, t.nm, o);
-    t.na += __shfl_xor_sync(0xffffffffu, t.na, o);
-    t.ne += __shfl_xor_sync(0xffffffffu, t.ne, o);
-    t.wide += __shfl_xor_sync(0xffffffffu, t.wide, o);
-  }
-  if (lane == 0) {
-    unsigned long long* tot = reinterpret_cast<unsigned long long*>(P.C.totals);
-    if (t.nm) atomicAdd(tot + 0, t.nm);
-    if (t.na) atomicAdd(tot + 2, t.na);
-    if (t.wide) atomicAdd(tot + 3, t.wide);
-    if (t.ne) atomicAdd(tot + 4, t.ne);
+  {
+    const unsigned long long nm = __reduce_add_sync(0xffffffffu, t.nm);
+    const unsigned long long na = __reduce_add_sync(0xffffffffu, t.na);
+    const unsigned long long ne = __reduce_add_sync(0xffffffffu, t.ne);
+    const unsigned long long wd = __reduce_add_sync(0xffffffffu, t.wide);
+    if (lane == 0) {
+      unsigned long long* tot = reinterpret_cast<unsigned long long*>(P.C.totals);
+      if (nm) atomicAdd(tot + 0, nm);
+      if (na) atomicAdd(tot + 2, na);
+      if (wd) atomicAdd(tot + 3, wd);
+      if (ne) atomicAdd(tot + 4, ne);
+    }
   }
 }
 
@@ -983,19 +982,18 @@ __global__ void __launch_bounds__(LT, MINB) predict_live_keys_coop_kernel(const 
       keys_write<G>(P, y0, t);
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    t.nm += __shfl_xor_sync(0xffffffffu, t.nm, o);
-    t.na += __shfl_xor_sync(0xffffffffu, t.na, o);
-    t.ne += __shfl_xor_sync(0xffffffffu, t.ne, o);
-    t.wide += __shfl_xor_sync(0xffffffffu, t.wide, o);
-  }
-  if (lane == 0) {
-    unsigned long long* tot = reinterpret_cast<unsigned long long*>(P.C.totals);
-    if (t.nm) atomicAdd(tot + 0, t.nm);
-    if (t.na) atomicAdd(tot + 2, t.na);
-    if (t.wide) atomicAdd(tot + 3, t.wide);
-    if (t.ne) atomicAdd(tot + 4, t.ne);
+  {
+    const unsigned long long nm = __reduce_add_sync(0xffffffffu, t.nm);
+    const unsigned long long na = __reduce_add_sync(0xffffffffu, t.na);
+    const unsigned long long ne = __reduce_add_sync(0xffffffffu, t.ne);
+    const unsigned long long wd = __reduce_add_sync(0xffffffffu, t.wide);
+    if (lane == 0) {
+      unsigned long long* tot = reinterpret_cast<unsigned long long*>(P.C.totals);
+      if (nm) atomicAdd(tot + 0, nm);
+      if (na) atomicAdd(tot + 2, na);
+      if (wd) atomicAdd(tot + 3, wd);
+      if (ne) atomicAdd(tot + 4, ne);
+    }
   }
   cg::grid_group grid = cg::this_grid();
   __threadfence();
@@ -1484,20 +1482,29 @@ static bool live_coop() {  // PASTE_LIVE_COOP=0: step + look-back copy as two la
 template <int G>
 static void launch_keys(const LiveParams& P, cudaStream_t st) {
   if (live_coop()) {
+    // register cap: 6 CTAs/SM -> 80 registers, no spills (38.9 us per 1M
+    // sessions queued); PASTE_LIVE_KEYS_MINB=7 -> 72 registers, 44 B spilled
+    // (40.6 us)
+    static int minb = 0;
+    if (minb == 0) {
+      const char* e = getenv("PASTE_LIVE_KEYS_MINB");
+      minb = e && atoi(e) == 7 ? 7 : 6;
+    }
+    const void* fn = minb == 6 ? (const void*)predict_live_keys_coop_kernel<G, 6>
+                               : (const void*)predict_live_keys_coop_kernel<G, 7>;
     static int sms = 0, oc = 0;
     if (sms == 0) {
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, predict_live_keys_coop_kernel<G, 7>, LT, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, fn, LT, 0);
       if (oc < 1) oc = 1;
     }
     const int64_t g1 = (P.win.n_sessions + LT - 1) / LT;
     const unsigned grid = (unsigned)(g1 < (int64_t)sms * oc ? g1 : (int64_t)sms * oc);
     LiveParams Q = P;
     void* args[] = {&Q};
-    cudaLaunchCooperativeKernel((const void*)predict_live_keys_coop_kernel<G, 7>, dim3(grid),
-                                dim3(LT), args, 0, st);
+    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(LT), args, 0, st);
     return;
   }
   static int sms = 0, o1 = 0;
