@@ -1,0 +1,95 @@
+"""Host side of the serving wire, on CPU: the packed narrow input layouts
+(EventBatch.narrowed, wire8_layout), the key-stream buffer layout
+(keys_layout) and CompactRecords.expand of a key + unit-reference download
+(PASTE_CF_KEYS | PASTE_CF_UNIQ) against hand-built plan entries -- bindings
+that share a resolution unit, an unresolved unit making its predictions
+PARTIAL and their admitted actions take the partial level, and a session
+without an entry."""
+
+import numpy as np
+
+from paper_2603_18897_b200 import _native
+from paper_2603_18897_b200.live import CompactRecords, EventBatch, keys_layout, wire8_layout
+from paper_2603_18897_b200.packing import C_FULL, C_PARTIAL, C_TOOL_ONLY
+
+
+def test_narrow_wire_layouts():
+    n = 37
+    tok = np.arange(n, dtype=np.int32) % 7
+    tok[3] = -1  # an LLM step
+    node = (np.arange(n, dtype=np.int32) * 11) % 500
+    ref = np.stack([node.astype(np.int64), np.zeros(n, np.int64)], axis=1)
+    b = EventBatch(tok, ref, np.zeros(1, np.uint8), node).narrowed()
+    off, size = wire8_layout(n)
+    assert off % 16 == 0 and off >= n and size == off + 2 * n
+    assert b.packed.size == size and b.node8 is None
+    assert np.array_equal(b.tok8, np.where(tok < 0, 255, tok))
+    assert np.array_equal(b.packed[:n], b.tok8)
+    assert np.array_equal(b.packed[off:off + 2 * n].view(np.uint16), node)
+    assert b.wire(False, narrow8=True)[0] is b.packed
+    # values that do not fit keep the wide forms
+    big = EventBatch(tok, ref, np.zeros(1, np.uint8), node + 70_000).narrowed()
+    assert big.tok8 is None and big.packed is None
+
+
+def test_keys_layout():
+    for n, cap, a16 in ((1, 8, True), (1000, 16000, True), (1000, 16000, False)):
+        k_off, a_off, size = keys_layout(n, cap, a16)
+        assert k_off >= 40 and a_off % 64 == 0 and a_off >= k_off + 2 * n
+        assert size == a_off + cap * (2 if a16 else 4)
+
+
+def _word(bind, rank, bslot, age, unit):
+    return np.uint64(bind | (rank << 32) | (bslot << 40) | (age << 48) | (unit << 56))
+
+
+def test_expand_unit_references():
+    K, B, n = 4, 2, 3
+    patterns = np.zeros(3, _native.PATTERN_DTYPE)
+    # p0: mapped, 2 bindings, tool 0; p1: unmapped, tool 1; p2: mapped, 1 binding, tool 0
+    patterns["target_tool"] = [0, 1, 0]
+    patterns["n_bind"] = [2, 0, 1]
+    patterns["flags"] = [1, 0, 1]
+    patterns["p"] = [0.5, 0.4, 0.25]
+    benefit = np.array([700.0, 300.0])
+    n_keys = 2
+    entries = (np.array([3, 0]), np.array([[0, 1, 2, -1], [-1] * 4], np.int32))
+    n_pred = np.array([3, 0])
+    n_act = np.array([2, 0])
+    acts = np.zeros((n_keys, K), np.uint16)
+    acts[0, 0] = 0 | (3 << 8) | (1 << 12)   # tool 0: rank 0, FULL level 3, partial level 1
+    acts[0, 1] = 1 | (1 << 8) | (1 << 12)   # tool 1: rank 1 (tool only), level 1
+    n_map = np.array([3, 0])
+    n_units = np.array([2, 0])
+    M = K * B
+    words = np.zeros((n_keys, M), np.uint64)
+    words[0, 0] = _word(10, 0, 0, 1, 0)  # p0 binding 0 -> unit 0
+    words[0, 1] = _word(11, 0, 1, 1, 1)  # p0 binding 1 -> unit 1
+    words[0, 2] = _word(12, 2, 0, 1, 0)  # p2 binding 0: the same resolution as unit 0
+    plan = (n_pred, n_act, acts, n_map, n_units, words)
+    keys = np.array([0, 0, 0xFFFF], np.uint16)
+    # session 0: both units resolved (region 1); session 1: unit 0 unresolved
+    arg = np.array([(1 << 11) | 5, (1 << 11) | 7, 0xFFFF, (1 << 11) | 9], np.uint16)
+    fmt = (_native.PASTE_CF_ENTRY16 | _native.PASTE_CF_KEYS | _native.PASTE_CF_UNIQ
+           | _native.PASTE_CF_ARG16)
+    rec = CompactRecords(K, B, np.zeros(0, np.uint16), keys, arg, np.zeros(0, np.uint8), fmt,
+                         entries, plan)
+    r = rec.expand(patterns, benefit).session_major()
+    assert r.n_pred.tolist() == [3, 3, 0] and r.n_act.tolist() == [2, 2, 0]
+    pat = r.pred_pat.reshape(n, K)
+    comp = r.pred_comp.reshape(n, K)
+    parg = r.pred_arg.reshape(n, K, B)
+    assert pat[0, :3].tolist() == [0, 1, 2] and pat[1, :3].tolist() == [0, 1, 2]
+    assert comp[0, :3].tolist() == [C_FULL, C_TOOL_ONLY, C_FULL]
+    assert comp[1, :3].tolist() == [C_PARTIAL, C_TOOL_ONLY, C_PARTIAL]
+    ev0, ev1 = 1 * n + 0, 1 * n + 1
+    assert parg[0, 0].tolist() == [(ev0 << 32) | 5, (ev0 << 32) | 7]
+    assert parg[0, 2, 0] == (ev0 << 32) | 5  # the shared unit's reference
+    assert parg[1, 0].tolist() == [-1, (ev1 << 32) | 9]
+    assert parg[1, 2, 0] == -1
+    lvl = r.act_level.reshape(n, K)
+    apred = r.act_pred.reshape(n, K)
+    util = r.act_util.reshape(n, K)
+    assert apred[0, :2].tolist() == [0, 1] and lvl[0, :2].tolist() == [3, 1]
+    assert lvl[1, :2].tolist() == [1, 1]  # PARTIAL rank 0: admitted at its partial level
+    assert util[0, 0] == 0.5 * 700.0 and util[0, 1] == 0.4 * 300.0
