@@ -782,9 +782,15 @@ int paste_resolve(const paste_resolve_desc* d, void* stream);
  * start index and fail tool) on the same source event resolve to the same
  * node, so the plan numbers them as units in first-use order (map word bits
  * 56-63, the count in header byte 3) and the host maps each binding to its
- * unit's reference.                                                        */
+ * unit's reference.
+ * PASTE_CF_KEY8 (with PASTE_CF_KEYS): the key stream holds one u8 per
+ * session instead of the u16 key: the entry's plan code, byte 8 of its
+ * live-plan header, which the caller assigns after paste_build_live_plan
+ * (one code per distinct non-empty entry content, 0xFF for every entry
+ * without predictions or actions; the host maps a code back to a
+ * representative key).  0xFF = no predictions.                           */
 enum { PASTE_CF_HDR8 = 1, PASTE_CF_PRED8 = 2, PASTE_CF_ARG16 = 4, PASTE_CF_ENTRY16 = 8,
-       PASTE_CF_KEYS = 16, PASTE_CF_UNIQ = 32 };
+       PASTE_CF_KEYS = 16, PASTE_CF_UNIQ = 32, PASTE_CF_KEY8 = 64 };
 typedef struct {
   void* hdr;         /* [n]                                                  */
   void* pred;

@@ -153,6 +153,7 @@ class CompactDesc(ctypes.Structure):
 
 PASTE_CF_HDR8, PASTE_CF_PRED8, PASTE_CF_ARG16, PASTE_CF_ENTRY16, PASTE_CF_KEYS = 1, 2, 4, 8, 16
 PASTE_CF_UNIQ = 32
+PASTE_CF_KEY8 = 64
 PASTE_COPY_H2D, PASTE_COPY_D2H, PASTE_COPY_D2D = 1, 2, 3
 PASTE_INGEST_MISSING, PASTE_INGEST_T_ORDER, PASTE_INGEST_EMPTY_TOOL = 0x100, 0x200, 0x400
 

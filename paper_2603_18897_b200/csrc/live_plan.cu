@@ -700,6 +700,16 @@ __device__ __forceinline__ void live_offsets(const LiveParams& P, int64_t tile, 
   }
 }
 
+// the session's key-stream element: the u16 match-table key, or with
+// PASTE_CF_KEY8 the entry's u8 plan code (header byte 8); all-ones = none
+template <int G>
+__device__ __forceinline__ void key_write(const paste_compact_desc& C, const Sess<G>& y) {
+  if (C.format & PASTE_CF_KEY8)
+    static_cast<uint8_t*>(C.pred)[y.s] = y.key >= 0 ? y.e[8] : (uint8_t)0xffu;
+  else
+    static_cast<uint16_t*>(C.pred)[y.s] = y.key >= 0 ? (uint16_t)y.key : (uint16_t)0xffffu;
+}
+
 // argument words a session writes: one per binding, or one per resolution
 // unit (PASTE_CF_UNIQ); none without predictions
 template <int G>
@@ -739,7 +749,7 @@ __device__ __forceinline__ void compact_write(const LiveParams& P, const Sess<G>
     }, units);
   }
   if (C.format & PASTE_CF_ENTRY16) {
-    static_cast<uint16_t*>(C.pred)[y.s] = y.e ? (uint16_t)y.key : (uint16_t)0xffffu;
+    key_write<G>(C, y);
   } else if (y.nm > 0) {
     const int32_t* pid = reinterpret_cast<const int32_t*>(y.e + P.L.off_pid);
     const uint8_t* comp = y.e + P.L.off_comp;
@@ -822,7 +832,7 @@ __device__ __forceinline__ void stage_write(const LiveParams& P, const Sess<G>& 
   }
   if (!(C.format & PASTE_CF_KEYS)) cf_hdr(C, y.s, y.nm, y.n_act);
   if (C.format & PASTE_CF_ENTRY16)
-    static_cast<uint16_t*>(C.pred)[y.s] = y.key >= 0 ? (uint16_t)y.key : (uint16_t)0xffffu;
+    key_write<G>(C, y);
   P.st_key[y.s] = y.key;
   P.st_cnt[y.s] = (uint32_t)y.nm | ((uint32_t)y.n_act << 5) | ((uint32_t)q << 10) |
                   ((uint32_t)y.n_err << 18);
@@ -903,7 +913,7 @@ __device__ __forceinline__ void keys_write(const LiveParams& P, const Sess<G>& y
       ++q;
     }, (C.format & PASTE_CF_UNIQ) != 0);
   }
-  static_cast<uint16_t*>(C.pred)[y.s] = y.key >= 0 ? (uint16_t)y.key : (uint16_t)0xffffu;
+  key_write<G>(C, y);
   t.nm += (unsigned)y.nm;
   t.na += (unsigned)y.n_act;
   t.ne += (unsigned)y.n_err;
@@ -1562,7 +1572,8 @@ extern "C" int paste_predict_live_compact(const paste_pool_desc* pool, paste_win
       ((c->format & PASTE_CF_ENTRY16) &&
        live_keys(pool, live_gather_depth(pool, windows->capacity)) >= 0xffff) ||
       ((c->format & PASTE_CF_KEYS) && !(c->format & PASTE_CF_ENTRY16)) ||
-      ((c->format & PASTE_CF_UNIQ) && !(c->format & PASTE_CF_KEYS))) {
+      ((c->format & PASTE_CF_UNIQ) && !(c->format & PASTE_CF_KEYS)) ||
+      ((c->format & PASTE_CF_KEY8) && !(c->format & PASTE_CF_KEYS))) {
     set_error("stream format outside the live plan's envelope");
     return PASTE_ERR_UNSUPPORTED;
   }

@@ -216,6 +216,7 @@ class LiveSessionTable:
         self._entries = None
         self.plan = None
         self._plan_host = None
+        self.plan_codes = None
         self._build_plan()
         # the 3-byte observe input and the key + argument serving streams
         # need the live-plan kernels
@@ -230,6 +231,10 @@ class LiveSessionTable:
             # one reference per distinct resolution (PASTE_CF_UNIQ)
             if os.environ.get("PASTE_NO_UNIQ") != "1":
                 self.sformat |= _native.PASTE_CF_UNIQ
+            # u8 plan codes instead of u16 keys when the distinct non-empty
+            # entries fit (PASTE_CF_KEY8): 1 B per session less to download
+            if self.plan_codes is not None and os.environ.get("PASTE_NO_KEY8") != "1":
+                self.sformat |= _native.PASTE_CF_KEY8
 
     def _build_plan(self) -> None:
         """Compile the live plan (paste_build_live_plan: per match-table key,
@@ -257,6 +262,30 @@ class LiveSessionTable:
         self._plan_bufs = (buf, walk)
         self.plan = LivePlan(ptr(buf), self.K, self.dpool.image.max_bindings, ptr(walk),
                              len(self.host_nodes) if walk is not None else 0)
+        self._assign_plan_codes()
+
+    def _assign_plan_codes(self) -> None:
+        """Number the plan's distinct non-empty entries (PASTE_CF_KEY8).
+        Everything the host expands from a key -- counts, pattern ids,
+        completeness, action codes, utilities, binding map words -- is the
+        entry's content, so keys with equal content may share one u8 code;
+        entries without predictions, actions or bindings all read as 0xFF,
+        like a session without a key.  The code goes into byte 8 of each
+        entry's header, which the serving kernels write to the key stream;
+        the host keeps one representative key per code (``plan_host()[6]``).
+        None (and the u16 key stream) when more than 255 codes are needed."""
+        self._plan_host = None
+        self.plan_codes = None
+        K, M = self.K, self.K * max(self.dpool.image.max_bindings, 1)
+        L = plan_layout_host(K, M)
+        got = plan_codes(self._plan_bufs[0].cpu().numpy().reshape(-1, L["stride"]), K, M)
+        if got is None:
+            return
+        codes, rep = got
+        t = self.torch
+        view = self._plan_bufs[0].view(-1, L["stride"])
+        view[:, 8].copy_(t.from_numpy(codes))
+        self.plan_codes = (codes, rep)
 
     def refresh_estimates(self, estimates) -> None:
         """Re-read ``benefit_of = estimates.duration`` for every tool (the
@@ -271,6 +300,11 @@ class LiveSessionTable:
             check(self.lib.paste_build_live_plan(ctypes.byref(self.pool_desc),
                                                  ctypes.byref(self.adm), self.K, self.W,
                                                  self.plan.plan, stream_handle()), self.lib)
+            self._entries = None
+            fmt8 = self.sformat & _native.PASTE_CF_KEY8
+            self._assign_plan_codes()  # entry contents changed: codes and host copy
+            if fmt8 and self.plan_codes is None:
+                self.sformat &= ~_native.PASTE_CF_KEY8
 
     # -- state upload ---------------------------------------------------------
 
@@ -423,21 +457,19 @@ class LiveSessionTable:
         per key (n_pred, n_act, action codes [keys, K] = slot | level if
         complete << 8 | level if PARTIAL << 12, n_map, n_units, map words
         [keys, M] = binding | rank << 32 | bslot << 40 | age << 48 | unit
-        << 56)."""
+        << 56, representative key per u8 plan code [256] (-1 = none) or
+        None)."""
         if self._plan_host is None:
             buf = self._plan_bufs[0].cpu().numpy()
             K, M = self.K, self.K * max(self.dpool.image.max_bindings, 1)
-            al = lambda x, a: (x + a - 1) // a * a  # noqa: E731  (live_plan.cu plan_layout)
-            off_comp = 16 + 4 * K
-            off_act = al(off_comp + K, 16)
-            off_util = al(off_act + 2 * K, 8)
-            off_map = off_util + 8 * K
-            stride = al(off_map + 8 * M, 16)
-            rows = buf.reshape(-1, stride)
+            L = plan_layout_host(K, M)
+            off_act, off_map = L["off_act"], L["off_map"]
+            rows = buf.reshape(-1, L["stride"])
             self._plan_host = (rows[:, 0].astype(np.int64), rows[:, 1].astype(np.int64),
                                rows[:, off_act:off_act + 2 * K].copy().view(np.uint16),
                                rows[:, 2].astype(np.int64), rows[:, 3].astype(np.int64),
-                               rows[:, off_map:off_map + 8 * M].copy().view(np.uint64))
+                               rows[:, off_map:off_map + 8 * M].copy().view(np.uint64),
+                               self.plan_codes[1] if self.plan_codes is not None else None)
         return self._plan_host
 
     def output_nbytes(self) -> int:
@@ -494,8 +526,12 @@ class CompactRecords:
         K, B = self.K, self.B
         keys = bool(self.fmt & _native.PASTE_CF_KEYS)
         if keys:  # counts from the key's live-plan entry
-            key = self.pred.astype(np.int64)
-            valid = key != 0xFFFF
+            if self.fmt & _native.PASTE_CF_KEY8:  # u8 plan code -> a key with its content
+                key = self.plan[6][self.pred.astype(np.int64)]
+                valid = key >= 0
+            else:
+                key = self.pred.astype(np.int64)
+                valid = key != 0xFFFF
             kk = np.where(valid, key, 0)
             n_pred = np.where(valid, self.plan[0][kk], 0)
             n_act = np.where(valid, self.plan[1][kk], 0)
@@ -516,7 +552,8 @@ class CompactRecords:
         if self.fmt & _native.PASTE_CF_ENTRY16:
             # the session's match-table entry lists its predictions; PARTIAL =
             # a mapped prediction with an unresolved reference
-            pid = self.entries[1][self.pred.astype(np.int64)[sess], slot].astype(np.int64)
+            kidx = kk if keys else self.pred.astype(np.int64)
+            pid = self.entries[1][kidx[sess], slot].astype(np.int64)
             mapped = (patterns["flags"][pid] & 1) != 0
             nb = np.where(mapped, patterns["n_bind"][pid], 0)
             res.pred_pat[sess * K + slot] = pid
@@ -588,7 +625,8 @@ def _compact_buffers(table: "LiveSessionTable", f: int | None = None):
     dev = t.device("cuda")
     entry = bool(f & _native.PASTE_CF_ENTRY16)
     if f & _native.PASTE_CF_KEYS:  # totals | keys | args in one buffer: one download copy
-        return _keys_buffers(t, n * K * B, n, bool(f & _native.PASTE_CF_ARG16), dev)
+        return _keys_buffers(t, n * K * B, n, bool(f & _native.PASTE_CF_ARG16), dev,
+                             kb=_key_bytes(f))
     return {"hdr": t.zeros(n, dtype=t.uint8 if f & _native.PASTE_CF_HDR8 else t.int16, device=dev),
             "pred": t.zeros(n if entry else n * K,
                             dtype=t.uint8 if f & _native.PASTE_CF_PRED8 and not entry else t.int16,
@@ -599,22 +637,74 @@ def _compact_buffers(table: "LiveSessionTable", f: int | None = None):
             "totals": t.zeros(5, dtype=t.int64, device=dev)}
 
 
-def keys_layout(n: int, arg_cap: int, a16: bool) -> tuple[int, int, int]:
+def keys_layout(n: int, arg_cap: int, a16: bool, kb: int = 2) -> tuple[int, int, int]:
     """Byte offsets of the key-stream buffer: totals (5 x i64) at 0, the
-    u16 keys at `k_off`, the argument words at `a_off`; `size` in total."""
+    keys (u16, or u8 plan codes: kb = 1) at `k_off`, the argument words at
+    `a_off`; `size` in total."""
     k_off = 64
-    a_off = (k_off + 2 * n + 63) // 64 * 64
+    a_off = (k_off + kb * n + 63) // 64 * 64
     return k_off, a_off, a_off + arg_cap * (2 if a16 else 4)
 
 
-def _keys_buffers(t, arg_cap: int, n: int, a16: bool, dev, pinned: bool = False) -> dict:
-    k_off, a_off, size = keys_layout(n, arg_cap, a16)
+def plan_codes(rows: np.ndarray, K: int, M: int):
+    """u8 plan codes of live-plan entries ``rows`` [keys, stride] (raw
+    bytes, plan_layout_host): one code per distinct non-empty content in
+    first-key order of np.unique, 0xFF for entries without predictions,
+    actions or bindings.  Returns (codes [keys], representative key per
+    code [256], -1 = unused), or None when more than 255 codes are needed."""
+    L = plan_layout_host(K, M)
+    nm, na, nmap = (rows[:, j].astype(np.int64) for j in (0, 1, 2))
+    live = (nm > 0) | (na > 0) | (nmap > 0)
+
+    def cols(off, width, slots, count):  # slots past an entry's count are never written
+        keep = np.arange(slots)[None, :] < count[:, None]
+        return np.where(np.repeat(keep, width, axis=1), rows[:, off:off + width * slots], 0)
+
+    content = np.concatenate([
+        rows[:, :4], cols(L["off_pid"], 4, K, nm), cols(L["off_comp"], 1, K, nm),
+        cols(L["off_act"], 2, K, na), cols(L["off_util"], 8, K, na),
+        cols(L["off_map"], 8, M, nmap)], axis=1)
+    idx = np.flatnonzero(live)
+    codes = np.full(len(rows), 0xFF, np.uint8)
+    rep = np.full(256, -1, np.int64)
+    if len(idx):
+        uniq, first, inv = np.unique(content[idx], axis=0, return_index=True,
+                                     return_inverse=True)
+        if len(uniq) > 255:
+            return None
+        codes[idx] = inv.reshape(-1).astype(np.uint8)
+        rep[:len(uniq)] = idx[first]
+    return codes, rep
+
+
+def _key_bytes(fmt: int) -> int:
+    """Bytes per session of the key stream: u8 plan codes or u16 keys."""
+    return 1 if fmt & _native.PASTE_CF_KEY8 else 2
+
+
+def plan_layout_host(K: int, M: int) -> dict:
+    """Byte offsets of a live-plan entry (live_plan.cu plan_layout): header
+    (n_pred, n_act, n_map, n_units bytes, i32 structural errors, u8 plan
+    code at 8), pattern ids, completeness, action codes, utilities, map
+    words."""
+    al = lambda x, a: (x + a - 1) // a * a  # noqa: E731
+    off_comp = 16 + 4 * K
+    off_act = al(off_comp + K, 16)
+    off_util = al(off_act + 2 * K, 8)
+    off_map = off_util + 8 * K
+    return {"off_pid": 16, "off_comp": off_comp, "off_act": off_act, "off_util": off_util,
+            "off_map": off_map, "stride": al(off_map + 8 * M, 16)}
+
+
+def _keys_buffers(t, arg_cap: int, n: int, a16: bool, dev, pinned: bool = False,
+                  kb: int = 2) -> dict:
+    k_off, a_off, size = keys_layout(n, arg_cap, a16, kb)
     blob = (t.empty(size, dtype=t.uint8, pin_memory=True) if pinned
             else t.zeros(size, dtype=t.uint8, device=dev))
     z = (lambda m, dt: t.empty(m, dtype=dt, pin_memory=True)) if pinned else \
         (lambda m, dt: t.zeros(m, dtype=dt, device=dev))
     return {"blob": blob, "totals": blob[:40].view(t.int64),
-            "pred": blob[k_off:k_off + 2 * n].view(t.int16),
+            "pred": blob[k_off:k_off + kb * n].view(t.int16 if kb == 2 else t.uint8),
             "arg": blob[a_off:a_off + arg_cap * (2 if a16 else 4)].view(t.int16 if a16 else t.int32),
             "hdr": z(16, t.int16), "act": z(16, t.uint8)}  # not written in this form
 
@@ -690,14 +780,16 @@ def _serve_state(table, depth: int, fmt: int) -> dict:
     keys = bool(fmt & _native.PASTE_CF_KEYS)
     if keys:
         pinned = [_keys_buffers(t, bufs[0]["arg"].numel(), table.n,
-                                bool(fmt & _native.PASTE_CF_ARG16), None, pinned=True)
+                                bool(fmt & _native.PASTE_CF_ARG16), None, pinned=True,
+                                kb=_key_bytes(fmt))
                   for _ in range(2 * depth)]
     else:
         pinned = [{k: t.empty(v.shape, dtype=v.dtype, pin_memory=True)
                    for k, v in bufs[0].items()} for _ in range(2 * depth)]
     entry = bool(fmt & _native.PASTE_CF_ENTRY16)
     vdt = {"hdr": np.uint8 if fmt & _native.PASTE_CF_HDR8 else np.uint16,
-           "pred": np.uint8 if fmt & _native.PASTE_CF_PRED8 and not entry else np.uint16,
+           "pred": (np.uint8 if (fmt & _native.PASTE_CF_PRED8 and not entry)
+                    or fmt & _native.PASTE_CF_KEY8 else np.uint16),
            "arg": np.uint16 if fmt & _native.PASTE_CF_ARG16 else np.uint32, "act": np.uint8}
     names = ("totals",) + _STREAMS
     hsets = [{"views": {k: h[k].numpy().view(vdt[k]) for k in _STREAMS},
@@ -778,7 +870,7 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
     copy_q = deque()
     H2D, D2H = _native.PASTE_COPY_H2D, _native.PASTE_COPY_D2H
     nh = 2 * depth  # pinned sets: a handed-out record outlives depth - 1 more steps
-    a_off = keys_layout(n, 0, True)[1] if keys else 0
+    a_off = keys_layout(n, 0, True, _key_bytes(fmt))[1] if keys else 0
 
     def actual_sizes(tot):
         P, A, Q = int(tot[0]), int(tot[1]), int(tot[2])

@@ -14,7 +14,8 @@ if not torch.cuda.is_available():  # pragma: no cover - CPU container
 
 from oracle import bridge  # noqa: E402
 from paper_2603_18897_b200 import admit  # noqa: E402
-from paper_2603_18897_b200._native import PASTE_CF_ENTRY16, PASTE_CF_KEYS, PASTE_CF_UNIQ  # noqa: E402
+from paper_2603_18897_b200._native import (PASTE_CF_ENTRY16, PASTE_CF_KEY8, PASTE_CF_KEYS,  # noqa: E402
+                                           PASTE_CF_UNIQ)
 from paper_2603_18897_b200.device_ops import DevicePool  # noqa: E402
 from paper_2603_18897_b200.live import LiveSessionTable  # noqa: E402
 from paper_2603_18897_b200.mining import load_pool  # noqa: E402
@@ -240,7 +241,7 @@ def test_compact_records_expand_to_the_full_records(fmt):
                                      "ship_bytes", "pred_stream", "pinned_inputs", "no_plan",
                                      "no_plan_pred_stream", "narrow8", "narrow8_pinned",
                                      "no_keys", "no_uniq", "tight_bound", "narrow2",
-                                     "narrow2_pinned"])
+                                     "narrow2_pinned", "key16"])
 def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
@@ -283,9 +284,12 @@ def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     else:
         assert pip.sformat & PASTE_CF_ENTRY16
     if variant == "no_keys":
-        pip.sformat &= ~(PASTE_CF_KEYS | PASTE_CF_UNIQ)
+        pip.sformat &= ~(PASTE_CF_KEYS | PASTE_CF_UNIQ | PASTE_CF_KEY8)
     if variant == "no_uniq":
         pip.sformat &= ~PASTE_CF_UNIQ
+    if variant == "key16":  # u16 match-table keys instead of u8 plan codes
+        assert pip.sformat & PASTE_CF_KEY8
+        pip.sformat &= ~PASTE_CF_KEY8
     if variant == "tight_bound":  # every step outgrows its download bound: the rest is fetched
         pip.serve_bound_margin = 64
     steps = 20
@@ -410,3 +414,40 @@ def test_node_codes_append_only_and_bounded():
     assert b.tolist() == [1, 3, 0] and c.host.numpy()[:4].tolist() == [5, 9, 700, 11]
     assert c.encode(np.arange(1000, 1300)) is None and c.n == 4
     assert c.encode(np.arange(1000, 1252)).max() == 255 and c.n == 256
+
+
+def test_serve_follows_estimate_updates():
+    """refresh_estimates between serve() calls: the plan's utilities and
+    per-tool winners change, so its u8 plan codes (PASTE_CF_KEY8) and the
+    host's copy of the plan are rebuilt; every served step still equals the
+    K-slot step under the same estimates."""
+    pool = load_pool("paper_2603_18897_b200/data/pool_motif_c3.json")
+    dp = DevicePool(pool)
+    policy = parse_policy(MOTIF_POLICY).policy
+    n = 4096
+    books = EstimateBook(), EstimateBook()
+    wl_a, wl_b = (LiveWorkload(dp.sigs, dp.keys, n, seed=13) for _ in range(2))
+    seq = LiveSessionTable(dp, n, wl_a.tmpl.nodes, wl_a.max_batch_bytes, policy, books[0])
+    pip = LiveSessionTable(dp, n, wl_b.tmpl.nodes, wl_b.max_batch_bytes, policy, books[1])
+    assert pip.sformat & PASTE_CF_KEY8
+    phases = [[], [("search", 700.0), ("web_fetch", 5000.0)], [("terminal", 1.5), ("search", 3.0)],
+              [("web_fetch", 0.0)]]
+    n_act = 0
+    for ups in phases:
+        for tool, ms in ups:
+            for b in books:
+                b.update(tool, ms)
+        if ups:
+            seq.refresh_estimates(books[0])
+            pip.refresh_estimates(books[1])
+        full = []
+        for _ in range(6):
+            seq.step(wl_a.next_batch())
+            full.append(seq.fetch().session_major())
+        got = [r.expand(dp.image.patterns, pip.benefit)
+               for r in pip.serve(wl_b.next_batch() for _ in range(6))]
+        assert len(got) == 6
+        for f, g in zip(full, got):
+            _compare(g, f)
+            n_act += int(f.n_act.sum())
+    assert n_act > 0

@@ -4,12 +4,16 @@
 (PASTE_CF_KEYS | PASTE_CF_UNIQ) against hand-built plan entries -- bindings
 that share a resolution unit, an unresolved unit making its predictions
 PARTIAL and their admitted actions take the partial level, and a session
-without an entry."""
+without an entry; and the u8 plan-code key stream (PASTE_CF_KEY8): the
+codes plan_codes assigns and the same expansion through them."""
 
 import numpy as np
 
 from paper_2603_18897_b200 import _native
-from paper_2603_18897_b200.live import CompactRecords, EventBatch, keys_layout, wire8_layout
+import pytest
+
+from paper_2603_18897_b200.live import (CompactRecords, EventBatch, keys_layout, plan_codes,
+                                         plan_layout_host, wire8_layout)
 from paper_2603_18897_b200.packing import C_FULL, C_PARTIAL, C_TOOL_ONLY
 
 
@@ -37,13 +41,51 @@ def test_keys_layout():
         k_off, a_off, size = keys_layout(n, cap, a16)
         assert k_off >= 40 and a_off % 64 == 0 and a_off >= k_off + 2 * n
         assert size == a_off + cap * (2 if a16 else 4)
+        k_off, a_off8, size8 = keys_layout(n, cap, a16, kb=1)  # u8 plan codes
+        assert a_off8 % 64 == 0 and k_off + n <= a_off8 <= a_off
+        assert size8 == a_off8 + cap * (2 if a16 else 4)
+
+
+def _plan_rows(K, M, entries):
+    """Raw live-plan rows; entries: per key (nm, na, n_map, pids, acts, utils,
+    words) or None (an empty entry); unused slots hold garbage."""
+    L = plan_layout_host(K, M)
+    rows = np.random.default_rng(5).integers(0, 256, (len(entries), L["stride"]), dtype=np.uint8)
+    for r, e in zip(rows, entries):
+        nm, na, nmap, pids, acts, utils, words = e or (0, 0, 0, [], [], [], [])
+        r[0], r[1], r[2], r[3] = nm, na, nmap, min(nmap, 1)
+        r[L["off_pid"]:L["off_pid"] + 4 * nm] = np.array(pids, np.int32).view(np.uint8)
+        r[L["off_comp"]:L["off_comp"] + nm] = 2
+        r[L["off_act"]:L["off_act"] + 2 * na] = np.array(acts, np.uint16).view(np.uint8)
+        r[L["off_util"]:L["off_util"] + 8 * na] = np.array(utils, np.float64).view(np.uint8)
+        r[L["off_map"]:L["off_map"] + 8 * nmap] = np.array(words, np.uint64).view(np.uint8)
+    return rows
+
+
+def test_plan_codes_share_equal_entries():
+    K, M = 4, 8
+    a = (2, 1, 0, [3, 5], [0x301], [1.5], [])
+    b = (1, 1, 1, [7], [0x300], [2.0], [9])
+    rows = _plan_rows(K, M, [None, a, b, a, None, b, a])
+    codes, rep = plan_codes(rows, K, M)
+    assert codes[0] == 0xFF and codes[4] == 0xFF  # empty entries: no key needed
+    assert codes[1] == codes[3] == codes[6] != codes[2] == codes[5]
+    for key in (1, 2, 3, 5, 6):  # the representative has the same content
+        r = rep[codes[key]]
+        assert r in (1, 2) and (r == 1) == (codes[key] == codes[1])
+    assert (rep[2:] == -1).all()
+    # more than 255 distinct contents: no u8 form
+    many = [(1, 0, 0, [i], [], [], []) for i in range(256)]
+    assert plan_codes(_plan_rows(K, M, many), K, M) is None
+    assert plan_codes(_plan_rows(K, M, many[:255]), K, M) is not None
 
 
 def _word(bind, rank, bslot, age, unit):
     return np.uint64(bind | (rank << 32) | (bslot << 40) | (age << 48) | (unit << 56))
 
 
-def test_expand_unit_references():
+@pytest.mark.parametrize("key8", [False, True])
+def test_expand_unit_references(key8):
     K, B, n = 4, 2, 3
     patterns = np.zeros(3, _native.PATTERN_DTYPE)
     # p0: mapped, 2 bindings, tool 0; p1: unmapped, tool 1; p2: mapped, 1 binding, tool 0
@@ -72,6 +114,12 @@ def test_expand_unit_references():
     arg = np.array([(1 << 11) | 5, (1 << 11) | 7, 0xFFFF, (1 << 11) | 9], np.uint16)
     fmt = (_native.PASTE_CF_ENTRY16 | _native.PASTE_CF_KEYS | _native.PASTE_CF_UNIQ
            | _native.PASTE_CF_ARG16)
+    if key8:  # u8 plan codes: code 0 stands for key 0, 0xFF for no entry
+        fmt |= _native.PASTE_CF_KEY8
+        rep = np.full(256, -1, np.int64)
+        rep[0] = 0
+        plan = plan + (rep,)
+        keys = np.array([0, 0, 0xFF], np.uint8)
     rec = CompactRecords(K, B, np.zeros(0, np.uint16), keys, arg, np.zeros(0, np.uint8), fmt,
                          entries, plan)
     r = rec.expand(patterns, benefit).session_major()
