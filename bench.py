@@ -344,8 +344,9 @@ def run_ours(args):
                 "h2d_bytes_per_step": h2d // S_, "d2h_bytes_per_step": d2h // S_,
                 "ms_per_step": 1e3 * e2e_s / S_,
                 "records": "narrow CSR streams, format bits %d (%s)" % (
-                    table.sformat, "per-session match-table key + refs%s; counts and actions "
+                    table.sformat, "per-session %s + refs%s; counts and actions "
                     "from the key's live-plan entry" % (
+                        "u8 plan code" if table.sformat & 64 else "u16 match-table key",
                         " (one per distinct resolution)" if table.sformat & 32 else "")
                     if table.sformat & 16 else
                     "per-session match-table key + refs + actions"
