@@ -290,9 +290,12 @@ def run_ours(args):
     # two batches past the timed ones keep the pipeline full at the end
     host_batches = []
     for i in range(W_ + S_ + 2):
-        # u8 token + u8 node code (the table's NodeCodes) on the wire when they
-        # fit, in one pinned buffer: one upload copy per step
-        b = wl.next_batch().narrowed(table.codes)
+        # a u8 event code per session (the table's EventCodes: (token, node
+        # array) pairs) on the wire when they fit, else u8 token + u8 node code
+        # (NodeCodes), in one pinned buffer: one upload copy per step
+        b = wl.next_batch().narrowed(table.codes,
+                                     None if os.environ.get("PASTE_NO_EVENT_CODES") == "1"
+                                     else table.ecodes)
         b.pin()
         b.tok = torch.from_numpy(b.tok).pin_memory()
         b.ref = torch.from_numpy(np.ascontiguousarray(b.ref)).pin_memory()
@@ -351,7 +354,9 @@ def run_ours(args):
                     if table.sformat & 16 else
                     "per-session match-table key + refs + actions"
                     if table.sformat & 8 else "per-prediction codes + refs + actions"),
-                "inputs": ("u8 token + u8 node code per session" if host_batches[-1].node8 is not None
+                "inputs": ("u8 event code (token, node array) per session"
+                           if host_batches[-1].ev8 is not None else
+                           "u8 token + u8 node code per session" if host_batches[-1].node8 is not None
                            else "u8 token + u16 node_base per session") if table.narrow8
                 else "i32 token + i32 node_base per session"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -164,6 +164,11 @@ typedef struct {
    * assigns codes to the node arrays (payload shapes) it has seen          */
   const uint8_t* new_node8;
   const int32_t* node_codes;
+  /* optional 1-byte wire form (with new_tok8 alone): new_tok8 holds a u8
+   * event code per session and event_codes[2 * code] is its token (-1 = LLM
+   * step), event_codes[2 * code + 1] its node_base; the caller assigns codes
+   * to the (token, node array) pairs it has seen                           */
+  const int32_t* event_codes;
 } paste_windows;
 
 enum { PASTE_C_FULL = 0, PASTE_C_PARTIAL = 1, PASTE_C_TOOL_ONLY = 2 };

@@ -59,7 +59,7 @@ class WindowsDesc(ctypes.Structure):
                 ("new_tok", c_void_p), ("new_ref", c_void_p), ("new_evt_base", c_int64),
                 ("new_byte_base", c_int64), ("stream_end", c_void_p), ("new_node", c_void_p),
                 ("new_tok8", c_void_p), ("new_node16", c_void_p), ("new_node8", c_void_p),
-                ("node_codes", c_void_p)]
+                ("node_codes", c_void_p), ("event_codes", c_void_p)]
 
 
 class PredictOut(ctypes.Structure):

@@ -279,8 +279,10 @@ __device__ __forceinline__ void front_load(const LiveParams& P, int64_t s, Front
   if (s >= P.win.n_sessions) return;
   f.cnt = P.win.count[s];
   if (P.win.new_tok8 != nullptr) {  // narrow wire form: u8 token, u16 node or u8 node code
-    f.t = P.win.new_tok8[s];
-    f.node = P.win.new_node8 != nullptr ? (int32_t)P.win.new_node8[s] : (int32_t)P.win.new_node16[s];
+    f.t = P.win.new_tok8[s];         // (or the u8 event code alone: event_codes)
+    f.node = P.win.new_node8 != nullptr    ? (int32_t)P.win.new_node8[s]
+             : P.win.new_node16 != nullptr ? (int32_t)P.win.new_node16[s]
+                                           : 0;
     return;
   }
   f.t = P.win.new_tok[s];
@@ -315,13 +317,19 @@ __device__ __forceinline__ void front_observe(const LiveParams& P, const FrontIn
   y.nm = y.n_act = y.n_map = y.n_err = 0;
   if (f.s >= n) return;
   const int64_t rbase = ring_base(P, f.s), rstride = ring_stride(P);
-  const int32_t t_in = (P.win.new_tok8 != nullptr && f.t == 255) ? -1 : f.t;
+  int32_t t_in = (P.win.new_tok8 != nullptr && f.t == 255) ? -1 : f.t;
+  int32_t node_in = f.node;
+  if (P.win.event_codes != nullptr) {  // 1-byte form: u8 event code -> (token, node_base)
+    const int2 e = __ldg(reinterpret_cast<const int2*>(P.win.event_codes) + f.t);
+    t_in = e.x;
+    node_in = e.y;
+  }
   const int head = (W & (W - 1)) == 0 ? (int)(f.cnt & (W - 1))
                    : f.cnt < (1ll << 31) ? (int)((uint32_t)f.cnt % (uint32_t)W)
                                          : (int)(f.cnt % W);
   y.ev0 = (int32_t)(P.win.new_evt_base + f.s);
   const bool narrow = P.win.new_node != nullptr || P.win.new_tok8 != nullptr;
-  y.node0 = narrow ? (int64_t)(P.win.new_node8 != nullptr ? __ldg(P.win.node_codes + f.node) : f.node)
+  y.node0 = narrow ? (int64_t)(P.win.new_node8 != nullptr ? __ldg(P.win.node_codes + f.node) : node_in)
                    : f.ref.node_base;
   P.win.refs[y.ev0] =
       paste_event_ref{y.node0, (narrow ? 0 : f.ref.byte_base) + P.win.new_byte_base};
@@ -1403,7 +1411,8 @@ static int live_prepare(const paste_pool_desc* pool, paste_windows* w, const pas
   PASTE_REQUIRE(pool && w && adm && plan && plan->plan, "null argument");
   PASTE_REQUIRE((w->new_tok != nullptr && (w->new_ref || w->new_node)) ||
                     (w->new_tok8 != nullptr &&
-                     (w->new_node16 != nullptr || (w->new_node8 != nullptr && w->node_codes != nullptr))),
+                     (w->new_node16 != nullptr || (w->new_node8 != nullptr && w->node_codes != nullptr) ||
+                      (w->event_codes != nullptr && !w->new_node16 && !w->new_node8))),
                 "the live kernel observes one new event per session");
   PASTE_REQUIRE(!w->stream_end, "stream-mode windows are not live sessions");
   PASTE_REQUIRE(w->capacity >= 1 && w->capacity <= 16, "live plan needs window capacity <= 16");

@@ -47,8 +47,10 @@ class NodeCodes:
         import torch
 
         self.lut = np.full(1 << 16, -1, np.int16)  # node_base -> code
-        self.host = torch.zeros(256, dtype=torch.int32).pin_memory()
-        self.dev = torch.zeros(256, dtype=torch.int32, device="cuda")
+        gpu = torch.cuda.is_available()  # (the host encoding alone runs without one)
+        self.host = torch.zeros(256, dtype=torch.int32)
+        self.host = self.host.pin_memory() if gpu else self.host
+        self.dev = torch.zeros(256, dtype=torch.int32, device="cuda") if gpu else None
         self.n = 0
         self.uploaded = 0
 
@@ -75,6 +77,53 @@ class NodeCodes:
             self.uploaded = self.n
 
 
+class EventCodes:
+    """u8 codes for the (token, node array) pairs of a live table's events:
+    the 1-byte wire form, decoded on the device through a 256-entry code ->
+    (token, node_base) table (paste_windows.event_codes).  Pairs are keyed
+    by (u8 token, NodeCodes node code); codes are only ever appended, so
+    steps in flight keep their meaning; past 256 pairs encode() returns
+    None and batches keep the 2-byte form."""
+
+    def __init__(self, nodes: NodeCodes):
+        import torch
+
+        self.nodes = nodes
+        self.lut = np.full(1 << 16, -1, np.int16)  # tok8 << 8 | node code -> code
+        gpu = torch.cuda.is_available()
+        self.host = torch.zeros(512, dtype=torch.int32)  # (token, node_base) per code
+        self.host = self.host.pin_memory() if gpu else self.host
+        self.dev = torch.zeros(512, dtype=torch.int32, device="cuda") if gpu else None
+        self.n = 0
+        self.uploaded = 0
+
+    def encode(self, tok8: np.ndarray, node8: np.ndarray) -> np.ndarray | None:
+        key = (tok8.astype(np.int32) << 8) | node8
+        code = self.lut[key]
+        missing = code < 0
+        if missing.any():
+            new = np.unique(key[missing])
+            if self.n + len(new) > 256:
+                return None
+            self.lut[new] = np.arange(self.n, self.n + len(new), dtype=np.int16)
+            pairs = self.host.numpy().reshape(256, 2)
+            t = new >> 8
+            pairs[self.n:self.n + len(new), 0] = np.where(t == 255, -1, t)
+            pairs[self.n:self.n + len(new), 1] = self.nodes.host.numpy()[new & 0xFF]
+            self.n += len(new)
+            code = self.lut[key]
+        return code.astype(np.uint8)
+
+    def upload(self, stream) -> None:
+        """Queue the table's new entries host -> device on `stream`."""
+        import torch
+
+        if self.n > self.uploaded:
+            with torch.cuda.stream(stream):
+                self.dev[:2 * self.n].copy_(self.host[:2 * self.n], non_blocking=True)
+            self.uploaded = self.n
+
+
 @dataclass
 class EventBatch:
     """One new tool event per session: tokens, batch-relative directory
@@ -88,14 +137,18 @@ class EventBatch:
     node16: object = None  # optional u16[n]: node_base (3-byte form)
     packed: object = None  # optional u8: tok8 and node16 / node8 in one buffer (wire8_layout)
     node8: object = None   # optional u8[n]: node code (2-byte form, NodeCodes of the table)
+    ev8: object = None     # optional u8[n]: event code (1-byte form, EventCodes of the table)
 
-    def narrowed(self, codes: "NodeCodes | None" = None) -> "EventBatch":
+    def narrowed(self, codes: "NodeCodes | None" = None,
+                 events: "EventCodes | None" = None) -> "EventBatch":
         """The narrow wire form alongside the others, when the values fit
         (signature ids < 255, node bases < 2^16): u8 token + u16 node_base
         (3 bytes), or with a live table's ``codes`` u8 token + u8 node code
         (2 bytes) while the table has seen at most 256 node arrays.  Both
         halves sit in one buffer (`packed`, wire8_layout), so a step uploads
-        them with one copy."""
+        them with one copy.  With the table's ``events`` as well, a u8 event
+        code per session (1 byte) while the table has seen at most 256
+        (token, node array) pairs; `packed` is then that code array."""
         tok = np.asarray(self.tok)
         node = np.asarray(self.node if self.node is not None else np.asarray(self.ref)[:, 0])
         if tok.size and (tok.max() >= 255 or node.max() >= (1 << 16) or node.min() < 0):
@@ -109,6 +162,10 @@ class EventBatch:
         if code is not None:
             node8 = packed[off:off + n]
             node8[:] = code
+            ev = events.encode(tok8, node8) if events is not None else None
+            if ev is not None:
+                return EventBatch(self.tok, self.ref, self.data, self.node, tok8, None, ev,
+                                  node8, ev)
             return EventBatch(self.tok, self.ref, self.data, self.node, tok8, None, packed, node8)
         node16 = packed[off:off + 2 * n].view(np.uint16)
         node16[:] = node
@@ -120,7 +177,9 @@ class EventBatch:
         upload."""
         import torch
 
-        if self.packed is not None and isinstance(self.packed, np.ndarray):
+        if self.ev8 is not None and isinstance(self.ev8, np.ndarray):
+            self.ev8 = self.packed = torch.from_numpy(self.ev8).pin_memory()
+        elif self.packed is not None and isinstance(self.packed, np.ndarray):
             n = len(self.tok8)
             off, _ = wire8_layout(n)
             self.packed = torch.from_numpy(self.packed).pin_memory()
@@ -223,6 +282,7 @@ class LiveSessionTable:
         self.narrow8 = (self.plan is not None and not ship_bytes and len(nodes) < (1 << 16)
                         and 2 * len(dpool.sigs) < 255)
         self.codes = NodeCodes() if self.narrow8 else None  # the 2-byte wire form
+        self.ecodes = EventCodes(self.codes) if self.narrow8 else None  # the 1-byte form
         self.new_tok8 = torch.zeros(n, dtype=torch.uint8, device=dev)
         self.new_node16 = torch.zeros(n, dtype=torch.int16, device=dev)
         self.staged8 = False
@@ -961,7 +1021,12 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
             trace.append({"u0": _tev(t, up)})
         st = sv["in"][k]
         narrow = b.node is not None and not table.ship_bytes
-        if (table.narrow8 and table.serve_fused and b.tok8 is not None
+        if table.narrow8 and table.serve_fused and b.ev8 is not None:  # 1 B: event code
+            narrow = "event"  # (not 1: True == 1 is the 8 B/session node form's flag)
+            table.codes.upload(up)
+            table.ecodes.upload(up)
+            wire = [(st["tok8"], b.ev8)]
+        elif (table.narrow8 and table.serve_fused and b.tok8 is not None
                 and b.node8 is not None):  # 2 B per session: token + node code
             narrow = 2
             table.codes.upload(up)
@@ -1014,6 +1079,10 @@ def serve(table: "LiveSessionTable", batches, depth: int = 4):
                 win.new_tok, win.new_node = None, None
                 win.new_tok8, win.new_node16 = ptr(st["tok8"]), None
                 win.new_node8, win.node_codes = ptr(st["node8"]), ptr(table.codes.dev)
+            elif narrow == "event":
+                win.new_tok, win.new_node = None, None
+                win.new_tok8, win.new_node16 = ptr(st["tok8"]), None
+                win.event_codes = ptr(table.ecodes.dev)
             sv["wins"][key] = win
         if table.plan is not None:
             scr = sv["scratch"][k]

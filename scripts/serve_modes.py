@@ -35,7 +35,8 @@ def main():
     steps = 6 if ncu else 40
     batches = []
     for _ in range(steps + 4):
-        b = wl.next_batch().narrowed(None if os.environ.get("WIRE3") == "1" else table.codes)
+        b = wl.next_batch().narrowed(None if os.environ.get("WIRE3") == "1" else table.codes,
+                                     table.ecodes if os.environ.get("WIRE1") == "1" else None)
         b.tok = torch.from_numpy(b.tok).pin_memory()
         b.node = torch.from_numpy(b.node).pin_memory()
         b.pin()

@@ -241,7 +241,7 @@ def test_compact_records_expand_to_the_full_records(fmt):
                                      "ship_bytes", "pred_stream", "pinned_inputs", "no_plan",
                                      "no_plan_pred_stream", "narrow8", "narrow8_pinned",
                                      "no_keys", "no_uniq", "tight_bound", "narrow2",
-                                     "narrow2_pinned", "key16"])
+                                     "narrow2_pinned", "key16", "narrow1", "narrow1_pinned"])
 def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
     """The pipelined serving loop (fused predict + compaction kernel, step
     i+1's upload / compute overlapping step i's download) returns exactly
@@ -308,7 +308,11 @@ def test_serve_pipeline_yields_the_step_records(variant, monkeypatch):
             if variant.startswith("narrow2"):  # u8 token + u8 node code on the wire
                 b = b.narrowed(pip.codes)
                 assert b.node8 is not None and pip.narrow8
-            if variant in ("pinned_inputs", "narrow8_pinned", "narrow2_pinned"):  # batched copies
+            if variant.startswith("narrow1"):  # u8 event code on the wire
+                b = b.narrowed(pip.codes, pip.ecodes)
+                assert b.ev8 is not None and pip.narrow8
+            if variant in ("pinned_inputs", "narrow8_pinned", "narrow2_pinned",
+                           "narrow1_pinned"):  # batched copies
                 b.tok = torch.from_numpy(b.tok).pin_memory()
                 b.node = torch.from_numpy(b.node).pin_memory()
                 b.ref = torch.from_numpy(np.ascontiguousarray(b.ref)).pin_memory()

@@ -12,7 +12,8 @@ import numpy as np
 from paper_2603_18897_b200 import _native
 import pytest
 
-from paper_2603_18897_b200.live import (CompactRecords, EventBatch, keys_layout, plan_codes,
+from paper_2603_18897_b200.live import (CompactRecords, EventBatch, EventCodes, NodeCodes,
+                                         keys_layout, plan_codes,
                                          plan_layout_host, wire8_layout)
 from paper_2603_18897_b200.packing import C_FULL, C_PARTIAL, C_TOOL_ONLY
 
@@ -34,6 +35,38 @@ def test_narrow_wire_layouts():
     # values that do not fit keep the wide forms
     big = EventBatch(tok, ref, np.zeros(1, np.uint8), node + 70_000).narrowed()
     assert big.tok8 is None and big.packed is None
+
+
+def test_event_codes_one_byte_form():
+    """(token, node array) pairs -> u8 event codes: append-only, the decode
+    table holds (token, node_base) with -1 for an LLM step, and past 256
+    pairs the batch keeps the 2-byte form."""
+    n = 500
+    rng = np.random.default_rng(3)
+    shapes = np.array([0, 40, 97, 300, 1200])
+    tok = rng.integers(-1, 12, n).astype(np.int32)
+    node = shapes[rng.integers(0, len(shapes), n)].astype(np.int32)
+    ref = np.stack([node.astype(np.int64), np.zeros(n, np.int64)], axis=1)
+    nc = NodeCodes()
+    ec = EventCodes(nc)
+    b = EventBatch(tok, ref, np.zeros(1, np.uint8), node).narrowed(nc, ec)
+    assert b.ev8 is not None and b.packed is b.ev8 and b.ev8.dtype == np.uint8
+    pairs = ec.host.numpy().reshape(256, 2)
+    assert np.array_equal(pairs[b.ev8, 0], tok) and np.array_equal(pairs[b.ev8, 1], node)
+    assert b.wire(False, narrow8=True)[0] is b.ev8
+    # the 2-byte halves are still there (stage() uses them)
+    assert np.array_equal(nc.host.numpy()[b.node8], node)
+    # codes are stable across batches; new pairs are appended
+    n0 = ec.n
+    b2 = EventBatch(tok[::-1].copy(), ref[::-1].copy(), np.zeros(1, np.uint8),
+                    node[::-1].copy()).narrowed(nc, ec)
+    assert ec.n == n0 and np.array_equal(b2.ev8, b.ev8[::-1])
+    # more than 256 distinct pairs: the 2-byte form
+    many_tok = np.repeat(np.arange(60, dtype=np.int32), 5)
+    many_node = np.tile(shapes.astype(np.int32), 60)
+    many = EventBatch(many_tok, np.stack([many_node.astype(np.int64), np.zeros(300, np.int64)], 1),
+                      np.zeros(1, np.uint8), many_node).narrowed(nc, ec)
+    assert many.ev8 is None and many.node8 is not None
 
 
 def test_keys_layout():
