@@ -26,7 +26,7 @@ wl = LiveWorkload(dp.sigs, dp.keys, n, seed=2603)
 table = LiveSessionTable(dp, n, wl.tmpl.nodes, wl.max_batch_bytes, policy, book, max_candidates=8)
 for _ in range(table.W + 2):
     table.step(wl.next_batch())
-batches = [wl.next_batch().narrowed(table.codes).pin() for _ in range(8)]
+batches = [wl.next_batch().narrowed(table.codes, table.ecodes).pin() for _ in range(8)]
 for _ in table.serve(batches[:6]):
     pass
 torch.cuda.synchronize()
@@ -47,17 +47,18 @@ def launch():
     assert rc == 0, rc
 
 
-def timed(reps=50, copies=False):
-    up_h = torch.empty(2_000_016, dtype=torch.uint8, pin_memory=True)
-    up_d = torch.empty(2_000_016, dtype=torch.uint8, device="cuda")
-    dn_h = torch.empty(3_500_000, dtype=torch.uint8, pin_memory=True)
-    dn_d = torch.empty(3_500_000, dtype=torch.uint8, device="cuda")
+def timed(reps=50, copies=False, up=True, down=True):
+    up_h = torch.empty(1_000_000, dtype=torch.uint8, pin_memory=True)
+    up_d = torch.empty(1_000_000, dtype=torch.uint8, device="cuda")
+    dn_h = torch.empty(2_500_000, dtype=torch.uint8, pin_memory=True)
+    dn_d = torch.empty(2_500_000, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
     ts = []
     for _ in range(reps):
-        if copies:
+        if copies and up:
             with torch.cuda.stream(s1):
                 up_d.copy_(up_h, non_blocking=True)
+        if copies and down:
             with torch.cuda.stream(s2):
                 dn_h.copy_(dn_d, non_blocking=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -73,6 +74,9 @@ def timed(reps=50, copies=False):
 
 print("kernels alone      ", timed())
 print("with PCIe copies   ", timed(copies=True))
+print("with H2D only      ", timed(copies=True, down=False))
+print("with D2H only      ", timed(copies=True, up=False))
+print("kernels alone again", timed())
 # queue pre-filled: host submission out of the timed path
 torch.cuda._sleep(5_000_000)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -82,3 +86,38 @@ for _ in range(40):
 e1.record(comp)
 e1.synchronize()
 print(f"40 back to back (queued)  {e0.elapsed_time(e1) / 40 * 1e3:.1f} us each")
+
+
+def queued_with_copies(up=True, down=True, reps=40):
+    """40 kernels back to back on the compute stream while 40 uploads / 40
+    downloads of the serving sizes run on two other streams, all queued
+    behind a sleep so host submission is out of the timed path."""
+    up_h = torch.empty(1_000_000, dtype=torch.uint8, pin_memory=True)
+    up_d = torch.empty(1_000_000, dtype=torch.uint8, device="cuda")
+    dn_h = torch.empty(2_500_000, dtype=torch.uint8, pin_memory=True)
+    dn_d = torch.empty(2_500_000, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    gate = torch.cuda.Event()
+    torch.cuda._sleep(5_000_000)
+    gate.record(comp)
+    s1.wait_event(gate)
+    s2.wait_event(gate)
+    for _ in range(reps):
+        if up:
+            with torch.cuda.stream(s1):
+                up_d.copy_(up_h, non_blocking=True)
+        if down:
+            with torch.cuda.stream(s2):
+                dn_h.copy_(dn_d, non_blocking=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    for _ in range(reps):
+        launch()
+    e1.record(comp)
+    torch.cuda.synchronize()
+    return f"{e0.elapsed_time(e1) / reps * 1e3:.1f} us each"
+
+
+print("queued, with both copies   ", queued_with_copies())
+print("queued, with H2D copies    ", queued_with_copies(down=False))
+print("queued, with D2H copies    ", queued_with_copies(up=False))
