@@ -76,7 +76,9 @@ def live():
         full.append(seq.fetch().session_major())
         seq.fetch_compact()  # compact.cu look-back compaction
     wire2 = os.environ.get("SAN_WIRE2") == "1"  # the 2-byte input (node codes), pinned
-    batches = (wl_b.next_batch().narrowed(pip.codes).pin() if wire2 else wl_b.next_batch()
+    wire1 = os.environ.get("SAN_WIRE1") == "1"  # the 1-byte input (event codes), pinned
+    batches = (wl_b.next_batch().narrowed(pip.codes, pip.ecodes).pin() if wire1
+               else wl_b.next_batch().narrowed(pip.codes).pin() if wire2 else wl_b.next_batch()
                for _ in range(steps))
     got = [r.expand(dp.image.patterns, pip.benefit) for r in pip.serve(batches)]
     for g, f in zip(got, full):
