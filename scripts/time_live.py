@@ -36,6 +36,8 @@ for _ in range(43):
 torch.cuda.synchronize()
 stream = torch.cuda.current_stream()
 for region, tok, node in staged[:3]:
+    if os.environ.get("WARM_FLUSH") == "1":  # warm-up steps exactly as the timed ones
+        bench.l2_flush(flush)
     table.launch(region, tok, new_node=node)
 ts = []
 for region, tok, node in staged[3:]:
@@ -52,3 +54,5 @@ dig = [int(v.to(torch.int64).sum()) if v.dtype != torch.float64 else float(v.sum
 print(f"MINB={os.environ.get('PASTE_LIVE_MINB', '7')} "
       f"median {statistics.median(us):.1f} us mean {statistics.mean(us):.1f} us min {min(us):.1f}; "
       f"digest {dig}")
+if os.environ.get("PER_STEP") == "1":
+    print("per step us:", " ".join(f"{u:.1f}" for u in us))
