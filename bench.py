@@ -669,7 +669,8 @@ def run_replay(args, world, rank, local):
     two_kernel = rb.tallies.cpu().numpy().tolist()
     fused = rb.launch_fused()
     step = rb.launch_fused if fused else rb.launch
-    for _ in range(args.warmup):
+    for _ in range(args.warmup):  # warm-up steps as the timed ones run
+        l2_flush(flush)
         step()
     torch.cuda.synchronize()
     steps = max(1, min(args.steps, 10))
@@ -833,7 +834,8 @@ def replay_pool_leg(args, pool_file, W, K, rank, steps, flush):
     two = rb.tallies.cpu().numpy().tolist()
     fused = rb.launch_fused()
     step = rb.launch_fused if fused else rb.launch
-    for _ in range(max(args.warmup, 1)):
+    for _ in range(max(args.warmup, 1)):  # warm-up steps as the timed ones run
+        l2_flush(flush)
         step()
     stream = torch.cuda.current_stream()
     t = 0.0
